@@ -1,0 +1,175 @@
+/*
+ * PLSS CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously correct binary64 implementation of Algorithm 1 (PLSS) of
+ * arXiv 2207.07615 with WI = I, used only by tests/, bench.py's cpu_baseline /
+ * reference arm and __graft_entry__.smoke() to check the CUDA path. It shares no code, header,
+ * table or constant generator with paper_2207_07615_b200/ and must never be linked into it.
+ *
+ * Compile: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC (see oracle/__init__.py).
+ * All sums are sequential in ascending index order, no FMA contraction, no compensated summation
+ * ("All arithmetic in binary64; no extended-precision accumulation").
+ *
+ * Readings of the paper used here (listed in DESIGN.md "Readings"):
+ *  R1  gamma = (theta/rho)*beta as in Algorithm 1 line "gamma_k=(theta_k/rho_k)*beta_k"
+ *      (Thm 4.1 proof L698/L704), NOT the misprinted theorem form L639-643.
+ *  R2  stop test right after rho is recomputed (after L804), <= comparison (L977, L992),
+ *      iters = number of updates applied to x, init update counts as 1; maxit caps iters.
+ *  R3  ||r0|| = 0 -> converged with 0 iterations; relative mode with ||b|| = 0 uses denominator 1.
+ *  R4  stop on the recursive residual r <- r - A p (L801), as Algorithm 1 does.
+ *  R5  breakdown guards phi <= 1e-300 (Y_VANISHED) and tau - 1 <= 1e-14 (STAGNATION)
+ *      (SPEC.md L147, L156); freeze mode for fixed-iteration timing: once hist <= FREEZE_H or a
+ *      guard fires (or tol is met), beta = gamma = 0 for the rest of the run.
+ *  R7  psi = y_k^T p_{k-1} is a diagnostic only (identity psi = -rho).
+ *  R8  tau = sqrt(theta*phi)/rho; beta = 1/((tau-1)*(tau+1)) in exactly Algorithm 1's order.
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string.h>
+#include <stdlib.h>
+
+#define OR_CONVERGED 0
+#define OR_MAXIT 1
+#define OR_Y_VANISHED 2
+#define OR_STAGNATION 3
+
+/* Per-iteration record, 8 doubles: hist, rho, phi, psi, theta, tau, beta, gamma. */
+#define REC 8
+
+/* y = A x over CSR: y_i = sum_j a_ij x_j in ascending j ("matvec"). */
+void oracle_spmv(int64_t m, const int32_t *row_ptr, const int32_t *col_idx, const double *val,
+                 const double *x, double *y) {
+    for (int64_t i = 0; i < m; ++i) {
+        double s = 0.0;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) s = s + val[k] * x[col_idx[k]];
+        y[i] = s;
+    }
+}
+
+/* v = A^T u over the CSC copy: v_j = sum_i a_ij u_i in ascending i. */
+void oracle_spmvT(int64_t n, const int32_t *col_ptr, const int32_t *row_idx, const double *val_t,
+                  const double *u, double *v) {
+    for (int64_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int64_t k = col_ptr[j]; k < col_ptr[j + 1]; ++k) s = s + val_t[k] * u[row_idx[k]];
+        v[j] = s;
+    }
+}
+
+static double dot(int64_t len, const double *a, const double *b) {
+    double s = 0.0;
+    for (int64_t i = 0; i < len; ++i) s = s + a[i] * b[i];
+    return s;
+}
+
+/*
+ * Algorithm 1, WI = I, following SURVEY.md 8(c)'s transcription.
+ * x0 may be NULL (zero). x (n) receives the final iterate. rec (nullable) receives
+ * (maxit+1)*REC doubles: rec[k*REC + 0..7] = hist_k, rho_k, phi, psi, theta, tau, beta, gamma
+ * where at k the values are those computed in loop step k (k = 0: initialization).
+ * freeze != 0: fixed-iteration mode (R5). Returns outcome; *iters_out = updates applied.
+ * P_out (nullable, maxit*n doubles) receives the updates p_1 .. p_iters (test pins only).
+ */
+int oracle_plss(int64_t m, int64_t n,
+                const int32_t *row_ptr, const int32_t *col_idx, const double *val,
+                const int32_t *col_ptr, const int32_t *row_idx, const double *val_t,
+                const double *b, const double *x0, double tol, int tol_mode, int32_t maxit,
+                int freeze, double freeze_h,
+                double *x, int32_t *iters_out, double *rec, double *P_out) {
+    double *r = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+    double *y = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *p = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *Ap = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+    int outcome = OR_MAXIT, frozen = 0, stopped = 0;
+    int32_t iters = 0;
+    if (rec) memset(rec, 0, sizeof(double) * (size_t)(maxit + 1) * REC);
+
+    /* nb = ||b||, denominator of the relative stop test (R3) */
+    double nb = sqrt(dot(m, b, b));
+    double nbd = (tol_mode == 0 && nb > 0.0) ? nb : 1.0;
+
+    /* x = x0; r = b - A x0  (Alg. 1) */
+    for (int64_t j = 0; j < n; ++j) x[j] = x0 ? x0[j] : 0.0;
+    for (int64_t i = 0; i < m; ++i) r[i] = b[i];
+    if (x0) {
+        oracle_spmv(m, row_ptr, col_idx, val, x0, Ap);
+        for (int64_t i = 0; i < m; ++i) r[i] = r[i] - Ap[i];
+    }
+    /* rho = r^T r; stop test before initialization (R2/R3) */
+    double rho = dot(m, r, r);
+    double h = sqrt(rho) / nbd;
+    if (rec) { rec[0] = h; rec[1] = rho; }
+    if (rho == 0.0 || h <= tol) {
+        if (!freeze) { outcome = OR_CONVERGED; goto done; }
+        frozen = 1; outcome = OR_CONVERGED; stopped = 1;
+    } else if (freeze && h <= freeze_h) {
+        frozen = 1;
+    }
+
+    /* y = A^T r; phi = y^T y; p = (rho/phi) y; theta = p^T p; x = x + p  (L786-797) */
+    oracle_spmvT(n, col_ptr, row_idx, val_t, r, y);
+    double phi = dot(n, y, y);
+    double gamma0 = 0.0;
+    if (phi <= 1e-300) {
+        if (!freeze) { outcome = OR_Y_VANISHED; goto done; }
+        if (!stopped) { outcome = OR_Y_VANISHED; stopped = 1; }
+        frozen = 1;
+    }
+    if (!frozen) gamma0 = rho / phi;
+    for (int64_t j = 0; j < n; ++j) p[j] = gamma0 * y[j];
+    double theta = dot(n, p, p);
+    for (int64_t j = 0; j < n; ++j) x[j] = x[j] + p[j];
+    iters = 1;
+    if (P_out) for (int64_t j = 0; j < n; ++j) P_out[j] = p[j];
+    if (rec) { rec[2] = phi; rec[4] = theta; rec[7] = gamma0; }
+
+    while (iters < maxit) {                                     /* L799 */
+        double *rk = rec ? rec + (size_t)iters * REC : NULL;
+        /* r = r - A p  (L801, eq:recRes) */
+        oracle_spmv(m, row_ptr, col_idx, val, p, Ap);
+        for (int64_t i = 0; i < m; ++i) r[i] = r[i] - Ap[i];
+        rho = dot(m, r, r);                                     /* L804 */
+        h = sqrt(rho) / nbd;
+        if (rk) { rk[0] = h; rk[1] = rho; }
+        if (h <= tol) {                                         /* stop test (R2) */
+            if (!freeze) { outcome = OR_CONVERGED; goto done; }
+            if (!stopped) { outcome = OR_CONVERGED; stopped = 1; }
+            frozen = 1;
+        } else if (freeze && h <= freeze_h) {
+            frozen = 1;
+        }
+        /* y = A^T r; phi = y^T y; psi = y^T p_{k-1}  (L802, L806; L671-672) */
+        oracle_spmvT(n, col_ptr, row_idx, val_t, r, y);
+        phi = dot(n, y, y);
+        double psi = dot(n, y, p);
+        double tau = 0.0, beta = 0.0, gamma = 0.0;
+        if (!frozen) {
+            tau = sqrt(theta * phi) / rho;                      /* L807 */
+            if (phi <= 1e-300) {
+                if (!freeze) { outcome = OR_Y_VANISHED; goto done; }
+                if (!stopped) { outcome = OR_Y_VANISHED; stopped = 1; }
+                frozen = 1;
+            } else if (tau - 1.0 <= 1e-14) {
+                if (!freeze) { outcome = OR_STAGNATION; goto done; }
+                if (!stopped) { outcome = OR_STAGNATION; stopped = 1; }
+                frozen = 1;
+            } else {
+                beta = 1.0 / ((tau - 1.0) * (tau + 1.0));        /* L807-808 */
+                gamma = (theta / rho) * beta;                    /* L809 (R1) */
+            }
+        }
+        /* p = beta p + gamma y; theta = p^T p; x = x + p  (L811-813) */
+        for (int64_t j = 0; j < n; ++j) p[j] = beta * p[j] + gamma * y[j];
+        theta = dot(n, p, p);
+        for (int64_t j = 0; j < n; ++j) x[j] = x[j] + p[j];
+        if (P_out) for (int64_t j = 0; j < n; ++j) P_out[(size_t)iters * n + j] = p[j];
+        iters += 1;
+        if (rk) { rk[2] = phi; rk[3] = psi; rk[4] = theta; rk[5] = tau; rk[6] = beta; rk[7] = gamma; }
+    }
+    if (!stopped) outcome = OR_MAXIT;
+done:
+    *iters_out = iters;
+    free(r); free(y); free(p); free(Ap);
+    return outcome;
+}
