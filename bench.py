@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""PLSS hot-path benchmark (BASELINE.json metric: PLSS iterations/s and achieved HBM GB/s).
+
+A "step" is one PLSS loop iteration (Algorithm 1: K1 r <- r - A p + rho, K2 y = A^T r
++ phi/psi + tail, K3 p/x update + theta) over the whole workload. Default workload: C5
+(BASELINE configs[4], the 1/2/4/8-GPU scaling config: m = 64M, n = 8M, 768M nnz,
+banded+random), run in freeze mode with tol 0 so every timed step does the same
+work. N > 1 (torchrun): row-block sharding, one NCCL all-reduce of n+1 doubles per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5|C3|C4|C2] [--impl reference]
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import plss_gen  # noqa: E402
+
+METRIC = "PLSS iterations/sec and achieved HBM GB/s (fraction of ~8 TB/s)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > i + 2 and s[i + 2] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------------------------
+def load_workload(name, rank, world, device):
+    """Returns dict of device tensors for this rank's row block + metadata."""
+    import torch
+    if name == "C5":
+        m, n = 64_000_000, 8_000_000
+        r0, r1 = plss_gen.row_block_bounds(m, world, rank)
+        d = plss_gen.make_c5_torch(device=device, m=m, n=n, rows=(r0, r1))
+        d.update(name="C5", tol=0.0, tol_mode=0, freeze=True, nnz_global=12 * m)
+        return d
+    s = plss_gen.make_config(name)
+    r0, r1 = plss_gen.row_block_bounds(s.m, world, rank)
+    blk = plss_gen.row_block(s, world, rank)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+    return {"name": name, "m": blk["m"], "n": s.n, "row_offset": r0, "m_global": s.m,
+            "row_ptr": t(blk["row_ptr"], torch.int32), "col_idx": t(blk["col_idx"], torch.int32),
+            "val": t(blk["val"], torch.float64), "col_ptr": t(blk["col_ptr"], torch.int32),
+            "row_idx": t(blk["row_idx"], torch.int32), "val_t": t(blk["val_t"], torch.float64),
+            "b": t(blk["b"], torch.float64), "tol": 0.0, "tol_mode": 0, "freeze": True,
+            "nnz_global": s.nnz}
+
+
+def workload_label(name):
+    return {
+        "C5": "C5: m=64M n=8M, 12 nnz/row (6 banded +-1024 of i*n/m, 6 uniform), N(0,1), 768M nnz",
+        "C3": "C3: 5-point Laplacian-like 2048^2 grid, 21M nnz",
+        "C4": "C4: power-law Zipf(2.1) rows clipped [1,4096], m=2M n=8M",
+        "C2": "C2: m=200k n=100k, 8 uniform nnz/row",
+    }.get(name, name)
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU baseline: the oracle on a bounded 1/100-scale sample of the same recipe
+# ---------------------------------------------------------------------------------------------
+def cpu_sample(name):
+    if name == "C5":
+        return plss_gen.make_config("C5s"), "C5 recipe at 1/100 scale (m=640k, n=80k, 7.68M nnz)"
+    if name == "C3":
+        return plss_gen.make_config("C3", N=512), "C3 recipe at 512^2 (1/16 scale)"
+    if name == "C4":
+        return plss_gen.make_config("C4", m=200_000, n=800_000, support=8000), "C4 recipe at 1/10 scale"
+    return plss_gen.make_config(name), f"{name} full"
+
+
+def run_oracle_steps(s, steps):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.plss(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t, s.b, tol=0.0,
+                maxit=steps, freeze=True)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(name, full_bytes, budget_s=15.0):
+    s, label = cpu_sample(name)
+    sb = plss_gen.bytes_per_iter(s.m, s.n, s.nnz)
+    t1 = run_oracle_steps(s, 5)
+    steps = int(max(5, min(2000, budget_s / max(t1 / 5, 1e-6))))
+    t = run_oracle_steps(s, steps)
+    gbs = sb * steps / t / 1e9
+    return {"value": gbs * 1e9 / full_bytes, "unit": "it/s", "cores": 1, "kind": "oracle",
+            "sample": f"{label}; {steps} loop steps in {t:.1f} s = {gbs:.2f} GB/s algorithmic; "
+                      f"it/s scaled to the full workload by algorithmic bytes/iter",
+            "oracle_gbs": gbs}
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm (--impl reference): the oracle as it stands, rank 0 only
+# ---------------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    name = args.workload
+    full = full_bytes_of(name)
+    s, label = cpu_sample(name)
+    sb = plss_gen.bytes_per_iter(s.m, s.n, s.nnz)
+    run_oracle_steps(s, max(1, args.warmup))
+    t = run_oracle_steps(s, args.steps)
+    gbs = sb * args.steps / t / 1e9
+    value = gbs * 1e9 / full
+    line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_label(name)},
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{label}; each step one oracle loop step; it/s scaled to the "
+                                       f"full workload by algorithmic bytes/iter ({gbs:.2f} GB/s)"},
+            "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def full_bytes_of(name):
+    return {"C5": plss_gen.bytes_per_iter(64_000_000, 8_000_000, 768_000_000),
+            "C3": plss_gen.bytes_per_iter(2048 ** 2, 2048 ** 2, 5 * 2048 ** 2 - 4 * 2048),
+            }.get(name) or (lambda s: plss_gen.bytes_per_iter(s.m, s.n, s.nnz))(plss_gen.make_config(name))
+
+
+# ---------------------------------------------------------------------------------------------
+# main (our arm)
+# ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--impl", default="plss", choices=["plss", "reference"])
+    ap.add_argument("--slabs", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=5)
+    ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2207_07615_b200 as pkg
+
+    assert args.warmup >= 3 or args.ncu, "timing rules: at least 3 warm-up steps"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pkg.load_library()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    w = load_workload(args.workload, rank, world, dev)
+    m_l, n = w["m"], w["n"]
+    nnz_l = int(w["col_idx"].numel())
+    A = pkg.Matrix(m_l, n, w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])
+    stream = torch.cuda.Stream(device=dev)
+    maxit_cap = args.warmup + args.steps + max(args.profile_steps, 1) + 8
+    if world > 1:
+        uid = pkg.plss_get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = pkg.plss_create_dist(A, w["row_offset"], w["m_global"], obj[0], rank, world,
+                                   slabs=args.slabs, maxit_cap=maxit_cap, stream=stream)
+    else:
+        ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=maxit_cap, stream=stream)
+    q = pkg.plss_query(ctx)
+    b = w["b"]
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: K steps, inputs resident in HBM (> L2 per step) ----------------
+    pkg.plss_start(ctx, b, None, tol=w["tol"], tol_mode=w["tol_mode"], maxit=maxit_cap, flags=1)
+    pkg.plss_step(ctx, args.warmup)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        pkg.plss_step(ctx, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    fin = pkg.plss_finish(ctx, None, want_hist=True)
+    iters_per_s = args.steps / (ms / 1e3)
+    B_global = plss_gen.bytes_per_iter(w["m_global"], n, w["nnz_global"])
+    if args.ncu:
+        if rank == 0:
+            print(json.dumps({"ncu_run": True, "ms_per_step": ms / args.steps}), flush=True)
+        return
+
+    # ---- per-kernel device times (CUDA events around each launch on the ctx stream) ----------
+    pkg.plss_start(ctx, b, None, tol=w["tol"], tol_mode=w["tol_mode"], maxit=maxit_cap, flags=1)
+    pkg.plss_step(ctx, 3)
+    kt = pkg.plss_profile(ctx, max(1, args.profile_steps))
+    k1_bytes = 12 * nnz_l + 4 * (m_l + 1) + 8 * n + 16 * m_l
+    k2_bytes = 12 * nnz_l + 4 * (n + 1) + 8 * m_l + 16 * n
+    k3_bytes = 40 * n
+    classes = {"k1_spmv_csr_resid": (kt["k1"], k1_bytes), "k2_spmv_csc_gather": (kt["k2"], k2_bytes),
+               "k3_pxupdate": (kt["k3"], k3_bytes)}
+    dom = max(classes, key=lambda c: classes[c][0])
+    dom_ms, dom_bytes = classes[dom]
+    peak, peak_src = _peaks()
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+
+    # ---- end-to-end through the public API: host b in, host x + history out, K steps ---------
+    pin_b = torch.empty(m_l, dtype=torch.float64, pin_memory=True)
+    pin_b.copy_(b.cpu())
+    pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    barrier()
+    t0 = time.perf_counter()
+    res = pkg.plss_solve(ctx, pin_b, None, tol=0.0, maxit=args.steps, flags=1, x=pin_x, want_hist=True)
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = {"value": args.steps / t_e2e, "unit": "it/s",
+           "h2d_bytes_per_step": 8 * m_l / args.steps,
+           "d2h_bytes_per_step": (8 * n + 8 * (args.steps + 1)) / args.steps,
+           "solve_iters": args.steps, "note": "one plss_solve from pinned host b to host x + history"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": iters_per_s, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_label(w["name"]), "m": w["m_global"], "n": n,
+                       "nnz": w["nnz_global"], "parallelism": f"row-block dp{world}" if world > 1 else "single",
+                       "slabs": q["slabs"], "freeze_mode": True, "tol": 0.0,
+                       "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
+                       "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8"},
+            "achieved_gbs": B_global * iters_per_s / 1e9,
+            "achieved_frac_of_peak": B_global * iters_per_s / 1e9 / peak,
+            "achieved_frac_of_8tbs": B_global * iters_per_s / 1e9 / 8000.0,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_step": dom_bytes, "kernel_ms_per_step": dom_ms},
+            "kernels_ms_per_step": kt,
+            "gpu_launches": args.steps * q["launches_per_step"],
+            "e2e": e2e,
+            "clocks": clocks,
+            "final_hist": float(fin["hist_full"][min(args.warmup + args.steps, maxit_cap) - 1]),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(w["name"], B_global)
+        print(json.dumps(line), flush=True)
+    pkg.plss_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

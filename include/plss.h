@@ -1,0 +1,160 @@
+/*
+ * plss.h -- C ABI of libplss, the B200 (sm_100a) hot path of PLSS with residual sketches
+ * (arXiv 2207.07615, "PLSS: A Projected Linear Systems Solver").
+ *
+ * What is computed: Algorithm 1 with WI = I for a consistent system
+ * A x = b, b in range(A) (eq:axb, L25-29), A in R^{m x n} sparse, square or rectangular:
+ *
+ *   init  : r = b - A x0; rho = r^T r; y = A^T r; phi = y^T y; p = (rho/phi) y;
+ *           theta = p^T p; x = x0 + p                                        (L784-797)
+ *   loop  : r <- r - A p  (eq:recRes L663-666)      rho = r^T r              (L801, L804)
+ *           stop if sqrt(rho)/||b|| <= tol                                   (L828-831, L977)
+ *           y = A^T r; phi = y^T y; psi = y^T p_{k-1} (diagnostic, L671-672) (L802, L806)
+ *           tau = sqrt(theta phi)/rho; beta = 1/((tau-1)(tau+1));
+ *           gamma = (theta/rho) beta                                         (L807-809)
+ *           p <- beta p + gamma y (Thm 4.1 eq:pkShort L628-712); theta = p^T p; x <- x + p
+ *                                                                            (L811-813)
+ * Readings where the paper is silent or misprinted are listed in DESIGN.md ("Readings"):
+ * gamma follows Algorithm 1 (L809), not the misprinted theorem statement (L639-643).
+ *
+ * Conventions
+ *  - Every call returns plss_status (0 = OK); no call aborts or exits the process.
+ *  - Index arrays are int32, values fp64 (binary64, round-to-nearest-even).
+ *  - CSR: row_ptr[m+1] (row_ptr[0] = 0, nondecreasing, row_ptr[m] = nnz), col_idx[nnz] strictly
+ *    ascending within each row, val[nnz]. CSC copy of the SAME matrix: col_ptr[n+1],
+ *    row_idx[nnz] strictly ascending within each column, val_t[nnz] (SPEC.md L29-35 invariants).
+ *  - "dev" pointers must be CUDA device memory of the ctx's device. Pointers marked
+ *    "host or dev" may be either; the library detects the kind with cudaPointerGetAttributes
+ *    and copies host data through the ctx stream.
+ *  - All work is enqueued on the ctx stream (the caller's, e.g. torch's current stream).
+ */
+#ifndef PLSS_H
+#define PLSS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLSS_REC 8  /* doubles per iteration record, see plss_solve / plss_finish `diag` */
+
+typedef struct plss_ctx plss_ctx; /* opaque; one per matrix (per rank) and stream */
+
+typedef enum {
+  PLSS_OK = 0,
+  PLSS_E_INVALID = 1, /* bad argument value (tol < 0, maxit < 1 or > maxit_cap, NULL ctx, ...)  */
+  PLSS_E_DIM = 2,     /* inconsistent dimensions / sizes / workspace too small                  */
+  PLSS_E_FORMAT = 3,  /* CSR/CSC invariant violated (validate = 1)                              */
+  PLSS_E_CUDA = 4,    /* a CUDA runtime call failed; see plss_last_error                        */
+  PLSS_E_NCCL = 5,    /* an NCCL call failed; see plss_last_error                               */
+  PLSS_E_NOMEM = 6,   /* host allocation failed                                                 */
+  PLSS_E_STATE = 7    /* call out of order (plss_step / plss_finish without plss_start)         */
+} plss_status;
+
+typedef enum {
+  PLSS_CONVERGED = 0,            /* sqrt(rho_k)/||b|| <= tol (relative) or sqrt(rho_k) <= tol */
+  PLSS_MAXIT = 1,                /* iteration cap reached                                      */
+  PLSS_BREAKDOWN_Y_VANISHED = 2, /* phi <= 1e-300 while rho above tol (b not in range(A))      */
+  PLSS_BREAKDOWN_STAGNATION = 3, /* tau - 1 <= 1e-14 (Cauchy-Schwarz equality)   */
+  PLSS_RUNNING = -1
+} plss_outcome;
+
+/* The matrix, as two borrowed DEVICE copies. The arrays must outlive the ctx and must not be
+ * mutated while it exists. They may be shared by several ctxs (e.g. one per stream). On a rank
+ * of a distributed solve, m and the arrays describe the LOCAL row block (rows rebased to 0) and
+ * n is the global column count. */
+typedef struct {
+  int64_t m, n, nnz;
+  const int32_t *row_ptr, *col_idx; /* CSR */
+  const double *val;
+  const int32_t *col_ptr, *row_idx; /* CSC copy of the same matrix */
+  const double *val_t;
+  int32_t validate; /* 1: O(nnz) device check of every invariant above, incl. CSR == CSC^T */
+} plss_matrix;
+
+typedef struct {
+  int32_t slabs;       /* row slabs that tile the gather of A^T r into L2 (0 = auto, 1 = off).
+                          With S > 1 the library keeps a slab-major CSC copy in the workspace. */
+  int32_t graph_chunk; /* iterations per CUDA-graph launch (0 = auto)                        */
+  int32_t maxit_cap;   /* largest maxit a solve on this ctx may request (sizes the history)  */
+  int32_t flags;       /* reserved, must be 0                                                 */
+} plss_options;
+
+/* Bytes of DEVICE workspace a ctx needs (vectors r, y, p, x, reduction partials, control block,
+ * history of (maxit_cap+1)*PLSS_REC doubles, tile maps, the optional slab-major CSC copy and,
+ * for plss_create_dist, the (n+1)-double AllReduce buffer). opt may be NULL (defaults).
+ * The caller allocates it (e.g. a torch uint8 tensor), 256-byte aligned, and keeps it alive
+ * for the ctx's lifetime. Returns 0 on invalid input. */
+size_t plss_workspace_bytes(const plss_matrix *A, const plss_options *opt);
+
+/* Create a single-device ctx. A: device arrays (see plss_matrix). workspace: dev, >= ws_bytes =
+ * plss_workspace_bytes(A, opt). cuda_stream: cudaStream_t (NULL = legacy default stream).
+ * Synchronizes the stream once (setup). Errors: E_INVALID, E_DIM, E_FORMAT, E_CUDA. */
+plss_status plss_create(const plss_matrix *A, const plss_options *opt, void *workspace,
+                        size_t ws_bytes, void *cuda_stream, plss_ctx **out);
+
+/* Distributed row-block ctx: this rank owns rows [row_offset, row_offset + A->m)
+ * of a global m_global x n matrix; x, p, y are replicated. Each iteration does local A p and
+ * A^T r and ONE ncclAllReduce(sum, fp64) of n+1 values (partial y and the local rho).
+ * id: 128 bytes from plss_get_unique_id on rank 0, broadcast by the caller (e.g. through
+ * torch.distributed). Collective: every rank must call it. Errors: as plss_create + E_NCCL. */
+plss_status plss_get_unique_id(uint8_t id[128]);
+plss_status plss_create_dist(const plss_matrix *A_local, int64_t row_offset, int64_t m_global,
+                             const uint8_t id[128], int32_t rank, int32_t nranks,
+                             const plss_options *opt, void *workspace, size_t ws_bytes,
+                             void *cuda_stream, plss_ctx **out);
+
+/* Full solve = plss_start + plss_step until done + plss_finish.
+ *  b      : host or dev, m (local rows on a rank) doubles.
+ *  x0     : host or dev, n doubles, or NULL for x0 = 0.
+ *  tol    : >= 0. tol_mode 0: stop when sqrt(rho)/||b|| <= tol (||b|| = 0 -> denominator 1);
+ *           1: stop when sqrt(rho) <= tol.
+ *  maxit  : 1 <= maxit <= maxit_cap; caps the number of updates x <- x + p.
+ *  flags  : bit0 = freeze mode (fixed-iteration timing): never stop early; once
+ *           sqrt(rho)/||b|| <= 64 eps, tol is met, or a breakdown guard fires, beta = gamma = 0
+ *           so x stays fixed while every kernel still runs with the same memory traffic.
+ *  x      : host or dev, n doubles, out (may alias x0).
+ *  iters  : host, out: updates applied.  outcome: host, out.
+ *  hist   : host, nullable, maxit+1 doubles: hist[k] = sqrt(rho_k)/||b|| (or sqrt(rho_k)).
+ *  diag   : host, nullable, (maxit+1)*PLSS_REC doubles; record k = {hist_k, rho_k, phi, psi,
+ *           theta, tau, beta, gamma} of loop step k (k = 0: initialization).
+ * Returns after the stream is synchronized. */
+plss_status plss_solve(plss_ctx *ctx, const double *b, const double *x0, double tol,
+                       int32_t tol_mode, int32_t maxit, int32_t flags, double *x, int32_t *iters,
+                       double *hist, double *diag, plss_outcome *outcome);
+
+/* Asynchronous pieces of plss_solve (same argument meaning), for timing and pipelining:
+ * plss_start copies b / x0 in and resets the device state; plss_step enqueues k more loop steps
+ * (CUDA graphs; steps after the stop condition are no-ops); plss_finish synchronizes and copies
+ * out x, iters, hist, diag, outcome. */
+plss_status plss_start(plss_ctx *ctx, const double *b, const double *x0, double tol,
+                       int32_t tol_mode, int32_t maxit, int32_t flags);
+plss_status plss_step(plss_ctx *ctx, int32_t k);
+plss_status plss_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
+                        plss_outcome *outcome);
+
+/* Test entry points. y = A x (x: dev n, y: dev m); v = A^T u (u: dev m,
+ * v: dev n). Sums are sequential in ascending index order per output element. Synchronous. */
+plss_status plss_spmv(plss_ctx *ctx, const double *x, double *y);
+plss_status plss_spmvT(plss_ctx *ctx, const double *u, double *v);
+
+/* Per-kernel device time of k loop steps launched one kernel at a time (not graphs), with CUDA
+ * events on the ctx stream around each launch; call after plss_start. ms (host, 5 doubles)
+ * receives the average per step of: K1 (all slabs), K2 (all slabs), the NCCL all-reduce,
+ * the distributed dots/tail kernel, K3. Synchronizes. */
+plss_status plss_profile(plss_ctx *ctx, int32_t k, double *ms);
+
+/* Introspection: kernel launches per loop step, number of slabs, grid sizes (for bench/ncu). */
+plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t *slabs,
+                       int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2);
+
+void plss_destroy(plss_ctx *ctx);
+const char *plss_status_str(plss_status s);
+const char *plss_last_error(const plss_ctx *ctx); /* NULL ctx: last error of create calls */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLSS_H */

@@ -1,0 +1,750 @@
+// plss.cu -- host side of libplss: the C ABI declared in include/plss.h.
+//
+// One ctx = one matrix on one device (one row block on a rank). Device memory comes from the
+// caller's workspace (torch); the library allocates only a few bytes of pinned host memory for
+// the done flag. The solve loop runs as CUDA graphs of `chunk` iterations; each iteration is
+//     for s in slabs: K1_s (r_s <- r_s - A_s p), K2_s (y += A_s^T r_s)     [2S launches]
+//     [rank > 1: ncclAllReduce(y | rho, n+1), K2b (phi, psi, tails)]
+//     K3 (p, x, theta)
+// K1_s and K2_s alternate so the slab of r that K1_s just wrote is gathered by K2_s while it is
+// still resident in L2.
+#include "../../include/plss.h"
+#include "plss_kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace plss;
+
+namespace {
+
+constexpr int MAXG = 2048;           // upper bound on persistent-CTA grid sizes (partials)
+constexpr int SCAN_ITEMS = 16;       // setup scan: items per thread
+constexpr size_t ALIGN = 256;
+
+std::string g_last_error;
+
+size_t align_up(size_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+
+int auto_slabs(int64_t m) {
+  const char* env = std::getenv("PLSS_SLABS");
+  if (env && std::atoi(env) > 0) return std::atoi(env);
+  const int64_t slab_bytes = 64ll << 20;  // r slab kept L2-resident between K1_s and K2_s
+  int64_t s = (m * 8 + slab_bytes - 1) / slab_bytes;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+}
+
+int64_t ntiles_of(int64_t nnz_s) { return std::max<int64_t>(1, (nnz_s + TILE - 1) / TILE); }
+
+struct Layout {
+  int S = 1;
+  bool dist = false;
+  int maxit_cap = 0;
+  size_t r, y, p, x, rec, ctl, counters, part1, part2, part3, partn, tile1, tile2, sptr, sidx,
+      sval, scan_cnt, scan_blk, buf, err, scalars, total;
+};
+
+bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, Layout* L) {
+  if (!A || A->m < 0 || A->n < 0 || A->nnz < 0 || A->nnz >= (1ll << 31)) return false;
+  plss_options o{};
+  if (opt) o = *opt;
+  int S = o.slabs > 0 ? o.slabs : auto_slabs(A->m);
+  if (A->m > 0) S = (int)std::min<int64_t>(S, A->m);
+  S = std::max(1, std::min(S, 64));
+  L->S = S;
+  L->dist = dist;
+  L->maxit_cap = o.maxit_cap > 0 ? o.maxit_cap : 20000;
+  const int64_t m = A->m, n = A->n, nnz = A->nnz;
+  const int64_t tiles_total = nnz / TILE + 2 * S + 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o2 = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o2; };
+  L->r = take(8 * m);
+  L->y = take(8 * (n + 1));      // dist: y | rho (the all-reduce buffer)
+  L->p = take(8 * n);
+  L->x = take(8 * n);
+  L->rec = take(8 * (size_t)(L->maxit_cap + 1) * REC);
+  L->ctl = take(sizeof(Ctl));
+  L->counters = take(64 * sizeof(unsigned));
+  L->part1 = take(16 * (size_t)MAXG * S);
+  L->part2 = take(16 * (size_t)MAXG);
+  L->part3 = take(16 * (size_t)MAXG);
+  L->partn = take(16 * (size_t)MAXG);
+  L->tile1 = take(4 * (size_t)(tiles_total + S));
+  L->tile2 = take(4 * (size_t)(tiles_total + S));
+  if (S > 1) {
+    L->sptr = take(4 * (size_t)S * (n + 1));
+    L->sidx = take(4 * (size_t)nnz);
+    L->sval = take(8 * (size_t)nnz);
+    L->scan_cnt = take(4 * (size_t)(n + 1));
+    L->scan_blk = take(4 * (size_t)((n + 1) / (NT * SCAN_ITEMS) + 2));
+  } else {
+    L->sptr = L->sidx = L->sval = L->scan_cnt = L->scan_blk = 0;
+  }
+  L->buf = L->y;
+  L->err = take(64);
+  L->scalars = take(64);
+  L->total = off;
+  return true;
+}
+
+// ---- setup scan (exclusive, int32, deterministic; one-time) --------------------------------
+__global__ void k_scan_local(int32_t* a, long long len, int32_t* blk) {
+  __shared__ int32_t tsum[NT];
+  const long long base = ((long long)blockIdx.x * NT + threadIdx.x) * SCAN_ITEMS;
+  int32_t s = 0;
+  for (int u = 0; u < SCAN_ITEMS; ++u) {
+    const long long i = base + u;
+    if (i < len) { const int32_t v = a[i]; a[i] = s; s += v; }
+  }
+  tsum[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int t = 0; t < NT; ++t) { const int32_t v = tsum[t]; tsum[t] = acc; acc += v; }
+    blk[blockIdx.x] = acc;
+  }
+  __syncthreads();
+  const int32_t off = tsum[threadIdx.x];
+  for (int u = 0; u < SCAN_ITEMS; ++u) {
+    const long long i = base + u;
+    if (i < len) a[i] += off;
+  }
+}
+__global__ void k_scan_blocks(int32_t* blk, int nb) {
+  int32_t acc = 0;
+  for (int b = 0; b < nb; ++b) { const int32_t v = blk[b]; blk[b] = acc; acc += v; }
+}
+__global__ void k_scan_add(int32_t* a, long long len, const int32_t* blk) {
+  const long long base = ((long long)blockIdx.x * NT + threadIdx.x) * SCAN_ITEMS;
+  const int32_t off = blk[blockIdx.x];
+  for (int u = 0; u < SCAN_ITEMS; ++u) {
+    const long long i = base + u;
+    if (i < len) a[i] += off;
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct plss_ctx {
+  int dev = 0;
+  cudaStream_t stream = nullptr;       // work stream (the caller's, or our own if it passed NULL)
+  cudaStream_t user_stream = nullptr;  // the caller's stream
+  bool own_stream = false;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  plss_matrix A{};
+  Layout L{};
+  int S = 1;
+  int64_t m = 0, n = 0, nnz = 0;
+  std::vector<int64_t> R, E;     // slab row bounds / entry bounds
+  char* ws = nullptr;
+  double *r = nullptr, *y = nullptr, *p = nullptr, *x = nullptr, *rec = nullptr;
+  Ctl* ctl = nullptr;
+  unsigned* counters = nullptr;
+  double *part1 = nullptr, *part2 = nullptr, *part3 = nullptr, *partn = nullptr;
+  double* scalars = nullptr;
+  std::vector<SpmvSeg> seg1, seg2;
+  std::vector<int> g1, g2;
+  int g3 = 1, gdots = 1, gnorm = 1;
+  int chunk = 16;
+  cudaGraphExec_t graph_chunk = nullptr, graph_one = nullptr;
+  // distributed
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  // solve state
+  bool started = false;
+  int maxit = 0, flags = 0;
+  int32_t* h_done = nullptr;     // pinned [2]
+  Ctl* h_ctl = nullptr;          // pinned staging
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::string err;
+};
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      set_err(ctx, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+      return PLSS_E_CUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+#define NK(call)                                                                    \
+  do {                                                                              \
+    ncclResult_t e_ = (call);                                                       \
+    if (e_ != ncclSuccess) {                                                        \
+      set_err(ctx, std::string(#call) + ": " + ncclGetErrorString(e_));             \
+      return PLSS_E_NCCL;                                                           \
+    }                                                                               \
+  } while (0)
+
+static void set_err(plss_ctx* ctx, const std::string& s) {
+  if (ctx) ctx->err = s;
+  g_last_error = s;
+}
+
+// order our work stream after / before the caller's stream when they differ
+static plss_status sync_in(plss_ctx* ctx) {
+  if (!ctx->own_stream) return PLSS_OK;
+  CK(cudaEventRecord(ctx->ev_in, ctx->user_stream));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0));
+  return PLSS_OK;
+}
+static plss_status sync_out(plss_ctx* ctx) {
+  if (!ctx->own_stream) return PLSS_OK;
+  CK(cudaEventRecord(ctx->ev_out, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->user_stream, ctx->ev_out, 0));
+  return PLSS_OK;
+}
+
+static int grid_for(int64_t work_units, int occ_per_sm, int sms) {
+  int64_t g = std::min<int64_t>(work_units, (int64_t)occ_per_sm * sms);
+  g = std::min<int64_t>(g, MAXG);
+  return (int)std::max<int64_t>(1, g);
+}
+
+// enqueue one loop step (also used inside graph capture)
+static plss_status enqueue_step(plss_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  for (int s = 0; s < ctx->S; ++s) {
+    k_spmv<ROLE_K1><<<ctx->g1[s], NT, 0, st>>>(ctx->seg1[s]);
+    if (ctx->seg2[s].finalize)
+      k_spmv<ROLE_K2DOTS><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+    else
+      k_spmv<ROLE_K2><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+  }
+  if (ctx->nranks > 1) {
+    NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
+    k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
+                                           ctx->part2, ctx->counters + 1);
+  }
+  k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
+                                     ctx->counters + 2);
+  CK(cudaGetLastError());
+  return PLSS_OK;
+}
+
+static plss_status build_graph(plss_ctx* ctx, int iters, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  plss_status st = PLSS_OK;
+  for (int i = 0; i < iters && st == PLSS_OK; ++i) st = enqueue_step(ctx);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (st != PLSS_OK) return st;
+  CK(e);
+  CK(cudaGraphInstantiate(out, g, 0));
+  CK(cudaGraphDestroy(g));
+  return PLSS_OK;
+}
+
+static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options* opt, void* workspace,
+                         size_t ws_bytes, void* stream, bool dist) {
+  ctx->A = *A;
+  ctx->m = A->m; ctx->n = A->n; ctx->nnz = A->nnz;
+  if (!compute_layout(A, opt, dist, &ctx->L)) { set_err(ctx, "invalid matrix sizes"); return PLSS_E_DIM; }
+  if (!workspace || ws_bytes < ctx->L.total) { set_err(ctx, "workspace too small"); return PLSS_E_DIM; }
+  if ((reinterpret_cast<uintptr_t>(workspace) & (ALIGN - 1)) != 0) { set_err(ctx, "workspace not 256-byte aligned"); return PLSS_E_INVALID; }
+  if (!A->row_ptr || !A->col_ptr || (A->nnz > 0 && (!A->col_idx || !A->val || !A->row_idx || !A->val_t))) {
+    set_err(ctx, "NULL matrix array"); return PLSS_E_INVALID;
+  }
+  if (opt && opt->flags != 0) { set_err(ctx, "options.flags must be 0"); return PLSS_E_INVALID; }
+  CK(cudaGetDevice(&ctx->dev));
+  ctx->user_stream = (cudaStream_t)stream;
+  if (ctx->user_stream == nullptr) {
+    // the legacy default stream cannot be captured into a graph: work on our own stream and
+    // order it against the caller's stream with events (sync_in / sync_out)
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  } else {
+    ctx->stream = ctx->user_stream;
+  }
+  CK(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  CK(cudaStreamSynchronize(ctx->user_stream));
+  cudaStream_t st = ctx->stream;
+  const Layout& L = ctx->L;
+  ctx->S = L.S;
+  ctx->ws = (char*)workspace;
+  char* w = ctx->ws;
+  ctx->r = (double*)(w + L.r); ctx->y = (double*)(w + L.y); ctx->p = (double*)(w + L.p);
+  ctx->x = (double*)(w + L.x); ctx->rec = (double*)(w + L.rec); ctx->ctl = (Ctl*)(w + L.ctl);
+  ctx->counters = (unsigned*)(w + L.counters);
+  ctx->part1 = (double*)(w + L.part1); ctx->part2 = (double*)(w + L.part2);
+  ctx->part3 = (double*)(w + L.part3); ctx->partn = (double*)(w + L.partn);
+  ctx->scalars = (double*)(w + L.scalars);
+  int* d_err = (int*)(w + L.err);
+  CK(cudaMemsetAsync(ctx->counters, 0, 64 * sizeof(unsigned), st));
+  CK(cudaMemsetAsync(ctx->part1, 0, 16 * (size_t)MAXG * L.S, st));
+  CK(cudaMemsetAsync(ctx->part2, 0, 16 * (size_t)MAXG, st));
+  CK(cudaMemsetAsync(ctx->part3, 0, 16 * (size_t)MAXG, st));
+  CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), st));
+  CK(cudaMemsetAsync(d_err, 0, 64, st));
+
+  const int64_t m = ctx->m, n = ctx->n, nnz = ctx->nnz;
+  // ---- validation --------------------------------------------------------------------------
+  if (A->validate) {
+    const int bs = 256;
+    k_validate<<<(unsigned)((std::max<int64_t>(m, 1) + bs - 1) / bs), bs, 0, st>>>(A->row_ptr, A->col_idx, A->val, m, n, nnz, d_err);
+    k_validate<<<(unsigned)((std::max<int64_t>(n, 1) + bs - 1) / bs), bs, 0, st>>>(A->col_ptr, A->row_idx, A->val_t, n, m, nnz, d_err + 1);
+    CK(cudaGetLastError());
+    int h_err[2] = {0, 0};
+    CK(cudaMemcpyAsync(h_err, d_err, sizeof(h_err), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_err[0] || h_err[1]) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "matrix format violation (csr flags %d, csc flags %d)", h_err[0], h_err[1]);
+      set_err(ctx, buf);
+      return PLSS_E_FORMAT;
+    }
+    if (n > 0)
+      k_validate_pair<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(A->row_ptr, A->col_idx, A->val, A->col_ptr, A->row_idx, A->val_t, n, d_err + 2);
+    CK(cudaGetLastError());
+    int h2 = 0;
+    CK(cudaMemcpyAsync(&h2, d_err + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h2) { set_err(ctx, "CSC copy is not the transpose of the CSR matrix"); return PLSS_E_FORMAT; }
+  }
+
+  // ---- slab bounds ---------------------------------------------------------------------------
+  const int S = ctx->S;
+  ctx->R.resize(S + 1);
+  ctx->E.resize(S + 1);
+  for (int s = 0; s <= S; ++s) ctx->R[s] = (m * s) / S;
+  {
+    std::vector<int32_t> tmp(S + 1);
+    for (int s = 0; s <= S; ++s)
+      CK(cudaMemcpyAsync(&tmp[s], A->row_ptr + ctx->R[s], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int s = 0; s <= S; ++s) ctx->E[s] = tmp[s];
+    if (ctx->E[0] != 0 || ctx->E[S] != nnz) { set_err(ctx, "row_ptr[0] != 0 or row_ptr[m] != nnz"); return PLSS_E_FORMAT; }
+  }
+
+  // ---- occupancy-derived persistent grids -----------------------------------------------------
+  int sms = 0, occ_spmv = 0, occ_vec = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_spmv, k_spmv<ROLE_K1>, NT, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_vec, k_pxupdate, NT, 0));
+  occ_spmv = std::max(1, occ_spmv);
+  occ_vec = std::max(1, occ_vec);
+
+  // ---- K1 segments (CSR row slabs) ----------------------------------------------------------
+  int32_t* tile1 = (int32_t*)(w + L.tile1);
+  int32_t* tile2 = (int32_t*)(w + L.tile2);
+  size_t t1off = 0, t2off = 0;
+  ctx->seg1.resize(S);
+  ctx->seg2.resize(S);
+  ctx->g1.resize(S);
+  ctx->g2.resize(S);
+  for (int s = 0; s < S; ++s) {
+    SpmvSeg& a = ctx->seg1[s];
+    memset(&a, 0, sizeof a);
+    const int64_t rows = ctx->R[s + 1] - ctx->R[s];
+    const int64_t nt = ntiles_of(ctx->E[s + 1] - ctx->E[s]);
+    a.ptr = A->row_ptr + ctx->R[s];
+    a.idx = A->col_idx;
+    a.val = A->val;
+    a.tile_first = tile1 + t1off;
+    a.e0 = ctx->E[s];
+    a.nrows = (int32_t)rows;
+    a.ntiles = (int32_t)nt;
+    a.g = ctx->p;
+    a.out = ctx->r + ctx->R[s];
+    a.partial = ctx->part1 + 2 * (size_t)MAXG * s;
+    a.part_base = ctx->part1;
+    a.nparts = MAXG * S;
+    a.finalize = (s == S - 1);
+    a.dist = dist ? 1 : 0;
+    a.counter = ctx->counters + 0;
+    a.ctl = ctx->ctl;
+    a.rec = ctx->rec;
+    a.rho_out = ctx->y + n;
+    k_tile_map<<<(unsigned)((nt + 1 + 255) / 256), 256, 0, st>>>(a.ptr, a.nrows, a.e0, a.ntiles, (int32_t*)a.tile_first);
+    t1off += nt + 1;
+    ctx->g1[s] = grid_for(nt, occ_spmv, sms);
+  }
+  CK(cudaGetLastError());
+
+  // ---- K2 segments (CSC, slab-major copy when S > 1) ----------------------------------------
+  int32_t *sptr = nullptr, *sidx = nullptr;
+  double* sval = nullptr;
+  if (S > 1) {
+    sptr = (int32_t*)(w + L.sptr);
+    sidx = (int32_t*)(w + L.sidx);
+    sval = (double*)(w + L.sval);
+    int32_t* blk = (int32_t*)(w + L.scan_blk);
+    const long long len = n + 1;
+    const unsigned nblk = (unsigned)((len + NT * SCAN_ITEMS - 1) / (NT * SCAN_ITEMS));
+    for (int s = 0; s < S; ++s) {
+      int32_t* sp = sptr + (size_t)s * (n + 1);
+      k_slab_count<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(A->col_ptr, A->row_idx, n, ctx->R[s], ctx->R[s + 1], sp);
+      k_scan_local<<<nblk, NT, 0, st>>>(sp, len, blk);
+      k_scan_blocks<<<1, 1, 0, st>>>(blk, (int)nblk);
+      k_scan_add<<<nblk, NT, 0, st>>>(sp, len, blk);
+        k_slab_copy<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(A->col_ptr, A->row_idx, A->val_t, n, ctx->R[s], ctx->R[s + 1], ctx->E[s], sp, sidx, sval);
+    }
+    CK(cudaGetLastError());
+  }
+  for (int s = 0; s < S; ++s) {
+    SpmvSeg& a = ctx->seg2[s];
+    memset(&a, 0, sizeof a);
+    const int64_t nt = ntiles_of(ctx->E[s + 1] - ctx->E[s]);
+    if (S > 1) {
+      a.ptr = sptr + (size_t)s * (n + 1);
+      a.idx = sidx;
+      a.val = sval;
+      a.e0 = ctx->E[s];
+      a.g = ctx->r + ctx->R[s];
+    } else {
+      a.ptr = A->col_ptr;
+      a.idx = A->row_idx;
+      a.val = A->val_t;
+      a.e0 = 0;
+      a.g = ctx->r;
+    }
+    a.tile_first = tile2 + t2off;
+    a.nrows = (int32_t)n;
+    a.ntiles = (int32_t)nt;
+    a.out = ctx->y;
+    a.pv = ctx->p;
+    a.partial = ctx->part2;
+    a.part_base = ctx->part2;
+    a.nparts = MAXG;
+    a.accumulate = (s > 0);
+    a.finalize = (!dist && s == S - 1);
+    a.counter = ctx->counters + 1;
+    a.ctl = ctx->ctl;
+    a.rec = ctx->rec;
+    k_tile_map<<<(unsigned)((nt + 1 + 255) / 256), 256, 0, st>>>(a.ptr, a.nrows, a.e0, a.ntiles, (int32_t*)a.tile_first);
+    t2off += nt + 1;
+    ctx->g2[s] = grid_for(nt, occ_spmv, sms);
+  }
+  CK(cudaGetLastError());
+  ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
+  ctx->gdots = grid_for((n + NT - 1) / NT + 1, occ_vec, sms);
+  ctx->gnorm = grid_for((m + NT - 1) / NT + 1, occ_vec, sms);
+
+  CK(cudaHostAlloc((void**)&ctx->h_done, 2 * sizeof(int32_t), cudaHostAllocDefault));
+  CK(cudaHostAlloc((void**)&ctx->h_ctl, sizeof(Ctl), cudaHostAllocDefault));
+  CK(cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming));
+  ctx->chunk = (opt && opt->graph_chunk > 0) ? opt->graph_chunk : 16;
+  CK(cudaStreamSynchronize(st));
+  return PLSS_OK;
+}
+
+static plss_status finish_create(plss_ctx* ctx) {
+  // graphs are captured after setup so their nodes carry the final kernel parameters
+  // (the device state they read is reset by plss_start); capture does not execute kernels
+  plss_status st = build_graph(ctx, ctx->chunk, &ctx->graph_chunk);
+  if (st != PLSS_OK) return st;
+  st = build_graph(ctx, 1, &ctx->graph_one);
+  if (st != PLSS_OK) return st;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PLSS_OK;
+}
+
+extern "C" {
+
+size_t plss_workspace_bytes(const plss_matrix* A, const plss_options* opt) {
+  Layout L;
+  if (!compute_layout(A, opt, false, &L)) return 0;
+  return L.total;
+}
+
+plss_status plss_create(const plss_matrix* A, const plss_options* opt, void* workspace, size_t ws_bytes,
+                        void* cuda_stream, plss_ctx** out) {
+  if (!A || !out) { g_last_error = "NULL argument"; return PLSS_E_INVALID; }
+  *out = nullptr;
+  plss_ctx* ctx = new (std::nothrow) plss_ctx();
+  if (!ctx) return PLSS_E_NOMEM;
+  plss_status st = setup(ctx, A, opt, workspace, ws_bytes, cuda_stream, false);
+  if (st == PLSS_OK) st = finish_create(ctx);
+  if (st != PLSS_OK) { g_last_error = ctx->err; plss_destroy(ctx); return st; }
+  *out = ctx;
+  return PLSS_OK;
+}
+
+plss_status plss_get_unique_id(uint8_t id[128]) {
+  if (!id) return PLSS_E_INVALID;
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) { g_last_error = ncclGetErrorString(r); return PLSS_E_NCCL; }
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  return PLSS_OK;
+}
+
+plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int64_t m_global,
+                             const uint8_t id[128], int32_t rank, int32_t nranks, const plss_options* opt,
+                             void* workspace, size_t ws_bytes, void* cuda_stream, plss_ctx** out) {
+  if (!A_local || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) { g_last_error = "invalid argument"; return PLSS_E_INVALID; }
+  if (row_offset < 0 || row_offset + A_local->m > m_global) { g_last_error = "row block outside the global matrix"; return PLSS_E_DIM; }
+  *out = nullptr;
+  plss_ctx* ctx = new (std::nothrow) plss_ctx();
+  if (!ctx) return PLSS_E_NOMEM;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, nranks > 1);
+  if (st == PLSS_OK && nranks > 1) {
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, u, rank);
+    if (r != ncclSuccess) { set_err(ctx, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); st = PLSS_E_NCCL; }
+  }
+  if (st == PLSS_OK) st = finish_create(ctx);
+  if (st != PLSS_OK) { g_last_error = ctx->err; plss_destroy(ctx); return st; }
+  *out = ctx;
+  return PLSS_OK;
+}
+
+plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
+                       int32_t maxit, int32_t flags) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap || (tol_mode != 0 && tol_mode != 1) ||
+      (flags & ~1) != 0) {
+    set_err(ctx, "invalid tol / tol_mode / maxit / flags");
+    return PLSS_E_INVALID;
+  }
+  if (!b && ctx->m > 0) { set_err(ctx, "b is NULL"); return PLSS_E_INVALID; }
+  cudaStream_t st = ctx->stream;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  const int64_t m = ctx->m, n = ctx->n;
+  Ctl& c = *ctx->h_ctl;
+  memset(&c, 0, sizeof c);
+  c.nbd = 1.0;
+  c.tol = tol;
+  c.freeze_h = 64.0 * 2.220446049250313e-16;
+  c.maxit = maxit;
+  c.freeze = flags & 1;
+  c.tol_mode = tol_mode;
+  c.outcome = OUT_RUNNING;
+  CK(cudaMemcpyAsync(ctx->ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->rec, 0, 8 * (size_t)(maxit + 1) * REC, st));
+  if (m > 0) CK(cudaMemcpyAsync(ctx->r, b, 8 * (size_t)m, is_device_ptr(b) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (n > 0) {
+    if (x0) {
+      const cudaMemcpyKind kind = is_device_ptr(x0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+      CK(cudaMemcpyAsync(ctx->p, x0, 8 * (size_t)n, kind, st));   // K1 of step 0 gathers x0: r = b - A x0
+      CK(cudaMemcpyAsync(ctx->x, x0, 8 * (size_t)n, kind, st));
+    } else {
+      CK(cudaMemsetAsync(ctx->p, 0, 8 * (size_t)n, st));
+      CK(cudaMemsetAsync(ctx->x, 0, 8 * (size_t)n, st));
+    }
+  }
+  if (ctx->nranks > 1) {
+    k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 0, ctx->scalars);
+    CK(cudaGetLastError());
+    NK(ncclAllReduce(ctx->scalars, ctx->scalars, 1, ncclFloat64, ncclSum, ctx->comm, st));
+    k_set_nbd<<<1, 1, 0, st>>>(ctx->ctl, ctx->scalars);
+  } else {
+    k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 1, nullptr);
+  }
+  CK(cudaGetLastError());
+  ctx->started = true;
+  ctx->maxit = maxit;
+  ctx->flags = flags;
+  return PLSS_OK;
+}
+
+plss_status plss_step(plss_ctx* ctx, int32_t k) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->started) { set_err(ctx, "plss_step before plss_start"); return PLSS_E_STATE; }
+  if (k < 0) return PLSS_E_INVALID;
+  for (int i = 0; i + ctx->chunk <= k; i += ctx->chunk) CK(cudaGraphLaunch(ctx->graph_chunk, ctx->stream));
+  for (int i = 0; i < k % ctx->chunk; ++i) CK(cudaGraphLaunch(ctx->graph_one, ctx->stream));
+  return PLSS_OK;
+}
+
+plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
+                        plss_outcome* outcome) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->started) { set_err(ctx, "plss_finish before plss_start"); return PLSS_E_STATE; }
+  cudaStream_t st = ctx->stream;
+  if (x && ctx->n > 0)
+    CK(cudaMemcpyAsync(x, ctx->x, 8 * (size_t)ctx->n, is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  std::vector<double> rec;
+  if (hist || diag) {
+    rec.resize((size_t)(ctx->maxit + 1) * REC);
+    CK(cudaMemcpyAsync(rec.data(), ctx->rec, 8 * rec.size(), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (sync_out(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  const Ctl& c = *ctx->h_ctl;
+  if (iters) *iters = c.iters;
+  if (outcome) *outcome = c.done ? (plss_outcome)c.outcome : PLSS_RUNNING;
+  if (hist) for (int k = 0; k <= ctx->maxit; ++k) hist[k] = rec[(size_t)k * REC];
+  if (diag) memcpy(diag, rec.data(), 8 * rec.size());
+  return PLSS_OK;
+}
+
+plss_status plss_solve(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
+                       int32_t maxit, int32_t flags, double* x, int32_t* iters, double* hist, double* diag,
+                       plss_outcome* outcome) {
+  plss_status s = plss_start(ctx, b, x0, tol, tol_mode, maxit, flags);
+  if (s != PLSS_OK) return s;
+  cudaStream_t st = ctx->stream;
+  // keep <= 2 chunks in flight; poll the device done flag of the older one
+  int issued = 0, slot = 0;
+  bool pending[2] = {false, false};
+  while (issued < maxit) {
+    const bool full = (maxit - issued) >= ctx->chunk;
+    if (full) {
+      CK(cudaGraphLaunch(ctx->graph_chunk, st));
+      issued += ctx->chunk;
+    } else {
+      for (int i = issued; i < maxit; ++i) CK(cudaGraphLaunch(ctx->graph_one, st));
+      issued = maxit;
+    }
+    CK(cudaMemcpyAsync(&ctx->h_done[slot], &ctx->ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ctx->ev[slot], st));
+    pending[slot] = true;
+    slot ^= 1;
+    if (pending[slot]) {
+      CK(cudaEventSynchronize(ctx->ev[slot]));
+      pending[slot] = false;
+      if (ctx->h_done[slot]) break;
+    }
+  }
+  return plss_finish(ctx, x, iters, hist, diag, outcome);
+}
+
+plss_status plss_spmv(plss_ctx* ctx, const double* x, double* y) {
+  if (!ctx || (!x && ctx->n > 0) || (!y && ctx->m > 0)) return PLSS_E_INVALID;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  for (int s = 0; s < ctx->S; ++s) {
+    SpmvSeg a = ctx->seg1[s];
+    a.g = x;
+    a.out = y + ctx->R[s];
+    a.ctl = nullptr;
+    k_spmv<ROLE_PLAIN><<<ctx->g1[s], NT, 0, ctx->stream>>>(a);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return sync_out(ctx);
+}
+
+plss_status plss_spmvT(plss_ctx* ctx, const double* u, double* v) {
+  if (!ctx || (!u && ctx->m > 0) || (!v && ctx->n > 0)) return PLSS_E_INVALID;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  for (int s = 0; s < ctx->S; ++s) {
+    SpmvSeg a = ctx->seg2[s];
+    a.g = u + ctx->R[s] * (ctx->S > 1 ? 1 : 0);
+    a.out = v;
+    a.ctl = nullptr;
+    a.finalize = 0;
+    k_spmv<ROLE_K2><<<ctx->g2[s], NT, 0, ctx->stream>>>(a);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return sync_out(ctx);
+}
+
+plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
+  if (!ctx || !ms || k < 1) return PLSS_E_INVALID;
+  if (!ctx->started) { set_err(ctx, "plss_profile before plss_start"); return PLSS_E_STATE; }
+  cudaStream_t st = ctx->stream;
+  const int nev = 2 * ctx->S + 4;
+  std::vector<cudaEvent_t> ev(nev);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[5] = {0, 0, 0, 0, 0};
+  for (int it = 0; it < k; ++it) {
+    int q = 0;
+    CK(cudaEventRecord(ev[q++], st));
+    for (int s = 0; s < ctx->S; ++s) {
+      k_spmv<ROLE_K1><<<ctx->g1[s], NT, 0, st>>>(ctx->seg1[s]);
+      CK(cudaEventRecord(ev[q++], st));
+      if (ctx->seg2[s].finalize) k_spmv<ROLE_K2DOTS><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+      else k_spmv<ROLE_K2><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+      CK(cudaEventRecord(ev[q++], st));
+    }
+    if (ctx->nranks > 1) {
+      NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
+      CK(cudaEventRecord(ev[q++], st));
+      k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
+                                             ctx->part2, ctx->counters + 1);
+      CK(cudaEventRecord(ev[q++], st));
+    }
+    k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
+                                       ctx->counters + 2);
+    CK(cudaEventRecord(ev[q++], st));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    float t;
+    int e = 0;
+    for (int s = 0; s < ctx->S; ++s) {
+      CK(cudaEventElapsedTime(&t, ev[e], ev[e + 1])); acc[0] += t;
+      CK(cudaEventElapsedTime(&t, ev[e + 1], ev[e + 2])); acc[1] += t;
+      e += 2;
+    }
+    if (ctx->nranks > 1) {
+      CK(cudaEventElapsedTime(&t, ev[e], ev[e + 1])); acc[2] += t;
+      CK(cudaEventElapsedTime(&t, ev[e + 1], ev[e + 2])); acc[3] += t;
+      e += 2;
+    }
+    CK(cudaEventElapsedTime(&t, ev[e], ev[e + 1])); acc[4] += t;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int i = 0; i < 5; ++i) ms[i] = acc[i] / k;
+  return PLSS_OK;
+}
+
+plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t* slabs, int32_t* tile_nnz,
+                       int32_t* grid_k1, int32_t* grid_k2) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (launches_per_step) *launches_per_step = 2 * ctx->S + 1 + (ctx->nranks > 1 ? 1 : 0);
+  if (slabs) *slabs = ctx->S;
+  if (tile_nnz) *tile_nnz = TILE;
+  if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];
+  if (grid_k2) *grid_k2 = ctx->g2.empty() ? 0 : ctx->g2[0];
+  return PLSS_OK;
+}
+
+void plss_destroy(plss_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->graph_chunk) cudaGraphExecDestroy(ctx->graph_chunk);
+  if (ctx->graph_one) cudaGraphExecDestroy(ctx->graph_one);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->h_done) cudaFreeHost(ctx->h_done);
+  if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* plss_status_str(plss_status s) {
+  switch (s) {
+    case PLSS_OK: return "ok";
+    case PLSS_E_INVALID: return "invalid argument";
+    case PLSS_E_DIM: return "dimension mismatch";
+    case PLSS_E_FORMAT: return "matrix format violation";
+    case PLSS_E_CUDA: return "CUDA error";
+    case PLSS_E_NCCL: return "NCCL error";
+    case PLSS_E_NOMEM: return "out of host memory";
+    case PLSS_E_STATE: return "call out of order";
+  }
+  return "unknown status";
+}
+
+const char* plss_last_error(const plss_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  return g_last_error.c_str();
+}
+
+}  // extern "C"

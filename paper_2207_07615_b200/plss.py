@@ -1,0 +1,322 @@
+"""Thin ctypes binding of libplss (include/plss.h): argument marshalling only.
+
+Every step of the PLSS path runs in libplss's sm_100a kernels; torch provides device memory
+(the matrix copies and the workspace), streams and, for the distributed path, the process group
+that broadcasts the NCCL unique id. There is no CPU fallback: if libplss.so is missing or no CUDA
+device is present, the calls raise.
+
+Names mirror the C ABI: plss_workspace_bytes, plss_create, plss_create_dist, plss_get_unique_id,
+plss_solve, plss_start, plss_step, plss_finish, plss_spmv, plss_spmvT, plss_query, plss_destroy.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libplss.so")
+REC = 8
+OUTCOMES = {0: "converged", 1: "maxit", 2: "y_vanished", 3: "stagnation", -1: "running"}
+
+# C ABI symbols declared in include/plss.h (checked by tests/test_abi.py)
+SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_create_dist",
+           "plss_solve", "plss_start", "plss_step", "plss_finish", "plss_spmv", "plss_spmvT",
+           "plss_profile", "plss_query", "plss_destroy", "plss_status_str", "plss_last_error"]
+
+
+class PlssError(RuntimeError):
+    pass
+
+
+class plss_matrix(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("n", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("val", ctypes.c_void_p),
+                ("col_ptr", ctypes.c_void_p), ("row_idx", ctypes.c_void_p), ("val_t", ctypes.c_void_p),
+                ("validate", ctypes.c_int32)]
+
+
+class plss_options(ctypes.Structure):
+    _fields_ = [("slabs", ctypes.c_int32), ("graph_chunk", ctypes.c_int32),
+                ("maxit_cap", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libplss.so (raises if it was not built). torch is imported first so that the NCCL
+    it bundles is the one libplss resolves."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    import torch  # noqa: F401  (loads torch's libnccl.so.2 / CUDA runtime)
+    if not os.path.exists(path):
+        raise PlssError(f"{path} is missing: run `python -m paper_2207_07615_b200.build` "
+                        "(no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    st = ctypes.c_int
+    lib.plss_workspace_bytes.argtypes = [ctypes.POINTER(plss_matrix), ctypes.POINTER(plss_options)]
+    lib.plss_workspace_bytes.restype = ctypes.c_size_t
+    lib.plss_create.argtypes = [ctypes.POINTER(plss_matrix), ctypes.POINTER(plss_options), P,
+                                ctypes.c_size_t, P, ctypes.POINTER(P)]
+    lib.plss_create.restype = st
+    lib.plss_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.plss_get_unique_id.restype = st
+    lib.plss_create_dist.argtypes = [ctypes.POINTER(plss_matrix), I64, I64, ctypes.c_char_p, I32, I32,
+                                     ctypes.POINTER(plss_options), P, ctypes.c_size_t, P,
+                                     ctypes.POINTER(P)]
+    lib.plss_create_dist.restype = st
+    lib.plss_solve.argtypes = [P, P, P, D, I32, I32, I32, P, ctypes.POINTER(I32), P, P,
+                               ctypes.POINTER(ctypes.c_int)]
+    lib.plss_solve.restype = st
+    lib.plss_start.argtypes = [P, P, P, D, I32, I32, I32]
+    lib.plss_start.restype = st
+    lib.plss_step.argtypes = [P, I32]
+    lib.plss_step.restype = st
+    lib.plss_finish.argtypes = [P, P, ctypes.POINTER(I32), P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_finish.restype = st
+    lib.plss_spmv.argtypes = [P, P, P]
+    lib.plss_spmv.restype = st
+    lib.plss_spmvT.argtypes = [P, P, P]
+    lib.plss_spmvT.restype = st
+    lib.plss_profile.argtypes = [P, I32, P]
+    lib.plss_profile.restype = st
+    lib.plss_query.argtypes = [P] + [ctypes.POINTER(I32)] * 5
+    lib.plss_query.restype = st
+    lib.plss_destroy.argtypes = [P]
+    lib.plss_destroy.restype = None
+    lib.plss_status_str.argtypes = [st]
+    lib.plss_status_str.restype = ctypes.c_char_p
+    lib.plss_last_error.argtypes = [P]
+    lib.plss_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(status: int, ctx_ptr=None):
+    if status != 0:
+        lib = load_library()
+        msg = lib.plss_last_error(ctx_ptr)
+        raise PlssError(f"{lib.plss_status_str(status).decode()}: {(msg or b'').decode()}")
+
+
+def _ptr(a) -> Optional[int]:
+    """Device or host address of a torch tensor / numpy array (None passes through)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+@dataclass
+class Matrix:
+    """Device CSR + CSC copies of A (torch tensors, int32 / float64), borrowed by a ctx."""
+    m: int
+    n: int
+    row_ptr: "object"
+    col_idx: "object"
+    val: "object"
+    col_ptr: "object"
+    row_idx: "object"
+    val_t: "object"
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @classmethod
+    def from_arrays(cls, m, n, row_ptr, col_idx, val, col_ptr, row_idx, val_t, device="cuda"):
+        import torch
+
+        def t(a, dt):
+            if isinstance(a, torch.Tensor):
+                return a.to(device=device, dtype=dt).contiguous()
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+        return cls(int(m), int(n), t(row_ptr, torch.int32), t(col_idx, torch.int32),
+                   t(val, torch.float64), t(col_ptr, torch.int32), t(row_idx, torch.int32),
+                   t(val_t, torch.float64))
+
+    def c_struct(self, validate=False) -> plss_matrix:
+        return plss_matrix(self.m, self.n, self.nnz, _ptr(self.row_ptr), _ptr(self.col_idx),
+                           _ptr(self.val), _ptr(self.col_ptr), _ptr(self.row_idx), _ptr(self.val_t),
+                           1 if validate else 0)
+
+
+def _opts(slabs=0, graph_chunk=0, maxit_cap=0):
+    return plss_options(int(slabs), int(graph_chunk), int(maxit_cap), 0)
+
+
+def plss_workspace_bytes(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=0) -> int:
+    lib = load_library()
+    ms = A.c_struct()
+    o = _opts(slabs, graph_chunk, maxit_cap)
+    nbytes = lib.plss_workspace_bytes(ctypes.byref(ms), ctypes.byref(o))
+    if nbytes == 0:
+        raise PlssError("invalid matrix sizes")
+    return int(nbytes)
+
+
+class Ctx:
+    """Owns the ctx handle, the torch workspace and references to the borrowed matrix."""
+
+    def __init__(self, handle, A: Matrix, workspace, stream, maxit_cap):
+        self.handle = handle
+        self.A = A
+        self.workspace = workspace
+        self.stream = stream
+        self.maxit_cap = maxit_cap
+        self._maxit = 0
+
+    @property
+    def m(self):
+        return self.A.m
+
+    @property
+    def n(self):
+        return self.A.n
+
+    def __del__(self):
+        try:
+            plss_destroy(self)
+        except Exception:
+            pass
+
+
+def _alloc_workspace(nbytes: int, device):
+    import torch
+    return torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+
+
+def _aligned(ws) -> int:
+    p = ws.data_ptr()
+    return (p + 255) // 256 * 256
+
+
+def plss_create(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False) -> Ctx:
+    lib = load_library()
+    nbytes = plss_workspace_bytes(A, slabs, graph_chunk, maxit_cap)
+    ws = _alloc_workspace(nbytes, A.row_ptr.device)
+    h = ctypes.c_void_p()
+    ms = A.c_struct(validate)
+    o = _opts(slabs, graph_chunk, maxit_cap)
+    _check(lib.plss_create(ctypes.byref(ms), ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream),
+                           ctypes.byref(h)))
+    return Ctx(h, A, ws, stream, maxit_cap)
+
+
+def plss_get_unique_id() -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.plss_get_unique_id(buf))
+    return buf.raw
+
+
+def plss_create_dist(A_local: Matrix, row_offset: int, m_global: int, uid: bytes, rank: int, nranks: int,
+                     slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False) -> Ctx:
+    lib = load_library()
+    nbytes = plss_workspace_bytes(A_local, slabs, graph_chunk, maxit_cap)
+    ws = _alloc_workspace(nbytes, A_local.row_ptr.device)
+    h = ctypes.c_void_p()
+    ms = A_local.c_struct(validate)
+    o = _opts(slabs, graph_chunk, maxit_cap)
+    _check(lib.plss_create_dist(ctypes.byref(ms), int(row_offset), int(m_global), uid, int(rank), int(nranks),
+                                ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream), ctypes.byref(h)))
+    return Ctx(h, A_local, ws, stream, maxit_cap)
+
+
+def plss_start(ctx: Ctx, b, x0=None, tol=1e-8, tol_mode=0, maxit=100, flags=0):
+    lib = load_library()
+    ctx._keep = (b, x0)
+    ctx._maxit = int(maxit)
+    _check(lib.plss_start(ctx.handle, _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), int(flags)),
+           ctx.handle)
+
+
+def plss_step(ctx: Ctx, k: int):
+    _check(load_library().plss_step(ctx.handle, int(k)), ctx.handle)
+
+
+def plss_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
+    """Returns dict(iters, outcome, hist, diag); x (host or device buffer) receives the iterate."""
+    lib = load_library()
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(ctx._maxit + 1) if want_hist else None
+    diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
+    _check(lib.plss_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+           ctx.handle)
+    return _result(it.value, oc.value, hist, diag, x)
+
+
+def _result(iters, oc, hist, diag, x):
+    out = {"iters": iters, "outcome": OUTCOMES.get(oc, str(oc)), "outcome_code": oc, "x": x}
+    if hist is not None:
+        nh = iters if oc == 1 else iters + 1
+        out["hist_full"] = hist
+        out["hist"] = hist[:max(1, min(nh, hist.shape[0]))].copy()
+    if diag is not None:
+        out["diag"] = diag
+    return out
+
+
+def plss_solve(ctx: Ctx, b, x0=None, tol=1e-8, tol_mode=0, maxit=100, flags=0, x=None,
+               want_hist=True, want_diag=False):
+    """Full solve. b / x0 / x may be device tensors or host arrays (numpy / CPU tensors).
+    If x is None a device tensor is allocated. Returns dict(x, iters, outcome, hist[, diag])."""
+    import torch
+    lib = load_library()
+    if x is None:
+        x = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(maxit + 1) if want_hist else None
+    diag = np.zeros((maxit + 1, REC)) if want_diag else None
+    ctx._maxit = int(maxit)
+    _check(lib.plss_solve(ctx.handle, _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), int(flags),
+                          _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if flags & 1:
+        res["hist"] = hist[:it.value].copy()
+    return res
+
+
+def plss_spmv(ctx: Ctx, x, y):
+    _check(load_library().plss_spmv(ctx.handle, _ptr(x), _ptr(y)), ctx.handle)
+    return y
+
+
+def plss_spmvT(ctx: Ctx, u, v):
+    _check(load_library().plss_spmvT(ctx.handle, _ptr(u), _ptr(v)), ctx.handle)
+    return v
+
+
+def plss_profile(ctx: Ctx, k: int) -> dict:
+    """Average device ms per loop step of each kernel class (CUDA events, non-graph launches)."""
+    ms = np.zeros(5)
+    _check(load_library().plss_profile(ctx.handle, int(k), _ptr(ms)), ctx.handle)
+    return dict(zip(["k1", "k2", "allreduce", "dots", "k3"], ms.tolist()))
+
+
+def plss_query(ctx: Ctx) -> dict:
+    vals = [ctypes.c_int32(0) for _ in range(5)]
+    _check(load_library().plss_query(ctx.handle, *[ctypes.byref(v) for v in vals]), ctx.handle)
+    keys = ["launches_per_step", "slabs", "tile_nnz", "grid_k1", "grid_k2"]
+    return {k: v.value for k, v in zip(keys, vals)}
+
+
+def plss_destroy(ctx: Ctx):
+    if ctx.handle:
+        load_library().plss_destroy(ctx.handle)
+        ctx.handle = None

@@ -225,56 +225,63 @@ def c5_banded(seed=0, m=64_000_000, n=8_000_000, band=6, unif=6, half=1024, maxi
 
 
 def make_c5_torch(device="cuda", seed=0, m=64_000_000, n=8_000_000, band=6, unif=6, half=1024,
-                  chunk=8_000_000):
+                  rows=None, chunk=1_000_000):
     """Full-size C5 generated on a device with torch's Philox stream (same recipe as
-    `c5_banded`, different stream). Returns a dict of torch tensors on `device`:
-    row_ptr, col_idx, val, col_ptr, row_idx, val_t (int32 / float64), b, x_star."""
+    `c5_banded`, different stream). Rows are drawn in chunks of `chunk` rows, chunk c from its
+    own generator seeded (seed, c), so any row block [r0, r1) aligned to chunks (every
+    m/G block for G in 1, 2, 4, 8) is generated identically on its own by the rank that owns
+    it. Returns a dict of torch tensors on `device` for the row block `rows` (default all):
+    row_ptr, col_idx, val (local CSR), col_ptr, row_idx, val_t (local CSC over all n columns),
+    b (local), x_star (full n), plus m, n, row_offset, m_global."""
     import torch
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
+    r0, r1 = (0, m) if rows is None else rows
+    assert r0 % chunk == 0 and (r1 % chunk == 0 or r1 == m), "row block must align to chunks"
     per = band + unif
     w = min(2 * half + 1, n)
-    col_idx = torch.empty(m * per, dtype=torch.int32, device=device)
-    for r0 in range(0, m, chunk):
-        r1 = min(m, r0 + chunk)
-        rows = torch.arange(r0, r1, device=device, dtype=torch.int64)
-        lo = torch.clamp(rows * n // m - half, 0, n - w)
+    gx = torch.Generator(device=device)
+    gx.manual_seed(seed * 1_000_003 + 999_999)
+    x_star = torch.randn(n, generator=gx, device=device, dtype=torch.float64)
+    ml = r1 - r0
+    col_idx = torch.empty(ml * per, dtype=torch.int32, device=device)
+    val = torch.empty(ml * per, dtype=torch.float64, device=device)
+    b = torch.empty(ml, dtype=torch.float64, device=device)
+    for c0 in range(r0, r1, chunk):
+        c1 = min(r1, c0 + chunk)
+        g = torch.Generator(device=device)
+        g.manual_seed(seed * 1_000_003 + c0 // chunk)
+        rws = torch.arange(c0, c1, device=device, dtype=torch.int64)
+        lo = torch.clamp(rws * n // m - half, 0, n - w)
 
         def draw(k, lo_k):
             bc = lo_k[:, None] + torch.randint(0, w, (k, band), generator=g, device=device)
             uc = torch.randint(0, n, (k, unif), generator=g, device=device)
             return torch.sort(torch.cat([bc, uc], dim=1), dim=1).values
 
-        cols = draw(r1 - r0, lo)
+        cols = draw(c1 - c0, lo)
         while True:
             dup = torch.nonzero((cols[:, 1:] == cols[:, :-1]).any(dim=1)).flatten()
             if dup.numel() == 0:
                 break
             cols[dup] = draw(dup.numel(), lo[dup])
-        col_idx[r0 * per:r1 * per] = cols.reshape(-1).to(torch.int32)
-        del cols, rows, lo
-    val = torch.randn(m * per, generator=g, device=device, dtype=torch.float64)
-    x_star = torch.randn(n, generator=g, device=device, dtype=torch.float64)
-    row_ptr = torch.arange(0, m * per + 1, per, device=device, dtype=torch.int32)
-    # b = A x* (input synthesis, library sparse product)
-    b = torch.empty(m, dtype=torch.float64, device=device)
-    for r0 in range(0, m, chunk):
-        r1 = min(m, r0 + chunk)
-        seg = slice(r0 * per, r1 * per)
-        prod = val[seg] * x_star[col_idx[seg].long()]
-        b[r0:r1] = prod.view(r1 - r0, per).sum(dim=1)
-        del prod
+        seg = slice((c0 - r0) * per, (c1 - r0) * per)
+        col_idx[seg] = cols.reshape(-1).to(torch.int32)
+        v = torch.randn((c1 - c0) * per, generator=g, device=device, dtype=torch.float64)
+        val[seg] = v
+        # b = A x* for these rows (input synthesis, library product)
+        b[c0 - r0:c1 - r0] = (v * x_star[cols.reshape(-1)]).view(c1 - c0, per).sum(dim=1)
+        del cols, rws, lo, v
+    row_ptr = torch.arange(0, ml * per + 1, per, device=device, dtype=torch.int32)
     # stable transpose on device (index work only)
     order = torch.sort(col_idx, stable=True).indices
-    row_idx = (order // per).to(torch.int32)   # row of each entry (row_ptr is i*per)
+    row_idx = torch.div(order, per, rounding_mode="floor").to(torch.int32)
     val_t = val[order]
     del order
     counts = torch.bincount(col_idx, minlength=n)
     col_ptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
     torch.cumsum(counts, 0, out=col_ptr[1:])
-    return {"m": m, "n": n, "row_ptr": row_ptr, "col_idx": col_idx, "val": val,
-            "col_ptr": col_ptr.to(torch.int32), "row_idx": row_idx, "val_t": val_t,
-            "b": b, "x_star": x_star}
+    return {"m": ml, "n": n, "row_offset": r0, "m_global": m, "row_ptr": row_ptr,
+            "col_idx": col_idx, "val": val, "col_ptr": col_ptr.to(torch.int32), "row_idx": row_idx,
+            "val_t": val_t, "b": b, "x_star": x_star}
 
 
 # name -> (factory, kwargs). "s" suffixes are scaled versions for parity tests on CPU time.

@@ -1,0 +1,69 @@
+"""The C-ABI library builds, loads and exports every symbol include/plss.h declares (no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2207_07615_b200 as pkg
+from paper_2207_07615_b200 import build as pbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "plss.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(plss_[a-z_T]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    pbuild.build()
+    return pkg.load_library()
+
+
+def test_header_symbols_exported(lib):
+    names = _header_functions()
+    assert len(names) >= 14
+    assert sorted(pkg.SYMBOLS) == names
+    for nm in names:
+        assert getattr(lib, nm) is not None
+
+
+def test_status_strings(lib):
+    assert lib.plss_status_str(0) == b"ok"
+    assert lib.plss_status_str(3) == b"matrix format violation"
+
+
+def test_workspace_bytes_host_only(lib):
+    m = pkg.plss.plss_matrix(1000, 500, 4000, None, None, None, None, None, None, 0)
+    o = pkg.plss.plss_options(1, 0, 100, 0)
+    nb = lib.plss_workspace_bytes(ctypes.byref(m), ctypes.byref(o))
+    assert nb >= 8 * (1000 + 3 * 500) + 8 * 101 * 8
+    o4 = pkg.plss.plss_options(4, 0, 100, 0)
+    nb4 = lib.plss_workspace_bytes(ctypes.byref(m), ctypes.byref(o4))
+    assert nb4 >= nb + 12 * 4000            # slab-major CSC copy
+    bad = pkg.plss.plss_matrix(-1, 5, 0, None, None, None, None, None, None, 0)
+    assert lib.plss_workspace_bytes(ctypes.byref(bad), None) == 0
+
+
+def test_null_ctx_is_an_error_not_a_crash(lib):
+    assert lib.plss_step(None, 1) == 1          # PLSS_E_INVALID
+    assert lib.plss_spmv(None, None, None) == 1
+    lib.plss_destroy(None)
+
+
+def test_product_does_not_import_oracle():
+    pkgdir = os.path.join(ROOT, "paper_2207_07615_b200")
+    for dirpath, _, files in os.walk(pkgdir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "plss_oracle" not in txt, f
+
+
+def test_build_targets_sm100a():
+    cmd = pbuild.command("/tmp/x.so")
+    assert "arch=compute_100a,code=sm_100a" in cmd

@@ -1,0 +1,319 @@
+"""GPU parity: libplss (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): relative residual history within 1e-9 over the first
+min(50, K_f) iterations (K_f = the window where two valid oracle orderings agree to 1e-11,
+SURVEY 8c-11), final ||x_gpu - x_oracle|| / ||x_oracle|| <= 1e-7, iterations within 2%.
+SpMV outputs are sequential ascending-index sums on both sides: bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import plss_gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+HIST_TOL = 1e-9
+X_TOL = 1e-7
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2207_07615_b200 import build as pbuild
+    pbuild.build()
+    import paper_2207_07615_b200 as p
+    p.load_library()
+    assert torch.cuda.is_available()
+    return p
+
+
+def _matrix(pkg, s):
+    return pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+
+
+def _gpu_solve(pkg, s, slabs=0, x0=None, **kw):
+    A = _matrix(pkg, s)
+    args = dict(tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit, flags=1 if s.freeze else 0)
+    args.update(kw)
+    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=max(args["maxit"], 1), validate=True)
+    b = torch.from_numpy(s.b).cuda()
+    xx0 = torch.from_numpy(x0).cuda() if x0 is not None else None
+    res = pkg.plss_solve(ctx, b, xx0, want_diag=True, **args)
+    res["xh"] = res["x"].cpu().numpy()
+    pkg.plss_destroy(ctx)
+    return res
+
+
+def _permuted(s, seed=3):
+    perm = np.random.default_rng(seed).permutation(s.m)
+    A = s.scipy_csr()[perm]
+    A.sort_indices()
+    return plss_gen._finish("perm", s.m, s.n, A.indptr, A.indices, A.data, None, s.tol, s.tol_mode,
+                            s.maxit, b=s.b[perm], freeze=s.freeze)
+
+
+def _window(s, ref, kmax=50):
+    """K_f: iterations where the oracle and a row-permuted oracle agree to 1e-11."""
+    other = oracle.plss_system(_permuted(s), maxit=min(s.maxit, kmax + 1))
+    h0, h1 = ref["hist"], other["hist"]
+    k = min(len(h0), len(h1), kmax)
+    rel = np.abs(h0[:k] - h1[:k]) / np.maximum(h0[:k], 1e-300)
+    bad = np.nonzero(rel > 1e-11)[0]
+    return int(bad[0]) if bad.size else k
+
+
+def _assert_parity(res, ref, kf, s):
+    assert res["outcome"] == ref["outcome"], (res["outcome"], ref["outcome"])
+    it_tol = max(1, int(np.ceil(0.02 * ref["iters"])))
+    assert abs(res["iters"] - ref["iters"]) <= it_tol, (res["iters"], ref["iters"])
+    k = min(kf, len(res["hist"]), len(ref["hist"]))
+    assert k >= 1
+    h_err = np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / np.maximum(ref["hist"][:k], 1e-300))
+    assert h_err <= HIST_TOL, (h_err, k)
+    nx = np.linalg.norm(ref["x"])
+    x_err = np.linalg.norm(res["xh"] - ref["x"]) / (nx if nx > 0 else 1.0)
+    assert x_err <= X_TOL, x_err
+    return h_err, x_err
+
+
+# ---------------------------------------------------------------------------------------------
+# SpMV entry points: bit-exact against the oracle's sequential sums
+# ---------------------------------------------------------------------------------------------
+
+def _ragged_system(seed=0, m=3000, n=5000):
+    """Zipf row lengths, empty rows, empty columns, rows longer than a tile (spill path)."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.zipf(1.8, m), n)
+    lens[::17] = 0                          # empty rows
+    lens[5] = n                             # a dense row, longer than a tile + spill
+    lens[6] = 4096
+    lens[7] = 33                            # just above the warp-cooperative threshold
+    cols = []
+    for L in lens:
+        c = np.sort(rng.choice(n, L, replace=False))
+        cols.append(c[c % 13 != 0])         # empty columns
+    lens = np.array([c.size for c in cols])
+    row_ptr = np.zeros(m + 1, np.int64)
+    np.cumsum(lens, out=row_ptr[1:])
+    col_idx = np.concatenate(cols)
+    val = rng.standard_normal(col_idx.size)
+    return plss_gen._finish("ragged", m, n, row_ptr, col_idx, val, rng.standard_normal(n), 1e-8, 0, 100)
+
+
+@pytest.mark.parametrize("slabs", [1, 3])
+def test_spmv_spmvT_bit_exact(pkg, slabs):
+    s = _ragged_system()
+    A = _matrix(pkg, s)
+    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=10, validate=True)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(s.n)
+    u = rng.standard_normal(s.m)
+    y = torch.empty(s.m, dtype=torch.float64, device="cuda")
+    v = torch.empty(s.n, dtype=torch.float64, device="cuda")
+    pkg.plss_spmv(ctx, torch.from_numpy(x).cuda(), y)
+    pkg.plss_spmvT(ctx, torch.from_numpy(u).cuda(), v)
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x))
+    np.testing.assert_array_equal(v.cpu().numpy(), oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u))
+    pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "C5xs"])
+def test_spmv_configs_bit_exact(pkg, name):
+    s = plss_gen.make_config(name)
+    for slabs in (1, 4):
+        A = _matrix(pkg, s)
+        ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=4)
+        x = np.random.default_rng(2).standard_normal(s.n)
+        u = np.random.default_rng(3).standard_normal(s.m)
+        y = torch.empty(s.m, dtype=torch.float64, device="cuda")
+        v = torch.empty(s.n, dtype=torch.float64, device="cuda")
+        pkg.plss_spmv(ctx, torch.from_numpy(x).cuda(), y)
+        pkg.plss_spmvT(ctx, torch.from_numpy(u).cuda(), v)
+        np.testing.assert_array_equal(y.cpu().numpy(), oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x))
+        np.testing.assert_array_equal(v.cpu().numpy(), oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u))
+        pkg.plss_destroy(ctx)
+
+
+# ---------------------------------------------------------------------------------------------
+# full solves vs the oracle
+# ---------------------------------------------------------------------------------------------
+
+def test_worked_example(pkg):
+    s = plss_gen.from_dense(np.diag([2.0, 1.0]), np.array([2.0, 1.0]), tol=1e-14, maxit=10)
+    res = _gpu_solve(pkg, s)
+    assert res["outcome"] == "converged" and res["iters"] == 2
+    np.testing.assert_allclose(res["xh"], [1.0, 1.0], atol=1e-14, rtol=0)
+    d = res["diag"]
+    assert abs(d[0, 7] - 5 / 17) <= 1e-15 and abs(d[1, 6] - 9 / 25) <= 1e-15 and abs(d[1, 7] - 17 / 20) <= 1e-15
+
+
+@pytest.mark.parametrize("name,slabs", [("C1", 0), ("C2s", 0), ("C2s", 3), ("C4s", 0), ("C5xs", 0),
+                                        ("C5xs", 4)])
+def test_solve_parity(pkg, name, slabs):
+    s = plss_gen.make_config(name)
+    if name == "C4s":
+        s.maxit = 400
+    ref = oracle.plss_system(s)
+    kf = _window(s, ref)
+    res = _gpu_solve(pkg, s, slabs=slabs)
+    _assert_parity(res, ref, kf, s)
+
+
+def test_solve_parity_c3_scaled(pkg):
+    s = plss_gen.make_config("C3", N=128)
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    _assert_parity(res, ref, 50, s)
+    assert np.max(np.abs(res["xh"] - 1.0)) <= 1e-5
+
+
+def test_solve_parity_c2_full(pkg):
+    s = plss_gen.make_config("C2")
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    _assert_parity(res, ref, _window(s, ref), s)
+
+
+def test_scalar_records_match_oracle(pkg):
+    s = plss_gen.make_config("C1")
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    d, r = res["diag"], ref["rec"]
+    for k in range(1, 30):
+        for col in (1, 2, 4, 6, 7):   # rho, phi, theta, beta, gamma
+            assert abs(d[k, col] - r[k, col]) <= 1e-9 * abs(r[k, col]), (k, col)
+        assert abs(d[k, 3] / d[k, 1] + 1) <= 1e-12        # psi = -rho (L671-672)
+
+
+def test_nonzero_x0(pkg):
+    s = plss_gen.make_config("C2s")
+    x0 = np.random.default_rng(5).standard_normal(s.n)
+    ref = oracle.plss_system(s, x0=x0)
+    res = _gpu_solve(pkg, s, x0=x0)
+    _assert_parity(res, ref, 30, s)
+
+
+def test_host_buffers_equal_device_buffers(pkg):
+    s = plss_gen.make_config("C2s")
+    A = _matrix(pkg, s)
+    ctx = pkg.plss_create(A, maxit_cap=s.maxit)
+    r_dev = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, maxit=s.maxit)
+    xh = np.zeros(s.n)
+    r_host = pkg.plss_solve(ctx, s.b.copy(), tol=s.tol, maxit=s.maxit, x=xh)
+    assert r_dev["iters"] == r_host["iters"]
+    np.testing.assert_array_equal(r_dev["x"].cpu().numpy(), xh)
+    pkg.plss_destroy(ctx)
+
+
+def test_deterministic_run_to_run(pkg):
+    s = plss_gen.make_config("C4s")
+    a = _gpu_solve(pkg, s, maxit=200)
+    b = _gpu_solve(pkg, s, maxit=200)
+    np.testing.assert_array_equal(a["xh"], b["xh"])
+    np.testing.assert_array_equal(a["hist"], b["hist"])
+
+
+def test_freeze_mode_fixed_iterations(pkg):
+    s = plss_gen.make_config("C5xs")
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    assert res["iters"] == s.maxit == ref["iters"]
+    assert res["outcome"] == ref["outcome"] == "maxit"
+    assert np.linalg.norm(res["xh"] - ref["x"]) / np.linalg.norm(ref["x"]) <= X_TOL
+    d = res["diag"]
+    frozen = np.nonzero(d[:s.maxit, 0] <= oracle.FREEZE_H)[0]
+    assert frozen.size and np.all(d[frozen[0] + 1:s.maxit, 6] == 0.0)
+
+
+# ---------------------------------------------------------------------------------------------
+# edge and degenerate cases
+# ---------------------------------------------------------------------------------------------
+
+def test_zero_rhs_converges_immediately(pkg):
+    s = plss_gen.make_config("C2s")
+    s.b = np.zeros(s.m)
+    res = _gpu_solve(pkg, s)
+    assert res["iters"] == 0 and res["outcome"] == "converged"
+    assert np.all(res["xh"] == 0.0)
+
+
+def test_exact_start(pkg):
+    s = plss_gen.make_config("C3", N=32)
+    res = _gpu_solve(pkg, s, x0=np.ones(s.n))
+    ref = oracle.plss_system(s, x0=np.ones(s.n))
+    assert res["iters"] == ref["iters"] and res["outcome"] == ref["outcome"]
+
+
+def test_y_vanished(pkg):
+    s = plss_gen.from_dense(np.array([[1.0], [0.0]]), np.array([0.0, 1.0]), keep_zeros=True,
+                            tol=1e-12, maxit=10)
+    res = _gpu_solve(pkg, s)
+    assert res["outcome"] == "y_vanished" and res["iters"] == 0
+
+
+def test_identity_one_step(pkg):
+    b = np.arange(1.0, 301.0)
+    s = plss_gen.from_dense(np.eye(300), b, tol=1e-15, maxit=5)
+    res = _gpu_solve(pkg, s)
+    assert res["iters"] == 1
+    np.testing.assert_array_equal(res["xh"], b)
+
+
+def test_empty_matrix(pkg):
+    m, n = 50, 40
+    s = plss_gen._finish("empty", m, n, np.zeros(m + 1, np.int64), np.zeros(0, np.int32), np.zeros(0), None,
+                         1e-8, 0, 5, b=np.zeros(m))
+    res = _gpu_solve(pkg, s)
+    assert res["iters"] == 0 and res["outcome"] == "converged"
+    s.b = np.ones(m)
+    res = _gpu_solve(pkg, s)
+    assert res["outcome"] == "y_vanished"
+
+
+def test_maxit_one_and_cap(pkg):
+    s = plss_gen.make_config("C1")
+    res = _gpu_solve(pkg, s, maxit=1)
+    ref = oracle.plss_system(s, maxit=1)
+    assert res["iters"] == ref["iters"] == 1 and res["outcome"] == ref["outcome"] == "maxit"
+    np.testing.assert_allclose(res["xh"], ref["x"], rtol=1e-12)
+    A = _matrix(pkg, s)
+    ctx = pkg.plss_create(A, maxit_cap=10)
+    with pytest.raises(pkg.PlssError):
+        pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), maxit=11)
+    with pytest.raises(pkg.PlssError):
+        pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=-1.0, maxit=5)
+    pkg.plss_destroy(ctx)
+
+
+def test_validation_rejects_bad_matrices(pkg):
+    s = plss_gen.make_config("C2s")
+    bad = plss_gen.make_config("C2s")
+    bad.col_idx = bad.col_idx.copy()
+    bad.col_idx[[8, 9]] = bad.col_idx[[9, 8]]           # unsorted row
+    with pytest.raises(pkg.PlssError, match="format"):
+        pkg.plss_create(_matrix(pkg, bad), validate=True)
+    bad = plss_gen.make_config("C2s")
+    bad.col_idx = bad.col_idx.copy()
+    bad.col_idx[0] = s.n + 5                             # out of range
+    with pytest.raises(pkg.PlssError, match="format"):
+        pkg.plss_create(_matrix(pkg, bad), validate=True)
+    bad = plss_gen.make_config("C2s")
+    bad.val_t = bad.val_t.copy()
+    bad.val_t[7] += 1.0                                  # CSC is not the transpose
+    with pytest.raises(pkg.PlssError, match="format"):
+        pkg.plss_create(_matrix(pkg, bad), validate=True)
+    bad = plss_gen.make_config("C2s")
+    bad.val = bad.val.copy()
+    bad.val[3] = np.nan
+    with pytest.raises(pkg.PlssError, match="format"):
+        pkg.plss_create(_matrix(pkg, bad), validate=True)
+
+
+def test_slabs_agree(pkg):
+    s = plss_gen.make_config("C5xs")
+    a = _gpu_solve(pkg, s, slabs=1)
+    b = _gpu_solve(pkg, s, slabs=7)
+    assert a["iters"] == b["iters"]
+    k = 25
+    assert np.max(np.abs(a["hist"][:k] - b["hist"][:k]) / a["hist"][:k]) <= 1e-11
