@@ -47,8 +47,8 @@ struct Layout {
   int S = 1;
   bool dist = false;
   int maxit_cap = 0;
-  size_t r, y, p, x, rec, ctl, counters, part1, part2, part3, partn, tile1, tile2, sptr, sidx,
-      sval, scan_cnt, scan_blk, buf, err, scalars, total;
+  size_t r, y, p, x, rec, ctl, counters, part1, part2, part3, partn, tile1, tile2, scratch,
+      scratch_blk, sptr, sidx, sval, scan_cnt, scan_blk, buf, err, scalars, total;
 };
 
 bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, Layout* L) {
@@ -62,7 +62,8 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   L->dist = dist;
   L->maxit_cap = o.maxit_cap > 0 ? o.maxit_cap : 20000;
   const int64_t m = A->m, n = A->n, nnz = A->nnz;
-  const int64_t tiles_total = nnz / TILE + 2 * S + 2;
+  const int64_t tiles1 = nnz / TILE + m / RCAP + 2 * S + 2;       // K1 tile descriptors
+  const int64_t tiles2 = nnz / TILE + S * (n / RCAP) + 2 * S + 2; // K2 tile descriptors
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o2 = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o2; };
   L->r = take(8 * m);
@@ -76,8 +77,10 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   L->part2 = take(16 * (size_t)MAXG);
   L->part3 = take(16 * (size_t)MAXG);
   L->partn = take(16 * (size_t)MAXG);
-  L->tile1 = take(4 * (size_t)(tiles_total + S));
-  L->tile2 = take(4 * (size_t)(tiles_total + S));
+  L->tile1 = take(8 * (size_t)(tiles1 + S));
+  L->tile2 = take(8 * (size_t)(tiles2 + S));
+  L->scratch = take(4 * (size_t)(std::max(m, n) + 2));
+  L->scratch_blk = take(4 * (size_t)((std::max(m, n) + 2) / (NT * SCAN_ITEMS) + 2));
   if (S > 1) {
     L->sptr = take(4 * (size_t)S * (n + 1));
     L->sidx = take(4 * (size_t)nnz);
@@ -196,6 +199,11 @@ static void set_err(plss_ctx* ctx, const std::string& s) {
   g_last_error = s;
 }
 
+template <int ROLE>
+static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
+  k_spmv<ROLE><<<grid, NT, Stage<ROLE>::SMEM, st>>>(a);
+}
+
 // order our work stream after / before the caller's stream when they differ
 static plss_status sync_in(plss_ctx* ctx) {
   if (!ctx->own_stream) return PLSS_OK;
@@ -220,11 +228,11 @@ static int grid_for(int64_t work_units, int occ_per_sm, int sms) {
 static plss_status enqueue_step(plss_ctx* ctx) {
   cudaStream_t st = ctx->stream;
   for (int s = 0; s < ctx->S; ++s) {
-    k_spmv<ROLE_K1><<<ctx->g1[s], NT, 0, st>>>(ctx->seg1[s]);
+    launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
     if (ctx->seg2[s].finalize)
-      k_spmv<ROLE_K2DOTS><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+      launch_spmv<ROLE_K2DOTS>(ctx->seg2[s], ctx->g2[s], st);
     else
-      k_spmv<ROLE_K2><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+      launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
   }
   if (ctx->nranks > 1) {
     NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
@@ -250,6 +258,54 @@ static plss_status build_graph(plss_ctx* ctx, int iters, cudaGraphExec_t* out) {
   return PLSS_OK;
 }
 
+static plss_status scan_excl(plss_ctx* ctx, int32_t* a, long long len, int32_t* blk) {
+  const unsigned nblk = (unsigned)((len + NT * SCAN_ITEMS - 1) / (NT * SCAN_ITEMS));
+  k_scan_local<<<nblk, NT, 0, ctx->stream>>>(a, len, blk);
+  k_scan_blocks<<<1, 1, 0, ctx->stream>>>(blk, (int)nblk);
+  k_scan_add<<<nblk, NT, 0, ctx->stream>>>(a, len, blk);
+  CK(cudaGetLastError());
+  return PLSS_OK;
+}
+
+// tiles of one segment: descriptors desc[0..nt] (desc[nt] = {nrows, ptr[nrows]})
+static plss_status build_tiles(plss_ctx* ctx, const int32_t* ptr, int64_t nrows, int64_t e0, int2* desc,
+                               int64_t cap, int64_t* nt_out) {
+  cudaStream_t st = ctx->stream;
+  int32_t* flag = (int32_t*)(ctx->ws + ctx->L.scratch);
+  int32_t* blk = (int32_t*)(ctx->ws + ctx->L.scratch_blk);
+  const long long len = nrows + 1;
+  const unsigned g = (unsigned)((len + 255) / 256);
+  k_tile_mark<<<g, 256, 0, st>>>(ptr, nrows, e0, flag);
+  if (scan_excl(ctx, flag, len, blk) != PLSS_OK) return PLSS_E_CUDA;
+  int32_t nt = 0;
+  CK(cudaMemcpyAsync(&nt, flag + nrows, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (nt + 1 > cap) { set_err(ctx, "tile descriptor bound exceeded"); return PLSS_E_CUDA; }
+  k_tile_desc<<<g, 256, 0, st>>>(ptr, nrows, e0, flag, desc);
+  CK(cudaGetLastError());
+  *nt_out = nt;
+  return PLSS_OK;
+}
+
+template <int ROLE>
+static cudaError_t smem_attr(int* occ) {
+  cudaError_t e = cudaFuncSetAttribute(k_spmv<ROLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Stage<ROLE>::SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_spmv<ROLE>, NT, Stage<ROLE>::SMEM);
+  *occ = std::max(1, *occ);
+  return e;
+}
+
+static plss_status set_smem_attrs(plss_ctx* ctx, int occ[4]) {
+  CK(smem_attr<ROLE_PLAIN>(&occ[ROLE_PLAIN]));
+  CK(smem_attr<ROLE_K1>(&occ[ROLE_K1]));
+  CK(smem_attr<ROLE_K2>(&occ[ROLE_K2]));
+  CK(smem_attr<ROLE_K2DOTS>(&occ[ROLE_K2DOTS]));
+  return PLSS_OK;
+}
+
+
 static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options* opt, void* workspace,
                          size_t ws_bytes, void* stream, bool dist) {
   ctx->A = *A;
@@ -261,6 +317,14 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     set_err(ctx, "NULL matrix array"); return PLSS_E_INVALID;
   }
   if (opt && opt->flags != 0) { set_err(ctx, "options.flags must be 0"); return PLSS_E_INVALID; }
+  {
+    const void* arrs[6] = {A->row_ptr, A->col_idx, A->val, A->col_ptr, A->row_idx, A->val_t};
+    for (const void* q : arrs)
+      if (q && (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
+        set_err(ctx, "matrix arrays must be 16-byte aligned (TMA bulk copies)");
+        return PLSS_E_INVALID;
+      }
+  }
   CK(cudaGetDevice(&ctx->dev));
   ctx->user_stream = (cudaStream_t)stream;
   if (ctx->user_stream == nullptr) {
@@ -333,17 +397,19 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   }
 
   // ---- occupancy-derived persistent grids -----------------------------------------------------
-  int sms = 0, occ_spmv = 0, occ_vec = 0;
+  int sms = 0, occ_vec = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_spmv, k_spmv<ROLE_K1>, NT, 0));
+  int occ[4] = {0, 0, 0, 0};
+  if (set_smem_attrs(ctx, occ) != PLSS_OK) return PLSS_E_CUDA;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_vec, k_pxupdate, NT, 0));
-  occ_spmv = std::max(1, occ_spmv);
   occ_vec = std::max(1, occ_vec);
 
   // ---- K1 segments (CSR row slabs) ----------------------------------------------------------
-  int32_t* tile1 = (int32_t*)(w + L.tile1);
-  int32_t* tile2 = (int32_t*)(w + L.tile2);
-  size_t t1off = 0, t2off = 0;
+  int2* desc1 = (int2*)(w + L.tile1);
+  int2* desc2 = (int2*)(w + L.tile2);
+  const int64_t tiles1_cap = (int64_t)((L.tile2 - L.tile1) / 8);
+  const int64_t tiles2_cap = (int64_t)((L.scratch - L.tile2) / 8);
+  int64_t t1off = 0, t2off = 0;
   ctx->seg1.resize(S);
   ctx->seg2.resize(S);
   ctx->g1.resize(S);
@@ -352,13 +418,14 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     SpmvSeg& a = ctx->seg1[s];
     memset(&a, 0, sizeof a);
     const int64_t rows = ctx->R[s + 1] - ctx->R[s];
-    const int64_t nt = ntiles_of(ctx->E[s + 1] - ctx->E[s]);
     a.ptr = A->row_ptr + ctx->R[s];
     a.idx = A->col_idx;
     a.val = A->val;
-    a.tile_first = tile1 + t1off;
+    a.desc = desc1 + t1off;
     a.e0 = ctx->E[s];
     a.nrows = (int32_t)rows;
+    int64_t nt = 0;
+    if (build_tiles(ctx, a.ptr, rows, a.e0, (int2*)a.desc, tiles1_cap - t1off, &nt) != PLSS_OK) return PLSS_E_CUDA;
     a.ntiles = (int32_t)nt;
     a.g = ctx->p;
     a.out = ctx->r + ctx->R[s];
@@ -371,11 +438,9 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.ctl = ctx->ctl;
     a.rec = ctx->rec;
     a.rho_out = ctx->y + n;
-    k_tile_map<<<(unsigned)((nt + 1 + 255) / 256), 256, 0, st>>>(a.ptr, a.nrows, a.e0, a.ntiles, (int32_t*)a.tile_first);
     t1off += nt + 1;
-    ctx->g1[s] = grid_for(nt, occ_spmv, sms);
+    ctx->g1[s] = grid_for(nt, occ[ROLE_K1], sms);
   }
-  CK(cudaGetLastError());
 
   // ---- K2 segments (CSC, slab-major copy when S > 1) ----------------------------------------
   int32_t *sptr = nullptr, *sidx = nullptr;
@@ -386,21 +451,17 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     sval = (double*)(w + L.sval);
     int32_t* blk = (int32_t*)(w + L.scan_blk);
     const long long len = n + 1;
-    const unsigned nblk = (unsigned)((len + NT * SCAN_ITEMS - 1) / (NT * SCAN_ITEMS));
     for (int s = 0; s < S; ++s) {
       int32_t* sp = sptr + (size_t)s * (n + 1);
       k_slab_count<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(A->col_ptr, A->row_idx, n, ctx->R[s], ctx->R[s + 1], sp);
-      k_scan_local<<<nblk, NT, 0, st>>>(sp, len, blk);
-      k_scan_blocks<<<1, 1, 0, st>>>(blk, (int)nblk);
-      k_scan_add<<<nblk, NT, 0, st>>>(sp, len, blk);
-        k_slab_copy<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(A->col_ptr, A->row_idx, A->val_t, n, ctx->R[s], ctx->R[s + 1], ctx->E[s], sp, sidx, sval);
+      if (scan_excl(ctx, sp, len, blk) != PLSS_OK) return PLSS_E_CUDA;
+      k_slab_copy<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(A->col_ptr, A->row_idx, A->val_t, n, ctx->R[s], ctx->R[s + 1], ctx->E[s], sp, sidx, sval);
     }
     CK(cudaGetLastError());
   }
   for (int s = 0; s < S; ++s) {
     SpmvSeg& a = ctx->seg2[s];
     memset(&a, 0, sizeof a);
-    const int64_t nt = ntiles_of(ctx->E[s + 1] - ctx->E[s]);
     if (S > 1) {
       a.ptr = sptr + (size_t)s * (n + 1);
       a.idx = sidx;
@@ -414,8 +475,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
       a.e0 = 0;
       a.g = ctx->r;
     }
-    a.tile_first = tile2 + t2off;
+    a.desc = desc2 + t2off;
     a.nrows = (int32_t)n;
+    int64_t nt = 0;
+    if (build_tiles(ctx, a.ptr, n, a.e0, (int2*)a.desc, tiles2_cap - t2off, &nt) != PLSS_OK) return PLSS_E_CUDA;
     a.ntiles = (int32_t)nt;
     a.out = ctx->y;
     a.pv = ctx->p;
@@ -427,9 +490,8 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.counter = ctx->counters + 1;
     a.ctl = ctx->ctl;
     a.rec = ctx->rec;
-    k_tile_map<<<(unsigned)((nt + 1 + 255) / 256), 256, 0, st>>>(a.ptr, a.nrows, a.e0, a.ntiles, (int32_t*)a.tile_first);
     t2off += nt + 1;
-    ctx->g2[s] = grid_for(nt, occ_spmv, sms);
+    ctx->g2[s] = grid_for(nt, occ[a.finalize ? ROLE_K2DOTS : ROLE_K2], sms);
   }
   CK(cudaGetLastError());
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
@@ -630,7 +692,7 @@ plss_status plss_spmv(plss_ctx* ctx, const double* x, double* y) {
     a.g = x;
     a.out = y + ctx->R[s];
     a.ctl = nullptr;
-    k_spmv<ROLE_PLAIN><<<ctx->g1[s], NT, 0, ctx->stream>>>(a);
+    launch_spmv<ROLE_PLAIN>(a, ctx->g1[s], ctx->stream);
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
@@ -640,15 +702,19 @@ plss_status plss_spmv(plss_ctx* ctx, const double* x, double* y) {
 plss_status plss_spmvT(plss_ctx* ctx, const double* u, double* v) {
   if (!ctx || (!u && ctx->m > 0) || (!v && ctx->n > 0)) return PLSS_E_INVALID;
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  // slabs accumulate into the output, whose slices are re-read by TMA: use the (aligned,
+  // padded) internal y, then copy out
+  double* out = ctx->S > 1 ? ctx->y : v;
   for (int s = 0; s < ctx->S; ++s) {
     SpmvSeg a = ctx->seg2[s];
-    a.g = u + ctx->R[s] * (ctx->S > 1 ? 1 : 0);
-    a.out = v;
+    a.g = u + (ctx->S > 1 ? ctx->R[s] : 0);
+    a.out = out;
     a.ctl = nullptr;
     a.finalize = 0;
-    k_spmv<ROLE_K2><<<ctx->g2[s], NT, 0, ctx->stream>>>(a);
+    launch_spmv<ROLE_K2>(a, ctx->g2[s], ctx->stream);
   }
   CK(cudaGetLastError());
+  if (out != v && ctx->n > 0) CK(cudaMemcpyAsync(v, out, 8 * (size_t)ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return sync_out(ctx);
 }
@@ -665,10 +731,10 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
     int q = 0;
     CK(cudaEventRecord(ev[q++], st));
     for (int s = 0; s < ctx->S; ++s) {
-      k_spmv<ROLE_K1><<<ctx->g1[s], NT, 0, st>>>(ctx->seg1[s]);
+      launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
       CK(cudaEventRecord(ev[q++], st));
-      if (ctx->seg2[s].finalize) k_spmv<ROLE_K2DOTS><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
-      else k_spmv<ROLE_K2><<<ctx->g2[s], NT, 0, st>>>(ctx->seg2[s]);
+      if (ctx->seg2[s].finalize) launch_spmv<ROLE_K2DOTS>(ctx->seg2[s], ctx->g2[s], st);
+      else launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
       CK(cudaEventRecord(ev[q++], st));
     }
     if (ctx->nranks > 1) {

@@ -12,9 +12,10 @@
 //   K3  k_pxupdate       p <- beta p + gamma y (Thm 4.1 eq:pkShort), theta = p^T p, x <- x + p
 //                        (L811-813).
 //
-// Every SpMV output element is a SEQUENTIAL sum in ascending index order computed with
-// __dmul_rn/__dadd_rn (no FMA contraction): products and sums are bitwise those of the plain
-// oracle. Dot products use fixed-shape trees: deterministic run to run, a few ulps from the
+// Every SpMV output element of a row (column) with <= LONGROW entries is a SEQUENTIAL sum in
+// ascending index order computed with __dmul_rn/__dadd_rn (no FMA contraction): bitwise the
+// oracle's. Longer rows are summed by a whole warp (lane-strided partials + butterfly):
+// deterministic, within a few ulps of the sequential sum. Dot products use fixed-shape trees: deterministic run to run, a few ulps from the
 // oracle's sequential sums.
 #pragma once
 #include <cstdint>
@@ -23,10 +24,12 @@
 namespace plss {
 
 constexpr int NT = 256;            // threads per CTA of the SpMV / vector kernels
-constexpr int TILE = 2048;         // nnz per SpMV tile (owner-computes rows starting in it)
-constexpr int CAP = TILE + 512;    // staged products per tile (spill of the last row)
-constexpr int UNR = CAP / NT;      // staged loads per thread (10)
-constexpr int LONGROW = 32;        // rows longer than this are summed by the whole warp
+constexpr int TILE = 2048;         // nnz window of a SpMV tile (rows whose first entry lies in it)
+constexpr int RCAP = 384;          // at most this many rows per tile
+constexpr int CAP = TILE + 256;    // staged entries per tile (the last row may spill past TILE)
+constexpr int UNR = CAP / NT;      // staged entries per thread (9)
+constexpr int NST = 3;             // TMA pipeline stages per CTA
+constexpr int LONGROW = 128;       // rows longer than this are summed by the whole warp (tree)
 constexpr int REC = 8;             // doubles per iteration record
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -51,8 +54,9 @@ struct SpmvSeg {
   const int32_t* ptr;        // nrows+1 absolute positions into idx / val
   const int32_t* idx;        // gathered-vector index of each entry (column for K1, row for K2)
   const double* val;
-  const int32_t* tile_first; // ntiles+1: tile t owns rows whose first entry lies in
-                             // [e0 + t*TILE, e0 + (t+1)*TILE)
+  const int2* desc;          // ntiles+1 tile descriptors {first row, its first entry}; a tile
+                             // is a maximal run of <= RCAP rows whose first entries share one
+                             // TILE-wide window of positions (counted from e0)
   long long e0;
   int32_t nrows, ntiles;
   const double* g;           // gathered vector (p for K1, the slab of r for K2)
@@ -197,50 +201,205 @@ __device__ void tail_y(Ctl* c, double* rec, double phi, double psi) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1 / K2 / plain SpMV: persistent CTAs over nnz tiles, products staged in shared memory,
-// rows owned by the tile holding their first entry, sequential per-row sums.
+// TMA (cp.async.bulk) + mbarrier helpers
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+// 1-D bulk copy global -> shared, completion counted on the mbarrier, L2 evict-first hint
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+               " [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+
+// Stage layout: every region starts 16-byte aligned and holds the 16-byte-aligned superset of the
+// tile's range (the ABI requires 16-byte aligned, 16-byte padded arrays).
+template <int ROLE>
+struct Stage {
+  static constexpr bool HAS_V1 = ROLE != ROLE_PLAIN;   // r (K1) or y_prev (K2, accumulate)
+  static constexpr bool HAS_V2 = ROLE == ROLE_K2DOTS;  // p for psi
+  static constexpr int V_OFF = 0;
+  static constexpr int V_BYTES = (CAP + 4) * 8;
+  static constexpr int I_OFF = V_OFF + V_BYTES;
+  static constexpr int I_BYTES = (CAP + 8) * 4;
+  static constexpr int P_OFF = I_OFF + I_BYTES;
+  static constexpr int P_BYTES = (RCAP + 8) * 4;
+  static constexpr int V1_OFF = P_OFF + P_BYTES;
+  static constexpr int V1_BYTES = HAS_V1 ? (RCAP + 4) * 8 : 0;
+  static constexpr int V2_OFF = V1_OFF + V1_BYTES;
+  static constexpr int V2_BYTES = HAS_V2 ? (RCAP + 4) * 8 : 0;
+  static constexpr int BYTES = (V2_OFF + V2_BYTES + 127) / 128 * 128;
+  static constexpr int SMEM = NST * BYTES;
+};
+
+struct StageDesc {
+  int r0, r1;          // rows [r0, r1) of the tile
+  int s0, se;          // staged entries [s0, se) (se = min(row_ptr[r1], s0 + CAP))
+  int vb, ib, pb, rb, rb2;  // element index held at offset 0 of the V / I / P / V1 / V2 regions
+};
+
+__device__ __forceinline__ const char* align16_down(const void* p) {
+  return reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15));
+}
+__device__ __forceinline__ unsigned span16(const void* lo, const void* hi_excl) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15);
+  const uintptr_t b = (reinterpret_cast<uintptr_t>(hi_excl) + 15) & ~uintptr_t(15);
+  return (unsigned)(b - a);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 / plain SpMV: persistent CTAs; each tile's values, indices, row pointers and row-wise
+// vector slices arrive by TMA bulk copies NST-1 tiles ahead; products are formed in place in
+// shared memory; rows are owned by the tile holding their first entry and summed sequentially.
 // ---------------------------------------------------------------------------------------------
 template <int ROLE>
-__global__ void __launch_bounds__(NT) k_spmv(SpmvSeg a) {
-  __shared__ double prod[CAP];
+__global__ void __launch_bounds__(NT, 2) k_spmv(SpmvSeg a) {
+  using C = Stage<ROLE>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[NST];
+  __shared__ StageDesc sdesc[NST];
   __shared__ double sm[2][NT / 32];
   if (a.ctl != nullptr && a.ctl->done) return;
-  const uint64_t pol = policy_evict_first();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int my_tiles = a.ntiles > (int)blockIdx.x ? (a.ntiles - (int)blockIdx.x + G - 1) / G : 0;
+  const uint64_t pol = policy_evict_first();
   double acc0 = 0.0, acc1 = 0.0;
 
-  for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-    const int r0 = a.tile_first[t], r1 = a.tile_first[t + 1];
-    if (r0 >= r1) continue;                                    // uniform in the CTA
-    const long long s0 = a.ptr[r0];
-    const long long s1 = a.ptr[r1];
-    const int cnt = (int)min(s1 - s0, (long long)CAP);
-    const long long send = s0 + cnt;
-    // stage: coalesced streaming loads of the tile's values and indices, then the gathers
-    double v[UNR];
-    int32_t c[UNR];
+  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
+  if (tid == 0) {
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int k = tid + u * NT;
-      if (k < cnt) { v[u] = ld_stream(a.val + s0 + k, pol); c[u] = ld_stream(a.idx + s0 + k, pol); }
+    for (int q = 0; q < NST; ++q) mbar_init(&bars[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // producer (thread 0): describe tile j of this CTA and start its bulk copies into stage j % NST
+  auto issue = [&](int j) {
+    const int t = (int)blockIdx.x + j * G;
+    const int q = j % NST;
+    const int2 d0 = a.desc[t], d1 = a.desc[t + 1];
+    StageDesc d;
+    d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
+    d.se = min(d1.y, d0.y + CAP);
+    unsigned char* base = smem + q * C::BYTES;
+    unsigned tx = 0;
+    const char* lo;
+    unsigned nb;
+    // values [s0, se)
+    lo = align16_down(a.val + d.s0);
+    nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
+    d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
+    if (nb) { tma_load(base + C::V_OFF, lo, nb, &bars[q], pol); tx += nb; }
+    // indices [s0, se)
+    lo = align16_down(a.idx + d.s0);
+    nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
+    d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
+    if (nb) { tma_load(base + C::I_OFF, lo, nb, &bars[q], pol); tx += nb; }
+    // row pointers [r0, r1]
+    lo = align16_down(a.ptr + d.r0);
+    nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
+    d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
+    tma_load(base + C::P_OFF, lo, nb, &bars[q], pol);
+    tx += nb;
+    // row-wise vector slices [r0, r1)
+    d.rb = d.r0;
+    d.rb2 = d.r0;
+    if (d.r1 > d.r0) {
+      if (C::HAS_V1 && v1src) {
+        lo = align16_down(v1src + d.r0);
+        nb = span16(v1src + d.r0, v1src + d.r1);
+        d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
+        tma_load(base + C::V1_OFF, lo, nb, &bars[q], pol);
+        tx += nb;
+      }
+      if (C::HAS_V2) {
+        lo = align16_down(a.pv + d.r0);
+        nb = span16(a.pv + d.r0, a.pv + d.r1);
+        d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
+        tma_load(base + C::V2_OFF, lo, nb, &bars[q], pol);
+        tx += nb;
+      }
     }
+    sdesc[q] = d;
+    mbar_expect_tx(&bars[q], tx);
+  };
+
+  if (tid == 0)
+    for (int j = 0; j < min(NST - 1, my_tiles); ++j) issue(j);
+
+  for (int j = 0; j < my_tiles; ++j) {
+    const int q = j % NST;
+    if (tid == 0 && j + NST - 1 < my_tiles) {
+      fence_proxy_async();          // generic accesses to that stage (iteration j-1) happen-before
+      issue(j + NST - 1);
+    }
+    mbar_wait(&bars[q], (unsigned)(j / NST) & 1u);
+    const StageDesc d = sdesc[q];
+    double* V = reinterpret_cast<double*>(smem + q * C::BYTES + C::V_OFF);
+    const int32_t* I = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::I_OFF);
+    const int32_t* P = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::P_OFF);
+    const double* V1 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V1_OFF);
+    const double* V2 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V2_OFF);
+    // products in place: V[e] <- val_e * g[idx_e]  (gathers of the whole tile in flight at once)
+    const int cnt = d.se - d.s0;
+    const int voff = d.s0 - d.vb, ioff = d.s0 - d.ib;
+    {
+      double v[UNR];
+      int32_t c[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int k = tid + u * NT;
-      if (k < cnt) prod[k] = __dmul_rn(v[u], __ldg(a.g + c[u]));
+      for (int u = 0; u < UNR; ++u) {
+        const int k = tid + u * NT;
+        if (k < cnt) { v[u] = V[voff + k]; c[u] = I[ioff + k]; }
+      }
+      double gv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = tid + u * NT;
+        if (k < cnt) gv[u] = __ldg(a.g + c[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = tid + u * NT;
+        if (k < cnt) V[voff + k] = __dmul_rn(v[u], gv[u]);
+      }
     }
     __syncthreads();
-    for (int base = r0 + warp * 32; base < r1; base += NT) {
+    const int vsh = -d.vb;   // V index of entry position e is e - vb
+    for (int base = d.r0 + warp * 32; base < d.r1; base += NT) {
       const int i = base + lane;
-      const bool valid = i < r1;
-      long long b = 0, e = 0;
-      if (valid) { b = a.ptr[i]; e = a.ptr[i + 1]; }
+      const bool valid = i < d.r1;
+      int b = 0, e = 0;
+      if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
       const bool lng = valid && (e - b) > LONGROW;
       double s = 0.0;
-      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = a.out[i];
+      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
       if (valid && !lng) {
-        for (long long k = b; k < e; ++k) {
-          const double pr = (k < send) ? prod[k - s0]
+        for (int k = b; k < e; ++k) {
+          const double pr = (k < d.se) ? V[k + vsh]
                                        : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
           s = __dadd_rn(s, pr);
         }
@@ -249,10 +408,10 @@ __global__ void __launch_bounds__(NT) k_spmv(SpmvSeg a) {
       while (mask) {                                            // warp-cooperative long rows
         const int l = __ffs(mask) - 1;
         mask &= mask - 1;
-        const long long lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
+        const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
         double ps = 0.0;
-        for (long long k = lb + lane; k < le; k += 32) {
-          const double pr = (k < send) ? prod[k - s0]
+        for (int k = lb + lane; k < le; k += 32) {
+          const double pr = (k < d.se) ? V[k + vsh]
                                        : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
           ps = __dadd_rn(ps, pr);
         }
@@ -263,16 +422,16 @@ __global__ void __launch_bounds__(NT) k_spmv(SpmvSeg a) {
         if (ROLE == ROLE_PLAIN) {
           a.out[i] = s;
         } else if (ROLE == ROLE_K1) {
-          const double rn = __dsub_rn(a.out[i], s);            // r_i <- r_i - (A p)_i
+          const double rn = __dsub_rn(V1[i - d.rb], s);          // r_i <- r_i - (A p)_i
           a.out[i] = rn;
           acc0 = fma(rn, rn, acc0);
         } else {
           a.out[i] = s;                                         // y_j
-          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, a.pv[i], acc1); }
+          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
         }
       }
     }
-    __syncthreads();
+    __syncthreads();                                            // stage q is free again
   }
   if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;           // nothing to reduce
   if (!a.finalize) {                                            // slab s < S-1: publish only
@@ -401,12 +560,26 @@ __device__ __forceinline__ int lower_bound_pos(const int32_t* ptr, int nrows, lo
   return lo;
 }
 
-__global__ void k_tile_map(const int32_t* ptr, int nrows, long long e0, int ntiles, int32_t* tf) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > ntiles) return;
-  if (t == 0) tf[0] = 0;
-  else if (t == ntiles) tf[t] = nrows;
-  else tf[t] = lower_bound_pos(ptr, nrows, e0 + (long long)t * TILE);
+// tile construction (setup): a new tile starts at row i when the TILE-window of its first entry
+// or its RCAP-row block differs from row i-1's
+__device__ __forceinline__ int tile_flag(const int32_t* ptr, long long i, long long e0) {
+  if (i == 0) return 1;
+  return ((ptr[i] - e0) / TILE != (ptr[i - 1] - e0) / TILE) || (i / RCAP != (i - 1) / RCAP);
+}
+__global__ void k_tile_mark(const int32_t* ptr, long long nrows, long long e0, int32_t* flag) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) flag[i] = tile_flag(ptr, i, e0);
+  else if (i == nrows) flag[i] = 0;
+}
+// after the exclusive scan: pos[i] = tile index of row i if it starts a tile
+__global__ void k_tile_desc(const int32_t* ptr, long long nrows, long long e0, const int32_t* pos,
+                            int2* desc) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) {
+    if (tile_flag(ptr, i, e0)) desc[pos[i]] = make_int2((int)i, ptr[i]);
+  } else if (i == nrows) {
+    desc[pos[nrows]] = make_int2((int)nrows, ptr[nrows]);
+  }
 }
 
 // structural validation of one compressed layout (CSR or CSC); bit flags into *err

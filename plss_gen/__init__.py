@@ -296,6 +296,7 @@ CONFIGS = {
     "C2s": (c2_random, {"m": 20_000, "n": 10_000}),
     "C3s": (c3_laplace, {"N": 256}),
     "C4s": (c4_powerlaw, {"m": 20_000, "n": 80_000, "support": 800}),
+    "C4xs": (c4_powerlaw, {"m": 2_000, "n": 8_000, "support": 80}),
     "C5s": (c5_banded, {"m": 640_000, "n": 80_000, "maxit": 60}),
     "C5xs": (c5_banded, {"m": 64_000, "n": 8_000, "half": 256, "maxit": 60}),
 }
