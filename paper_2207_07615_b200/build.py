@@ -63,5 +63,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: dict) -> str:
+    """Tuning variant (e.g. libplss_t2048.so with -DPLSS_TILE=2048), selected at run time through
+    the PLSS_LIB environment variable. The default build is libplss.so."""
+    out = os.path.join(HERE, f"libplss_{name}.so")
+    extra = [f"-D{k}={v}" for k, v in defines.items()]
+    res = subprocess.run(command(out, extra), capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr)
+        raise RuntimeError(f"nvcc failed building {out}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

@@ -201,7 +201,7 @@ static void set_err(plss_ctx* ctx, const std::string& s) {
 
 template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
-  k_spmv<ROLE><<<grid, NT, Stage<ROLE>::SMEM, st>>>(a);
+  k_spmv<ROLE><<<grid, NTS, Stage<ROLE>::SMEM, st>>>(a);
 }
 
 // order our work stream after / before the caller's stream when they differ
@@ -292,7 +292,7 @@ static cudaError_t smem_attr(int* occ) {
   cudaError_t e = cudaFuncSetAttribute(k_spmv<ROLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Stage<ROLE>::SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_spmv<ROLE>, NT, Stage<ROLE>::SMEM);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_spmv<ROLE>, NTS, Stage<ROLE>::SMEM);
   *occ = std::max(1, *occ);
   return e;
 }

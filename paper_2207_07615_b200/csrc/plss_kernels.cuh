@@ -23,12 +23,32 @@
 
 namespace plss {
 
-constexpr int NT = 256;            // threads per CTA of the SpMV / vector kernels
-constexpr int TILE = 2048;         // nnz window of a SpMV tile (rows whose first entry lies in it)
-constexpr int RCAP = 384;          // at most this many rows per tile
-constexpr int CAP = TILE + 256;    // staged entries per tile (the last row may spill past TILE)
-constexpr int UNR = CAP / NT;      // staged entries per thread (9)
-constexpr int NST = 3;             // TMA pipeline stages per CTA
+#ifndef PLSS_TILE
+#define PLSS_TILE 1024
+#endif
+#ifndef PLSS_NST
+#define PLSS_NST 2
+#endif
+#ifndef PLSS_MINB
+#define PLSS_MINB 4
+#endif
+#ifndef PLSS_KDESIGN
+#define PLSS_KDESIGN 2      // 2: CTA-synchronous TMA tiles; 3: warp-specialized producer/consumers
+#endif
+constexpr int NT = 256;                 // threads per CTA of the vector kernels
+constexpr int NCW = 8;                  // consumer warps per SpMV CTA
+#if PLSS_KDESIGN == 2
+constexpr int NTS = NT;                 // SpMV CTA: 8 warps, thread 0 also issues the TMA copies
+#else
+constexpr int NTS = (NCW + 1) * 32;     // SpMV CTA: 8 consumer warps + 1 TMA producer warp
+#endif
+constexpr int TILE = PLSS_TILE;         // nnz window of a SpMV tile (rows whose first entry lies in it)
+constexpr int SUBW = TILE / NCW;        // nnz sub-window of one consumer warp
+constexpr int RCAP = TILE / 4;          // at most this many rows per tile
+constexpr int CAP = TILE + TILE / 4;    // staged entries per tile (the last row may spill past TILE)
+constexpr int WUNR = 4;                 // gathers in flight per lane per batch
+constexpr int NST = PLSS_NST;           // TMA pipeline stages per CTA
+constexpr int MINB = PLSS_MINB;         // CTAs per SM the SpMV kernel is compiled for
 constexpr int LONGROW = 128;       // rows longer than this are summed by the whole warp (tree)
 constexpr int REC = 8;             // doubles per iteration record
 constexpr unsigned FULL = 0xffffffffu;
@@ -104,7 +124,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Fixed-shape block reduction of two values; result valid in thread 0.
-__device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[NT / 32]) {
+constexpr int MAXW = 16;  // max warps per CTA of any kernel here
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[MAXW]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   a = warp_sum(a);
   b = warp_sum(b);
@@ -112,8 +134,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[NT
   __syncthreads();
   if (threadIdx.x == 0) {
     double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) { s0 += sm[0][w]; s1 += sm[1][w]; }
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { s0 += sm[0][w]; s1 += sm[1][w]; }
     a = s0; b = s1;
   }
   __syncthreads();
@@ -125,7 +146,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[NT
 // (a, b) = totals in thread 0.
 __device__ __forceinline__ bool publish_and_elect(double& a, double& b, double* partial,
                                                   const double* part_base, int nparts,
-                                                  unsigned* counter, double (*sm)[NT / 32]) {
+                                                  unsigned* counter, double (*sm)[MAXW]) {
   __shared__ int s_last;
   block_sum2(a, b, sm);
   if (threadIdx.x == 0) {
@@ -139,7 +160,7 @@ __device__ __forceinline__ bool publish_and_elect(double& a, double& b, double* 
   if (!s_last) return false;
   __threadfence();
   double s0 = 0.0, s1 = 0.0;
-  for (int q = threadIdx.x; q < nparts; q += NT) {
+  for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
     s0 += __ldcg(part_base + 2 * q);
     s1 += __ldcg(part_base + 2 * q + 1);
   }
@@ -227,6 +248,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   } while (!ok);
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // 1-D bulk copy global -> shared, completion counted on the mbarrier, L2 evict-first hint
 __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar,
                                          uint64_t pol) {
@@ -270,18 +294,19 @@ __device__ __forceinline__ unsigned span16(const void* lo, const void* hi_excl) 
   return (unsigned)(b - a);
 }
 
+#if PLSS_KDESIGN == 2
 // ---------------------------------------------------------------------------------------------
 // K1 / K2 / plain SpMV: persistent CTAs; each tile's values, indices, row pointers and row-wise
 // vector slices arrive by TMA bulk copies NST-1 tiles ahead; products are formed in place in
 // shared memory; rows are owned by the tile holding their first entry and summed sequentially.
 // ---------------------------------------------------------------------------------------------
 template <int ROLE>
-__global__ void __launch_bounds__(NT, 2) k_spmv(SpmvSeg a) {
+__global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
   using C = Stage<ROLE>;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[NST];
   __shared__ StageDesc sdesc[NST];
-  __shared__ double sm[2][NT / 32];
+  __shared__ double sm[2][MAXW];
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
@@ -368,21 +393,21 @@ __global__ void __launch_bounds__(NT, 2) k_spmv(SpmvSeg a) {
     const int cnt = d.se - d.s0;
     const int voff = d.s0 - d.vb, ioff = d.s0 - d.ib;
     {
-      double v[UNR];
-      int32_t c[UNR];
+      double v[CAP / NT + 1];
+      int32_t c[CAP / NT + 1];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
+      for (int u = 0; u < (CAP + NT - 1) / NT; ++u) {
         const int k = tid + u * NT;
         if (k < cnt) { v[u] = V[voff + k]; c[u] = I[ioff + k]; }
       }
-      double gv[UNR];
+      double gv[CAP / NT + 1];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
+      for (int u = 0; u < (CAP + NT - 1) / NT; ++u) {
         const int k = tid + u * NT;
         if (k < cnt) gv[u] = __ldg(a.g + c[u]);
       }
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
+      for (int u = 0; u < (CAP + NT - 1) / NT; ++u) {
         const int k = tid + u * NT;
         if (k < cnt) V[voff + k] = __dmul_rn(v[u], gv[u]);
       }
@@ -449,13 +474,231 @@ __global__ void __launch_bounds__(NT, 2) k_spmv(SpmvSeg a) {
   }
 }
 
+#else
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 / plain SpMV. Persistent, warp-specialized CTAs:
+//   producer warp : for each of the CTA's tiles, one lane waits for the stage to be released
+//                   (empty mbarrier), then starts TMA bulk copies of the tile's values, indices,
+//                   row pointers and row-wise vector slices (full mbarrier, expect_tx);
+//   8 consumer warps: each owns the rows of the tile whose first entry lies in its 1/8 of the
+//                   tile's nnz window, forms their products in place (gathers of the whole warp
+//                   range in flight), sums each row sequentially (lane per row; warp tree for rows
+//                   > LONGROW), writes the epilogue and releases the stage -- warps never wait for
+//                   each other, only for data.
+// ---------------------------------------------------------------------------------------------
+template <int ROLE>
+__global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
+  using C = Stage<ROLE>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[NST], empty[NST];
+  __shared__ StageDesc sdesc[NST];
+  __shared__ double sm[2][MAXW];
+  if (a.ctl != nullptr && a.ctl->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // contiguous tile range per CTA: consecutive tiles share descriptor loads and gather locality
+  const int G = gridDim.x;
+  const int t_first = (int)(((long long)a.ntiles * blockIdx.x) / G);
+  const int my_tiles = (int)(((long long)a.ntiles * (blockIdx.x + 1)) / G) - t_first;
+  const uint64_t pol = policy_evict_first();
+  double acc0 = 0.0, acc1 = 0.0;
+  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < NST; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], NCW); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ------------------------------ producer ------------------------------------------------
+    // descriptors of the next 32 tiles are loaded by the 32 lanes one batch ahead
+    auto load_batch = [&](int jb, int2& dl, int2& dx) {
+      const int t = t_first + jb + lane;
+      dl = (jb + lane <= my_tiles) ? a.desc[t] : make_int2(0, 0);
+      dx = (jb + 32 <= my_tiles) ? a.desc[t_first + jb + 32] : make_int2(0, 0);
+    };
+    int2 dl, dx, nl = make_int2(0, 0), nx = make_int2(0, 0);
+    load_batch(0, dl, dx);
+    for (int jb = 0; jb < my_tiles; jb += 32) {
+      if (jb + 32 < my_tiles) load_batch(jb + 32, nl, nx);
+      const int cnt = min(32, my_tiles - jb);
+      for (int jj = 0; jj < cnt; ++jj) {
+        const int j = jb + jj;
+        int2 d0, d1;
+        d0.x = __shfl_sync(FULL, dl.x, jj); d0.y = __shfl_sync(FULL, dl.y, jj);
+        const int src = jj < 31 ? jj + 1 : 0;
+        d1.x = __shfl_sync(FULL, jj < 31 ? dl.x : dx.x, src);
+        d1.y = __shfl_sync(FULL, jj < 31 ? dl.y : dx.y, src);
+        if (lane == 0) {
+        const int q = j % NST;
+        if (j >= NST) mbar_wait(&empty[q], (unsigned)(j / NST - 1) & 1u);
+        fence_proxy_async();
+        StageDesc d;
+        d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
+        d.se = min(d1.y, d0.y + CAP);
+        unsigned char* base = smem + q * C::BYTES;
+        unsigned tx = 0, nb;
+        const char* lo;
+        lo = align16_down(a.val + d.s0);
+        nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
+        d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
+        if (nb) { tma_load(base + C::V_OFF, lo, nb, &full[q], pol); tx += nb; }
+        lo = align16_down(a.idx + d.s0);
+        nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
+        d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
+        if (nb) { tma_load(base + C::I_OFF, lo, nb, &full[q], pol); tx += nb; }
+        lo = align16_down(a.ptr + d.r0);
+        nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
+        d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
+        tma_load(base + C::P_OFF, lo, nb, &full[q], pol);
+        tx += nb;
+        d.rb = d.r0;
+        d.rb2 = d.r0;
+        if (C::HAS_V1 && v1src) {
+          lo = align16_down(v1src + d.r0);
+          nb = span16(v1src + d.r0, v1src + d.r1);
+          d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
+          tma_load(base + C::V1_OFF, lo, nb, &full[q], pol);
+          tx += nb;
+        }
+        if (C::HAS_V2) {
+          lo = align16_down(a.pv + d.r0);
+          nb = span16(a.pv + d.r0, a.pv + d.r1);
+          d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
+          tma_load(base + C::V2_OFF, lo, nb, &full[q], pol);
+          tx += nb;
+        }
+        sdesc[q] = d;
+        mbar_expect_tx(&full[q], tx);
+        }
+        __syncwarp();
+      }
+      dl = nl;
+      dx = nx;
+    }
+  } else {
+    // ------------------------------ consumers -----------------------------------------------
+    for (int j = 0; j < my_tiles; ++j) {
+      const int q = j % NST;
+      mbar_wait(&full[q], (unsigned)(j / NST) & 1u);
+      const StageDesc d = sdesc[q];
+      double* V = reinterpret_cast<double*>(smem + q * C::BYTES + C::V_OFF);
+      const int32_t* I = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::I_OFF);
+      const int32_t* P = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::P_OFF);
+      const double* V1 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V1_OFF);
+      const double* V2 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V2_OFF);
+      // this warp's rows: first entry in [s0 + warp*SUBW, s0 + (warp+1)*SUBW) (last warp: to r1)
+      int wr0, wr1;
+      {
+        const long long lo_key = (long long)d.s0 + (long long)warp * SUBW;
+        const long long hi_key = (long long)d.s0 + (long long)(warp + 1) * SUBW;
+        int lo = d.r0, hi = d.r1;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (P[mid - d.pb] < lo_key) lo = mid + 1; else hi = mid; }
+        wr0 = (warp == 0) ? d.r0 : lo;
+        lo = wr0; hi = d.r1;
+        if (warp == NCW - 1) lo = d.r1;
+        else while (lo < hi) { const int mid = (lo + hi) >> 1; if (P[mid - d.pb] < hi_key) lo = mid + 1; else hi = mid; }
+        wr1 = lo;
+      }
+      if (wr0 < wr1) {
+        // products in place over the warp's staged entries
+        const int e0 = P[wr0 - d.pb];
+        const int e1 = min(P[wr1 - d.pb], d.se);
+        const int voff = -d.vb, ioff = -d.ib;
+        for (int k0 = e0; k0 < e1; k0 += 32 * WUNR) {
+          int32_t c[WUNR];
+          double v[WUNR], gv[WUNR];
+#pragma unroll
+          for (int u = 0; u < WUNR; ++u) {
+            const int k = k0 + lane + u * 32;
+            if (k < e1) { c[u] = I[k + ioff]; v[u] = V[k + voff]; }
+          }
+#pragma unroll
+          for (int u = 0; u < WUNR; ++u) {
+            const int k = k0 + lane + u * 32;
+            if (k < e1) gv[u] = __ldg(a.g + c[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < WUNR; ++u) {
+            const int k = k0 + lane + u * 32;
+            if (k < e1) V[k + voff] = __dmul_rn(v[u], gv[u]);
+          }
+        }
+        __syncwarp();
+        const int vsh = -d.vb;
+        for (int rb = wr0; rb < wr1; rb += 32) {
+          const int i = rb + lane;
+          const bool valid = i < wr1;
+          int b = 0, e = 0;
+          if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
+          const bool lng = valid && (e - b) > LONGROW;
+          double s = 0.0;
+          if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
+          if (valid && !lng) {
+            for (int k = b; k < e; ++k) {
+              const double pr = (k < d.se) ? V[k + vsh]
+                                           : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
+              s = __dadd_rn(s, pr);
+            }
+          }
+          unsigned mask = __ballot_sync(FULL, lng);
+          while (mask) {                                        // warp-cooperative long rows
+            const int l = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
+            double ps = 0.0;
+            for (int k = lb + lane; k < le; k += 32) {
+              const double pr = (k < d.se) ? V[k + vsh]
+                                           : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
+              ps = __dadd_rn(ps, pr);
+            }
+            ps = warp_sum(ps);
+            if (lane == l) s = __dadd_rn(s, ps);
+          }
+          if (valid) {
+            if (ROLE == ROLE_PLAIN) {
+              a.out[i] = s;
+            } else if (ROLE == ROLE_K1) {
+              const double rn = __dsub_rn(V1[i - d.rb], s);      // r_i <- r_i - (A p)_i
+              a.out[i] = rn;
+              acc0 = fma(rn, rn, acc0);
+            } else {
+              a.out[i] = s;                                     // y_j
+              if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[q]);                    // stage q released by this warp
+    }
+  }
+  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;           // nothing to reduce
+  __syncthreads();
+  if (!a.finalize) {                                            // slab s < S-1: publish only
+    block_sum2(acc0, acc1, sm);
+    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
+    return;
+  }
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = acc0;                              // local rho -> all-reduce buffer
+    else tail_rho(a.ctl, a.rec, acc0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
+#endif
+
 // ---------------------------------------------------------------------------------------------
 // K3: p <- beta p + gamma y; theta = p^T p; x <- x + p  (L811-813); init: p = gamma y (L795)
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
                                                  double* __restrict__ x, long long n, Ctl* c,
                                                  double* rec, double* partial, unsigned* counter) {
-  __shared__ double sm[2][NT / 32];
+  __shared__ double sm[2][MAXW];
   if (c->done) return;
   const int k = c->iters;
   const bool init = (k == 0);
@@ -509,7 +752,7 @@ __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const d
 __global__ void __launch_bounds__(NT) k_dots_tail(const double* __restrict__ y, const double* __restrict__ p,
                                                   long long n, const double* rho_g, Ctl* c,
                                                   double* rec, double* partial, unsigned* counter) {
-  __shared__ double sm[2][NT / 32];
+  __shared__ double sm[2][MAXW];
   if (c->done) return;
   double a0 = 0.0, a1 = 0.0;
   for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT) {
@@ -528,7 +771,7 @@ __global__ void __launch_bounds__(NT) k_dots_tail(const double* __restrict__ y, 
 __global__ void __launch_bounds__(NT) k_norm_b(const double* __restrict__ r, long long m, Ctl* c,
                                                double* partial, unsigned* counter, int set_nbd,
                                                double* out) {
-  __shared__ double sm[2][NT / 32];
+  __shared__ double sm[2][MAXW];
   double a0 = 0.0, a1 = 0.0;
   for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < m; i += (long long)gridDim.x * NT)
     a0 = fma(r[i], r[i], a0);

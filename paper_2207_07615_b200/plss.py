@@ -47,12 +47,13 @@ class plss_options(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
+def load_library(path: str = None):
     """Load libplss.so (raises if it was not built). torch is imported first so that the NCCL
-    it bundles is the one libplss resolves."""
+    it bundles is the one libplss resolves. PLSS_LIB selects a tuning-variant build."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PLSS_LIB") or LIB_PATH
     import torch  # noqa: F401  (loads torch's libnccl.so.2 / CUDA runtime)
     if not os.path.exists(path):
         raise PlssError(f"{path} is missing: run `python -m paper_2207_07615_b200.build` "
