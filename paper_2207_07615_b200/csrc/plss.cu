@@ -164,7 +164,8 @@ struct plss_ctx {
   int g3 = 1, gdots = 1, gnorm = 1;
   int chunk = 16;
   cudaGraphExec_t graph_chunk = nullptr, graph_one = nullptr;
-  // distributed
+  // distributed (created by plss_create_dist, any nranks >= 1)
+  bool dist = false;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // solve state
@@ -234,7 +235,7 @@ static plss_status enqueue_step(plss_ctx* ctx) {
     else
       launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
   }
-  if (ctx->nranks > 1) {
+  if (ctx->dist) {
     NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
     k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
                                            ctx->part2, ctx->counters + 1);
@@ -559,8 +560,9 @@ plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int
   if (!ctx) return PLSS_E_NOMEM;
   ctx->rank = rank;
   ctx->nranks = nranks;
-  plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, nranks > 1);
-  if (st == PLSS_OK && nranks > 1) {
+  ctx->dist = true;
+  plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, true);
+  if (st == PLSS_OK) {
     ncclUniqueId u;
     memcpy(&u, id, 128);
     ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, u, rank);
@@ -606,7 +608,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
       CK(cudaMemsetAsync(ctx->x, 0, 8 * (size_t)n, st));
     }
   }
-  if (ctx->nranks > 1) {
+  if (ctx->dist) {
     k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 0, ctx->scalars);
     CK(cudaGetLastError());
     NK(ncclAllReduce(ctx->scalars, ctx->scalars, 1, ncclFloat64, ncclSum, ctx->comm, st));
@@ -737,7 +739,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       else launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
       CK(cudaEventRecord(ev[q++], st));
     }
-    if (ctx->nranks > 1) {
+    if (ctx->dist) {
       NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
       CK(cudaEventRecord(ev[q++], st));
       k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
@@ -756,7 +758,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       CK(cudaEventElapsedTime(&t, ev[e + 1], ev[e + 2])); acc[1] += t;
       e += 2;
     }
-    if (ctx->nranks > 1) {
+    if (ctx->dist) {
       CK(cudaEventElapsedTime(&t, ev[e], ev[e + 1])); acc[2] += t;
       CK(cudaEventElapsedTime(&t, ev[e + 1], ev[e + 2])); acc[3] += t;
       e += 2;
@@ -771,7 +773,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
 plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t* slabs, int32_t* tile_nnz,
                        int32_t* grid_k1, int32_t* grid_k2) {
   if (!ctx) return PLSS_E_INVALID;
-  if (launches_per_step) *launches_per_step = 2 * ctx->S + 1 + (ctx->nranks > 1 ? 1 : 0);
+  if (launches_per_step) *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0);
   if (slabs) *slabs = ctx->S;
   if (tile_nnz) *tile_nnz = TILE;
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];

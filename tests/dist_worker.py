@@ -1,0 +1,111 @@
+"""torchrun worker for the row-block tests.
+
+--backend nccl : each rank solves its row block with libplss's plss_create_dist on cuda:LOCAL_RANK
+                 (the NCCL unique id travels through torch.distributed).
+--backend gloo : CPU-only check of the host-side plumbing and of the row-block decomposition the
+                 dist ctx implements: local r_g <- r_g - A_g p, local A_g^T r_g and r_g^T r_g
+                 packed into ONE (n+1) buffer, summed across ranks (gloo all_reduce), then the
+                 replicated scalar tail and p/x update. Products use the oracle's SpMVs (test
+                 infrastructure); the unique id from plss_get_unique_id is broadcast as in bench.py.
+Rank 0 writes hist and x to --out.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import plss_gen  # noqa: E402
+
+
+def gloo_solve(s, blk, dist, torch, maxit):
+    import oracle
+    n = s.n
+    r = blk["b"].copy()
+    nb2 = torch.tensor([float(r @ r)], dtype=torch.float64)
+    dist.all_reduce(nb2)
+    nbd = float(np.sqrt(nb2.item()))
+    p = np.zeros(n)
+    x = np.zeros(n)
+    hist, theta, iters = [], 0.0, 0
+    buf = torch.zeros(n + 1, dtype=torch.float64)
+    while True:
+        if iters > 0:
+            r = r - oracle.spmv(blk["m"], blk["row_ptr"], blk["col_idx"], blk["val"], p)
+        buf[:n] = torch.from_numpy(oracle.spmvT(n, blk["col_ptr"], blk["row_idx"], blk["val_t"], r))
+        buf[n] = float(r @ r)
+        dist.all_reduce(buf)                           # the one collective per iteration
+        y = buf[:n].numpy()
+        rho = float(buf[n])
+        h = np.sqrt(rho) / nbd
+        hist.append(h)
+        if rho == 0.0 or h <= s.tol:
+            break
+        phi = float(y @ y)
+        if iters == 0:
+            p = (rho / phi) * y
+        else:
+            tau = np.sqrt(theta * phi) / rho
+            beta = 1.0 / ((tau - 1.0) * (tau + 1.0))
+            gamma = (theta / rho) * beta
+            p = beta * p + gamma * y
+        theta = float(p @ p)
+        x = x + p
+        iters += 1
+        if iters >= maxit:
+            break
+    return np.array(hist), x, iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--backend", default="gloo")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--config", default="C2s")
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    s = plss_gen.make_config(args.config)
+    blk = plss_gen.row_block(s, world, rank)
+    if args.backend == "gloo":
+        dist.init_process_group("gloo")
+        uid = None
+        if rank == 0:
+            import paper_2207_07615_b200 as pkg
+            uid = pkg.plss_get_unique_id()
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        assert isinstance(obj[0], bytes) and len(obj[0]) == 128
+        hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit)
+    else:
+        import paper_2207_07615_b200 as pkg
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = pkg.plss_get_unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        A = pkg.Matrix.from_arrays(blk["m"], s.n, blk["row_ptr"], blk["col_idx"], blk["val"],
+                                   blk["col_ptr"], blk["row_idx"], blk["val_t"])
+        ctx = pkg.plss_create_dist(A, blk["row_offset"], s.m, obj[0], rank, world, maxit_cap=s.maxit,
+                                   validate=True)
+        res = pkg.plss_solve(ctx, torch.from_numpy(blk["b"]).cuda(), tol=s.tol, maxit=s.maxit)
+        hist, x, iters = res["hist"], res["x"].cpu().numpy(), res["iters"]
+        # every rank holds the same replicated x, bitwise
+        xt = torch.from_numpy(x).cuda()
+        xs = [torch.empty_like(xt) for _ in range(world)]
+        dist.all_gather(xs, xt)
+        assert all(torch.equal(xs[0], q) for q in xs)
+        pkg.plss_destroy(ctx)
+    if rank == 0:
+        np.savez(args.out, hist=hist, x=x, iters=iters)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

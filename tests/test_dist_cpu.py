@@ -1,0 +1,47 @@
+"""World-size-2 gloo test (CPU) of the row-block path's host logic and decomposition."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+
+import oracle
+import plss_gen
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _run(world, cfg, tmp_path):
+    out = tmp_path / f"res_{world}.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "dist_worker.py"), "--backend", "gloo", "--out", str(out),
+           "--config", cfg]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1")
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env, capture_output=True)
+    return np.load(out)
+
+
+def test_row_blocks_world2_match_oracle(tmp_path):
+    s = plss_gen.make_config("C2s")
+    ref = oracle.plss_system(s)
+    r = _run(2, "C2s", tmp_path)
+    assert abs(int(r["iters"]) - ref["iters"]) <= max(1, int(np.ceil(0.02 * ref["iters"])))
+    k = min(50, len(ref["hist"]))
+    assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+    assert np.linalg.norm(r["x"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
+
+
+def test_row_block_bounds_partition():
+    for m in (0, 1, 7, 64_000_000):
+        for G in (1, 2, 4, 8):
+            b = [plss_gen.row_block_bounds(m, G, g) for g in range(G)]
+            assert b[0][0] == 0 and b[-1][1] == m
+            assert all(b[i][1] == b[i + 1][0] for i in range(G - 1))

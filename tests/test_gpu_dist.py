@@ -1,0 +1,76 @@
+"""Distributed (row-block) path of libplss on the GPU.
+
+With one GPU the dist ctx runs with nranks = 1: the same code path (K1 publishing the local rho,
+K2 writing the local y, ncclAllReduce of n+1 doubles, the dots/tail kernel) over a real
+single-rank NCCL communicator. With >= 2 GPUs, `test_two_ranks_torchrun` launches 2 ranks.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import plss_gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2207_07615_b200 import build as pbuild
+    pbuild.build()
+    import paper_2207_07615_b200 as p
+    p.load_library()
+    return p
+
+
+def _dist_solve(pkg, s, slabs=1, **kw):
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    uid = pkg.plss_get_unique_id()
+    args = dict(tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit, flags=1 if s.freeze else 0)
+    args.update(kw)
+    ctx = pkg.plss_create_dist(A, 0, s.m, uid, 0, 1, slabs=slabs, maxit_cap=args["maxit"], validate=True)
+    assert pkg.plss_query(ctx)["launches_per_step"] == 2 * slabs + 2
+    res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), **args)
+    res["xh"] = res["x"].cpu().numpy()
+    pkg.plss_destroy(ctx)
+    return res
+
+
+@pytest.mark.parametrize("name,slabs", [("C1", 1), ("C2s", 1), ("C2s", 3), ("C5xs", 2)])
+def test_dist_single_rank_parity(pkg, name, slabs):
+    s = plss_gen.make_config(name)
+    ref = oracle.plss_system(s)
+    res = _dist_solve(pkg, s, slabs=slabs)
+    assert res["outcome"] == ref["outcome"]
+    assert abs(res["iters"] - ref["iters"]) <= max(1, int(np.ceil(0.02 * ref["iters"])))
+    k = min(25, len(ref["hist"]), len(res["hist"]))
+    assert np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+    assert np.linalg.norm(res["xh"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
+
+
+def test_dist_zero_rhs(pkg):
+    s = plss_gen.make_config("C2s")
+    s.b = np.zeros(s.m)
+    res = _dist_solve(pkg, s)
+    assert res["iters"] == 0 and res["outcome"] == "converged"
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_ranks_torchrun(tmp_path):
+    script = os.path.join(ROOT, "tests", "dist_worker.py")
+    out = tmp_path / "res.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", script, "--backend", "nccl",
+           "--out", str(out)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    r = np.load(out)
+    s = plss_gen.make_config("C5xs")
+    ref = oracle.plss_system(s)
+    k = 25
+    assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+    assert np.linalg.norm(r["x"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
