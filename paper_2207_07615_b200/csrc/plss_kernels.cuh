@@ -27,25 +27,43 @@ namespace plss {
 #define PLSS_TILE 1024
 #endif
 #ifndef PLSS_NST
-#define PLSS_NST 2
+#define PLSS_NST 3
 #endif
 #ifndef PLSS_MINB
-#define PLSS_MINB 4
+#define PLSS_MINB 3
 #endif
 #ifndef PLSS_KDESIGN
-#define PLSS_KDESIGN 2      // 2: CTA-synchronous TMA tiles; 3: warp-specialized producer/consumers
-#endif
+#define PLSS_KDESIGN 4      // 4: CTA TMA tiles, gathers of tile j+1 overlap the rows of tile j
+#endif                      // 2: CTA-synchronous TMA tiles; 3: warp-specialized producer/consumers
 constexpr int NT = 256;                 // threads per CTA of the vector kernels
 constexpr int NCW = 8;                  // consumer warps per SpMV CTA
-#if PLSS_KDESIGN == 2
+#ifndef PLSS_WPC
+#define PLSS_WPC 4
+#endif
+constexpr int WPC = PLSS_WPC;           // design 5: autonomous warps per CTA
+#if PLSS_KDESIGN == 2 || PLSS_KDESIGN == 4
 constexpr int NTS = NT;                 // SpMV CTA: 8 warps, thread 0 also issues the TMA copies
+#elif PLSS_KDESIGN == 5
+constexpr int NTS = WPC * 32;           // SpMV CTA: WPC warps, each its own TMA pipeline
 #else
 constexpr int NTS = (NCW + 1) * 32;     // SpMV CTA: 8 consumer warps + 1 TMA producer warp
 #endif
 constexpr int TILE = PLSS_TILE;         // nnz window of a SpMV tile (rows whose first entry lies in it)
 constexpr int SUBW = TILE / NCW;        // nnz sub-window of one consumer warp
 constexpr int RCAP = TILE / 4;          // at most this many rows per tile
-constexpr int CAP = TILE + TILE / 4;    // staged entries per tile (the last row may spill past TILE)
+#ifndef PLSS_ABLATE
+#define PLSS_ABLATE 0       // timing experiments only: 1 = no gathers, 2 = no row phase
+#endif
+#ifndef PLSS_RLAST
+#define PLSS_RLAST 0
+#endif
+#ifndef PLSS_CONTIG
+#define PLSS_CONTIG 0
+#endif
+#ifndef PLSS_SLACK
+#define PLSS_SLACK (PLSS_TILE / 4)
+#endif
+constexpr int CAP = TILE + PLSS_SLACK;  // staged entries per tile (the last row may spill past TILE)
 constexpr int WUNR = 4;                 // gathers in flight per lane per batch
 constexpr int NST = PLSS_NST;           // TMA pipeline stages per CTA
 constexpr int MINB = PLSS_MINB;         // CTAs per SM the SpMV kernel is compiled for
@@ -97,6 +115,14 @@ struct SpmvSeg {
 // ---------------------------------------------------------------------------------------------
 // memory helpers
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -276,7 +302,7 @@ struct Stage {
   static constexpr int V2_OFF = V1_OFF + V1_BYTES;
   static constexpr int V2_BYTES = HAS_V2 ? (RCAP + 4) * 8 : 0;
   static constexpr int BYTES = (V2_OFF + V2_BYTES + 127) / 128 * 128;
-  static constexpr int SMEM = NST * BYTES;
+  static constexpr int SMEM = (PLSS_KDESIGN == 5 ? WPC : 1) * NST * BYTES;
 };
 
 struct StageDesc {
@@ -310,8 +336,17 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
+#if PLSS_CONTIG
+  // contiguous tile range per CTA: consecutive tiles reuse the gathered vector's lines in L1
+  const int t_first = (int)(((long long)a.ntiles * blockIdx.x) / G);
+  const int my_tiles = (int)(((long long)a.ntiles * (blockIdx.x + 1)) / G) - t_first;
+#else
   const int my_tiles = a.ntiles > (int)blockIdx.x ? (a.ntiles - (int)blockIdx.x + G - 1) / G : 0;
+#endif
   const uint64_t pol = policy_evict_first();
+#if PLSS_RLAST
+  const uint64_t pol_last = policy_evict_last();
+#endif
   double acc0 = 0.0, acc1 = 0.0;
 
   const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
@@ -324,7 +359,11 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
 
   // producer (thread 0): describe tile j of this CTA and start its bulk copies into stage j % NST
   auto issue = [&](int j) {
+#if PLSS_CONTIG
+    const int t = t_first + j;
+#else
     const int t = (int)blockIdx.x + j * G;
+#endif
     const int q = j % NST;
     const int2 d0 = a.desc[t], d1 = a.desc[t + 1];
     StageDesc d;
@@ -393,41 +432,247 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
     const int cnt = d.se - d.s0;
     const int voff = d.s0 - d.vb, ioff = d.s0 - d.ib;
     {
-      double v[CAP / NT + 1];
-      int32_t c[CAP / NT + 1];
+      constexpr int GU = (CAP + NT - 1) / NT;
+      double gv[GU];
 #pragma unroll
-      for (int u = 0; u < (CAP + NT - 1) / NT; ++u) {
+      for (int u = 0; u < GU; ++u) {
         const int k = tid + u * NT;
-        if (k < cnt) { v[u] = V[voff + k]; c[u] = I[ioff + k]; }
-      }
-      double gv[CAP / NT + 1];
-#pragma unroll
-      for (int u = 0; u < (CAP + NT - 1) / NT; ++u) {
-        const int k = tid + u * NT;
-        if (k < cnt) gv[u] = __ldg(a.g + c[u]);
+#if PLSS_ABLATE & 1
+        if (k < cnt) gv[u] = (double)I[ioff + k];              // ablation: no gather
+#else
+        if (k < cnt) gv[u] = __ldg(a.g + I[ioff + k]);
+#endif
       }
 #pragma unroll
-      for (int u = 0; u < (CAP + NT - 1) / NT; ++u) {
+      for (int u = 0; u < GU; ++u) {
         const int k = tid + u * NT;
-        if (k < cnt) V[voff + k] = __dmul_rn(v[u], gv[u]);
+        if (k < cnt) V[voff + k] = __dmul_rn(V[voff + k], gv[u]);
       }
     }
     __syncthreads();
     const int vsh = -d.vb;   // V index of entry position e is e - vb
-    for (int base = d.r0 + warp * 32; base < d.r1; base += NT) {
+    // rows spread evenly over the 8 warps (a tile of short rows has far fewer rows than threads)
+    const int rpw = (d.r1 - d.r0 + NT / 32 - 1) / (NT / 32);
+    const int wlo = d.r0 + warp * rpw, whi = min(d.r1, wlo + rpw);
+#if PLSS_ABLATE & 2
+    if (tid < d.r1 - d.r0) { if (ROLE == ROLE_K1) { a.out[d.r0 + tid] = V[tid + d.s0 - d.vb]; } else a.out[d.r0 + tid] = V[tid + d.s0 - d.vb]; }
+    for (int base = whi; base < whi; base += 32) {            // ablation: no row phase
+#else
+    for (int base = wlo; base < whi; base += 32) {
+#endif
       const int i = base + lane;
-      const bool valid = i < d.r1;
+      const bool valid = i < whi;
       int b = 0, e = 0;
       if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
       const bool lng = valid && (e - b) > LONGROW;
       double s = 0.0;
       if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
       if (valid && !lng) {
-        for (int k = b; k < e; ++k) {
+        const int es = min(e, d.se);
+        int k = b;
+#pragma unroll 1
+        for (; k + 4 <= es; k += 4) {                       // staged products, 4 loads in flight
+          const double p0 = V[k + vsh], p1 = V[k + 1 + vsh], p2 = V[k + 2 + vsh], p3 = V[k + 3 + vsh];
+          s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
+        }
+        for (; k < es; ++k) s = __dadd_rn(s, V[k + vsh]);
+        for (; k < e; ++k)                                   // spill past the staged window
+          s = __dadd_rn(s, __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol))));
+      }
+      unsigned mask = __ballot_sync(FULL, lng);
+      while (mask) {                                            // warp-cooperative long rows
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
+        double ps = 0.0;
+        for (int k = lb + lane; k < le; k += 32) {
           const double pr = (k < d.se) ? V[k + vsh]
                                        : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
-          s = __dadd_rn(s, pr);
+          ps = __dadd_rn(ps, pr);
         }
+        ps = warp_sum(ps);
+        if (lane == l) s = __dadd_rn(s, ps);
+      }
+      if (valid) {
+        if (ROLE == ROLE_PLAIN) {
+          a.out[i] = s;
+        } else if (ROLE == ROLE_K1) {
+          const double rn = __dsub_rn(V1[i - d.rb], s);          // r_i <- r_i - (A p)_i
+#if PLSS_RLAST
+          st_hint(a.out + i, rn, pol_last);                     // keep r_s in L2 for K2_s
+#else
+          a.out[i] = rn;
+#endif
+          acc0 = fma(rn, rn, acc0);
+        } else {
+          a.out[i] = s;                                         // y_j
+          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
+        }
+      }
+    }
+    __syncthreads();                                            // stage q is free again
+  }
+  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;           // nothing to reduce
+  if (!a.finalize) {                                            // slab s < S-1: publish only
+    block_sum2(acc0, acc1, sm);
+    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
+    return;
+  }
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = acc0;                              // local rho -> all-reduce buffer
+    else tail_rho(a.ctl, a.rec, acc0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
+#elif PLSS_KDESIGN == 4
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 / plain SpMV: persistent CTAs, software-pipelined over tiles. Each tile's values,
+// indices, row pointers and row-wise vector slices arrive by TMA bulk copies (thread 0,
+// cp.async.bulk + mbarrier) two tiles ahead; while the rows of tile j are summed, the gathers of
+// tile j+1 are already in flight; their products are then formed in place in shared memory.
+// Rows are owned by the tile holding their first entry and summed sequentially (lane per row).
+// ---------------------------------------------------------------------------------------------
+template <int ROLE>
+__global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
+  using C = Stage<ROLE>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[NST];
+  __shared__ StageDesc sdesc[NST];
+  __shared__ double sm[2][MAXW];
+  if (a.ctl != nullptr && a.ctl->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+#if PLSS_CONTIG
+  // contiguous tile range per CTA: consecutive tiles reuse the gathered vector's lines in L1
+  const int t_first = (int)(((long long)a.ntiles * blockIdx.x) / G);
+  const int my_tiles = (int)(((long long)a.ntiles * (blockIdx.x + 1)) / G) - t_first;
+#else
+  const int my_tiles = a.ntiles > (int)blockIdx.x ? (a.ntiles - (int)blockIdx.x + G - 1) / G : 0;
+#endif
+  const uint64_t pol = policy_evict_first();
+  double acc0 = 0.0, acc1 = 0.0;
+
+  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < NST; ++q) mbar_init(&bars[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // producer (thread 0): describe tile j of this CTA and start its bulk copies into stage j % NST
+  auto issue = [&](int j) {
+#if PLSS_CONTIG
+    const int t = t_first + j;
+#else
+    const int t = (int)blockIdx.x + j * G;
+#endif
+    const int q = j % NST;
+    const int2 d0 = a.desc[t], d1 = a.desc[t + 1];
+    StageDesc d;
+    d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
+    d.se = min(d1.y, d0.y + CAP);
+    unsigned char* base = smem + q * C::BYTES;
+    unsigned tx = 0;
+    const char* lo;
+    unsigned nb;
+    // values [s0, se)
+    lo = align16_down(a.val + d.s0);
+    nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
+    d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
+    if (nb) { tma_load(base + C::V_OFF, lo, nb, &bars[q], pol); tx += nb; }
+    // indices [s0, se)
+    lo = align16_down(a.idx + d.s0);
+    nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
+    d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
+    if (nb) { tma_load(base + C::I_OFF, lo, nb, &bars[q], pol); tx += nb; }
+    // row pointers [r0, r1]
+    lo = align16_down(a.ptr + d.r0);
+    nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
+    d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
+    tma_load(base + C::P_OFF, lo, nb, &bars[q], pol);
+    tx += nb;
+    // row-wise vector slices [r0, r1)
+    d.rb = d.r0;
+    d.rb2 = d.r0;
+    if (d.r1 > d.r0) {
+      if (C::HAS_V1 && v1src) {
+        lo = align16_down(v1src + d.r0);
+        nb = span16(v1src + d.r0, v1src + d.r1);
+        d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
+        tma_load(base + C::V1_OFF, lo, nb, &bars[q], pol);
+        tx += nb;
+      }
+      if (C::HAS_V2) {
+        lo = align16_down(a.pv + d.r0);
+        nb = span16(a.pv + d.r0, a.pv + d.r1);
+        d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
+        tma_load(base + C::V2_OFF, lo, nb, &bars[q], pol);
+        tx += nb;
+      }
+    }
+    sdesc[q] = d;
+    mbar_expect_tx(&bars[q], tx);
+  };
+
+  constexpr int GU = (CAP + NT - 1) / NT;     // gathers per thread per tile
+  // gathers of tile j: issued into registers, committed (products in place) later
+  auto gather_issue = [&](int j, double (&gv)[GU]) {
+    const int q = j % NST;
+    const StageDesc& d = sdesc[q];
+    const int32_t* I = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::I_OFF);
+    const int cnt = d.se - d.s0, ioff = d.s0 - d.ib;
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int k = tid + u * NT;
+      if (k < cnt) gv[u] = __ldg(a.g + I[ioff + k]);
+    }
+  };
+  auto gather_commit = [&](int j, const double (&gv)[GU]) {
+    const int q = j % NST;
+    const StageDesc& d = sdesc[q];
+    double* V = reinterpret_cast<double*>(smem + q * C::BYTES + C::V_OFF);
+    const int cnt = d.se - d.s0, voff = d.s0 - d.vb;
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int k = tid + u * NT;
+      if (k < cnt) V[voff + k] = __dmul_rn(V[voff + k], gv[u]);
+    }
+  };
+  auto rows = [&](int j) {
+    const int q = j % NST;
+    const StageDesc d = sdesc[q];
+    const double* V = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V_OFF);
+    const int32_t* P = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::P_OFF);
+    const double* V1 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V1_OFF);
+    const double* V2 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V2_OFF);
+    const int vsh = -d.vb;   // V index of entry position e is e - vb
+    // rows spread evenly over the 8 warps (a tile of short rows has far fewer rows than threads)
+    const int rpw = (d.r1 - d.r0 + NT / 32 - 1) / (NT / 32);
+    const int wlo = d.r0 + warp * rpw, whi = min(d.r1, wlo + rpw);
+    for (int base = wlo; base < whi; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < whi;
+      int b = 0, e = 0;
+      if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
+      const bool lng = valid && (e - b) > LONGROW;
+      double s = 0.0;
+      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
+      if (valid && !lng) {
+        const int es = min(e, d.se);
+        int k = b;
+#pragma unroll 1
+        for (; k + 4 <= es; k += 4) {                       // staged products, 4 loads in flight
+          const double p0 = V[k + vsh], p1 = V[k + 1 + vsh], p2 = V[k + 2 + vsh], p3 = V[k + 3 + vsh];
+          s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
+        }
+        for (; k < es; ++k) s = __dadd_rn(s, V[k + vsh]);
+        for (; k < e; ++k)                                   // spill past the staged window
+          s = __dadd_rn(s, __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol))));
       }
       unsigned mask = __ballot_sync(FULL, lng);
       while (mask) {                                            // warp-cooperative long rows
@@ -456,7 +701,31 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
         }
       }
     }
-    __syncthreads();                                            // stage q is free again
+  };
+
+  static_assert(NST >= 3, "software pipeline needs 3 stages: rows(j), gathers(j+1), TMA(j+2)");
+  if (tid == 0)
+    for (int j = 0; j < min(NST - 1, my_tiles); ++j) issue(j);
+  double gv[GU];
+  if (my_tiles > 0) {
+    mbar_wait(&bars[0], 0u);
+    gather_issue(0, gv);
+    gather_commit(0, gv);
+  }
+  __syncthreads();
+  for (int j = 0; j < my_tiles; ++j) {
+    if (tid == 0 && j + NST - 1 < my_tiles) {
+      fence_proxy_async();          // generic accesses to that stage (tile j-1) happen-before
+      issue(j + NST - 1);
+    }
+    const bool next = j + 1 < my_tiles;
+    if (next) {
+      mbar_wait(&bars[(j + 1) % NST], (unsigned)((j + 1) / NST) & 1u);
+      gather_issue(j + 1, gv);      // in flight while the rows of tile j are summed
+    }
+    rows(j);
+    if (next) gather_commit(j + 1, gv);
+    __syncthreads();
   }
   if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;           // nothing to reduce
   if (!a.finalize) {                                            // slab s < S-1: publish only
@@ -468,6 +737,211 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
   if (tid != 0) return;
   if (ROLE == ROLE_K1) {
     if (a.dist) *a.rho_out = acc0;                              // local rho -> all-reduce buffer
+    else tail_rho(a.ctl, a.rec, acc0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
+#elif PLSS_KDESIGN == 5
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 / plain SpMV, warp-autonomous pipelines. Every warp owns a contiguous range of small
+// tiles (TILE entries, <= TILE/4 rows) and its own NST-stage ring of shared memory: lane 0
+// issues the TMA bulk copies of tile j+NST-1 (values, indices, row pointers, row-wise vector
+// slices) while the warp forms the products of tile j (all its gathers in flight) and sums its
+// rows sequentially (lane per row). No CTA-wide barrier: a warp waiting on a slow gather never
+// holds up the other warps.
+// ---------------------------------------------------------------------------------------------
+template <int ROLE>
+__global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
+  using C = Stage<ROLE>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[WPC][NST];
+  __shared__ StageDesc sdesc[WPC][NST];
+  __shared__ double sm[2][MAXW];
+  if (a.ctl != nullptr && a.ctl->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long GW = (long long)gridDim.x * WPC;
+  const long long gw = (long long)blockIdx.x * WPC + warp;
+  const int t_first = (int)(((long long)a.ntiles * gw) / GW);
+  const int my_tiles = (int)(((long long)a.ntiles * (gw + 1)) / GW) - t_first;
+  const uint64_t pol = policy_evict_first();
+  double acc0 = 0.0, acc1 = 0.0;
+  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
+  unsigned char* wsm = smem + warp * NST * C::BYTES;
+  uint64_t* wb = bars[warp];
+  StageDesc* wd = sdesc[warp];
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NST; ++q) mbar_init(&wb[q], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // tile descriptors, 32 per batch, the next batch prefetched
+  int cur = -1;
+  int2 bl = make_int2(0, 0), bx = make_int2(0, 0), nl = make_int2(0, 0), nx = make_int2(0, 0);
+  auto load_batch = [&](int jb, int2& l, int2& x) {
+    const int t = t_first + jb + lane;
+    l = (jb + lane <= my_tiles) ? a.desc[t] : make_int2(0, 0);
+    x = (jb + 32 <= my_tiles) ? a.desc[t_first + jb + 32] : make_int2(0, 0);
+  };
+  auto desc_of = [&](int j, int2& d0, int2& d1) {   // warp-uniform j
+    const int jb = j & ~31;
+    if (jb != cur) {
+      if (cur >= 0 && jb == cur + 32) { bl = nl; bx = nx; } else load_batch(jb, bl, bx);
+      cur = jb;
+      if (jb + 32 < my_tiles) load_batch(jb + 32, nl, nx);
+    }
+    const int jj = j - jb;
+    d0.x = __shfl_sync(FULL, bl.x, jj);
+    d0.y = __shfl_sync(FULL, bl.y, jj);
+    const int ax = __shfl_sync(FULL, bl.x, (jj + 1) & 31), ay = __shfl_sync(FULL, bl.y, (jj + 1) & 31);
+    const int cx = __shfl_sync(FULL, bx.x, 0), cy = __shfl_sync(FULL, bx.y, 0);
+    d1.x = jj < 31 ? ax : cx;
+    d1.y = jj < 31 ? ay : cy;
+  };
+  auto issue = [&](int j, int2 d0, int2 d1) {      // lane 0 only
+    const int q = j % NST;
+    StageDesc d;
+    d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
+    d.se = min(d1.y, d0.y + CAP);
+    unsigned char* base = wsm + q * C::BYTES;
+    unsigned tx = 0, nb;
+    const char* lo;
+    lo = align16_down(a.val + d.s0);
+    nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
+    d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
+    if (nb) { tma_load(base + C::V_OFF, lo, nb, &wb[q], pol); tx += nb; }
+    lo = align16_down(a.idx + d.s0);
+    nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
+    d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
+    if (nb) { tma_load(base + C::I_OFF, lo, nb, &wb[q], pol); tx += nb; }
+    lo = align16_down(a.ptr + d.r0);
+    nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
+    d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
+    tma_load(base + C::P_OFF, lo, nb, &wb[q], pol);
+    tx += nb;
+    d.rb = d.r0;
+    d.rb2 = d.r0;
+    if (C::HAS_V1 && v1src) {
+      lo = align16_down(v1src + d.r0);
+      nb = span16(v1src + d.r0, v1src + d.r1);
+      d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
+      tma_load(base + C::V1_OFF, lo, nb, &wb[q], pol);
+      tx += nb;
+    }
+    if (C::HAS_V2) {
+      lo = align16_down(a.pv + d.r0);
+      nb = span16(a.pv + d.r0, a.pv + d.r1);
+      d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
+      tma_load(base + C::V2_OFF, lo, nb, &wb[q], pol);
+      tx += nb;
+    }
+    wd[q] = d;
+    mbar_expect_tx(&wb[q], tx);
+  };
+
+  for (int j = 0; j < min(NST - 1, my_tiles); ++j) {
+    int2 d0, d1;
+    desc_of(j, d0, d1);
+    if (lane == 0) issue(j, d0, d1);
+  }
+  constexpr int GU = (CAP + 31) / 32;
+  for (int j = 0; j < my_tiles; ++j) {
+    const int q = j % NST;
+    if (j + NST - 1 < my_tiles) {
+      int2 d0, d1;
+      desc_of(j + NST - 1, d0, d1);
+      if (lane == 0) {
+        fence_proxy_async();        // this warp's generic accesses to that stage (tile j-1) happen-before
+        issue(j + NST - 1, d0, d1);
+      }
+    }
+    mbar_wait(&wb[q], (unsigned)(j / NST) & 1u);
+    const StageDesc d = wd[q];
+    double* V = reinterpret_cast<double*>(wsm + q * C::BYTES + C::V_OFF);
+    const int32_t* I = reinterpret_cast<const int32_t*>(wsm + q * C::BYTES + C::I_OFF);
+    const int32_t* P = reinterpret_cast<const int32_t*>(wsm + q * C::BYTES + C::P_OFF);
+    const double* V1 = reinterpret_cast<const double*>(wsm + q * C::BYTES + C::V1_OFF);
+    const double* V2 = reinterpret_cast<const double*>(wsm + q * C::BYTES + C::V2_OFF);
+    {
+      const int cnt = d.se - d.s0;
+      const int voff = d.s0 - d.vb, ioff = d.s0 - d.ib;
+      double gv[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int k = lane + u * 32;
+        if (k < cnt) gv[u] = __ldg(a.g + I[ioff + k]);
+      }
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int k = lane + u * 32;
+        if (k < cnt) V[voff + k] = __dmul_rn(V[voff + k], gv[u]);
+      }
+    }
+    __syncwarp();
+    const int vsh = -d.vb;
+    for (int base = d.r0; base < d.r1; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < d.r1;
+      int b = 0, e = 0;
+      if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
+      const bool lng = valid && (e - b) > LONGROW;
+      double s = 0.0;
+      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
+      if (valid && !lng) {
+        const int es = min(e, d.se);
+        int k = b;
+#pragma unroll 1
+        for (; k + 4 <= es; k += 4) {
+          const double p0 = V[k + vsh], p1 = V[k + 1 + vsh], p2 = V[k + 2 + vsh], p3 = V[k + 3 + vsh];
+          s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
+        }
+        for (; k < es; ++k) s = __dadd_rn(s, V[k + vsh]);
+        for (; k < e; ++k)
+          s = __dadd_rn(s, __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol))));
+      }
+      unsigned mask = __ballot_sync(FULL, lng);
+      while (mask) {
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
+        double ps = 0.0;
+        for (int k = lb + lane; k < le; k += 32) {
+          const double pr = (k < d.se) ? V[k + vsh]
+                                       : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
+          ps = __dadd_rn(ps, pr);
+        }
+        ps = warp_sum(ps);
+        if (lane == l) s = __dadd_rn(s, ps);
+      }
+      if (valid) {
+        if (ROLE == ROLE_PLAIN) {
+          a.out[i] = s;
+        } else if (ROLE == ROLE_K1) {
+          const double rn = __dsub_rn(V1[i - d.rb], s);
+          a.out[i] = rn;
+          acc0 = fma(rn, rn, acc0);
+        } else {
+          a.out[i] = s;
+          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;
+  __syncthreads();
+  if (!a.finalize) {
+    block_sum2(acc0, acc1, sm);
+    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
+    return;
+  }
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = acc0;
     else tail_rho(a.ctl, a.rec, acc0);
   } else if (ROLE == ROLE_K2DOTS) {
     tail_y(a.ctl, a.rec, acc0, acc1);
