@@ -19,6 +19,8 @@
  *
  * Conventions
  *  - Every call returns plss_status (0 = OK); no call aborts or exits the process.
+ *  - Matrix arrays must be 16-byte aligned with 16-byte padded allocations (TMA bulk copies read
+ *    the 16-byte superset of a range); plss_create checks the alignment.
  *  - Index arrays are int32, values fp64 (binary64, round-to-nearest-even).
  *  - CSR: row_ptr[m+1] (row_ptr[0] = 0, nondecreasing, row_ptr[m] = nnz), col_idx[nnz] strictly
  *    ascending within each row, val[nnz]. CSC copy of the SAME matrix: col_ptr[n+1],
@@ -79,12 +81,13 @@ typedef struct {
                           With S > 1 the library keeps a slab-major CSC copy in the workspace. */
   int32_t graph_chunk; /* iterations per CUDA-graph launch (0 = auto)                        */
   int32_t maxit_cap;   /* largest maxit a solve on this ctx may request (sizes the history)  */
-  int32_t flags;       /* reserved, must be 0                                                 */
+  int32_t flags;       /* bit0: disable the SELL-32 format (saves its ~2 x 1.15 nnz x 12 B of
+                          workspace); other bits must be 0                                 */
 } plss_options;
 
 /* Bytes of DEVICE workspace a ctx needs (vectors r, y, p, x, reduction partials, control block,
- * history of (maxit_cap+1)*PLSS_REC doubles, tile maps, the optional slab-major CSC copy and,
- * for plss_create_dist, the (n+1)-double AllReduce buffer). opt may be NULL (defaults).
+ * history of (maxit_cap+1)*PLSS_REC doubles, tile maps, the optional slab-major CSC copy, the
+ * SELL-32 copies of A (unless opt->flags bit0) and the (n+1)-double AllReduce buffer). opt may be NULL (defaults).
  * The caller allocates it (e.g. a torch uint8 tensor), 256-byte aligned, and keeps it alive
  * for the ctx's lifetime. Returns 0 on invalid input. */
 size_t plss_workspace_bytes(const plss_matrix *A, const plss_options *opt);
@@ -146,9 +149,12 @@ plss_status plss_spmvT(plss_ctx *ctx, const double *u, double *v);
  * the distributed dots/tail kernel, K3. Synchronizes. */
 plss_status plss_profile(plss_ctx *ctx, int32_t k, double *ms);
 
-/* Introspection: kernel launches per loop step, number of slabs, grid sizes (for bench/ncu). */
+/* Introspection (bench / ncu): kernel launches per loop step, number of row slabs, CSR-tile nnz
+ * window, grid sizes of the first K1 / K2 launch, and how many of the 2*slabs SpMV segments use
+ * the SELL-32 format (the rest use TMA-staged CSR tiles). Any pointer may be NULL. */
 plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t *slabs,
-                       int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2);
+                       int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2,
+                       int32_t *sell_segments);
 
 void plss_destroy(plss_ctx *ctx);
 const char *plss_status_str(plss_status s);

@@ -49,6 +49,9 @@ struct Layout {
   int maxit_cap = 0;
   size_t r, y, p, x, rec, ctl, counters, part1, part2, part3, partn, tile1, tile2, scratch,
       scratch_blk, sptr, sidx, sval, scan_cnt, scan_blk, buf, err, scalars, total;
+  bool sell = true;
+  size_t s1idx, s1val, s1perm, s1sptr, s2idx, s2val, s2perm, s2sptr;
+  int64_t s1cap, s2cap, s1slots, s2slots, s1sp, s2sp;  // pool capacities (entries / slots / sptr)
 };
 
 bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, Layout* L) {
@@ -80,6 +83,24 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   L->tile1 = take(8 * (size_t)(tiles1 + S));
   L->tile2 = take(8 * (size_t)(tiles2 + S));
   L->scratch = take(4 * (size_t)(std::max(m, n) + 2));
+  // SELL-32 pools (K1 over the CSR row slabs, K2 over the CSC slabs); opt.flags bit0 disables
+  L->sell = !(o.flags & 1);
+  if (L->sell) {
+    L->s1cap = nnz * 115 / 100 + 4096ll * S;
+    L->s2cap = nnz * 115 / 100 + 4096ll * S;
+    L->s1slots = (m / 32 + 2 * S + 1) * 32;
+    L->s2slots = (int64_t)S * (n / 32 + 2) * 32;
+    L->s1sp = m / 32 + 3 * S + 2;
+    L->s2sp = (int64_t)S * (n / 32 + 3) + 2;
+    L->s1idx = take(4 * (size_t)L->s1cap);
+    L->s1val = take(8 * (size_t)L->s1cap);
+    L->s1perm = take(4 * (size_t)L->s1slots);
+    L->s1sptr = take(4 * (size_t)L->s1sp);
+    L->s2idx = take(4 * (size_t)L->s2cap);
+    L->s2val = take(8 * (size_t)L->s2cap);
+    L->s2perm = take(4 * (size_t)L->s2slots);
+    L->s2sptr = take(4 * (size_t)L->s2sp);
+  }
   L->scratch_blk = take(4 * (size_t)((std::max(m, n) + 2) / (NT * SCAN_ITEMS) + 2));
   if (S > 1) {
     L->sptr = take(4 * (size_t)S * (n + 1));
@@ -202,7 +223,10 @@ static void set_err(plss_ctx* ctx, const std::string& s) {
 
 template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
-  k_spmv<ROLE><<<grid, NTS, Stage<ROLE>::SMEM, st>>>(a);
+  if (a.fmt == 1)
+    k_sell<ROLE><<<grid, NT, 0, st>>>(a);
+  else
+    k_spmv<ROLE><<<grid, NTS, Stage<ROLE>::SMEM, st>>>(a);
 }
 
 // order our work stream after / before the caller's stream when they differ
@@ -307,6 +331,67 @@ static plss_status set_smem_attrs(plss_ctx* ctx, int occ[4]) {
 }
 
 
+// SELL pool cursor of one side (K1 or K2)
+struct SellPool {
+  int32_t *idx, *perm, *sptr;
+  double* val;
+  int64_t cap, slots, sp;      // capacities
+  int64_t used, used_slots, used_sp;
+};
+
+// Convert one segment (CSR-like: ptr[nrows+1] absolute positions, idx, val) to SELL-32 if the
+// padding stays small: unsorted when rows are (nearly) uniform, else sigma-sorted windows of 256.
+static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool, int sms, int occ) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nrows = a.nrows;
+  const int64_t nsl = (nrows + 31) / 32;
+  if (nrows == 0 || nnz_seg == 0) return PLSS_OK;
+  if (pool.used_slots + nsl * 32 > pool.slots || pool.used_sp + nsl + 1 > pool.sp) return PLSS_OK;
+  int32_t* len = (int32_t*)(ctx->ws + ctx->L.scratch);
+  int32_t* blk = (int32_t*)(ctx->ws + ctx->L.scratch_blk);
+  int32_t* sp = pool.sptr + pool.used_sp;
+  int32_t* perm = pool.perm + pool.used_slots;
+  const unsigned g = (unsigned)((nrows + 255) / 256);
+  const unsigned gs = (unsigned)((nsl + 1 + 255) / 256);
+  k_row_len<<<g, 256, 0, st>>>(a.ptr, nrows, len);
+  int64_t steps = 0;
+  const int32_t* use_perm = nullptr;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      k_sigma_sort<<<(unsigned)((nrows + SIGMA - 1) / SIGMA), SIGMA, 0, st>>>(len, nrows, nsl * 32, perm);
+      use_perm = perm;
+    }
+    k_slice_len<<<gs, 256, 0, st>>>(len, use_perm, nrows, nsl, sp);
+    if (scan_excl(ctx, sp, nsl + 1, blk) != PLSS_OK) return PLSS_E_CUDA;
+    int32_t tot[2] = {0, 0};                          // sp[nsl-1], sp[nsl]
+    CK(cudaMemcpyAsync(tot, sp + nsl - 1, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    steps = tot[1];
+    // padding of the partial last slice is bounded (one slice per segment): not counted
+    const int64_t padded = steps * 32 - (nsl * 32 - nrows) * (int64_t)(tot[1] - tot[0]);
+    const double limit = pass == 0 ? 1.03 : 1.15;
+    if ((double)padded <= limit * (double)nnz_seg + 1024.0) break;
+    if (pass == 1) return PLSS_OK;                    // too irregular: stay on CSR tiles
+  }
+  if (pool.used + steps * 32 > pool.cap) return PLSS_OK;
+  int32_t* sidx = pool.idx + pool.used;
+  double* sval = pool.val + pool.used;
+  k_sell_fill<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, st>>>(a.ptr, a.idx, a.val, use_perm, nrows, nsl, sp,
+                                                                  sidx, sval);
+  CK(cudaGetLastError());
+  a.fmt = 1;
+  a.nslices = (int32_t)nsl;
+  a.sptr = sp;
+  a.perm = use_perm;
+  a.idx = sidx;
+  a.val = sval;
+  pool.used += steps * 32;
+  pool.used_slots += nsl * 32;
+  pool.used_sp += nsl + 1;
+  (void)sms; (void)occ;
+  return PLSS_OK;
+}
+
 static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options* opt, void* workspace,
                          size_t ws_bytes, void* stream, bool dist) {
   ctx->A = *A;
@@ -317,7 +402,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (!A->row_ptr || !A->col_ptr || (A->nnz > 0 && (!A->col_idx || !A->val || !A->row_idx || !A->val_t))) {
     set_err(ctx, "NULL matrix array"); return PLSS_E_INVALID;
   }
-  if (opt && opt->flags != 0) { set_err(ctx, "options.flags must be 0"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & ~1) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
   {
     const void* arrs[6] = {A->row_ptr, A->col_idx, A->val, A->col_ptr, A->row_idx, A->val_t};
     for (const void* q : arrs)
@@ -404,6 +489,19 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (set_smem_attrs(ctx, occ) != PLSS_OK) return PLSS_E_CUDA;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_vec, k_pxupdate, NT, 0));
   occ_vec = std::max(1, occ_vec);
+  int occ_sell = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sell, k_sell<ROLE_K2DOTS>, NT, 0));
+  occ_sell = std::max(1, occ_sell);
+  SellPool pool1{}, pool2{};
+  if (L.sell) {
+    pool1 = SellPool{(int32_t*)(w + L.s1idx), (int32_t*)(w + L.s1perm), (int32_t*)(w + L.s1sptr),
+                     (double*)(w + L.s1val), L.s1cap, L.s1slots, L.s1sp, 0, 0, 0};
+    pool2 = SellPool{(int32_t*)(w + L.s2idx), (int32_t*)(w + L.s2perm), (int32_t*)(w + L.s2sptr),
+                     (double*)(w + L.s2val), L.s2cap, L.s2slots, L.s2sp, 0, 0, 0};
+  }
+  auto sell_grid = [&](const SpmvSeg& a) {
+    return grid_for(((int64_t)a.nslices + NT / 32 - 1) / (NT / 32), occ_sell, sms);
+  };
 
   // ---- K1 segments (CSR row slabs) ----------------------------------------------------------
   int2* desc1 = (int2*)(w + L.tile1);
@@ -441,6 +539,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.rho_out = ctx->y + n;
     t1off += nt + 1;
     ctx->g1[s] = grid_for(nt, occ[ROLE_K1], sms);
+    if (L.sell) {
+      if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool1, sms, occ_sell) != PLSS_OK) return PLSS_E_CUDA;
+      if (a.fmt == 1) ctx->g1[s] = sell_grid(a);
+    }
   }
 
   // ---- K2 segments (CSC, slab-major copy when S > 1) ----------------------------------------
@@ -493,6 +595,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.rec = ctx->rec;
     t2off += nt + 1;
     ctx->g2[s] = grid_for(nt, occ[a.finalize ? ROLE_K2DOTS : ROLE_K2], sms);
+    if (L.sell) {
+      if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool2, sms, occ_sell) != PLSS_OK) return PLSS_E_CUDA;
+      if (a.fmt == 1) ctx->g2[s] = sell_grid(a);
+    }
   }
   CK(cudaGetLastError());
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
@@ -771,8 +877,14 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
 }
 
 plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t* slabs, int32_t* tile_nnz,
-                       int32_t* grid_k1, int32_t* grid_k2) {
+                       int32_t* grid_k1, int32_t* grid_k2, int32_t* sell_segments) {
   if (!ctx) return PLSS_E_INVALID;
+  if (sell_segments) {
+    int c = 0;
+    for (auto& a : ctx->seg1) c += a.fmt == 1;
+    for (auto& a : ctx->seg2) c += a.fmt == 1;
+    *sell_segments = c;
+  }
   if (launches_per_step) *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0);
   if (slabs) *slabs = ctx->S;
   if (tile_nnz) *tile_nnz = TILE;

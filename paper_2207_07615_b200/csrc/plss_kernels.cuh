@@ -27,14 +27,14 @@ namespace plss {
 #define PLSS_TILE 1024
 #endif
 #ifndef PLSS_NST
-#define PLSS_NST 3
+#define PLSS_NST 2
 #endif
 #ifndef PLSS_MINB
-#define PLSS_MINB 3
+#define PLSS_MINB 4
 #endif
 #ifndef PLSS_KDESIGN
-#define PLSS_KDESIGN 4      // 4: CTA TMA tiles, gathers of tile j+1 overlap the rows of tile j
-#endif                      // 2: CTA-synchronous TMA tiles; 3: warp-specialized producer/consumers
+#define PLSS_KDESIGN 2      // CSR-tile kernel design: 2 CTA-synchronous TMA tiles (default);
+#endif                      // 3 warp-specialized; 4 software-pipelined; 5 warp-autonomous
 constexpr int NT = 256;                 // threads per CTA of the vector kernels
 constexpr int NCW = 8;                  // consumer warps per SpMV CTA
 #ifndef PLSS_WPC
@@ -110,6 +110,12 @@ struct SpmvSeg {
   Ctl* ctl;
   double* rec;
   double* rho_out;           // dist: where the local rho goes (all-reduce buffer [n])
+  // SELL-32 format (fmt = 1): slice s holds rows perm[32s .. 32s+31] column-major, entry j of
+  // its lane l at (sptr[s] + j) * 32 + l; padding entries have index -1
+  int32_t fmt;               // 0: CSR tiles through TMA (k_spmv), 1: SELL-32 (k_sell)
+  int32_t nslices;
+  const int32_t* sptr;       // nslices+1 slice starts in 32-entry steps
+  const int32_t* perm;       // slot -> segment-local row (sigma-sorted), -1 for padding; or NULL
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -1165,6 +1171,148 @@ __global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
 }
 
 #endif
+
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 / plain SpMV over SELL-32 (sliced ELLPACK, slices of 32 rows, sigma-sorted by length
+// when rows vary). One warp streams one slice: at step j lane l loads entry j of its row with
+// fully coalesced 128-bit-per-quarter-warp loads (idx 128 B, val 256 B per step), gathers g and
+// adds the product to its row sum in ascending entry order (bitwise the oracle's sequential sum).
+// No shared memory: on B200 the SpMV is bound by L1 data-pipe wavefronts, and staging through
+// shared memory costs more of them than it saves (profiles/r01_notes.md).
+// ---------------------------------------------------------------------------------------------
+#ifndef PLSS_SU
+#define PLSS_SU 8
+#endif
+#ifndef PLSS_SELL_MINB
+#define PLSS_SELL_MINB 4
+#endif
+constexpr int SU = PLSS_SU;             // steps (entries per lane) in flight
+constexpr int SELL_MINB = PLSS_SELL_MINB;
+
+template <int ROLE>
+__global__ void __launch_bounds__(NT, SELL_MINB) k_sell(SpmvSeg a) {
+  __shared__ double sm[2][MAXW];
+  if (a.ctl != nullptr && a.ctl->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pol = policy_evict_first();
+  double acc0 = 0.0, acc1 = 0.0;
+  const int wtotal = gridDim.x * (NT / 32);
+  for (int sl = blockIdx.x * (NT / 32) + warp; sl < a.nslices; sl += wtotal) {
+    const int st0 = a.sptr[sl], L = a.sptr[sl + 1] - st0;
+    const int slot = sl * 32 + lane;
+    const int row = a.perm ? a.perm[slot] : slot;
+    const bool valid = row >= 0 && row < a.nrows;
+    double s = 0.0;
+    if (ROLE >= ROLE_K2 && valid && a.accumulate) s = a.out[row];
+    const int32_t* ip = a.idx + (long long)st0 * 32 + lane;
+    const double* vp = a.val + (long long)st0 * 32 + lane;
+    int j = 0;
+    for (; j + SU <= L; j += SU) {
+      int32_t c[SU];
+      double v[SU], gv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
+    }
+    if (j < L) {
+      int32_t c[SU];
+      double v[SU], gv[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        c[u] = -1;
+        if (j + u < L) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
+    }
+    if (valid) {
+      if (ROLE == ROLE_PLAIN) {
+        a.out[row] = s;
+      } else if (ROLE == ROLE_K1) {
+        const double rn = __dsub_rn(a.out[row], s);             // r_i <- r_i - (A p)_i
+        a.out[row] = rn;
+        acc0 = fma(rn, rn, acc0);
+      } else {
+        a.out[row] = s;                                         // y_j
+        if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, a.pv[row], acc1); }
+      }
+    }
+  }
+  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;
+  if (!a.finalize) {
+    block_sum2(acc0, acc1, sm);
+    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
+    return;
+  }
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = acc0;
+    else tail_rho(a.ctl, a.rec, acc0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
+// ---- SELL-32 construction (setup, once per segment) ------------------------------------------
+__global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) len[i] = ptr[i + 1] - ptr[i];
+}
+// sigma-sort: within each window of SIGMA rows, slots ordered by length descending (stable)
+constexpr int SIGMA = 256;
+__global__ void __launch_bounds__(SIGMA) k_sigma_sort(const int32_t* len, long long nrows, long long nslots,
+                                                      int32_t* perm) {
+  __shared__ int32_t sl[SIGMA];
+  const long long w0 = (long long)blockIdx.x * SIGMA;
+  const int t = threadIdx.x;
+  const long long i = w0 + t;
+  sl[t] = i < nrows ? len[i] : -1;                               // missing rows sort last
+  __syncthreads();
+  const int mine = sl[t];
+  int rank = 0;
+  for (int q = 0; q < SIGMA; ++q) {
+    const int o = sl[q];
+    rank += (o > mine) || (o == mine && q < t);
+  }
+  if (w0 + rank < nslots) perm[w0 + rank] = i < nrows ? (int32_t)i : -1;
+}
+__global__ void k_slice_len(const int32_t* len, const int32_t* perm, long long nrows, long long nslices,
+                            int32_t* slen) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > nslices) return;
+  if (s == nslices) { slen[s] = 0; return; }
+  int mx = 0;
+  for (int l = 0; l < 32; ++l) {
+    const long long slot = s * 32 + l;
+    const long long row = perm ? perm[slot] : slot;
+    if (row >= 0 && row < nrows) mx = max(mx, len[row]);
+  }
+  slen[s] = mx;
+}
+// thread per slot: copy its row's entries (column-major within the slice), pad with index -1
+__global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double* val, const int32_t* perm,
+                            long long nrows, long long nslices, const int32_t* sptr, int32_t* sidx,
+                            double* sval) {
+  const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nslices * 32) return;
+  const long long s = slot >> 5;
+  const int lane = (int)(slot & 31);
+  const long long row = perm ? perm[slot] : slot;
+  const int L = sptr[s + 1] - sptr[s];
+  long long b = 0, e = 0;
+  if (row >= 0 && row < nrows) { b = ptr[row]; e = ptr[row + 1]; }
+  for (int j = 0; j < L; ++j) {
+    const long long dst = ((long long)sptr[s] + j) * 32 + lane;
+    if (b + j < e) { sidx[dst] = idx[b + j]; sval[dst] = val[b + j]; }
+    else { sidx[dst] = -1; sval[dst] = 0.0; }
+  }
+}
 
 // ---------------------------------------------------------------------------------------------
 // K3: p <- beta p + gamma y; theta = p^T p; x <- x + p  (L811-813); init: p = gamma y (L795)

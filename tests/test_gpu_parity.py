@@ -45,11 +45,11 @@ def _matrix(pkg, s):
     return pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
 
 
-def _gpu_solve(pkg, s, slabs=0, x0=None, **kw):
+def _gpu_solve(pkg, s, slabs=0, x0=None, sell=True, **kw):
     A = _matrix(pkg, s)
     args = dict(tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit, flags=1 if s.freeze else 0)
     args.update(kw)
-    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=max(args["maxit"], 1), validate=True)
+    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=max(args["maxit"], 1), validate=True, sell=sell)
     b = torch.from_numpy(s.b).cuda()
     xx0 = torch.from_numpy(x0).cuda() if x0 is not None else None
     res = pkg.plss_solve(ctx, b, xx0, want_diag=True, **args)
@@ -119,11 +119,11 @@ def _ragged_system(seed=0, m=3000, n=5000):
     return plss_gen._finish("ragged", m, n, row_ptr, col_idx, val, rng.standard_normal(n), 1e-8, 0, 100)
 
 
-@pytest.mark.parametrize("slabs", [1, 3])
-def test_spmv_spmvT_bit_exact(pkg, slabs):
+@pytest.mark.parametrize("slabs,sell", [(1, True), (3, True), (1, False), (3, False)])
+def test_spmv_spmvT_bit_exact(pkg, slabs, sell):
     s = _ragged_system()
     A = _matrix(pkg, s)
-    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=10, validate=True)
+    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=10, validate=True, sell=sell)
     rng = np.random.default_rng(1)
     x = rng.standard_normal(s.n)
     u = rng.standard_normal(s.m)
@@ -142,9 +142,15 @@ def test_spmv_spmvT_bit_exact(pkg, slabs):
 @pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "C5xs"])
 def test_spmv_configs_bit_exact(pkg, name):
     s = plss_gen.make_config(name)
-    for slabs in (1, 4):
+    for slabs, sell in ((1, True), (4, True), (1, False), (4, False)):
         A = _matrix(pkg, s)
-        ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=4)
+        ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=4, sell=sell)
+        q = pkg.plss_query(ctx)
+        if not sell:
+            assert q["sell_segments"] == 0
+        elif name in ("C1", "C2s", "C5xs"):
+            # regular rows: SELL-32 for every CSR slab; CSC slabs of short columns may stay on tiles
+            assert q["sell_segments"] == 2 if slabs == 1 else q["sell_segments"] >= q["slabs"]
         x = np.random.default_rng(2).standard_normal(s.n)
         u = np.random.default_rng(3).standard_normal(s.m)
         y = torch.empty(s.m, dtype=torch.float64, device="cuda")
@@ -171,14 +177,15 @@ def test_worked_example(pkg):
     assert abs(d[0, 7] - 5 / 17) <= 1e-15 and abs(d[1, 6] - 9 / 25) <= 1e-15 and abs(d[1, 7] - 17 / 20) <= 1e-15
 
 
-@pytest.mark.parametrize("name,slabs", [("C1", 0), ("C2s", 0), ("C2s", 3), ("C4s", 0), ("C4xs", 0),
-                                        ("C5xs", 0), ("C5xs", 4)])
-def test_solve_parity(pkg, name, slabs):
+@pytest.mark.parametrize("name,slabs,sell", [("C1", 0, True), ("C2s", 0, True), ("C2s", 3, True),
+                                             ("C2s", 3, False), ("C4s", 0, True), ("C4xs", 0, True),
+                                             ("C5xs", 0, True), ("C5xs", 4, True), ("C5xs", 4, False)])
+def test_solve_parity(pkg, name, slabs, sell):
     s = plss_gen.make_config(name)
     if name == "C4s":
         s.maxit = 400          # ill-conditioned; not converged: compared within the parity floor
     ref = oracle.plss_system(s)
-    res = _gpu_solve(pkg, s, slabs=slabs)
+    res = _gpu_solve(pkg, s, slabs=slabs, sell=sell)
     _assert_parity(res, ref, _floor(s, ref), s)
     if name.startswith("C4"):
         empty = np.diff(s.col_ptr) == 0      # x in range(A^T): empty columns stay exactly 0
