@@ -196,6 +196,7 @@ def main():
     ap.add_argument("--impl", default="plss", choices=["plss", "reference"])
     ap.add_argument("--slabs", type=int, default=0)
     ap.add_argument("--no-sell", action="store_true", help="CSR tiles only (no SELL-32 copies)")
+    ap.add_argument("--no-window", action="store_true", help="SELL-32 without shared-memory windows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
@@ -236,9 +237,10 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         ctx = pkg.plss_create_dist(A, w["row_offset"], w["m_global"], obj[0], rank, world,
                                    slabs=args.slabs, maxit_cap=maxit_cap, stream=stream,
-                                   sell=not args.no_sell)
+                                   sell=not args.no_sell, window=not args.no_window)
     else:
-        ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=maxit_cap, stream=stream, sell=not args.no_sell)
+        ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=maxit_cap, stream=stream, sell=not args.no_sell,
+                              window=not args.no_window)
     q = pkg.plss_query(ctx)
     b = w["b"]
     torch.cuda.synchronize()
@@ -307,7 +309,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_label(w["name"]), "m": w["m_global"], "n": n,
                        "nnz": w["nnz_global"], "parallelism": f"row-block dp{world}" if world > 1 else "single",
-                       "slabs": q["slabs"], "sell_segments": q["sell_segments"], "freeze_mode": True,
+                       "slabs": q["slabs"], "sell_segments": q["sell_segments"],
+                       "window_segments": q["window_segments"], "freeze_mode": True,
                        "tol": 0.0,
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
                        "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8"},

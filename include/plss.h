@@ -82,7 +82,9 @@ typedef struct {
   int32_t graph_chunk; /* iterations per CUDA-graph launch (0 = auto)                        */
   int32_t maxit_cap;   /* largest maxit a solve on this ctx may request (sizes the history)  */
   int32_t flags;       /* bit0: disable the SELL-32 format (saves its ~2 x 1.15 nnz x 12 B of
-                          workspace); other bits must be 0                                 */
+                          workspace); bit1: disable the shared-memory windows of the gathered
+                          vector (SELL segments then gather every entry from global memory);
+                          other bits must be 0                                             */
 } plss_options;
 
 /* Bytes of DEVICE workspace a ctx needs (vectors r, y, p, x, reduction partials, control block,
@@ -150,11 +152,12 @@ plss_status plss_spmvT(plss_ctx *ctx, const double *u, double *v);
 plss_status plss_profile(plss_ctx *ctx, int32_t k, double *ms);
 
 /* Introspection (bench / ncu): kernel launches per loop step, number of row slabs, CSR-tile nnz
- * window, grid sizes of the first K1 / K2 launch, and how many of the 2*slabs SpMV segments use
- * the SELL-32 format (the rest use TMA-staged CSR tiles). Any pointer may be NULL. */
+ * window, grid sizes of the first K1 / K2 launch, how many of the 2*slabs SpMV segments use
+ * the SELL-32 format (the rest use TMA-staged CSR tiles) and how many of those gather through a
+ * shared-memory window of the gathered vector. Any pointer may be NULL. */
 plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t *slabs,
                        int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2,
-                       int32_t *sell_segments);
+                       int32_t *sell_segments, int32_t *window_segments);
 
 void plss_destroy(plss_ctx *ctx);
 const char *plss_status_str(plss_status s);

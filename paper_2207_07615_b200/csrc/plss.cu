@@ -41,7 +41,7 @@ int auto_slabs(int64_t m) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
 }
 
-int64_t ntiles_of(int64_t nnz_s) { return std::max<int64_t>(1, (nnz_s + TILE - 1) / TILE); }
+[[maybe_unused]] int64_t ntiles_of(int64_t nnz_s) { return std::max<int64_t>(1, (nnz_s + TILE - 1) / TILE); }
 
 struct Layout {
   int S = 1;
@@ -50,7 +50,8 @@ struct Layout {
   size_t r, y, p, x, rec, ctl, counters, part1, part2, part3, partn, tile1, tile2, scratch,
       scratch_blk, sptr, sidx, sval, scan_cnt, scan_blk, buf, err, scalars, total;
   bool sell = true;
-  size_t s1idx, s1val, s1perm, s1sptr, s2idx, s2val, s2perm, s2sptr;
+  size_t s1idx, s1val, s1perm, s1sptr, s2idx, s2val, s2perm, s2sptr, s1win, s2win, cblk, slpart;
+  bool window = true;
   int64_t s1cap, s2cap, s1slots, s2slots, s1sp, s2sp;  // pool capacities (entries / slots / sptr)
 };
 
@@ -100,6 +101,12 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
     L->s2val = take(8 * (size_t)L->s2cap);
     L->s2perm = take(4 * (size_t)L->s2slots);
     L->s2sptr = take(4 * (size_t)L->s2sp);
+    // window blocks (NSB slices each) of the windowed SELL segments; opt.flags bit1 disables
+    L->window = !(o.flags & 2);
+    L->s1win = take(8 * (size_t)(L->s1sp / 4 + 2 * S + 2));     // window blocks: nsb >= 4 slices
+    L->s2win = take(8 * (size_t)(L->s2sp / 4 + 2 * S + 2));
+    L->cblk = take(4 * (size_t)(MAXG + 1) * 2 * S);
+    L->slpart = take(16 * (size_t)(std::max(m, n) / 32 + 2));
   }
   L->scratch_blk = take(4 * (size_t)((std::max(m, n) + 2) / (NT * SCAN_ITEMS) + 2));
   if (S > 1) {
@@ -223,7 +230,11 @@ static void set_err(plss_ctx* ctx, const std::string& s) {
 
 template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
-  if (a.fmt == 1)
+  if (a.fmt == 2)
+    k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
+  else if (a.fmt == 3)
+    k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(a);
+  else if (a.fmt == 1)
     k_sell<ROLE><<<grid, NT, 0, st>>>(a);
   else
     k_spmv<ROLE><<<grid, NTS, Stage<ROLE>::SMEM, st>>>(a);
@@ -337,7 +348,83 @@ struct SellPool {
   double* val;
   int64_t cap, slots, sp;      // capacities
   int64_t used, used_slots, used_sp;
+  int2* win;                   // window descriptors (one per NSB-slice block)
+  int64_t wcap, used_w;
+  int32_t* cblk;               // CTA block ranges (MAXG+1 per segment)
+  int64_t used_c;
 };
+
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
+// Give a SELL segment a shared-memory window of its gathered vector g (length glen) when enough of
+// its entries fall into per-block windows of `win` doubles ("Windows").
+// One 1024-thread CTA per SM over contiguous entry-balanced slice ranges (fmt 3).
+static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sms, int* grid_out) {
+  if (a.fmt != 1) return PLSS_OK;
+  const int nblocks = (a.nslices + NSB - 1) / NSB;
+  const int grid = std::max(1, std::min(std::min(nblocks, sms), MAXG));
+  int32_t* cblk = pool.cblk + pool.used_c;
+  k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.sptr, a.nslices, NSB, nblocks, grid, cblk);
+  CK(cudaGetLastError());
+  pool.used_c += MAXG + 1;
+  a.cblk = cblk;
+  a.fmt = 3;
+  *grid_out = grid;
+  return PLSS_OK;
+}
+
+static plss_status try_window(plss_ctx* ctx, SpmvSeg& a, const double* g, int64_t glen, int64_t nnz_seg,
+                              int win, int nsb, SellPool& pool, int sms, int* grid_out) {
+  cudaStream_t st = ctx->stream;
+  if (a.fmt != 1 || win <= 0 || nnz_seg == 0) return PLSS_OK;
+  win &= ~7;
+  if (glen - 2 < win) win = (int)((glen - 2) & ~7ll);
+  if (win < 256) return PLSS_OK;
+  nsb = std::max(4, std::min(nsb, 64));
+  const int ring = win + win / 2 + 8;              // advance allowance: (WST-1) blocks in flight
+  if ((size_t)ring * 8 > 200 * 1024) return PLSS_OK;
+  const int nblocks = (a.nslices + nsb - 1) / nsb;
+  if (pool.used_w + nblocks > pool.wcap) return PLSS_OK;
+  int2* wlo = pool.win + pool.used_w;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sellw<ROLE_K2DOTS>, NTW, (size_t)ring * 8));
+  if (occ < 1) return PLSS_OK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nblocks, (int64_t)occ * sms), MAXG));
+  // bins: win/4 wide (at most 16384 of them), windows of kb bins
+  int64_t bw = std::max<int64_t>(win / 4, (glen + 16383) / 16384);
+  const int nbins = (int)((glen + bw - 1) / bw);
+  const int kb = (int)std::max<int64_t>(1, win / bw);
+  const int goff = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
+  unsigned long long* covered = (unsigned long long*)(ctx->ws + ctx->L.err + 16);
+  CK(cudaMemsetAsync(covered, 0, 8, st));
+  k_win_choose<<<nblocks, 256, (size_t)nbins * 4, st>>>(a.sptr, a.idx, a.nslices, nsb, (int)glen, win, (int)bw,
+                                                         nbins, kb, goff, std::max(64, win / 16), wlo, covered);
+  CK(cudaGetLastError());
+  unsigned long long cov = 0;
+  CK(cudaMemcpyAsync(&cov, covered, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((double)cov < 0.1 * (double)nnz_seg) return PLSS_OK;          // too little locality
+  int32_t* cblk = pool.cblk + pool.used_c;
+  k_cta_ranges<<<(grid + 256) / 256, 256, 0, st>>>(a.sptr, a.nslices, nsb, nblocks, grid, cblk);
+  k_win_chain<<<(grid + 255) / 256, 256, 0, st>>>(wlo, cblk, grid, win, ring);
+  CK(cudaGetLastError());
+  a.cblk = cblk;
+  a.slpart = (double*)(ctx->ws + ctx->L.slpart);
+  pool.used_c += MAXG + 1;
+  a.fmt = 2;
+  a.win = win;
+  a.ring = ring;
+  a.nblocks = nblocks;
+  a.glen = (int32_t)glen;
+  a.nsb = nsb;
+  a.wlo = wlo;
+  pool.used_w += nblocks;
+  *grid_out = grid;
+  return PLSS_OK;
+}
 
 // Convert one segment (CSR-like: ptr[nrows+1] absolute positions, idx, val) to SELL-32 if the
 // padding stays small: unsorted when rows are (nearly) uniform, else sigma-sorted windows of 256.
@@ -402,7 +489,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (!A->row_ptr || !A->col_ptr || (A->nnz > 0 && (!A->col_idx || !A->val || !A->row_idx || !A->val_t))) {
     set_err(ctx, "NULL matrix array"); return PLSS_E_INVALID;
   }
-  if (opt && (opt->flags & ~1) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & ~3) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
   {
     const void* arrs[6] = {A->row_ptr, A->col_idx, A->val, A->col_ptr, A->row_idx, A->val_t};
     for (const void* q : arrs)
@@ -495,10 +582,28 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   SellPool pool1{}, pool2{};
   if (L.sell) {
     pool1 = SellPool{(int32_t*)(w + L.s1idx), (int32_t*)(w + L.s1perm), (int32_t*)(w + L.s1sptr),
-                     (double*)(w + L.s1val), L.s1cap, L.s1slots, L.s1sp, 0, 0, 0};
+                     (double*)(w + L.s1val), L.s1cap, L.s1slots, L.s1sp, 0, 0, 0,
+                     (int2*)(w + L.s1win), L.s1sp / 4 + 2 * S + 2, 0, (int32_t*)(w + L.cblk), 0};
     pool2 = SellPool{(int32_t*)(w + L.s2idx), (int32_t*)(w + L.s2perm), (int32_t*)(w + L.s2sptr),
-                     (double*)(w + L.s2val), L.s2cap, L.s2slots, L.s2sp, 0, 0, 0};
+                     (double*)(w + L.s2val), L.s2cap, L.s2slots, L.s2sp, 0, 0, 0,
+                     (int2*)(w + L.s2win), L.s2sp / 4 + 2 * S + 2, 0,
+                     (int32_t*)(w + L.cblk) + (size_t)(MAXG + 1) * S, 0};
+    // windowed kernels: up to ~200 KB of dynamic shared memory for the ring
+    CK(cudaFuncSetAttribute(k_sellw<ROLE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_sellw<ROLE_K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_sellw<ROLE_K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_sellw<ROLE_K2DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_win_choose, cudaFuncAttributeMaxDynamicSharedMemorySize, 16385 * 4));
   }
+  // Shared-memory windows (fmt 2) are opt-in: correct and bit-exact, but on every config measured
+  // slower than L1-cached gathers ("Windows"). opt.flags bit1 disables them
+  // even when requested through PLSS_WIN1 / PLSS_WIN2 (window lengths in doubles).
+  const int win1 = L.window ? env_int("PLSS_WIN1", 0) : 0;       // window of p (K1)
+  const int win2 = L.window ? env_int("PLSS_WIN2", 0) : 0;       // window of r_s (K2)
+  // fmt 3 (one 1024-thread CTA per SM over contiguous slice ranges): K1 by default (C5: 2.5-2.7
+  // vs 2.9 ms), not K2 (4.9 vs 4.6 ms). PLSS_SELLC: 0 off, 1 K1, 2 K1 + K2.
+  const int contig = env_int("PLSS_SELLC", 1);
+  const int nsb1 = env_int("PLSS_NSB1", 16), nsb2 = env_int("PLSS_NSB2", 8);   // slices per window block
   auto sell_grid = [&](const SpmvSeg& a) {
     return grid_for(((int64_t)a.nslices + NT / 32 - 1) / (NT / 32), occ_sell, sms);
   };
@@ -542,6 +647,9 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     if (L.sell) {
       if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool1, sms, occ_sell) != PLSS_OK) return PLSS_E_CUDA;
       if (a.fmt == 1) ctx->g1[s] = sell_grid(a);
+      if (try_window(ctx, a, ctx->p, n, ctx->E[s + 1] - ctx->E[s], win1, nsb1, pool1, sms, &ctx->g1[s]) != PLSS_OK)
+        return PLSS_E_CUDA;
+      if (contig >= 1 && make_contig(ctx, a, pool1, sms, &ctx->g1[s]) != PLSS_OK) return PLSS_E_CUDA;
     }
   }
 
@@ -598,6 +706,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     if (L.sell) {
       if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool2, sms, occ_sell) != PLSS_OK) return PLSS_E_CUDA;
       if (a.fmt == 1) ctx->g2[s] = sell_grid(a);
+      if (try_window(ctx, a, a.g, ctx->R[s + 1] - ctx->R[s], ctx->E[s + 1] - ctx->E[s], win2, nsb2, pool2, sms,
+                     &ctx->g2[s]) != PLSS_OK)
+        return PLSS_E_CUDA;
+      if (contig >= 2 && make_contig(ctx, a, pool2, sms, &ctx->g2[s]) != PLSS_OK) return PLSS_E_CUDA;
     }
   }
   CK(cudaGetLastError());
@@ -877,13 +989,19 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
 }
 
 plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t* slabs, int32_t* tile_nnz,
-                       int32_t* grid_k1, int32_t* grid_k2, int32_t* sell_segments) {
+                       int32_t* grid_k1, int32_t* grid_k2, int32_t* sell_segments, int32_t* window_segments) {
   if (!ctx) return PLSS_E_INVALID;
   if (sell_segments) {
     int c = 0;
-    for (auto& a : ctx->seg1) c += a.fmt == 1;
-    for (auto& a : ctx->seg2) c += a.fmt == 1;
+    for (auto& a : ctx->seg1) c += a.fmt >= 1;
+    for (auto& a : ctx->seg2) c += a.fmt >= 1;
     *sell_segments = c;
+  }
+  if (window_segments) {
+    int c = 0;
+    for (auto& a : ctx->seg1) c += a.fmt == 2;
+    for (auto& a : ctx->seg2) c += a.fmt == 2;
+    *window_segments = c;
   }
   if (launches_per_step) *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0);
   if (slabs) *slabs = ctx->S;

@@ -19,6 +19,7 @@
 // oracle's sequential sums.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace plss {
@@ -112,10 +113,17 @@ struct SpmvSeg {
   double* rho_out;           // dist: where the local rho goes (all-reduce buffer [n])
   // SELL-32 format (fmt = 1): slice s holds rows perm[32s .. 32s+31] column-major, entry j of
   // its lane l at (sptr[s] + j) * 32 + l; padding entries have index -1
-  int32_t fmt;               // 0: CSR tiles through TMA (k_spmv), 1: SELL-32 (k_sell)
+  int32_t fmt;               // 0: CSR tiles through TMA (k_spmv), 1: SELL-32 (k_sell),
+                             // 2: SELL-32 + shared-memory window of g (k_sellw)
   int32_t nslices;
   const int32_t* sptr;       // nslices+1 slice starts in 32-entry steps
   const int32_t* perm;       // slot -> segment-local row (sigma-sorted), -1 for padding; or NULL
+  // window (fmt = 2): blocks of NSB consecutive slices; block b gathers g[lo_b, lo_b + win) from a
+  // ring of `ring` doubles in shared memory, every other entry from global memory
+  int32_t win, ring, nblocks, glen, nsb;
+  const int2* wlo;           // per block {lo_b, flags}: 1 = reload the whole window, 2 = no window
+  const int32_t* cblk;       // grid+1 block bounds of the CTAs (balanced by stored entries)
+  double* slpart;            // per-slice dot partials (fixed-order reduction, deterministic)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -129,10 +137,23 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+__device__ __forceinline__ void st_stream(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
 }
 // Streaming (read-once) loads of the matrix arrays: no L1 allocation, L2 evict-first, so the
 // gathered vector keeps its L2 residency.
@@ -156,7 +177,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Fixed-shape block reduction of two values; result valid in thread 0.
-constexpr int MAXW = 16;  // max warps per CTA of any kernel here
+constexpr int MAXW = 32;  // max warps per CTA of any kernel here
 
 __device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[MAXW]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -272,16 +293,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Watchdog for every spin wait: a pipeline bug traps (the launch fails with an error) instead
+// of hanging the device. 2^35 cycles is ~17 s at 2 GHz, far beyond any legitimate wait.
+__device__ __forceinline__ void spin_guard(long long t0) {
+  if (clock64() - t0 > (1ll << 35)) __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   uint32_t ok;
-  do {
+  long long t0 = 0;
+  for (int it = 0;; ++it) {
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
                  " selp.u32 %0, 1, 0, p;\n}"
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-  } while (!ok);
+    if (ok) break;
+    if (it == 0) t0 = clock64(); else spin_guard(t0);
+  }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// bulk prefetch of [p, p + bytes) into L2 (TMA unit; no registers, no completion tracking)
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 // 1-D bulk copy global -> shared, completion counted on the mbarrier, L2 evict-first hint
 __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar,
@@ -1187,23 +1220,71 @@ __global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
 #define PLSS_SELL_MINB 4
 #endif
 constexpr int SU = PLSS_SU;             // steps (entries per lane) in flight
+constexpr int NSB = 16;                 // slices per window / CTA-range block
+#ifndef PLSS_HINTS
+#define PLSS_HINTS 0                    // L2 policies: old r / y evict-first, new r evict-last
+#endif
+#ifndef PLSS_PF
+#define PLSS_PF 0                       // L2 bulk prefetch of the streams: slices (blocks) ahead
+#endif
 constexpr int SELL_MINB = PLSS_SELL_MINB;
 
-template <int ROLE>
-__global__ void __launch_bounds__(NT, SELL_MINB) k_sell(SpmvSeg a) {
+// BS = 256: persistent grid, slices dealt round-robin over all warps of the grid.
+// BS = 1024 (one CTA per SM, fmt 3): CTA c walks the contiguous, entry-balanced slice range
+// [cblk[c], cblk[c+1]) * NSB with its 32 warps interleaved, so the band of g that consecutive
+// slices share stays in that SM's L1 (C5's K2: ~130 KB of r per 32 columns).
+template <int ROLE, int BS = NT>
+__global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   __shared__ double sm[2][MAXW];
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = policy_evict_first();
+#if PLSS_HINTS
+  const uint64_t pol_keep = PLSS_HINTS == 1 ? policy_evict_last() : policy_evict_normal();
+#endif
   double acc0 = 0.0, acc1 = 0.0;
-  const int wtotal = gridDim.x * (NT / 32);
-  for (int sl = blockIdx.x * (NT / 32) + warp; sl < a.nslices; sl += wtotal) {
-    const int st0 = a.sptr[sl], L = a.sptr[sl + 1] - st0;
-    const int slot = sl * 32 + lane;
-    const int row = a.perm ? a.perm[slot] : slot;
+  int sl_begin, sl_end, wtotal;
+  if (BS == NT) {
+    sl_begin = blockIdx.x * (NT / 32) + warp; sl_end = a.nslices; wtotal = gridDim.x * (NT / 32);
+  } else {
+    sl_begin = a.cblk[blockIdx.x] * NSB + warp;
+    sl_end = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices);
+    wtotal = BS / 32;
+  }
+  // slice metadata (start, end, row of this lane) is loaded one slice ahead: the stream loads of
+  // a slice then wait for DRAM only, not for an L2 round trip to sptr / perm first
+  int m0 = 0, m1 = 0, mrow = -1;
+  if (sl_begin < sl_end) {
+    m0 = a.sptr[sl_begin]; m1 = a.sptr[sl_begin + 1];
+    mrow = a.perm ? a.perm[sl_begin * 32 + lane] : sl_begin * 32 + lane;
+  }
+  for (int sl = sl_begin; sl < sl_end; sl += wtotal) {
+    const int st0 = m0, L = m1 - m0, row_cur = mrow;
+    if (sl + wtotal < sl_end) {
+      const int nx = sl + wtotal;
+      m0 = a.sptr[nx]; m1 = a.sptr[nx + 1];
+      mrow = a.perm ? a.perm[nx * 32 + lane] : nx * 32 + lane;
+    }
+#if PLSS_PF
+    if (lane < PLSS_PF && sl + (lane + 1) * wtotal < a.nslices) {   // streams of this warp's next slices -> L2
+      const int nx = sl + (lane + 1) * wtotal;
+      const long long e0 = (long long)a.sptr[nx] * 32, e1 = (long long)a.sptr[nx + 1] * 32;
+      if (e1 > e0) {
+        prefetch_l2(a.idx + e0, (unsigned)(e1 - e0) * 4u);
+        prefetch_l2(a.val + e0, (unsigned)(e1 - e0) * 8u);
+      }
+    }
+#endif
+    const int row = row_cur;
     const bool valid = row >= 0 && row < a.nrows;
     double s = 0.0;
+#if PLSS_HINTS
+    if (ROLE >= ROLE_K2 && valid && a.accumulate) s = ld_hint(a.out + row, pol);  // y: read once per slab
+    const double r_old = (ROLE == ROLE_K1 && valid) ? ld_hint(a.out + row, pol) : 0.0;
+#else
     if (ROLE >= ROLE_K2 && valid && a.accumulate) s = a.out[row];
+    const double r_old = (ROLE == ROLE_K1 && valid) ? a.out[row] : 0.0;   // issued early
+#endif
     const int32_t* ip = a.idx + (long long)st0 * 32 + lane;
     const double* vp = a.val + (long long)st0 * 32 + lane;
     int j = 0;
@@ -1213,7 +1294,13 @@ __global__ void __launch_bounds__(NT, SELL_MINB) k_sell(SpmvSeg a) {
 #pragma unroll
       for (int u = 0; u < SU; ++u) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
 #pragma unroll
-      for (int u = 0; u < SU; ++u) gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
+      for (int u = 0; u < SU; ++u) {
+#if PLSS_ABLATE & 4
+        gv[u] = (double)c[u];                                   // ablation: no gathers
+#else
+        gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
+#endif
+      }
 #pragma unroll
       for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
     }
@@ -1226,7 +1313,13 @@ __global__ void __launch_bounds__(NT, SELL_MINB) k_sell(SpmvSeg a) {
         if (j + u < L) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
       }
 #pragma unroll
-      for (int u = 0; u < SU; ++u) gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
+      for (int u = 0; u < SU; ++u) {
+#if PLSS_ABLATE & 4
+        gv[u] = (double)c[u];                                   // ablation: no gathers
+#else
+        gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
+#endif
+      }
 #pragma unroll
       for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
     }
@@ -1234,12 +1327,21 @@ __global__ void __launch_bounds__(NT, SELL_MINB) k_sell(SpmvSeg a) {
       if (ROLE == ROLE_PLAIN) {
         a.out[row] = s;
       } else if (ROLE == ROLE_K1) {
-        const double rn = __dsub_rn(a.out[row], s);             // r_i <- r_i - (A p)_i
+        const double rn = __dsub_rn(r_old, s);                  // r_i <- r_i - (A p)_i
+#if PLSS_HINTS
+        st_stream(a.out + row, rn, pol_keep);                   // gathered by K2 of this slab next
+#else
         a.out[row] = rn;
+#endif
         acc0 = fma(rn, rn, acc0);
       } else {
+#if PLSS_HINTS
+        st_stream(a.out + row, s, pol);                         // y_j (re-read by the next slab / K3)
+        if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, ld_hint(a.pv + row, pol), acc1); }
+#else
         a.out[row] = s;                                         // y_j
         if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, a.pv[row], acc1); }
+#endif
       }
     }
   }
@@ -1256,6 +1358,350 @@ __global__ void __launch_bounds__(NT, SELL_MINB) k_sell(SpmvSeg a) {
     else tail_rho(a.ctl, a.rec, acc0);
   } else if (ROLE == ROLE_K2DOTS) {
     tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 / plain SpMV over SELL-32 with a sliding shared-memory WINDOW of the gathered vector.
+// Banded matrices (C3's stencil, C5's band half) gather most entries of a run of rows from a
+// narrow range of g. Each CTA walks a contiguous, entry-balanced range of blocks (nsb slices
+// each); block b's window g[lo_b, lo_b + win) lives in a ring of `ring` doubles
+// (slot = (row + goff) mod ring, goff = 16-byte phase of g), loaded by TMA bulk copies: only the
+// rows new to block b, up to WST-1 blocks ahead, one copy landing before the next is issued (a
+// block also reads rows earlier copies brought in). Setup keeps lo_b nondecreasing with
+// lo_b - lo_{b-WST+1} <= ring - win - 2 so a load never overwrites rows a block still in flight
+// may read; otherwise the block is a `reset` (whole window reloaded once all earlier blocks are
+// done). Entries inside the window read the ring, the rest gather from global memory. The sum
+// order is unchanged (ascending, __dadd_rn/__dmul_rn): bitwise the k_sell result.
+// Warp specialization: NWC consumer warps take slices in order from a shared counter (slices of a
+// sigma window are longest-first: LPT scheduling), grabbing the next slice and prefetching its
+// metadata while the current one runs; one producer warp issues the window loads; full/empty
+// mbarriers per stage. Dot partials are reduced per slice and summed in slice order
+// (deterministic although slices are taken in a run-dependent order).
+// ---------------------------------------------------------------------------------------------
+#ifndef PLSS_NWC
+#define PLSS_NWC 31
+#endif
+constexpr int NWC = PLSS_NWC;             // consumer warps per windowed CTA
+constexpr int NTW = (NWC + 1) * 32;       // + 1 producer warp
+#ifndef PLSS_SUW
+#define PLSS_SUW 6
+#endif
+constexpr int SUW = PLSS_SUW;             // steps in flight per lane (windowed kernel)
+#ifndef PLSS_WST
+#define PLSS_WST 4
+#endif
+#ifndef PLSS_WCHECK
+#define PLSS_WCHECK 0                     // debug: compare every ring read with global memory
+#endif
+constexpr int WST = PLSS_WST;             // window pipeline stages (blocks in flight)
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, unsigned cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
+
+template <int ROLE>
+__global__ void __launch_bounds__(NTW, 1) k_sellw(SpmvSeg a) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ uint64_t full[WST], empty[WST];
+  __shared__ int s_next;
+  __shared__ volatile int s_issued;                // last block (relative) whose load was issued
+  __shared__ double sm[2][MAXW];
+  if (a.ctl != nullptr && a.ctl->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nsb = a.nsb;
+  const int b0 = a.cblk[blockIdx.x], b1 = a.cblk[blockIdx.x + 1];
+  const int sl0 = b0 * nsb, sl1 = min(b1 * nsb, a.nslices);
+  const int W = a.win, R = a.ring;
+  const int goff = (int)((reinterpret_cast<uintptr_t>(a.g) >> 3) & 1);
+  // window start of block b with the 16-byte phase of this g (setup used the phase of its g)
+  auto lo_of = [&](int lo) {
+    if ((lo + goff) & 1) lo += lo > 0 ? -1 : 1;
+    return lo;
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < WST; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], (unsigned)nsb); }
+    s_next = sl0 + NWC;                              // slices sl0 .. sl0+NWC-1 are taken statically
+    s_issued = -1;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  double acc0 = 0.0, acc1 = 0.0;
+
+  if (warp == NWC) {
+    // ---- producer: window loads -------------------------------------------------------------
+    if (lane == 0) {
+      const uint64_t pol_g = policy_evict_last();
+      int cur = -1;                                  // lo of the window in the ring (-1: none)
+      int waited = -1;                               // blocks <= waited (relative) are done
+      auto wait_done = [&](int jj) {                 // wait until relative blocks <= jj are done
+        for (int k = waited + 1; k <= jj; ++k) mbar_wait(&empty[k % WST], (unsigned)(k / WST) & 1u);
+        if (jj > waited) waited = jj;
+      };
+      for (int b = b0; b < b1; ++b) {
+        const int j = b - b0, q = j % WST;
+        const int2 wb = a.wlo[b];
+        wait_done(j - WST);                          // stage q is free
+        const bool nowin = wb.y & 2;
+        const bool reset = !nowin && (cur < 0 || (wb.y & 1));
+        if (reset) wait_done(j - 1);                 // nothing in flight reads the ring
+        const int lo = lo_of(wb.x);
+        const int from = nowin ? 0 : reset ? lo : max(lo, cur + W), to = nowin ? 0 : lo + W;
+        if (!nowin) cur = lo;
+        unsigned bytes = 0;
+        fence_proxy_async();
+        if (to > from) {
+          const int s = (from + goff) % R;
+          const int n1 = min(to - from, R - s);
+          tma_load(ring + s, a.g + from, (unsigned)n1 * 8u, &full[q], pol_g);
+          bytes = (unsigned)n1 * 8u;
+          if (to - from > n1) {
+            tma_load(ring, a.g + from + n1, (unsigned)(to - from - n1) * 8u, &full[q], pol_g);
+            bytes += (unsigned)(to - from - n1) * 8u;
+          }
+        }
+        mbar_expect_tx(&full[q], bytes);
+#if PLSS_WCHECK
+        if (blockIdx.x < 4) printf("WLOAD cta %d b %d j %d lo %d flags %d reset %d from %d to %d cur %d\n", blockIdx.x, b, j, lo, wb.y, (int)reset, from, to, cur);
+#endif
+        const int cnt = min((b + 1) * nsb, a.nslices) - b * nsb;     // partial last block
+        if (cnt < nsb) mbar_arrive_cnt(&empty[q], (unsigned)(nsb - cnt));
+        // Loads land in order: block j reads ring rows that earlier blocks' copies brought in, so
+        // "block j's bytes arrived" must imply every earlier copy arrived too.
+        mbar_wait(&full[q], (unsigned)(j / WST) & 1u);
+        s_issued = j;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- consumers: one slice at a time, in order; the next one's metadata in flight ----------
+    const uint64_t pol = policy_evict_first();
+    int sl = sl0 + warp;                             // first slice: static
+    int m0 = 0, m1 = 0, mrow = -1;
+    int2 mw = make_int2(0, 0);
+    auto meta = [&](int t) {
+      m0 = a.sptr[t]; m1 = a.sptr[t + 1];
+      mrow = a.perm ? a.perm[t * 32 + lane] : t * 32 + lane;
+      mw = a.wlo[t / nsb];
+    };
+    if (sl < sl1) meta(sl);
+    while (sl < sl1) {
+      const int st0 = m0, L = m1 - m0, row = mrow;
+      const int2 wb = mw;
+      int nx = 0;
+      if (lane == 0) nx = atomicAdd(&s_next, 1);
+      nx = __shfl_sync(FULL, nx, 0);
+      if (nx < sl1) meta(nx);
+      const int b = sl / nsb, j = b - b0, q = j % WST;
+      const int lo = lo_of(wb.x);
+      const int Wb = (wb.y & 2) ? 0 : W;             // no window for this block
+      const int slo = (lo + goff) % R;
+      const bool valid = row >= 0 && row < a.nrows;
+      double s = 0.0;
+      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = a.out[row];
+      const double r_old = (ROLE == ROLE_K1 && valid) ? a.out[row] : 0.0;   // issued early
+      const int32_t* ip = a.idx + (long long)st0 * 32 + lane;
+      const double* vp = a.val + (long long)st0 * 32 + lane;
+      // Parity waits alias across two phases: wait on block j's phase only once j was issued
+      // (issuing j required block j-WST done, so stage q's barrier is exactly at j's phase).
+      if (s_issued < j) {
+        const long long t0 = clock64();
+        while (s_issued < j) { __nanosleep(64); spin_guard(t0); }
+      }
+      mbar_wait(&full[q], (unsigned)(j / WST) & 1u);
+      auto gather = [&](int c) -> double {
+        const unsigned d = (unsigned)(c - lo);
+        if (d < (unsigned)Wb) {
+          int k = slo + (int)d;
+          if (k >= R) k -= R;
+#if PLSS_WCHECK
+          const double rv = ring[k], gvv = __ldg(a.g + c);
+          if (__double_as_longlong(rv) != __double_as_longlong(gvv))
+            printf("WCHECK blk %d cta %d b %d j %d sl %d c %d lo %d W %d R %d slo %d k %d flags %d issued %d\n",
+                   blockIdx.x, blockIdx.x, b, j, sl, c, lo, W, R, slo, k, wb.y, (int)s_issued);
+          return rv;
+#else
+          return ring[k];
+#endif
+        }
+        return c >= 0 ? __ldg(a.g + c) : 0.0;
+      };
+      int jj = 0;
+      for (; jj + SUW <= L; jj += SUW) {
+        int32_t c[SUW];
+        double v[SUW], gv[SUW];
+#pragma unroll
+        for (int u = 0; u < SUW; ++u) { c[u] = ld_stream(ip + (jj + u) * 32, pol); v[u] = ld_stream(vp + (jj + u) * 32, pol); }
+#pragma unroll
+        for (int u = 0; u < SUW; ++u) gv[u] = gather(c[u]);
+#pragma unroll
+        for (int u = 0; u < SUW; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
+      }
+      if (jj < L) {
+        int32_t c[SUW];
+        double v[SUW], gv[SUW];
+#pragma unroll
+        for (int u = 0; u < SUW; ++u) {
+          c[u] = -1;
+          if (jj + u < L) { c[u] = ld_stream(ip + (jj + u) * 32, pol); v[u] = ld_stream(vp + (jj + u) * 32, pol); }
+        }
+#pragma unroll
+        for (int u = 0; u < SUW; ++u) gv[u] = gather(c[u]);
+#pragma unroll
+        for (int u = 0; u < SUW; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[q]);                    // this slice no longer reads the ring
+      double d0 = 0.0, d1 = 0.0;
+      if (valid) {
+        if (ROLE == ROLE_PLAIN) {
+          a.out[row] = s;
+        } else if (ROLE == ROLE_K1) {
+          const double rn = __dsub_rn(r_old, s);                // r_i <- r_i - (A p)_i
+          a.out[row] = rn;
+          d0 = rn * rn;
+        } else {
+          a.out[row] = s;                                       // y_j
+          if (ROLE == ROLE_K2DOTS) { d0 = s * s; d1 = s * a.pv[row]; }
+        }
+      }
+      if (ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS) {
+        d0 = warp_sum(d0);
+        d1 = warp_sum(d1);
+        if (lane == 0) { a.slpart[2 * sl] = d0; a.slpart[2 * sl + 1] = d1; }
+      }
+      sl = nx;
+    }
+  }
+  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;
+  __syncthreads();
+  for (int q = sl0 + tid; q < sl1; q += NTW) { acc0 += a.slpart[2 * q]; acc1 += a.slpart[2 * q + 1]; }
+  if (!a.finalize) {
+    block_sum2(acc0, acc1, sm);
+    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
+    return;
+  }
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = acc0;
+    else tail_rho(a.ctl, a.rec, acc0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
+// ---- window choice (setup, once per segment) ------------------------------------------------
+// Block b: histogram of its gathered indices in bins of bw; the window starts where `kb`
+// consecutive bins hold the most entries (ties: lowest); then clamped to [0, glen - win - 2] and
+// given the 16-byte phase of g. A block whose window would hold fewer than `thr` entries gets no
+// window (flag 2: loading it would cost more than it saves); the others add their exact
+// in-window count to *covered.
+__global__ void __launch_bounds__(256) k_win_choose(const int32_t* sptr, const int32_t* sidx, int nslices,
+                                                    int nsb, int glen, int win, int bw, int nbins, int kb, int goff,
+                                                    int thr, int2* wlo, unsigned long long* covered) {
+  extern __shared__ int32_t hist[];
+  __shared__ int s_cnt[8], s_pos[8];
+  __shared__ unsigned s_sum[8];
+  const int b = blockIdx.x, t = threadIdx.x;
+  const long long e0 = (long long)sptr[b * nsb] * 32, e1 = (long long)sptr[min((b + 1) * nsb, nslices)] * 32;
+  for (int i = t; i < nbins; i += 256) hist[i] = 0;
+  __syncthreads();
+  for (long long e = e0 + t; e < e1; e += 256) {
+    const int c = sidx[e];
+    if (c >= 0) atomicAdd(&hist[c / bw], 1);
+  }
+  __syncthreads();
+  int best = -1, bpos = 0;
+  const int ncand = max(1, nbins - kb + 1);
+  for (int i = t; i < ncand; i += 256) {
+    int sum = 0;
+    for (int q = 0; q < kb && i + q < nbins; ++q) sum += hist[i + q];
+    if (sum > best) { best = sum; bpos = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ob = __shfl_xor_sync(FULL, best, o), op = __shfl_xor_sync(FULL, bpos, o);
+    if (ob > best || (ob == best && op < bpos)) { best = ob; bpos = op; }
+  }
+  if ((t & 31) == 0) { s_cnt[t >> 5] = best; s_pos[t >> 5] = bpos; }
+  __syncthreads();
+  __shared__ int s_lo;
+  if (t == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (s_cnt[w] > best || (s_cnt[w] == best && s_pos[w] < bpos)) { best = s_cnt[w]; bpos = s_pos[w]; }
+    long long lo = (long long)bpos * bw - (long long)(win - kb * bw) / 2;
+    lo = max(0ll, min(lo, (long long)glen - win - 2));
+    if ((lo + goff) & 1) lo += lo > 0 ? -1 : 1;
+    s_lo = (int)lo;
+  }
+  __syncthreads();
+  const int lo = s_lo;
+  unsigned cnt = 0;
+  for (long long e = e0 + t; e < e1; e += 256) cnt += (unsigned)(sidx[e] - lo) < (unsigned)win;
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+  if ((t & 31) == 0) s_sum[t >> 5] = cnt;
+  __syncthreads();
+  if (t == 0) {
+    unsigned tot = 0;
+    for (int w = 0; w < 8; ++w) tot += s_sum[w];
+    const bool use = (int)tot >= thr;
+    wlo[b] = make_int2(lo, use ? 0 : 2);
+    if (use) atomicAdd(covered, (unsigned long long)tot);
+  }
+}
+
+// Per CTA range (the grid is fixed at setup): keep the windows of the windowed blocks
+// nondecreasing with lo_b - lo_k <= ring - win - 2 for every windowed block k among the WST-1
+// blocks before b (those may still be in flight while b's rows are loaded). Small violations are
+// clamped, large ones become `reset` blocks (flag 1). Blocks without a window (flag 2) are
+// transparent.
+__global__ void k_win_chain(int2* wlo, const int32_t* cblk, int grid, int win, int ring) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= grid) return;
+  const int b0 = cblk[c], b1 = cblk[c + 1];
+  const int adv = ring - win - 2, slack = win / 8;
+  int prev = -1;                                 // lo of the last windowed block
+  int hist[WST];                                 // lo of the last WST-1 blocks (-1: no window)
+  for (int k = 0; k < WST; ++k) hist[k] = -1;
+  for (int b = b0; b < b1; ++b) {
+    int2 w = wlo[b];
+    const int slot = (b - b0) % WST;
+    if (w.y & 2) { hist[slot] = -1; continue; }
+    int oldest = -1;                             // smallest lo among the in-flight window blocks
+    for (int k = 1; k < WST; ++k) {
+      const int h = hist[((b - b0) - k + WST * 4) % WST];
+      if ((b - b0) - k >= 0 && h >= 0 && (oldest < 0 || h < oldest)) oldest = h;
+    }
+    int lo = w.x, reset = 0;
+    if (prev < 0) {
+      reset = 1;
+    } else if (lo < prev) {
+      if (prev - lo <= slack) lo = prev; else reset = 1;
+    }
+    if (!reset && oldest >= 0 && lo - oldest > adv) {
+      if (lo - oldest - adv <= slack) lo = oldest + adv; else reset = 1;
+      if (!reset && lo < prev) lo = prev;        // cannot happen with monotone windows; keep safe
+      if (!reset && lo - oldest > adv) reset = 1;
+    }
+    wlo[b] = make_int2(lo, reset);
+    hist[slot] = lo;
+    prev = lo;
+  }
+}
+
+// CTA c of a windowed launch owns blocks [cblk[c], cblk[c+1]): the first block whose stored
+// entries start at or after c/grid of the segment's total (work balance when row lengths vary,
+// e.g. C5's K2 slabs where a band of columns holds 9x the entries of the rest).
+__global__ void k_cta_ranges(const int32_t* sptr, int nslices, int nsb, int nblocks, int grid, int32_t* cblk) {
+  const long long total = sptr[nslices];
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= grid; c += gridDim.x * blockDim.x) {
+    const long long target = (total * c + grid - 1) / grid;
+    int lo = 0, hi = nblocks;                                   // first b with start(b) >= target
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((long long)sptr[min(mid * nsb, nslices)] < target) lo = mid + 1; else hi = mid;
+    }
+    cblk[c] = c == 0 ? 0 : c == grid ? nblocks : lo;
   }
 }
 

@@ -87,7 +87,7 @@ def load_library(path: str = None):
     lib.plss_spmvT.restype = st
     lib.plss_profile.argtypes = [P, I32, P]
     lib.plss_profile.restype = st
-    lib.plss_query.argtypes = [P] + [ctypes.POINTER(I32)] * 6
+    lib.plss_query.argtypes = [P] + [ctypes.POINTER(I32)] * 7
     lib.plss_query.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
@@ -155,14 +155,14 @@ class Matrix:
                            1 if validate else 0)
 
 
-def _opts(slabs=0, graph_chunk=0, maxit_cap=0, sell=True):
-    return plss_options(int(slabs), int(graph_chunk), int(maxit_cap), 0 if sell else 1)
+def _opts(slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True):
+    return plss_options(int(slabs), int(graph_chunk), int(maxit_cap), (0 if sell else 1) | (0 if window else 2))
 
 
-def plss_workspace_bytes(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=0, sell=True) -> int:
+def plss_workspace_bytes(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True) -> int:
     lib = load_library()
     ms = A.c_struct()
-    o = _opts(slabs, graph_chunk, maxit_cap, sell)
+    o = _opts(slabs, graph_chunk, maxit_cap, sell, window)
     nbytes = lib.plss_workspace_bytes(ctypes.byref(ms), ctypes.byref(o))
     if nbytes == 0:
         raise PlssError("invalid matrix sizes")
@@ -206,13 +206,13 @@ def _aligned(ws) -> int:
 
 
 def plss_create(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False,
-                sell=True) -> Ctx:
+                sell=True, window=True) -> Ctx:
     lib = load_library()
-    nbytes = plss_workspace_bytes(A, slabs, graph_chunk, maxit_cap, sell)
+    nbytes = plss_workspace_bytes(A, slabs, graph_chunk, maxit_cap, sell, window)
     ws = _alloc_workspace(nbytes, A.row_ptr.device)
     h = ctypes.c_void_p()
     ms = A.c_struct(validate)
-    o = _opts(slabs, graph_chunk, maxit_cap, sell)
+    o = _opts(slabs, graph_chunk, maxit_cap, sell, window)
     _check(lib.plss_create(ctypes.byref(ms), ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream),
                            ctypes.byref(h)))
     return Ctx(h, A, ws, stream, maxit_cap)
@@ -226,13 +226,14 @@ def plss_get_unique_id() -> bytes:
 
 
 def plss_create_dist(A_local: Matrix, row_offset: int, m_global: int, uid: bytes, rank: int, nranks: int,
-                     slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False, sell=True) -> Ctx:
+                     slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False, sell=True,
+                     window=True) -> Ctx:
     lib = load_library()
-    nbytes = plss_workspace_bytes(A_local, slabs, graph_chunk, maxit_cap, sell)
+    nbytes = plss_workspace_bytes(A_local, slabs, graph_chunk, maxit_cap, sell, window)
     ws = _alloc_workspace(nbytes, A_local.row_ptr.device)
     h = ctypes.c_void_p()
     ms = A_local.c_struct(validate)
-    o = _opts(slabs, graph_chunk, maxit_cap, sell)
+    o = _opts(slabs, graph_chunk, maxit_cap, sell, window)
     _check(lib.plss_create_dist(ctypes.byref(ms), int(row_offset), int(m_global), uid, int(rank), int(nranks),
                                 ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream), ctypes.byref(h)))
     return Ctx(h, A_local, ws, stream, maxit_cap)
@@ -312,9 +313,9 @@ def plss_profile(ctx: Ctx, k: int) -> dict:
 
 
 def plss_query(ctx: Ctx) -> dict:
-    vals = [ctypes.c_int32(0) for _ in range(6)]
+    vals = [ctypes.c_int32(0) for _ in range(7)]
     _check(load_library().plss_query(ctx.handle, *[ctypes.byref(v) for v in vals]), ctx.handle)
-    keys = ["launches_per_step", "slabs", "tile_nnz", "grid_k1", "grid_k2", "sell_segments"]
+    keys = ["launches_per_step", "slabs", "tile_nnz", "grid_k1", "grid_k2", "sell_segments", "window_segments"]
     return {k: v.value for k, v in zip(keys, vals)}
 
 
