@@ -371,6 +371,7 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   CK(cudaGetLastError());
   pool.used_c += MAXG + 1;
   a.cblk = cblk;
+  a.slpart = (double*)(ctx->ws + ctx->L.slpart);
   a.fmt = 3;
   *grid_out = grid;
   return PLSS_OK;
@@ -600,9 +601,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   // even when requested through PLSS_WIN1 / PLSS_WIN2 (window lengths in doubles).
   const int win1 = L.window ? env_int("PLSS_WIN1", 0) : 0;       // window of p (K1)
   const int win2 = L.window ? env_int("PLSS_WIN2", 0) : 0;       // window of r_s (K2)
-  // fmt 3 (one 1024-thread CTA per SM over contiguous slice ranges): K1 by default (C5: 2.5-2.7
-  // vs 2.9 ms), not K2 (4.9 vs 4.6 ms). PLSS_SELLC: 0 off, 1 K1, 2 K1 + K2.
-  const int contig = env_int("PLSS_SELLC", 1);
+  // fmt 3 (one 1024-thread CTA per SM over a contiguous entry-balanced slice range, warps taking
+  // slices in order): default for K1 and K2 (C5: K1 2.6-2.7 vs 2.9-3.0 ms, K2 4.06 vs 4.66 ms with
+  // fmt 1). PLSS_SELLC: 0 off, 1 K1 only, 2 K1 + K2.
+  const int contig = env_int("PLSS_SELLC", 2);
   const int nsb1 = env_int("PLSS_NSB1", 16), nsb2 = env_int("PLSS_NSB2", 8);   // slices per window block
   auto sell_grid = [&](const SpmvSeg& a) {
     return grid_for(((int64_t)a.nslices + NT / 32 - 1) / (NT / 32), occ_sell, sms);
@@ -628,6 +630,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.desc = desc1 + t1off;
     a.e0 = ctx->E[s];
     a.nrows = (int32_t)rows;
+    a.row0 = (int32_t)ctx->R[s];
     int64_t nt = 0;
     if (build_tiles(ctx, a.ptr, rows, a.e0, (int2*)a.desc, tiles1_cap - t1off, &nt) != PLSS_OK) return PLSS_E_CUDA;
     a.ntiles = (int32_t)nt;
@@ -688,6 +691,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     }
     a.desc = desc2 + t2off;
     a.nrows = (int32_t)n;
+    a.row0 = (int32_t)ctx->R[s];
     int64_t nt = 0;
     if (build_tiles(ctx, a.ptr, n, a.e0, (int2*)a.desc, tiles2_cap - t2off, &nt) != PLSS_OK) return PLSS_E_CUDA;
     a.ntiles = (int32_t)nt;

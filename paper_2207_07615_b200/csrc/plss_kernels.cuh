@@ -121,6 +121,7 @@ struct SpmvSeg {
   // window (fmt = 2): blocks of NSB consecutive slices; block b gathers g[lo_b, lo_b + win) from a
   // ring of `ring` doubles in shared memory, every other entry from global memory
   int32_t win, ring, nblocks, glen, nsb;
+  int32_t row0;              // first row of this segment in the matrix (ablation experiments only)
   const int2* wlo;           // per block {lo_b, flags}: 1 = reload the whole window, 2 = no window
   const int32_t* cblk;       // grid+1 block bounds of the CTAs (balanced by stored entries)
   double* slpart;            // per-slice dot partials (fixed-order reduction, deterministic)
@@ -1221,131 +1222,145 @@ __global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
 #endif
 constexpr int SU = PLSS_SU;             // steps (entries per lane) in flight
 constexpr int NSB = 16;                 // slices per window / CTA-range block
-#ifndef PLSS_HINTS
-#define PLSS_HINTS 0                    // L2 policies: old r / y evict-first, new r evict-last
-#endif
-#ifndef PLSS_PF
-#define PLSS_PF 0                       // L2 bulk prefetch of the streams: slices (blocks) ahead
-#endif
 constexpr int SELL_MINB = PLSS_SELL_MINB;
 
-// BS = 256: persistent grid, slices dealt round-robin over all warps of the grid.
-// BS = 1024 (one CTA per SM, fmt 3): CTA c walks the contiguous, entry-balanced slice range
-// [cblk[c], cblk[c+1]) * NSB with its 32 warps interleaved, so the band of g that consecutive
-// slices share stays in that SM's L1 (C5's K2: ~130 KB of r per 32 columns).
+// Gather of g[c] (c = -1: padding). Ablation builds (timing experiments only, never correct):
+// 4 = no gathers (the index as value), 8 = C5's band gathers free, 16 = gathers from an 8 MB hot set.
+__device__ __forceinline__ double sell_gather(const SpmvSeg& a, int c, int row, int role) {
+#if PLSS_ABLATE & 4
+  return (double)c;
+#elif PLSS_ABLATE & 8
+  const bool rowwise = role == ROLE_K1 || role == ROLE_PLAIN;
+  const long long gi = (long long)row + (rowwise ? a.row0 : 0), gc = (long long)c + (rowwise ? 0 : a.row0);
+  const bool band = rowwise ? (llabs(gc - gi / 8) <= 1100) : (llabs(gc / 8 - gi) <= 1100);
+  return c < 0 ? 0.0 : band ? 1.0 : __ldg(a.g + c);
+#elif PLSS_ABLATE & 16
+  return c >= 0 ? __ldg(a.g + (c & 0xFFFFF)) : 0.0;
+#else
+  (void)row; (void)role;
+  return c >= 0 ? __ldg(a.g + c) : 0.0;
+#endif
+}
+
+// s += sum over the slice's steps [0, L) of val * g[idx], lane = one row, ascending step order,
+// SU steps in flight per lane (loads of a batch issued before its gathers, gathers before sums).
+template <int ROLE>
+__device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L, int lane, int row, double s,
+                                               uint64_t pol) {
+  const int32_t* ip = a.idx + (long long)st0 * 32 + lane;
+  const double* vp = a.val + (long long)st0 * 32 + lane;
+  int j = 0;
+  for (; j + SU <= L; j += SU) {
+    int32_t c[SU];
+    double v[SU], gv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u], row, ROLE);
+#pragma unroll
+    for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
+  }
+  if (j < L) {
+    int32_t c[SU];
+    double v[SU], gv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      c[u] = -1;
+      if (j + u < L) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u], row, ROLE);
+#pragma unroll
+    for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
+  }
+  return s;
+}
+
+// BS = NT (fmt 1): persistent grid, slices dealt round-robin over all warps of the grid; each
+//   thread accumulates its rows' dot contributions (static assignment: deterministic).
+// BS = 1024 (fmt 3): one CTA per SM walks the contiguous, entry-balanced slice range
+//   [cblk[c], cblk[c+1]) * NSB; its 32 warps take slices in order from a shared counter (rows of
+//   very different lengths balance across warps; consecutive in-flight slices share their band of
+//   g in L1). Slice order is run-dependent, so dots are reduced per slice (slpart) and summed in
+//   slice order (deterministic).
+// Slice metadata (start, length, this lane's row) is loaded one slice ahead, so a slice's stream
+// loads wait for DRAM only, not for an L2 round trip to sptr / perm first.
 template <int ROLE, int BS = NT>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
+  constexpr bool DYN = BS != NT;
+  constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
   __shared__ double sm[2][MAXW];
+  __shared__ int s_next;
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = policy_evict_first();
-#if PLSS_HINTS
-  const uint64_t pol_keep = PLSS_HINTS == 1 ? policy_evict_last() : policy_evict_normal();
-#endif
   double acc0 = 0.0, acc1 = 0.0;
-  int sl_begin, sl_end, wtotal;
-  if (BS == NT) {
-    sl_begin = blockIdx.x * (NT / 32) + warp; sl_end = a.nslices; wtotal = gridDim.x * (NT / 32);
+  int sl0, sl1, stride;
+  if (!DYN) {
+    sl0 = blockIdx.x * (NT / 32); sl1 = a.nslices; stride = gridDim.x * (NT / 32);
   } else {
-    sl_begin = a.cblk[blockIdx.x] * NSB + warp;
-    sl_end = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices);
-    wtotal = BS / 32;
+    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices); stride = BS / 32;
+    if (tid == 0) s_next = sl0 + BS / 32;           // slices sl0 .. sl0+31 are taken statically
+    __syncthreads();
   }
-  // slice metadata (start, end, row of this lane) is loaded one slice ahead: the stream loads of
-  // a slice then wait for DRAM only, not for an L2 round trip to sptr / perm first
+  int sl = sl0 + warp;
   int m0 = 0, m1 = 0, mrow = -1;
-  if (sl_begin < sl_end) {
-    m0 = a.sptr[sl_begin]; m1 = a.sptr[sl_begin + 1];
-    mrow = a.perm ? a.perm[sl_begin * 32 + lane] : sl_begin * 32 + lane;
-  }
-  for (int sl = sl_begin; sl < sl_end; sl += wtotal) {
-    const int st0 = m0, L = m1 - m0, row_cur = mrow;
-    if (sl + wtotal < sl_end) {
-      const int nx = sl + wtotal;
-      m0 = a.sptr[nx]; m1 = a.sptr[nx + 1];
-      mrow = a.perm ? a.perm[nx * 32 + lane] : nx * 32 + lane;
+  auto meta = [&](int t) {
+    m0 = a.sptr[t]; m1 = a.sptr[t + 1];
+    mrow = a.perm ? a.perm[t * 32 + lane] : t * 32 + lane;
+  };
+  if (sl < sl1) meta(sl);
+  while (sl < sl1) {
+    const int st0 = m0, L = m1 - m0, row = mrow;
+    int nx;
+    if (!DYN) {
+      nx = sl + stride;
+    } else {
+      nx = 0;
+      if (lane == 0) nx = atomicAdd(&s_next, 1);
+      nx = __shfl_sync(FULL, nx, 0);
     }
-#if PLSS_PF
-    if (lane < PLSS_PF && sl + (lane + 1) * wtotal < a.nslices) {   // streams of this warp's next slices -> L2
-      const int nx = sl + (lane + 1) * wtotal;
-      const long long e0 = (long long)a.sptr[nx] * 32, e1 = (long long)a.sptr[nx + 1] * 32;
-      if (e1 > e0) {
-        prefetch_l2(a.idx + e0, (unsigned)(e1 - e0) * 4u);
-        prefetch_l2(a.val + e0, (unsigned)(e1 - e0) * 8u);
-      }
-    }
-#endif
-    const int row = row_cur;
+    if (nx < sl1) meta(nx);
     const bool valid = row >= 0 && row < a.nrows;
     double s = 0.0;
-#if PLSS_HINTS
-    if (ROLE >= ROLE_K2 && valid && a.accumulate) s = ld_hint(a.out + row, pol);  // y: read once per slab
-    const double r_old = (ROLE == ROLE_K1 && valid) ? ld_hint(a.out + row, pol) : 0.0;
-#else
+#if !(PLSS_ABLATE & 32)
     if (ROLE >= ROLE_K2 && valid && a.accumulate) s = a.out[row];
+#endif
     const double r_old = (ROLE == ROLE_K1 && valid) ? a.out[row] : 0.0;   // issued early
-#endif
-    const int32_t* ip = a.idx + (long long)st0 * 32 + lane;
-    const double* vp = a.val + (long long)st0 * 32 + lane;
-    int j = 0;
-    for (; j + SU <= L; j += SU) {
-      int32_t c[SU];
-      double v[SU], gv[SU];
-#pragma unroll
-      for (int u = 0; u < SU; ++u) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-#if PLSS_ABLATE & 4
-        gv[u] = (double)c[u];                                   // ablation: no gathers
-#else
-        gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
-#endif
-      }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
-    }
-    if (j < L) {
-      int32_t c[SU];
-      double v[SU], gv[SU];
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        c[u] = -1;
-        if (j + u < L) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
-      }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-#if PLSS_ABLATE & 4
-        gv[u] = (double)c[u];                                   // ablation: no gathers
-#else
-        gv[u] = c[u] >= 0 ? __ldg(a.g + c[u]) : 0.0;
-#endif
-      }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
-    }
+    s = sell_row_sum<ROLE>(a, st0, L, lane, row, s, pol);
+    double d0 = 0.0, d1 = 0.0;
     if (valid) {
       if (ROLE == ROLE_PLAIN) {
         a.out[row] = s;
       } else if (ROLE == ROLE_K1) {
         const double rn = __dsub_rn(r_old, s);                  // r_i <- r_i - (A p)_i
-#if PLSS_HINTS
-        st_stream(a.out + row, rn, pol_keep);                   // gathered by K2 of this slab next
-#else
         a.out[row] = rn;
-#endif
-        acc0 = fma(rn, rn, acc0);
+        d0 = rn * rn;
       } else {
-#if PLSS_HINTS
-        st_stream(a.out + row, s, pol);                         // y_j (re-read by the next slab / K3)
-        if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, ld_hint(a.pv + row, pol), acc1); }
+#if PLSS_ABLATE & 32
+        if (s == 1234.5) a.out[row] = s;                        // ablation: no y write
 #else
         a.out[row] = s;                                         // y_j
-        if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, a.pv[row], acc1); }
 #endif
+        if (ROLE == ROLE_K2DOTS) { d0 = s * s; d1 = s * a.pv[row]; }
       }
     }
+    if (DOTS) {
+      if (!DYN) {
+        acc0 += d0; acc1 += d1;
+      } else {
+        d0 = warp_sum(d0);
+        d1 = warp_sum(d1);
+        if (lane == 0) { a.slpart[2 * sl] = d0; a.slpart[2 * sl + 1] = d1; }
+      }
+    }
+    sl = nx;
   }
-  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;
+  if (!DOTS) return;
+  if (DYN) {
+    __syncthreads();
+    for (int q = sl0 + tid; q < sl1; q += BS) { acc0 += a.slpart[2 * q]; acc1 += a.slpart[2 * q + 1]; }
+  }
   if (!a.finalize) {
     block_sum2(acc0, acc1, sm);
     if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
