@@ -40,6 +40,21 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _traffic(workload, kernel_class, launches_per_step):
+    """DRAM bytes (read + write) per step of the dominant kernel class, from the committed
+    `ncu --set full` capture (profiles/r01_ncu_traffic_c5.json: per-launch averages x launches per
+    step). None when no capture of this workload exists."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic_c5.json")
+    if workload != "C5" or not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        d = json.load(f)
+    e = d["per_launch"].get(kernel_class)
+    if e is None:
+        return None, None
+    return e["dram_bytes"] * launches_per_step, f"{os.path.relpath(path, ROOT)}: {d['source']}"
+
+
 # ---------------------------------------------------------------------------------------------
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------------------------
@@ -283,6 +298,7 @@ def main():
     dom_ms, dom_bytes = classes[dom]
     peak, peak_src = _peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    traffic, traffic_src = _traffic(w["name"], dom, q["slabs"])
 
     # ---- end-to-end through the public API: host b in, host x + history out, K steps ---------
     pin_b = torch.empty(m_l, dtype=torch.float64, pin_memory=True)
@@ -318,7 +334,8 @@ def main():
             "achieved_frac_of_peak": B_global * iters_per_s / 1e9 / peak,
             "achieved_frac_of_8tbs": B_global * iters_per_s / 1e9 / 8000.0,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_step": dom_bytes, "kernel_ms_per_step": dom_ms},
             "kernels_ms_per_step": kt,
             "gpu_launches": args.steps * q["launches_per_step"],

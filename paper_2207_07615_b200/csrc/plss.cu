@@ -610,6 +610,16 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     return grid_for(((int64_t)a.nslices + NT / 32 - 1) / (NT / 32), occ_sell, sms);
   };
 
+  // ---- L2 cache policies (uniform kernel parameters, see SpmvSeg::pol_first) -------------------
+  uint64_t pols[2] = {0, 0};
+  {
+    uint64_t* d_pol = (uint64_t*)(w + L.err + 32);
+    k_policies<<<1, 1, 0, st>>>(d_pol);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(pols, d_pol, sizeof pols, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
   // ---- K1 segments (CSR row slabs) ----------------------------------------------------------
   int2* desc1 = (int2*)(w + L.tile1);
   int2* desc2 = (int2*)(w + L.tile2);
@@ -623,6 +633,8 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   for (int s = 0; s < S; ++s) {
     SpmvSeg& a = ctx->seg1[s];
     memset(&a, 0, sizeof a);
+    a.pol_first = pols[0];
+    a.pol_last = pols[1];
     const int64_t rows = ctx->R[s + 1] - ctx->R[s];
     a.ptr = A->row_ptr + ctx->R[s];
     a.idx = A->col_idx;
@@ -676,6 +688,8 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   for (int s = 0; s < S; ++s) {
     SpmvSeg& a = ctx->seg2[s];
     memset(&a, 0, sizeof a);
+    a.pol_first = pols[0];
+    a.pol_last = pols[1];
     if (S > 1) {
       a.ptr = sptr + (size_t)s * (n + 1);
       a.idx = sidx;

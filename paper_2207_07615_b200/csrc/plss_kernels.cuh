@@ -33,33 +33,14 @@ namespace plss {
 #ifndef PLSS_MINB
 #define PLSS_MINB 4
 #endif
-#ifndef PLSS_KDESIGN
-#define PLSS_KDESIGN 2      // CSR-tile kernel design: 2 CTA-synchronous TMA tiles (default);
-#endif                      // 3 warp-specialized; 4 software-pipelined; 5 warp-autonomous
 constexpr int NT = 256;                 // threads per CTA of the vector kernels
-constexpr int NCW = 8;                  // consumer warps per SpMV CTA
-#ifndef PLSS_WPC
-#define PLSS_WPC 4
-#endif
-constexpr int WPC = PLSS_WPC;           // design 5: autonomous warps per CTA
-#if PLSS_KDESIGN == 2 || PLSS_KDESIGN == 4
-constexpr int NTS = NT;                 // SpMV CTA: 8 warps, thread 0 also issues the TMA copies
-#elif PLSS_KDESIGN == 5
-constexpr int NTS = WPC * 32;           // SpMV CTA: WPC warps, each its own TMA pipeline
-#else
-constexpr int NTS = (NCW + 1) * 32;     // SpMV CTA: 8 consumer warps + 1 TMA producer warp
-#endif
+constexpr int NCW = 8;                  // warps per CSR-tile SpMV CTA
+constexpr int NTS = NT;                 // CSR-tile CTA: 8 warps, thread 0 also issues the TMA copies
 constexpr int TILE = PLSS_TILE;         // nnz window of a SpMV tile (rows whose first entry lies in it)
 constexpr int SUBW = TILE / NCW;        // nnz sub-window of one consumer warp
 constexpr int RCAP = TILE / 4;          // at most this many rows per tile
 #ifndef PLSS_ABLATE
 #define PLSS_ABLATE 0       // timing experiments only: 1 = no gathers, 2 = no row phase
-#endif
-#ifndef PLSS_RLAST
-#define PLSS_RLAST 0
-#endif
-#ifndef PLSS_CONTIG
-#define PLSS_CONTIG 0
 #endif
 #ifndef PLSS_SLACK
 #define PLSS_SLACK (PLSS_TILE / 4)
@@ -122,6 +103,10 @@ struct SpmvSeg {
   // ring of `ring` doubles in shared memory, every other entry from global memory
   int32_t win, ring, nblocks, glen, nsb;
   int32_t row0;              // first row of this segment in the matrix (ablation experiments only)
+  // L2 cache policies (createpolicy values computed once at setup by k_policies). Passed as kernel
+  // parameters they sit in uniform registers: a per-thread createpolicy result costs one R2UR
+  // (XU pipe) per cache-hinted load, which saturated the XU pipe of K1 (profiles/r01_notes.md).
+  uint64_t pol_first, pol_last;
   const int2* wlo;           // per block {lo_b, flags}: 1 = reload the whole window, 2 = no window
   const int32_t* cblk;       // grid+1 block bounds of the CTAs (balanced by stored entries)
   double* slpart;            // per-slice dot partials (fixed-order reduction, deterministic)
@@ -342,7 +327,7 @@ struct Stage {
   static constexpr int V2_OFF = V1_OFF + V1_BYTES;
   static constexpr int V2_BYTES = HAS_V2 ? (RCAP + 4) * 8 : 0;
   static constexpr int BYTES = (V2_OFF + V2_BYTES + 127) / 128 * 128;
-  static constexpr int SMEM = (PLSS_KDESIGN == 5 ? WPC : 1) * NST * BYTES;
+  static constexpr int SMEM = NST * BYTES;
 };
 
 struct StageDesc {
@@ -360,9 +345,9 @@ __device__ __forceinline__ unsigned span16(const void* lo, const void* hi_excl) 
   return (unsigned)(b - a);
 }
 
-#if PLSS_KDESIGN == 2
 // ---------------------------------------------------------------------------------------------
-// K1 / K2 / plain SpMV: persistent CTAs; each tile's values, indices, row pointers and row-wise
+// K1 / K2 / plain SpMV over CSR tiles (fmt 0; segments whose SELL-32 padding would be too large,
+// e.g. power-law rows): persistent CTAs; each tile's values, indices, row pointers and row-wise
 // vector slices arrive by TMA bulk copies NST-1 tiles ahead; products are formed in place in
 // shared memory; rows are owned by the tile holding their first entry and summed sequentially.
 // ---------------------------------------------------------------------------------------------
@@ -376,17 +361,8 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
-#if PLSS_CONTIG
-  // contiguous tile range per CTA: consecutive tiles reuse the gathered vector's lines in L1
-  const int t_first = (int)(((long long)a.ntiles * blockIdx.x) / G);
-  const int my_tiles = (int)(((long long)a.ntiles * (blockIdx.x + 1)) / G) - t_first;
-#else
   const int my_tiles = a.ntiles > (int)blockIdx.x ? (a.ntiles - (int)blockIdx.x + G - 1) / G : 0;
-#endif
-  const uint64_t pol = policy_evict_first();
-#if PLSS_RLAST
-  const uint64_t pol_last = policy_evict_last();
-#endif
+  const uint64_t pol = a.pol_first;
   double acc0 = 0.0, acc1 = 0.0;
 
   const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
@@ -399,11 +375,7 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
 
   // producer (thread 0): describe tile j of this CTA and start its bulk copies into stage j % NST
   auto issue = [&](int j) {
-#if PLSS_CONTIG
-    const int t = t_first + j;
-#else
     const int t = (int)blockIdx.x + j * G;
-#endif
     const int q = j % NST;
     const int2 d0 = a.desc[t], d1 = a.desc[t + 1];
     StageDesc d;
@@ -538,11 +510,7 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
           a.out[i] = s;
         } else if (ROLE == ROLE_K1) {
           const double rn = __dsub_rn(V1[i - d.rb], s);          // r_i <- r_i - (A p)_i
-#if PLSS_RLAST
-          st_hint(a.out + i, rn, pol_last);                     // keep r_s in L2 for K2_s
-#else
           a.out[i] = rn;
-#endif
           acc0 = fma(rn, rn, acc0);
         } else {
           a.out[i] = s;                                         // y_j
@@ -567,644 +535,6 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
     tail_y(a.ctl, a.rec, acc0, acc1);
   }
 }
-
-#elif PLSS_KDESIGN == 4
-// ---------------------------------------------------------------------------------------------
-// K1 / K2 / plain SpMV: persistent CTAs, software-pipelined over tiles. Each tile's values,
-// indices, row pointers and row-wise vector slices arrive by TMA bulk copies (thread 0,
-// cp.async.bulk + mbarrier) two tiles ahead; while the rows of tile j are summed, the gathers of
-// tile j+1 are already in flight; their products are then formed in place in shared memory.
-// Rows are owned by the tile holding their first entry and summed sequentially (lane per row).
-// ---------------------------------------------------------------------------------------------
-template <int ROLE>
-__global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
-  using C = Stage<ROLE>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bars[NST];
-  __shared__ StageDesc sdesc[NST];
-  __shared__ double sm[2][MAXW];
-  if (a.ctl != nullptr && a.ctl->done) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-#if PLSS_CONTIG
-  // contiguous tile range per CTA: consecutive tiles reuse the gathered vector's lines in L1
-  const int t_first = (int)(((long long)a.ntiles * blockIdx.x) / G);
-  const int my_tiles = (int)(((long long)a.ntiles * (blockIdx.x + 1)) / G) - t_first;
-#else
-  const int my_tiles = a.ntiles > (int)blockIdx.x ? (a.ntiles - (int)blockIdx.x + G - 1) / G : 0;
-#endif
-  const uint64_t pol = policy_evict_first();
-  double acc0 = 0.0, acc1 = 0.0;
-
-  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
-  if (tid == 0) {
-#pragma unroll
-    for (int q = 0; q < NST; ++q) mbar_init(&bars[q], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  // producer (thread 0): describe tile j of this CTA and start its bulk copies into stage j % NST
-  auto issue = [&](int j) {
-#if PLSS_CONTIG
-    const int t = t_first + j;
-#else
-    const int t = (int)blockIdx.x + j * G;
-#endif
-    const int q = j % NST;
-    const int2 d0 = a.desc[t], d1 = a.desc[t + 1];
-    StageDesc d;
-    d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
-    d.se = min(d1.y, d0.y + CAP);
-    unsigned char* base = smem + q * C::BYTES;
-    unsigned tx = 0;
-    const char* lo;
-    unsigned nb;
-    // values [s0, se)
-    lo = align16_down(a.val + d.s0);
-    nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
-    d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
-    if (nb) { tma_load(base + C::V_OFF, lo, nb, &bars[q], pol); tx += nb; }
-    // indices [s0, se)
-    lo = align16_down(a.idx + d.s0);
-    nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
-    d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
-    if (nb) { tma_load(base + C::I_OFF, lo, nb, &bars[q], pol); tx += nb; }
-    // row pointers [r0, r1]
-    lo = align16_down(a.ptr + d.r0);
-    nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
-    d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
-    tma_load(base + C::P_OFF, lo, nb, &bars[q], pol);
-    tx += nb;
-    // row-wise vector slices [r0, r1)
-    d.rb = d.r0;
-    d.rb2 = d.r0;
-    if (d.r1 > d.r0) {
-      if (C::HAS_V1 && v1src) {
-        lo = align16_down(v1src + d.r0);
-        nb = span16(v1src + d.r0, v1src + d.r1);
-        d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
-        tma_load(base + C::V1_OFF, lo, nb, &bars[q], pol);
-        tx += nb;
-      }
-      if (C::HAS_V2) {
-        lo = align16_down(a.pv + d.r0);
-        nb = span16(a.pv + d.r0, a.pv + d.r1);
-        d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
-        tma_load(base + C::V2_OFF, lo, nb, &bars[q], pol);
-        tx += nb;
-      }
-    }
-    sdesc[q] = d;
-    mbar_expect_tx(&bars[q], tx);
-  };
-
-  constexpr int GU = (CAP + NT - 1) / NT;     // gathers per thread per tile
-  // gathers of tile j: issued into registers, committed (products in place) later
-  auto gather_issue = [&](int j, double (&gv)[GU]) {
-    const int q = j % NST;
-    const StageDesc& d = sdesc[q];
-    const int32_t* I = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::I_OFF);
-    const int cnt = d.se - d.s0, ioff = d.s0 - d.ib;
-#pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      const int k = tid + u * NT;
-      if (k < cnt) gv[u] = __ldg(a.g + I[ioff + k]);
-    }
-  };
-  auto gather_commit = [&](int j, const double (&gv)[GU]) {
-    const int q = j % NST;
-    const StageDesc& d = sdesc[q];
-    double* V = reinterpret_cast<double*>(smem + q * C::BYTES + C::V_OFF);
-    const int cnt = d.se - d.s0, voff = d.s0 - d.vb;
-#pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      const int k = tid + u * NT;
-      if (k < cnt) V[voff + k] = __dmul_rn(V[voff + k], gv[u]);
-    }
-  };
-  auto rows = [&](int j) {
-    const int q = j % NST;
-    const StageDesc d = sdesc[q];
-    const double* V = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V_OFF);
-    const int32_t* P = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::P_OFF);
-    const double* V1 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V1_OFF);
-    const double* V2 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V2_OFF);
-    const int vsh = -d.vb;   // V index of entry position e is e - vb
-    // rows spread evenly over the 8 warps (a tile of short rows has far fewer rows than threads)
-    const int rpw = (d.r1 - d.r0 + NT / 32 - 1) / (NT / 32);
-    const int wlo = d.r0 + warp * rpw, whi = min(d.r1, wlo + rpw);
-    for (int base = wlo; base < whi; base += 32) {
-      const int i = base + lane;
-      const bool valid = i < whi;
-      int b = 0, e = 0;
-      if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
-      const bool lng = valid && (e - b) > LONGROW;
-      double s = 0.0;
-      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
-      if (valid && !lng) {
-        const int es = min(e, d.se);
-        int k = b;
-#pragma unroll 1
-        for (; k + 4 <= es; k += 4) {                       // staged products, 4 loads in flight
-          const double p0 = V[k + vsh], p1 = V[k + 1 + vsh], p2 = V[k + 2 + vsh], p3 = V[k + 3 + vsh];
-          s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
-        }
-        for (; k < es; ++k) s = __dadd_rn(s, V[k + vsh]);
-        for (; k < e; ++k)                                   // spill past the staged window
-          s = __dadd_rn(s, __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol))));
-      }
-      unsigned mask = __ballot_sync(FULL, lng);
-      while (mask) {                                            // warp-cooperative long rows
-        const int l = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
-        double ps = 0.0;
-        for (int k = lb + lane; k < le; k += 32) {
-          const double pr = (k < d.se) ? V[k + vsh]
-                                       : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
-          ps = __dadd_rn(ps, pr);
-        }
-        ps = warp_sum(ps);
-        if (lane == l) s = __dadd_rn(s, ps);
-      }
-      if (valid) {
-        if (ROLE == ROLE_PLAIN) {
-          a.out[i] = s;
-        } else if (ROLE == ROLE_K1) {
-          const double rn = __dsub_rn(V1[i - d.rb], s);          // r_i <- r_i - (A p)_i
-          a.out[i] = rn;
-          acc0 = fma(rn, rn, acc0);
-        } else {
-          a.out[i] = s;                                         // y_j
-          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
-        }
-      }
-    }
-  };
-
-  static_assert(NST >= 3, "software pipeline needs 3 stages: rows(j), gathers(j+1), TMA(j+2)");
-  if (tid == 0)
-    for (int j = 0; j < min(NST - 1, my_tiles); ++j) issue(j);
-  double gv[GU];
-  if (my_tiles > 0) {
-    mbar_wait(&bars[0], 0u);
-    gather_issue(0, gv);
-    gather_commit(0, gv);
-  }
-  __syncthreads();
-  for (int j = 0; j < my_tiles; ++j) {
-    if (tid == 0 && j + NST - 1 < my_tiles) {
-      fence_proxy_async();          // generic accesses to that stage (tile j-1) happen-before
-      issue(j + NST - 1);
-    }
-    const bool next = j + 1 < my_tiles;
-    if (next) {
-      mbar_wait(&bars[(j + 1) % NST], (unsigned)((j + 1) / NST) & 1u);
-      gather_issue(j + 1, gv);      // in flight while the rows of tile j are summed
-    }
-    rows(j);
-    if (next) gather_commit(j + 1, gv);
-    __syncthreads();
-  }
-  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;           // nothing to reduce
-  if (!a.finalize) {                                            // slab s < S-1: publish only
-    block_sum2(acc0, acc1, sm);
-    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
-    return;
-  }
-  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
-  if (tid != 0) return;
-  if (ROLE == ROLE_K1) {
-    if (a.dist) *a.rho_out = acc0;                              // local rho -> all-reduce buffer
-    else tail_rho(a.ctl, a.rec, acc0);
-  } else if (ROLE == ROLE_K2DOTS) {
-    tail_y(a.ctl, a.rec, acc0, acc1);
-  }
-}
-
-#elif PLSS_KDESIGN == 5
-// ---------------------------------------------------------------------------------------------
-// K1 / K2 / plain SpMV, warp-autonomous pipelines. Every warp owns a contiguous range of small
-// tiles (TILE entries, <= TILE/4 rows) and its own NST-stage ring of shared memory: lane 0
-// issues the TMA bulk copies of tile j+NST-1 (values, indices, row pointers, row-wise vector
-// slices) while the warp forms the products of tile j (all its gathers in flight) and sums its
-// rows sequentially (lane per row). No CTA-wide barrier: a warp waiting on a slow gather never
-// holds up the other warps.
-// ---------------------------------------------------------------------------------------------
-template <int ROLE>
-__global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
-  using C = Stage<ROLE>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bars[WPC][NST];
-  __shared__ StageDesc sdesc[WPC][NST];
-  __shared__ double sm[2][MAXW];
-  if (a.ctl != nullptr && a.ctl->done) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long GW = (long long)gridDim.x * WPC;
-  const long long gw = (long long)blockIdx.x * WPC + warp;
-  const int t_first = (int)(((long long)a.ntiles * gw) / GW);
-  const int my_tiles = (int)(((long long)a.ntiles * (gw + 1)) / GW) - t_first;
-  const uint64_t pol = policy_evict_first();
-  double acc0 = 0.0, acc1 = 0.0;
-  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
-  unsigned char* wsm = smem + warp * NST * C::BYTES;
-  uint64_t* wb = bars[warp];
-  StageDesc* wd = sdesc[warp];
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < NST; ++q) mbar_init(&wb[q], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-
-  // tile descriptors, 32 per batch, the next batch prefetched
-  int cur = -1;
-  int2 bl = make_int2(0, 0), bx = make_int2(0, 0), nl = make_int2(0, 0), nx = make_int2(0, 0);
-  auto load_batch = [&](int jb, int2& l, int2& x) {
-    const int t = t_first + jb + lane;
-    l = (jb + lane <= my_tiles) ? a.desc[t] : make_int2(0, 0);
-    x = (jb + 32 <= my_tiles) ? a.desc[t_first + jb + 32] : make_int2(0, 0);
-  };
-  auto desc_of = [&](int j, int2& d0, int2& d1) {   // warp-uniform j
-    const int jb = j & ~31;
-    if (jb != cur) {
-      if (cur >= 0 && jb == cur + 32) { bl = nl; bx = nx; } else load_batch(jb, bl, bx);
-      cur = jb;
-      if (jb + 32 < my_tiles) load_batch(jb + 32, nl, nx);
-    }
-    const int jj = j - jb;
-    d0.x = __shfl_sync(FULL, bl.x, jj);
-    d0.y = __shfl_sync(FULL, bl.y, jj);
-    const int ax = __shfl_sync(FULL, bl.x, (jj + 1) & 31), ay = __shfl_sync(FULL, bl.y, (jj + 1) & 31);
-    const int cx = __shfl_sync(FULL, bx.x, 0), cy = __shfl_sync(FULL, bx.y, 0);
-    d1.x = jj < 31 ? ax : cx;
-    d1.y = jj < 31 ? ay : cy;
-  };
-  auto issue = [&](int j, int2 d0, int2 d1) {      // lane 0 only
-    const int q = j % NST;
-    StageDesc d;
-    d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
-    d.se = min(d1.y, d0.y + CAP);
-    unsigned char* base = wsm + q * C::BYTES;
-    unsigned tx = 0, nb;
-    const char* lo;
-    lo = align16_down(a.val + d.s0);
-    nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
-    d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
-    if (nb) { tma_load(base + C::V_OFF, lo, nb, &wb[q], pol); tx += nb; }
-    lo = align16_down(a.idx + d.s0);
-    nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
-    d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
-    if (nb) { tma_load(base + C::I_OFF, lo, nb, &wb[q], pol); tx += nb; }
-    lo = align16_down(a.ptr + d.r0);
-    nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
-    d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
-    tma_load(base + C::P_OFF, lo, nb, &wb[q], pol);
-    tx += nb;
-    d.rb = d.r0;
-    d.rb2 = d.r0;
-    if (C::HAS_V1 && v1src) {
-      lo = align16_down(v1src + d.r0);
-      nb = span16(v1src + d.r0, v1src + d.r1);
-      d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
-      tma_load(base + C::V1_OFF, lo, nb, &wb[q], pol);
-      tx += nb;
-    }
-    if (C::HAS_V2) {
-      lo = align16_down(a.pv + d.r0);
-      nb = span16(a.pv + d.r0, a.pv + d.r1);
-      d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
-      tma_load(base + C::V2_OFF, lo, nb, &wb[q], pol);
-      tx += nb;
-    }
-    wd[q] = d;
-    mbar_expect_tx(&wb[q], tx);
-  };
-
-  for (int j = 0; j < min(NST - 1, my_tiles); ++j) {
-    int2 d0, d1;
-    desc_of(j, d0, d1);
-    if (lane == 0) issue(j, d0, d1);
-  }
-  constexpr int GU = (CAP + 31) / 32;
-  for (int j = 0; j < my_tiles; ++j) {
-    const int q = j % NST;
-    if (j + NST - 1 < my_tiles) {
-      int2 d0, d1;
-      desc_of(j + NST - 1, d0, d1);
-      if (lane == 0) {
-        fence_proxy_async();        // this warp's generic accesses to that stage (tile j-1) happen-before
-        issue(j + NST - 1, d0, d1);
-      }
-    }
-    mbar_wait(&wb[q], (unsigned)(j / NST) & 1u);
-    const StageDesc d = wd[q];
-    double* V = reinterpret_cast<double*>(wsm + q * C::BYTES + C::V_OFF);
-    const int32_t* I = reinterpret_cast<const int32_t*>(wsm + q * C::BYTES + C::I_OFF);
-    const int32_t* P = reinterpret_cast<const int32_t*>(wsm + q * C::BYTES + C::P_OFF);
-    const double* V1 = reinterpret_cast<const double*>(wsm + q * C::BYTES + C::V1_OFF);
-    const double* V2 = reinterpret_cast<const double*>(wsm + q * C::BYTES + C::V2_OFF);
-    {
-      const int cnt = d.se - d.s0;
-      const int voff = d.s0 - d.vb, ioff = d.s0 - d.ib;
-      double gv[GU];
-#pragma unroll
-      for (int u = 0; u < GU; ++u) {
-        const int k = lane + u * 32;
-        if (k < cnt) gv[u] = __ldg(a.g + I[ioff + k]);
-      }
-#pragma unroll
-      for (int u = 0; u < GU; ++u) {
-        const int k = lane + u * 32;
-        if (k < cnt) V[voff + k] = __dmul_rn(V[voff + k], gv[u]);
-      }
-    }
-    __syncwarp();
-    const int vsh = -d.vb;
-    for (int base = d.r0; base < d.r1; base += 32) {
-      const int i = base + lane;
-      const bool valid = i < d.r1;
-      int b = 0, e = 0;
-      if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
-      const bool lng = valid && (e - b) > LONGROW;
-      double s = 0.0;
-      if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
-      if (valid && !lng) {
-        const int es = min(e, d.se);
-        int k = b;
-#pragma unroll 1
-        for (; k + 4 <= es; k += 4) {
-          const double p0 = V[k + vsh], p1 = V[k + 1 + vsh], p2 = V[k + 2 + vsh], p3 = V[k + 3 + vsh];
-          s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
-        }
-        for (; k < es; ++k) s = __dadd_rn(s, V[k + vsh]);
-        for (; k < e; ++k)
-          s = __dadd_rn(s, __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol))));
-      }
-      unsigned mask = __ballot_sync(FULL, lng);
-      while (mask) {
-        const int l = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
-        double ps = 0.0;
-        for (int k = lb + lane; k < le; k += 32) {
-          const double pr = (k < d.se) ? V[k + vsh]
-                                       : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
-          ps = __dadd_rn(ps, pr);
-        }
-        ps = warp_sum(ps);
-        if (lane == l) s = __dadd_rn(s, ps);
-      }
-      if (valid) {
-        if (ROLE == ROLE_PLAIN) {
-          a.out[i] = s;
-        } else if (ROLE == ROLE_K1) {
-          const double rn = __dsub_rn(V1[i - d.rb], s);
-          a.out[i] = rn;
-          acc0 = fma(rn, rn, acc0);
-        } else {
-          a.out[i] = s;
-          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;
-  __syncthreads();
-  if (!a.finalize) {
-    block_sum2(acc0, acc1, sm);
-    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
-    return;
-  }
-  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
-  if (tid != 0) return;
-  if (ROLE == ROLE_K1) {
-    if (a.dist) *a.rho_out = acc0;
-    else tail_rho(a.ctl, a.rec, acc0);
-  } else if (ROLE == ROLE_K2DOTS) {
-    tail_y(a.ctl, a.rec, acc0, acc1);
-  }
-}
-
-#else
-// ---------------------------------------------------------------------------------------------
-// K1 / K2 / plain SpMV. Persistent, warp-specialized CTAs:
-//   producer warp : for each of the CTA's tiles, one lane waits for the stage to be released
-//                   (empty mbarrier), then starts TMA bulk copies of the tile's values, indices,
-//                   row pointers and row-wise vector slices (full mbarrier, expect_tx);
-//   8 consumer warps: each owns the rows of the tile whose first entry lies in its 1/8 of the
-//                   tile's nnz window, forms their products in place (gathers of the whole warp
-//                   range in flight), sums each row sequentially (lane per row; warp tree for rows
-//                   > LONGROW), writes the epilogue and releases the stage -- warps never wait for
-//                   each other, only for data.
-// ---------------------------------------------------------------------------------------------
-template <int ROLE>
-__global__ void __launch_bounds__(NTS, MINB) k_spmv(SpmvSeg a) {
-  using C = Stage<ROLE>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[NST], empty[NST];
-  __shared__ StageDesc sdesc[NST];
-  __shared__ double sm[2][MAXW];
-  if (a.ctl != nullptr && a.ctl->done) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // contiguous tile range per CTA: consecutive tiles share descriptor loads and gather locality
-  const int G = gridDim.x;
-  const int t_first = (int)(((long long)a.ntiles * blockIdx.x) / G);
-  const int my_tiles = (int)(((long long)a.ntiles * (blockIdx.x + 1)) / G) - t_first;
-  const uint64_t pol = policy_evict_first();
-  double acc0 = 0.0, acc1 = 0.0;
-  const double* v1src = (ROLE == ROLE_K1 || a.accumulate) ? a.out : nullptr;
-  if (tid == 0) {
-#pragma unroll
-    for (int q = 0; q < NST; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], NCW); }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == NCW) {
-    // ------------------------------ producer ------------------------------------------------
-    // descriptors of the next 32 tiles are loaded by the 32 lanes one batch ahead
-    auto load_batch = [&](int jb, int2& dl, int2& dx) {
-      const int t = t_first + jb + lane;
-      dl = (jb + lane <= my_tiles) ? a.desc[t] : make_int2(0, 0);
-      dx = (jb + 32 <= my_tiles) ? a.desc[t_first + jb + 32] : make_int2(0, 0);
-    };
-    int2 dl, dx, nl = make_int2(0, 0), nx = make_int2(0, 0);
-    load_batch(0, dl, dx);
-    for (int jb = 0; jb < my_tiles; jb += 32) {
-      if (jb + 32 < my_tiles) load_batch(jb + 32, nl, nx);
-      const int cnt = min(32, my_tiles - jb);
-      for (int jj = 0; jj < cnt; ++jj) {
-        const int j = jb + jj;
-        int2 d0, d1;
-        d0.x = __shfl_sync(FULL, dl.x, jj); d0.y = __shfl_sync(FULL, dl.y, jj);
-        const int src = jj < 31 ? jj + 1 : 0;
-        d1.x = __shfl_sync(FULL, jj < 31 ? dl.x : dx.x, src);
-        d1.y = __shfl_sync(FULL, jj < 31 ? dl.y : dx.y, src);
-        if (lane == 0) {
-        const int q = j % NST;
-        if (j >= NST) mbar_wait(&empty[q], (unsigned)(j / NST - 1) & 1u);
-        fence_proxy_async();
-        StageDesc d;
-        d.r0 = d0.x; d.r1 = d1.x; d.s0 = d0.y;
-        d.se = min(d1.y, d0.y + CAP);
-        unsigned char* base = smem + q * C::BYTES;
-        unsigned tx = 0, nb;
-        const char* lo;
-        lo = align16_down(a.val + d.s0);
-        nb = d.se > d.s0 ? span16(a.val + d.s0, a.val + d.se) : 0;
-        d.vb = d.s0 - (int)((a.val + d.s0) - reinterpret_cast<const double*>(lo));
-        if (nb) { tma_load(base + C::V_OFF, lo, nb, &full[q], pol); tx += nb; }
-        lo = align16_down(a.idx + d.s0);
-        nb = d.se > d.s0 ? span16(a.idx + d.s0, a.idx + d.se) : 0;
-        d.ib = d.s0 - (int)((a.idx + d.s0) - reinterpret_cast<const int32_t*>(lo));
-        if (nb) { tma_load(base + C::I_OFF, lo, nb, &full[q], pol); tx += nb; }
-        lo = align16_down(a.ptr + d.r0);
-        nb = span16(a.ptr + d.r0, a.ptr + d.r1 + 1);
-        d.pb = d.r0 - (int)((a.ptr + d.r0) - reinterpret_cast<const int32_t*>(lo));
-        tma_load(base + C::P_OFF, lo, nb, &full[q], pol);
-        tx += nb;
-        d.rb = d.r0;
-        d.rb2 = d.r0;
-        if (C::HAS_V1 && v1src) {
-          lo = align16_down(v1src + d.r0);
-          nb = span16(v1src + d.r0, v1src + d.r1);
-          d.rb = d.r0 - (int)((v1src + d.r0) - reinterpret_cast<const double*>(lo));
-          tma_load(base + C::V1_OFF, lo, nb, &full[q], pol);
-          tx += nb;
-        }
-        if (C::HAS_V2) {
-          lo = align16_down(a.pv + d.r0);
-          nb = span16(a.pv + d.r0, a.pv + d.r1);
-          d.rb2 = d.r0 - (int)((a.pv + d.r0) - reinterpret_cast<const double*>(lo));
-          tma_load(base + C::V2_OFF, lo, nb, &full[q], pol);
-          tx += nb;
-        }
-        sdesc[q] = d;
-        mbar_expect_tx(&full[q], tx);
-        }
-        __syncwarp();
-      }
-      dl = nl;
-      dx = nx;
-    }
-  } else {
-    // ------------------------------ consumers -----------------------------------------------
-    for (int j = 0; j < my_tiles; ++j) {
-      const int q = j % NST;
-      mbar_wait(&full[q], (unsigned)(j / NST) & 1u);
-      const StageDesc d = sdesc[q];
-      double* V = reinterpret_cast<double*>(smem + q * C::BYTES + C::V_OFF);
-      const int32_t* I = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::I_OFF);
-      const int32_t* P = reinterpret_cast<const int32_t*>(smem + q * C::BYTES + C::P_OFF);
-      const double* V1 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V1_OFF);
-      const double* V2 = reinterpret_cast<const double*>(smem + q * C::BYTES + C::V2_OFF);
-      // this warp's rows: first entry in [s0 + warp*SUBW, s0 + (warp+1)*SUBW) (last warp: to r1)
-      int wr0, wr1;
-      {
-        const long long lo_key = (long long)d.s0 + (long long)warp * SUBW;
-        const long long hi_key = (long long)d.s0 + (long long)(warp + 1) * SUBW;
-        int lo = d.r0, hi = d.r1;
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (P[mid - d.pb] < lo_key) lo = mid + 1; else hi = mid; }
-        wr0 = (warp == 0) ? d.r0 : lo;
-        lo = wr0; hi = d.r1;
-        if (warp == NCW - 1) lo = d.r1;
-        else while (lo < hi) { const int mid = (lo + hi) >> 1; if (P[mid - d.pb] < hi_key) lo = mid + 1; else hi = mid; }
-        wr1 = lo;
-      }
-      if (wr0 < wr1) {
-        // products in place over the warp's staged entries
-        const int e0 = P[wr0 - d.pb];
-        const int e1 = min(P[wr1 - d.pb], d.se);
-        const int voff = -d.vb, ioff = -d.ib;
-        for (int k0 = e0; k0 < e1; k0 += 32 * WUNR) {
-          int32_t c[WUNR];
-          double v[WUNR], gv[WUNR];
-#pragma unroll
-          for (int u = 0; u < WUNR; ++u) {
-            const int k = k0 + lane + u * 32;
-            if (k < e1) { c[u] = I[k + ioff]; v[u] = V[k + voff]; }
-          }
-#pragma unroll
-          for (int u = 0; u < WUNR; ++u) {
-            const int k = k0 + lane + u * 32;
-            if (k < e1) gv[u] = __ldg(a.g + c[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < WUNR; ++u) {
-            const int k = k0 + lane + u * 32;
-            if (k < e1) V[k + voff] = __dmul_rn(v[u], gv[u]);
-          }
-        }
-        __syncwarp();
-        const int vsh = -d.vb;
-        for (int rb = wr0; rb < wr1; rb += 32) {
-          const int i = rb + lane;
-          const bool valid = i < wr1;
-          int b = 0, e = 0;
-          if (valid) { b = P[i - d.pb]; e = P[i + 1 - d.pb]; }
-          const bool lng = valid && (e - b) > LONGROW;
-          double s = 0.0;
-          if (ROLE >= ROLE_K2 && valid && a.accumulate) s = V1[i - d.rb];
-          if (valid && !lng) {
-            for (int k = b; k < e; ++k) {
-              const double pr = (k < d.se) ? V[k + vsh]
-                                           : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
-              s = __dadd_rn(s, pr);
-            }
-          }
-          unsigned mask = __ballot_sync(FULL, lng);
-          while (mask) {                                        // warp-cooperative long rows
-            const int l = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int lb = __shfl_sync(FULL, b, l), le = __shfl_sync(FULL, e, l);
-            double ps = 0.0;
-            for (int k = lb + lane; k < le; k += 32) {
-              const double pr = (k < d.se) ? V[k + vsh]
-                                           : __dmul_rn(ld_stream(a.val + k, pol), __ldg(a.g + ld_stream(a.idx + k, pol)));
-              ps = __dadd_rn(ps, pr);
-            }
-            ps = warp_sum(ps);
-            if (lane == l) s = __dadd_rn(s, ps);
-          }
-          if (valid) {
-            if (ROLE == ROLE_PLAIN) {
-              a.out[i] = s;
-            } else if (ROLE == ROLE_K1) {
-              const double rn = __dsub_rn(V1[i - d.rb], s);      // r_i <- r_i - (A p)_i
-              a.out[i] = rn;
-              acc0 = fma(rn, rn, acc0);
-            } else {
-              a.out[i] = s;                                     // y_j
-              if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[q]);                    // stage q released by this warp
-    }
-  }
-  if (ROLE == ROLE_PLAIN || ROLE == ROLE_K2) return;           // nothing to reduce
-  __syncthreads();
-  if (!a.finalize) {                                            // slab s < S-1: publish only
-    block_sum2(acc0, acc1, sm);
-    if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
-    return;
-  }
-  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
-  if (tid != 0) return;
-  if (ROLE == ROLE_K1) {
-    if (a.dist) *a.rho_out = acc0;                              // local rho -> all-reduce buffer
-    else tail_rho(a.ctl, a.rec, acc0);
-  } else if (ROLE == ROLE_K2DOTS) {
-    tail_y(a.ctl, a.rec, acc0, acc1);
-  }
-}
-
-#endif
 
 // ---------------------------------------------------------------------------------------------
 // K1 / K2 / plain SpMV over SELL-32 (sliced ELLPACK, slices of 32 rows, sigma-sorted by length
@@ -1293,7 +623,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   __shared__ int s_next;
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = a.pol_first;
   double acc0 = 0.0, acc1 = 0.0;
   int sl0, sl1, stride;
   if (!DYN) {
@@ -1446,7 +776,7 @@ __global__ void __launch_bounds__(NTW, 1) k_sellw(SpmvSeg a) {
   if (warp == NWC) {
     // ---- producer: window loads -------------------------------------------------------------
     if (lane == 0) {
-      const uint64_t pol_g = policy_evict_last();
+      const uint64_t pol_g = a.pol_last;
       int cur = -1;                                  // lo of the window in the ring (-1: none)
       int waited = -1;                               // blocks <= waited (relative) are done
       auto wait_done = [&](int jj) {                 // wait until relative blocks <= jj are done
@@ -1490,7 +820,7 @@ __global__ void __launch_bounds__(NTW, 1) k_sellw(SpmvSeg a) {
     __syncwarp();
   } else {
     // ---- consumers: one slice at a time, in order; the next one's metadata in flight ----------
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = a.pol_first;
     int sl = sl0 + warp;                             // first slice: static
     int m0 = 0, m1 = 0, mrow = -1;
     int2 mw = make_int2(0, 0);
@@ -1877,6 +1207,11 @@ __global__ void k_set_nbd(Ctl* c, const double* nb2) {
 // ---------------------------------------------------------------------------------------------
 // setup kernels (once per ctx)
 // ---------------------------------------------------------------------------------------------
+__global__ void k_policies(uint64_t* out) {
+  out[0] = policy_evict_first();
+  out[1] = policy_evict_last();
+}
+
 __device__ __forceinline__ int lower_bound_pos(const int32_t* ptr, int nrows, long long key) {
   int lo = 0, hi = nrows;
   while (lo < hi) {

@@ -13,6 +13,6 @@ tail -c 3000 gpurun_out/bench_${TAG}.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_(sell|spmv|pxupdate|dots_tail|norm_b|set_nbd)' -c 400 --csv \
   --log-file gpurun_out/launches_${TAG}.csv python bench.py --ncu --steps 2 --warmup 1 > gpurun_out/ncu_list_${TAG}.log 2>&1
 echo "ncu list rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_sell|k_spmv|k_pxupdate' -s 17 -c 17 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_sell|k_spmv|k_pxupdate' -s 17 -c 5 \
   -o gpurun_out/prof_${TAG} -f python bench.py --ncu --steps 2 --warmup 1 > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "ncu full rc=$?"
