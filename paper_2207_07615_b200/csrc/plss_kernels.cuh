@@ -552,6 +552,12 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
 #endif
 constexpr int SU = PLSS_SU;             // steps (entries per lane) in flight
 constexpr int NSB = 16;                 // slices per window / CTA-range block
+constexpr int SIGMA = 256;              // rows per sigma-sort window (SELL-32 construction)
+constexpr int SPW = SIGMA / 32;         // slices per sigma window
+constexpr int YQ = 8;                   // fmt 3 K2: sigma windows staged in shared memory at once
+#ifndef PLSS_YSTAGE
+#define PLSS_YSTAGE 1
+#endif
 constexpr int SELL_MINB = PLSS_SELL_MINB;
 
 // Gather of g[c] (c = -1: padding). Ablation builds (timing experiments only, never correct):
@@ -619,8 +625,15 @@ template <int ROLE, int BS = NT>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
+  // fmt 3 K2 with a sigma perm: y results go through a per-sigma-window shared buffer (indexed by
+  // row, not slot) and the warp that completes a window writes its SIGMA values coalesced,
+  // instead of 32 scattered 8-byte stores per slice. In-flight slices (<= 32 + 1) span at most
+  // 6 windows, so YQ = 8 buffers are never reused while still filling.
+  constexpr bool YST = DYN && (ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && PLSS_YSTAGE;
   __shared__ double sm[2][MAXW];
   __shared__ int s_next;
+  __shared__ double s_y[YST ? YQ : 1][YST ? SIGMA : 1];
+  __shared__ int s_ycnt[YST ? YQ : 1];
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = a.pol_first;
@@ -631,6 +644,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   } else {
     sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices); stride = BS / 32;
     if (tid == 0) s_next = sl0 + BS / 32;           // slices sl0 .. sl0+31 are taken statically
+    if (YST && tid < YQ) s_ycnt[tid] = 0;
     __syncthreads();
   }
   int sl = sl0 + warp;
@@ -641,7 +655,12 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   };
   if (sl < sl1) meta(sl);
   while (sl < sl1) {
-    const int st0 = m0, L = m1 - m0, row = mrow;
+    const int st0 = m0, L = m1 - m0;
+#if PLSS_ABLATE & 64
+    const int row = (ROLE >= ROLE_K2 && mrow >= 0) ? min(sl * 32 + lane, a.nrows - 1) : mrow;  // ablation: y coalesced
+#else
+    const int row = mrow;
+#endif
     int nx;
     if (!DYN) {
       nx = sl + stride;
@@ -670,9 +689,30 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #if PLSS_ABLATE & 32
         if (s == 1234.5) a.out[row] = s;                        // ablation: no y write
 #else
-        a.out[row] = s;                                         // y_j
+        if (YST && a.perm) s_y[(sl / SPW) % YQ][row % SIGMA] = s;   // staged (row - window base)
+        else a.out[row] = s;                                    // y_j
 #endif
         if (ROLE == ROLE_K2DOTS) { d0 = s * s; d1 = s * a.pv[row]; }
+      }
+    }
+    if (YST && a.perm) {
+      const int w = sl / SPW, q = w % YQ;
+      const int nsw = min(SPW, a.nslices - w * SPW);           // slices of this sigma window
+      __threadfence_block();                                    // this warp's s_y stores before the count
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&s_ycnt[q], 1) == nsw - 1;
+      last = __shfl_sync(FULL, last, 0);
+      if (last) {                                               // window complete: write it out
+        __threadfence_block();                                  // the other warps' s_y stores are visible
+        const int r0 = w * SIGMA;
+#pragma unroll
+        for (int u = 0; u < SIGMA / 32; ++u) {
+          const int r = r0 + u * 32 + lane;
+          if (r < a.nrows) a.out[r] = s_y[q][u * 32 + lane];
+        }
+        __syncwarp();
+        if (lane == 0) s_ycnt[q] = 0;
       }
     }
     if (DOTS) {
@@ -1056,7 +1096,6 @@ __global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
   if (i < nrows) len[i] = ptr[i + 1] - ptr[i];
 }
 // sigma-sort: within each window of SIGMA rows, slots ordered by length descending (stable)
-constexpr int SIGMA = 256;
 __global__ void __launch_bounds__(SIGMA) k_sigma_sort(const int32_t* len, long long nrows, long long nslots,
                                                       int32_t* perm) {
   __shared__ int32_t sl[SIGMA];
