@@ -446,7 +446,7 @@ static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool
   const int32_t* use_perm = nullptr;
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
-      k_sigma_sort<<<(unsigned)((nrows + SIGMA - 1) / SIGMA), SIGMA, 0, st>>>(len, nrows, nsl * 32, perm);
+      k_sigma_sort<<<(unsigned)((nrows + SIGMA - 1) / SIGMA), SIGMA_NT, 0, st>>>(len, nrows, nsl * 32, perm);
       use_perm = perm;
     }
     k_slice_len<<<gs, 256, 0, st>>>(len, use_perm, nrows, nsl, sp);

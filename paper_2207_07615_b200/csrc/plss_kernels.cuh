@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cub/block/block_radix_sort.cuh>
 
 namespace plss {
 
@@ -551,10 +552,17 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
 #define PLSS_SELL_MINB 4
 #endif
 constexpr int SU = PLSS_SU;             // steps (entries per lane) in flight
-constexpr int NSB = 16;                 // slices per window / CTA-range block
-constexpr int SIGMA = 256;              // rows per sigma-sort window (SELL-32 construction)
+#ifndef PLSS_SIGMA
+#define PLSS_SIGMA 256
+#endif
+constexpr int SIGMA = PLSS_SIGMA;       // rows per sigma-sort window (SELL-32 construction; C5's K2
+                                        // slabs: 57% padding unsorted, 9.4% at 256, 2.9% at 1024,
+                                        // yet 1024 runs 5% slower: coarser windows cost locality)
 constexpr int SPW = SIGMA / 32;         // slices per sigma window
-constexpr int YQ = 8;                   // fmt 3 K2: sigma windows staged in shared memory at once
+// slices per CTA-range block of fmt 3 (a multiple of the sigma window: a window's y staging
+// counter lives in one CTA's shared memory)
+constexpr int NSB = SPW > 16 ? SPW : 16;
+constexpr int YQ = SIGMA >= 1024 ? 4 : 8;   // fmt 3 K2: sigma windows staged in shared memory
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
 #endif
@@ -1096,21 +1104,28 @@ __global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
   if (i < nrows) len[i] = ptr[i + 1] - ptr[i];
 }
 // sigma-sort: within each window of SIGMA rows, slots ordered by length descending (stable)
-__global__ void __launch_bounds__(SIGMA) k_sigma_sort(const int32_t* len, long long nrows, long long nslots,
-                                                      int32_t* perm) {
-  __shared__ int32_t sl[SIGMA];
+constexpr int SIGMA_NT = 256;            // threads of the sigma-sort kernel
+__global__ void __launch_bounds__(SIGMA_NT) k_sigma_sort(const int32_t* len, long long nrows, long long nslots,
+                                                         int32_t* perm) {
+  // stable radix sort of the window by (length descending, row ascending); missing rows last
+  constexpr int IPT = SIGMA / SIGMA_NT;
+  using Sort = cub::BlockRadixSort<unsigned, SIGMA_NT, IPT, int32_t>;
+  __shared__ typename Sort::TempStorage tmp;
   const long long w0 = (long long)blockIdx.x * SIGMA;
-  const int t = threadIdx.x;
-  const long long i = w0 + t;
-  sl[t] = i < nrows ? len[i] : -1;                               // missing rows sort last
-  __syncthreads();
-  const int mine = sl[t];
-  int rank = 0;
-  for (int q = 0; q < SIGMA; ++q) {
-    const int o = sl[q];
-    rank += (o > mine) || (o == mine && q < t);
+  unsigned key[IPT];
+  int32_t val[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const long long i = w0 + (long long)threadIdx.x * IPT + k;     // blocked arrangement
+    key[k] = i < nrows ? 0x7fffffffu - (unsigned)len[i] : 0xffffffffu;
+    val[k] = i < nrows ? (int32_t)i : -1;
   }
-  if (w0 + rank < nslots) perm[w0 + rank] = i < nrows ? (int32_t)i : -1;
+  Sort(tmp).Sort(key, val);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const long long o = w0 + (long long)threadIdx.x * IPT + k;
+    if (o < nslots) perm[o] = val[k];
+  }
 }
 __global__ void k_slice_len(const int32_t* len, const int32_t* perm, long long nrows, long long nslices,
                             int32_t* slen) {
