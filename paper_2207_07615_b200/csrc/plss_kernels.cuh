@@ -562,7 +562,10 @@ constexpr int SPW = SIGMA / 32;         // slices per sigma window
 // slices per CTA-range block of fmt 3 (a multiple of the sigma window: a window's y staging
 // counter lives in one CTA's shared memory)
 constexpr int NSB = SPW > 16 ? SPW : 16;
-constexpr int YQ = SIGMA >= 1024 ? 4 : 8;   // fmt 3 K2: sigma windows staged in shared memory
+#ifndef PLSS_PAIR
+#define PLSS_PAIR 1                     // fmt 3: consecutive slices a warp sums together
+#endif
+constexpr int YQ = (SIGMA >= 1024 ? 4 : 8) * PLSS_PAIR;  // fmt 3 K2: sigma windows staged in smem
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
 #endif
@@ -620,6 +623,41 @@ __device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L,
   return s;
 }
 
+// P slices at once (fmt 3): lane l sums row l of each of P consecutive slices, SU/P steps of each
+// in flight per batch, so the latency chains of P rows overlap and per-slice costs are shared.
+template <int ROLE, int P>
+__device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)[P], const int (&L)[P], int lane,
+                                              const int (&row)[P], double (&s)[P], uint64_t pol) {
+  constexpr int SUP = SU / P;
+  int Lmax = 0;
+#pragma unroll
+  for (int q = 0; q < P; ++q) Lmax = max(Lmax, L[q]);
+  for (int j = 0; j < Lmax; j += SUP) {
+    int32_t c[P][SUP];
+    double v[P][SUP], gv[P][SUP];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int u = 0; u < SUP; ++u) {
+        c[q][u] = -1;
+        if (j + u < L[q]) {
+          const long long e = ((long long)st0[q] + j + u) * 32 + lane;
+          c[q][u] = ld_stream(a.idx + e, pol);
+          v[q][u] = ld_stream(a.val + e, pol);
+        }
+      }
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int u = 0; u < SUP; ++u) gv[q][u] = sell_gather(a, c[q][u], row[q], ROLE);
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int u = 0; u < SUP; ++u)
+        if (c[q][u] >= 0) s[q] = __dadd_rn(s[q], __dmul_rn(v[q][u], gv[q][u]));
+  }
+}
+
 // BS = NT (fmt 1): persistent grid, slices dealt round-robin over all warps of the grid; each
 //   thread accumulates its rows' dot contributions (static assignment: deterministic).
 // BS = 1024 (fmt 3): one CTA per SM walks the contiguous, entry-balanced slice range
@@ -633,11 +671,13 @@ template <int ROLE, int BS = NT>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
+  constexpr int P = DYN ? PLSS_PAIR : 1;         // slices per warp unit
   // fmt 3 K2 with a sigma perm: y results go through a per-sigma-window shared buffer (indexed by
   // row, not slot) and the warp that completes a window writes its SIGMA values coalesced,
-  // instead of 32 scattered 8-byte stores per slice. In-flight slices (<= 32 + 1) span at most
-  // 6 windows, so YQ = 8 buffers are never reused while still filling.
+  // instead of 32 scattered 8-byte stores per slice. In-flight slices (<= 32 P + P) span at most
+  // YQ - 2 windows, so the buffers are never reused while still filling.
   constexpr bool YST = DYN && (ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && PLSS_YSTAGE;
+  static_assert(SPW % P == 0 && NSB % P == 0, "a warp unit must not straddle a sigma window");
   __shared__ double sm[2][MAXW];
   __shared__ int s_next;
   __shared__ double s_y[YST ? YQ : 1][YST ? SIGMA : 1];
@@ -650,66 +690,100 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   if (!DYN) {
     sl0 = blockIdx.x * (NT / 32); sl1 = a.nslices; stride = gridDim.x * (NT / 32);
   } else {
-    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices); stride = BS / 32;
-    if (tid == 0) s_next = sl0 + BS / 32;           // slices sl0 .. sl0+31 are taken statically
+    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices); stride = P * BS / 32;
+    if (tid == 0) s_next = sl0 + P * (BS / 32);     // the first unit of each warp is static
     if (YST && tid < YQ) s_ycnt[tid] = 0;
     __syncthreads();
   }
-  int sl = sl0 + warp;
-  int m0 = 0, m1 = 0, mrow = -1;
+  int su = sl0 + warp * P;                          // first slice of this warp's unit
+  int m0[P], m1[P], mrow[P];
   auto meta = [&](int t) {
-    m0 = a.sptr[t]; m1 = a.sptr[t + 1];
-    mrow = a.perm ? a.perm[t * 32 + lane] : t * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      if (t + q < sl1) {
+        m0[q] = a.sptr[t + q]; m1[q] = a.sptr[t + q + 1];
+        mrow[q] = a.perm ? a.perm[(t + q) * 32 + lane] : (t + q) * 32 + lane;
+      } else {
+        m0[q] = 0; m1[q] = 0; mrow[q] = -1;
+      }
+    }
   };
-  if (sl < sl1) meta(sl);
-  while (sl < sl1) {
-    const int st0 = m0, L = m1 - m0;
+  if (su < sl1) meta(su);
+  while (su < sl1) {
+    int st0[P], L[P], row[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      st0[q] = m0[q]; L[q] = m1[q] - m0[q];
 #if PLSS_ABLATE & 64
-    const int row = (ROLE >= ROLE_K2 && mrow >= 0) ? min(sl * 32 + lane, a.nrows - 1) : mrow;  // ablation: y coalesced
+      row[q] = (ROLE >= ROLE_K2 && mrow[q] >= 0) ? min((su + q) * 32 + lane, a.nrows - 1) : mrow[q];
 #else
-    const int row = mrow;
+      row[q] = mrow[q];
 #endif
+    }
+    const int cnt = min(P, sl1 - su);               // slices of this unit that exist
     int nx;
     if (!DYN) {
-      nx = sl + stride;
+      nx = su + stride;
     } else {
       nx = 0;
-      if (lane == 0) nx = atomicAdd(&s_next, 1);
+      if (lane == 0) nx = atomicAdd(&s_next, P);
       nx = __shfl_sync(FULL, nx, 0);
     }
     if (nx < sl1) meta(nx);
-    const bool valid = row >= 0 && row < a.nrows;
-    double s = 0.0;
+    bool valid[P];
+    double s[P], r_old[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      valid[q] = row[q] >= 0 && row[q] < a.nrows;
+      s[q] = 0.0;
 #if !(PLSS_ABLATE & 32)
-    if (ROLE >= ROLE_K2 && valid && a.accumulate) s = a.out[row];
+      if (ROLE >= ROLE_K2 && valid[q] && a.accumulate) s[q] = a.out[row[q]];
 #endif
-    const double r_old = (ROLE == ROLE_K1 && valid) ? a.out[row] : 0.0;   // issued early
-    s = sell_row_sum<ROLE>(a, st0, L, lane, row, s, pol);
-    double d0 = 0.0, d1 = 0.0;
-    if (valid) {
-      if (ROLE == ROLE_PLAIN) {
-        a.out[row] = s;
-      } else if (ROLE == ROLE_K1) {
-        const double rn = __dsub_rn(r_old, s);                  // r_i <- r_i - (A p)_i
-        a.out[row] = rn;
-        d0 = rn * rn;
-      } else {
+      r_old[q] = (ROLE == ROLE_K1 && valid[q]) ? a.out[row[q]] : 0.0;   // issued early
+    }
+    if (P == 1) {
+      s[0] = sell_row_sum<ROLE>(a, st0[0], L[0], lane, row[0], s[0], pol);
+    } else {
+      sell_rows_sum<ROLE, P>(a, st0, L, lane, row, s, pol);
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      if (q >= cnt) break;
+      double d0 = 0.0, d1 = 0.0;
+      if (valid[q]) {
+        if (ROLE == ROLE_PLAIN) {
+          a.out[row[q]] = s[q];
+        } else if (ROLE == ROLE_K1) {
+          const double rn = __dsub_rn(r_old[q], s[q]);          // r_i <- r_i - (A p)_i
+          a.out[row[q]] = rn;
+          d0 = rn * rn;
+        } else {
 #if PLSS_ABLATE & 32
-        if (s == 1234.5) a.out[row] = s;                        // ablation: no y write
+          if (s[q] == 1234.5) a.out[row[q]] = s[q];             // ablation: no y write
 #else
-        if (YST && a.perm) s_y[(sl / SPW) % YQ][row % SIGMA] = s;   // staged (row - window base)
-        else a.out[row] = s;                                    // y_j
+          if (YST && a.perm) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = s[q];  // staged (row - window base)
+          else a.out[row[q]] = s[q];                            // y_j
 #endif
-        if (ROLE == ROLE_K2DOTS) { d0 = s * s; d1 = s * a.pv[row]; }
+          if (ROLE == ROLE_K2DOTS) { d0 = s[q] * s[q]; d1 = s[q] * a.pv[row[q]]; }
+        }
+      }
+      if (DOTS) {
+        if (!DYN) {
+          acc0 += d0; acc1 += d1;
+        } else {
+          d0 = warp_sum(d0);
+          d1 = warp_sum(d1);
+          if (lane == 0) { a.slpart[2 * (su + q)] = d0; a.slpart[2 * (su + q) + 1] = d1; }
+        }
       }
     }
     if (YST && a.perm) {
-      const int w = sl / SPW, q = w % YQ;
+      const int w = su / SPW, qw = w % YQ;
       const int nsw = min(SPW, a.nslices - w * SPW);           // slices of this sigma window
       __threadfence_block();                                    // this warp's s_y stores before the count
       __syncwarp();
       int last = 0;
-      if (lane == 0) last = atomicAdd(&s_ycnt[q], 1) == nsw - 1;
+      if (lane == 0) last = atomicAdd(&s_ycnt[qw], cnt) + cnt == nsw;
       last = __shfl_sync(FULL, last, 0);
       if (last) {                                               // window complete: write it out
         __threadfence_block();                                  // the other warps' s_y stores are visible
@@ -717,22 +791,13 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #pragma unroll
         for (int u = 0; u < SIGMA / 32; ++u) {
           const int r = r0 + u * 32 + lane;
-          if (r < a.nrows) a.out[r] = s_y[q][u * 32 + lane];
+          if (r < a.nrows) a.out[r] = s_y[qw][u * 32 + lane];
         }
         __syncwarp();
-        if (lane == 0) s_ycnt[q] = 0;
+        if (lane == 0) s_ycnt[qw] = 0;
       }
     }
-    if (DOTS) {
-      if (!DYN) {
-        acc0 += d0; acc1 += d1;
-      } else {
-        d0 = warp_sum(d0);
-        d1 = warp_sum(d1);
-        if (lane == 0) { a.slpart[2 * sl] = d0; a.slpart[2 * sl + 1] = d1; }
-      }
-    }
-    sl = nx;
+    su = nx;
   }
   if (!DOTS) return;
   if (DYN) {
