@@ -1169,7 +1169,7 @@ __global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
   if (i < nrows) len[i] = ptr[i + 1] - ptr[i];
 }
 // sigma-sort: within each window of SIGMA rows, slots ordered by length descending (stable)
-constexpr int SIGMA_NT = 256;            // threads of the sigma-sort kernel
+constexpr int SIGMA_NT = SIGMA < 256 ? SIGMA : 256;   // threads of the sigma-sort kernel
 __global__ void __launch_bounds__(SIGMA_NT) k_sigma_sort(const int32_t* len, long long nrows, long long nslots,
                                                          int32_t* perm) {
   // stable radix sort of the window by (length descending, row ascending); missing rows last
