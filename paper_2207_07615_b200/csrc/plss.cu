@@ -51,6 +51,8 @@ struct Layout {
       scratch_blk, sptr, sidx, sval, scan_cnt, scan_blk, buf, err, scalars, total;
   bool sell = true;
   size_t s1idx, s1val, s1perm, s1sptr, s2idx, s2val, s2perm, s2sptr, s1win, s2win, cblk, slpart;
+  size_t s1aux, s2aux;           // globally sorted segments: long-row lists + unit-weight prefixes
+  int64_t s1auxn, s2auxn;
   bool window = true;
   int64_t s1cap, s2cap, s1slots, s2slots, s1sp, s2sp;  // pool capacities (entries / slots / sptr)
 };
@@ -106,7 +108,12 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
     L->s1win = take(8 * (size_t)(L->s1sp / 4 + 2 * S + 2));     // window blocks: nsb >= 4 slices
     L->s2win = take(8 * (size_t)(L->s2sp / 4 + 2 * S + 2));
     L->cblk = take(4 * (size_t)(MAXG + 1) * 2 * S);
-    L->slpart = take(16 * (size_t)(std::max(m, n) / 32 + 2));
+    // units of one segment: slices + long rows (<= nnz / (LONGROW + 1) of them)
+    L->slpart = take(16 * (size_t)(std::max(m, n) / 32 + nnz / (LONGROW + 1) + 4));
+    L->s1auxn = 2 * (m / 32 + nnz / (LONGROW + 1) + 4 * S + 8);
+    L->s2auxn = 2 * ((int64_t)S * (n / 32) + nnz / (LONGROW + 1) + 4 * S + 8);
+    L->s1aux = take(4 * (size_t)L->s1auxn);
+    L->s2aux = take(4 * (size_t)L->s2auxn);
   }
   L->scratch_blk = take(4 * (size_t)((std::max(m, n) + 2) / (NT * SCAN_ITEMS) + 2));
   if (S > 1) {
@@ -232,6 +239,8 @@ template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
   if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
+  else if (a.fmt == 3 && a.nlong > 0)
+    k_sell<ROLE, 1024, true><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 3)
     k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 1)
@@ -352,6 +361,8 @@ struct SellPool {
   int64_t wcap, used_w;
   int32_t* cblk;               // CTA block ranges (MAXG+1 per segment)
   int64_t used_c;
+  int32_t* aux;                // long-row lists and unit-weight prefixes (global-sort segments)
+  int64_t auxn, used_aux;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -364,10 +375,14 @@ static int env_int(const char* name, int dflt) {
 // One 1024-thread CTA per SM over contiguous entry-balanced slice ranges (fmt 3).
 static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sms, int* grid_out) {
   if (a.fmt != 1) return PLSS_OK;
-  const int nblocks = (a.nslices + NSB - 1) / NSB;
+  const int nunits = a.nslices + a.nlong;
+  const int nblocks = (nunits + NSB - 1) / NSB;
   const int grid = std::max(1, std::min(std::min(nblocks, sms), MAXG));
   int32_t* cblk = pool.cblk + pool.used_c;
-  k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.sptr, a.nslices, NSB, nblocks, grid, cblk);
+  if (a.uw)
+    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk);
+  else
+    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.sptr, 32, nunits, NSB, nblocks, grid, cblk);
   CK(cudaGetLastError());
   pool.used_c += MAXG + 1;
   a.cblk = cblk;
@@ -380,7 +395,7 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
 static plss_status try_window(plss_ctx* ctx, SpmvSeg& a, const double* g, int64_t glen, int64_t nnz_seg,
                               int win, int nsb, SellPool& pool, int sms, int* grid_out) {
   cudaStream_t st = ctx->stream;
-  if (a.fmt != 1 || win <= 0 || nnz_seg == 0) return PLSS_OK;
+  if (a.fmt != 1 || a.gsort || win <= 0 || nnz_seg == 0) return PLSS_OK;
   win &= ~7;
   if (glen - 2 < win) win = (int)((glen - 2) & ~7ll);
   if (win < 256) return PLSS_OK;
@@ -409,7 +424,7 @@ static plss_status try_window(plss_ctx* ctx, SpmvSeg& a, const double* g, int64_
   CK(cudaStreamSynchronize(st));
   if ((double)cov < 0.1 * (double)nnz_seg) return PLSS_OK;          // too little locality
   int32_t* cblk = pool.cblk + pool.used_c;
-  k_cta_ranges<<<(grid + 256) / 256, 256, 0, st>>>(a.sptr, a.nslices, nsb, nblocks, grid, cblk);
+  k_cta_ranges<<<(grid + 256) / 256, 256, 0, st>>>(a.sptr, 32, a.nslices, nsb, nblocks, grid, cblk);
   k_win_chain<<<(grid + 255) / 256, 256, 0, st>>>(wlo, cblk, grid, win, ring);
   CK(cudaGetLastError());
   a.cblk = cblk;
@@ -429,6 +444,87 @@ static plss_status try_window(plss_ctx* ctx, SpmvSeg& a, const double* g, int64_
 
 // Convert one segment (CSR-like: ptr[nrows+1] absolute positions, idx, val) to SELL-32 if the
 // padding stays small: unsorted when rows are (nearly) uniform, else sigma-sorted windows of 256.
+// Rows too irregular for windowed sigma sorting (power-law lengths): sort ALL rows of the segment
+// by length (setup only, on the host: a stable counting sort), put rows of <= LONGROW entries into
+// SELL-32 slices (padding from equal-length neighbours only) and make every longer row a warp unit
+// (fmt 3 only; its sum is a fixed lane-strided tree, like the CSR-tile kernel's long rows).
+static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nrows = a.nrows;
+  if (PLSS_PAIR > 1 || !env_int("PLSS_GSORT", 1)) return PLSS_OK;   // long-row units: one slice per unit
+  std::vector<int32_t> len(nrows);
+  CK(cudaMemcpyAsync(len.data(), ctx->ws + ctx->L.scratch, 4 * (size_t)nrows, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> cnt(LONGROW + 2, 0);
+  std::vector<int32_t> lrows;
+  for (int64_t i = 0; i < nrows; ++i) {
+    if (len[i] > LONGROW) lrows.push_back((int32_t)i); else cnt[len[i]]++;
+  }
+  const int64_t nshort = nrows - (int64_t)lrows.size();
+  const int64_t nsl = (nshort + 31) / 32;
+  const int64_t nunits = nsl + (int64_t)lrows.size();
+  if (pool.used_slots + nsl * 32 > pool.slots || pool.used_sp + nsl + 1 > pool.sp ||
+      pool.used_aux + (int64_t)lrows.size() + nunits + 1 > pool.auxn)
+    return PLSS_OK;
+  // stable counting sort, length descending
+  std::vector<int64_t> off(LONGROW + 2, 0);
+  for (int l = LONGROW, acc = 0; l >= 0; --l) { off[l] = acc; acc += (int)cnt[l]; }
+  std::vector<int32_t> perm(nsl * 32, -1);
+  for (int64_t i = 0; i < nrows; ++i)
+    if (len[i] <= LONGROW) perm[off[len[i]]++] = (int32_t)i;
+  std::vector<int32_t> sp(nsl + 1, 0), uw(nunits + 1, 0);
+  int64_t steps = 0, stored = 0;
+  for (int64_t s2 = 0; s2 < nsl; ++s2) {
+    sp[s2] = (int32_t)steps;
+    uw[s2] = (int32_t)stored;
+    const int32_t r = perm[s2 * 32];
+    const int64_t L = r >= 0 ? len[r] : 0;          // longest row of the slice (sorted)
+    steps += L;
+    stored += 32 * L;
+  }
+  sp[nsl] = (int32_t)steps;
+  for (size_t k = 0; k < lrows.size(); ++k) {
+    uw[nsl + k] = (int32_t)stored;
+    stored += len[lrows[k]];
+  }
+  uw[nunits] = (int32_t)stored;
+  if (stored >= (1ll << 31) || pool.used + steps * 32 > pool.cap) return PLSS_OK;
+  if ((double)(steps * 32) > 1.15 * (double)nnz_seg + 32.0 * 32 * (LONGROW + 1)) return PLSS_OK;
+  int32_t* d_perm = pool.perm + pool.used_slots;
+  int32_t* d_sp = pool.sptr + pool.used_sp;
+  int32_t* d_lrows = pool.aux + pool.used_aux;
+  int32_t* d_uw = d_lrows + lrows.size();
+  CK(cudaMemcpyAsync(d_perm, perm.data(), 4 * perm.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_sp, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice, st));
+  if (!lrows.empty()) CK(cudaMemcpyAsync(d_lrows, lrows.data(), 4 * lrows.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_uw, uw.data(), 4 * uw.size(), cudaMemcpyHostToDevice, st));
+  int32_t* sidx = pool.idx + pool.used;
+  double* sval = pool.val + pool.used;
+  if (nsl > 0)
+    k_sell_fill<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, st>>>(a.ptr, a.idx, a.val, d_perm, nrows, nsl, d_sp,
+                                                                    sidx, sval);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));                    // the host vectors go out of scope
+  a.fmt = 1;
+  a.gsort = 1;
+  a.nslices = (int32_t)nsl;
+  a.sptr = d_sp;
+  a.perm = d_perm;
+  a.nlong = (int32_t)lrows.size();
+  a.lrows = d_lrows;
+  a.lptr = a.ptr;
+  a.lidx = a.idx;
+  a.lval = a.val;
+  a.uw = d_uw;
+  a.idx = sidx;
+  a.val = sval;
+  pool.used += steps * 32;
+  pool.used_slots += nsl * 32;
+  pool.used_sp += nsl + 1;
+  pool.used_aux += (int64_t)lrows.size() + nunits + 1;
+  return PLSS_OK;
+}
+
 static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool, int sms, int occ) {
   cudaStream_t st = ctx->stream;
   const int64_t nrows = a.nrows;
@@ -459,7 +555,7 @@ static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool
     const int64_t padded = steps * 32 - (nsl * 32 - nrows) * (int64_t)(tot[1] - tot[0]);
     const double limit = pass == 0 ? 1.03 : 1.15;
     if ((double)padded <= limit * (double)nnz_seg + 1024.0) break;
-    if (pass == 1) return PLSS_OK;                    // too irregular: stay on CSR tiles
+    if (pass == 1) return try_sell_global(ctx, a, nnz_seg, pool);   // power-law rows
   }
   if (pool.used + steps * 32 > pool.cap) return PLSS_OK;
   int32_t* sidx = pool.idx + pool.used;
@@ -584,11 +680,13 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (L.sell) {
     pool1 = SellPool{(int32_t*)(w + L.s1idx), (int32_t*)(w + L.s1perm), (int32_t*)(w + L.s1sptr),
                      (double*)(w + L.s1val), L.s1cap, L.s1slots, L.s1sp, 0, 0, 0,
-                     (int2*)(w + L.s1win), L.s1sp / 4 + 2 * S + 2, 0, (int32_t*)(w + L.cblk), 0};
+                     (int2*)(w + L.s1win), L.s1sp / 4 + 2 * S + 2, 0, (int32_t*)(w + L.cblk), 0,
+                     (int32_t*)(w + L.s1aux), L.s1auxn, 0};
     pool2 = SellPool{(int32_t*)(w + L.s2idx), (int32_t*)(w + L.s2perm), (int32_t*)(w + L.s2sptr),
                      (double*)(w + L.s2val), L.s2cap, L.s2slots, L.s2sp, 0, 0, 0,
                      (int2*)(w + L.s2win), L.s2sp / 4 + 2 * S + 2, 0,
-                     (int32_t*)(w + L.cblk) + (size_t)(MAXG + 1) * S, 0};
+                     (int32_t*)(w + L.cblk) + (size_t)(MAXG + 1) * S, 0,
+                     (int32_t*)(w + L.s2aux), L.s2auxn, 0};
     // windowed kernels: up to ~200 KB of dynamic shared memory for the ring
     CK(cudaFuncSetAttribute(k_sellw<ROLE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_sellw<ROLE_K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -664,7 +762,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
       if (a.fmt == 1) ctx->g1[s] = sell_grid(a);
       if (try_window(ctx, a, ctx->p, n, ctx->E[s + 1] - ctx->E[s], win1, nsb1, pool1, sms, &ctx->g1[s]) != PLSS_OK)
         return PLSS_E_CUDA;
-      if (contig >= 1 && make_contig(ctx, a, pool1, sms, &ctx->g1[s]) != PLSS_OK) return PLSS_E_CUDA;
+      if ((contig >= 1 || a.gsort) && make_contig(ctx, a, pool1, sms, &ctx->g1[s]) != PLSS_OK) return PLSS_E_CUDA;
     }
   }
 
@@ -727,7 +825,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
       if (try_window(ctx, a, a.g, ctx->R[s + 1] - ctx->R[s], ctx->E[s + 1] - ctx->E[s], win2, nsb2, pool2, sms,
                      &ctx->g2[s]) != PLSS_OK)
         return PLSS_E_CUDA;
-      if (contig >= 2 && make_contig(ctx, a, pool2, sms, &ctx->g2[s]) != PLSS_OK) return PLSS_E_CUDA;
+      if ((contig >= 2 || a.gsort) && make_contig(ctx, a, pool2, sms, &ctx->g2[s]) != PLSS_OK) return PLSS_E_CUDA;
     }
   }
   CK(cudaGetLastError());

@@ -104,6 +104,15 @@ struct SpmvSeg {
   // ring of `ring` doubles in shared memory, every other entry from global memory
   int32_t win, ring, nblocks, glen, nsb;
   int32_t row0;              // first row of this segment in the matrix (ablation experiments only)
+  // Globally length-sorted SELL (power-law rows, fmt 3 only): perm is a global row order, rows
+  // longer than LONGROW are not in the slices but are warp units nslices .. nslices+nlong-1
+  // (row lrows[u - nslices], entries [lptr[row], lptr[row+1]) of the segment's CSR-like arrays).
+  int32_t gsort, nlong;
+  const int32_t* lrows;
+  const int32_t* lptr;
+  const int32_t* lidx;
+  const double* lval;
+  const int32_t* uw;         // nunits+1 prefix of stored entries per unit (CTA balance), or NULL
   // L2 cache policies (createpolicy values computed once at setup by k_policies). Passed as kernel
   // parameters they sit in uniform registers: a per-thread createpolicy result costs one R2UR
   // (XU pipe) per cache-hinted load, which saturated the XU pipe of K1 (profiles/r01_notes.md).
@@ -667,7 +676,7 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 //   slice order (deterministic).
 // Slice metadata (start, length, this lane's row) is loaded one slice ahead, so a slice's stream
 // loads wait for DRAM only, not for an L2 round trip to sptr / perm first.
-template <int ROLE, int BS = NT>
+template <int ROLE, int BS = NT, bool LU = false>     // LU: the segment has long-row units (gsort)
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
@@ -690,7 +699,8 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   if (!DYN) {
     sl0 = blockIdx.x * (NT / 32); sl1 = a.nslices; stride = gridDim.x * (NT / 32);
   } else {
-    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices); stride = P * BS / 32;
+    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices + (LU ? a.nlong : 0));
+    stride = P * BS / 32;
     if (tid == 0) s_next = sl0 + P * (BS / 32);     // the first unit of each warp is static
     if (YST && tid < YQ) s_ycnt[tid] = 0;
     __syncthreads();
@@ -700,7 +710,10 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   auto meta = [&](int t) {
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      if (t + q < sl1) {
+      if (LU && t + q < sl1 && t + q >= a.nslices) {   // long-row unit (gsort): whole warp, one row
+        const int r = a.lrows[t + q - a.nslices];
+        m0[q] = a.lptr[r]; m1[q] = a.lptr[r + 1]; mrow[q] = r;
+      } else if (t + q < sl1) {
         m0[q] = a.sptr[t + q]; m1[q] = a.sptr[t + q + 1];
         mrow[q] = a.perm ? a.perm[(t + q) * 32 + lane] : (t + q) * 32 + lane;
       } else {
@@ -741,7 +754,29 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #endif
       r_old[q] = (ROLE == ROLE_K1 && valid[q]) ? a.out[row[q]] : 0.0;   // issued early
     }
-    if (P == 1) {
+    const bool longu = LU && DYN && P == 1 && su >= a.nslices;   // warp-uniform
+    if (longu) {
+      // long row (> LONGROW entries): lane-strided partial sums, fixed butterfly, added to the
+      // row's start value (r for K1 is subtracted below; y of earlier slabs for K2)
+      double ps = 0.0;
+      for (int k0 = st0[0]; k0 < st0[0] + L[0]; k0 += 32 * SU) {
+        int32_t c[SU];
+        double v[SU], gv[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          const int k = k0 + u * 32 + lane;
+          c[u] = -1;
+          if (k < st0[0] + L[0]) { c[u] = ld_stream(a.lidx + k, pol); v[u] = ld_stream(a.lval + k, pol); }
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u], row[0], ROLE);
+#pragma unroll
+        for (int u = 0; u < SU; ++u) if (c[u] >= 0) ps = __dadd_rn(ps, __dmul_rn(v[u], gv[u]));
+      }
+      ps = warp_sum(ps);
+      s[0] = ROLE == ROLE_K1 ? ps : __dadd_rn(s[0], ps);
+      if (lane != 0) valid[0] = false;                    // lane 0 writes the row
+    } else if (P == 1) {
       s[0] = sell_row_sum<ROLE>(a, st0[0], L[0], lane, row[0], s[0], pol);
     } else {
       sell_rows_sum<ROLE, P>(a, st0, L, lane, row, s, pol);
@@ -761,7 +796,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #if PLSS_ABLATE & 32
           if (s[q] == 1234.5) a.out[row[q]] = s[q];             // ablation: no y write
 #else
-          if (YST && a.perm) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = s[q];  // staged (row - window base)
+          if (YST && a.perm && !a.gsort) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = s[q];  // staged
           else a.out[row[q]] = s[q];                            // y_j
 #endif
           if (ROLE == ROLE_K2DOTS) { d0 = s[q] * s[q]; d1 = s[q] * a.pv[row[q]]; }
@@ -777,7 +812,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
         }
       }
     }
-    if (YST && a.perm) {
+    if (YST && a.perm && !a.gsort) {
       const int w = su / SPW, qw = w % YQ;
       const int nsw = min(SPW, a.nslices - w * SPW);           // slices of this sigma window
       __threadfence_block();                                    // this warp's s_y stores before the count
@@ -1150,14 +1185,20 @@ __global__ void k_win_chain(int2* wlo, const int32_t* cblk, int grid, int win, i
 // CTA c of a windowed launch owns blocks [cblk[c], cblk[c+1]): the first block whose stored
 // entries start at or after c/grid of the segment's total (work balance when row lengths vary,
 // e.g. C5's K2 slabs where a band of columns holds 9x the entries of the rest).
-__global__ void k_cta_ranges(const int32_t* sptr, int nslices, int nsb, int nblocks, int grid, int32_t* cblk) {
-  const long long total = sptr[nslices];
+__global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, int nblocks, int grid,
+                             int32_t* cblk) {
+  // w: prefix over units (nunits+1 entries); unit cost = (w[u+1] - w[u]) * wscale + UNIT_COST
+  // (a unit also costs its metadata loads, row outputs and dot partial: without that term the
+  // empty slices of a segment -- C4's empty columns sort last -- all fall to the last CTA)
+  constexpr long long UNIT_COST = 32 * 4;
+  const long long total = (long long)w[nunits] * wscale + (long long)nunits * UNIT_COST;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= grid; c += gridDim.x * blockDim.x) {
     const long long target = (total * c + grid - 1) / grid;
     int lo = 0, hi = nblocks;                                   // first b with start(b) >= target
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if ((long long)sptr[min(mid * nsb, nslices)] < target) lo = mid + 1; else hi = mid;
+      const int u = min(mid * nsb, nunits);
+      if ((long long)w[u] * wscale + (long long)u * UNIT_COST < target) lo = mid + 1; else hi = mid;
     }
     cblk[c] = c == 0 ? 0 : c == grid ? nblocks : lo;
   }
