@@ -240,7 +240,9 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
   if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
   else if (a.fmt == 3 && a.nlong > 0)
-    k_sell<ROLE, 1024, true><<<grid, 1024, 0, st>>>(a);
+    k_sell<ROLE, 1024, true><<<grid, 1024, 0, st>>>(a);            // gsort: no y staging
+  else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort)     // K2 with a sigma perm: staged y
+    k_sell<ROLE, 1024, false, true><<<grid, 1024, YSTAGE_SMEM, st>>>(a);
   else if (a.fmt == 3)
     k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 1)
@@ -693,6 +695,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     CK(cudaFuncSetAttribute(k_sellw<ROLE_K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_sellw<ROLE_K2DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_win_choose, cudaFuncAttributeMaxDynamicSharedMemorySize, 16385 * 4));
+    CK(cudaFuncSetAttribute(k_sell<ROLE_K2, 1024, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            YSTAGE_SMEM));
+    CK(cudaFuncSetAttribute(k_sell<ROLE_K2DOTS, 1024, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            YSTAGE_SMEM));
   }
   // Shared-memory windows (fmt 2) are opt-in: correct and bit-exact, but on every config measured
   // slower than L1-cached gathers ("Windows"). opt.flags bit1 disables them

@@ -574,7 +574,17 @@ constexpr int NSB = SPW > 16 ? SPW : 16;
 #ifndef PLSS_PAIR
 #define PLSS_PAIR 1                     // fmt 3: consecutive slices a warp sums together
 #endif
-constexpr int YQ = (SIGMA >= 1024 ? 4 : 8) * PLSS_PAIR;  // fmt 3 K2: sigma windows staged in smem
+#ifndef PLSS_UNIT_COST
+#define PLSS_UNIT_COST 128              // fmt 3 CTA balance: cost of a unit beyond its stored entries
+#endif
+#ifndef PLSS_YQ
+#define PLSS_YQ 16
+#endif
+// fmt 3 K2: sigma windows staged in shared memory at once (dynamic smem, YQ * SIGMA * 8 bytes),
+// and the ring of per-window staging decisions (YD windows)
+constexpr int YQ = PLSS_YQ;
+constexpr int YSTAGE_SMEM = YQ * SIGMA * 8;
+constexpr int YD = 1024;
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
 #endif
@@ -676,7 +686,8 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 //   slice order (deterministic).
 // Slice metadata (start, length, this lane's row) is loaded one slice ahead, so a slice's stream
 // loads wait for DRAM only, not for an L2 round trip to sptr / perm first.
-template <int ROLE, int BS = NT, bool LU = false>     // LU: the segment has long-row units (gsort)
+// LU: the segment has long-row units (gsort); YS: the K2 segment's y is staged (sigma perm)
+template <int ROLE, int BS = NT, bool LU = false, bool YS = false>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
@@ -685,12 +696,15 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   // row, not slot) and the warp that completes a window writes its SIGMA values coalesced,
   // instead of 32 scattered 8-byte stores per slice. In-flight slices (<= 32 P + P) span at most
   // YQ - 2 windows, so the buffers are never reused while still filling.
-  constexpr bool YST = DYN && (ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && PLSS_YSTAGE;
+  constexpr bool YST = YS && DYN && (ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && PLSS_YSTAGE;
   static_assert(SPW % P == 0 && NSB % P == 0, "a warp unit must not straddle a sigma window");
   __shared__ double sm[2][MAXW];
   __shared__ int s_next;
-  __shared__ double s_y[YST ? YQ : 1][YST ? SIGMA : 1];
+  extern __shared__ __align__(16) double s_ydyn[];  // [YQ][SIGMA] when YST (dynamic smem)
+  double (*s_y)[SIGMA] = reinterpret_cast<double (*)[SIGMA]>(s_ydyn);
   __shared__ int s_ycnt[YST ? YQ : 1];
+  __shared__ int s_ytag[YST ? YQ : 1];              // window a y slot holds (-1: free)
+  __shared__ int s_ydec[YST ? YD : 1];              // window W's decision: W * 2 + staged
   if (a.ctl != nullptr && a.ctl->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = a.pol_first;
@@ -702,7 +716,8 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
     sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices + (LU ? a.nlong : 0));
     stride = P * BS / 32;
     if (tid == 0) s_next = sl0 + P * (BS / 32);     // the first unit of each warp is static
-    if (YST && tid < YQ) s_ycnt[tid] = 0;
+    if (YST && tid < YQ) { s_ycnt[tid] = 0; s_ytag[tid] = -1; }
+    if (YST) for (int q = tid; q < YD; q += BS) s_ydec[q] = -2;
     __syncthreads();
   }
   int su = sl0 + warp * P;                          // first slice of this warp's unit
@@ -721,8 +736,35 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       }
     }
   };
+  // y staging without waits on a held slot. Ring slots are reused every YQ sigma windows, and a
+  // straggler (the longest slice of a sigma window is its first) can still own a slot when a later
+  // window maps to it. So the window's fate is decided when its FIRST slice is ticketed (tickets
+  // are in order): staged if its slot is free (claimed by tag), else its slices write y directly.
+  // The window's other slices read the decision right after taking their tickets (at most a few
+  // instructions after it is made). A staged window releases its slot when complete.
+  constexpr bool YSTG = YST;
+  auto ydecide = [&](int first_slice) {             // lane 0 / thread 0
+    const int W = first_slice / SPW;
+    const int staged = atomicCAS(&s_ytag[W % YQ], -1, W) == -1;
+    *(volatile int*)&s_ydec[W % YD] = W * 2 + staged;
+  };
+  auto ymode = [&](int sl) -> int {                 // whole warp: 1 = staged
+    int v = 0;
+    if (lane == 0) {
+      const int W = sl / SPW;
+      const long long t0 = clock64();
+      while (((v = *(volatile int*)&s_ydec[W % YD]) >> 1) != W) { __nanosleep(32); spin_guard(t0); }
+    }
+    return __shfl_sync(FULL, v, 0) & 1;
+  };
+  if (YSTG && DYN && a.perm && !a.gsort) {
+    if (tid == 0)
+      for (int f = sl0; f < min(sl0 + P * (BS / 32), sl1); f += SPW) ydecide(f);
+    __syncthreads();
+  }
   if (su < sl1) meta(su);
   while (su < sl1) {
+    const bool stage = YSTG && a.perm && !a.gsort && ymode(su);
     int st0[P], L[P], row[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
@@ -739,7 +781,10 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       nx = su + stride;
     } else {
       nx = 0;
-      if (lane == 0) nx = atomicAdd(&s_next, P);
+      if (lane == 0) {
+        nx = atomicAdd(&s_next, P);
+        if (YSTG && a.perm && !a.gsort && nx < sl1 && nx % SPW == 0) ydecide(nx);
+      }
       nx = __shfl_sync(FULL, nx, 0);
     }
     if (nx < sl1) meta(nx);
@@ -796,7 +841,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #if PLSS_ABLATE & 32
           if (s[q] == 1234.5) a.out[row[q]] = s[q];             // ablation: no y write
 #else
-          if (YST && a.perm && !a.gsort) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = s[q];  // staged
+          if (stage) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = s[q];  // staged
           else a.out[row[q]] = s[q];                            // y_j
 #endif
           if (ROLE == ROLE_K2DOTS) { d0 = s[q] * s[q]; d1 = s[q] * a.pv[row[q]]; }
@@ -812,7 +857,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
         }
       }
     }
-    if (YST && a.perm && !a.gsort) {
+    if (stage) {
       const int w = su / SPW, qw = w % YQ;
       const int nsw = min(SPW, a.nslices - w * SPW);           // slices of this sigma window
       __threadfence_block();                                    // this warp's s_y stores before the count
@@ -829,7 +874,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
           if (r < a.nrows) a.out[r] = s_y[qw][u * 32 + lane];
         }
         __syncwarp();
-        if (lane == 0) s_ycnt[qw] = 0;
+        if (lane == 0) { s_ycnt[qw] = 0; __threadfence_block(); atomicExch(&s_ytag[qw], -1); }
       }
     }
     su = nx;
@@ -1190,7 +1235,7 @@ __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, 
   // w: prefix over units (nunits+1 entries); unit cost = (w[u+1] - w[u]) * wscale + UNIT_COST
   // (a unit also costs its metadata loads, row outputs and dot partial: without that term the
   // empty slices of a segment -- C4's empty columns sort last -- all fall to the last CTA)
-  constexpr long long UNIT_COST = 32 * 4;
+  constexpr long long UNIT_COST = PLSS_UNIT_COST;
   const long long total = (long long)w[nunits] * wscale + (long long)nunits * UNIT_COST;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= grid; c += gridDim.x * blockDim.x) {
     const long long target = (total * c + grid - 1) / grid;
