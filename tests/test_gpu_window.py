@@ -157,3 +157,20 @@ def test_formats_spmv_bit_exact(pkg, case, sellc, slabs):
     ref_v = oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u)
     np.testing.assert_array_equal(v[clen <= 128], ref_v[clen <= 128])
     pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("slabs", [3, 4, 7])
+def test_repeated_spmv_bitwise_stable(pkg, slabs):
+    """Races in the shared-memory staging of K2's sigma-permuted y (a ring slot reused while a
+    straggler slice still owns it) show up as run-to-run differences: repeat and compare."""
+    s = CASES["C5xs"]()
+    x = np.random.default_rng(2).standard_normal(s.n)
+    u = np.random.default_rng(3).standard_normal(s.m)
+    ref_y = oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x)
+    ref_v = oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u)
+    ctx = pkg.plss_create(_matrix(pkg, s), slabs=slabs, maxit_cap=4)
+    for _ in range(8):
+        y, v = _spmv_pair(pkg, ctx, s, x, u)
+        np.testing.assert_array_equal(y, ref_y)
+        np.testing.assert_array_equal(v, ref_v)
+    pkg.plss_destroy(ctx)
