@@ -381,10 +381,14 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   const int nblocks = (nunits + NSB - 1) / NSB;
   const int grid = std::max(1, std::min(std::min(nblocks, sms), MAXG));
   int32_t* cblk = pool.cblk + pool.used_c;
+  // CTA balance: a unit costs its stored entries plus a fixed overhead (metadata loads, row
+  // outputs, dot partial); sigma-permuted slices also pay the scattered / staged y. Measured best:
+  // 128 entries (C4's global-sort segments; 256: -15%), 256 for sigma-permuted ones (C5 K2 +3%).
+  const int uc = (a.perm && !a.gsort) ? env_int("PLSS_UC_SIG", 256) : env_int("PLSS_UC", 128);
   if (a.uw)
-    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk);
+    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk, uc);
   else
-    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.sptr, 32, nunits, NSB, nblocks, grid, cblk);
+    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.sptr, 32, nunits, NSB, nblocks, grid, cblk, uc);
   CK(cudaGetLastError());
   pool.used_c += MAXG + 1;
   a.cblk = cblk;
@@ -426,7 +430,7 @@ static plss_status try_window(plss_ctx* ctx, SpmvSeg& a, const double* g, int64_
   CK(cudaStreamSynchronize(st));
   if ((double)cov < 0.1 * (double)nnz_seg) return PLSS_OK;          // too little locality
   int32_t* cblk = pool.cblk + pool.used_c;
-  k_cta_ranges<<<(grid + 256) / 256, 256, 0, st>>>(a.sptr, 32, a.nslices, nsb, nblocks, grid, cblk);
+  k_cta_ranges<<<(grid + 256) / 256, 256, 0, st>>>(a.sptr, 32, a.nslices, nsb, nblocks, grid, cblk, 128);
   k_win_chain<<<(grid + 255) / 256, 256, 0, st>>>(wlo, cblk, grid, win, ring);
   CK(cudaGetLastError());
   a.cblk = cblk;

@@ -574,9 +574,6 @@ constexpr int NSB = SPW > 16 ? SPW : 16;
 #ifndef PLSS_PAIR
 #define PLSS_PAIR 1                     // fmt 3: consecutive slices a warp sums together
 #endif
-#ifndef PLSS_UNIT_COST
-#define PLSS_UNIT_COST 128              // fmt 3 CTA balance: cost of a unit beyond its stored entries
-#endif
 #ifndef PLSS_YQ
 #define PLSS_YQ 16
 #endif
@@ -1231,11 +1228,11 @@ __global__ void k_win_chain(int2* wlo, const int32_t* cblk, int grid, int win, i
 // entries start at or after c/grid of the segment's total (work balance when row lengths vary,
 // e.g. C5's K2 slabs where a band of columns holds 9x the entries of the rest).
 __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, int nblocks, int grid,
-                             int32_t* cblk) {
+                             int32_t* cblk, int unit_cost) {
   // w: prefix over units (nunits+1 entries); unit cost = (w[u+1] - w[u]) * wscale + UNIT_COST
   // (a unit also costs its metadata loads, row outputs and dot partial: without that term the
   // empty slices of a segment -- C4's empty columns sort last -- all fall to the last CTA)
-  constexpr long long UNIT_COST = PLSS_UNIT_COST;
+  const long long UNIT_COST = unit_cost;
   const long long total = (long long)w[nunits] * wscale + (long long)nunits * UNIT_COST;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= grid; c += gridDim.x * blockDim.x) {
     const long long target = (total * c + grid - 1) / grid;
