@@ -562,11 +562,11 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
 #endif
 constexpr int SU = PLSS_SU;             // steps (entries per lane) in flight
 #ifndef PLSS_SIGMA
-#define PLSS_SIGMA 256
+#define PLSS_SIGMA 512
 #endif
 constexpr int SIGMA = PLSS_SIGMA;       // rows per sigma-sort window (SELL-32 construction; C5's K2
-                                        // slabs: 57% padding unsorted, 9.4% at 256, 2.9% at 1024,
-                                        // yet 1024 runs 5% slower: coarser windows cost locality)
+                                        // slabs: 57% padding unsorted, 9.4% at 256, 2.9% at 1024;
+                                        // 512 measured best, +0.8% over 256, 1024 ties 256)
 constexpr int SPW = SIGMA / 32;         // slices per sigma window
 // slices per CTA-range block of fmt 3 (a multiple of the sigma window: a window's y staging
 // counter lives in one CTA's shared memory)
@@ -575,7 +575,7 @@ constexpr int NSB = SPW > 16 ? SPW : 16;
 #define PLSS_PAIR 1                     // fmt 3: consecutive slices a warp sums together
 #endif
 #ifndef PLSS_YQ
-#define PLSS_YQ 16
+#define PLSS_YQ 8
 #endif
 // fmt 3 K2: sigma windows staged in shared memory at once (dynamic smem, YQ * SIGMA * 8 bytes),
 // and the ring of per-window staging decisions (YD windows)
