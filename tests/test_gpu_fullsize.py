@@ -1,0 +1,127 @@
+"""GPU parity at BASELINE.json's full sizes, in the configuration bench.py times (default options:
+auto slabs, SELL-32 fmt 3, freeze mode for C5).
+
+C5 (64M x 8M, 768M nnz) is too large for the CPU oracle to solve in test time, so it is checked on
+sampled outputs the oracle computes one by one (SpMV rows / SpMV^T columns: bitwise, every sum is
+sequential in ascending index order on both sides) and through properties of Algorithm 1 that hold
+at any size (Thm 3.1 / eq:orthogonal-updates: psi_k = y_k^T p_{k-1} = -rho_k, mutually
+orthogonal updates so ||x_k||^2 = sum_j theta_j; convergence to the unique solution x* of the
+consistent full-column-rank system; the recursive residual tracks the true one). C3 (2048^2 grid)
+and C4 (2M x 8M power-law) are compared with the oracle over their first iterations.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import plss_gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2207_07615_b200 import build as pbuild
+    pbuild.build()
+    import paper_2207_07615_b200 as p
+    p.load_library()
+    assert torch.cuda.is_available()
+    return p
+
+
+@pytest.fixture(scope="module")
+def c5(pkg):
+    d = plss_gen.make_c5_torch(device="cuda")
+    A = pkg.Matrix(d["m"], d["n"], d["row_ptr"], d["col_idx"], d["val"], d["col_ptr"], d["row_idx"], d["val_t"])
+    ctx = pkg.plss_create(A, maxit_cap=64)
+    yield d, ctx
+    pkg.plss_destroy(ctx)
+    torch.cuda.empty_cache()
+
+
+def _sub_csr(ptr, idx, val, rows):
+    """Host CSR of the selected rows (columns) of a device CSR (CSC)."""
+    r = torch.from_numpy(rows).to(ptr.device)
+    b = ptr[r].long()
+    e = ptr[r + 1].long()
+    lens = (e - b).cpu().numpy()
+    pos = torch.cat([torch.arange(int(x), int(y), device=ptr.device) for x, y in zip(b.tolist(), e.tolist())])
+    sp = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(lens, out=sp[1:])
+    return sp, idx[pos].cpu().numpy(), val[pos].cpu().numpy()
+
+
+def test_c5_full_spmv_sampled_bitwise(pkg, c5):
+    d, ctx = c5
+    m, n = d["m"], d["n"]
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(n)
+    u = rng.standard_normal(m)
+    y = torch.empty(m, dtype=torch.float64, device="cuda")
+    v = torch.empty(n, dtype=torch.float64, device="cuda")
+    pkg.plss_spmv(ctx, torch.from_numpy(x).cuda(), y)
+    pkg.plss_spmvT(ctx, torch.from_numpy(u).cuda(), v)
+    rows = np.sort(rng.choice(m, 4096, replace=False))
+    sp, ci, vv = _sub_csr(d["row_ptr"], d["col_idx"], d["val"], rows)
+    np.testing.assert_array_equal(y[torch.from_numpy(rows).cuda()].cpu().numpy(),
+                                  oracle.spmv(len(rows), sp, ci, vv, x))
+    # columns: the band region and the rest, plus the first / last columns (window clipping)
+    cols = np.unique(np.concatenate([rng.choice(n, 4096, replace=False), [0, 1, n - 2, n - 1]]))
+    sp, ri, vt = _sub_csr(d["col_ptr"], d["row_idx"], d["val_t"], cols)
+    np.testing.assert_array_equal(v[torch.from_numpy(cols).cuda()].cpu().numpy(),
+                                  oracle.spmv(len(cols), sp, ri, vt, u))
+
+
+def test_c5_full_solve_properties(pkg, c5):
+    d, ctx = c5
+    m, n = d["m"], d["n"]
+    k = 40
+    res = pkg.plss_solve(ctx, d["b"], tol=0.0, maxit=k, flags=1, want_diag=True)
+    x = res["x"]
+    diag = res["diag"][:k]
+    hist, rho, psi, theta = diag[:, 0], diag[:, 1], diag[:, 3], diag[:, 4]
+    # convergence to the unique solution x* (b = A x*, full column rank, kappa ~ 3)
+    xs = d["x_star"]
+    assert float(torch.linalg.norm(x - xs) / torch.linalg.norm(xs)) <= 1e-10
+    # the true residual agrees with the recursive one at convergence
+    ax = torch.empty(m, dtype=torch.float64, device="cuda")
+    pkg.plss_spmv(ctx, x, ax)
+    rel_true = float(torch.linalg.norm(d["b"] - ax) / torch.linalg.norm(d["b"]))
+    assert rel_true <= 1e-12 and hist[k - 1] <= 1e-12
+    # psi_k = -rho_k (eq:orthogonal-updates) while the iteration is live
+    live = np.nonzero(hist[1:] > 1e-8)[0] + 1
+    assert live.size >= 5
+    np.testing.assert_allclose(psi[live] / rho[live], -1.0, rtol=0, atol=1e-9)
+    # mutually orthogonal updates: ||x_k||^2 = sum_j theta_j (x0 = 0)
+    xx = float(torch.dot(x, x))
+    assert abs(xx - theta.sum()) <= 1e-10 * xx
+
+
+def test_c3_full_parity_first_iterations(pkg):
+    s = plss_gen.make_config("C3")                 # 2048^2 grid, 21M nnz
+    k = 40
+    ref = oracle.plss_system(s, maxit=k)
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create(A, maxit_cap=k)
+    res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, maxit=k)
+    pkg.plss_destroy(ctx)
+    assert res["iters"] == ref["iters"] == k and res["outcome"] == ref["outcome"] == "maxit"
+    h, hr = res["hist"][:k], ref["hist"][:k]
+    assert np.max(np.abs(h - hr) / hr) <= 1e-9
+    xr = ref["x"]
+    assert np.linalg.norm(res["x"].cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-7
+
+
+def test_c4_full_parity_first_iterations(pkg):
+    from test_gpu_parity import _assert_parity, _floor
+    s = plss_gen.make_config("C4")                 # 2M x 8M, power-law rows (global-sort SELL)
+    s.maxit = 100
+    ref = oracle.plss_system(s)
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create(A, maxit_cap=s.maxit)
+    res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, maxit=s.maxit)
+    pkg.plss_destroy(ctx)
+    res["xh"] = res["x"].cpu().numpy()
+    _assert_parity(res, ref, _floor(s, ref), s)
+    empty = np.diff(s.col_ptr) == 0                # x stays in range(A^T): empty columns are 0
+    assert empty.any() and np.all(res["xh"][empty] == 0.0)
