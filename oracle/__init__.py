@@ -4,7 +4,8 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl refer
 import this package. The product path (paper_2207_07615_b200/) never imports it and never falls
 back to it.
 
-* `plss_oracle.c`   -- Algorithm 1 in plain binary64 C, sequential sums.
+* `plss_oracle.c`   -- Algorithm 1 (PAPER.md L773-816) in plain binary64 C, sequential sums;
+                       WI = I (PLSS) or a diagonal WI (PLSS W, L714-765), `column_norms`.
 * `exact.py`        -- the same algorithm in exact rational arithmetic (fractions.Fraction).
 * `dense.py`        -- brute-force pins: pseudo-inverse min-norm solution (Thm 3.1 / Cor 3.3),
                        the closed-form update eq:pkLong (L151-167) with the residual sketch
@@ -49,9 +50,10 @@ def _load():
         P = ctypes.c_void_p
         lib.oracle_spmv.argtypes = [ctypes.c_int64, P, P, P, P, P]
         lib.oracle_spmvT.argtypes = [ctypes.c_int64, P, P, P, P, P]
-        lib.oracle_plss.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, P, P, P, P, P,
+        lib.oracle_plss.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, P, P, P, P, P, P,
                                     ctypes.c_double, ctypes.c_int, ctypes.c_int32, ctypes.c_int,
                                     ctypes.c_double, P, P, P, P]
+        lib.oracle_column_norms.argtypes = [ctypes.c_int64, P, P, P]
         lib.oracle_plss.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -87,9 +89,19 @@ def spmvT(n, col_ptr, row_idx, val_t, u):
     return out
 
 
+def column_norms(n, col_ptr, val_t):
+    """c_j = ||A_{:,j}|| (ascending sum of squares, sqrt; zero columns 1): PLSS W's WI diagonal."""
+    lib = _load()
+    cp, vt = _i32(col_ptr), _f64(val_t)
+    c = np.empty(n, dtype=np.float64)
+    lib.oracle_column_norms(n, _p(cp), _p(vt), _p(c))
+    return c
+
+
 def plss(m, n, row_ptr, col_idx, val, col_ptr, row_idx, val_t, b, x0=None, tol=1e-8,
-         tol_mode=0, maxit=100, freeze=False, freeze_h=FREEZE_H, keep_updates=False):
-    """Algorithm 1 (WI = I). Returns dict(x, iters, outcome, rec[(maxit+1), 8], hist[, P]).
+         tol_mode=0, maxit=100, freeze=False, freeze_h=FREEZE_H, keep_updates=False, wi=None):
+    """Algorithm 1 (WI = I, or WI = diag(wi): PLSS W). Returns dict(x, iters, outcome,
+    rec[(maxit+1), 8], hist[, P]).
 
     keep_updates: also return P[iters, n], the updates p_1..p_iters (small cases only)."""
     lib = _load()
@@ -97,11 +109,12 @@ def plss(m, n, row_ptr, col_idx, val, col_ptr, row_idx, val_t, b, x0=None, tol=1
     cp, ri, vt = _i32(col_ptr), _i32(row_idx), _f64(val_t)
     bb = _f64(b)
     xx0 = _f64(x0) if x0 is not None else None
+    ww = _f64(wi) if wi is not None else None
     x = np.empty(n, dtype=np.float64)
     it = ctypes.c_int32(0)
     rec = np.zeros((maxit + 1, REC), dtype=np.float64)
     P = np.zeros((maxit, n), dtype=np.float64) if keep_updates else None
-    out = lib.oracle_plss(m, n, _p(rp), _p(ci), _p(v), _p(cp), _p(ri), _p(vt), _p(bb), _p(xx0),
+    out = lib.oracle_plss(m, n, _p(rp), _p(ci), _p(v), _p(cp), _p(ri), _p(vt), _p(bb), _p(xx0), _p(ww),
                           float(tol), int(tol_mode), int(maxit), int(bool(freeze)), float(freeze_h),
                           _p(x), ctypes.byref(it), _p(rec), _p(P))
     iters = it.value

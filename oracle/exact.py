@@ -1,6 +1,7 @@
 """Exact-rational Algorithm 1 -- TEST INFRASTRUCTURE ONLY.
 
-Algorithm 1 with WI = I in fractions.Fraction arithmetic. Algorithm 1's
+Algorithm 1 with WI = I or a rational diagonal WI, in fractions.Fraction
+arithmetic. Algorithm 1's
 tau = sqrt(theta*phi)/rho only enters through (tau-1)(tau+1) = theta*phi/rho^2 - 1, so
 beta = 1/((tau-1)(tau+1)) = rho^2/(theta*phi - rho^2) is rational (Thm 4.1 proof, PAPER.md
 L697-707) and gamma = (theta/rho)*beta (L809). No square root is ever needed; the stop test is
@@ -29,8 +30,10 @@ def dotq(a, b) -> Fraction:
     return sum((ai * bi for ai, bi in zip(a, b)), Fraction(0))
 
 
-def plss_exact(A, b, x0=None, maxit=None):
-    """Run Algorithm 1 exactly until r = 0 (or maxit updates).
+def plss_exact(A, b, x0=None, maxit=None, wi=None):
+    """Run Algorithm 1 exactly until r = 0 (or maxit updates). wi: the diagonal of WI (rational;
+    None = identity): WIy = y ./ wi, phi = y^T WIy, p = beta p + gamma WIy, theta = p^T (WI p)
+    (PLSS W).
 
     Returns dict with x, iters, converged, and per-step lists: rho (rho_0..), p (p_1..),
     r (r_0..), y (y_1..), beta, gamma, psi (y_k^T p_{k-1}, k >= 2).
@@ -40,6 +43,9 @@ def plss_exact(A, b, x0=None, maxit=None):
     n = len(A[0]) if m else 0
     b = [_F(v) for v in b]
     x = [_F(v) for v in x0] if x0 is not None else [Fraction(0)] * n
+    w = [_F(v) for v in wi] if wi is not None else [Fraction(1)] * n
+    wdiv = lambda y: [yi / wj for yi, wj in zip(y, w)]           # WI \ y  (L788, L805)
+    wdot = lambda p: sum((pi * wj * pi for pi, wj in zip(p, w)), Fraction(0))   # p^T (WI p)
     maxit = maxit if maxit is not None else 4 * max(m, n, 1)
     r = [bi - ai for bi, ai in zip(b, matvec(A, x))]          # r0 = b - A x0   (L786)
     out = {"rho": [], "p": [], "r": [list(r)], "y": [], "beta": [], "gamma": [], "psi": [],
@@ -49,11 +55,12 @@ def plss_exact(A, b, x0=None, maxit=None):
     if rho == 0:
         return dict(out, x=x, iters=0, converged=True)
     y = matvecT(A, r)                                          # y1 = A^T r0  (L786)
-    phi = dotq(y, y)                                           # (L789)
+    wy = wdiv(y)
+    phi = dotq(y, wy)                                          # (L789)
     if phi == 0:
         return dict(out, x=x, iters=0, converged=False)
-    p = [rho / phi * yi for yi in y]                           # p1 = (rho/phi) y  (L795)
-    theta = dotq(p, p)                                         # (L796)
+    p = [rho / phi * yi for yi in wy]                          # p1 = (rho/phi) WIy  (L795)
+    theta = wdot(p)                                            # (L796)
     x = [xi + pi for xi, pi in zip(x, p)]                      # (L797)
     out["y"].append(y); out["p"].append(p); out["phi"].append(phi); out["theta"].append(theta)
     iters = 1
@@ -65,15 +72,16 @@ def plss_exact(A, b, x0=None, maxit=None):
         if rho == 0:
             return dict(out, x=x, iters=iters, converged=True)
         y = matvecT(A, r)                                      # (L802)
-        phi = dotq(y, y)                                       # (L806)
+        wy = wdiv(y)                                           # (L805)
+        phi = dotq(y, wy)                                      # (L806)
         out["psi"].append(dotq(y, p))
         denom = theta * phi - rho * rho                        # rho^2((tau-1)(tau+1))
         if denom == 0 or phi == 0:
             return dict(out, x=x, iters=iters, converged=False)
         beta = rho * rho / denom                               # (L807-808)
         gamma = (theta / rho) * beta                           # (L809)
-        p = [beta * pi + gamma * yi for pi, yi in zip(p, y)]   # (L811)
-        theta = dotq(p, p)                                     # (L812)
+        p = [beta * pi + gamma * yi for pi, yi in zip(p, wy)]  # (L811)
+        theta = wdot(p)                                        # (L812)
         x = [xi + pi for xi, pi in zip(x, p)]                  # (L813)
         out["y"].append(y); out["p"].append(p); out["beta"].append(beta)
         out["gamma"].append(gamma); out["phi"].append(phi); out["theta"].append(theta)

@@ -2,7 +2,8 @@
  * PLSS CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
  *
  * Plain, slow, obviously correct binary64 implementation of Algorithm 1 (PLSS) of
- * arXiv 2207.07615 with WI = I, used only by tests/, bench.py's cpu_baseline /
+ * arXiv 2207.07615 with WI = I, or a diagonal WI = B^T B given as a vector
+ * (PLSS W, L714-765 / L777-783), used only by tests/, bench.py's cpu_baseline /
  * reference arm and __graft_entry__.smoke() to check the CUDA path. It shares no code, header,
  * table or constant generator with paper_2207_07615_b200/ and must never be linked into it.
  *
@@ -37,6 +38,17 @@
 /* Per-iteration record, 8 doubles: hist, rho, phi, psi, theta, tau, beta, gamma. */
 #define REC 8
 
+/* Column norms c_j = ||A_{:,j}|| (sum of squares in ascending row order, then sqrt); zero columns
+ * get 1. PLSS W takes WI = diag(c), i.e. W = diag(1/||A_{:,j}||) (PAPER.md L761-764,
+ * L977-979). */
+void oracle_column_norms(int64_t n, const int32_t *col_ptr, const double *val_t, double *c) {
+    for (int64_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int64_t k = col_ptr[j]; k < col_ptr[j + 1]; ++k) s = s + val_t[k] * val_t[k];
+        c[j] = s > 0.0 ? sqrt(s) : 1.0;
+    }
+}
+
 /* y = A x over CSR: y_i = sum_j a_ij x_j in ascending j ("matvec"). */
 void oracle_spmv(int64_t m, const int32_t *row_ptr, const int32_t *col_idx, const double *val,
                  const double *x, double *y) {
@@ -63,8 +75,17 @@ static double dot(int64_t len, const double *a, const double *b) {
     return s;
 }
 
+/* theta = p^T (WI p) with WI = diag(wi), or p^T p when wi is NULL (Alg. 1) */
+static double wdot(int64_t len, const double *p, const double *wi) {
+    double s = 0.0;
+    for (int64_t i = 0; i < len; ++i) s = s + p[i] * (wi ? wi[i] * p[i] : p[i]);
+    return s;
+}
+
 /*
- * Algorithm 1, WI = I, following SURVEY.md 8(c)'s transcription.
+ * Algorithm 1, following SURVEY.md 8(c)'s transcription. wi (nullable, n):
+ * the diagonal of WI; NULL is WI = I. WIy = WI \ y = y ./ wi (L788, L805, applied element-wise as
+ * the paper does for diagonal WI, L819-821).
  * x0 may be NULL (zero). x (n) receives the final iterate. rec (nullable) receives
  * (maxit+1)*REC doubles: rec[k*REC + 0..7] = hist_k, rho_k, phi, psi, theta, tau, beta, gamma
  * where at k the values are those computed in loop step k (k = 0: initialization).
@@ -74,11 +95,12 @@ static double dot(int64_t len, const double *a, const double *b) {
 int oracle_plss(int64_t m, int64_t n,
                 const int32_t *row_ptr, const int32_t *col_idx, const double *val,
                 const int32_t *col_ptr, const int32_t *row_idx, const double *val_t,
-                const double *b, const double *x0, double tol, int tol_mode, int32_t maxit,
-                int freeze, double freeze_h,
+                const double *b, const double *x0, const double *wi, double tol, int tol_mode,
+                int32_t maxit, int freeze, double freeze_h,
                 double *x, int32_t *iters_out, double *rec, double *P_out) {
     double *r = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
     double *y = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *wy = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     double *p = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     double *Ap = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
     int outcome = OR_MAXIT, frozen = 0, stopped = 0;
@@ -107,9 +129,11 @@ int oracle_plss(int64_t m, int64_t n,
         frozen = 1;
     }
 
-    /* y = A^T r; phi = y^T y; p = (rho/phi) y; theta = p^T p; x = x + p  (L786-797) */
+    /* y = A^T r; WIy = WI \ y; phi = y^T WIy; p = (rho/phi) WIy; theta = p^T (WI p); x = x + p
+     * (L786-797) */
     oracle_spmvT(n, col_ptr, row_idx, val_t, r, y);
-    double phi = dot(n, y, y);
+    for (int64_t j = 0; j < n; ++j) wy[j] = wi ? y[j] / wi[j] : y[j];
+    double phi = dot(n, y, wy);
     double gamma0 = 0.0;
     if (phi <= 1e-300) {
         if (!freeze) { outcome = OR_Y_VANISHED; goto done; }
@@ -117,8 +141,8 @@ int oracle_plss(int64_t m, int64_t n,
         frozen = 1;
     }
     if (!frozen) gamma0 = rho / phi;
-    for (int64_t j = 0; j < n; ++j) p[j] = gamma0 * y[j];
-    double theta = dot(n, p, p);
+    for (int64_t j = 0; j < n; ++j) p[j] = gamma0 * wy[j];
+    double theta = wdot(n, p, wi);
     for (int64_t j = 0; j < n; ++j) x[j] = x[j] + p[j];
     iters = 1;
     if (P_out) for (int64_t j = 0; j < n; ++j) P_out[j] = p[j];
@@ -139,9 +163,10 @@ int oracle_plss(int64_t m, int64_t n,
         } else if (freeze && h <= freeze_h) {
             frozen = 1;
         }
-        /* y = A^T r; phi = y^T y; psi = y^T p_{k-1}  (L802, L806; L671-672) */
+        /* y = A^T r; WIy = WI \ y; phi = y^T WIy; psi = y^T p_{k-1}  (L802, L805-806; L671-672) */
         oracle_spmvT(n, col_ptr, row_idx, val_t, r, y);
-        phi = dot(n, y, y);
+        for (int64_t j = 0; j < n; ++j) wy[j] = wi ? y[j] / wi[j] : y[j];
+        phi = dot(n, y, wy);
         double psi = dot(n, y, p);
         double tau = 0.0, beta = 0.0, gamma = 0.0;
         if (!frozen) {
@@ -159,9 +184,9 @@ int oracle_plss(int64_t m, int64_t n,
                 gamma = (theta / rho) * beta;                    /* L809 (R1) */
             }
         }
-        /* p = beta p + gamma y; theta = p^T p; x = x + p  (L811-813) */
-        for (int64_t j = 0; j < n; ++j) p[j] = beta * p[j] + gamma * y[j];
-        theta = dot(n, p, p);
+        /* p = beta p + gamma WIy; theta = p^T (WI p); x = x + p  (L811-813) */
+        for (int64_t j = 0; j < n; ++j) p[j] = beta * p[j] + gamma * wy[j];
+        theta = wdot(n, p, wi);
         for (int64_t j = 0; j < n; ++j) x[j] = x[j] + p[j];
         if (P_out) for (int64_t j = 0; j < n; ++j) P_out[(size_t)iters * n + j] = p[j];
         iters += 1;
@@ -170,6 +195,6 @@ int oracle_plss(int64_t m, int64_t n,
     if (!stopped) outcome = OR_MAXIT;
 done:
     *iters_out = iters;
-    free(r); free(y); free(p); free(Ap);
+    free(r); free(y); free(wy); free(p); free(Ap);
     return outcome;
 }

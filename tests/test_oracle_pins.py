@@ -377,3 +377,90 @@ def test_parity_floor_row_permutation():
     other = oracle.plss_system(t, maxit=50, tol=0.0)
     d = np.abs(base["hist"] - other["hist"]) / base["hist"]
     assert d.max() <= 1e-11
+
+
+# ---------------------------------------------------------------------------------------------
+# PLSS W (diagonal WI, PAPER.md L714-765 / Algorithm 1 with B^T B): NEXT-1
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape,seed", [((7, 4), 0), ((5, 8), 1), ((6, 6), 2), ((9, 5), 3)])
+def test_plssw_exact_terminates_at_min_wi_norm_solution(shape, seed):
+    """With WI = diag(w) > 0 the iteration is plain PLSS on A_W = A R_W^T (W = R_W^T R_W = WI^-1,
+    L716-721): it terminates in rank(A) steps, the updates are WI-orthogonal, psi_k = -rho_{k-1}
+    still holds (y^T p is invariant under the transformation), and from x0 = 0 the limit is the
+    minimum WI-norm solution x = W A^T (A W A^T)^+ b."""
+    rng = np.random.default_rng(seed + 100)
+    m, n = shape
+    A = rng.integers(-4, 5, size=shape).tolist()
+    w = [Fraction(int(v)) for v in rng.integers(1, 10, size=n)]
+    xs = rng.integers(-3, 4, size=n).tolist()
+    Aq = [[Fraction(a) for a in row] for row in A]
+    b = exact.matvec(Aq, [Fraction(v) for v in xs])
+    rk = exact.rank_exact(A)
+    out = exact.plss_exact(A, b, wi=w)
+    assert out["converged"] and out["iters"] == rk
+    P = out["p"]
+    for i in range(len(P)):
+        for j in range(i):
+            assert sum((pi * wk * pj for pi, wk, pj in zip(P[i], w, P[j])), Fraction(0)) == 0
+    for k, psi in enumerate(out["psi"]):
+        assert psi == -out["rho"][k + 1]
+    x = out["x"]
+    assert exact.matvec(Aq, x) == b
+    # x = W A^T z for some z: x ./ (1/w) = WI x lies in range(A^T)
+    wx = [xi * wi for xi, wi in zip(x, w)]
+    At = [list(col) for col in zip(*Aq)]
+    assert exact.rank_exact([row + [v] for row, v in zip(At, wx)]) == rk
+
+
+def test_plssw_unit_weights_are_plss_bitwise():
+    for name in ("C1", "C2s"):
+        s = plss_gen.make_config(name)
+        a = oracle.plss_system(s)
+        b = oracle.plss_system(s, wi=np.ones(s.n))
+        np.testing.assert_array_equal(a["x"], b["x"])
+        np.testing.assert_array_equal(a["rec"], b["rec"])
+
+
+@pytest.mark.parametrize("shape,seed", [((12, 6), 4), ((8, 14), 5)])
+def test_plssw_fp64_tracks_exact(shape, seed):
+    rng = np.random.default_rng(seed)
+    m, n = shape
+    A = rng.integers(-4, 5, size=shape)
+    w = rng.integers(1, 10, size=n)
+    xs = rng.integers(-3, 4, size=n)
+    b = A @ xs
+    ex = exact.plss_exact(A.tolist(), [Fraction(int(v)) for v in b], wi=[Fraction(int(v)) for v in w])
+    s = plss_gen.from_dense(A.astype(float), b.astype(float), tol=1e-13, maxit=min(m, n) + 4)
+    fp = oracle.plss_system(s, wi=w.astype(float))
+    assert fp["outcome"] == "converged"
+    xe = np.array([float(v) for v in ex["x"]])
+    assert np.linalg.norm(fp["x"] - xe) <= 1e-10 * np.linalg.norm(xe)
+    for k in range(1, min(len(ex["rho"]), len(fp["hist"])) - 1):
+        rho_e = float(ex["rho"][k])
+        assert abs(fp["rec"][k, 1] - rho_e) <= 1e-9 * max(rho_e, float(ex["rho"][0]) * 1e-12)
+
+
+def test_plssw_equals_plss_on_column_scaled_matrix():
+    """The paper's derivation (eq:pkTransrec -> eq:pkShortW): PLSS W on A with WI = diag(c) is PLSS
+    on A_W = A diag(c)^-1/2 with x = diag(c)^-1/2 x_W; the residuals, hence hist, coincide."""
+    s = plss_gen.make_config("C2s")
+    c = oracle.column_norms(s.n, s.col_ptr, s.val_t)
+    d = 1.0 / np.sqrt(c)
+    sw = plss_gen._finish("C2s-scaled", s.m, s.n, s.row_ptr, s.col_idx, s.val * d[s.col_idx], None,
+                          s.tol, s.tol_mode, s.maxit, b=s.b)
+    a = oracle.plss_system(s, wi=c, maxit=60)
+    b = oracle.plss_system(sw, maxit=60)
+    k = min(len(a["hist"]), len(b["hist"]), 40)
+    np.testing.assert_allclose(a["hist"][:k], b["hist"][:k], rtol=1e-9, atol=0)
+    xw = d * b["x"]
+    assert np.linalg.norm(a["x"] - xw) <= 1e-8 * np.linalg.norm(xw)
+
+
+def test_column_norms():
+    s = plss_gen.make_config("C4xs")                 # has empty columns
+    c = oracle.column_norms(s.n, s.col_ptr, s.val_t)
+    dense_norms = np.sqrt(np.bincount(s.col_idx, weights=s.val ** 2, minlength=s.n))
+    empty = np.diff(s.col_ptr) == 0
+    assert empty.any() and np.all(c[empty] == 1.0)
+    np.testing.assert_allclose(c[~empty], dense_norms[~empty], rtol=1e-14)
