@@ -140,6 +140,19 @@ plss_status plss_step(plss_ctx *ctx, int32_t k);
 plss_status plss_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
                         plss_outcome *outcome);
 
+/* PLSS W (Algorithm 1's optional B^T B, L777-783): wi (host or dev, n doubles,
+ * finite and > 0) is the diagonal of WI = B^T B = W^{-1}; later solves on this ctx use
+ * WIy = y ./ wi, phi = y^T WIy, p = beta p + gamma WIy, theta = p^T (WI p). wi = NULL restores
+ * WI = I. Copies wi into the workspace; synchronizes. Errors: E_INVALID (bad entries).
+ * On a distributed ctx every rank passes the same (global) wi. */
+plss_status plss_set_wi(plss_ctx *ctx, const double *wi);
+
+/* c_j = ||A_{:,j}|| (sum of squares in ascending row order, then sqrt; zero columns 1, SPEC.md
+ * L137) into c (host or dev, n doubles): the paper's PLSS W weights, WI = diag(c) i.e.
+ * W = diag(1/||A_{:,j}||) (L761-764, L977-979). On a distributed ctx the per-rank sums are
+ * all-reduced (collective). Synchronizes. */
+plss_status plss_column_norms(plss_ctx *ctx, double *c);
+
 /* Test entry points. y = A x (x: dev n, y: dev m); v = A^T u (u: dev m,
  * v: dev n). Sums are sequential in ascending index order per output element. Synchronous. */
 plss_status plss_spmv(plss_ctx *ctx, const double *x, double *y);

@@ -1,11 +1,11 @@
 """paper_2207_07615_b200 -- B200-native hot path of PLSS (arXiv 2207.07615, Algorithm 1).
 
 The product is libplss.so (csrc/, C ABI in include/plss.h): fp64 sm_100a kernels for the
-residual-sketch iteration r <- r - A p, y = A^T r, p <- beta p + gamma y, x <- x + p, plus a
-row-block NCCL path. `plss` is the thin Python binding (same names as the C ABI).
+residual-sketch iteration r <- r - A p, y = A^T r, p <- beta p + gamma y, x <- x + p (with an
+optional diagonal WI: PLSS W), plus a row-block NCCL path. `plss` is the thin Python binding (same names as the C ABI).
 """
 from .plss import (  # noqa: F401
     Ctx, Matrix, PlssError, load_library, plss_create, plss_create_dist, plss_destroy, plss_finish,
     plss_get_unique_id, plss_profile, plss_query, plss_solve, plss_spmv, plss_spmvT, plss_start, plss_step,
-    plss_workspace_bytes, SYMBOLS, REC, OUTCOMES,
+    plss_workspace_bytes, plss_set_wi, plss_column_norms, SYMBOLS, REC, OUTCOMES,
 )

@@ -47,6 +47,7 @@ struct Layout {
   int S = 1;
   bool dist = false;
   int maxit_cap = 0;
+  size_t wi;
   size_t r, y, p, x, rec, ctl, counters, part1, part2, part3, partn, tile1, tile2, scratch,
       scratch_blk, sptr, sidx, sval, scan_cnt, scan_blk, buf, err, scalars, total;
   bool sell = true;
@@ -126,6 +127,7 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
     L->sptr = L->sidx = L->sval = L->scan_cnt = L->scan_blk = 0;
   }
   L->buf = L->y;
+  L->wi = take(8 * (size_t)(n + 1));   // PLSS W: the diagonal of WI (16-byte reads in K3)
   L->err = take(64);
   L->scalars = take(64);
   L->total = off;
@@ -190,6 +192,8 @@ struct plss_ctx {
   std::vector<int64_t> R, E;     // slab row bounds / entry bounds
   char* ws = nullptr;
   double *r = nullptr, *y = nullptr, *p = nullptr, *x = nullptr, *rec = nullptr;
+  double* wi = nullptr;          // diagonal of WI (PLSS W), valid when `weighted`
+  bool weighted = false;
   Ctl* ctl = nullptr;
   unsigned* counters = nullptr;
   double *part1 = nullptr, *part2 = nullptr, *part3 = nullptr, *partn = nullptr;
@@ -284,10 +288,10 @@ static plss_status enqueue_step(plss_ctx* ctx) {
   if (ctx->dist) {
     NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
     k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
-                                           ctx->part2, ctx->counters + 1);
+                                           ctx->part2, ctx->counters + 1, ctx->wi);
   }
   k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
-                                     ctx->counters + 2);
+                                     ctx->counters + 2, ctx->wi);
   CK(cudaGetLastError());
   return PLSS_OK;
 }
@@ -625,6 +629,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   ctx->part1 = (double*)(w + L.part1); ctx->part2 = (double*)(w + L.part2);
   ctx->part3 = (double*)(w + L.part3); ctx->partn = (double*)(w + L.partn);
   ctx->scalars = (double*)(w + L.scalars);
+  ctx->wi = (double*)(w + L.wi);
   int* d_err = (int*)(w + L.err);
   CK(cudaMemsetAsync(ctx->counters, 0, 64 * sizeof(unsigned), st));
   CK(cudaMemsetAsync(ctx->part1, 0, 16 * (size_t)MAXG * L.S, st));
@@ -819,6 +824,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.ntiles = (int32_t)nt;
     a.out = ctx->y;
     a.pv = ctx->p;
+    a.wi = ctx->wi;
     a.partial = ctx->part2;
     a.part_base = ctx->part2;
     a.nparts = MAXG;
@@ -938,6 +944,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
   c.maxit = maxit;
   c.freeze = flags & 1;
   c.tol_mode = tol_mode;
+  c.weighted = ctx->weighted ? 1 : 0;
   c.outcome = OUT_RUNNING;
   CK(cudaMemcpyAsync(ctx->ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ctx->rec, 0, 8 * (size_t)(maxit + 1) * REC, st));
@@ -1087,11 +1094,11 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
       CK(cudaEventRecord(ev[q++], st));
       k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
-                                             ctx->part2, ctx->counters + 1);
+                                             ctx->part2, ctx->counters + 1, ctx->wi);
       CK(cudaEventRecord(ev[q++], st));
     }
     k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
-                                       ctx->counters + 2);
+                                       ctx->counters + 2, ctx->wi);
     CK(cudaEventRecord(ev[q++], st));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
@@ -1135,6 +1142,47 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];
   if (grid_k2) *grid_k2 = ctx->g2.empty() ? 0 : ctx->g2[0];
   return PLSS_OK;
+}
+
+plss_status plss_set_wi(plss_ctx* ctx, const double* wi) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!wi) { ctx->weighted = false; return PLSS_OK; }
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = ctx->n;
+  if (n > 0) {
+    CK(cudaMemcpyAsync(ctx->wi, wi, 8 * (size_t)n, is_device_ptr(wi) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    int* d_err = (int*)(ctx->ws + ctx->L.err);
+    CK(cudaMemsetAsync(d_err, 0, 4, st));
+    k_check_positive<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ctx->wi, n, d_err);
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, d_err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h) { set_err(ctx, "WI diagonal entries must be finite and > 0"); return PLSS_E_INVALID; }
+  }
+  ctx->weighted = true;
+  return sync_out(ctx);
+}
+
+plss_status plss_column_norms(plss_ctx* ctx, double* c) {
+  if (!ctx || (!c && ctx->n > 0)) return PLSS_E_INVALID;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = ctx->n;
+  if (n == 0) return sync_out(ctx);
+  // sums of squares into the scan scratch region is too small for n doubles: use y (n+1 doubles),
+  // which holds no state between solves
+  double* tmp = ctx->y;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  k_colsq<<<g, 256, 0, st>>>(ctx->A.col_ptr, ctx->A.val_t, n, tmp);
+  CK(cudaGetLastError());
+  if (ctx->dist) NK(ncclAllReduce(tmp, tmp, (size_t)n, ncclFloat64, ncclSum, ctx->comm, st));
+  k_colnorm_finish<<<g, 256, 0, st>>>(tmp, n);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c, tmp, 8 * (size_t)n, is_device_ptr(c) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return sync_out(ctx);
 }
 
 void plss_destroy(plss_ctx* ctx) {

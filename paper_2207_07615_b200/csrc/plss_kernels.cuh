@@ -66,6 +66,7 @@ struct Ctl {
   double rho, phi, psi, theta, beta, gamma;
   double nb2;       // ||b||^2 (local on a rank before the all-reduce)
   int32_t iters, maxit, done, frozen, stopped, outcome, freeze, tol_mode;
+  int32_t weighted; // PLSS W: WI = diag(wi) (Algorithm 1 with B^T B)
 };
 
 enum Role { ROLE_PLAIN = 0, ROLE_K1 = 1, ROLE_K2 = 2, ROLE_K2DOTS = 3 };
@@ -117,6 +118,7 @@ struct SpmvSeg {
   // parameters they sit in uniform registers: a per-thread createpolicy result costs one R2UR
   // (XU pipe) per cache-hinted load, which saturated the XU pipe of K1 (profiles/r01_notes.md).
   uint64_t pol_first, pol_last;
+  const double* wi;          // K2's last slab: the diagonal of WI (used when ctl->weighted)
   const int2* wlo;           // per block {lo_b, flags}: 1 = reload the whole window, 2 = no window
   const int32_t* cblk;       // grid+1 block bounds of the CTAs (balanced by stored entries)
   double* slpart;            // per-slice dot partials (fixed-order reduction, deterministic)
@@ -164,6 +166,21 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
                : "=r"(v) : "l"(p), "l"(pol));
   return v;
+}
+
+// K2's last slab (phi, psi): y_j = s gives phi's term y_j WIy_j and psi's y_j p_j; returns what K3
+// consumes, WIy_j = y_j / wi_j under PLSS W (WI \\ y applied element-wise, L805, L819-821), else y_j.
+__device__ __forceinline__ double k2_final(const double* wi, bool wtd, const double* pv, long long row, double s,
+                                           double& d0, double& d1) {
+  if (wtd) {
+    const double wy = __ddiv_rn(s, wi[row]);
+    d0 = s * wy;
+    d1 = s * pv[row];
+    return wy;
+  }
+  d0 = s * s;
+  d1 = s * pv[row];
+  return s;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -369,6 +386,7 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
   __shared__ StageDesc sdesc[NST];
   __shared__ double sm[2][MAXW];
   if (a.ctl != nullptr && a.ctl->done) return;
+  const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   const int my_tiles = a.ntiles > (int)blockIdx.x ? (a.ntiles - (int)blockIdx.x + G - 1) / G : 0;
@@ -522,9 +540,13 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
           const double rn = __dsub_rn(V1[i - d.rb], s);          // r_i <- r_i - (A p)_i
           a.out[i] = rn;
           acc0 = fma(rn, rn, acc0);
+        } else if (ROLE == ROLE_K2DOTS) {
+          double d0, d1;
+          a.out[i] = k2_final(a.wi, wtd, a.pv, i, s, d0, d1);  // y_j (WIy_j under PLSS W)
+          acc0 += d0;
+          acc1 += d1;
         } else {
           a.out[i] = s;                                         // y_j
-          if (ROLE == ROLE_K2DOTS) { acc0 = fma(s, s, acc0); acc1 = fma(s, V2[i - d.rb2], acc1); }
         }
       }
     }
@@ -703,6 +725,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   __shared__ int s_ytag[YST ? YQ : 1];              // window a y slot holds (-1: free)
   __shared__ int s_ydec[YST ? YD : 1];              // window W's decision: W * 2 + staged
   if (a.ctl != nullptr && a.ctl->done) return;
+  const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = a.pol_first;
   double acc0 = 0.0, acc1 = 0.0;
@@ -838,10 +861,11 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #if PLSS_ABLATE & 32
           if (s[q] == 1234.5) a.out[row[q]] = s[q];             // ablation: no y write
 #else
-          if (stage) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = s[q];  // staged
-          else a.out[row[q]] = s[q];                            // y_j
+          // y_j, or under PLSS W in the last slab WIy_j (what K3 consumes)
+          const double yv = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, row[q], s[q], d0, d1) : s[q];
+          if (stage) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = yv;  // staged
+          else a.out[row[q]] = yv;
 #endif
-          if (ROLE == ROLE_K2DOTS) { d0 = s[q] * s[q]; d1 = s[q] * a.pv[row[q]]; }
         }
       }
       if (DOTS) {
@@ -942,6 +966,7 @@ __global__ void __launch_bounds__(NTW, 1) k_sellw(SpmvSeg a) {
   __shared__ volatile int s_issued;                // last block (relative) whose load was issued
   __shared__ double sm[2][MAXW];
   if (a.ctl != nullptr && a.ctl->done) return;
+  const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nsb = a.nsb;
   const int b0 = a.cblk[blockIdx.x], b1 = a.cblk[blockIdx.x + 1];
@@ -1095,9 +1120,10 @@ __global__ void __launch_bounds__(NTW, 1) k_sellw(SpmvSeg a) {
           const double rn = __dsub_rn(r_old, s);                // r_i <- r_i - (A p)_i
           a.out[row] = rn;
           d0 = rn * rn;
+        } else if (ROLE == ROLE_K2DOTS) {
+          a.out[row] = k2_final(a.wi, wtd, a.pv, row, s, d0, d1);   // y_j (WIy_j under PLSS W)
         } else {
           a.out[row] = s;                                       // y_j
-          if (ROLE == ROLE_K2DOTS) { d0 = s * s; d1 = s * a.pv[row]; }
         }
       }
       if (ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS) {
@@ -1312,9 +1338,11 @@ __global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
                                                  double* __restrict__ x, long long n, Ctl* c,
-                                                 double* rec, double* partial, unsigned* counter) {
+                                                 double* rec, double* partial, unsigned* counter,
+                                                 const double* __restrict__ wi) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
+  const bool wtd = wi != nullptr && c->weighted;       // theta = p^T (WI p) under PLSS W (L812)
   const int k = c->iters;
   const bool init = (k == 0);
   const double beta = c->beta, gamma = c->gamma;
@@ -1340,15 +1368,21 @@ __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const d
     xx.x = __dadd_rn(xx.x, pp.x);
     xx.y = __dadd_rn(xx.y, pp.y);
     __stcs(x2 + i, xx);
-    acc = fma(pp.x, pp.x, acc);
-    acc = fma(pp.y, pp.y, acc);
+    if (wtd) {
+      const double2 w = __ldg(reinterpret_cast<const double2*>(wi) + i);
+      acc = fma(pp.x, w.x * pp.x, acc);
+      acc = fma(pp.y, w.y * pp.y, acc);
+    } else {
+      acc = fma(pp.x, pp.x, acc);
+      acc = fma(pp.y, pp.y, acc);
+    }
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const long long i = n - 1;
     const double pp = init ? __dmul_rn(gamma, y[i]) : __dadd_rn(__dmul_rn(beta, p[i]), __dmul_rn(gamma, y[i]));
     p[i] = pp;
     x[i] = __dadd_rn(x[i], pp);
-    acc = fma(pp, pp, acc);
+    acc = fma(pp, wtd ? wi[i] * pp : pp, acc);
   }
   if (!publish_and_elect(acc, dummy, partial, partial, gridDim.x, counter, sm)) return;
   if (threadIdx.x != 0) return;
@@ -1364,15 +1398,23 @@ __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const d
 // ---------------------------------------------------------------------------------------------
 // distributed: phi, psi over the replicated (all-reduced) y, then both tails (K2b)
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_dots_tail(const double* __restrict__ y, const double* __restrict__ p,
+__global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const double* __restrict__ p,
                                                   long long n, const double* rho_g, Ctl* c,
-                                                  double* rec, double* partial, unsigned* counter) {
+                                                  double* rec, double* partial, unsigned* counter,
+                                                  const double* __restrict__ wi) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
+  const bool wtd = wi != nullptr && c->weighted;
   double a0 = 0.0, a1 = 0.0;
   for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT) {
     const double yy = y[i];
-    a0 = fma(yy, yy, a0);
+    if (wtd) {                                      // y <- WIy in place (what K3 consumes)
+      const double wy = __ddiv_rn(yy, wi[i]);
+      y[i] = wy;
+      a0 = fma(yy, wy, a0);
+    } else {
+      a0 = fma(yy, yy, a0);
+    }
     a1 = fma(yy, p[i], a1);
   }
   if (!publish_and_elect(a0, a1, partial, partial, gridDim.x, counter, sm)) return;
@@ -1409,6 +1451,22 @@ __global__ void k_set_nbd(Ctl* c, const double* nb2) {
 // ---------------------------------------------------------------------------------------------
 // setup kernels (once per ctx)
 // ---------------------------------------------------------------------------------------------
+// column sums of squares (ascending row order) of a CSC; finish: sqrt, zero columns -> 1
+__global__ void k_colsq(const int32_t* col_ptr, const double* val_t, long long n, double* c) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (long long k = col_ptr[j]; k < col_ptr[j + 1]; ++k) s = __dadd_rn(s, __dmul_rn(val_t[k], val_t[k]));
+  c[j] = s;
+}
+__global__ void k_colnorm_finish(double* c, long long n) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) c[j] = c[j] > 0.0 ? __dsqrt_rn(c[j]) : 1.0;
+}
+__global__ void k_check_positive(const double* w, long long n, int* err) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n && !(w[j] > 0.0 && isfinite(w[j]))) atomicOr(err, 1);
+}
 __global__ void k_policies(uint64_t* out) {
   out[0] = policy_evict_first();
   out[1] = policy_evict_last();

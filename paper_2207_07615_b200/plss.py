@@ -25,7 +25,8 @@ OUTCOMES = {0: "converged", 1: "maxit", 2: "y_vanished", 3: "stagnation", -1: "r
 # C ABI symbols declared in include/plss.h (checked by tests/test_abi.py)
 SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_create_dist",
            "plss_solve", "plss_start", "plss_step", "plss_finish", "plss_spmv", "plss_spmvT",
-           "plss_profile", "plss_query", "plss_destroy", "plss_status_str", "plss_last_error"]
+           "plss_profile", "plss_query", "plss_destroy", "plss_status_str", "plss_last_error",
+           "plss_set_wi", "plss_column_norms"]
 
 
 class PlssError(RuntimeError):
@@ -89,6 +90,10 @@ def load_library(path: str = None):
     lib.plss_profile.restype = st
     lib.plss_query.argtypes = [P] + [ctypes.POINTER(I32)] * 7
     lib.plss_query.restype = st
+    lib.plss_set_wi.argtypes = [P, P]
+    lib.plss_set_wi.restype = st
+    lib.plss_column_norms.argtypes = [P, P]
+    lib.plss_column_norms.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
     lib.plss_status_str.argtypes = [st]
@@ -293,6 +298,21 @@ def plss_solve(ctx: Ctx, b, x0=None, tol=1e-8, tol_mode=0, maxit=100, flags=0, x
     if flags & 1:
         res["hist"] = hist[:it.value].copy()
     return res
+
+
+def plss_set_wi(ctx: Ctx, wi=None):
+    """PLSS W: WI = diag(wi) for later solves (None: WI = I)."""
+    ctx._wi = wi
+    _check(load_library().plss_set_wi(ctx.handle, _ptr(wi)), ctx.handle)
+
+
+def plss_column_norms(ctx: Ctx, out=None):
+    """c_j = ||A_{:,j}|| (zero columns 1) as a device tensor (or into `out`)."""
+    import torch
+    if out is None:
+        out = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
+    _check(load_library().plss_column_norms(ctx.handle, _ptr(out)), ctx.handle)
+    return out
 
 
 def plss_spmv(ctx: Ctx, x, y):

@@ -74,3 +74,21 @@ def test_two_ranks_torchrun(tmp_path):
     k = 25
     assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
     assert np.linalg.norm(r["x"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
+
+
+def test_dist_single_rank_plssw(pkg):
+    s = plss_gen.make_config("C2s")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=2, maxit_cap=s.maxit)
+    c = pkg.plss_column_norms(ctx)
+    c_ref = oracle.column_norms(s.n, s.col_ptr, s.val_t)
+    np.testing.assert_array_equal(c.cpu().numpy(), c_ref)
+    pkg.plss_set_wi(ctx, c)
+    res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, maxit=s.maxit)
+    ref = oracle.plss_system(s, wi=c_ref)
+    pkg.plss_destroy(ctx)
+    assert res["outcome"] == ref["outcome"]
+    assert abs(res["iters"] - ref["iters"]) <= max(1, int(np.ceil(0.02 * ref["iters"])))
+    k = min(25, len(ref["hist"]), len(res["hist"]))
+    assert np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+    assert np.linalg.norm(res["x"].cpu().numpy() - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7

@@ -349,3 +349,64 @@ def test_slabs_agree(pkg):
     assert a["iters"] == b["iters"]
     k = 25
     assert np.max(np.abs(a["hist"][:k] - b["hist"][:k]) / a["hist"][:k]) <= 1e-11
+
+
+# ---------------------------------------------------------------------------------------------
+# PLSS W (diagonal WI = diag(||A_{:,j}||), NEXT-1): same kernels, K2's last slab stores WIy and
+# weights phi, K3 weights theta
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,slabs", [("C1", 0), ("C2s", 0), ("C2s", 3), ("C4s", 0), ("C4xs", 0),
+                                        ("C5xs", 0), ("C5xs", 4)])
+def test_plssw_solve_parity(pkg, name, slabs):
+    s = plss_gen.make_config(name)
+    if name.startswith("C4"):
+        # ill-conditioned: thousands of iterations past the loss of orthogonality make the count
+        # rounding-sensitive beyond a single permuted-oracle floor sample (R11); compare the
+        # capped runs within the floor instead
+        s.maxit = 400
+    A = _matrix(pkg, s)
+    ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=s.maxit, validate=True)
+    c = pkg.plss_column_norms(ctx)
+    c_ref = oracle.column_norms(s.n, s.col_ptr, s.val_t)
+    np.testing.assert_array_equal(c.cpu().numpy(), c_ref)          # same sums, same sqrt
+    pkg.plss_set_wi(ctx, c)
+    res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit,
+                         flags=1 if s.freeze else 0, want_diag=True)
+    res["xh"] = res["x"].cpu().numpy()
+    ref = oracle.plss_system(s, wi=c_ref)
+    # parity floor of the weighted oracle (row-permuted ordering)
+    other = oracle.plss_system(_permuted(s), wi=c_ref, maxit=ref["rec"].shape[0] - 1)
+    k = min(len(ref["hist"]), len(other["hist"]), 50)
+    rel = np.abs(ref["hist"][:k] - other["hist"][:k]) / np.maximum(ref["hist"][:k], 1e-300)
+    bad = np.nonzero(rel > 1e-11)[0]
+    nx = np.linalg.norm(ref["x"])
+    fl = {"kf": int(bad[0]) if bad.size else k, "diters": abs(other["iters"] - ref["iters"]),
+          "dx": np.linalg.norm(other["x"] - ref["x"]) / (nx if nx > 0 else 1.0)}
+    _assert_parity(res, ref, fl, s)
+    # WI-orthogonality identity psi_k = -rho_{k-1}, as for PLSS (invariant under the transform)
+    d = res["diag"]
+    live = [kk for kk in range(1, min(res["iters"], 20)) if d[kk, 0] > 1e-8]
+    for kk in live:
+        assert abs(d[kk, 3] / d[kk, 1] + 1.0) <= 1e-8
+    # WI = I again reproduces plain PLSS on the same ctx
+    pkg.plss_set_wi(ctx, None)
+    plain = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit,
+                           flags=1 if s.freeze else 0)
+    ref0 = oracle.plss_system(s)
+    assert plain["iters"] == ref0["iters"] or abs(plain["iters"] - ref0["iters"]) <= max(1, int(0.02 * ref0["iters"])) \
+        or name.startswith("C4")
+    pkg.plss_destroy(ctx)
+
+
+def test_plssw_rejects_bad_weights(pkg):
+    s = plss_gen.make_config("C1")
+    ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=4)
+    w = np.ones(s.n)
+    w[3] = 0.0
+    with pytest.raises(pkg.PlssError, match="invalid"):
+        pkg.plss_set_wi(ctx, w)
+    w[3] = np.nan
+    with pytest.raises(pkg.PlssError, match="invalid"):
+        pkg.plss_set_wi(ctx, w)
+    pkg.plss_destroy(ctx)
