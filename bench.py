@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--slabs", type=int, default=0)
     ap.add_argument("--no-sell", action="store_true", help="CSR tiles only (no SELL-32 copies)")
     ap.add_argument("--no-window", action="store_true", help="SELL-32 without shared-memory windows")
+    ap.add_argument("--plss-w", action="store_true",
+                    help="PLSS W: WI = diag(||A_{:,j}||) (the paper's second variant; default PLSS, WI = I)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
@@ -258,6 +260,8 @@ def main():
                               window=not args.no_window)
     q = pkg.plss_query(ctx)
     b = w["b"]
+    if args.plss_w:
+        pkg.plss_set_wi(ctx, pkg.plss_column_norms(ctx))
     torch.cuda.synchronize()
 
     # ---- device-timed region: K steps, inputs resident in HBM (> L2 per step) ----------------
@@ -327,7 +331,7 @@ def main():
                        "nnz": w["nnz_global"], "parallelism": f"row-block dp{world}" if world > 1 else "single",
                        "slabs": q["slabs"], "sell_segments": q["sell_segments"],
                        "window_segments": q["window_segments"], "freeze_mode": True,
-                       "tol": 0.0,
+                       "tol": 0.0, "variant": "PLSS W (WI = diag(||A_:,j||))" if args.plss_w else "PLSS (WI = I)",
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
                        "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8"},
             "achieved_gbs": B_global * iters_per_s / 1e9,
