@@ -172,6 +172,42 @@ plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t 
                        int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2,
                        int32_t *sell_segments, int32_t *window_segments);
 
+/* ---- Randomized projection ("Rand. Proj.", the paper's comparison method) ----
+ * eq:pkLong with W = I and a fresh random sketch S_k in R^{m x r} each
+ * iteration (L171-176; Experiment I L985-991: standard normal, r = 10; Experiment III L1164-1170:
+ * sparse normal; Fig. 2):
+ *   Y = A^T S_k; M = Y^T Y; v = S_k^T r_{k-1}; z = M^+ v (pivoted Cholesky at the numerical rank,
+ *   DESIGN.md reading R8); p_k = Y z; x_k = x_{k-1} + p_k; r_k = r_{k-1} - A p_k (K1: rho, stop test
+ *   sqrt(rho_k)/||b|| <= tol or sqrt(rho_k) <= tol, as plss_solve).
+ * S_k comes from the counter-based generator of DESIGN.md reading R7, keyed by (seed, k, row,
+ * column): entry (i, c) does not depend on m. density = 1: standard normal; density < 1: each
+ * entry is kept with that probability (sparse normal).
+ * Runs on a single-device ctx (E_INVALID on a distributed one) and uses the ctx's r, p, x,
+ * control block and history: a PLSS solve in progress on the same ctx is invalidated (and an
+ * RP solve by plss_start). r: 1..64. workspace: dev, 256-byte aligned, >= ws_bytes =
+ * plss_rp_workspace_bytes(ctx, r) (S: m r, Y: n r doubles + partials); the caller keeps it
+ * alive until plss_rp_finish. maxit <= the ctx's maxit_cap.
+ * record k of `diag` = {hist_k, rho_k, numerical rank of Y_k^T Y_k, 0...}. */
+size_t plss_rp_workspace_bytes(const plss_ctx *ctx, int32_t r); /* 0 on invalid input */
+plss_status plss_rp_solve(plss_ctx *ctx, int32_t r, uint64_t seed, double density, void *workspace,
+                          size_t ws_bytes, const double *b, const double *x0, double tol,
+                          int32_t tol_mode, int32_t maxit, double *x, int32_t *iters, double *hist,
+                          double *diag, plss_outcome *outcome);
+/* Asynchronous pieces of plss_rp_solve (as plss_start / plss_step / plss_finish). */
+plss_status plss_rp_start(plss_ctx *ctx, int32_t r, uint64_t seed, double density, void *workspace,
+                          size_t ws_bytes, const double *b, const double *x0, double tol,
+                          int32_t tol_mode, int32_t maxit);
+plss_status plss_rp_step(plss_ctx *ctx, int32_t k);
+plss_status plss_rp_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
+                           plss_outcome *outcome);
+/* Test entry points. plss_rp_sketch writes S_k (dev, m x r row-major) of iteration k >= 1 (uses
+ * `workspace` for nothing but its size check). plss_spmmT: Y = A^T S (S: dev m x r row-major,
+ * Y: dev n x r row-major); Y[j, c] is the sequential ascending-row sum of column c.
+ * Synchronous. */
+plss_status plss_rp_sketch(plss_ctx *ctx, int32_t r, uint64_t seed, double density, int32_t k,
+                           void *workspace, size_t ws_bytes, double *S);
+plss_status plss_spmmT(plss_ctx *ctx, int32_t r, const double *S, double *Y);
+
 void plss_destroy(plss_ctx *ctx);
 const char *plss_status_str(plss_status s);
 const char *plss_last_error(const plss_ctx *ctx); /* NULL ctx: last error of create calls */

@@ -10,6 +10,7 @@
 // still resident in L2.
 #include "../../include/plss.h"
 #include "plss_kernels.cuh"
+#include "rp_kernels.cuh"
 
 #include <nccl.h>
 
@@ -213,6 +214,11 @@ struct plss_ctx {
   int32_t* h_done = nullptr;     // pinned [2]
   Ctl* h_ctl = nullptr;          // pinned staging
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  // randomized projection (plss_rp_*): shares r, p, x, ctl, rec and the K1 segments
+  bool rp_started = false;
+  RpArgs rp{};
+  int rp_gspmm = 1, rp_gupd = 1;
+  cudaGraphExec_t rp_graph_chunk = nullptr, rp_graph_one = nullptr;
   std::string err;
 };
 
@@ -969,6 +975,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
   }
   CK(cudaGetLastError());
   ctx->started = true;
+  ctx->rp_started = false;
   ctx->maxit = maxit;
   ctx->flags = flags;
   return PLSS_OK;
@@ -1185,11 +1192,278 @@ plss_status plss_column_norms(plss_ctx* ctx, double* c) {
   return sync_out(ctx);
 }
 
+}  // extern "C"
+
+// ---- randomized projection (rp_kernels.cuh) ----------------------------------
+static int rp_sms(const plss_ctx* ctx) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev);
+  return std::max(1, sms);
+}
+static void rp_grids(const plss_ctx* ctx, int r, int* g_gen, int* g_gram) {
+  const int sms = rp_sms(ctx);
+  const int h = (r + 1) / 2;
+  const int64_t rows_gen = RP_NT / h, rows_gram = RP_TILE / r;
+  *g_gen = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + rows_gen - 1) / rows_gen, 4 * sms));
+  *g_gram = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + rows_gram - 1) / rows_gram, 4 * sms));
+}
+static uint64_t rp_key(uint64_t seed) {   // mix64(seed), host copy of the device finalizer
+  uint64_t z = seed;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static size_t rp_bytes(const plss_ctx* ctx, int r) {
+  int gg, gm;
+  rp_grids(ctx, r, &gg, &gm);
+  const size_t np = (size_t)r * (r + 1) / 2;
+  return align_up(8 * (size_t)ctx->m * r + 16) + align_up(8 * (size_t)ctx->n * r + 16) +
+         align_up(8 * (size_t)gg * r) + align_up(8 * (size_t)gm * np) + align_up(8 * (size_t)RP_RMAX);
+}
+static bool rp_valid(const plss_ctx* ctx, int r, double density) {
+  return ctx && !ctx->dist && r >= 1 && r <= RP_RMAX && density > 0.0 && density <= 1.0;
+}
+// carve the caller's workspace; fills everything but ctl / rec / k_fixed / res
+static plss_status rp_args(plss_ctx* ctx, int r, uint64_t seed, double density, void* ws, size_t bytes, RpArgs* out) {
+  if (!ws || bytes < rp_bytes(ctx, r) || ((uintptr_t)ws % ALIGN) != 0) {
+    set_err(ctx, "randomized projection workspace missing, misaligned or smaller than plss_rp_workspace_bytes");
+    return PLSS_E_DIM;
+  }
+  RpArgs a{};
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.r = r;
+  a.h = (r + 1) / 2;
+  a.key = rp_key(seed);
+  a.density = density;
+  rp_grids(ctx, r, &a.grid_gen, &a.grid_gram);
+  char* w = (char*)ws;
+  size_t off = 0;
+  auto take = [&](size_t nb) { char* q = w + off; off += align_up(nb); return q; };
+  a.S = (double*)take(8 * (size_t)ctx->m * r + 16);
+  a.Y = (double*)take(8 * (size_t)ctx->n * r + 16);
+  a.vpart = (double*)take(8 * (size_t)a.grid_gen * r);
+  a.mpart = (double*)take(8 * (size_t)a.grid_gram * r * (r + 1) / 2);
+  a.z = (double*)take(8 * (size_t)RP_RMAX);
+  a.p = ctx->p;
+  a.x = ctx->x;
+  a.col_ptr = ctx->A.col_ptr;
+  a.row_idx = ctx->A.row_idx;
+  a.val_t = ctx->A.val_t;
+  *out = a;
+  return PLSS_OK;
+}
+static void rp_launch_spmm(const RpArgs& a, int grid, cudaStream_t st) {
+  if (a.r <= 2) k_rp_spmm<2, 1><<<grid, RP_NT, 0, st>>>(a);
+  else if (a.r <= 4) k_rp_spmm<4, 1><<<grid, RP_NT, 0, st>>>(a);
+  else if (a.r <= 8) k_rp_spmm<8, 1><<<grid, RP_NT, 0, st>>>(a);
+  else if (a.r <= 16) k_rp_spmm<16, 1><<<grid, RP_NT, 0, st>>>(a);
+  else if (a.r <= 32) k_rp_spmm<32, 1><<<grid, RP_NT, 0, st>>>(a);
+  else k_rp_spmm<32, 2><<<grid, RP_NT, 0, st>>>(a);
+}
+static int rp_spmm_grid(const plss_ctx* ctx, int r) {
+  int g = 1;
+  while (g < r && g < 32) g <<= 1;
+  const int64_t cols_per_cta = (int64_t)(RP_NT / 32) * (32 / g);
+  return (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + cols_per_cta - 1) / cols_per_cta, 8 * (int64_t)rp_sms(ctx)));
+}
+static plss_status rp_enqueue_step(plss_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  const RpArgs& a = ctx->rp;
+  k_rp_gen<<<a.grid_gen, RP_NT, 0, st>>>(a);
+  rp_launch_spmm(a, ctx->rp_gspmm, st);
+  k_rp_gram<<<a.grid_gram, RP_NT, 0, st>>>(a);
+  k_rp_solve<<<1, RP_NT, 0, st>>>(a);
+  k_rp_update<<<ctx->rp_gupd, RP_NT, 0, st>>>(a);
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
+  CK(cudaGetLastError());
+  return PLSS_OK;
+}
+static plss_status rp_build_graph(plss_ctx* ctx, int iters, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  plss_status st = PLSS_OK;
+  for (int i = 0; i < iters && st == PLSS_OK; ++i) st = rp_enqueue_step(ctx);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (st != PLSS_OK) return st;
+  CK(e);
+  CK(cudaGraphInstantiate(out, g, 0));
+  CK(cudaGraphDestroy(g));
+  return PLSS_OK;
+}
+
+extern "C" {
+
+size_t plss_rp_workspace_bytes(const plss_ctx* ctx, int32_t r) {
+  if (!rp_valid(ctx, r, 1.0)) return 0;
+  return rp_bytes(ctx, r);
+}
+
+plss_status plss_rp_start(plss_ctx* ctx, int32_t r, uint64_t seed, double density, void* workspace,
+                          size_t ws_bytes, const double* b, const double* x0, double tol, int32_t tol_mode,
+                          int32_t maxit) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!rp_valid(ctx, r, density) || !(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap ||
+      (tol_mode != 0 && tol_mode != 1)) {
+    set_err(ctx, ctx->dist ? "randomized projection runs on a single-device ctx"
+                           : "invalid r (1..64) / density (0, 1] / tol / tol_mode / maxit");
+    return PLSS_E_INVALID;
+  }
+  if (!b && ctx->m > 0) { set_err(ctx, "b is NULL"); return PLSS_E_INVALID; }
+  RpArgs a;
+  plss_status ps = rp_args(ctx, r, seed, density, workspace, ws_bytes, &a);
+  if (ps != PLSS_OK) return ps;
+  a.res = ctx->r;
+  a.ctl = ctx->ctl;
+  a.rec = ctx->rec;
+  a.k_fixed = 0;
+  cudaStream_t st = ctx->stream;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  const int64_t m = ctx->m, n = ctx->n;
+  Ctl& c = *ctx->h_ctl;
+  memset(&c, 0, sizeof c);
+  c.nbd = 1.0;
+  c.tol = tol;
+  c.maxit = maxit;
+  c.tol_mode = tol_mode;
+  c.outcome = OUT_RUNNING;
+  CK(cudaMemcpyAsync(ctx->ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->rec, 0, 8 * (size_t)(maxit + 1) * REC, st));
+  if (m > 0) CK(cudaMemcpyAsync(ctx->r, b, 8 * (size_t)m, is_device_ptr(b) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (n > 0) {
+    if (x0) {
+      const cudaMemcpyKind kind = is_device_ptr(x0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+      CK(cudaMemcpyAsync(ctx->p, x0, 8 * (size_t)n, kind, st));   // K1 below gathers x0: r = b - A x0
+      CK(cudaMemcpyAsync(ctx->x, x0, 8 * (size_t)n, kind, st));
+    } else {
+      CK(cudaMemsetAsync(ctx->p, 0, 8 * (size_t)n, st));
+      CK(cudaMemsetAsync(ctx->x, 0, 8 * (size_t)n, st));
+    }
+  }
+  k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 1, nullptr);
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);   // r_0, rho_0, stop test
+  CK(cudaGetLastError());
+  ctx->rp = a;
+  ctx->rp_gspmm = rp_spmm_grid(ctx, r);
+  ctx->rp_gupd = (int)std::max<int64_t>(1, std::min<int64_t>((n + RP_NT - 1) / RP_NT, 8 * (int64_t)rp_sms(ctx)));
+  if (ctx->rp_graph_chunk) { CK(cudaGraphExecDestroy(ctx->rp_graph_chunk)); ctx->rp_graph_chunk = nullptr; }
+  if (ctx->rp_graph_one) { CK(cudaGraphExecDestroy(ctx->rp_graph_one)); ctx->rp_graph_one = nullptr; }
+  if ((ps = rp_build_graph(ctx, ctx->chunk, &ctx->rp_graph_chunk)) != PLSS_OK) return ps;
+  if ((ps = rp_build_graph(ctx, 1, &ctx->rp_graph_one)) != PLSS_OK) return ps;
+  ctx->started = false;          // the PLSS loop state is overwritten
+  ctx->rp_started = true;
+  ctx->maxit = maxit;
+  return PLSS_OK;
+}
+
+plss_status plss_rp_step(plss_ctx* ctx, int32_t k) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->rp_started) { set_err(ctx, "plss_rp_step before plss_rp_start"); return PLSS_E_STATE; }
+  if (k < 0) return PLSS_E_INVALID;
+  for (int i = 0; i + ctx->chunk <= k; i += ctx->chunk) CK(cudaGraphLaunch(ctx->rp_graph_chunk, ctx->stream));
+  for (int i = 0; i < k % ctx->chunk; ++i) CK(cudaGraphLaunch(ctx->rp_graph_one, ctx->stream));
+  return PLSS_OK;
+}
+
+plss_status plss_rp_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
+                           plss_outcome* outcome) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->rp_started) { set_err(ctx, "plss_rp_finish before plss_rp_start"); return PLSS_E_STATE; }
+  cudaStream_t st = ctx->stream;
+  if (x && ctx->n > 0)
+    CK(cudaMemcpyAsync(x, ctx->x, 8 * (size_t)ctx->n, is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  std::vector<double> rec;
+  if (hist || diag) {
+    rec.resize((size_t)(ctx->maxit + 1) * REC);
+    CK(cudaMemcpyAsync(rec.data(), ctx->rec, 8 * rec.size(), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (sync_out(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  const Ctl& c = *ctx->h_ctl;
+  if (iters) *iters = c.iters;
+  if (outcome) *outcome = c.done ? (plss_outcome)c.outcome : (c.iters >= c.maxit ? PLSS_MAXIT : PLSS_RUNNING);
+  if (hist) for (int k = 0; k <= ctx->maxit; ++k) hist[k] = rec[(size_t)k * REC];
+  if (diag) memcpy(diag, rec.data(), 8 * rec.size());
+  return PLSS_OK;
+}
+
+plss_status plss_rp_solve(plss_ctx* ctx, int32_t r, uint64_t seed, double density, void* workspace,
+                          size_t ws_bytes, const double* b, const double* x0, double tol, int32_t tol_mode,
+                          int32_t maxit, double* x, int32_t* iters, double* hist, double* diag,
+                          plss_outcome* outcome) {
+  plss_status s = plss_rp_start(ctx, r, seed, density, workspace, ws_bytes, b, x0, tol, tol_mode, maxit);
+  if (s != PLSS_OK) return s;
+  cudaStream_t st = ctx->stream;
+  int issued = 0, slot = 0;
+  bool pending[2] = {false, false};
+  while (issued < maxit) {
+    if (maxit - issued >= ctx->chunk) {
+      CK(cudaGraphLaunch(ctx->rp_graph_chunk, st));
+      issued += ctx->chunk;
+    } else {
+      for (int i = issued; i < maxit; ++i) CK(cudaGraphLaunch(ctx->rp_graph_one, st));
+      issued = maxit;
+    }
+    CK(cudaMemcpyAsync(&ctx->h_done[slot], &ctx->ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ctx->ev[slot], st));
+    pending[slot] = true;
+    slot ^= 1;
+    if (pending[slot]) {
+      CK(cudaEventSynchronize(ctx->ev[slot]));
+      pending[slot] = false;
+      if (ctx->h_done[slot]) break;
+    }
+  }
+  return plss_rp_finish(ctx, x, iters, hist, diag, outcome);
+}
+
+plss_status plss_rp_sketch(plss_ctx* ctx, int32_t r, uint64_t seed, double density, int32_t k, void* workspace,
+                           size_t ws_bytes, double* S) {
+  if (!ctx || !rp_valid(ctx, r, density) || k < 1 || (!S && ctx->m > 0)) return PLSS_E_INVALID;
+  RpArgs a;
+  plss_status ps = rp_args(ctx, r, seed, density, workspace, ws_bytes, &a);
+  if (ps != PLSS_OK) return ps;
+  a.S = S;
+  a.res = nullptr;
+  a.ctl = nullptr;
+  a.k_fixed = k;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  k_rp_gen<<<a.grid_gen, RP_NT, 0, ctx->stream>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return sync_out(ctx);
+}
+
+plss_status plss_spmmT(plss_ctx* ctx, int32_t r, const double* S, double* Y) {
+  if (!ctx || r < 1 || r > RP_RMAX || (!S && ctx->m > 0) || (!Y && ctx->n > 0)) return PLSS_E_INVALID;
+  RpArgs a{};
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.r = r;
+  a.S = const_cast<double*>(S);
+  a.Y = Y;
+  a.col_ptr = ctx->A.col_ptr;
+  a.row_idx = ctx->A.row_idx;
+  a.val_t = ctx->A.val_t;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  rp_launch_spmm(a, rp_spmm_grid(ctx, r), ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return sync_out(ctx);
+}
+
+}  // extern "C"
+
+extern "C" {
+
 void plss_destroy(plss_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->graph_chunk) cudaGraphExecDestroy(ctx->graph_chunk);
   if (ctx->graph_one) cudaGraphExecDestroy(ctx->graph_one);
+  if (ctx->rp_graph_chunk) cudaGraphExecDestroy(ctx->rp_graph_chunk);
+  if (ctx->rp_graph_one) cudaGraphExecDestroy(ctx->rp_graph_one);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->h_done) cudaFreeHost(ctx->h_done);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);

@@ -26,7 +26,8 @@ OUTCOMES = {0: "converged", 1: "maxit", 2: "y_vanished", 3: "stagnation", -1: "r
 SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_create_dist",
            "plss_solve", "plss_start", "plss_step", "plss_finish", "plss_spmv", "plss_spmvT",
            "plss_profile", "plss_query", "plss_destroy", "plss_status_str", "plss_last_error",
-           "plss_set_wi", "plss_column_norms"]
+           "plss_set_wi", "plss_column_norms", "plss_rp_workspace_bytes", "plss_rp_solve", "plss_rp_start",
+           "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT"]
 
 
 class PlssError(RuntimeError):
@@ -94,6 +95,22 @@ def load_library(path: str = None):
     lib.plss_set_wi.restype = st
     lib.plss_column_norms.argtypes = [P, P]
     lib.plss_column_norms.restype = st
+    U64 = ctypes.c_uint64
+    lib.plss_rp_workspace_bytes.argtypes = [P, I32]
+    lib.plss_rp_workspace_bytes.restype = ctypes.c_size_t
+    lib.plss_rp_start.argtypes = [P, I32, U64, D, P, ctypes.c_size_t, P, P, D, I32, I32]
+    lib.plss_rp_start.restype = st
+    lib.plss_rp_step.argtypes = [P, I32]
+    lib.plss_rp_step.restype = st
+    lib.plss_rp_finish.argtypes = [P, P, ctypes.POINTER(I32), P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_rp_finish.restype = st
+    lib.plss_rp_solve.argtypes = [P, I32, U64, D, P, ctypes.c_size_t, P, P, D, I32, I32, P, ctypes.POINTER(I32),
+                                  P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_rp_solve.restype = st
+    lib.plss_rp_sketch.argtypes = [P, I32, U64, D, I32, P, ctypes.c_size_t, P]
+    lib.plss_rp_sketch.restype = st
+    lib.plss_spmmT.argtypes = [P, I32, P, P]
+    lib.plss_spmmT.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
     lib.plss_status_str.argtypes = [st]
@@ -337,6 +354,89 @@ def plss_query(ctx: Ctx) -> dict:
     _check(load_library().plss_query(ctx.handle, *[ctypes.byref(v) for v in vals]), ctx.handle)
     keys = ["launches_per_step", "slabs", "tile_nnz", "grid_k1", "grid_k2", "sell_segments", "window_segments"]
     return {k: v.value for k, v in zip(keys, vals)}
+
+
+def _rp_workspace(ctx: Ctx, r: int):
+    """Device workspace of randomized projection with sketch size r, cached on the ctx."""
+    nbytes = int(load_library().plss_rp_workspace_bytes(ctx.handle, int(r)))
+    if nbytes == 0:
+        raise PlssError("plss_rp_workspace_bytes: invalid r (1..64) or distributed ctx")
+    ws = getattr(ctx, "_rp_ws", None)
+    if ws is None or ws.numel() < nbytes + 256:
+        ctx._rp_ws = None
+        ws = ctx._rp_ws = _alloc_workspace(nbytes, ctx.A.row_ptr.device)
+    return _aligned(ws), nbytes
+
+
+def plss_rp_start(ctx: Ctx, b, r=10, seed=0, density=1.0, x0=None, tol=1e-8, tol_mode=0, maxit=100):
+    """Randomized projection (eq:pkLong, fresh Gaussian S_k): start (see include/plss.h)."""
+    lib = load_library()
+    wp, nb = _rp_workspace(ctx, r)
+    ctx._keep = (b, x0)
+    ctx._maxit = int(maxit)
+    _check(lib.plss_rp_start(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density), wp, nb, _ptr(b),
+                             _ptr(x0), float(tol), int(tol_mode), int(maxit)), ctx.handle)
+
+
+def plss_rp_step(ctx: Ctx, k: int):
+    _check(load_library().plss_rp_step(ctx.handle, int(k)), ctx.handle)
+
+
+def plss_rp_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
+    lib = load_library()
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(ctx._maxit + 1) if want_hist else None
+    diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
+    _check(lib.plss_rp_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+           ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if hist is not None:
+        res["hist"] = hist[:it.value + 1].copy()
+    return res
+
+
+def plss_rp_solve(ctx: Ctx, b, r=10, seed=0, density=1.0, x0=None, tol=1e-8, tol_mode=0, maxit=100, x=None,
+                  want_hist=True, want_diag=False):
+    """Full randomized-projection solve. Returns dict(x, iters, outcome, hist[0..iters][, diag])."""
+    import torch
+    lib = load_library()
+    if x is None:
+        x = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
+    wp, nb = _rp_workspace(ctx, r)
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(maxit + 1) if want_hist else None
+    diag = np.zeros((maxit + 1, REC)) if want_diag else None
+    ctx._maxit = int(maxit)
+    _check(lib.plss_rp_solve(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density), wp, nb, _ptr(b),
+                             _ptr(x0), float(tol), int(tol_mode), int(maxit), _ptr(x), ctypes.byref(it),
+                             _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if hist is not None:
+        res["hist"] = hist[:it.value + 1].copy()
+    return res
+
+
+def plss_rp_sketch(ctx: Ctx, r, seed, k, density=1.0, out=None):
+    """S_k (m x r, device) of the randomized-projection generator (test entry point)."""
+    import torch
+    if out is None:
+        out = torch.empty((ctx.m, r), dtype=torch.float64, device=ctx.A.row_ptr.device)
+    wp, nb = _rp_workspace(ctx, r)
+    _check(load_library().plss_rp_sketch(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density),
+                                         int(k), wp, nb, _ptr(out)), ctx.handle)
+    return out
+
+
+def plss_spmmT(ctx: Ctx, S, Y=None):
+    """Y = A^T S (S: device m x r row-major) -> device n x r."""
+    import torch
+    r = int(S.shape[1])
+    if Y is None:
+        Y = torch.empty((ctx.n, r), dtype=torch.float64, device=S.device)
+    _check(load_library().plss_spmmT(ctx.handle, r, _ptr(S), _ptr(Y)), ctx.handle)
+    return Y
 
 
 def plss_destroy(ctx: Ctx):
