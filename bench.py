@@ -8,6 +8,7 @@ banded+random), run in freeze mode with tol 0 so every timed step 
 work. N > 1 (torchrun): row-block sharding, one NCCL all-reduce of n+1 doubles per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5|C3|C4|C2] [--impl reference]
+    python bench.py --method rp [--rp-r 5] [--rp-density 1.0]   # randomized projection (NEXT-2)
 
 Prints ONE JSON line (rank 0).
 """
@@ -29,6 +30,16 @@ sys.path.insert(0, ROOT)
 import plss_gen  # noqa: E402
 
 METRIC = "PLSS iterations/sec and achieved HBM GB/s (fraction of ~8 TB/s)"
+RP_METRIC = "Rand. Proj. (eq:pkLong, fresh Gaussian S_k) iterations/sec and achieved HBM GB/s"
+
+
+def rp_bytes_per_iter(m, n, nnz, r):
+    """Algorithmic bytes of one randomized-projection step: sketch write +
+    r read (8 m (r+1)); A^T S: CSC stream + S once + Y write (12 nnz + 4 (n+1) + 8 m r + 8 n r);
+    Gram: Y (8 n r); update: Y, x rw, p (8 n r + 24 n); K1: CSR stream, p, r rw
+    (12 nnz + 4 (m+1) + 8 n + 16 m)."""
+    return (8 * m * (r + 1) + 12 * nnz + 4 * (n + 1) + 8 * m * r + 8 * n * r + 8 * n * r + 8 * n * r + 24 * n
+            + 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m)
 
 
 def _peaks():
@@ -40,11 +51,11 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic(workload, kernel_class, launches_per_step):
+def _traffic(workload, kernel_class, launches_per_step, capture="r01_ncu_traffic_c5.json"):
     """DRAM bytes (read + write) per step of the dominant kernel class, from the committed
-    `ncu --set full` capture (profiles/r01_ncu_traffic_c5.json: per-launch averages x launches per
-    step). None when no capture of this workload exists."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic_c5.json")
+    `ncu --set full` capture (profiles/r01_ncu_traffic_c5*.json: per-launch averages x launches
+    per step). None when no capture of this workload exists."""
+    path = os.path.join(ROOT, "profiles", capture)
     if workload != "C5" or not os.path.exists(path):
         return None, None
     with open(path) as f:
@@ -217,7 +228,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
+    ap.add_argument("--method", default="plss", choices=["plss", "rp"],
+                    help="rp: randomized projection (the paper's comparison method, NEXT-2)")
+    ap.add_argument("--rp-r", type=int, default=5, help="sketch size r (Experiment III: 5 for n > 1e5)")
+    ap.add_argument("--rp-density", type=float, default=1.0, help="< 1: sparse normal sketch")
     args = ap.parse_args()
+    if args.method == "rp":
+        return main_rp(args)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -353,6 +370,128 @@ def main():
     pkg.plss_destroy(ctx)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------------
+# randomized projection (--method rp): single device (the method is not row-block sharded here)
+# ---------------------------------------------------------------------------------------------
+def rp_cpu_leg(name, r, density, full_bytes, steps=None, budget_s=15.0):
+    """The randomized-projection oracle on the 1/100-scale sample; it/s scaled by bytes/iter."""
+    from oracle import randproj as orp
+    s, label = cpu_sample(name)
+    A = s.scipy_csr()
+    sb = rp_bytes_per_iter(s.m, s.n, s.nnz, r)
+    t0 = time.perf_counter()
+    orp.randproj(A, s.b, r=r, seed=1, maxit=2, density=density)
+    t1 = (time.perf_counter() - t0) / 2
+    k = steps or int(max(2, min(200, budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    orp.randproj(A, s.b, r=r, seed=1, maxit=k, density=density)
+    t = time.perf_counter() - t0
+    gbs = sb * k / t / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+    return {"value": gbs * 1e9 / full_bytes, "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": f"{label}; {k} randomized-projection steps (r={r}) in {t:.1f} s = {gbs:.2f} GB/s "
+                      f"algorithmic (numpy/scipy, BLAS threads up to {cores}); it/s scaled to the full "
+                      f"workload by algorithmic bytes/iter", "oracle_gbs": gbs}
+
+
+def main_rp(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    r, dens = args.rp_r, args.rp_density
+    name = args.workload
+    if name == "C5":
+        m, n, nnz = 64_000_000, 8_000_000, 768_000_000
+    else:
+        s0 = plss_gen.make_config(name)
+        m, n, nnz = s0.m, s0.n, s0.nnz
+    B = rp_bytes_per_iter(m, n, nnz, r)
+    label = workload_label(name) + f"; randomized projection r={r}" + (f", sparse S density {dens}" if dens < 1 else "")
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        leg = rp_cpu_leg(name, r, dens, B, steps=max(1, args.steps))
+        v = leg["value"]
+        print(json.dumps({"metric": RP_METRIC, "value": v, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": label}, "cpu_baseline": leg,
+                          "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+    import torch
+    import paper_2207_07615_b200 as pkg
+    assert world == 1, "randomized projection: single device (bench.py --method rp runs without torchrun)"
+    assert args.warmup >= 3 or args.ncu, "timing rules: at least 3 warm-up steps"
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pkg.load_library()
+    w = load_workload(name, 0, 1, dev)
+    A = pkg.Matrix(w["m"], w["n"], w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])
+    stream = torch.cuda.Stream(device=dev)
+    cap = args.warmup + args.steps + max(args.profile_steps, 1) + 8
+    ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=cap, stream=stream)
+    q = pkg.plss_query(ctx)
+    b = w["b"]
+    torch.cuda.synchronize()
+    pkg.plss_rp_start(ctx, b, r=r, seed=1, density=dens, tol=0.0, maxit=cap)
+    pkg.plss_rp_step(ctx, args.warmup)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        pkg.plss_rp_step(ctx, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    fin = pkg.plss_rp_finish(ctx, None, want_hist=True)
+    its = args.steps / (ms / 1e3)
+    if args.ncu:
+        print(json.dumps({"ncu_run": True, "ms_per_step": ms / args.steps}), flush=True)
+        return
+    pkg.plss_rp_start(ctx, b, r=r, seed=1, density=dens, tol=0.0, maxit=cap)
+    pkg.plss_rp_step(ctx, 2)
+    kt = pkg.plss_rp_profile(ctx, max(1, args.profile_steps))
+    cls = {"rp_spmm_AtS": (kt["spmm"], 12 * nnz + 4 * (n + 1) + 8 * m * r + 8 * n * r),
+           "rp_sketch_gen": (kt["gen"], 8 * m * (r + 1)),
+           "k1_spmv_csr_resid": (kt["k1"], 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m),
+           "rp_gram": (kt["gram"], 8 * n * r), "rp_update": (kt["update"], 8 * n * r + 24 * n)}
+    dom = max(cls, key=lambda c: cls[c][0])
+    dom_ms, dom_bytes = cls[dom]
+    peak, peak_src = _peaks()
+    traffic, traffic_src = (_traffic(name, dom, 1, "r01_ncu_traffic_c5_rp.json") if (r == 5 and dens == 1.0)
+                            else (None, None))
+    pin_b = torch.empty(w["m"], dtype=torch.float64, pin_memory=True)
+    pin_b.copy_(b.cpu())
+    pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pkg.plss_rp_solve(ctx, pin_b, r=r, seed=1, density=dens, tol=0.0, maxit=args.steps, x=pin_x)
+    t_e2e = time.perf_counter() - t0
+    line = {"metric": RP_METRIC, "value": its, "unit": "it/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": label, "m": m, "n": n, "nnz": nnz, "r": r, "density": dens,
+                       "parallelism": "single", "slabs": q["slabs"], "tol": 0.0,
+                       "l2": f"inputs larger than L2: {B / 1e9:.2f} GB algorithmic per step",
+                       "bytes_per_step_model": "24 nnz + (16 r + 28) m + (24 r + 36) n + 8"},
+            "achieved_gbs": B * its / 1e9, "achieved_frac_of_peak": B * its / 1e9 / peak,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak, "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src, "algorithmic_bytes_per_step": dom_bytes,
+                         "kernel_ms_per_step": dom_ms},
+            "kernels_ms_per_step": kt, "gpu_launches": args.steps * (5 + q["slabs"]),
+            "e2e": {"value": args.steps / t_e2e, "unit": "it/s", "h2d_bytes_per_step": 8 * w["m"] / args.steps,
+                    "d2h_bytes_per_step": (8 * n + 8 * (args.steps + 1)) / args.steps, "solve_iters": args.steps,
+                    "note": "one plss_rp_solve from pinned host b to host x + history"},
+            "clocks": clk.summary(), "final_hist": float(fin["hist_full"][args.warmup + args.steps])}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = rp_cpu_leg(name, r, dens, B)
+    print(json.dumps(line), flush=True)
+    pkg.plss_destroy(ctx)
 
 
 if __name__ == "__main__":

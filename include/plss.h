@@ -177,16 +177,17 @@ plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t 
  * iteration (L171-176; Experiment I L985-991: standard normal, r = 10; Experiment III L1164-1170:
  * sparse normal; Fig. 2):
  *   Y = A^T S_k; M = Y^T Y; v = S_k^T r_{k-1}; z = M^+ v (pivoted Cholesky at the numerical rank,
- *   DESIGN.md reading R8); p_k = Y z; x_k = x_{k-1} + p_k; r_k = r_{k-1} - A p_k (K1: rho, stop test
+ *   DESIGN.md reading R18); p_k = Y z; x_k = x_{k-1} + p_k; r_k = r_{k-1} - A p_k (K1: rho, stop test
  *   sqrt(rho_k)/||b|| <= tol or sqrt(rho_k) <= tol, as plss_solve).
- * S_k comes from the counter-based generator of DESIGN.md reading R7, keyed by (seed, k, row,
+ * S_k comes from the counter-based generator of DESIGN.md reading R17, keyed by (seed, k, row,
  * column): entry (i, c) does not depend on m. density = 1: standard normal; density < 1: each
  * entry is kept with that probability (sparse normal).
  * Runs on a single-device ctx (E_INVALID on a distributed one) and uses the ctx's r, p, x,
  * control block and history: a PLSS solve in progress on the same ctx is invalidated (and an
  * RP solve by plss_start). r: 1..64. workspace: dev, 256-byte aligned, >= ws_bytes =
  * plss_rp_workspace_bytes(ctx, r) (S: m r, Y: n r doubles + partials); the caller keeps it
- * alive until plss_rp_finish. maxit <= the ctx's maxit_cap.
+ * alive until plss_rp_finish. maxit <= the ctx's maxit_cap. S_k is kept in binary32 (m x
+ * 8 ceil(r/8) floats); every product and sum of the projection is fp64.
  * record k of `diag` = {hist_k, rho_k, numerical rank of Y_k^T Y_k, 0...}. */
 size_t plss_rp_workspace_bytes(const plss_ctx *ctx, int32_t r); /* 0 on invalid input */
 plss_status plss_rp_solve(plss_ctx *ctx, int32_t r, uint64_t seed, double density, void *workspace,
@@ -200,13 +201,18 @@ plss_status plss_rp_start(plss_ctx *ctx, int32_t r, uint64_t seed, double densit
 plss_status plss_rp_step(plss_ctx *ctx, int32_t k);
 plss_status plss_rp_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
                            plss_outcome *outcome);
-/* Test entry points. plss_rp_sketch writes S_k (dev, m x r row-major) of iteration k >= 1 (uses
- * `workspace` for nothing but its size check). plss_spmmT: Y = A^T S (S: dev m x r row-major,
- * Y: dev n x r row-major); Y[j, c] is the sequential ascending-row sum of column c.
- * Synchronous. */
+/* Per-kernel device time of k randomized-projection steps launched one kernel at a time (CUDA
+ * events on the ctx stream), after plss_rp_start; ms (host, 6 doubles) receives the average per
+ * step of: sketch + S^T r, A^T S, Gram, r x r solve, p/x update, K1 (all slabs). Synchronizes. */
+plss_status plss_rp_profile(plss_ctx *ctx, int32_t k, double *ms);
+/* Test entry points. plss_rp_sketch writes S_k of iteration k >= 1 as binary32 (reading R17)
+ * into S (dev, m x ld row-major floats; ld even, r <= ld <= 512; columns r..ld-1 are written 0).
+ * plss_spmmT: Y = A^T S (S: dev binary32 m x ld row-major, ld >= r; Y: dev fp64 n x r
+ * row-major); Y[j, c] is the sequential ascending-row fp64 sum of val * (double)S[row, c] -- the
+ * kernel the solves use (they keep S with ld = 8 ceil(r/8)). Synchronous. */
 plss_status plss_rp_sketch(plss_ctx *ctx, int32_t r, uint64_t seed, double density, int32_t k,
-                           void *workspace, size_t ws_bytes, double *S);
-plss_status plss_spmmT(plss_ctx *ctx, int32_t r, const double *S, double *Y);
+                           int32_t ld, float *S);
+plss_status plss_spmmT(plss_ctx *ctx, int32_t r, int32_t ld, const float *S, double *Y);
 
 void plss_destroy(plss_ctx *ctx);
 const char *plss_status_str(plss_status s);

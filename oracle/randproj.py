@@ -2,7 +2,7 @@
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference` legs may
 import this module. It shares no code with the CUDA path (paper_2207_07615_b200/); the two sides
-implement the same counter-based sketch generator independently (reading R7).
+implement the same counter-based sketch generator independently (reading R17).
 
 The method: eq:pkLong with W = I,
 
@@ -13,21 +13,28 @@ L985-991, r = 10; Fig. 2, r = 10/20/40) or sparse normal (`sprandn`,
 L1164-1170, r = 5 or 50). "If S_k is not in the range of A, the inverse ... is replaced by the
 pseudo-inverse" (L166-167). Each iteration "recomputes Y_k = A^T S_k, Y_k^T Y_k and a solve with
 the latter matrix" (L989-991). As in PLSS (eq:recRes, L663-666) the residual is carried
-recursively, r_k = r_{k-1} - A p_k (reading R7).
+recursively, r_k = r_{k-1} - A p_k (reading R19).
 
 Functions
-* `sketch(seed, k, m, r, density)` -- S_k (m x r), the generator of reading R7:
+* `sketch(seed, k, m, r, density)` -- S_k (m x r), the generator of reading R17. Entries are
+  IEEE binary32 normals (stored here as float64 values): the paper fixes only "random standard
+  normal" (L989-990), and eq:pkLong is the exact projection for whatever S_k is used, so the
+  sketch needs no fp64 precision while the projection itself is computed in fp64.
     word(ctr)   = mix64(key + (ctr + 1) * G),  key = mix64(seed), G = 0x9E3779B97F4A7C15,
                   mix64 = the splitmix64 finalizer (xor-shift 30 / *0xBF58476D1CE4E5B9 /
                   xor-shift 27 / *0x94D049BB133111EB / xor-shift 31), all mod 2^64;
     pair (i, q) of row i holds columns 2q, 2q+1 (h = ceil(r/2) pairs per row);
-    ctr         = (((k*2^32 + i)*h + q) * 64 + a) * 4 + w   (attempt a < 64, word w < 4; a row's
-                  entries depend on (seed, k, i, r) only, not on m: row blocks draw the same S);
-    uniforms    u = 2*((word >> 11) * 2^-53) - 1 (w = 0), v likewise (w = 1), in [-1, 1);
-    Marsaglia's polar method: the first attempt with 0 < s = u*u + v*v < 1 gives
-                  f = sqrt(-2 ln(s) / s), S[i, 2q] = u f, S[i, 2q+1] = v f (no attempt: 0, 0);
-    ln          = `ln_unit` below: frexp, one atanh series, only IEEE +,-,*,/ (no FMA);
-    sparse S    (density < 1): entry (i, 2q+e) is kept iff (word(w = 2+e) >> 11) * 2^-53 < density.
+    ctr         = ((k*2^32 + i)*h + q) * 256 + w   (word w < 4; a row's entries depend on
+                  (seed, k, i, r) only, not on m: row blocks draw the same S);
+    uniforms    (binary32) from ONE word per pair (ctr with w = 0):
+                  u1 = 1 - (word >> 40) * 2^-24 in (0, 1],  u2 = ((word >> 16) & (2^24-1)) * 2^-24 in [0, 1);
+    Box-Muller (binary32): R = sqrt(-2 ln u1), theta = 2 pi u2,
+                  S[i, 2q] = R cos(theta), S[i, 2q+1] = R sin(theta);
+    ln          = `ln_unit32`: frexp, one atanh series, only IEEE +,-,*,/ in binary32 (no FMA);
+    sin / cos   = `sincos_2pi32`: exact octant reduction of 8 u2, Taylor polynomials of sin and cos
+                  on [0, pi/4] (binary32 Horner, no FMA), octant symmetries;
+    sparse S    (density < 1): entry (i, 2q+e) is kept iff (word(w = 2+e) >> 11) * 2^-53 < density
+                  (compared in binary64).
   With every operation correctly rounded and in a fixed order, the CUDA side reproduces S
   bitwise (tests/test_gpu_randproj.py).
 * `randproj(...)` -- the iteration above, dense pseudo-inverse, sequential stop test on the
@@ -47,10 +54,16 @@ import scipy.sparse as sp
 _G = np.uint64(0x9E3779B97F4A7C15)
 _C1 = np.uint64(0xBF58476D1CE4E5B9)
 _C2 = np.uint64(0x94D049BB133111EB)
-_ATTEMPTS = 64
-_LN2 = 0.6931471805599453                       # RN(ln 2)
-_SQRT_HALF = 0.7071067811865476
-_ATANH_COEF = [1.0 / (2 * j + 1) for j in range(11, -1, -1)]   # 1/23, 1/21, ..., 1/3, 1
+_F32 = np.float32
+LN2_32 = _F32(0.6931471805599453)               # RN32(ln 2) = 0x3F317218
+SQRT_HALF_32 = _F32(0.7071067811865476)         # RN32(sqrt(1/2)) = 0x3F3504F3
+_ATANH_COEF_32 = [_F32(1.0) / _F32(2 * j + 1) for j in range(5, -1, -1)]   # RN32(1/11), ..., 1
+PI4_32 = _F32(np.pi / 4)                         # RN32(pi/4) = 0x3F490FDB
+# Taylor coefficients RN32(+-1/(2j+1)!) (sin) and RN32(+-1/(2j)!) (cos), highest degree first
+_SIN_COEF_32 = [_F32(1.0) / _F32(362880.0), _F32(-1.0) / _F32(5040.0), _F32(1.0) / _F32(120.0),
+                _F32(-1.0) / _F32(6.0), _F32(1.0)]
+_COS_COEF_32 = [_F32(-1.0) / _F32(3628800.0), _F32(1.0) / _F32(40320.0), _F32(-1.0) / _F32(720.0),
+                _F32(1.0) / _F32(24.0), _F32(-0.5), _F32(1.0)]
 
 
 def mix64(z):
@@ -70,50 +83,77 @@ def _unit(w):
     return (w >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
 
-def ln_unit(s):
-    """ln(s) for s in (0, 1): s = m 2^e with m in [sqrt(1/2), sqrt(2)), f = (m-1)/(m+1),
-    ln m = 2 f (1 + f^2/3 + f^4/5 + ... + f^22/23) by Horner, ln s = e ln2 + ln m.
-    |f| <= 0.1716, so the truncated series is exact to ~1e-17 relative."""
-    s = np.asarray(s, dtype=np.float64)
-    mant, e = np.frexp(s)                      # s = mant 2^e, mant in [0.5, 1)
-    small = mant < _SQRT_HALF
-    mant = np.where(small, mant * 2.0, mant)
-    e = np.where(small, e - 1, e).astype(np.float64)
-    f = (mant - 1.0) / (mant + 1.0)
+def ln_unit32(s):
+    """ln(s) for binary32 s in (0, 1), every operation in binary32: s = m 2^e with m in
+    [sqrt(1/2), sqrt(2)), f = (m-1)/(m+1), ln m = 2 f (1 + f^2/3 + ... + f^10/11) by Horner,
+    ln s = e ln2 + ln m. |f| <= 0.1716, so the truncated series is exact to ~2e-9 relative."""
+    s = np.asarray(s, dtype=_F32)
+    mant, e = np.frexp(s)                      # exact; mant float32 in [0.5, 1)
+    small = mant < SQRT_HALF_32
+    mant = np.where(small, mant * _F32(2.0), mant).astype(_F32)
+    e = np.where(small, e - 1, e).astype(_F32)
+    f = (mant - _F32(1.0)) / (mant + _F32(1.0))
     f2 = f * f
-    t = np.full_like(f, _ATANH_COEF[0])
-    for c in _ATANH_COEF[1:]:
+    t = np.full_like(f, _ATANH_COEF_32[0])
+    for c in _ATANH_COEF_32[1:]:
         t = t * f2 + c
-    return e * _LN2 + (2.0 * f) * t
+    return e * LN2_32 + (_F32(2.0) * f) * t
+
+
+def sincos_2pi32(u2):
+    """(sin, cos)(2 pi u2) in binary32 for u2 in [0, 1) with 24-bit granularity: x = 8 u2 (exact),
+    octant o = floor(x), f = x - o (exact), f <- 1 - f on odd octants (exact), phi = f RN32(pi/4),
+    Taylor sin phi (to phi^9) and cos phi (to phi^10) by Horner in phi^2, octant symmetries."""
+    u2 = np.asarray(u2, dtype=_F32)
+    x = u2 * _F32(8.0)
+    o = np.floor(x).astype(np.int64)
+    f = x - o.astype(_F32)
+    odd = (o & 1) == 1
+    f = np.where(odd, _F32(1.0) - f, f).astype(_F32)
+    phi = f * PI4_32
+    p2 = phi * phi
+    ts = np.full_like(p2, _SIN_COEF_32[0])
+    for c in _SIN_COEF_32[1:]:
+        ts = ts * p2 + c
+    sn = phi * ts
+    tc = np.full_like(p2, _COS_COEF_32[0])
+    for c in _COS_COEF_32[1:]:
+        tc = tc * p2 + c
+    cs = tc
+    # octant o: (sin theta, cos theta) from (sn, cs) of phi
+    sin_t = np.select([o == 0, o == 1, o == 2, o == 3, o == 4, o == 5, o == 6],
+                      [sn, cs, cs, sn, -sn, -cs, -cs], -sn).astype(_F32)
+    cos_t = np.select([o == 0, o == 1, o == 2, o == 3, o == 4, o == 5, o == 6],
+                      [cs, sn, -sn, -cs, -cs, -sn, sn], cs).astype(_F32)
+    return sin_t, cos_t
 
 
 def sketch(seed: int, k: int, m: int, r: int, density: float = 1.0) -> np.ndarray:
-    """S_k in R^{m x r} (row-major), reading R7. k is the 1-based iteration index."""
+    """S_k in R^{m x r} (row-major), reading R17. k is the 1-based iteration index."""
+    return sketch_rows(seed, k, np.arange(m), r, density)
+
+
+def sketch_rows(seed: int, k: int, rows, r: int, density: float = 1.0) -> np.ndarray:
+    """Rows `rows` of S_k (a row depends on (seed, k, i, r) only)."""
+    rows = np.asarray(rows, dtype=np.uint64)
+    m = rows.size
     h = (r + 1) // 2
     key = mix64(np.array([seed & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64))[0]
-    i = np.repeat(np.arange(m, dtype=np.uint64), h)
+    i = np.repeat(rows, h)
     q = np.tile(np.arange(h, dtype=np.uint64), m)
     base = ((np.uint64(k) << np.uint64(32)) + i) * np.uint64(h) + q
-    z0 = np.zeros(m * h)
-    z1 = np.zeros(m * h)
-    todo = np.arange(m * h)
-    for a in range(_ATTEMPTS):
-        if todo.size == 0:
-            break
-        c = (base[todo] * np.uint64(_ATTEMPTS) + np.uint64(a)) * np.uint64(4)
-        u = 2.0 * _unit(_word(key, c)) - 1.0
-        v = 2.0 * _unit(_word(key, c + np.uint64(1))) - 1.0
-        s = u * u + v * v
-        ok = (s > 0.0) & (s < 1.0)
-        so = s[ok]
-        f = np.sqrt((-2.0 * ln_unit(so)) / so)
-        z0[todo[ok]] = u[ok] * f
-        z1[todo[ok]] = v[ok] * f
-        todo = todo[~ok]
+    w = _word(key, base * np.uint64(256))
+    u1 = _F32(1.0) - (w >> np.uint64(40)).astype(_F32) * _F32(2.0 ** -24)
+    u2 = ((w >> np.uint64(16)) & np.uint64(0xFFFFFF)).astype(_F32) * _F32(2.0 ** -24)
+    rad = np.sqrt(_F32(-2.0) * ln_unit32(u1))
+    sn, cs = sincos_2pi32(u2)
+    z0 = (rad * cs).astype(_F32)
+    z1 = (rad * sn).astype(_F32)
     if density < 1.0:
-        c = base * np.uint64(_ATTEMPTS * 4)
-        z0 = np.where(_unit(_word(key, c + np.uint64(2))) < density, z0, 0.0)
-        z1 = np.where(_unit(_word(key, c + np.uint64(3))) < density, z1, 0.0)
+        c = base * np.uint64(256)
+        z0 = np.where(_unit(_word(key, c + np.uint64(2))) < density, z0, _F32(0.0))
+        z1 = np.where(_unit(_word(key, c + np.uint64(3))) < density, z1, _F32(0.0))
+    assert z0.dtype == _F32 and z1.dtype == _F32
     S = np.empty((m, 2 * h))
     S[:, 0::2] = z0.reshape(m, h)
     S[:, 1::2] = z1.reshape(m, h)
@@ -149,7 +189,7 @@ def randproj(A, b, r: int, seed: int, maxit: int, tol: float = 0.0, tol_mode: in
             z = np.linalg.pinv(M) @ v            # (.)^+ (L166-167)
             p = Y @ z
             x = x + p                            # eq:xko
-            res = res - A @ p                    # r_k = r_{k-1} - A p_k (reading R7)
+            res = res - A @ p                    # r_k = r_{k-1} - A p_k (reading R19)
             rho = float(res @ res)
             hist.append(np.sqrt(rho) / nb)
             ranks.append(int(np.linalg.matrix_rank(M)))

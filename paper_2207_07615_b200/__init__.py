@@ -9,5 +9,5 @@ from .plss import (  # noqa: F401
     Ctx, Matrix, PlssError, load_library, plss_create, plss_create_dist, plss_destroy, plss_finish,
     plss_get_unique_id, plss_profile, plss_query, plss_solve, plss_spmv, plss_spmvT, plss_start, plss_step,
     plss_workspace_bytes, plss_set_wi, plss_column_norms, SYMBOLS, REC, OUTCOMES,
-    plss_rp_solve, plss_rp_start, plss_rp_step, plss_rp_finish, plss_rp_sketch, plss_spmmT,
+    plss_rp_solve, plss_rp_start, plss_rp_step, plss_rp_finish, plss_rp_sketch, plss_spmmT, plss_rp_profile, rp_ld,
 )

@@ -1200,11 +1200,12 @@ static int rp_sms(const plss_ctx* ctx) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev);
   return std::max(1, sms);
 }
-static void rp_grids(const plss_ctx* ctx, int r, int* g_gen, int* g_gram) {
+static int rp_ld(int r) { return (r + 7) / 8 * 8; }   // S row stride (floats): whole 32-byte sectors
+static void rp_grids(const plss_ctx* ctx, int r, int ld, int* g_gen, int* g_gram) {
   const int sms = rp_sms(ctx);
-  const int h = (r + 1) / 2;
-  const int64_t rows_gen = RP_NT / h, rows_gram = RP_TILE / r;
-  *g_gen = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + rows_gen - 1) / rows_gen, 4 * sms));
+  const int64_t rows_gen = RP_NT / ((r + 1) / 2), rows_gram = RP_TILE / r;
+  (void)ld;
+  *g_gen = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + rows_gen - 1) / rows_gen, 8 * sms));
   *g_gram = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + rows_gram - 1) / rows_gram, 4 * sms));
 }
 static uint64_t rp_key(uint64_t seed) {   // mix64(seed), host copy of the device finalizer
@@ -1215,10 +1216,10 @@ static uint64_t rp_key(uint64_t seed) {   // mix64(seed), host copy of the devic
 }
 static size_t rp_bytes(const plss_ctx* ctx, int r) {
   int gg, gm;
-  rp_grids(ctx, r, &gg, &gm);
+  rp_grids(ctx, r, rp_ld(r), &gg, &gm);
   const size_t np = (size_t)r * (r + 1) / 2;
-  return align_up(8 * (size_t)ctx->m * r + 16) + align_up(8 * (size_t)ctx->n * r + 16) +
-         align_up(8 * (size_t)gg * r) + align_up(8 * (size_t)gm * np) + align_up(8 * (size_t)RP_RMAX);
+  return align_up(4 * (size_t)ctx->m * rp_ld(r) + 16) + align_up(8 * (size_t)ctx->n * r + 16) +
+         align_up(8 * (size_t)gg * r) + align_up(8 * (size_t)gm * np) + align_up(8 * (size_t)RP_RMAX) + align_up(256);
 }
 static bool rp_valid(const plss_ctx* ctx, int r, double density) {
   return ctx && !ctx->dist && r >= 1 && r <= RP_RMAX && density > 0.0 && density <= 1.0;
@@ -1234,17 +1235,20 @@ static plss_status rp_args(plss_ctx* ctx, int r, uint64_t seed, double density, 
   a.n = ctx->n;
   a.r = r;
   a.h = (r + 1) / 2;
+  a.ld = rp_ld(r);
   a.key = rp_key(seed);
   a.density = density;
-  rp_grids(ctx, r, &a.grid_gen, &a.grid_gram);
+  rp_grids(ctx, r, a.ld, &a.grid_gen, &a.grid_gram);
   char* w = (char*)ws;
   size_t off = 0;
   auto take = [&](size_t nb) { char* q = w + off; off += align_up(nb); return q; };
-  a.S = (double*)take(8 * (size_t)ctx->m * r + 16);
+  a.S = (float*)take(4 * (size_t)ctx->m * a.ld + 16);
   a.Y = (double*)take(8 * (size_t)ctx->n * r + 16);
   a.vpart = (double*)take(8 * (size_t)a.grid_gen * r);
   a.mpart = (double*)take(8 * (size_t)a.grid_gram * r * (r + 1) / 2);
   a.z = (double*)take(8 * (size_t)RP_RMAX);
+  a.colctr = (unsigned*)take(256);
+  a.pol_stream = ctx->seg1.empty() ? 0ull : ctx->seg1[0].pol_first;
   a.p = ctx->p;
   a.x = ctx->x;
   a.col_ptr = ctx->A.col_ptr;
@@ -1254,18 +1258,23 @@ static plss_status rp_args(plss_ctx* ctx, int r, uint64_t seed, double density, 
   return PLSS_OK;
 }
 static void rp_launch_spmm(const RpArgs& a, int grid, cudaStream_t st) {
-  if (a.r <= 2) k_rp_spmm<2, 1><<<grid, RP_NT, 0, st>>>(a);
-  else if (a.r <= 4) k_rp_spmm<4, 1><<<grid, RP_NT, 0, st>>>(a);
-  else if (a.r <= 8) k_rp_spmm<8, 1><<<grid, RP_NT, 0, st>>>(a);
+  if (a.r <= 8) k_rp_spmm<8, 1><<<grid, RP_NT, 0, st>>>(a);
   else if (a.r <= 16) k_rp_spmm<16, 1><<<grid, RP_NT, 0, st>>>(a);
   else if (a.r <= 32) k_rp_spmm<32, 1><<<grid, RP_NT, 0, st>>>(a);
   else k_rp_spmm<32, 2><<<grid, RP_NT, 0, st>>>(a);
 }
-static int rp_spmm_grid(const plss_ctx* ctx, int r) {
-  int g = 1;
+// one resident wave: the kernel takes columns from a global counter
+static int rp_spmm_grid(const plss_ctx* ctx, int r, int ld) {
+  int occ = 1;
+  (void)ld;
+  const void* fn = r <= 8 ? (const void*)k_rp_spmm<8, 1> : r <= 16 ? (const void*)k_rp_spmm<16, 1>
+                 : r <= 32 ? (const void*)k_rp_spmm<32, 1> : (const void*)k_rp_spmm<32, 2>;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, RP_NT, 0) != cudaSuccess || occ < 1) occ = 1;
+  int g = 8;                                        // lanes per column
   while (g < r && g < 32) g <<= 1;
-  const int64_t cols_per_cta = (int64_t)(RP_NT / 32) * (32 / g);
-  return (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + cols_per_cta - 1) / cols_per_cta, 8 * (int64_t)rp_sms(ctx)));
+  const int cpw = 32 / g;                           // columns per warp
+  const int64_t cols_per_cta = (int64_t)(RP_NT / 32) * cpw;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + cols_per_cta - 1) / cols_per_cta, (int64_t)occ * rp_sms(ctx)));
 }
 static plss_status rp_enqueue_step(plss_ctx* ctx) {
   cudaStream_t st = ctx->stream;
@@ -1344,7 +1353,7 @@ plss_status plss_rp_start(plss_ctx* ctx, int32_t r, uint64_t seed, double densit
   for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);   // r_0, rho_0, stop test
   CK(cudaGetLastError());
   ctx->rp = a;
-  ctx->rp_gspmm = rp_spmm_grid(ctx, r);
+  ctx->rp_gspmm = rp_spmm_grid(ctx, r, rp_ld(r));
   ctx->rp_gupd = (int)std::max<int64_t>(1, std::min<int64_t>((n + RP_NT - 1) / RP_NT, 8 * (int64_t)rp_sms(ctx)));
   if (ctx->rp_graph_chunk) { CK(cudaGraphExecDestroy(ctx->rp_graph_chunk)); ctx->rp_graph_chunk = nullptr; }
   if (ctx->rp_graph_one) { CK(cudaGraphExecDestroy(ctx->rp_graph_one)); ctx->rp_graph_one = nullptr; }
@@ -1418,16 +1427,58 @@ plss_status plss_rp_solve(plss_ctx* ctx, int32_t r, uint64_t seed, double densit
   return plss_rp_finish(ctx, x, iters, hist, diag, outcome);
 }
 
-plss_status plss_rp_sketch(plss_ctx* ctx, int32_t r, uint64_t seed, double density, int32_t k, void* workspace,
-                           size_t ws_bytes, double* S) {
-  if (!ctx || !rp_valid(ctx, r, density) || k < 1 || (!S && ctx->m > 0)) return PLSS_E_INVALID;
-  RpArgs a;
-  plss_status ps = rp_args(ctx, r, seed, density, workspace, ws_bytes, &a);
-  if (ps != PLSS_OK) return ps;
+plss_status plss_rp_profile(plss_ctx* ctx, int32_t k, double* ms) {
+  if (!ctx || !ms || k < 1) return PLSS_E_INVALID;
+  if (!ctx->rp_started) { set_err(ctx, "plss_rp_profile before plss_rp_start"); return PLSS_E_STATE; }
+  cudaStream_t st = ctx->stream;
+  const RpArgs& a = ctx->rp;
+  constexpr int NK = 6;
+  cudaEvent_t ev[NK + 1];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[NK] = {0, 0, 0, 0, 0, 0};
+  for (int it = 0; it < k; ++it) {
+    CK(cudaEventRecord(ev[0], st));
+    k_rp_gen<<<a.grid_gen, RP_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[1], st));
+    rp_launch_spmm(a, ctx->rp_gspmm, st);
+    CK(cudaEventRecord(ev[2], st));
+    k_rp_gram<<<a.grid_gram, RP_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[3], st));
+    k_rp_solve<<<1, RP_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[4], st));
+    k_rp_update<<<ctx->rp_gupd, RP_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[5], st));
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
+    CK(cudaEventRecord(ev[6], st));
+    CK(cudaGetLastError());
+    CK(cudaEventSynchronize(ev[6]));
+    for (int j = 0; j < NK; ++j) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
+      acc[j] += t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int j = 0; j < NK; ++j) ms[j] = acc[j] / k;
+  return PLSS_OK;
+}
+
+plss_status plss_rp_sketch(plss_ctx* ctx, int32_t r, uint64_t seed, double density, int32_t k, int32_t ld,
+                           float* S) {
+  if (!ctx || !rp_valid(ctx, r, density) || k < 1 || ld < r || (ld & 1) || ld > 2 * RP_NT || (!S && ctx->m > 0))
+    return PLSS_E_INVALID;
+  RpArgs a{};
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.r = r;
+  a.h = (r + 1) / 2;
+  a.ld = ld;
+  a.key = rp_key(seed);
+  a.density = density;
   a.S = S;
-  a.res = nullptr;
-  a.ctl = nullptr;
   a.k_fixed = k;
+  int gm;
+  rp_grids(ctx, r, ld, &a.grid_gen, &gm);
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
   k_rp_gen<<<a.grid_gen, RP_NT, 0, ctx->stream>>>(a);
   CK(cudaGetLastError());
@@ -1435,20 +1486,25 @@ plss_status plss_rp_sketch(plss_ctx* ctx, int32_t r, uint64_t seed, double densi
   return sync_out(ctx);
 }
 
-plss_status plss_spmmT(plss_ctx* ctx, int32_t r, const double* S, double* Y) {
-  if (!ctx || r < 1 || r > RP_RMAX || (!S && ctx->m > 0) || (!Y && ctx->n > 0)) return PLSS_E_INVALID;
+plss_status plss_spmmT(plss_ctx* ctx, int32_t r, int32_t ld, const float* S, double* Y) {
+  if (!ctx || r < 1 || r > RP_RMAX || ld < r || (!S && ctx->m > 0) || (!Y && ctx->n > 0)) return PLSS_E_INVALID;
   RpArgs a{};
   a.m = ctx->m;
   a.n = ctx->n;
   a.r = r;
-  a.S = const_cast<double*>(S);
+  a.ld = ld;
+  a.S = const_cast<float*>(S);
   a.Y = Y;
   a.col_ptr = ctx->A.col_ptr;
   a.row_idx = ctx->A.row_idx;
   a.val_t = ctx->A.val_t;
+  a.pol_stream = ctx->seg1.empty() ? 0ull : ctx->seg1[0].pol_first;
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
-  rp_launch_spmm(a, rp_spmm_grid(ctx, r), ctx->stream);
+  CK(cudaMallocAsync((void**)&a.colctr, sizeof(unsigned), ctx->stream));
+  CK(cudaMemsetAsync(a.colctr, 0, sizeof(unsigned), ctx->stream));
+  rp_launch_spmm(a, rp_spmm_grid(ctx, r, ld), ctx->stream);
   CK(cudaGetLastError());
+  CK(cudaFreeAsync(a.colctr, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return sync_out(ctx);
 }

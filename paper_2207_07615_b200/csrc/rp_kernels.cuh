@@ -6,14 +6,16 @@
 //   p_k = Y_k (Y_k^T Y_k)^+ S_k^T r_{k-1},  Y_k = A^T S_k,   x_k = x_{k-1} + p_k,  r_k = r_{k-1} - A p_k
 //
 // One iteration = five kernels here + K1 of the PLSS path (r <- r - A p, rho, stop test):
-//   k_rp_gen    S_k (row-major m x r) from the counter-based generator of DESIGN.md reading R7,
-//               fused with the per-CTA partials of v = S_k^T r_{k-1}
-//   k_rp_spmm   Y_k = A^T S_k as a gather over the CSC copy: a group of G lanes per column, lane c
-//               sums column c of Y sequentially in ascending row order (bitwise the oracle's
-//               per-column sequential sums for equal S)
+//   k_rp_gen    S_k (binary32, row-major m x ld, rows padded with zeros to ld = 8 ceil(r/8) floats
+//               = whole 32-byte sectors) from the counter-based generator of DESIGN.md reading R17,
+//               fused with the per-CTA partials of v = S_k^T r_{k-1} (fp64)
+//   k_rp_spmm   Y_k = A^T S_k as a gather over the CSC copy: a group of G lanes per column loads G
+//               (row, value) entries at once (coalesced), broadcasts them by shuffles and keeps 8
+//               row gathers of S in flight per lane; lane c sums column c of Y sequentially in
+//               ascending row order in fp64 (bitwise the oracle's per-column sequential sums)
 //   k_rp_gram   per-CTA partials of the upper triangle of Y_k^T Y_k (fixed order)
 //   k_rp_solve  one CTA: sums the partials in CTA order, pivoted Cholesky of the r x r Gram
-//               matrix truncated at its numerical rank, z = M^+-equivalent solve (reading R8),
+//               matrix truncated at its numerical rank, z = M^+-equivalent solve (reading R18),
 //               iteration counter
 //   k_rp_update p = Y z, x <- x + p
 #pragma once
@@ -23,12 +25,11 @@
 namespace plss {
 
 constexpr int RP_RMAX = 64;        // largest sketch size r
-constexpr int RP_ATT = 64;         // polar-method attempts per pair (P(all rejected) ~ 1e-43)
 constexpr int RP_NT = 256;
 constexpr int RP_TILE = 4096;      // doubles of Y per shared-memory tile of the Gram kernel (32 KB)
 constexpr int RP_PPT = (RP_RMAX * (RP_RMAX + 1) / 2 + RP_NT - 1) / RP_NT;   // Gram pairs per thread
 
-// ---- counter-based sketch generator (reading R7; the oracle implements the same definition) ----
+// ---- counter-based sketch generator (reading R17; the oracle implements the same definition) ----
 __device__ __forceinline__ uint64_t rp_mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -40,49 +41,71 @@ __device__ __forceinline__ uint64_t rp_word(uint64_t key, uint64_t ctr) {
 __device__ __forceinline__ double rp_unit(uint64_t w) {       // 53-bit uniform in [0, 1), exact
   return __dmul_rn((double)(w >> 11), 0x1p-53);
 }
-// ln(s), s in (0, 1): frexp, m in [sqrt(1/2), sqrt(2)), f = (m-1)/(m+1),
-// ln m = 2 f (1 + f^2/3 + ... + f^22/23) by Horner, ln s = e ln2 + ln m; every op correctly
-// rounded, no contraction: bitwise the oracle's ln_unit.
-__device__ __forceinline__ double rp_ln(double s) {
+// ln(s), binary32 s in (0, 1), every op binary32 and correctly rounded (no contraction):
+// frexp, m in [sqrt(1/2), sqrt(2)), f = (m-1)/(m+1), ln m = 2 f (1 + f^2/3 + ... + f^10/11) by
+// Horner, ln s = e ln2 + ln m: bitwise the oracle's ln_unit32.
+__device__ __forceinline__ float rp_ln32(float s) {
   int e;
-  double mt = frexp(s, &e);
-  if (mt < 0.7071067811865476) { mt = __dmul_rn(mt, 2.0); e -= 1; }
-  const double f = __ddiv_rn(__dadd_rn(mt, -1.0), __dadd_rn(mt, 1.0));
-  const double f2 = __dmul_rn(f, f);
-  double t = 1.0 / 23.0;
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 21.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 19.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 17.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 15.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 13.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 11.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 9.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 7.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 5.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0 / 3.0);
-  t = __dadd_rn(__dmul_rn(t, f2), 1.0);
-  return __dadd_rn(__dmul_rn((double)e, 0.6931471805599453), __dmul_rn(__dmul_rn(2.0, f), t));
+  float mt = frexpf(s, &e);
+  if (mt < __uint_as_float(0x3F3504F3u)) { mt = __fmul_rn(mt, 2.0f); e -= 1; }   // RN32(sqrt(1/2))
+  const float f = __fdiv_rn(__fadd_rn(mt, -1.0f), __fadd_rn(mt, 1.0f));
+  const float f2 = __fmul_rn(f, f);
+  float t = 1.0f / 11.0f;
+  t = __fadd_rn(__fmul_rn(t, f2), 1.0f / 9.0f);
+  t = __fadd_rn(__fmul_rn(t, f2), 1.0f / 7.0f);
+  t = __fadd_rn(__fmul_rn(t, f2), 1.0f / 5.0f);
+  t = __fadd_rn(__fmul_rn(t, f2), 1.0f / 3.0f);
+  t = __fadd_rn(__fmul_rn(t, f2), 1.0f);
+  return __fadd_rn(__fmul_rn((float)e, __uint_as_float(0x3F317218u)), __fmul_rn(__fmul_rn(2.0f, f), t));
 }
-// the normal pair (S[i, 2q], S[i, 2q+1]) of pair counter `base` = ((k 2^32 + i) h + q)
-__device__ __forceinline__ void rp_pair(uint64_t key, uint64_t base, double density, double& z0, double& z1) {
-  z0 = 0.0;
-  z1 = 0.0;
-  for (int a = 0; a < RP_ATT; ++a) {
-    const uint64_t c = (base * RP_ATT + (uint64_t)a) * 4ull;
-    const double u = __dadd_rn(__dmul_rn(2.0, rp_unit(rp_word(key, c))), -1.0);
-    const double v = __dadd_rn(__dmul_rn(2.0, rp_unit(rp_word(key, c + 1ull))), -1.0);
-    const double s = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
-    if (s > 0.0 && s < 1.0) {
-      const double f = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, rp_ln(s)), s));
-      z0 = __dmul_rn(u, f);
-      z1 = __dmul_rn(v, f);
-      break;
-    }
+// (sin, cos)(2 pi u2), binary32, u2 in [0, 1) with 24-bit granularity: exact octant reduction,
+// Taylor polynomials on [0, pi/4] by Horner (no contraction), octant symmetries; bitwise the
+// oracle's sincos_2pi32.
+__device__ __forceinline__ void rp_sincos_2pi32(float u2, float& sin_t, float& cos_t) {
+  const float x = __fmul_rn(u2, 8.0f);
+  const int o = (int)x;                                   // floor (x >= 0)
+  float f = __fadd_rn(x, -(float)o);
+  if (o & 1) f = __fadd_rn(1.0f, -f);
+  const float phi = __fmul_rn(f, __uint_as_float(0x3F490FDBu));   // RN32(pi/4)
+  const float p2 = __fmul_rn(phi, phi);
+  float ts = 1.0f / 362880.0f;
+  ts = __fadd_rn(__fmul_rn(ts, p2), -1.0f / 5040.0f);
+  ts = __fadd_rn(__fmul_rn(ts, p2), 1.0f / 120.0f);
+  ts = __fadd_rn(__fmul_rn(ts, p2), -1.0f / 6.0f);
+  ts = __fadd_rn(__fmul_rn(ts, p2), 1.0f);
+  const float sn = __fmul_rn(phi, ts);
+  float cs = -1.0f / 3628800.0f;
+  cs = __fadd_rn(__fmul_rn(cs, p2), 1.0f / 40320.0f);
+  cs = __fadd_rn(__fmul_rn(cs, p2), -1.0f / 720.0f);
+  cs = __fadd_rn(__fmul_rn(cs, p2), 1.0f / 24.0f);
+  cs = __fadd_rn(__fmul_rn(cs, p2), -0.5f);
+  cs = __fadd_rn(__fmul_rn(cs, p2), 1.0f);
+  switch (o) {
+    case 0: sin_t = sn; cos_t = cs; break;
+    case 1: sin_t = cs; cos_t = sn; break;
+    case 2: sin_t = cs; cos_t = -sn; break;
+    case 3: sin_t = sn; cos_t = -cs; break;
+    case 4: sin_t = -sn; cos_t = -cs; break;
+    case 5: sin_t = -cs; cos_t = -sn; break;
+    case 6: sin_t = -cs; cos_t = sn; break;
+    default: sin_t = -sn; cos_t = cs; break;
   }
+}
+// the binary32 normal pair (S[i, 2q], S[i, 2q+1]) of pair counter `base` = ((k 2^32 + i) h + q):
+// Box-Muller from one 64-bit word (no rejection, so warps never diverge)
+__device__ __forceinline__ void rp_pair(uint64_t key, uint64_t base, double density, float& z0, float& z1) {
+  const uint64_t c = base * 256ull;
+  const uint64_t w = rp_word(key, c);
+  const float u1 = __fadd_rn(1.0f, -__fmul_rn((float)(uint32_t)(w >> 40), 0x1p-24f));
+  const float u2 = __fmul_rn((float)(uint32_t)((w >> 16) & 0xFFFFFFull), 0x1p-24f);
+  const float rad = __fsqrt_rn(__fmul_rn(-2.0f, rp_ln32(u1)));
+  float sn, cs;
+  rp_sincos_2pi32(u2, sn, cs);
+  z0 = __fmul_rn(rad, cs);
+  z1 = __fmul_rn(rad, sn);
   if (density < 1.0) {
-    const uint64_t c = base * (uint64_t)(RP_ATT * 4);
-    if (!(rp_unit(rp_word(key, c + 2ull)) < density)) z0 = 0.0;
-    if (!(rp_unit(rp_word(key, c + 3ull)) < density)) z1 = 0.0;
+    if (!(rp_unit(rp_word(key, c + 2ull)) < density)) z0 = 0.0f;
+    if (!(rp_unit(rp_word(key, c + 3ull)) < density)) z1 = 0.0f;
   }
 }
 
@@ -90,10 +113,11 @@ __device__ __forceinline__ void rp_pair(uint64_t key, uint64_t base, double dens
 struct RpArgs {
   int64_t m, n;
   int32_t r, h;              // sketch size, pairs per row = ceil(r/2)
+  int32_t ld;                // row stride of S in floats (even, >= r; 8 ceil(r/8) inside solves)
   uint64_t key;              // mix64(seed)
   double density;            // 1: dense normal S; < 1: each entry kept with this probability
   int64_t k_fixed;           // > 0: generate S_{k_fixed} (test entry point, no ctl)
-  double* S;                 // m x r row-major
+  float* S;                  // m x ld row-major, binary32, columns >= r zero
   double* Y;                 // n x r row-major
   const double* res;         // r_{k-1} (for v = S^T r), or NULL
   double* vpart;             // [grid_gen][r]
@@ -105,6 +129,8 @@ struct RpArgs {
   const int32_t* row_idx;
   const double* val_t;
   int32_t grid_gen, grid_gram;
+  unsigned* colctr;          // k_rp_spmm's column-chunk counter (k_rp_gen of the step zeroes it)
+  uint64_t pol_stream;       // L2 evict-first policy for the index / value streams
   Ctl* ctl;
   double* rec;
 };
@@ -113,30 +139,35 @@ __device__ __forceinline__ bool rp_done(const RpArgs& a) { return a.ctl != nullp
 
 // S_k and v partials. CTA b owns rows [b*per, (b+1)*per); thread t -> pair q = t % h of rows
 // lr = t / h, lr + rpp, ... (rpp = 256 / h rows per pass): consecutive threads write consecutive
-// doubles. v partial of column c: sum over the CTA's threads of that column in lr order.
+// 8-byte pairs; the thread of the last pair also zeroes the row's padding [2h, ld), so whole
+// padded rows are written. v partial of column c: sum over the CTA's threads of that column in
+// lr order.
 __global__ void __launch_bounds__(RP_NT) k_rp_gen(RpArgs a) {
   if (rp_done(a)) return;
+  if (a.colctr && blockIdx.x == 0 && threadIdx.x == 0) *a.colctr = 0u;
   __shared__ double red[2][RP_NT];
-  const int h = a.h, r = a.r;
+  const int h = a.h, r = a.r, ld = a.ld;
   const int rpp = RP_NT / h;
   const int t = threadIdx.x, lr = t / h, q = t % h;
   const uint64_t k = a.k_fixed > 0 ? (uint64_t)a.k_fixed : (uint64_t)(a.ctl->iters + 1);
   const int64_t per = (a.m + gridDim.x - 1) / gridDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(a.m, i0 + per);
   const int c0 = 2 * q;
-  const bool has1 = c0 + 1 < r;
+  const bool tail = q == h - 1;
   double acc0 = 0.0, acc1 = 0.0;
   if (lr < rpp) {
     for (int64_t i = i0 + lr; i < i1; i += rpp) {
-      double z0, z1;
+      float z0, z1;
       rp_pair(a.key, ((k << 32) + (uint64_t)i) * (uint64_t)h + (uint64_t)q, a.density, z0, z1);
-      double* row = a.S + i * r;
-      row[c0] = z0;
-      if (has1) row[c0 + 1] = z1;
+      if (c0 + 1 >= r) z1 = 0.0f;
+      float* row = a.S + i * ld;
+      *reinterpret_cast<float2*>(row + c0) = make_float2(z0, z1);
+      if (tail)
+        for (int c = 2 * h; c < ld; c += 2) *reinterpret_cast<float2*>(row + c) = make_float2(0.0f, 0.0f);
       if (a.res) {
         const double ri = a.res[i];
-        acc0 = __dadd_rn(acc0, __dmul_rn(z0, ri));
-        acc1 = __dadd_rn(acc1, __dmul_rn(z1, ri));
+        acc0 = __dadd_rn(acc0, __dmul_rn((double)z0, ri));
+        acc1 = __dadd_rn(acc1, __dmul_rn((double)z1, ri));
       }
     }
   }
@@ -152,55 +183,82 @@ __global__ void __launch_bounds__(RP_NT) k_rp_gen(RpArgs a) {
   }
 }
 
-// Y = A^T S: G lanes per column (G = pow2 >= r, <= 32), lane g sums columns g, g + G (CPL = 2
-// for r > 32). Entries are taken 4 at a time (independent gathers in flight), added in order.
+__device__ __forceinline__ int ld_stream_i32(const int32_t* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 template <int G, int CPL>
 __global__ void __launch_bounds__(RP_NT) k_rp_spmm(RpArgs a) {
   if (rp_done(a)) return;
-  const int r = a.r;
+  constexpr int U = 8;                              // gathers in flight per lane (16: slower, more
+                                                    // registers, fewer warps)
+  constexpr int CPW = 32 / G;                       // columns per warp
+  const int r = a.r, ld = a.ld;
   const int lane = threadIdx.x & 31;
   const int sub = lane / G, g = lane % G;
-  constexpr int CPW = 32 / G;                       // columns per warp
-  const int64_t warp = ((int64_t)blockIdx.x * RP_NT + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * RP_NT) >> 5;
-  for (int64_t j = warp * CPW + sub; j < a.n; j += nwarps * CPW) {
-    const int b = __ldg(a.col_ptr + j), e = __ldg(a.col_ptr + j + 1);
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (sub * G));
+  const uint64_t pol = a.pol_stream;
+  // Columns are taken CPW at a time from a global counter: every warp works at the same moving
+  // frontier, so the S rows of the band part of neighbouring columns are reused from L2 (a static
+  // grid-stride split lets warps drift apart and loses that reuse).
+  for (;;) {
+    unsigned chunk = 0;
+    if (lane == 0) chunk = atomicAdd(a.colctr, 1u);
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    const int64_t jb = (int64_t)chunk * CPW;
+    if (jb >= a.n) break;
+    const int64_t j = jb + sub;
+    int b = 0, e = 0;
+    if (j < a.n) { b = __ldg(a.col_ptr + j); e = __ldg(a.col_ptr + j + 1); }
     double acc[CPL];
 #pragma unroll
     for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
-    int t = b;
-    for (; t + 4 <= e; t += 4) {
-      int ri[4];
-      double vv[4];
+    int ci = 0;
+    double cv = 0.0;
+    if (b + g < e) { ci = ld_stream_i32(a.row_idx + b + g, pol); cv = ld_stream_f64(a.val_t + b + g, pol); }
+    for (int t0 = b; t0 < e; t0 += G) {             // uniform within the group
+      int ni = 0;
+      double nv = 0.0;
+      if (t0 + G + g < e) { ni = ld_stream_i32(a.row_idx + t0 + G + g, pol); nv = ld_stream_f64(a.val_t + t0 + G + g, pol); }
+      const int cnt = min(G, e - t0);
 #pragma unroll
-      for (int w = 0; w < 4; ++w) { ri[w] = __ldg(a.row_idx + t + w); vv[w] = __ldg(a.val_t + t + w); }
-      double sv[4][CPL];
+      for (int u0 = 0; u0 < G; u0 += U) {
+        if (u0 >= cnt) break;
+        float sv[U][CPL];
+        double vv[U];
 #pragma unroll
-      for (int w = 0; w < 4; ++w)
+        for (int u = 0; u < U; ++u) {
+          const int iu = __shfl_sync(gmask, ci, u0 + u, G);
+          vv[u] = __shfl_sync(gmask, cv, u0 + u, G);
 #pragma unroll
-        for (int u = 0; u < CPL; ++u) {
-          const int c = g + u * G;
-          sv[w][u] = c < r ? __ldg(a.S + (int64_t)ri[w] * r + c) : 0.0;
+          for (int w = 0; w < CPL; ++w) {
+            const int c = g + w * G;
+            sv[u][w] = (u0 + u < cnt && c < r) ? __ldg(a.S + (int64_t)iu * ld + c) : 0.0f;
+          }
         }
 #pragma unroll
-      for (int w = 0; w < 4; ++w)
+        for (int u = 0; u < U; ++u) {
+          if (u0 + u < cnt) {
 #pragma unroll
-        for (int u = 0; u < CPL; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(vv[w], sv[w][u]));
-    }
-    for (; t < e; ++t) {
-      const int ri = __ldg(a.row_idx + t);
-      const double vv = __ldg(a.val_t + t);
-#pragma unroll
-      for (int u = 0; u < CPL; ++u) {
-        const int c = g + u * G;
-        const double sv = c < r ? __ldg(a.S + (int64_t)ri * r + c) : 0.0;
-        acc[u] = __dadd_rn(acc[u], __dmul_rn(vv, sv));
+            for (int w = 0; w < CPL; ++w) acc[w] = __dadd_rn(acc[w], __dmul_rn(vv[u], (double)sv[u][w]));
+          }
+        }
       }
+      ci = ni;
+      cv = nv;
     }
+    if (j < a.n) {
 #pragma unroll
-    for (int u = 0; u < CPL; ++u) {
-      const int c = g + u * G;
-      if (c < r) a.Y[j * r + c] = acc[u];
+      for (int w = 0; w < CPL; ++w) {
+        const int c = g + w * G;
+        if (c < r) __stcs(a.Y + j * r + c, acc[w]);
+      }
     }
   }
 }
@@ -267,7 +325,7 @@ __global__ void __launch_bounds__(RP_NT) k_rp_gram(RpArgs a) {
 // One CTA: M = sum of Gram partials, v = sum of v partials (CTA order), pivoted Cholesky
 // M = P L L^T P^T stopped when the largest remaining pivot <= r eps max_j M_jj (numerical rank),
 // z = P [L11^-T L11^-1 (P^T v)_1 ; 0]. For a consistent system v = Y^T e lies in range(M) and
-// null(M) = null(Y), so Y z equals Y M^+ v (reading R8).
+// null(M) = null(Y), so Y z equals Y M^+ v (reading R18).
 __global__ void __launch_bounds__(RP_NT) k_rp_solve(RpArgs a) {
   if (rp_done(a)) return;
   __shared__ double M[RP_RMAX][RP_RMAX + 1];

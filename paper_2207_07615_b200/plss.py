@@ -27,7 +27,7 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_solve", "plss_start", "plss_step", "plss_finish", "plss_spmv", "plss_spmvT",
            "plss_profile", "plss_query", "plss_destroy", "plss_status_str", "plss_last_error",
            "plss_set_wi", "plss_column_norms", "plss_rp_workspace_bytes", "plss_rp_solve", "plss_rp_start",
-           "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT"]
+           "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile"]
 
 
 class PlssError(RuntimeError):
@@ -107,9 +107,11 @@ def load_library(path: str = None):
     lib.plss_rp_solve.argtypes = [P, I32, U64, D, P, ctypes.c_size_t, P, P, D, I32, I32, P, ctypes.POINTER(I32),
                                   P, P, ctypes.POINTER(ctypes.c_int)]
     lib.plss_rp_solve.restype = st
-    lib.plss_rp_sketch.argtypes = [P, I32, U64, D, I32, P, ctypes.c_size_t, P]
+    lib.plss_rp_sketch.argtypes = [P, I32, U64, D, I32, I32, P]
     lib.plss_rp_sketch.restype = st
-    lib.plss_spmmT.argtypes = [P, I32, P, P]
+    lib.plss_rp_profile.argtypes = [P, I32, P]
+    lib.plss_rp_profile.restype = st
+    lib.plss_spmmT.argtypes = [P, I32, I32, P, P]
     lib.plss_spmmT.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
@@ -418,24 +420,37 @@ def plss_rp_solve(ctx: Ctx, b, r=10, seed=0, density=1.0, x0=None, tol=1e-8, tol
     return res
 
 
-def plss_rp_sketch(ctx: Ctx, r, seed, k, density=1.0, out=None):
-    """S_k (m x r, device) of the randomized-projection generator (test entry point)."""
+def plss_rp_profile(ctx: Ctx, k: int) -> dict:
+    """Average device ms per randomized-projection step of each kernel (CUDA events)."""
+    ms = np.zeros(6)
+    _check(load_library().plss_rp_profile(ctx.handle, int(k), _ptr(ms)), ctx.handle)
+    return dict(zip(["gen", "spmm", "gram", "solve", "update", "k1"], ms.tolist()))
+
+
+def rp_ld(r: int) -> int:
+    """Row stride (floats) of S inside randomized-projection solves: whole 32-byte sectors."""
+    return (int(r) + 7) // 8 * 8
+
+
+def plss_rp_sketch(ctx: Ctx, r, seed, k, density=1.0, ld=None, out=None):
+    """S_k (device float32, m x ld; columns >= r are 0) of the randomized-projection generator."""
     import torch
+    ld = rp_ld(r) if ld is None else int(ld)
     if out is None:
-        out = torch.empty((ctx.m, r), dtype=torch.float64, device=ctx.A.row_ptr.device)
-    wp, nb = _rp_workspace(ctx, r)
+        out = torch.empty((ctx.m, ld), dtype=torch.float32, device=ctx.A.row_ptr.device)
     _check(load_library().plss_rp_sketch(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density),
-                                         int(k), wp, nb, _ptr(out)), ctx.handle)
+                                         int(k), ld, _ptr(out)), ctx.handle)
     return out
 
 
-def plss_spmmT(ctx: Ctx, S, Y=None):
-    """Y = A^T S (S: device m x r row-major) -> device n x r."""
+def plss_spmmT(ctx: Ctx, S, r=None, Y=None):
+    """Y = A^T S[:, :r] (S: device float32 m x ld row-major) -> device float64 n x r."""
     import torch
-    r = int(S.shape[1])
+    ld = int(S.shape[1])
+    r = ld if r is None else int(r)
     if Y is None:
         Y = torch.empty((ctx.n, r), dtype=torch.float64, device=S.device)
-    _check(load_library().plss_spmmT(ctx.handle, r, _ptr(S), _ptr(Y)), ctx.handle)
+    _check(load_library().plss_spmmT(ctx.handle, r, ld, _ptr(S), _ptr(Y)), ctx.handle)
     return Y
 
 

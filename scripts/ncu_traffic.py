@@ -6,8 +6,9 @@ import re
 import subprocess
 import sys
 
-KIND = re.compile(r"k_(?:spmv|sellw?)<(\d)")
-NAME = {"1": "k1_spmv_csr_resid", "2": "k2_spmv_csc_gather", "3": "k2_spmv_csc_gather"}
+KIND = re.compile(r"k_(?:spmv|sellw?)<(\d)|k_rp_(spmm|gen|gram|update)")
+NAME = {"1": "k1_spmv_csr_resid", "2": "k2_spmv_csc_gather", "3": "k2_spmv_csc_gather",
+        "spmm": "rp_spmm_AtS", "gen": "rp_sketch_gen", "gram": "rp_gram", "update": "rp_update"}
 
 
 def main(path, note):
@@ -18,9 +19,10 @@ def main(path, note):
     acc = {}
     for r in rows[2:]:
         m = KIND.search(r[col["Kernel Name"]])
-        if not m or m.group(1) not in NAME:
+        key = m and (m.group(1) or m.group(2))
+        if not key or key not in NAME:
             continue
-        k = NAME[m.group(1)]
+        k = NAME[key]
         rd = float(r[col["dram__bytes_read.sum"]].replace(",", ""))
         wr = float(r[col["dram__bytes_write.sum"]].replace(",", ""))
         t = float(r[col["gpu__time_duration.sum"]].replace(",", ""))

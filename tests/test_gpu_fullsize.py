@@ -125,3 +125,49 @@ def test_c4_full_parity_first_iterations(pkg):
     _assert_parity(res, ref, _floor(s, ref), s)
     empty = np.diff(s.col_ptr) == 0                # x stays in range(A^T): empty columns are 0
     assert empty.any() and np.all(res["xh"][empty] == 0.0)
+
+
+def test_c5_full_randproj_sampled_and_projection(pkg, c5):
+    """Randomized projection (NEXT-2) at C5 scale, r = 5 (Experiment III's choice for n > 1e5,
+    P:L1168-1170): sampled rows of S_k bitwise the oracle generator (rows depend on (seed, k, i)
+    only), sampled columns of A^T S bitwise the oracle's sequential sums over those rows, and the
+    projection property of eq:pkLong: p_k is orthogonal to the new error x* - x_k, with the
+    recursive residual tracking the true one."""
+    from oracle import randproj as orp
+    d, ctx = c5
+    m, n, r = d["m"], d["n"], 5
+    rng = np.random.default_rng(12)
+    S = pkg.plss_rp_sketch(ctx, r, seed=3, k=2)                  # binary32, m x 8
+    rows = np.concatenate([[0], np.sort(rng.choice(m, 4096, replace=False)), [m - 1]])
+    Sh = S[torch.from_numpy(rows).cuda()].cpu().numpy()
+    np.testing.assert_array_equal(Sh[:, :r].astype(np.float64), orp.sketch_rows(3, 2, rows, r))
+    assert not Sh[:, r:].any()
+    # A^T S: the GPU S is checked on samples above; Y's sampled columns are recomputed from the
+    # ORACLE's rows of S (no oracle input comes from the CUDA path)
+    Y = pkg.plss_spmmT(ctx, S, r=r)
+    cols = np.unique(np.concatenate([rng.choice(n, 2048, replace=False), [0, n - 1]]))
+    sp, ri, vt = _sub_csr(d["col_ptr"], d["row_idx"], d["val_t"], cols)
+    Srows = orp.sketch_rows(3, 2, ri, r)
+    loc = np.arange(len(ri), dtype=np.int32)
+    ref = np.stack([oracle.spmv(len(cols), sp, loc, vt, np.ascontiguousarray(Srows[:, c])) for c in range(r)], axis=1)
+    np.testing.assert_array_equal(Y[torch.from_numpy(cols).cuda()].cpu().numpy(), ref)
+    del S, Y
+    torch.cuda.empty_cache()
+    xs = d["x_star"]
+    pkg.plss_rp_start(ctx, d["b"], r=r, seed=3, tol=0.0, maxit=6)
+    x_prev = torch.zeros(n, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(x_prev)
+    ax = torch.empty(m, dtype=torch.float64, device="cuda")
+    nb = float(torch.linalg.norm(d["b"]))
+    for k in range(1, 7):
+        pkg.plss_rp_step(ctx, 1)
+        out = pkg.plss_rp_finish(ctx, x=x, want_hist=True)
+        assert out["iters"] == k
+        p = x - x_prev
+        e = xs - x
+        cosv = float(torch.dot(p, e)) / (float(torch.linalg.norm(p)) * float(torch.linalg.norm(e)))
+        assert abs(cosv) <= 1e-8, (k, cosv)
+        pkg.plss_spmv(ctx, x, ax)
+        true_h = float(torch.linalg.norm(d["b"] - ax)) / nb
+        assert abs(out["hist_full"][k] - true_h) <= 1e-10 * true_h
+        x_prev.copy_(x)

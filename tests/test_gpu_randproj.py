@@ -2,11 +2,11 @@
 oracle (oracle/randproj.py), through the C ABI.
 
 * The sketch S_k: bitwise (both sides implement the same counter-based generator from correctly
-  rounded operations only, reading R7), dense and sparse, ragged row counts, r odd/even.
+  rounded operations only, reading R17), dense and sparse, ragged row counts, r odd/even.
 * Y = A^T S (plss_spmmT): bitwise the oracle's per-column sequential sums.
 * Solves: hist within 1e-9 (relative) over the iterations, final x within 1e-7, equal iteration
   counts, outcomes and Gram ranks; the rank-deficient r > n case (pseudo-inverse branch, reading
-  R8) reaches A^+ b in one step.
+  R18) reaches A^+ b in one step.
 """
 import numpy as np
 import pytest
@@ -52,9 +52,11 @@ def _small(seed=0, m=1000, n=300, per_row=6):
 def test_sketch_bitwise(pkg, r, density):
     s = _small(m=10_007 if r <= 10 else 2_003)
     ctx = _ctx(pkg, s)
-    for k in (1, 7):
-        S = pkg.plss_rp_sketch(ctx, r, seed=123, k=k, density=density).cpu().numpy()
-        np.testing.assert_array_equal(S, rp.sketch(123, k, s.m, r, density))
+    for k, ld in ((1, None), (7, r + (r & 1))):
+        S = pkg.plss_rp_sketch(ctx, r, seed=123, k=k, density=density, ld=ld).cpu().numpy()
+        assert S.dtype == np.float32 and S.shape[1] >= r
+        np.testing.assert_array_equal(S[:, :r].astype(np.float64), rp.sketch(123, k, s.m, r, density))
+        assert not S[:, r:].any()
     pkg.plss_destroy(ctx)
 
 
@@ -65,7 +67,9 @@ def test_spmmT_bitwise(pkg, case, r):
          "C3_64": lambda: plss_gen.make_config("C3", N=64)}[case]()
     ctx = _ctx(pkg, s)
     S = rp.sketch(5, 1, s.m, r)
-    Y = pkg.plss_spmmT(ctx, torch.from_numpy(S).cuda()).cpu().numpy()
+    S32 = np.zeros((s.m, pkg.rp_ld(r)), dtype=np.float32)
+    S32[:, :r] = S
+    Y = pkg.plss_spmmT(ctx, torch.from_numpy(S32).cuda(), r=r).cpu().numpy()
     ref = np.stack([oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, np.ascontiguousarray(S[:, c]))
                     for c in range(r)], axis=1)
     np.testing.assert_array_equal(Y, ref)

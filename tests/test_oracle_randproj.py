@@ -8,8 +8,9 @@ mathematics fix, independent of the oracle's own route (pinv of the r x r Gram m
 * r = m (a square, almost surely invertible S): range(A^T S) = range(A^T), one step reaches the
   minimum-norm solution A^+ b from x0 = 0 -- and for m > n the Gram matrix S^T A A^T S is
   singular, so this exercises the pseudo-inverse branch (L166-167).
-* The sampler: ln_unit against math.log, moments and Kolmogorov-Smirnov statistic of S against
-  N(0, 1), independence of iterations / seeds, the sparse density.
+* The sampler (Box-Muller in binary32): ln_unit32 and sincos_2pi32 against libm, moments and
+  Kolmogorov-Smirnov statistic of S against N(0, 1), independence of iterations / seeds, the
+  sparse density.
 """
 import math
 
@@ -31,15 +32,34 @@ def _system(seed=0, m=60, n=25, dens=0.3):
     return A.tocsr(), xs, A @ xs
 
 
-def test_ln_unit_matches_libm():
-    rng = np.random.default_rng(0)
-    s = np.concatenate([rng.random(20000), [1e-300, 2.0 ** -1074, 0.5, 0.7071067811865476,
-                                            0.7071067811865475, 1 - 2.0 ** -53]])
+def test_sincos_2pi32_matches_libm():
+    assert rp.PI4_32.view(np.uint32) == 0x3F490FDB
+    u2 = np.concatenate([np.arange(0, 1 << 24, 997), np.arange(8) << 21, (np.arange(8) << 21) + 1,
+                         (np.arange(1, 9) << 21) - 1]).astype(np.float32) * np.float32(2.0 ** -24)
+    sn, cs = rp.sincos_2pi32(u2)
+    assert sn.dtype == np.float32 and cs.dtype == np.float32
+    th = 2 * np.pi * u2.astype(np.float64)
+    assert np.max(np.abs(sn - np.sin(th))) <= 3e-7 and np.max(np.abs(cs - np.cos(th))) <= 3e-7
+    assert np.max(np.abs(sn.astype(np.float64) ** 2 + cs.astype(np.float64) ** 2 - 1)) <= 1e-6
+
+
+def test_ln_unit32_matches_libm_and_constants():
+    assert rp.LN2_32.view(np.uint32) == 0x3F317218 and rp.SQRT_HALF_32.view(np.uint32) == 0x3F3504F3
+    assert abs(float(rp.LN2_32) - math.log(2)) <= np.spacing(np.float32(0.69)) / 2
+    rng = np.random.default_rng(1)
+    s = np.concatenate([rng.random(20000).astype(np.float32), np.float32([2.0 ** -46, 0.5, 0.70710677,
+                                                                         0.7071068, 1 - 2.0 ** -24])])
     s = s[s > 0]
-    got = rp.ln_unit(s)
-    ref = np.array([math.log(v) for v in s])
-    ulps = np.abs(got - ref) / np.spacing(np.abs(ref))
+    got = rp.ln_unit32(s)
+    assert got.dtype == np.float32
+    ref = np.array([math.log(float(v)) for v in s])
+    ulps = np.abs(got.astype(np.float64) - ref) / np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
     assert ulps.max() <= 3
+
+
+def test_sketch_entries_are_binary32():
+    S = rp.sketch(4, 3, 3000, 7, density=0.5)
+    np.testing.assert_array_equal(S.astype(np.float32).astype(np.float64), S)
 
 
 def test_sketch_is_standard_normal():
