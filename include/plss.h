@@ -214,6 +214,36 @@ plss_status plss_rp_sketch(plss_ctx *ctx, int32_t r, uint64_t seed, double densi
                            int32_t ld, float *S);
 plss_status plss_spmmT(plss_ctx *ctx, int32_t r, int32_t ld, const float *S, double *Y);
 
+/* ---- PLSS Kaczmarz (section 7) ----
+ * Identity-column sketches S_k = [e_{i_1} .. e_{i_k}] in the caller's row order `rows`, with the
+ * history-corrected row action eq:pkKacz (L952-956):
+ *   d = Theta^{-1/2} P^T a_i (P^T a_i read from the stored [A p_1 .. A p_{k-1}], L961-966),
+ *   gamma = r_{k-1}[i] / ((||a_i|| - ||d||)(||a_i|| + ||d||)), p_k = gamma (a_i - P Theta^{-1} P^T a_i),
+ *   x_k = x_{k-1} + p_k, r_k = r_{k-1} - A p_k; stop test as plss_solve.
+ * A row with ||a_i||^2 - ||d||^2 <= 1e-14 ||a_i||^2 (already in the span of the history, or empty)
+ * or r_{k-1}[i] = 0 (already satisfied) is skipped: p_k = 0, nothing is appended, the step still
+ * counts (reading R20). After kmax stored updates
+ * the history P, A P, Theta is cleared and later updates start a new one at the current x (R21).
+ * Single-device ctx (E_INVALID on a distributed one); shares the ctx's r, p, x, control block and
+ * history like randomized projection. rows: host or dev, maxit int32 row indices in [0, m)
+ * (E_INVALID otherwise). workspace: dev, 256-byte aligned, >= plss_kz_workspace_bytes(ctx, kmax)
+ * = 8 (n + m) kmax bytes for P and A P + O(m + n + kmax); alive until plss_kz_finish.
+ * record k of `diag` = {hist_k, rho_k, skipped (0/1), gamma, theta_k, history size after step}. */
+size_t plss_kz_workspace_bytes(const plss_ctx *ctx, int32_t kmax); /* 0 on invalid input */
+plss_status plss_kz_solve(plss_ctx *ctx, int32_t kmax, void *workspace, size_t ws_bytes,
+                          const int32_t *rows, const double *b, const double *x0, double tol,
+                          int32_t tol_mode, int32_t maxit, double *x, int32_t *iters, double *hist,
+                          double *diag, plss_outcome *outcome);
+plss_status plss_kz_start(plss_ctx *ctx, int32_t kmax, void *workspace, size_t ws_bytes,
+                          const int32_t *rows, const double *b, const double *x0, double tol,
+                          int32_t tol_mode, int32_t maxit);
+plss_status plss_kz_step(plss_ctx *ctx, int32_t k);
+plss_status plss_kz_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
+                           plss_outcome *outcome);
+/* Per-kernel device ms per step (CUDA events, one kernel at a time) after plss_kz_start; ms (host,
+ * 4 doubles): row preparation, the P GEMV + update, A p_k (SpMV), residual + record. */
+plss_status plss_kz_profile(plss_ctx *ctx, int32_t k, double *ms);
+
 void plss_destroy(plss_ctx *ctx);
 const char *plss_status_str(plss_status s);
 const char *plss_last_error(const plss_ctx *ctx); /* NULL ctx: last error of create calls */

@@ -16,7 +16,8 @@ P_{k-1}^T a_{i_k} is read from the stored [A p_1 ... A p_{k-1}] (row i_k of that
 L961-966: (A p_j)_i = a_i^T p_j); A p_k is computed once per step and appended; the residual is
 carried as r_k = r_{k-1} - A p_k (reading R19's recursive residual; e_{i_k}^T (b - A x_{k-1}) is
 r_{k-1}[i_k]). Readings (R20, R21): a row with ||a||^2 - ||d||^2 <= 1e-14 ||a||^2 (in
-the span of the history, or empty) is skipped (p_k = 0, nothing appended); after `kmax` stored
+the span of the history, or empty) or already satisfied (r_{k-1}[i_k] = 0: p_k = 0, and a zero
+column would make Theta singular) is skipped (p_k = 0, nothing appended); after `kmax` stored
 updates the history is cleared and the next updates start a new history at the current x.
 
 Parity pins (tests/test_oracle_kaczmarz.py): the worked diag(2,1) example (SPEC.md L326-349:
@@ -69,7 +70,7 @@ def kz_solve(A, b, rows, maxit, tol=0.0, tol_mode=0, x0=None, kmax=None, keep=Fa
             dd = float(np.sum(g * g / th)) if len(g) else 0.0      # ||d||^2
             na, nd = np.sqrt(aa), np.sqrt(dd)
             denom = (na - nd) * (na + nd)
-            if aa == 0.0 or denom <= SKIP_REL * aa:
+            if aa == 0.0 or denom <= SKIP_REL * aa or r[i] == 0.0:
                 skipped += 1                            # reading R20
                 p = None
             else:

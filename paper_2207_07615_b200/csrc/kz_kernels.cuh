@@ -1,0 +1,175 @@
+// kz_kernels.cuh -- sm_100a device code of PLSS Kaczmarz (section 7,
+// L931-967): identity-column sketches S_k = [e_{i_1} .. e_{i_k}] in a given row order, so
+// y_k = a_{i_k} (row i_k of A) and, with the orthogonal history P_{k-1}, Theta_{k-1} = diag(p_j^T p_j)
+// (eq:pkKacz, L952-956):
+//
+//   d = Theta^{-1/2} P^T a_i,   gamma = r_{k-1}[i] / ((||a_i|| - ||d||)(||a_i|| + ||d||)),
+//   p_k = gamma (a_i - P Theta^{-1} P^T a_i),   x_k = x_{k-1} + p_k,   r_k = r_{k-1} - A p_k
+//
+// P^T a_i is row i of the stored [A p_1 .. A p_{k-1}] (L961-966), so a step costs one pass over
+// the n x hk history P (the GEMV, the HBM-bound part), one SpMV for A p_k and vector work:
+//   k_kz_prep   one CTA: swap the dense copy of row i into `arow`, ||a_i||^2, g_j = AP[j][i],
+//               w_j = g_j / theta_j, ||d||^2, gamma, skip flag (reading R20: row in the span of
+//               the history, empty, or already satisfied)
+//   k_kz_gemv   p_l = gamma (arow_l - sum_j P[j][l] w_j) (ascending j), p -> pk and P[:, hk],
+//               x += p, per-CTA partials of theta = p^T p
+//   (SpMV)      apk = A pk (the PLSS K1 segments in plain mode)
+//   k_kz_resid  r -= apk, rho, AP[:, hk] = apk; last CTA: theta_hk, hk++ (reset at kmax, R21),
+//               iteration record, stop test
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace plss {
+
+constexpr int KZ_NT = 256;
+constexpr double KZ_SKIP_REL = 1e-14;
+
+struct KzState {
+  int32_t hk;        // stored updates in the history
+  int32_t skip;      // this step's row is skipped (p = 0)
+  int32_t prev_row;  // row whose entries sit in arow (-1: none)
+  int32_t skipped;   // rows skipped so far
+  double gamma;
+};
+
+struct KzArgs {
+  int64_t m, n;
+  int32_t kmax;
+  const int32_t* row_ptr;    // CSR of A (borrowed)
+  const int32_t* col_idx;
+  const double* val;
+  const int32_t* rows;       // row schedule, one per step
+  double* P;                 // n x kmax, column j at P + j n
+  double* AP;                // m x kmax, column j = A p_j
+  double* theta;             // [kmax]
+  double* w;                 // [kmax] Theta^{-1} P^T a_i
+  double* arow;              // [n] dense copy of the current row, zero elsewhere
+  double* pk;                // [n] the current update (input of the SpMV)
+  double* apk;               // [m] A p_k
+  double* r;
+  double* x;
+  double* part_th;           // [grid_gemv] theta partials
+  double* part_rho;          // [2 grid_res] rho partials (publish_and_elect pairs)
+  unsigned* counter;
+  KzState* st;
+  Ctl* ctl;
+  double* rec;
+  int32_t grid_gemv, grid_res;
+};
+
+__device__ __forceinline__ bool kz_done(const KzArgs& a) { return a.ctl->done != 0; }
+
+__global__ void __launch_bounds__(KZ_NT) k_kz_prep(KzArgs a) {
+  if (kz_done(a)) return;
+  __shared__ double sm[2][MAXW];
+  const int t = threadIdx.x;
+  KzState* st = a.st;
+  const int i = a.rows[a.ctl->iters];
+  const int prev = st->prev_row;
+  if (prev >= 0)
+    for (int e = a.row_ptr[prev] + t; e < a.row_ptr[prev + 1]; e += KZ_NT) a.arow[a.col_idx[e]] = 0.0;
+  __syncthreads();
+  double aa = 0.0, dd = 0.0;
+  for (int e = a.row_ptr[i] + t; e < a.row_ptr[i + 1]; e += KZ_NT) {
+    const double v = a.val[e];
+    a.arow[a.col_idx[e]] = v;
+    aa = __dadd_rn(aa, __dmul_rn(v, v));
+  }
+  const int hk = st->hk;
+  for (int j = t; j < hk; j += KZ_NT) {
+    const double g = a.AP[(int64_t)j * a.m + i];
+    const double th = a.theta[j];
+    a.w[j] = __ddiv_rn(g, th);
+    dd = __dadd_rn(dd, __ddiv_rn(__dmul_rn(g, g), th));
+  }
+  block_sum2(aa, dd, sm);
+  if (t == 0) {
+    const double na = __dsqrt_rn(aa), nd = __dsqrt_rn(dd);
+    const double denom = __dmul_rn(__dadd_rn(na, -nd), __dadd_rn(na, nd));
+    const double ri = a.r[i];
+    const bool skip = aa == 0.0 || denom <= KZ_SKIP_REL * aa || ri == 0.0;   // reading R20
+    st->skip = skip ? 1 : 0;
+    st->gamma = skip ? 0.0 : __ddiv_rn(ri, denom);
+    st->prev_row = i;
+    if (skip) st->skipped += 1;
+  }
+}
+
+// p = gamma (arow - P w). CTA b owns a contiguous range of l; each thread walks its l's and sums
+// the hk history columns in ascending j, 8 loads in flight.
+__global__ void __launch_bounds__(KZ_NT) k_kz_gemv(KzArgs a) {
+  if (kz_done(a)) return;
+  __shared__ double sm[2][MAXW];
+  const KzState* st = a.st;
+  const int hk = st->hk, skip = st->skip;
+  const double gamma = st->gamma;
+  const int64_t per = (a.n + gridDim.x - 1) / gridDim.x;
+  const int64_t l0 = (int64_t)blockIdx.x * per, l1 = min(a.n, l0 + per);
+  double* Pnew = a.P + (int64_t)hk * a.n;
+  double th = 0.0, zero = 0.0;
+  for (int64_t l = l0 + threadIdx.x; l < l1; l += KZ_NT) {
+    double t = 0.0;
+    const double* col = a.P + l;
+    int j = 0;
+    for (; j + 8 <= hk; j += 8) {
+      double pv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pv[u] = __ldg(col + (int64_t)(j + u) * a.n);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t = __dadd_rn(t, __dmul_rn(pv[u], __ldg(a.w + j + u)));
+    }
+    for (; j < hk; ++j) t = __dadd_rn(t, __dmul_rn(__ldg(col + (int64_t)j * a.n), __ldg(a.w + j)));
+    const double p = skip ? 0.0 : __dmul_rn(gamma, __dadd_rn(a.arow[l], -t));
+    a.pk[l] = p;
+    if (!skip) {
+      Pnew[l] = p;
+      a.x[l] = __dadd_rn(a.x[l], p);
+    }
+    th = __dadd_rn(th, __dmul_rn(p, p));
+  }
+  block_sum2(th, zero, sm);
+  if (threadIdx.x == 0) a.part_th[blockIdx.x] = th;
+}
+
+__global__ void __launch_bounds__(KZ_NT) k_kz_resid(KzArgs a) {
+  if (kz_done(a)) return;
+  __shared__ double sm[2][MAXW];
+  const KzState* st = a.st;
+  const int hk = st->hk, skip = st->skip;
+  const int64_t per = (a.m + gridDim.x - 1) / gridDim.x;
+  const int64_t l0 = (int64_t)blockIdx.x * per, l1 = min(a.m, l0 + per);
+  double* APnew = a.AP + (int64_t)hk * a.m;
+  double rho = 0.0, zero = 0.0;
+  for (int64_t l = l0 + threadIdx.x; l < l1; l += KZ_NT) {
+    const double q = a.apk[l];
+    const double rl = __dadd_rn(a.r[l], -q);
+    a.r[l] = rl;
+    if (!skip) APnew[l] = q;
+    rho = __dadd_rn(rho, __dmul_rn(rl, rl));
+  }
+  if (!publish_and_elect(rho, zero, a.part_rho, a.part_rho, gridDim.x, a.counter, sm)) return;
+  if (threadIdx.x != 0) return;
+  KzState* ws = a.st;
+  Ctl* c = a.ctl;
+  double thv = 0.0;
+  for (int g = 0; g < a.grid_gemv; ++g) thv = __dadd_rn(thv, a.part_th[g]);
+  if (!skip) {
+    a.theta[hk] = thv;
+    ws->hk = (hk + 1 == a.kmax) ? 0 : hk + 1;          // reading R21: history reset at kmax
+  }
+  const int k = c->iters + 1;
+  c->iters = k;
+  const double h = __ddiv_rn(__dsqrt_rn(rho), c->nbd);
+  double* rk = a.rec + (size_t)k * REC;
+  rk[0] = h;
+  rk[1] = rho;
+  rk[2] = (double)skip;
+  rk[3] = ws->gamma;
+  rk[4] = thv;
+  rk[5] = (double)ws->hk;
+  c->rho = rho;
+  if (rho == 0.0 || h <= c->tol) { c->done = 1; c->outcome = OUT_CONVERGED; }
+}
+
+}  // namespace plss

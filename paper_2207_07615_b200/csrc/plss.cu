@@ -11,6 +11,7 @@
 #include "../../include/plss.h"
 #include "plss_kernels.cuh"
 #include "rp_kernels.cuh"
+#include "kz_kernels.cuh"
 
 #include <nccl.h>
 
@@ -219,6 +220,11 @@ struct plss_ctx {
   RpArgs rp{};
   int rp_gspmm = 1, rp_gupd = 1;
   cudaGraphExec_t rp_graph_chunk = nullptr, rp_graph_one = nullptr;
+  // PLSS Kaczmarz (plss_kz_*): shares r, p, x, ctl, rec and the K1 segments
+  bool kz_started = false;
+  KzArgs kz{};
+  std::vector<SpmvSeg> kz_seg;   // K1 segments in plain mode: apk = A pk
+  cudaGraphExec_t kz_graph_chunk = nullptr, kz_graph_one = nullptr;
   std::string err;
 };
 
@@ -976,6 +982,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
   CK(cudaGetLastError());
   ctx->started = true;
   ctx->rp_started = false;
+  ctx->kz_started = false;
   ctx->maxit = maxit;
   ctx->flags = flags;
   return PLSS_OK;
@@ -1194,6 +1201,102 @@ plss_status plss_column_norms(plss_ctx* ctx, double* c) {
 
 }  // extern "C"
 
+// ---- shared by the alternative methods (randomized projection, PLSS Kaczmarz) -------------------
+// copy out x / iters / history of a run that uses the ctx's x, ctl and rec
+static plss_status alt_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
+                              plss_outcome* outcome) {
+  cudaStream_t st = ctx->stream;
+  if (x && ctx->n > 0)
+    CK(cudaMemcpyAsync(x, ctx->x, 8 * (size_t)ctx->n, is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  std::vector<double> rec;
+  if (hist || diag) {
+    rec.resize((size_t)(ctx->maxit + 1) * REC);
+    CK(cudaMemcpyAsync(rec.data(), ctx->rec, 8 * rec.size(), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (sync_out(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  const Ctl& c = *ctx->h_ctl;
+  if (iters) *iters = c.iters;
+  if (outcome) *outcome = c.done ? (plss_outcome)c.outcome : (c.iters >= c.maxit ? PLSS_MAXIT : PLSS_RUNNING);
+  if (hist) for (int k = 0; k <= ctx->maxit; ++k) hist[k] = rec[(size_t)k * REC];
+  if (diag) memcpy(diag, rec.data(), 8 * rec.size());
+  return PLSS_OK;
+}
+// launch up to maxit steps (graphs of ctx->chunk), <= 2 chunks in flight, stop once done
+static plss_status alt_run(plss_ctx* ctx, cudaGraphExec_t gchunk, cudaGraphExec_t gone, int maxit) {
+  cudaStream_t st = ctx->stream;
+  int issued = 0, slot = 0;
+  bool pending[2] = {false, false};
+  while (issued < maxit) {
+    if (maxit - issued >= ctx->chunk) {
+      CK(cudaGraphLaunch(gchunk, st));
+      issued += ctx->chunk;
+    } else {
+      for (int i = issued; i < maxit; ++i) CK(cudaGraphLaunch(gone, st));
+      issued = maxit;
+    }
+    CK(cudaMemcpyAsync(&ctx->h_done[slot], &ctx->ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ctx->ev[slot], st));
+    pending[slot] = true;
+    slot ^= 1;
+    if (pending[slot]) {
+      CK(cudaEventSynchronize(ctx->ev[slot]));
+      pending[slot] = false;
+      if (ctx->h_done[slot]) break;
+    }
+  }
+  return PLSS_OK;
+}
+static plss_status alt_build_graph(plss_ctx* ctx, plss_status (*enqueue)(plss_ctx*), int iters, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  plss_status st = PLSS_OK;
+  for (int i = 0; i < iters && st == PLSS_OK; ++i) st = enqueue(ctx);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (st != PLSS_OK) return st;
+  CK(e);
+  CK(cudaGraphInstantiate(out, g, 0));
+  CK(cudaGraphDestroy(g));
+  return PLSS_OK;
+}
+// common start of an alternative method: control block, history, r = b, x = p = x0 (or 0), ||b||,
+// then K1 over the slabs: r_0 = b - A x0, rho_0, record 0 and the stop test
+static plss_status alt_start(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
+                             int32_t maxit) {
+  cudaStream_t st = ctx->stream;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  const int64_t m = ctx->m, n = ctx->n;
+  Ctl& c = *ctx->h_ctl;
+  memset(&c, 0, sizeof c);
+  c.nbd = 1.0;
+  c.tol = tol;
+  c.maxit = maxit;
+  c.tol_mode = tol_mode;
+  c.outcome = OUT_RUNNING;
+  CK(cudaMemcpyAsync(ctx->ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->rec, 0, 8 * (size_t)(maxit + 1) * REC, st));
+  if (m > 0) CK(cudaMemcpyAsync(ctx->r, b, 8 * (size_t)m, is_device_ptr(b) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (n > 0) {
+    if (x0) {
+      const cudaMemcpyKind kind = is_device_ptr(x0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+      CK(cudaMemcpyAsync(ctx->p, x0, 8 * (size_t)n, kind, st));   // K1 below gathers x0: r = b - A x0
+      CK(cudaMemcpyAsync(ctx->x, x0, 8 * (size_t)n, kind, st));
+    } else {
+      CK(cudaMemsetAsync(ctx->p, 0, 8 * (size_t)n, st));
+      CK(cudaMemsetAsync(ctx->x, 0, 8 * (size_t)n, st));
+    }
+  }
+  k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 1, nullptr);
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
+  CK(cudaGetLastError());
+  ctx->started = false;          // the PLSS loop state is overwritten
+  ctx->rp_started = false;
+  ctx->kz_started = false;
+  ctx->maxit = maxit;
+  return PLSS_OK;
+}
+
 // ---- randomized projection (rp_kernels.cuh) ----------------------------------
 static int rp_sms(const plss_ctx* ctx) {
   int sms = 148;
@@ -1288,18 +1391,6 @@ static plss_status rp_enqueue_step(plss_ctx* ctx) {
   CK(cudaGetLastError());
   return PLSS_OK;
 }
-static plss_status rp_build_graph(plss_ctx* ctx, int iters, cudaGraphExec_t* out) {
-  cudaGraph_t g;
-  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  plss_status st = PLSS_OK;
-  for (int i = 0; i < iters && st == PLSS_OK; ++i) st = rp_enqueue_step(ctx);
-  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
-  if (st != PLSS_OK) return st;
-  CK(e);
-  CK(cudaGraphInstantiate(out, g, 0));
-  CK(cudaGraphDestroy(g));
-  return PLSS_OK;
-}
 
 extern "C" {
 
@@ -1326,42 +1417,16 @@ plss_status plss_rp_start(plss_ctx* ctx, int32_t r, uint64_t seed, double densit
   a.ctl = ctx->ctl;
   a.rec = ctx->rec;
   a.k_fixed = 0;
-  cudaStream_t st = ctx->stream;
-  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
-  const int64_t m = ctx->m, n = ctx->n;
-  Ctl& c = *ctx->h_ctl;
-  memset(&c, 0, sizeof c);
-  c.nbd = 1.0;
-  c.tol = tol;
-  c.maxit = maxit;
-  c.tol_mode = tol_mode;
-  c.outcome = OUT_RUNNING;
-  CK(cudaMemcpyAsync(ctx->ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(ctx->rec, 0, 8 * (size_t)(maxit + 1) * REC, st));
-  if (m > 0) CK(cudaMemcpyAsync(ctx->r, b, 8 * (size_t)m, is_device_ptr(b) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-  if (n > 0) {
-    if (x0) {
-      const cudaMemcpyKind kind = is_device_ptr(x0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-      CK(cudaMemcpyAsync(ctx->p, x0, 8 * (size_t)n, kind, st));   // K1 below gathers x0: r = b - A x0
-      CK(cudaMemcpyAsync(ctx->x, x0, 8 * (size_t)n, kind, st));
-    } else {
-      CK(cudaMemsetAsync(ctx->p, 0, 8 * (size_t)n, st));
-      CK(cudaMemsetAsync(ctx->x, 0, 8 * (size_t)n, st));
-    }
-  }
-  k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 1, nullptr);
-  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);   // r_0, rho_0, stop test
-  CK(cudaGetLastError());
+  if ((ps = alt_start(ctx, b, x0, tol, tol_mode, maxit)) != PLSS_OK) return ps;
+  const int64_t n = ctx->n;
   ctx->rp = a;
   ctx->rp_gspmm = rp_spmm_grid(ctx, r, rp_ld(r));
   ctx->rp_gupd = (int)std::max<int64_t>(1, std::min<int64_t>((n + RP_NT - 1) / RP_NT, 8 * (int64_t)rp_sms(ctx)));
   if (ctx->rp_graph_chunk) { CK(cudaGraphExecDestroy(ctx->rp_graph_chunk)); ctx->rp_graph_chunk = nullptr; }
   if (ctx->rp_graph_one) { CK(cudaGraphExecDestroy(ctx->rp_graph_one)); ctx->rp_graph_one = nullptr; }
-  if ((ps = rp_build_graph(ctx, ctx->chunk, &ctx->rp_graph_chunk)) != PLSS_OK) return ps;
-  if ((ps = rp_build_graph(ctx, 1, &ctx->rp_graph_one)) != PLSS_OK) return ps;
-  ctx->started = false;          // the PLSS loop state is overwritten
+  if ((ps = alt_build_graph(ctx, rp_enqueue_step, ctx->chunk, &ctx->rp_graph_chunk)) != PLSS_OK) return ps;
+  if ((ps = alt_build_graph(ctx, rp_enqueue_step, 1, &ctx->rp_graph_one)) != PLSS_OK) return ps;
   ctx->rp_started = true;
-  ctx->maxit = maxit;
   return PLSS_OK;
 }
 
@@ -1378,23 +1443,7 @@ plss_status plss_rp_finish(plss_ctx* ctx, double* x, int32_t* iters, double* his
                            plss_outcome* outcome) {
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->rp_started) { set_err(ctx, "plss_rp_finish before plss_rp_start"); return PLSS_E_STATE; }
-  cudaStream_t st = ctx->stream;
-  if (x && ctx->n > 0)
-    CK(cudaMemcpyAsync(x, ctx->x, 8 * (size_t)ctx->n, is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-  std::vector<double> rec;
-  if (hist || diag) {
-    rec.resize((size_t)(ctx->maxit + 1) * REC);
-    CK(cudaMemcpyAsync(rec.data(), ctx->rec, 8 * rec.size(), cudaMemcpyDeviceToHost, st));
-  }
-  CK(cudaStreamSynchronize(st));
-  if (sync_out(ctx) != PLSS_OK) return PLSS_E_CUDA;
-  const Ctl& c = *ctx->h_ctl;
-  if (iters) *iters = c.iters;
-  if (outcome) *outcome = c.done ? (plss_outcome)c.outcome : (c.iters >= c.maxit ? PLSS_MAXIT : PLSS_RUNNING);
-  if (hist) for (int k = 0; k <= ctx->maxit; ++k) hist[k] = rec[(size_t)k * REC];
-  if (diag) memcpy(diag, rec.data(), 8 * rec.size());
-  return PLSS_OK;
+  return alt_finish(ctx, x, iters, hist, diag, outcome);
 }
 
 plss_status plss_rp_solve(plss_ctx* ctx, int32_t r, uint64_t seed, double density, void* workspace,
@@ -1403,27 +1452,7 @@ plss_status plss_rp_solve(plss_ctx* ctx, int32_t r, uint64_t seed, double densit
                           plss_outcome* outcome) {
   plss_status s = plss_rp_start(ctx, r, seed, density, workspace, ws_bytes, b, x0, tol, tol_mode, maxit);
   if (s != PLSS_OK) return s;
-  cudaStream_t st = ctx->stream;
-  int issued = 0, slot = 0;
-  bool pending[2] = {false, false};
-  while (issued < maxit) {
-    if (maxit - issued >= ctx->chunk) {
-      CK(cudaGraphLaunch(ctx->rp_graph_chunk, st));
-      issued += ctx->chunk;
-    } else {
-      for (int i = issued; i < maxit; ++i) CK(cudaGraphLaunch(ctx->rp_graph_one, st));
-      issued = maxit;
-    }
-    CK(cudaMemcpyAsync(&ctx->h_done[slot], &ctx->ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(ctx->ev[slot], st));
-    pending[slot] = true;
-    slot ^= 1;
-    if (pending[slot]) {
-      CK(cudaEventSynchronize(ctx->ev[slot]));
-      pending[slot] = false;
-      if (ctx->h_done[slot]) break;
-    }
-  }
+  if ((s = alt_run(ctx, ctx->rp_graph_chunk, ctx->rp_graph_one, maxit)) != PLSS_OK) return s;
   return plss_rp_finish(ctx, x, iters, hist, diag, outcome);
 }
 
@@ -1511,6 +1540,171 @@ plss_status plss_spmmT(plss_ctx* ctx, int32_t r, int32_t ld, const float* S, dou
 
 }  // extern "C"
 
+// ---- PLSS Kaczmarz (kz_kernels.cuh) ------------------------------------------
+static void kz_grids(const plss_ctx* ctx, int* g_gemv, int* g_res) {
+  const int sms = rp_sms(ctx);
+  *g_gemv = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + KZ_NT - 1) / KZ_NT, 4 * (int64_t)sms));
+  *g_res = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + KZ_NT - 1) / KZ_NT, 4 * (int64_t)sms));
+}
+static size_t kz_bytes(const plss_ctx* ctx, int kmax) {
+  int gg, gr;
+  kz_grids(ctx, &gg, &gr);
+  const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
+  return align_up(8 * n * K) + align_up(8 * m * K) + 2 * align_up(8 * K) + 2 * align_up(8 * n) + align_up(8 * m) +
+         align_up(8 * (size_t)gg) + align_up(16 * (size_t)gr) + align_up(256) + align_up(sizeof(KzState)) +
+         align_up(4 * (size_t)(ctx->L.maxit_cap + 1));
+}
+static plss_status kz_enqueue_step(plss_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  const KzArgs& a = ctx->kz;
+  k_kz_prep<<<1, KZ_NT, 0, st>>>(a);
+  k_kz_gemv<<<a.grid_gemv, KZ_NT, 0, st>>>(a);
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
+  k_kz_resid<<<a.grid_res, KZ_NT, 0, st>>>(a);
+  CK(cudaGetLastError());
+  return PLSS_OK;
+}
+
+extern "C" {
+
+size_t plss_kz_workspace_bytes(const plss_ctx* ctx, int32_t kmax) {
+  if (!ctx || ctx->dist || kmax < 1) return 0;
+  return kz_bytes(ctx, kmax);
+}
+
+plss_status plss_kz_start(plss_ctx* ctx, int32_t kmax, void* workspace, size_t ws_bytes, const int32_t* rows,
+                          const double* b, const double* x0, double tol, int32_t tol_mode, int32_t maxit) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (ctx->dist || kmax < 1 || !(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap ||
+      (tol_mode != 0 && tol_mode != 1) || !rows) {
+    set_err(ctx, ctx->dist ? "PLSS Kaczmarz runs on a single-device ctx"
+                           : "invalid kmax / tol / tol_mode / maxit, or rows is NULL");
+    return PLSS_E_INVALID;
+  }
+  if (!b && ctx->m > 0) { set_err(ctx, "b is NULL"); return PLSS_E_INVALID; }
+  if (!workspace || ws_bytes < kz_bytes(ctx, kmax) || ((uintptr_t)workspace % ALIGN) != 0) {
+    set_err(ctx, "PLSS Kaczmarz workspace missing, misaligned or smaller than plss_kz_workspace_bytes");
+    return PLSS_E_DIM;
+  }
+  cudaStream_t st = ctx->stream;
+  std::vector<int32_t> hrows((size_t)maxit);
+  CK(cudaMemcpyAsync(hrows.data(), rows, 4 * (size_t)maxit, is_device_ptr(rows) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int32_t i : hrows)
+    if (i < 0 || i >= ctx->m) { set_err(ctx, "row index out of range in the Kaczmarz row schedule"); return PLSS_E_INVALID; }
+  KzArgs a{};
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.kmax = kmax;
+  a.row_ptr = ctx->A.row_ptr;
+  a.col_idx = ctx->A.col_idx;
+  a.val = ctx->A.val;
+  kz_grids(ctx, &a.grid_gemv, &a.grid_res);
+  char* w = (char*)workspace;
+  size_t off = 0;
+  auto take = [&](size_t nb) { char* q = w + off; off += align_up(nb); return q; };
+  const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
+  a.P = (double*)take(8 * n * K);
+  a.AP = (double*)take(8 * m * K);
+  a.theta = (double*)take(8 * K);
+  a.w = (double*)take(8 * K);
+  a.arow = (double*)take(8 * n);
+  a.pk = (double*)take(8 * n);
+  a.apk = (double*)take(8 * m);
+  a.part_th = (double*)take(8 * (size_t)a.grid_gemv);
+  a.part_rho = (double*)take(16 * (size_t)a.grid_res);
+  a.counter = (unsigned*)take(256);
+  a.st = (KzState*)take(sizeof(KzState));
+  int32_t* drows = (int32_t*)take(4 * (size_t)(ctx->L.maxit_cap + 1));
+  a.rows = drows;
+  a.r = ctx->r;
+  a.x = ctx->x;
+  a.ctl = ctx->ctl;
+  a.rec = ctx->rec;
+  plss_status ps = alt_start(ctx, b, x0, tol, tol_mode, maxit);
+  if (ps != PLSS_OK) return ps;
+  KzState s0{};
+  s0.prev_row = -1;
+  CK(cudaMemcpyAsync(drows, hrows.data(), 4 * (size_t)maxit, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(a.st, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(a.counter, 0, 256, st));
+  if (n > 0) CK(cudaMemsetAsync(a.arow, 0, 8 * n, st));
+  CK(cudaStreamSynchronize(st));   // hrows / s0 are host temporaries
+  ctx->kz = a;
+  ctx->kz_seg = ctx->seg1;
+  for (int s = 0; s < ctx->S; ++s) {
+    SpmvSeg& g = ctx->kz_seg[s];
+    g.g = a.pk;
+    g.out = a.apk + ctx->R[s];
+    g.ctl = ctx->ctl;                // no-op once done
+  }
+  if (ctx->kz_graph_chunk) { CK(cudaGraphExecDestroy(ctx->kz_graph_chunk)); ctx->kz_graph_chunk = nullptr; }
+  if (ctx->kz_graph_one) { CK(cudaGraphExecDestroy(ctx->kz_graph_one)); ctx->kz_graph_one = nullptr; }
+  if ((ps = alt_build_graph(ctx, kz_enqueue_step, ctx->chunk, &ctx->kz_graph_chunk)) != PLSS_OK) return ps;
+  if ((ps = alt_build_graph(ctx, kz_enqueue_step, 1, &ctx->kz_graph_one)) != PLSS_OK) return ps;
+  ctx->kz_started = true;
+  return PLSS_OK;
+}
+
+plss_status plss_kz_step(plss_ctx* ctx, int32_t k) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->kz_started) { set_err(ctx, "plss_kz_step before plss_kz_start"); return PLSS_E_STATE; }
+  if (k < 0) return PLSS_E_INVALID;
+  for (int i = 0; i + ctx->chunk <= k; i += ctx->chunk) CK(cudaGraphLaunch(ctx->kz_graph_chunk, ctx->stream));
+  for (int i = 0; i < k % ctx->chunk; ++i) CK(cudaGraphLaunch(ctx->kz_graph_one, ctx->stream));
+  return PLSS_OK;
+}
+
+plss_status plss_kz_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
+                           plss_outcome* outcome) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->kz_started) { set_err(ctx, "plss_kz_finish before plss_kz_start"); return PLSS_E_STATE; }
+  return alt_finish(ctx, x, iters, hist, diag, outcome);
+}
+
+plss_status plss_kz_solve(plss_ctx* ctx, int32_t kmax, void* workspace, size_t ws_bytes, const int32_t* rows,
+                          const double* b, const double* x0, double tol, int32_t tol_mode, int32_t maxit, double* x,
+                          int32_t* iters, double* hist, double* diag, plss_outcome* outcome) {
+  plss_status s = plss_kz_start(ctx, kmax, workspace, ws_bytes, rows, b, x0, tol, tol_mode, maxit);
+  if (s != PLSS_OK) return s;
+  if ((s = alt_run(ctx, ctx->kz_graph_chunk, ctx->kz_graph_one, maxit)) != PLSS_OK) return s;
+  return plss_kz_finish(ctx, x, iters, hist, diag, outcome);
+}
+
+plss_status plss_kz_profile(plss_ctx* ctx, int32_t k, double* ms) {
+  if (!ctx || !ms || k < 1) return PLSS_E_INVALID;
+  if (!ctx->kz_started) { set_err(ctx, "plss_kz_profile before plss_kz_start"); return PLSS_E_STATE; }
+  cudaStream_t st = ctx->stream;
+  const KzArgs& a = ctx->kz;
+  constexpr int NK = 4;
+  cudaEvent_t ev[NK + 1];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[NK] = {0, 0, 0, 0};
+  for (int it = 0; it < k; ++it) {
+    CK(cudaEventRecord(ev[0], st));
+    k_kz_prep<<<1, KZ_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[1], st));
+    k_kz_gemv<<<a.grid_gemv, KZ_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[2], st));
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
+    CK(cudaEventRecord(ev[3], st));
+    k_kz_resid<<<a.grid_res, KZ_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[4], st));
+    CK(cudaGetLastError());
+    CK(cudaEventSynchronize(ev[4]));
+    for (int j = 0; j < NK; ++j) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
+      acc[j] += t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int j = 0; j < NK; ++j) ms[j] = acc[j] / k;
+  return PLSS_OK;
+}
+
+}  // extern "C"
+
 extern "C" {
 
 void plss_destroy(plss_ctx* ctx) {
@@ -1520,6 +1714,8 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->graph_one) cudaGraphExecDestroy(ctx->graph_one);
   if (ctx->rp_graph_chunk) cudaGraphExecDestroy(ctx->rp_graph_chunk);
   if (ctx->rp_graph_one) cudaGraphExecDestroy(ctx->rp_graph_one);
+  if (ctx->kz_graph_chunk) cudaGraphExecDestroy(ctx->kz_graph_chunk);
+  if (ctx->kz_graph_one) cudaGraphExecDestroy(ctx->kz_graph_one);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->h_done) cudaFreeHost(ctx->h_done);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);

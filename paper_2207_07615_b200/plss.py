@@ -27,7 +27,9 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_solve", "plss_start", "plss_step", "plss_finish", "plss_spmv", "plss_spmvT",
            "plss_profile", "plss_query", "plss_destroy", "plss_status_str", "plss_last_error",
            "plss_set_wi", "plss_column_norms", "plss_rp_workspace_bytes", "plss_rp_solve", "plss_rp_start",
-           "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile"]
+           "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile",
+           "plss_kz_workspace_bytes", "plss_kz_solve", "plss_kz_start", "plss_kz_step", "plss_kz_finish",
+           "plss_kz_profile"]
 
 
 class PlssError(RuntimeError):
@@ -113,6 +115,19 @@ def load_library(path: str = None):
     lib.plss_rp_profile.restype = st
     lib.plss_spmmT.argtypes = [P, I32, I32, P, P]
     lib.plss_spmmT.restype = st
+    lib.plss_kz_workspace_bytes.argtypes = [P, I32]
+    lib.plss_kz_workspace_bytes.restype = ctypes.c_size_t
+    lib.plss_kz_start.argtypes = [P, I32, P, ctypes.c_size_t, P, P, P, D, I32, I32]
+    lib.plss_kz_start.restype = st
+    lib.plss_kz_step.argtypes = [P, I32]
+    lib.plss_kz_step.restype = st
+    lib.plss_kz_finish.argtypes = [P, P, ctypes.POINTER(I32), P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_kz_finish.restype = st
+    lib.plss_kz_solve.argtypes = [P, I32, P, ctypes.c_size_t, P, P, P, D, I32, I32, P, ctypes.POINTER(I32), P, P,
+                                  ctypes.POINTER(ctypes.c_int)]
+    lib.plss_kz_solve.restype = st
+    lib.plss_kz_profile.argtypes = [P, I32, P]
+    lib.plss_kz_profile.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
     lib.plss_status_str.argtypes = [st]
@@ -452,6 +467,84 @@ def plss_spmmT(ctx: Ctx, S, r=None, Y=None):
         Y = torch.empty((ctx.n, r), dtype=torch.float64, device=S.device)
     _check(load_library().plss_spmmT(ctx.handle, r, ld, _ptr(S), _ptr(Y)), ctx.handle)
     return Y
+
+
+def _kz_workspace(ctx: Ctx, kmax: int):
+    nbytes = int(load_library().plss_kz_workspace_bytes(ctx.handle, int(kmax)))
+    if nbytes == 0:
+        raise PlssError("plss_kz_workspace_bytes: invalid kmax or distributed ctx")
+    ws = getattr(ctx, "_kz_ws", None)
+    if ws is None or ws.numel() < nbytes + 256:
+        ctx._kz_ws = None
+        ws = ctx._kz_ws = _alloc_workspace(nbytes, ctx.A.row_ptr.device)
+    return _aligned(ws), nbytes
+
+
+def _rows_arg(rows):
+    if isinstance(rows, np.ndarray) or not hasattr(rows, "data_ptr"):
+        return np.ascontiguousarray(rows, dtype=np.int32)
+    import torch
+    return rows.to(dtype=torch.int32).contiguous()
+
+
+def plss_kz_start(ctx: Ctx, b, rows, kmax=None, x0=None, tol=1e-8, tol_mode=0, maxit=100):
+    """PLSS Kaczmarz (eq:pkKacz) over the row order `rows` (host or device int32, >= maxit)."""
+    lib = load_library()
+    kmax = int(maxit if kmax is None else kmax)
+    wp, nb = _kz_workspace(ctx, kmax)
+    rr = _rows_arg(rows)
+    ctx._keep = (b, x0, rr)
+    ctx._maxit = int(maxit)
+    _check(lib.plss_kz_start(ctx.handle, kmax, wp, nb, _ptr(rr), _ptr(b), _ptr(x0), float(tol), int(tol_mode),
+                             int(maxit)), ctx.handle)
+
+
+def plss_kz_step(ctx: Ctx, k: int):
+    _check(load_library().plss_kz_step(ctx.handle, int(k)), ctx.handle)
+
+
+def plss_kz_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
+    lib = load_library()
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(ctx._maxit + 1) if want_hist else None
+    diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
+    _check(lib.plss_kz_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+           ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if hist is not None:
+        res["hist"] = hist[:it.value + 1].copy()
+    return res
+
+
+def plss_kz_solve(ctx: Ctx, b, rows, kmax=None, x0=None, tol=1e-8, tol_mode=0, maxit=100, x=None,
+                  want_hist=True, want_diag=False):
+    """Full PLSS Kaczmarz solve. Returns dict(x, iters, outcome, hist[0..iters][, diag])."""
+    import torch
+    lib = load_library()
+    if x is None:
+        x = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
+    kmax = int(maxit if kmax is None else kmax)
+    wp, nb = _kz_workspace(ctx, kmax)
+    rr = _rows_arg(rows)
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(maxit + 1) if want_hist else None
+    diag = np.zeros((maxit + 1, REC)) if want_diag else None
+    ctx._maxit = int(maxit)
+    _check(lib.plss_kz_solve(ctx.handle, kmax, wp, nb, _ptr(rr), _ptr(b), _ptr(x0), float(tol), int(tol_mode),
+                             int(maxit), _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+           ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if hist is not None:
+        res["hist"] = hist[:it.value + 1].copy()
+    return res
+
+
+def plss_kz_profile(ctx: Ctx, k: int) -> dict:
+    ms = np.zeros(4)
+    _check(load_library().plss_kz_profile(ctx.handle, int(k), _ptr(ms)), ctx.handle)
+    return dict(zip(["prep", "gemv", "spmv", "resid"], ms.tolist()))
 
 
 def plss_destroy(ctx: Ctx):
