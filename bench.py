@@ -9,6 +9,7 @@ work. N > 1 (torchrun): row-block sharding, one NCCL all-reduce of n+1 doubles p
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5|C3|C4|C2] [--impl reference]
     python bench.py --method rp [--rp-r 5] [--rp-density 1.0]   # randomized projection (NEXT-2)
+    python bench.py --method kz [--workload C2]                   # PLSS Kaczmarz (NEXT-3)
 
 Prints ONE JSON line (rank 0).
 """
@@ -31,6 +32,14 @@ import plss_gen  # noqa: E402
 
 METRIC = "PLSS iterations/sec and achieved HBM GB/s (fraction of ~8 TB/s)"
 RP_METRIC = "Rand. Proj. (eq:pkLong, fresh Gaussian S_k) iterations/sec and achieved HBM GB/s"
+KZ_METRIC = "PLSS Kaczmarz (eq:pkKacz) iterations/sec and achieved HBM GB/s"
+
+
+def kz_bytes_per_iter(m, n, nnz, hk):
+    """Algorithmic bytes of one PLSS Kaczmarz step with hk stored updates:
+    GEMV: P (8 n hk) + arow, pk, new P column, x rw (40 n); SpMV A p: 12 nnz + 4 (m+1) + 8 n + 8 m;
+    residual: r rw, apk, new A P column (32 m); prep: hk values of A P and theta, w (24 hk)."""
+    return 8 * n * hk + 40 * n + 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m + 32 * m + 24 * hk
 
 
 def rp_bytes_per_iter(m, n, nnz, r):
@@ -228,13 +237,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
-    ap.add_argument("--method", default="plss", choices=["plss", "rp"],
-                    help="rp: randomized projection (the paper's comparison method, NEXT-2)")
+    ap.add_argument("--method", default="plss", choices=["plss", "rp", "kz"],
+                    help="rp: randomized projection (the paper's comparison method, NEXT-2); "
+                         "kz: PLSS Kaczmarz (section 7, NEXT-3)")
     ap.add_argument("--rp-r", type=int, default=5, help="sketch size r (Experiment III: 5 for n > 1e5)")
     ap.add_argument("--rp-density", type=float, default=1.0, help="< 1: sparse normal sketch")
     args = ap.parse_args()
     if args.method == "rp":
         return main_rp(args)
+    if args.method == "kz":
+        if args.workload == "C5":
+            args.workload = "C2"          # the history grows as 8 (m + n) bytes per step: C2, not C5
+        if "--steps" not in sys.argv:
+            args.steps = 1000
+        return main_kz(args)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -490,6 +506,127 @@ def main_rp(args):
             "clocks": clk.summary(), "final_hist": float(fin["hist_full"][args.warmup + args.steps])}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = rp_cpu_leg(name, r, dens, B)
+    print(json.dumps(line), flush=True)
+    pkg.plss_destroy(ctx)
+
+
+# ---------------------------------------------------------------------------------------------
+# PLSS Kaczmarz (--method kz): single device; a step's cost grows with the stored history hk
+# ---------------------------------------------------------------------------------------------
+def kz_cpu_leg(s, label, rows, full_bytes_fn, steps=None, budget_s=15.0):
+    """The Kaczmarz oracle on the same workload for a bounded number of steps from hk = 0; its
+    algorithmic GB/s (kz_bytes_per_iter at each step's hk) converts to it/s for the GPU window."""
+    from oracle import kaczmarz as okz
+    A = s.scipy_csr()
+    t0 = time.perf_counter()
+    okz.kz_solve(A, s.b, rows, maxit=5)
+    t1 = (time.perf_counter() - t0) / 5
+    k = steps or int(max(20, min(400, budget_s / max(t1 * 8, 1e-6))))   # per-step cost grows with k
+    t0 = time.perf_counter()
+    okz.kz_solve(A, s.b, rows, maxit=k)
+    t = time.perf_counter() - t0
+    byts = sum(kz_bytes_per_iter(s.m, s.n, s.nnz, h) for h in range(k))
+    gbs = byts / t / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+    return {"value": gbs * 1e9 / full_bytes_fn, "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": f"{label}; the first {k} PLSS Kaczmarz steps (history 0..{k - 1}) in {t:.1f} s = "
+                      f"{gbs:.2f} GB/s algorithmic (numpy/scipy, BLAS threads up to {cores}); it/s scaled "
+                      f"to the GPU's timed window by algorithmic bytes/iter", "oracle_gbs": gbs}
+
+
+def main_kz(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    name = args.workload
+    s = plss_gen.make_config(name)
+    m, n, nnz = s.m, s.n, s.nnz
+    W, K = args.warmup, args.steps
+    rows_all = np.random.default_rng(1).permutation(m)
+    cap = W + K + max(args.profile_steps, 1) + 8
+    rows = np.resize(rows_all, cap).astype(np.int32)
+    hk_mean = W + (K - 1) / 2.0                      # history size over the timed steps (no skips)
+    B = kz_bytes_per_iter(m, n, nnz, hk_mean)
+    label = workload_label(name) + f"; PLSS Kaczmarz, random row order, timed steps with history {W}..{W + K - 1}"
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        leg = kz_cpu_leg(s, workload_label(name), rows, B, steps=max(1, args.steps))
+        v = leg["value"]
+        print(json.dumps({"metric": KZ_METRIC, "value": v, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": label}, "cpu_baseline": leg,
+                          "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+    import torch
+    import paper_2207_07615_b200 as pkg
+    assert world == 1, "PLSS Kaczmarz: single device (bench.py --method kz runs without torchrun)"
+    assert args.warmup >= 3 or args.ncu, "timing rules: at least 3 warm-up steps"
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pkg.load_library()
+    A = pkg.Matrix.from_arrays(m, n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=cap, stream=stream)
+    q = pkg.plss_query(ctx)
+    b = torch.from_numpy(s.b).to(dev)
+    drows = torch.from_numpy(rows).to(dev)
+    torch.cuda.synchronize()
+    pkg.plss_kz_start(ctx, b, drows, kmax=cap, tol=0.0, maxit=cap)
+    pkg.plss_kz_step(ctx, W)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        pkg.plss_kz_step(ctx, K)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    fin = pkg.plss_kz_finish(ctx, None, want_hist=True, want_diag=True)
+    skipped = int(fin["diag"][1:W + K + 1, 2].sum())
+    its = K / (ms / 1e3)
+    if args.ncu:
+        print(json.dumps({"ncu_run": True, "ms_per_step": ms / K}), flush=True)
+        return
+    kt = pkg.plss_kz_profile(ctx, max(1, args.profile_steps))      # steps with history ~ W + K
+    hk_prof = W + K - skipped + (max(1, args.profile_steps) - 1) / 2.0
+    cls = {"kz_gemv_history": (kt["gemv"], 8 * n * hk_prof + 40 * n),
+           "kz_spmv_Ap": (kt["spmv"], 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m),
+           "kz_resid": (kt["resid"], 32 * m), "kz_prep": (kt["prep"], 24 * hk_prof)}
+    dom = max(cls, key=lambda c: cls[c][0])
+    dom_ms, dom_bytes = cls[dom]
+    peak, peak_src = _peaks()
+    pin_b = torch.empty(m, dtype=torch.float64, pin_memory=True)
+    pin_b.copy_(b.cpu())
+    pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pkg.plss_kz_solve(ctx, pin_b, rows, kmax=cap, tol=0.0, maxit=W + K, x=pin_x)
+    t_e2e = time.perf_counter() - t0
+    line = {"metric": KZ_METRIC, "value": its, "unit": "it/s", "n_gpus": 1, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": label, "m": m, "n": n, "nnz": nnz, "history_mean": hk_mean,
+                       "parallelism": "single", "slabs": q["slabs"], "tol": 0.0, "skipped_rows": skipped,
+                       "l2": f"history P is {8 * n * (W + K) / 1e9:.2f} GB at the end (> L2 after "
+                             f"{126e6 / (8 * n):.0f} steps); A is {12 * nnz / 1e6:.0f} MB (L2-resident)",
+                       "bytes_per_step_model": "8 n hk + 48 n + 12 nnz + 44 m + 24 hk + 4"},
+            "achieved_gbs": B * its / 1e9, "achieved_frac_of_peak": B * its / 1e9 / peak,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "peak_source": peak_src, "algorithmic_bytes_per_step": dom_bytes,
+                         "kernel_ms_per_step": dom_ms, "history_at_profile": hk_prof},
+            "kernels_ms_per_step": kt, "gpu_launches": K * (3 + q["slabs"]),
+            "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": (8 * m + 4 * (W + K)) / (W + K),
+                    "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
+                    "note": "one plss_kz_solve from pinned host b and host rows to host x + history "
+                            "(steps from history 0, so cheaper on average than the timed window)"},
+            "clocks": clk.summary(), "final_hist": float(fin["hist_full"][W + K])}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = kz_cpu_leg(s, workload_label(name), rows, B)
     print(json.dumps(line), flush=True)
     pkg.plss_destroy(ctx)
 

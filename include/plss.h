@@ -241,7 +241,8 @@ plss_status plss_kz_step(plss_ctx *ctx, int32_t k);
 plss_status plss_kz_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
                            plss_outcome *outcome);
 /* Per-kernel device ms per step (CUDA events, one kernel at a time) after plss_kz_start; ms (host,
- * 4 doubles): row preparation, the P GEMV + update, A p_k (SpMV), residual + record. */
+ * 4 doubles): 0 (the row preparation runs inside the residual kernel), the P GEMV + update,
+ * A p_k (SpMV), residual + record + next row preparation. */
 plss_status plss_kz_profile(plss_ctx *ctx, int32_t k, double *ms);
 
 void plss_destroy(plss_ctx *ctx);

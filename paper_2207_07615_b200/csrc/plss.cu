@@ -1543,7 +1543,7 @@ plss_status plss_spmmT(plss_ctx* ctx, int32_t r, int32_t ld, const float* S, dou
 // ---- PLSS Kaczmarz (kz_kernels.cuh) ------------------------------------------
 static void kz_grids(const plss_ctx* ctx, int* g_gemv, int* g_res) {
   const int sms = rp_sms(ctx);
-  *g_gemv = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + KZ_NT - 1) / KZ_NT, 4 * (int64_t)sms));
+  *g_gemv = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + KZ_TL - 1) / KZ_TL, 8 * (int64_t)sms));
   *g_res = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + KZ_NT - 1) / KZ_NT, 4 * (int64_t)sms));
 }
 static size_t kz_bytes(const plss_ctx* ctx, int kmax) {
@@ -1557,7 +1557,6 @@ static size_t kz_bytes(const plss_ctx* ctx, int kmax) {
 static plss_status kz_enqueue_step(plss_ctx* ctx) {
   cudaStream_t st = ctx->stream;
   const KzArgs& a = ctx->kz;
-  k_kz_prep<<<1, KZ_NT, 0, st>>>(a);
   k_kz_gemv<<<a.grid_gemv, KZ_NT, 0, st>>>(a);
   for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
   k_kz_resid<<<a.grid_res, KZ_NT, 0, st>>>(a);
@@ -1631,6 +1630,8 @@ plss_status plss_kz_start(plss_ctx* ctx, int32_t kmax, void* workspace, size_t w
   if (n > 0) CK(cudaMemsetAsync(a.arow, 0, 8 * n, st));
   CK(cudaStreamSynchronize(st));   // hrows / s0 are host temporaries
   ctx->kz = a;
+  k_kz_prep<<<1, KZ_NT, 0, st>>>(a);   // the first step's row; later steps' rows are prepared by k_kz_resid
+  CK(cudaGetLastError());
   ctx->kz_seg = ctx->seg1;
   for (int s = 0; s < ctx->S; ++s) {
     SpmvSeg& g = ctx->kz_seg[s];
@@ -1682,8 +1683,7 @@ plss_status plss_kz_profile(plss_ctx* ctx, int32_t k, double* ms) {
   double acc[NK] = {0, 0, 0, 0};
   for (int it = 0; it < k; ++it) {
     CK(cudaEventRecord(ev[0], st));
-    k_kz_prep<<<1, KZ_NT, 0, st>>>(a);
-    CK(cudaEventRecord(ev[1], st));
+    CK(cudaEventRecord(ev[1], st));     // row preparation is fused into k_kz_resid (slot 0 stays ~0)
     k_kz_gemv<<<a.grid_gemv, KZ_NT, 0, st>>>(a);
     CK(cudaEventRecord(ev[2], st));
     for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);

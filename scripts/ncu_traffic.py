@@ -6,9 +6,10 @@ import re
 import subprocess
 import sys
 
-KIND = re.compile(r"k_(?:spmv|sellw?)<(\d)|k_rp_(spmm|gen|gram|update)")
+KIND = re.compile(r"k_(?:spmv|sellw?)<(\d)|k_rp_(spmm|gen|gram|update)|k_kz_(gemv|resid)")
 NAME = {"1": "k1_spmv_csr_resid", "2": "k2_spmv_csc_gather", "3": "k2_spmv_csc_gather",
-        "spmm": "rp_spmm_AtS", "gen": "rp_sketch_gen", "gram": "rp_gram", "update": "rp_update"}
+        "spmm": "rp_spmm_AtS", "gen": "rp_sketch_gen", "gram": "rp_gram", "update": "rp_update",
+        "gemv": "kz_gemv_history", "resid": "kz_resid"}
 
 
 def main(path, note):
@@ -19,7 +20,7 @@ def main(path, note):
     acc = {}
     for r in rows[2:]:
         m = KIND.search(r[col["Kernel Name"]])
-        key = m and (m.group(1) or m.group(2))
+        key = m and (m.group(1) or m.group(2) or m.group(3))
         if not key or key not in NAME:
             continue
         k = NAME[key]
