@@ -245,6 +245,37 @@ plss_status plss_kz_finish(plss_ctx *ctx, double *x, int32_t *iters, double *his
  * A p_k (SpMV), residual + record + next row preparation. */
 plss_status plss_kz_profile(plss_ctx *ctx, int32_t k, double *ms);
 
+/* ---- Growing-sketch engine, triangular factorization (section 2.4, Thm 2.1 / Cor 2.2,
+ * L284-441) ----
+ * For a sketch column s_k per step -- sketch 0: residual s_k = r_{k-1} (eq:S; Thm 4.1: PLSS's
+ * updates); 1: identity s_k = e_{rows[k-1]} (section 7: PLSS Kaczmarz's updates); 2: Gaussian
+ * s_k = column 0 of randomized projection's binary32 generator (reading R17) keyed by seed --
+ * with y_k = A^T s_k and the stored Y (n x hk), R = [t_1 .. t_hk], D = diag(1/delta_j):
+ *   g = Y^T y_k; t_hat = R D R^T g; delta = y_k^T y_k - g^T t_hat;
+ *   p_k = (s_k^T r_{k-1} / delta) (y_k - Y t_hat)   (eq:compute-pk-alpha1, no solves);
+ *   append y_k, t_hat, 1/delta; x_k = x_{k-1} + p_k; r_k = r_{k-1} - A p_k; stop test as plss_solve.
+ * A step with delta <= 1e-14 y^T y, y = 0 or s^T r = 0 is skipped (p = 0, nothing appended;
+ * reading R22); after kmax stored columns the history is cleared (R21). rows: host or dev,
+ * maxit indices in [0, m) (identity sketch only; may be NULL otherwise). Single-device ctx;
+ * shares the ctx's r, y, p, x, control block and history. workspace: dev, 256-byte aligned,
+ * >= plss_eg_workspace_bytes(ctx, kmax) = 8 n kmax + 8 kmax^2 bytes + O(m + n).
+ * record k of `diag` = {hist_k, rho_k, delta_k, skipped (0/1), s_k^T r_{k-1}, history size}. */
+size_t plss_eg_workspace_bytes(const plss_ctx *ctx, int32_t kmax); /* 0 on invalid input */
+plss_status plss_eg_solve(plss_ctx *ctx, int32_t sketch, int32_t kmax, void *workspace,
+                          size_t ws_bytes, const int32_t *rows, uint64_t seed, const double *b,
+                          const double *x0, double tol, int32_t tol_mode, int32_t maxit, double *x,
+                          int32_t *iters, double *hist, double *diag, plss_outcome *outcome);
+plss_status plss_eg_start(plss_ctx *ctx, int32_t sketch, int32_t kmax, void *workspace,
+                          size_t ws_bytes, const int32_t *rows, uint64_t seed, const double *b,
+                          const double *x0, double tol, int32_t tol_mode, int32_t maxit);
+plss_status plss_eg_step(plss_ctx *ctx, int32_t k);
+plss_status plss_eg_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
+                           plss_outcome *outcome);
+/* Per-kernel device ms per step (CUDA events, one kernel at a time) after plss_eg_start; ms
+ * (host, 5 doubles): sketch + y = A^T s, Y^T y partials, triangular update, p = coef (y - Y t_hat),
+ * K1 (r <- r - A p). */
+plss_status plss_eg_profile(plss_ctx *ctx, int32_t k, double *ms);
+
 void plss_destroy(plss_ctx *ctx);
 const char *plss_status_str(plss_status s);
 const char *plss_last_error(const plss_ctx *ctx); /* NULL ctx: last error of create calls */

@@ -12,6 +12,7 @@
 #include "plss_kernels.cuh"
 #include "rp_kernels.cuh"
 #include "kz_kernels.cuh"
+#include "eg_kernels.cuh"
 
 #include <nccl.h>
 
@@ -225,6 +226,11 @@ struct plss_ctx {
   KzArgs kz{};
   std::vector<SpmvSeg> kz_seg;   // K1 segments in plain mode: apk = A pk
   cudaGraphExec_t kz_graph_chunk = nullptr, kz_graph_one = nullptr;
+  // growing-sketch engine (plss_eg_*): shares r, y, p, x, ctl, rec and the K1 / K2 segments
+  bool eg_started = false;
+  EgArgs eg{};
+  std::vector<SpmvSeg> eg_seg;   // K2 segments gathering the sketch column: y = A^T s
+  cudaGraphExec_t eg_graph_chunk = nullptr, eg_graph_one = nullptr;
   std::string err;
 };
 
@@ -983,6 +989,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
   ctx->started = true;
   ctx->rp_started = false;
   ctx->kz_started = false;
+  ctx->eg_started = false;
   ctx->maxit = maxit;
   ctx->flags = flags;
   return PLSS_OK;
@@ -1293,6 +1300,7 @@ static plss_status alt_start(plss_ctx* ctx, const double* b, const double* x0, d
   ctx->started = false;          // the PLSS loop state is overwritten
   ctx->rp_started = false;
   ctx->kz_started = false;
+  ctx->eg_started = false;
   ctx->maxit = maxit;
   return PLSS_OK;
 }
@@ -1705,6 +1713,192 @@ plss_status plss_kz_profile(plss_ctx* ctx, int32_t k, double* ms) {
 
 }  // extern "C"
 
+// ---- growing-sketch engine, triangular factorization (eg_kernels.cuh) --------
+static void eg_grids(const plss_ctx* ctx, int* g_t, int* g_s, int* g_g) {
+  const int sms = rp_sms(ctx);
+  *g_t = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + 511) / 512, 2 * (int64_t)sms));
+  *g_s = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + EG_NT - 1) / EG_NT, 4 * (int64_t)sms));
+  *g_g = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + 63) / 64, 8 * (int64_t)sms));
+}
+static size_t eg_bytes(const plss_ctx* ctx, int kmax) {
+  int gt, gs, gg;
+  eg_grids(ctx, &gt, &gs, &gg);
+  const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
+  return align_up(8 * n * K) + align_up(8 * K * K) + 3 * align_up(8 * K) + align_up(8 * (K + 1) * (size_t)gt) +
+         align_up(8 * (size_t)gs) + align_up(8 * m) + align_up(sizeof(EgState)) + align_up(4 * (size_t)(ctx->L.maxit_cap + 1));
+}
+static plss_status eg_enqueue_step(plss_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  const EgArgs& a = ctx->eg;
+  if (a.mode == EG_IDENTITY) {
+    k_eg_row<<<1, EG_NT, 0, st>>>(a);
+  } else {
+    if (a.mode == EG_GAUSSIAN) k_eg_gauss<<<a.grid_s, EG_NT, 0, st>>>(a);
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->eg_seg[s], ctx->g2[s], st);   // y = A^T s
+  }
+  k_eg_gemvT<<<a.grid_t, EG_NT, 0, st>>>(a);
+  k_eg_tri<<<1, EG_NT, 0, st>>>(a);
+  k_eg_gemv<<<a.grid_g, EG_NT, 0, st>>>(a);
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);     // r -= A p, rho, stop
+  CK(cudaGetLastError());
+  return PLSS_OK;
+}
+
+extern "C" {
+
+size_t plss_eg_workspace_bytes(const plss_ctx* ctx, int32_t kmax) {
+  if (!ctx || ctx->dist || kmax < 1) return 0;
+  return eg_bytes(ctx, kmax);
+}
+
+plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* workspace, size_t ws_bytes,
+                          const int32_t* rows, uint64_t seed, const double* b, const double* x0, double tol,
+                          int32_t tol_mode, int32_t maxit) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (ctx->dist || kmax < 1 || sketch < EG_RESIDUAL || sketch > EG_GAUSSIAN || !(tol >= 0.0) || maxit < 1 ||
+      maxit > ctx->L.maxit_cap || (tol_mode != 0 && tol_mode != 1) || (sketch == EG_IDENTITY && !rows)) {
+    set_err(ctx, ctx->dist ? "the growing-sketch engine runs on a single-device ctx"
+                           : "invalid sketch / kmax / tol / tol_mode / maxit, or rows is NULL for identity sketches");
+    return PLSS_E_INVALID;
+  }
+  if (!b && ctx->m > 0) { set_err(ctx, "b is NULL"); return PLSS_E_INVALID; }
+  if (!workspace || ws_bytes < eg_bytes(ctx, kmax) || ((uintptr_t)workspace % ALIGN) != 0) {
+    set_err(ctx, "engine workspace missing, misaligned or smaller than plss_eg_workspace_bytes");
+    return PLSS_E_DIM;
+  }
+  cudaStream_t st = ctx->stream;
+  std::vector<int32_t> hrows;
+  if (sketch == EG_IDENTITY) {
+    hrows.resize((size_t)maxit);
+    CK(cudaMemcpyAsync(hrows.data(), rows, 4 * (size_t)maxit, is_device_ptr(rows) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int32_t i : hrows)
+      if (i < 0 || i >= ctx->m) { set_err(ctx, "row index out of range in the identity sketch"); return PLSS_E_INVALID; }
+  }
+  EgArgs a{};
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.kmax = kmax;
+  a.mode = sketch;
+  a.row_ptr = ctx->A.row_ptr;
+  a.col_idx = ctx->A.col_idx;
+  a.val = ctx->A.val;
+  a.key = rp_key(seed);
+  eg_grids(ctx, &a.grid_t, &a.grid_s, &a.grid_g);
+  char* w = (char*)workspace;
+  size_t off = 0;
+  auto take = [&](size_t nb) { char* q = w + off; off += align_up(nb); return q; };
+  const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
+  a.Y = (double*)take(8 * n * K);
+  a.R = (double*)take(8 * K * K);
+  a.dinv = (double*)take(8 * K);
+  a.gv = (double*)take(8 * K);
+  a.th = (double*)take(8 * K);
+  a.part = (double*)take(8 * (K + 1) * (size_t)a.grid_t);
+  a.part_rs = (double*)take(8 * (size_t)a.grid_s);
+  a.s = (double*)take(8 * m);
+  a.st = (EgState*)take(sizeof(EgState));
+  int32_t* drows = (int32_t*)take(4 * (size_t)(ctx->L.maxit_cap + 1));
+  a.rows = drows;
+  a.y = ctx->y;
+  a.p = ctx->p;
+  a.x = ctx->x;
+  a.r = ctx->r;
+  a.ctl = ctx->ctl;
+  a.rec = ctx->rec;
+  plss_status ps = alt_start(ctx, b, x0, tol, tol_mode, maxit);
+  if (ps != PLSS_OK) return ps;
+  EgState s0{};
+  s0.prev_row = -1;
+  CK(cudaMemcpyAsync(a.st, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+  if (!hrows.empty()) CK(cudaMemcpyAsync(drows, hrows.data(), 4 * (size_t)maxit, cudaMemcpyHostToDevice, st));
+  if (n > 0) CK(cudaMemsetAsync(ctx->y, 0, 8 * n, st));
+  CK(cudaStreamSynchronize(st));   // host temporaries
+  ctx->eg = a;
+  ctx->eg_seg = ctx->seg2;
+  for (int s = 0; s < ctx->S; ++s) {
+    SpmvSeg& g = ctx->eg_seg[s];
+    const double* src = sketch == EG_GAUSSIAN ? a.s : ctx->r;
+    g.g = src + (ctx->S > 1 ? ctx->R[s] : 0);
+    g.out = ctx->y;
+    g.finalize = 0;
+    g.ctl = ctx->ctl;
+  }
+  if (ctx->eg_graph_chunk) { CK(cudaGraphExecDestroy(ctx->eg_graph_chunk)); ctx->eg_graph_chunk = nullptr; }
+  if (ctx->eg_graph_one) { CK(cudaGraphExecDestroy(ctx->eg_graph_one)); ctx->eg_graph_one = nullptr; }
+  if ((ps = alt_build_graph(ctx, eg_enqueue_step, ctx->chunk, &ctx->eg_graph_chunk)) != PLSS_OK) return ps;
+  if ((ps = alt_build_graph(ctx, eg_enqueue_step, 1, &ctx->eg_graph_one)) != PLSS_OK) return ps;
+  ctx->eg_started = true;
+  return PLSS_OK;
+}
+
+plss_status plss_eg_step(plss_ctx* ctx, int32_t k) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->eg_started) { set_err(ctx, "plss_eg_step before plss_eg_start"); return PLSS_E_STATE; }
+  if (k < 0) return PLSS_E_INVALID;
+  for (int i = 0; i + ctx->chunk <= k; i += ctx->chunk) CK(cudaGraphLaunch(ctx->eg_graph_chunk, ctx->stream));
+  for (int i = 0; i < k % ctx->chunk; ++i) CK(cudaGraphLaunch(ctx->eg_graph_one, ctx->stream));
+  return PLSS_OK;
+}
+
+plss_status plss_eg_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
+                           plss_outcome* outcome) {
+  if (!ctx) return PLSS_E_INVALID;
+  if (!ctx->eg_started) { set_err(ctx, "plss_eg_finish before plss_eg_start"); return PLSS_E_STATE; }
+  return alt_finish(ctx, x, iters, hist, diag, outcome);
+}
+
+plss_status plss_eg_solve(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* workspace, size_t ws_bytes,
+                          const int32_t* rows, uint64_t seed, const double* b, const double* x0, double tol,
+                          int32_t tol_mode, int32_t maxit, double* x, int32_t* iters, double* hist, double* diag,
+                          plss_outcome* outcome) {
+  plss_status s = plss_eg_start(ctx, sketch, kmax, workspace, ws_bytes, rows, seed, b, x0, tol, tol_mode, maxit);
+  if (s != PLSS_OK) return s;
+  if ((s = alt_run(ctx, ctx->eg_graph_chunk, ctx->eg_graph_one, maxit)) != PLSS_OK) return s;
+  return plss_eg_finish(ctx, x, iters, hist, diag, outcome);
+}
+
+plss_status plss_eg_profile(plss_ctx* ctx, int32_t k, double* ms) {
+  if (!ctx || !ms || k < 1) return PLSS_E_INVALID;
+  if (!ctx->eg_started) { set_err(ctx, "plss_eg_profile before plss_eg_start"); return PLSS_E_STATE; }
+  cudaStream_t st = ctx->stream;
+  const EgArgs& a = ctx->eg;
+  constexpr int NK = 5;
+  cudaEvent_t ev[NK + 1];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[NK] = {0, 0, 0, 0, 0};
+  for (int it = 0; it < k; ++it) {
+    CK(cudaEventRecord(ev[0], st));
+    if (a.mode == EG_IDENTITY) {
+      k_eg_row<<<1, EG_NT, 0, st>>>(a);
+    } else {
+      if (a.mode == EG_GAUSSIAN) k_eg_gauss<<<a.grid_s, EG_NT, 0, st>>>(a);
+      for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->eg_seg[s], ctx->g2[s], st);
+    }
+    CK(cudaEventRecord(ev[1], st));
+    k_eg_gemvT<<<a.grid_t, EG_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[2], st));
+    k_eg_tri<<<1, EG_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[3], st));
+    k_eg_gemv<<<a.grid_g, EG_NT, 0, st>>>(a);
+    CK(cudaEventRecord(ev[4], st));
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
+    CK(cudaEventRecord(ev[5], st));
+    CK(cudaGetLastError());
+    CK(cudaEventSynchronize(ev[5]));
+    for (int j = 0; j < NK; ++j) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
+      acc[j] += t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int j = 0; j < NK; ++j) ms[j] = acc[j] / k;
+  return PLSS_OK;
+}
+
+}  // extern "C"
+
 extern "C" {
 
 void plss_destroy(plss_ctx* ctx) {
@@ -1716,6 +1910,8 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->rp_graph_one) cudaGraphExecDestroy(ctx->rp_graph_one);
   if (ctx->kz_graph_chunk) cudaGraphExecDestroy(ctx->kz_graph_chunk);
   if (ctx->kz_graph_one) cudaGraphExecDestroy(ctx->kz_graph_one);
+  if (ctx->eg_graph_chunk) cudaGraphExecDestroy(ctx->eg_graph_chunk);
+  if (ctx->eg_graph_one) cudaGraphExecDestroy(ctx->eg_graph_one);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->h_done) cudaFreeHost(ctx->h_done);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);

@@ -29,7 +29,8 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_set_wi", "plss_column_norms", "plss_rp_workspace_bytes", "plss_rp_solve", "plss_rp_start",
            "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile",
            "plss_kz_workspace_bytes", "plss_kz_solve", "plss_kz_start", "plss_kz_step", "plss_kz_finish",
-           "plss_kz_profile"]
+           "plss_kz_profile", "plss_eg_workspace_bytes", "plss_eg_solve", "plss_eg_start", "plss_eg_step",
+           "plss_eg_finish", "plss_eg_profile"]
 
 
 class PlssError(RuntimeError):
@@ -128,6 +129,19 @@ def load_library(path: str = None):
     lib.plss_kz_solve.restype = st
     lib.plss_kz_profile.argtypes = [P, I32, P]
     lib.plss_kz_profile.restype = st
+    lib.plss_eg_workspace_bytes.argtypes = [P, I32]
+    lib.plss_eg_workspace_bytes.restype = ctypes.c_size_t
+    lib.plss_eg_start.argtypes = [P, I32, I32, P, ctypes.c_size_t, P, U64, P, P, D, I32, I32]
+    lib.plss_eg_start.restype = st
+    lib.plss_eg_step.argtypes = [P, I32]
+    lib.plss_eg_step.restype = st
+    lib.plss_eg_finish.argtypes = [P, P, ctypes.POINTER(I32), P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_eg_finish.restype = st
+    lib.plss_eg_solve.argtypes = [P, I32, I32, P, ctypes.c_size_t, P, U64, P, P, D, I32, I32, P, ctypes.POINTER(I32),
+                                  P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_eg_solve.restype = st
+    lib.plss_eg_profile.argtypes = [P, I32, P]
+    lib.plss_eg_profile.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
     lib.plss_status_str.argtypes = [st]
@@ -545,6 +559,81 @@ def plss_kz_profile(ctx: Ctx, k: int) -> dict:
     ms = np.zeros(4)
     _check(load_library().plss_kz_profile(ctx.handle, int(k), _ptr(ms)), ctx.handle)
     return dict(zip(["prep", "gemv", "spmv", "resid"], ms.tolist()))
+
+
+EG_SKETCH = {"residual": 0, "identity": 1, "gaussian": 2}
+
+
+def _eg_workspace(ctx: Ctx, kmax: int):
+    nbytes = int(load_library().plss_eg_workspace_bytes(ctx.handle, int(kmax)))
+    if nbytes == 0:
+        raise PlssError("plss_eg_workspace_bytes: invalid kmax or distributed ctx")
+    ws = getattr(ctx, "_eg_ws", None)
+    if ws is None or ws.numel() < nbytes + 256:
+        ctx._eg_ws = None
+        ws = ctx._eg_ws = _alloc_workspace(nbytes, ctx.A.row_ptr.device)
+    return _aligned(ws), nbytes
+
+
+def plss_eg_start(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, x0=None, tol=1e-8, tol_mode=0,
+                  maxit=100):
+    """Growing-sketch engine (Thm 2.1 / Cor 2.2) with residual / identity / gaussian sketch columns."""
+    lib = load_library()
+    kmax = int(maxit if kmax is None else kmax)
+    wp, nb = _eg_workspace(ctx, kmax)
+    rr = _rows_arg(rows) if rows is not None else None
+    ctx._keep = (b, x0, rr)
+    ctx._maxit = int(maxit)
+    _check(lib.plss_eg_start(ctx.handle, EG_SKETCH[sketch], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                             _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit)), ctx.handle)
+
+
+def plss_eg_step(ctx: Ctx, k: int):
+    _check(load_library().plss_eg_step(ctx.handle, int(k)), ctx.handle)
+
+
+def plss_eg_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
+    lib = load_library()
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(ctx._maxit + 1) if want_hist else None
+    diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
+    _check(lib.plss_eg_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+           ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if hist is not None:
+        res["hist"] = hist[:it.value + 1].copy()
+    return res
+
+
+def plss_eg_solve(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, x0=None, tol=1e-8, tol_mode=0,
+                  maxit=100, x=None, want_hist=True, want_diag=False):
+    """Full engine solve. Returns dict(x, iters, outcome, hist[0..iters][, diag])."""
+    import torch
+    lib = load_library()
+    if x is None:
+        x = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
+    kmax = int(maxit if kmax is None else kmax)
+    wp, nb = _eg_workspace(ctx, kmax)
+    rr = _rows_arg(rows) if rows is not None else None
+    it = ctypes.c_int32(0)
+    oc = ctypes.c_int(0)
+    hist = np.zeros(maxit + 1) if want_hist else None
+    diag = np.zeros((maxit + 1, REC)) if want_diag else None
+    ctx._maxit = int(maxit)
+    _check(lib.plss_eg_solve(ctx.handle, EG_SKETCH[sketch], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                             _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), _ptr(x), ctypes.byref(it),
+                             _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
+    res = _result(it.value, oc.value, hist, diag, x)
+    if hist is not None:
+        res["hist"] = hist[:it.value + 1].copy()
+    return res
+
+
+def plss_eg_profile(ctx: Ctx, k: int) -> dict:
+    ms = np.zeros(5)
+    _check(load_library().plss_eg_profile(ctx.handle, int(k), _ptr(ms)), ctx.handle)
+    return dict(zip(["sketch", "gemvT", "tri", "gemv", "k1"], ms.tolist()))
 
 
 def plss_destroy(ctx: Ctx):
