@@ -10,6 +10,7 @@ work. N > 1 (torchrun): row-block sharding, one NCCL all-reduce of n+1 doubles p
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5|C3|C4|C2] [--impl reference]
     python bench.py --method rp [--rp-r 5] [--rp-density 1.0]   # randomized projection (NEXT-2)
     python bench.py --method kz [--workload C2]                   # PLSS Kaczmarz (NEXT-3)
+    python bench.py --method eg [--eg-sketch gaussian]            # growing-sketch engine (NEXT-4)
 
 Prints ONE JSON line (rank 0).
 """
@@ -33,6 +34,17 @@ import plss_gen  # noqa: E402
 METRIC = "PLSS iterations/sec and achieved HBM GB/s (fraction of ~8 TB/s)"
 RP_METRIC = "Rand. Proj. (eq:pkLong, fresh Gaussian S_k) iterations/sec and achieved HBM GB/s"
 KZ_METRIC = "PLSS Kaczmarz (eq:pkKacz) iterations/sec and achieved HBM GB/s"
+EG_METRIC = "growing-sketch engine (Thm 2.1 / Cor 2.2) iterations/sec and achieved HBM GB/s"
+
+
+def eg_bytes_per_iter(m, n, nnz, hk, sketch):
+    """Algorithmic bytes of one engine step with hk stored columns: sketch
+    (Gaussian: s write + r read 16 m; residual / Gaussian: y = A^T s, 12 nnz + 4 (n+1) + 8 m + 8 n;
+    identity: the row, ~0); Y^T y: 8 n hk + 8 n; triangular update: 8 hk^2 (R twice, halves);
+    p = coef (y - Y t_hat): 8 n hk + 40 n (y, p, new Y column, x rw); K1: 12 nnz + 4 (m+1) + 8 n + 16 m."""
+    sk = {"gaussian": 16 * m + 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n,
+          "residual": 12 * nnz + 4 * (n + 1) + 8 * m + 8 * n, "identity": 0}[sketch]
+    return sk + 16 * n * hk + 48 * n + 8 * hk * hk + 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m
 
 
 def kz_bytes_per_iter(m, n, nnz, hk):
@@ -237,9 +249,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
-    ap.add_argument("--method", default="plss", choices=["plss", "rp", "kz"],
+    ap.add_argument("--method", default="plss", choices=["plss", "rp", "kz", "eg"],
                     help="rp: randomized projection (the paper's comparison method, NEXT-2); "
-                         "kz: PLSS Kaczmarz (section 7, NEXT-3)")
+                         "kz: PLSS Kaczmarz (section 7, NEXT-3); eg: growing-sketch engine (NEXT-4)")
+    ap.add_argument("--eg-sketch", default="gaussian", choices=["residual", "identity", "gaussian"])
     ap.add_argument("--rp-r", type=int, default=5, help="sketch size r (Experiment III: 5 for n > 1e5)")
     ap.add_argument("--rp-density", type=float, default=1.0, help="< 1: sparse normal sketch")
     args = ap.parse_args()
@@ -251,6 +264,12 @@ def main():
         if "--steps" not in sys.argv:
             args.steps = 1000
         return main_kz(args)
+    if args.method == "eg":
+        if args.workload == "C5":
+            args.workload = "C2"          # the stored Y grows by 8 n bytes per step
+        if "--steps" not in sys.argv:
+            args.steps = 500
+        return main_eg(args)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -627,6 +646,112 @@ def main_kz(args):
             "clocks": clk.summary(), "final_hist": float(fin["hist_full"][W + K])}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = kz_cpu_leg(s, workload_label(name), rows, B)
+    print(json.dumps(line), flush=True)
+    pkg.plss_destroy(ctx)
+
+
+# ---------------------------------------------------------------------------------------------
+# growing-sketch engine (--method eg): single device
+# ---------------------------------------------------------------------------------------------
+def main_eg(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    name, sk = args.workload, args.eg_sketch
+    s = plss_gen.make_config(name)
+    m, n, nnz = s.m, s.n, s.nnz
+    W, K = args.warmup, args.steps
+    cap = W + K + max(args.profile_steps, 1) + 8
+    rows = np.resize(np.random.default_rng(1).permutation(m), cap).astype(np.int32)
+    hk_mean = W + (K - 1) / 2.0
+    B = eg_bytes_per_iter(m, n, nnz, hk_mean, sk)
+    label = (workload_label(name) + f"; growing-sketch engine (triangular factorization), {sk} sketch columns, "
+             f"timed steps with history {W}..{W + K - 1}")
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import engine as oeg
+        k = max(1, min(args.steps, 150))
+        t0 = time.perf_counter()
+        oeg.tri_engine(s.scipy_csr(), s.b, sketch=sk, maxit=k, rows=rows, seed=1)
+        t = time.perf_counter() - t0
+        gbs = sum(eg_bytes_per_iter(m, n, nnz, h, sk) for h in range(k)) / t / 1e9
+        v = gbs * 1e9 / B
+        cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+        leg = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle",
+               "sample": f"the first {k} engine steps of the oracle in {t:.1f} s = {gbs:.2f} GB/s algorithmic, "
+                         f"scaled to the timed window by bytes/iter"}
+        print(json.dumps({"metric": EG_METRIC, "value": v, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": label}, "cpu_baseline": leg,
+                          "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+    import torch
+    import paper_2207_07615_b200 as pkg
+    assert world == 1, "growing-sketch engine: single device"
+    assert args.warmup >= 3 or args.ncu, "timing rules: at least 3 warm-up steps"
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pkg.load_library()
+    A = pkg.Matrix.from_arrays(m, n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=cap, stream=stream)
+    q = pkg.plss_query(ctx)
+    b = torch.from_numpy(s.b).to(dev)
+    drows = torch.from_numpy(rows).to(dev)
+    torch.cuda.synchronize()
+    pkg.plss_eg_start(ctx, b, sketch=sk, kmax=cap, rows=drows, seed=1, tol=0.0, maxit=cap)
+    pkg.plss_eg_step(ctx, W)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        pkg.plss_eg_step(ctx, K)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    fin = pkg.plss_eg_finish(ctx, None, want_hist=True, want_diag=True)
+    skipped = int(fin["diag"][1:W + K + 1, 3].sum())
+    its = K / (ms / 1e3)
+    if args.ncu:
+        print(json.dumps({"ncu_run": True, "ms_per_step": ms / K}), flush=True)
+        return
+    kt = pkg.plss_eg_profile(ctx, max(1, args.profile_steps))
+    hk_prof = W + K - skipped + (max(1, args.profile_steps) - 1) / 2.0
+    cls = {"eg_gemvT_history": (kt["gemvT"], 8 * n * hk_prof + 8 * n),
+           "eg_gemv_history": (kt["gemv"], 8 * n * hk_prof + 40 * n),
+           "eg_tri": (kt["tri"], 8 * hk_prof * hk_prof), "k1_spmv_csr_resid": (kt["k1"], 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m)}
+    dom = max(cls, key=lambda c: cls[c][0])
+    dom_ms, dom_bytes = cls[dom]
+    peak, peak_src = _peaks()
+    pin_b = torch.empty(m, dtype=torch.float64, pin_memory=True)
+    pin_b.copy_(b.cpu())
+    pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pkg.plss_eg_solve(ctx, pin_b, sketch=sk, kmax=cap, rows=rows, seed=1, tol=0.0, maxit=W + K, x=pin_x)
+    t_e2e = time.perf_counter() - t0
+    line = {"metric": EG_METRIC, "value": its, "unit": "it/s", "n_gpus": 1, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": label, "m": m, "n": n, "nnz": nnz, "sketch": sk, "history_mean": hk_mean,
+                       "parallelism": "single", "slabs": q["slabs"], "tol": 0.0, "skipped_steps": skipped,
+                       "l2": f"stored Y is {8 * n * (W + K) / 1e9:.2f} GB at the end (> L2 after "
+                             f"{126e6 / (8 * n):.0f} steps)",
+                       "bytes_per_step_model": "sketch + 16 n hk + 8 hk^2 + 48 n + K1"},
+            "achieved_gbs": B * its / 1e9, "achieved_frac_of_peak": B * its / 1e9 / peak,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_bytes / (dom_ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "peak_source": peak_src, "algorithmic_bytes_per_step": dom_bytes,
+                         "kernel_ms_per_step": dom_ms, "history_at_profile": hk_prof},
+            "kernels_ms_per_step": kt, "gpu_launches": K * (5 + 2 * q["slabs"]),
+            "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": 8 * m / (W + K),
+                    "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
+                    "note": "one plss_eg_solve from pinned host b to host x + history (from history 0)"},
+            "clocks": clk.summary(), "final_hist": float(fin["hist_full"][W + K])}
     print(json.dumps(line), flush=True)
     pkg.plss_destroy(ctx)
 

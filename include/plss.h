@@ -272,7 +272,8 @@ plss_status plss_eg_step(plss_ctx *ctx, int32_t k);
 plss_status plss_eg_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
                            plss_outcome *outcome);
 /* Per-kernel device ms per step (CUDA events, one kernel at a time) after plss_eg_start; ms
- * (host, 5 doubles): sketch + y = A^T s, Y^T y partials, triangular update, p = coef (y - Y t_hat),
+ * (host, 5 doubles): sketch + y = A^T s, Y^T y (partials + their reduction), triangular update,
+ * p = coef (y - Y t_hat),
  * K1 (r <- r - A p). */
 plss_status plss_eg_profile(plss_ctx *ctx, int32_t k, double *ms);
 

@@ -11,11 +11,14 @@
 //   k_eg_row    identity sketch: one CTA swaps row i into the dense y (y_k = a_i), s^T r = r[i]
 //   k_eg_gauss  Gaussian sketch: s_i = binary32 normal (randomized projection's generator, r = 1),
 //               partials of s^T r; y = A^T s follows by the K2 segments
-//   k_eg_gemvT  partials of Y^T y and y^T y: CTA b stages tiles of y in shared memory, thread j
-//               walks column j of its row range (ascending l)
-//   k_eg_tri    one CTA: fixed-order sums of the partials, u = R^T g, u ./= delta, t_hat = R u,
-//               delta, coefficient, skip (reading R22), append t_hat to R and 1/delta to D,
-//               iteration counter
+//   k_eg_gemvT  partials of Y^T y and y^T y over CTA b's row range: a warp per column j, lanes over
+//               the rows (coalesced 256-byte reads of Y, y from L1), fixed butterfly per column
+//   k_eg_red    fixed-order sums of the partials (a warp per entry, many CTAs): g, y^T y, s^T r
+//   k_eg_triu   u = D R^T g: a warp per column of R (coalesced), many CTAs
+//   k_eg_trit   t_hat = R u: CTAs of 32 rows, 8 warps striding the columns (coalesced 256-byte
+//               rows of R), fixed-order combination; delta partials; the last CTA: delta,
+//               coefficient, skip (reading R22), append t_hat to R and 1/delta to D, iteration
+//               counter
 //   k_eg_gemv   p = coef (y - Y t_hat) (history split in 4, fixed-order combination), x += p,
 //               append y to Y
 #pragma once
@@ -53,8 +56,12 @@ struct EgArgs {
   double* Y;                  // n x kmax, column-major
   double* R;                  // kmax x kmax, column-major (t_hat_j in column j, rows < j)
   double* dinv;               // [kmax] 1/delta_j
-  double* gv;                 // [kmax] g, then u
+  double* gv;                 // [kmax + 2] g | y^T y | s^T r (Gaussian)
   double* th;                 // [kmax] t_hat of this step
+  double* uv;                 // [kmax] u = D R^T g
+  double* part_tri;           // [2 grid_tri] delta partial pairs (publish_and_elect)
+  unsigned* counter;
+  int32_t grid_tri;
   double* part;               // [grid_t][kmax + 1] partials of Y^T y | y^T y
   double* part_rs;            // [grid_s] partials of s^T r (Gaussian)
   double* p;
@@ -97,111 +104,147 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gauss(EgArgs a) {
   if (threadIdx.x == 0) a.part_rs[blockIdx.x] = acc;
 }
 
-// partials of g_j = Y[:, j]^T y (j < hk) and y^T y over CTA b's contiguous row range
+// partials of g_j = Y[:, j]^T y (j < hk) and y^T y over CTA b's contiguous row range: warp w takes
+// columns w, w + 8, ..., four at a time (independent loads in flight), lanes stride the rows
 __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   if (eg_done(a)) return;
-  __shared__ double ys[EG_TILE];
-  __shared__ double sm[2][MAXW];
   const int hk = a.st->hk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = EG_NT / 32;
   const int64_t per = (a.n + gridDim.x - 1) / gridDim.x;
   const int64_t l0 = (int64_t)blockIdx.x * per, l1 = min(a.n, l0 + per);
   double* out = a.part + (size_t)blockIdx.x * (a.kmax + 1);
-  double yy = 0.0, z = 0.0;
-  for (int64_t l = l0 + threadIdx.x; l < l1; l += EG_NT) {
-    const double v = a.y[l];
-    yy = __dadd_rn(yy, __dmul_rn(v, v));
+  if (warp == 0) {
+    double yy = 0.0;
+    for (int64_t l = l0 + lane; l < l1; l += 32) {
+      const double v = __ldg(a.y + l);
+      yy = __dadd_rn(yy, __dmul_rn(v, v));
+    }
+    yy = warp_sum(yy);
+    if (lane == 0) out[a.kmax] = yy;
   }
-  block_sum2(yy, z, sm);
-  if (threadIdx.x == 0) out[a.kmax] = yy;
-  for (int jb = 0; jb < hk; jb += EG_NT) {
-    const int j = jb + threadIdx.x;
-    double acc = 0.0;
-    for (int64_t t0 = l0; t0 < l1; t0 += EG_TILE) {
-      const int cnt = (int)min((int64_t)EG_TILE, l1 - t0);
-      __syncthreads();
-      for (int e = threadIdx.x; e < cnt; e += EG_NT) ys[e] = a.y[t0 + e];
-      __syncthreads();
-      if (j < hk) {
-        const double* col = a.Y + (int64_t)j * a.n + t0;
-        int e = 0;
-        for (; e + 8 <= cnt; e += 8) {
-          double yv[8];
+  // columns j, j + NW, j + 2 NW, j + 3 NW at once, rows two per lane step: 8 independent loads
+  int j = warp;
+  for (; j + 3 * NW < hk; j += 4 * NW) {
+    const double* c[4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) yv[u] = __ldg(col + e + u);
+    for (int q = 0; q < 4; ++q) c[q] = a.Y + (int64_t)(j + q * NW) * a.n;
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t l = l0 + lane;
+    for (; l + 32 < l1; l += 64) {
+      const double y0 = __ldg(a.y + l), y1 = __ldg(a.y + l + 32);
+      double v0[4], v1[4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(yv[u], ys[e + u]));
-        }
-        for (; e < cnt; ++e) acc = __dadd_rn(acc, __dmul_rn(__ldg(col + e), ys[e]));
+      for (int q = 0; q < 4; ++q) { v0[q] = __ldg(c[q] + l); v1[q] = __ldg(c[q] + l + 32); }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        sa[q] = __dadd_rn(sa[q], __dmul_rn(v0[q], y0));
+        sb[q] = __dadd_rn(sb[q], __dmul_rn(v1[q], y1));
       }
     }
-    if (j < hk) out[j] = acc;
+    if (l < l1) {
+      const double y0 = __ldg(a.y + l);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sa[q] = __dadd_rn(sa[q], __dmul_rn(__ldg(c[q] + l), y0));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double v = warp_sum(__dadd_rn(sa[q], sb[q]));
+      if (lane == 0) out[j + q * NW] = v;
+    }
+  }
+  for (; j < hk; j += NW) {
+    const double* c0 = a.Y + (int64_t)j * a.n;
+    double s0 = 0.0;
+    for (int64_t l = l0 + lane; l < l1; l += 32) s0 = __dadd_rn(s0, __dmul_rn(__ldg(c0 + l), __ldg(a.y + l)));
+    s0 = warp_sum(s0);
+    if (lane == 0) out[j] = s0;
   }
 }
 
-__global__ void __launch_bounds__(EG_NT) k_eg_tri(EgArgs a) {
+// gv[e] = sum over the gemvT CTAs of part[.][e] for e < hk, gv[kmax] = y^T y, gv[kmax+1] = s^T r
+// (Gaussian): one warp per entry, lane-strided partial sums in CTA order, fixed butterfly
+__global__ void __launch_bounds__(EG_NT) k_eg_red(EgArgs a) {
+  if (eg_done(a)) return;
+  const int hk = a.st->hk, K = a.kmax, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (EG_NT / 32) + (threadIdx.x >> 5);
+  if (e > hk + 1) return;
+  double s = 0.0;
+  if (e <= hk) {
+    const int col = e < hk ? e : K;
+    for (int g = lane; g < a.grid_t; g += 32) s = __dadd_rn(s, a.part[(size_t)g * (K + 1) + col]);
+  } else if (a.mode == EG_GAUSSIAN) {
+    for (int g = lane; g < a.grid_s; g += 32) s = __dadd_rn(s, a.part_rs[g]);
+  }
+  s = warp_sum(s);
+  if (lane == 0) a.gv[e < hk ? e : (e == hk ? K : K + 1)] = s;
+}
+
+// u_j = (sum_{i<j} R[i][j] g_i - g_j) / delta_j for j < hk: one warp per j
+__global__ void __launch_bounds__(EG_NT) k_eg_triu(EgArgs a) {
+  if (eg_done(a)) return;
+  const int hk = a.st->hk, K = a.kmax, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (EG_NT / 32) + (threadIdx.x >> 5);
+  if (j >= hk) return;
+  const double* Rc = a.R + (size_t)j * K;
+  double s = 0.0;
+  for (int i = lane; i < j; i += 32) s = __dadd_rn(s, __dmul_rn(Rc[i], a.gv[i]));
+  s = warp_sum(s);
+  if (lane == 0) a.uv[j] = __dmul_rn(__dadd_rn(s, -a.gv[j]), a.dinv[j]);
+}
+
+// t_hat_i = sum_{j>i} R[i][j] u_j - u_i for the CTA's 32 rows i; delta = y^T y - g^T t_hat
+__global__ void __launch_bounds__(EG_NT) k_eg_trit(EgArgs a) {
   if (eg_done(a)) return;
   __shared__ double sm[2][MAXW];
-  __shared__ double s_yy, s_rs;
+  __shared__ double pt[EG_NT / 32][32];
   EgState* st = a.st;
-  const int hk = st->hk, K = a.kmax, t = threadIdx.x, lane = t & 31;
-  // g_j and y^T y: one warp per entry, lane-strided over the CTA partials, fixed butterfly
-  for (int e = t >> 5; e <= hk; e += EG_NT / 32) {
-    const int col = e < hk ? e : K;
-    double s = 0.0;
-    for (int g = lane; g < a.grid_t; g += 32) s = __dadd_rn(s, a.part[(size_t)g * (K + 1) + col]);
-    s = warp_sum(s);
-    if (lane == 0) { if (e < hk) a.gv[e] = s; else s_yy = s; }
+  const int hk = st->hk, K = a.kmax, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = EG_NT / 32;
+  const int i = blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (blockIdx.x * 32 < hk) {
+    for (int j = blockIdx.x * 32 + 1 + warp; j < hk; j += NW)
+      if (j > i) acc = __dadd_rn(acc, __dmul_rn(a.R[(size_t)j * K + i], a.uv[j]));
   }
-  if (t == 0) {
-    double rs;
-    if (a.mode == EG_RESIDUAL) rs = a.ctl->rho;                    // r^T r of the last K1
-    else if (a.mode == EG_IDENTITY) rs = a.r[st->cur_row];
-    else { rs = 0.0; for (int g = 0; g < a.grid_s; ++g) rs = __dadd_rn(rs, a.part_rs[g]); }
-    s_rs = rs;
-  }
+  pt[warp][lane] = acc;
   __syncthreads();
-  // u = R^T g: u_j = sum_{i<j} R[i][j] g_i - g_j, then u_j /= delta_j (stored in th)
-  for (int j = t; j < hk; j += EG_NT) {
-    const double* Rc = a.R + (size_t)j * K;
-    double u = 0.0;
-    for (int i = 0; i < j; ++i) u = __dadd_rn(u, __dmul_rn(Rc[i], a.gv[i]));
-    a.th[j] = __dmul_rn(__dadd_rn(u, -a.gv[j]), a.dinv[j]);
-  }
-  __syncthreads();
-  // t_hat = R u: t_hat_i = sum_{j>i} R[i][j] u_j - u_i; delta partial g_i t_hat_i
   double gt = 0.0, z = 0.0;
-  for (int i = t; i < hk; i += EG_NT) {
-    double v = 0.0;
-    for (int j = i + 1; j < hk; ++j) v = __dadd_rn(v, __dmul_rn(a.R[(size_t)j * K + i], a.th[j]));
-    const double ti = __dadd_rn(v, -a.th[i]);
-    a.R[(size_t)hk * K + i] = ti;              // next column of R (valid only if not skipped)
-    gt = __dadd_rn(gt, __dmul_rn(a.gv[i], ti));
+  if (warp == 0 && i < hk) {
+    double t = pt[0][lane];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) t = __dadd_rn(t, pt[w][lane]);
+    t = __dadd_rn(t, -a.uv[i]);
+    a.th[i] = t;
+    a.R[(size_t)hk * K + i] = t;               // next column of R (kept only if not skipped)
+    gt = __dmul_rn(a.gv[i], t);
   }
-  block_sum2(gt, z, sm);
-  __syncthreads();
-  for (int i = t; i < hk; i += EG_NT) a.th[i] = a.R[(size_t)hk * K + i];
-  if (t == 0) {
-    const double yy = s_yy, rs = s_rs;
-    const double delta = __dadd_rn(yy, -gt);
-    const bool skip = yy == 0.0 || delta <= EG_SKIP_REL * yy || rs == 0.0;   // reading R22
-    st->skip = skip ? 1 : 0;
-    st->coef = skip ? 0.0 : __ddiv_rn(rs, delta);
-    st->hk_use = hk;
-    if (!skip) {
-      a.dinv[hk] = __ddiv_rn(1.0, delta);
-      st->hk = (hk + 1 == K) ? 0 : hk + 1;     // reading R21 / R22: history reset at kmax
-    } else {
-      st->skipped += 1;
-    }
-    Ctl* c = a.ctl;
-    const int k = c->iters + 1;
-    c->iters = k;
-    double* rk = a.rec + (size_t)k * REC;
-    rk[2] = delta;
-    rk[3] = (double)skip;
-    rk[4] = rs;
-    rk[5] = (double)st->hk;
+  if (!publish_and_elect(gt, z, a.part_tri, a.part_tri, gridDim.x, a.counter, sm)) return;
+  if (threadIdx.x != 0) return;
+  double rs;
+  if (a.mode == EG_RESIDUAL) rs = a.ctl->rho;                      // r^T r of the last K1
+  else if (a.mode == EG_IDENTITY) rs = __ldcg(a.r + st->cur_row);
+  else rs = a.gv[K + 1];
+  const double yy = a.gv[K];
+  const double delta = __dadd_rn(yy, -gt);
+  const bool skip = yy == 0.0 || delta <= EG_SKIP_REL * yy || rs == 0.0;     // reading R22
+  st->skip = skip ? 1 : 0;
+  st->coef = skip ? 0.0 : __ddiv_rn(rs, delta);
+  st->hk_use = hk;
+  if (!skip) {
+    a.dinv[hk] = __ddiv_rn(1.0, delta);
+    st->hk = (hk + 1 == K) ? 0 : hk + 1;       // reading R21 / R22: history reset at kmax
+  } else {
+    st->skipped += 1;
   }
+  Ctl* c = a.ctl;
+  const int k = c->iters + 1;
+  c->iters = k;
+  double* rk = a.rec + (size_t)k * REC;
+  rk[2] = delta;
+  rk[3] = (double)skip;
+  rk[4] = rs;
+  rk[5] = (double)st->hk;
 }
 
 // p = coef (y - Y t_hat): tiles of 64 l, 4 groups each summing a quarter of the history columns

@@ -1716,7 +1716,7 @@ plss_status plss_kz_profile(plss_ctx* ctx, int32_t k, double* ms) {
 // ---- growing-sketch engine, triangular factorization (eg_kernels.cuh) --------
 static void eg_grids(const plss_ctx* ctx, int* g_t, int* g_s, int* g_g) {
   const int sms = rp_sms(ctx);
-  *g_t = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + 511) / 512, 2 * (int64_t)sms));
+  *g_t = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + 255) / 256, 2 * (int64_t)sms));
   *g_s = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + EG_NT - 1) / EG_NT, 4 * (int64_t)sms));
   *g_g = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + 63) / 64, 8 * (int64_t)sms));
 }
@@ -1724,7 +1724,7 @@ static size_t eg_bytes(const plss_ctx* ctx, int kmax) {
   int gt, gs, gg;
   eg_grids(ctx, &gt, &gs, &gg);
   const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
-  return align_up(8 * n * K) + align_up(8 * K * K) + 3 * align_up(8 * K) + align_up(8 * (K + 1) * (size_t)gt) +
+  return align_up(8 * n * K) + align_up(8 * K * K) + 4 * align_up(8 * (K + 2)) + align_up(16 * (K / 32 + 1)) + align_up(256) + align_up(8 * (K + 1) * (size_t)gt) +
          align_up(8 * (size_t)gs) + align_up(8 * m) + align_up(sizeof(EgState)) + align_up(4 * (size_t)(ctx->L.maxit_cap + 1));
 }
 static plss_status eg_enqueue_step(plss_ctx* ctx) {
@@ -1737,7 +1737,9 @@ static plss_status eg_enqueue_step(plss_ctx* ctx) {
     for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->eg_seg[s], ctx->g2[s], st);   // y = A^T s
   }
   k_eg_gemvT<<<a.grid_t, EG_NT, 0, st>>>(a);
-  k_eg_tri<<<1, EG_NT, 0, st>>>(a);
+  k_eg_red<<<(a.kmax + 2 + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
+  k_eg_triu<<<(a.kmax + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
+  k_eg_trit<<<a.grid_tri, EG_NT, 0, st>>>(a);
   k_eg_gemv<<<a.grid_g, EG_NT, 0, st>>>(a);
   for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);     // r -= A p, rho, stop
   CK(cudaGetLastError());
@@ -1791,9 +1793,13 @@ plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* wor
   const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
   a.Y = (double*)take(8 * n * K);
   a.R = (double*)take(8 * K * K);
-  a.dinv = (double*)take(8 * K);
-  a.gv = (double*)take(8 * K);
-  a.th = (double*)take(8 * K);
+  a.dinv = (double*)take(8 * (K + 2));
+  a.gv = (double*)take(8 * (K + 2));
+  a.th = (double*)take(8 * (K + 2));
+  a.uv = (double*)take(8 * (K + 2));
+  a.grid_tri = (int)(K / 32 + 1);
+  a.part_tri = (double*)take(16 * (K / 32 + 1));
+  a.counter = (unsigned*)take(256);
   a.part = (double*)take(8 * (K + 1) * (size_t)a.grid_t);
   a.part_rs = (double*)take(8 * (size_t)a.grid_s);
   a.s = (double*)take(8 * m);
@@ -1811,6 +1817,7 @@ plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* wor
   EgState s0{};
   s0.prev_row = -1;
   CK(cudaMemcpyAsync(a.st, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(a.counter, 0, 256, st));
   if (!hrows.empty()) CK(cudaMemcpyAsync(drows, hrows.data(), 4 * (size_t)maxit, cudaMemcpyHostToDevice, st));
   if (n > 0) CK(cudaMemsetAsync(ctx->y, 0, 8 * n, st));
   CK(cudaStreamSynchronize(st));   // host temporaries
@@ -1877,8 +1884,10 @@ plss_status plss_eg_profile(plss_ctx* ctx, int32_t k, double* ms) {
     }
     CK(cudaEventRecord(ev[1], st));
     k_eg_gemvT<<<a.grid_t, EG_NT, 0, st>>>(a);
+    k_eg_red<<<(a.kmax + 2 + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
     CK(cudaEventRecord(ev[2], st));
-    k_eg_tri<<<1, EG_NT, 0, st>>>(a);
+    k_eg_triu<<<(a.kmax + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
+    k_eg_trit<<<a.grid_tri, EG_NT, 0, st>>>(a);
     CK(cudaEventRecord(ev[3], st));
     k_eg_gemv<<<a.grid_g, EG_NT, 0, st>>>(a);
     CK(cudaEventRecord(ev[4], st));

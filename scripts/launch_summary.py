@@ -4,7 +4,7 @@ import re
 import sys
 from collections import defaultdict
 
-OURS = re.compile(r"k_(?:spmv|sellw?)<(\d)[^>]*>|k_rp_[a-z]+|k_kz_[a-z]+|k_pxupdate|k_norm_b|k_dots_tail|k_set_nbd|k_tile_|k_scan_|k_slab_|k_validate")
+OURS = re.compile(r"k_(?:spmv|sellw?)<(\d)[^>]*>|k_rp_[a-z]+|k_kz_[a-z]+|k_eg_[a-zT]+|k_pxupdate|k_norm_b|k_dots_tail|k_set_nbd|k_tile_|k_scan_|k_slab_|k_validate")
 ROLE = {"0": "k_spmv<plain>", "1": "k1_spmv_csr_resid", "2": "k2_spmv_csc_gather", "3": "k2_spmv_csc_gather+dots"}
 
 
@@ -24,7 +24,7 @@ def main(path):
     for name, ns, g, b in rows:
         agg[name][0] += 1
         agg[name][1] += ns
-    hot = {k: v for k, v in agg.items() if k.startswith(("k1", "k2", "k_px", "k_dots", "k_rp", "k_kz", "k_spmv<plain>"))}
+    hot = {k: v for k, v in agg.items() if k.startswith(("k1", "k2", "k_px", "k_dots", "k_rp", "k_kz", "k_eg", "k_spmv<plain>"))}
     tot = sum(v[1] for v in hot.values())
     print(f"{'kernel':32s} {'launches':>8s} {'total us':>10s} {'avg us':>9s} {'share of step':>14s}")
     for k, (c, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):

@@ -171,3 +171,19 @@ def test_c5_full_randproj_sampled_and_projection(pkg, c5):
         true_h = float(torch.linalg.norm(d["b"] - ax)) / nb
         assert abs(out["hist_full"][k] - true_h) <= 1e-10 * true_h
         x_prev.copy_(x)
+
+
+def test_c5_full_engine_residual_sketch_is_plss(pkg, c5):
+    """Thm 4.1 at C5 scale: the general growing-sketch engine with residual sketches (Cor 2.2:
+    p_k = (r^T r / delta)(y - Y t_hat)) produces the same residual history as PLSS's short
+    recursion over the first iterations (both on the GPU, the engine from the oracle-pinned
+    triangular recursion)."""
+    d, ctx = c5
+    k = 12
+    a = pkg.plss_solve(ctx, d["b"], tol=0.0, maxit=k, flags=0)
+    e = pkg.plss_eg_solve(ctx, d["b"], sketch="residual", maxit=k, tol=0.0)
+    torch.cuda.empty_cache()
+    assert a["iters"] == e["iters"] == k
+    np.testing.assert_allclose(e["hist"][:k], a["hist"][:k], rtol=1e-9)
+    xa, xe = a["x"], e["x"]
+    assert float(torch.linalg.norm(xa - xe) / torch.linalg.norm(xa)) <= 1e-9
