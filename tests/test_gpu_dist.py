@@ -92,3 +92,20 @@ def test_dist_single_rank_plssw(pkg):
     k = min(25, len(ref["hist"]), len(res["hist"]))
     assert np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
     assert np.linalg.norm(res["x"].cpu().numpy() - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
+
+
+def test_dist_ctx_rejects_single_device_methods(pkg):
+    """Randomized projection, PLSS Kaczmarz and the growing-sketch engine run on single-device
+    ctxs only (include/plss.h): a distributed ctx reports E_INVALID with a message, and its PLSS
+    solve still works afterwards."""
+    s = plss_gen.make_config("C2s")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, maxit_cap=100)
+    for call in (lambda: pkg.plss_rp_solve(ctx, s.b, r=4, maxit=3),
+                 lambda: pkg.plss_kz_solve(ctx, s.b, np.arange(3), maxit=3),
+                 lambda: pkg.plss_eg_solve(ctx, s.b, sketch="residual", maxit=3)):
+        with pytest.raises(pkg.PlssError):
+            call()
+    out = pkg.plss_solve(ctx, s.b, tol=1e-6, maxit=100)
+    assert out["outcome"] in ("converged", "maxit") and out["iters"] > 0
+    pkg.plss_destroy(ctx)
