@@ -23,9 +23,14 @@ Readings (R22): delta_k <= 1e-14 y_k^T y_k (y_k numerically in range(Y
 or s_k^T r_{k-1} = 0 skip the step (p_k = 0, nothing appended); after kmax stored columns the
 history is cleared (as R21). The residual is recursive (R19).
 
+`qr_engine` is the QR variant (section 2.3, eq:ykeqQR / eq:pkQR, L247-282): Y_k = Q_k T_k by a
+Householder QR (LAPACK through numpy, recomputed each step: the definition, not the update) and
+p_k = (s_k^T r_{k-1} / r_kk) q_k with q_k, r_kk the last column of Q_k and last diagonal of T_k;
+the skip rule compares r_kk^2 (= delta_k) with 1e-14 y_k^T y_k.
+
 Parity pins (tests/test_oracle_engine.py): R D R^T equals inv(Y^T Y) (Thm 2.1); iterates equal
-eq:pkLong with the same sketch through a dense pseudo-inverse; residual sketch == the PLSS oracle
-(Thm 4.1); identity sketch == the PLSS Kaczmarz oracle; orthogonal updates.
+eq:pkLong with the same sketch through a dense pseudo-inverse (both engines); residual sketch ==
+the PLSS oracle (Thm 4.1); identity sketch == the PLSS Kaczmarz oracle; orthogonal updates.
 """
 from __future__ import annotations
 
@@ -111,6 +116,60 @@ def tri_engine(A, b, sketch="residual", maxit=100, tol=0.0, tol_mode=0, x0=None,
             k = maxit
     out = {"x": x, "iters": k, "outcome": outcome, "hist": np.array(hist), "skipped": skipped,
            "delta": np.array(deltas)}
+    if keep:
+        out["P"] = allP
+    return out
+
+
+def qr_engine(A, b, sketch="residual", maxit=100, tol=0.0, tol_mode=0, x0=None, rows=None, seed=0,
+              kmax=None, keep=False):
+    """eq:pkQR: p_k = (s_k^T r_{k-1} / r_kk) q_k from the Householder QR of Y_k (section 2.3)."""
+    A = sp.csr_matrix(A) if not sp.issparse(A) else A.tocsr()
+    m, n = A.shape
+    b = np.asarray(b, dtype=np.float64)
+    kmax = maxit if kmax is None else int(kmax)
+    x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
+    r = b - A @ x
+    nb = float(np.linalg.norm(b)) if tol_mode == 0 else 1.0
+    nb = nb if nb > 0 else 1.0
+    rho = float(r @ r)
+    hist = [np.sqrt(rho) / nb]
+    Y, allP = [], []
+    skipped = 0
+    outcome = "maxit"
+    k = 0
+    if rho == 0.0 or hist[0] <= tol:
+        outcome = "converged"
+    else:
+        for k in range(1, maxit + 1):
+            s = sketch_column(sketch, k, m, r, rows, seed)
+            y = A.T @ s
+            rs = float(s @ r)
+            yy = float(y @ y)
+            if len(Y) < n and yy > 0.0:
+                Q, T = np.linalg.qr(np.stack(Y + [y], axis=1))     # Householder (LAPACK geqrf)
+                rkk = float(T[-1, -1])
+            else:
+                rkk = 0.0
+            if yy == 0.0 or rkk * rkk <= SKIP_REL * yy or rs == 0.0:
+                skipped += 1                                       # reading R22
+            else:
+                p = (rs / rkk) * Q[:, -1]                          # eq:pkQR
+                x = x + p
+                r = r - A @ p
+                Y.append(y)
+                if keep:
+                    allP.append(p)
+                if len(Y) == kmax:
+                    Y = []
+            rho = float(r @ r)
+            hist.append(np.sqrt(rho) / nb)
+            if rho == 0.0 or hist[-1] <= tol:
+                outcome = "converged"
+                break
+        else:
+            k = maxit
+    out = {"x": x, "iters": k, "outcome": outcome, "hist": np.array(hist), "skipped": skipped}
     if keep:
         out["P"] = allP
     return out

@@ -64,6 +64,21 @@ def test_equals_pk_long_all_sketches():
                 np.testing.assert_allclose(x, xr, rtol=0, atol=1e-8 * max(1.0, np.linalg.norm(xr)))
 
 
+def test_qr_engine_equals_pk_long_and_triangular():
+    for kind in ("residual", "identity", "gaussian"):
+        A, b = _system(7)
+        rows = np.random.default_rng(2).permutation(A.shape[0])
+        K = 10
+        ref = _pk_long_sketch(A, b, kind, K, rows, 3)
+        q = engine.qr_engine(A, b, sketch=kind, maxit=K, rows=rows, seed=3, keep=True)
+        t = engine.tri_engine(A, b, sketch=kind, maxit=K, rows=rows, seed=3)
+        x = np.zeros(A.shape[1])
+        for p, xr in zip(q["P"], ref):
+            x = x + p
+            np.testing.assert_allclose(x, xr, rtol=0, atol=1e-8 * max(1.0, np.linalg.norm(xr)))
+        np.testing.assert_allclose(q["hist"], t["hist"], rtol=1e-8, atol=1e-15)
+
+
 def test_residual_sketch_is_plss():
     s = plss_gen.make_config("C1")
     ref = oracle.plss_system(s, maxit=40, tol=0.0)
