@@ -47,6 +47,11 @@ def eg_bytes_per_iter(m, n, nnz, hk, sketch):
     return sk + 16 * n * hk + 48 * n + 8 * hk * hk + 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m
 
 
+def eg_qr_bytes_per_iter(m, n, nnz, hk, sketch):
+    """The QR variant streams the store four times (V^T y, y - V b, V^T v, e_h - V z)."""
+    return eg_bytes_per_iter(m, n, nnz, hk, sketch) + 16 * n * hk + 48 * n
+
+
 def kz_bytes_per_iter(m, n, nnz, hk):
     """Algorithmic bytes of one PLSS Kaczmarz step with hk stored updates:
     GEMV: P (8 n hk) + arow, pk, new P column, x rw (40 n); SpMV A p: 12 nnz + 4 (m+1) + 8 n + 8 m;
@@ -253,6 +258,7 @@ def main():
                     help="rp: randomized projection (the paper's comparison method, NEXT-2); "
                          "kz: PLSS Kaczmarz (section 7, NEXT-3); eg: growing-sketch engine (NEXT-4)")
     ap.add_argument("--eg-sketch", default="gaussian", choices=["residual", "identity", "gaussian"])
+    ap.add_argument("--eg-factor", default="triangular", choices=["triangular", "qr"])
     ap.add_argument("--rp-r", type=int, default=5, help="sketch size r (Experiment III: 5 for n > 1e5)")
     ap.add_argument("--rp-density", type=float, default=1.0, help="< 1: sparse normal sketch")
     args = ap.parse_args()
@@ -663,8 +669,9 @@ def main_eg(args):
     cap = W + K + max(args.profile_steps, 1) + 8
     rows = np.resize(np.random.default_rng(1).permutation(m), cap).astype(np.int32)
     hk_mean = W + (K - 1) / 2.0
-    B = eg_bytes_per_iter(m, n, nnz, hk_mean, sk)
-    label = (workload_label(name) + f"; growing-sketch engine (triangular factorization), {sk} sketch columns, "
+    fac = args.eg_factor
+    B = (eg_bytes_per_iter if fac == "triangular" else eg_qr_bytes_per_iter)(m, n, nnz, hk_mean, sk)
+    label = (workload_label(name) + f"; growing-sketch engine ({fac} factorization), {sk} sketch columns, "
              f"timed steps with history {W}..{W + K - 1}")
     if args.impl == "reference":
         if rank != 0:
@@ -672,9 +679,11 @@ def main_eg(args):
         from oracle import engine as oeg
         k = max(1, min(args.steps, 150))
         t0 = time.perf_counter()
-        oeg.tri_engine(s.scipy_csr(), s.b, sketch=sk, maxit=k, rows=rows, seed=1)
+        (oeg.tri_engine if fac == "triangular" else oeg.qr_engine)(s.scipy_csr(), s.b, sketch=sk, maxit=k, rows=rows,
+                                                                    seed=1)
         t = time.perf_counter() - t0
-        gbs = sum(eg_bytes_per_iter(m, n, nnz, h, sk) for h in range(k)) / t / 1e9
+        bfn = eg_bytes_per_iter if fac == "triangular" else eg_qr_bytes_per_iter
+        gbs = sum(bfn(m, n, nnz, h, sk) for h in range(k)) / t / 1e9
         v = gbs * 1e9 / B
         cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
         leg = {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle",
@@ -702,7 +711,7 @@ def main_eg(args):
     b = torch.from_numpy(s.b).to(dev)
     drows = torch.from_numpy(rows).to(dev)
     torch.cuda.synchronize()
-    pkg.plss_eg_start(ctx, b, sketch=sk, kmax=cap, rows=drows, seed=1, tol=0.0, maxit=cap)
+    pkg.plss_eg_start(ctx, b, sketch=sk, kmax=cap, rows=drows, seed=1, tol=0.0, maxit=cap, factor=fac)
     pkg.plss_eg_step(ctx, W)
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -723,7 +732,9 @@ def main_eg(args):
     hk_prof = W + K - skipped + (max(1, args.profile_steps) - 1) / 2.0
     cls = {"eg_gemvT_history": (kt["gemvT"], 8 * n * hk_prof + 8 * n),
            "eg_gemv_history": (kt["gemv"], 8 * n * hk_prof + 40 * n),
-           "eg_tri": (kt["tri"], 8 * hk_prof * hk_prof), "k1_spmv_csr_resid": (kt["k1"], 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m)}
+           "eg_tri": (kt["tri"], 8 * hk_prof * hk_prof if fac == "triangular"
+                      else 16 * n * hk_prof + 48 * n + 8 * hk_prof * hk_prof),   # QR: w = y - V b, V^T v, T
+           "k1_spmv_csr_resid": (kt["k1"], 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m)}
     dom = max(cls, key=lambda c: cls[c][0])
     dom_ms, dom_bytes = cls[dom]
     peak, peak_src = _peaks()
@@ -732,12 +743,13 @@ def main_eg(args):
     pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    pkg.plss_eg_solve(ctx, pin_b, sketch=sk, kmax=cap, rows=rows, seed=1, tol=0.0, maxit=W + K, x=pin_x)
+    pkg.plss_eg_solve(ctx, pin_b, sketch=sk, kmax=cap, rows=rows, seed=1, tol=0.0, maxit=W + K, x=pin_x, factor=fac)
     t_e2e = time.perf_counter() - t0
     line = {"metric": EG_METRIC, "value": its, "unit": "it/s", "n_gpus": 1, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": label, "m": m, "n": n, "nnz": nnz, "sketch": sk, "history_mean": hk_mean,
+            "config": {"workload": label, "m": m, "n": n, "nnz": nnz, "sketch": sk, "factor": fac,
+                       "history_mean": hk_mean,
                        "parallelism": "single", "slabs": q["slabs"], "tol": 0.0, "skipped_steps": skipped,
                        "l2": f"stored Y is {8 * n * (W + K) / 1e9:.2f} GB at the end (> L2 after "
                              f"{126e6 / (8 * n):.0f} steps)",

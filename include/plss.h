@@ -259,15 +259,21 @@ plss_status plss_kz_profile(plss_ctx *ctx, int32_t k, double *ms);
  * maxit indices in [0, m) (identity sketch only; may be NULL otherwise). Single-device ctx;
  * shares the ctx's r, y, p, x, control block and history. workspace: dev, 256-byte aligned,
  * >= plss_eg_workspace_bytes(ctx, kmax) = 8 n kmax + 8 kmax^2 bytes + O(m + n).
+ * factor 0: the triangular factorization above; factor 1: the QR variant (section 2.3, eq:pkQR,
+ * L247-282): Y_k = Q_k T_k kept as Householder reflectors in compact WY form Q = I - V T V^T
+ * (V in the Y store, T in the R store), p_k = (s_k^T r_{k-1} / r_kk) q_k with q_k = Q_k e_k;
+ * delta_k = r_kk^2 (four passes over the store per step instead of two).
  * record k of `diag` = {hist_k, rho_k, delta_k, skipped (0/1), s_k^T r_{k-1}, history size}. */
 size_t plss_eg_workspace_bytes(const plss_ctx *ctx, int32_t kmax); /* 0 on invalid input */
-plss_status plss_eg_solve(plss_ctx *ctx, int32_t sketch, int32_t kmax, void *workspace,
-                          size_t ws_bytes, const int32_t *rows, uint64_t seed, const double *b,
-                          const double *x0, double tol, int32_t tol_mode, int32_t maxit, double *x,
-                          int32_t *iters, double *hist, double *diag, plss_outcome *outcome);
-plss_status plss_eg_start(plss_ctx *ctx, int32_t sketch, int32_t kmax, void *workspace,
-                          size_t ws_bytes, const int32_t *rows, uint64_t seed, const double *b,
-                          const double *x0, double tol, int32_t tol_mode, int32_t maxit);
+plss_status plss_eg_solve(plss_ctx *ctx, int32_t sketch, int32_t factor, int32_t kmax,
+                          void *workspace, size_t ws_bytes, const int32_t *rows, uint64_t seed,
+                          const double *b, const double *x0, double tol, int32_t tol_mode,
+                          int32_t maxit, double *x, int32_t *iters, double *hist, double *diag,
+                          plss_outcome *outcome);
+plss_status plss_eg_start(plss_ctx *ctx, int32_t sketch, int32_t factor, int32_t kmax,
+                          void *workspace, size_t ws_bytes, const int32_t *rows, uint64_t seed,
+                          const double *b, const double *x0, double tol, int32_t tol_mode,
+                          int32_t maxit);
 plss_status plss_eg_step(plss_ctx *ctx, int32_t k);
 plss_status plss_eg_finish(plss_ctx *ctx, double *x, int32_t *iters, double *hist, double *diag,
                            plss_outcome *outcome);

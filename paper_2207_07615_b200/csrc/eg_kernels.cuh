@@ -21,6 +21,14 @@
 //               counter
 //   k_eg_gemv   p = coef (y - Y t_hat) (history split in 4, fixed-order combination), x += p,
 //               append y to Y
+//
+// QR variant (section 2.3, eq:ykeqQR / eq:pkQR, L247-282), compact WY: Q_h = H_1 .. H_h = I - V T V^T
+// (Householder H_j = I - tau_j v_j v_j^T, V n x h unit-trapezoidal, T h x h upper triangular):
+//   a = V^T y (k_eg_gemvT / k_eg_red), b = T^T a (k_qr_b), w = Q_h^T y = y - V b (k_qr_w; its last
+//   CTA forms the reflector of w[h:]: alpha = -sign(w_h) ||w[h:]||, v = w[h:] - alpha e_h,
+//   tau = 2 / v^T v, r_hh = alpha), V[:, h] = v (k_qr_v), c = V^T v (gemvT / red),
+//   T[:, h] = [-tau T c; tau] and z = T_{h+1} V_{h+1}^T e_h (k_qr_tri, one pass over T's rows),
+//   q = e_h - V z, p = (s^T r / r_hh) q (k_eg_gemv<QR>)
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -41,11 +49,12 @@ struct EgState {
   int32_t skipped;
   int32_t cur_row;
   double coef;
+  double alpha, tau, vh;   // QR: r_hh, the new reflector's tau and its entry h
 };
 
 struct EgArgs {
   int64_t m, n;
-  int32_t kmax, mode;
+  int32_t kmax, mode, factor;  // factor 0: triangular R D R^T, 1: Householder QR (compact WY)
   const int32_t* row_ptr;
   const int32_t* col_idx;
   const double* val;
@@ -62,6 +71,12 @@ struct EgArgs {
   double* part_tri;           // [2 grid_tri] delta partial pairs (publish_and_elect)
   unsigned* counter;
   int32_t grid_tri;
+  // QR variant: V lives in Y, T in R
+  double* w;                  // [n] Q_h^T y, then v
+  double* cv;                 // [kmax + 2] V^T v
+  double* zv;                 // [kmax + 2] T_{h+1} V_{h+1}^T e_h
+  double* part_w;             // [2 grid_g] sigma partial pairs
+  unsigned* counter2;
   double* part;               // [grid_t][kmax + 1] partials of Y^T y | y^T y
   double* part_rs;            // [grid_s] partials of s^T r (Gaussian)
   double* p;
@@ -106,18 +121,20 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gauss(EgArgs a) {
 
 // partials of g_j = Y[:, j]^T y (j < hk) and y^T y over CTA b's contiguous row range: warp w takes
 // columns w, w + 8, ..., four at a time (independent loads in flight), lanes stride the rows
+template <int SRC>                      // 0: y (Y^T y and y^T y), 1: w = v (QR: V^T v)
 __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   if (eg_done(a)) return;
   const int hk = a.st->hk;
+  const double* vec = SRC == 0 ? a.y : a.w;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = EG_NT / 32;
   const int64_t per = (a.n + gridDim.x - 1) / gridDim.x;
   const int64_t l0 = (int64_t)blockIdx.x * per, l1 = min(a.n, l0 + per);
   double* out = a.part + (size_t)blockIdx.x * (a.kmax + 1);
-  if (warp == 0) {
+  if (SRC == 0 && warp == 0) {
     double yy = 0.0;
     for (int64_t l = l0 + lane; l < l1; l += 32) {
-      const double v = __ldg(a.y + l);
+      const double v = __ldg(vec + l);
       yy = __dadd_rn(yy, __dmul_rn(v, v));
     }
     yy = warp_sum(yy);
@@ -132,7 +149,7 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
     double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
     int64_t l = l0 + lane;
     for (; l + 32 < l1; l += 64) {
-      const double y0 = __ldg(a.y + l), y1 = __ldg(a.y + l + 32);
+      const double y0 = __ldg(vec + l), y1 = __ldg(vec + l + 32);
       double v0[4], v1[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) { v0[q] = __ldg(c[q] + l); v1[q] = __ldg(c[q] + l + 32); }
@@ -143,7 +160,7 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
       }
     }
     if (l < l1) {
-      const double y0 = __ldg(a.y + l);
+      const double y0 = __ldg(vec + l);
 #pragma unroll
       for (int q = 0; q < 4; ++q) sa[q] = __dadd_rn(sa[q], __dmul_rn(__ldg(c[q] + l), y0));
     }
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   for (; j < hk; j += NW) {
     const double* c0 = a.Y + (int64_t)j * a.n;
     double s0 = 0.0;
-    for (int64_t l = l0 + lane; l < l1; l += 32) s0 = __dadd_rn(s0, __dmul_rn(__ldg(c0 + l), __ldg(a.y + l)));
+    for (int64_t l = l0 + lane; l < l1; l += 32) s0 = __dadd_rn(s0, __dmul_rn(__ldg(c0 + l), __ldg(vec + l)));
     s0 = warp_sum(s0);
     if (lane == 0) out[j] = s0;
   }
@@ -164,11 +181,12 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
 
 // gv[e] = sum over the gemvT CTAs of part[.][e] for e < hk, gv[kmax] = y^T y, gv[kmax+1] = s^T r
 // (Gaussian): one warp per entry, lane-strided partial sums in CTA order, fixed butterfly
+template <int DST>                      // 0: gv (+ y^T y, s^T r), 1: cv (QR: V^T v only)
 __global__ void __launch_bounds__(EG_NT) k_eg_red(EgArgs a) {
   if (eg_done(a)) return;
   const int hk = a.st->hk, K = a.kmax, lane = threadIdx.x & 31;
   const int e = blockIdx.x * (EG_NT / 32) + (threadIdx.x >> 5);
-  if (e > hk + 1) return;
+  if (e > hk + 1 || (DST == 1 && e >= hk)) return;
   double s = 0.0;
   if (e <= hk) {
     const int col = e < hk ? e : K;
@@ -177,7 +195,10 @@ __global__ void __launch_bounds__(EG_NT) k_eg_red(EgArgs a) {
     for (int g = lane; g < a.grid_s; g += 32) s = __dadd_rn(s, a.part_rs[g]);
   }
   s = warp_sum(s);
-  if (lane == 0) a.gv[e < hk ? e : (e == hk ? K : K + 1)] = s;
+  if (lane == 0) {
+    if (DST == 1) a.cv[e] = s;
+    else a.gv[e < hk ? e : (e == hk ? K : K + 1)] = s;
+  }
 }
 
 // u_j = (sum_{i<j} R[i][j] g_i - g_j) / delta_j for j < hk: one warp per j
@@ -247,17 +268,21 @@ __global__ void __launch_bounds__(EG_NT) k_eg_trit(EgArgs a) {
   rk[5] = (double)st->hk;
 }
 
-// p = coef (y - Y t_hat): tiles of 64 l, 4 groups each summing a quarter of the history columns
+// p = coef (y - Y t_hat): tiles of 64 l, 4 groups each summing a quarter of the history columns.
+// QR: p = coef (e_h - V z) over the h + 1 columns of V_{h+1} (the new column is already in V).
+template <int QR>
 __global__ void __launch_bounds__(EG_NT) k_eg_gemv(EgArgs a) {
   if (eg_done(a)) return;
   constexpr int TL = 64, JS = EG_NT / TL;
   __shared__ double part[JS][TL];
   const EgState* st = a.st;
-  const int hk = st->hk_use, skip = st->skip;
+  const int hu = st->hk_use, skip = st->skip;
+  const int hk = QR ? hu + 1 : hu;
+  const double* wt = QR ? a.zv : a.th;
   const double coef = st->coef;
   const int tl = threadIdx.x % TL, js = threadIdx.x / TL;
   const int j0 = (int)((int64_t)hk * js / JS), j1 = (int)((int64_t)hk * (js + 1) / JS);
-  double* Ynew = a.Y + (int64_t)hk * a.n;
+  double* Ynew = a.Y + (int64_t)hu * a.n;
   for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < a.n; l0 += (int64_t)gridDim.x * TL) {
     const int64_t l = l0 + tl;
     double t = 0.0;
@@ -269,9 +294,9 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemv(EgArgs a) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) pv[u] = __ldg(col + (int64_t)(j + u) * a.n);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t = __dadd_rn(t, __dmul_rn(pv[u], __ldg(a.th + j + u)));
+        for (int u = 0; u < 8; ++u) t = __dadd_rn(t, __dmul_rn(pv[u], __ldg(wt + j + u)));
       }
-      for (; j < j1; ++j) t = __dadd_rn(t, __dmul_rn(__ldg(col + (int64_t)j * a.n), __ldg(a.th + j)));
+      for (; j < j1; ++j) t = __dadd_rn(t, __dmul_rn(__ldg(col + (int64_t)j * a.n), __ldg(wt + j)));
     }
     part[js][tl] = t;
     __syncthreads();
@@ -279,16 +304,160 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemv(EgArgs a) {
       double tt = part[0][tl];
 #pragma unroll
       for (int q = 1; q < JS; ++q) tt = __dadd_rn(tt, part[q][tl]);
-      const double yl = a.y[l];
+      const double yl = QR ? (l == hu ? 1.0 : 0.0) : a.y[l];
       const double pl = skip ? 0.0 : __dmul_rn(coef, __dadd_rn(yl, -tt));
       a.p[l] = pl;
       if (!skip) {
-        Ynew[l] = yl;
+        if (!QR) Ynew[l] = yl;
         a.x[l] = __dadd_rn(a.x[l], pl);
       }
     }
     __syncthreads();
   }
+}
+
+// ---- QR variant ------------------------------------------------------------------------------
+// b_j = sum_{i <= j} T[i][j] a_i (b = T^T a), one warp per column j of T
+__global__ void __launch_bounds__(EG_NT) k_qr_b(EgArgs a) {
+  if (eg_done(a)) return;
+  const int hk = a.st->hk, K = a.kmax, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (EG_NT / 32) + (threadIdx.x >> 5);
+  if (j >= hk) return;
+  const double* Tc = a.R + (size_t)j * K;
+  double s = 0.0;
+  for (int i = lane; i <= j; i += 32) s = __dadd_rn(s, __dmul_rn(Tc[i], a.gv[i]));
+  s = warp_sum(s);
+  if (lane == 0) a.uv[j] = s;
+}
+
+// w = y - V b (history split), sigma = ||w[h:]||^2; the last CTA forms the reflector
+__global__ void __launch_bounds__(EG_NT) k_qr_w(EgArgs a) {
+  if (eg_done(a)) return;
+  constexpr int TL = 64, JS = EG_NT / TL;
+  __shared__ double part[JS][TL];
+  __shared__ double sm[2][MAXW];
+  EgState* st = a.st;
+  const int hk = st->hk;
+  const int tl = threadIdx.x % TL, js = threadIdx.x / TL;
+  const int j0 = (int)((int64_t)hk * js / JS), j1 = (int)((int64_t)hk * (js + 1) / JS);
+  double sig = 0.0, z = 0.0;
+  for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < a.n; l0 += (int64_t)gridDim.x * TL) {
+    const int64_t l = l0 + tl;
+    double t = 0.0;
+    if (l < a.n) {
+      const double* col = a.Y + l;
+      int j = j0;
+      for (; j + 8 <= j1; j += 8) {
+        double pv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pv[u] = __ldg(col + (int64_t)(j + u) * a.n);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t = __dadd_rn(t, __dmul_rn(pv[u], __ldg(a.uv + j + u)));
+      }
+      for (; j < j1; ++j) t = __dadd_rn(t, __dmul_rn(__ldg(col + (int64_t)j * a.n), __ldg(a.uv + j)));
+    }
+    part[js][tl] = t;
+    __syncthreads();
+    if (js == 0 && l < a.n) {
+      double tt = part[0][tl];
+#pragma unroll
+      for (int q = 1; q < JS; ++q) tt = __dadd_rn(tt, part[q][tl]);
+      const double wl = __dadd_rn(a.y[l], -tt);
+      a.w[l] = wl;
+      if (l >= hk) sig = __dadd_rn(sig, __dmul_rn(wl, wl));
+    }
+    __syncthreads();
+  }
+  if (!publish_and_elect(sig, z, a.part_w, a.part_w, gridDim.x, a.counter2, sm)) return;
+  if (threadIdx.x != 0) return;
+  double rs;
+  if (a.mode == EG_RESIDUAL) rs = a.ctl->rho;
+  else if (a.mode == EG_IDENTITY) rs = __ldcg(a.r + st->cur_row);
+  else rs = a.gv[a.kmax + 1];
+  const double yy = a.gv[a.kmax];
+  const bool skip = yy == 0.0 || hk >= a.n || sig <= EG_SKIP_REL * yy || rs == 0.0;    // reading R22
+  double alpha = 0.0, tau = 0.0, vh = 0.0;
+  if (!skip) {
+    const double wh = __ldcg(a.w + hk);
+    alpha = wh >= 0.0 ? -__dsqrt_rn(sig) : __dsqrt_rn(sig);
+    vh = __dadd_rn(wh, -alpha);
+    const double vv = __dadd_rn(__dadd_rn(sig, -__dmul_rn(wh, wh)), __dmul_rn(vh, vh));
+    tau = __ddiv_rn(2.0, vv);
+  }
+  st->skip = skip ? 1 : 0;
+  st->alpha = alpha;
+  st->tau = tau;
+  st->vh = vh;
+  st->coef = skip ? 0.0 : __ddiv_rn(rs, alpha);           // p = (s^T r / r_hh) q, r_hh = alpha
+  a.rec[(size_t)(a.ctl->iters + 1) * REC + 4] = rs;
+}
+
+// v = [0 (l < h); vh (l = h); w_l (l > h)] into w and, unless skipped, into V[:, h]
+__global__ void __launch_bounds__(EG_NT) k_qr_v(EgArgs a) {
+  if (eg_done(a)) return;
+  const EgState* st = a.st;
+  const int hk = st->hk, skip = st->skip;
+  const double vh = st->vh;
+  double* Vn = a.Y + (int64_t)hk * a.n;
+  for (int64_t l = (int64_t)blockIdx.x * EG_NT + threadIdx.x; l < a.n; l += (int64_t)gridDim.x * EG_NT) {
+    const double v = l < hk ? 0.0 : (l == hk ? vh : a.w[l]);
+    a.w[l] = v;
+    if (!skip) Vn[l] = v;
+  }
+}
+
+// t_i = -tau sum_{i <= j < h} T[i][j] c_j (the new column of T) and
+// z_i = sum_{i <= j < h} T[i][j] g_j + t_i vh with g_j = V[h][j] (row h of V) for the CTA's 32 rows;
+// the last CTA: z_h = tau vh, T[h][h] = tau, history size, iteration counter, record
+__global__ void __launch_bounds__(EG_NT) k_qr_tri(EgArgs a) {
+  if (eg_done(a)) return;
+  __shared__ double sm[2][MAXW];
+  __shared__ double pt[EG_NT / 32][32], pz[EG_NT / 32][32];
+  EgState* st = a.st;
+  const int hk = st->hk, K = a.kmax, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = EG_NT / 32;
+  const int i = blockIdx.x * 32 + lane;
+  const double tau = st->tau, vh = st->vh;
+  double at = 0.0, az = 0.0;
+  if (blockIdx.x * 32 < hk) {
+    for (int j = blockIdx.x * 32 + warp; j < hk; j += NW) {
+      if (j >= i) {
+        const double tij = a.R[(size_t)j * K + i];
+        at = __dadd_rn(at, __dmul_rn(tij, a.cv[j]));
+        az = __dadd_rn(az, __dmul_rn(tij, __ldg(a.Y + (int64_t)j * a.n + hk)));
+      }
+    }
+  }
+  pt[warp][lane] = at;
+  pz[warp][lane] = az;
+  __syncthreads();
+  if (warp == 0 && i < hk) {
+    double t = pt[0][lane], zz = pz[0][lane];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) { t = __dadd_rn(t, pt[w][lane]); zz = __dadd_rn(zz, pz[w][lane]); }
+    const double ti = -__dmul_rn(tau, t);
+    a.R[(size_t)hk * K + i] = ti;                        // new column of T (kept only if not skipped)
+    a.zv[i] = __dadd_rn(zz, __dmul_rn(ti, vh));
+  }
+  double z0 = 0.0, z1 = 0.0;
+  if (!publish_and_elect(z0, z1, a.part_tri, a.part_tri, gridDim.x, a.counter, sm)) return;
+  if (threadIdx.x != 0) return;
+  const int skip = st->skip;
+  a.zv[hk] = __dmul_rn(tau, vh);
+  st->hk_use = hk;
+  if (!skip) {
+    a.R[(size_t)hk * K + hk] = tau;
+    st->hk = (hk + 1 == K) ? 0 : hk + 1;
+  } else {
+    st->skipped += 1;
+  }
+  Ctl* c = a.ctl;
+  const int k = c->iters + 1;
+  c->iters = k;
+  double* rk = a.rec + (size_t)k * REC;
+  rk[2] = __dmul_rn(st->alpha, st->alpha);            // r_hh^2 = delta_k
+  rk[3] = (double)skip;
+  rk[5] = (double)st->hk;
 }
 
 }  // namespace plss

@@ -1724,11 +1724,11 @@ static size_t eg_bytes(const plss_ctx* ctx, int kmax) {
   int gt, gs, gg;
   eg_grids(ctx, &gt, &gs, &gg);
   const size_t m = (size_t)ctx->m, n = (size_t)ctx->n, K = (size_t)kmax;
-  return align_up(8 * n * K) + align_up(8 * K * K) + 4 * align_up(8 * (K + 2)) + align_up(16 * (K / 32 + 1)) + align_up(256) + align_up(8 * (K + 1) * (size_t)gt) +
+  return align_up(8 * n * K) + align_up(8 * K * K) + 6 * align_up(8 * (K + 2)) + align_up(16 * (K / 32 + 1)) + align_up(256) +
+         align_up(8 * n) + align_up(16 * (size_t)gg) + align_up(256) + align_up(8 * (K + 1) * (size_t)gt) +
          align_up(8 * (size_t)gs) + align_up(8 * m) + align_up(sizeof(EgState)) + align_up(4 * (size_t)(ctx->L.maxit_cap + 1));
 }
-static plss_status eg_enqueue_step(plss_ctx* ctx) {
-  cudaStream_t st = ctx->stream;
+static void eg_enqueue_sketch(plss_ctx* ctx, cudaStream_t st) {
   const EgArgs& a = ctx->eg;
   if (a.mode == EG_IDENTITY) {
     k_eg_row<<<1, EG_NT, 0, st>>>(a);
@@ -1736,11 +1736,35 @@ static plss_status eg_enqueue_step(plss_ctx* ctx) {
     if (a.mode == EG_GAUSSIAN) k_eg_gauss<<<a.grid_s, EG_NT, 0, st>>>(a);
     for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->eg_seg[s], ctx->g2[s], st);   // y = A^T s
   }
-  k_eg_gemvT<<<a.grid_t, EG_NT, 0, st>>>(a);
-  k_eg_red<<<(a.kmax + 2 + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
-  k_eg_triu<<<(a.kmax + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
-  k_eg_trit<<<a.grid_tri, EG_NT, 0, st>>>(a);
-  k_eg_gemv<<<a.grid_g, EG_NT, 0, st>>>(a);
+}
+// the factorization part of a step (between the sketch and K1); `ev` (optional) receives events
+// after the Y^T y reduction and after the triangular / reflector work (plss_eg_profile)
+static void eg_enqueue_factor(plss_ctx* ctx, cudaStream_t st, cudaEvent_t ev_a, cudaEvent_t ev_b) {
+  const EgArgs& a = ctx->eg;
+  const int gred = (a.kmax + 2 + EG_NT / 32 - 1) / (EG_NT / 32);
+  k_eg_gemvT<0><<<a.grid_t, EG_NT, 0, st>>>(a);
+  k_eg_red<0><<<gred, EG_NT, 0, st>>>(a);
+  if (ev_a) cudaEventRecord(ev_a, st);
+  if (a.factor == 0) {
+    k_eg_triu<<<gred, EG_NT, 0, st>>>(a);
+    k_eg_trit<<<a.grid_tri, EG_NT, 0, st>>>(a);
+    if (ev_b) cudaEventRecord(ev_b, st);
+    k_eg_gemv<0><<<a.grid_g, EG_NT, 0, st>>>(a);
+  } else {
+    k_qr_b<<<gred, EG_NT, 0, st>>>(a);
+    k_qr_w<<<a.grid_g, EG_NT, 0, st>>>(a);
+    k_qr_v<<<a.grid_s, EG_NT, 0, st>>>(a);
+    k_eg_gemvT<1><<<a.grid_t, EG_NT, 0, st>>>(a);
+    k_eg_red<1><<<gred, EG_NT, 0, st>>>(a);
+    k_qr_tri<<<a.grid_tri, EG_NT, 0, st>>>(a);
+    if (ev_b) cudaEventRecord(ev_b, st);
+    k_eg_gemv<1><<<a.grid_g, EG_NT, 0, st>>>(a);
+  }
+}
+static plss_status eg_enqueue_step(plss_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  eg_enqueue_sketch(ctx, st);
+  eg_enqueue_factor(ctx, st, nullptr, nullptr);
   for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);     // r -= A p, rho, stop
   CK(cudaGetLastError());
   return PLSS_OK;
@@ -1753,11 +1777,12 @@ size_t plss_eg_workspace_bytes(const plss_ctx* ctx, int32_t kmax) {
   return eg_bytes(ctx, kmax);
 }
 
-plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* workspace, size_t ws_bytes,
-                          const int32_t* rows, uint64_t seed, const double* b, const double* x0, double tol,
-                          int32_t tol_mode, int32_t maxit) {
+plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t factor, int32_t kmax, void* workspace,
+                          size_t ws_bytes, const int32_t* rows, uint64_t seed, const double* b, const double* x0,
+                          double tol, int32_t tol_mode, int32_t maxit) {
   if (!ctx) return PLSS_E_INVALID;
-  if (ctx->dist || kmax < 1 || sketch < EG_RESIDUAL || sketch > EG_GAUSSIAN || !(tol >= 0.0) || maxit < 1 ||
+  if (ctx->dist || kmax < 1 || sketch < EG_RESIDUAL || sketch > EG_GAUSSIAN || (factor != 0 && factor != 1) ||
+      !(tol >= 0.0) || maxit < 1 ||
       maxit > ctx->L.maxit_cap || (tol_mode != 0 && tol_mode != 1) || (sketch == EG_IDENTITY && !rows)) {
     set_err(ctx, ctx->dist ? "the growing-sketch engine runs on a single-device ctx"
                            : "invalid sketch / kmax / tol / tol_mode / maxit, or rows is NULL for identity sketches");
@@ -1782,6 +1807,7 @@ plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* wor
   a.n = ctx->n;
   a.kmax = kmax;
   a.mode = sketch;
+  a.factor = factor;
   a.row_ptr = ctx->A.row_ptr;
   a.col_idx = ctx->A.col_idx;
   a.val = ctx->A.val;
@@ -1800,6 +1826,11 @@ plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* wor
   a.grid_tri = (int)(K / 32 + 1);
   a.part_tri = (double*)take(16 * (K / 32 + 1));
   a.counter = (unsigned*)take(256);
+  a.cv = (double*)take(8 * (K + 2));
+  a.zv = (double*)take(8 * (K + 2));
+  a.w = (double*)take(8 * n);
+  a.part_w = (double*)take(16 * (size_t)a.grid_g);
+  a.counter2 = (unsigned*)take(256);
   a.part = (double*)take(8 * (K + 1) * (size_t)a.grid_t);
   a.part_rs = (double*)take(8 * (size_t)a.grid_s);
   a.s = (double*)take(8 * m);
@@ -1818,6 +1849,7 @@ plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* wor
   s0.prev_row = -1;
   CK(cudaMemcpyAsync(a.st, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(a.counter, 0, 256, st));
+  CK(cudaMemsetAsync(a.counter2, 0, 256, st));
   if (!hrows.empty()) CK(cudaMemcpyAsync(drows, hrows.data(), 4 * (size_t)maxit, cudaMemcpyHostToDevice, st));
   if (n > 0) CK(cudaMemsetAsync(ctx->y, 0, 8 * n, st));
   CK(cudaStreamSynchronize(st));   // host temporaries
@@ -1855,11 +1887,11 @@ plss_status plss_eg_finish(plss_ctx* ctx, double* x, int32_t* iters, double* his
   return alt_finish(ctx, x, iters, hist, diag, outcome);
 }
 
-plss_status plss_eg_solve(plss_ctx* ctx, int32_t sketch, int32_t kmax, void* workspace, size_t ws_bytes,
-                          const int32_t* rows, uint64_t seed, const double* b, const double* x0, double tol,
-                          int32_t tol_mode, int32_t maxit, double* x, int32_t* iters, double* hist, double* diag,
-                          plss_outcome* outcome) {
-  plss_status s = plss_eg_start(ctx, sketch, kmax, workspace, ws_bytes, rows, seed, b, x0, tol, tol_mode, maxit);
+plss_status plss_eg_solve(plss_ctx* ctx, int32_t sketch, int32_t factor, int32_t kmax, void* workspace,
+                          size_t ws_bytes, const int32_t* rows, uint64_t seed, const double* b, const double* x0,
+                          double tol, int32_t tol_mode, int32_t maxit, double* x, int32_t* iters, double* hist,
+                          double* diag, plss_outcome* outcome) {
+  plss_status s = plss_eg_start(ctx, sketch, factor, kmax, workspace, ws_bytes, rows, seed, b, x0, tol, tol_mode, maxit);
   if (s != PLSS_OK) return s;
   if ((s = alt_run(ctx, ctx->eg_graph_chunk, ctx->eg_graph_one, maxit)) != PLSS_OK) return s;
   return plss_eg_finish(ctx, x, iters, hist, diag, outcome);
@@ -1869,27 +1901,15 @@ plss_status plss_eg_profile(plss_ctx* ctx, int32_t k, double* ms) {
   if (!ctx || !ms || k < 1) return PLSS_E_INVALID;
   if (!ctx->eg_started) { set_err(ctx, "plss_eg_profile before plss_eg_start"); return PLSS_E_STATE; }
   cudaStream_t st = ctx->stream;
-  const EgArgs& a = ctx->eg;
   constexpr int NK = 5;
   cudaEvent_t ev[NK + 1];
   for (auto& e : ev) CK(cudaEventCreate(&e));
   double acc[NK] = {0, 0, 0, 0, 0};
   for (int it = 0; it < k; ++it) {
     CK(cudaEventRecord(ev[0], st));
-    if (a.mode == EG_IDENTITY) {
-      k_eg_row<<<1, EG_NT, 0, st>>>(a);
-    } else {
-      if (a.mode == EG_GAUSSIAN) k_eg_gauss<<<a.grid_s, EG_NT, 0, st>>>(a);
-      for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->eg_seg[s], ctx->g2[s], st);
-    }
+    eg_enqueue_sketch(ctx, st);
     CK(cudaEventRecord(ev[1], st));
-    k_eg_gemvT<<<a.grid_t, EG_NT, 0, st>>>(a);
-    k_eg_red<<<(a.kmax + 2 + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
-    CK(cudaEventRecord(ev[2], st));
-    k_eg_triu<<<(a.kmax + EG_NT / 32 - 1) / (EG_NT / 32), EG_NT, 0, st>>>(a);
-    k_eg_trit<<<a.grid_tri, EG_NT, 0, st>>>(a);
-    CK(cudaEventRecord(ev[3], st));
-    k_eg_gemv<<<a.grid_g, EG_NT, 0, st>>>(a);
+    eg_enqueue_factor(ctx, st, ev[2], ev[3]);
     CK(cudaEventRecord(ev[4], st));
     for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
     CK(cudaEventRecord(ev[5], st));

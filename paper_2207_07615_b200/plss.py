@@ -131,14 +131,14 @@ def load_library(path: str = None):
     lib.plss_kz_profile.restype = st
     lib.plss_eg_workspace_bytes.argtypes = [P, I32]
     lib.plss_eg_workspace_bytes.restype = ctypes.c_size_t
-    lib.plss_eg_start.argtypes = [P, I32, I32, P, ctypes.c_size_t, P, U64, P, P, D, I32, I32]
+    lib.plss_eg_start.argtypes = [P, I32, I32, I32, P, ctypes.c_size_t, P, U64, P, P, D, I32, I32]
     lib.plss_eg_start.restype = st
     lib.plss_eg_step.argtypes = [P, I32]
     lib.plss_eg_step.restype = st
     lib.plss_eg_finish.argtypes = [P, P, ctypes.POINTER(I32), P, P, ctypes.POINTER(ctypes.c_int)]
     lib.plss_eg_finish.restype = st
-    lib.plss_eg_solve.argtypes = [P, I32, I32, P, ctypes.c_size_t, P, U64, P, P, D, I32, I32, P, ctypes.POINTER(I32),
-                                  P, P, ctypes.POINTER(ctypes.c_int)]
+    lib.plss_eg_solve.argtypes = [P, I32, I32, I32, P, ctypes.c_size_t, P, U64, P, P, D, I32, I32, P,
+                                  ctypes.POINTER(I32), P, P, ctypes.POINTER(ctypes.c_int)]
     lib.plss_eg_solve.restype = st
     lib.plss_eg_profile.argtypes = [P, I32, P]
     lib.plss_eg_profile.restype = st
@@ -562,6 +562,7 @@ def plss_kz_profile(ctx: Ctx, k: int) -> dict:
 
 
 EG_SKETCH = {"residual": 0, "identity": 1, "gaussian": 2}
+EG_FACTOR = {"triangular": 0, "qr": 1}
 
 
 def _eg_workspace(ctx: Ctx, kmax: int):
@@ -576,15 +577,16 @@ def _eg_workspace(ctx: Ctx, kmax: int):
 
 
 def plss_eg_start(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, x0=None, tol=1e-8, tol_mode=0,
-                  maxit=100):
-    """Growing-sketch engine (Thm 2.1 / Cor 2.2) with residual / identity / gaussian sketch columns."""
+                  maxit=100, factor="triangular"):
+    """Growing-sketch engine (Thm 2.1 / Cor 2.2, or the QR variant of section 2.3: factor="qr") with
+    residual / identity / gaussian sketch columns."""
     lib = load_library()
     kmax = int(maxit if kmax is None else kmax)
     wp, nb = _eg_workspace(ctx, kmax)
     rr = _rows_arg(rows) if rows is not None else None
     ctx._keep = (b, x0, rr)
     ctx._maxit = int(maxit)
-    _check(lib.plss_eg_start(ctx.handle, EG_SKETCH[sketch], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
+    _check(lib.plss_eg_start(ctx.handle, EG_SKETCH[sketch], EG_FACTOR[factor], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
                              _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit)), ctx.handle)
 
 
@@ -607,7 +609,7 @@ def plss_eg_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
 
 
 def plss_eg_solve(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, x0=None, tol=1e-8, tol_mode=0,
-                  maxit=100, x=None, want_hist=True, want_diag=False):
+                  maxit=100, x=None, want_hist=True, want_diag=False, factor="triangular"):
     """Full engine solve. Returns dict(x, iters, outcome, hist[0..iters][, diag])."""
     import torch
     lib = load_library()
@@ -621,7 +623,7 @@ def plss_eg_solve(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, 
     hist = np.zeros(maxit + 1) if want_hist else None
     diag = np.zeros((maxit + 1, REC)) if want_diag else None
     ctx._maxit = int(maxit)
-    _check(lib.plss_eg_solve(ctx.handle, EG_SKETCH[sketch], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
+    _check(lib.plss_eg_solve(ctx.handle, EG_SKETCH[sketch], EG_FACTOR[factor], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
                              _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), _ptr(x), ctypes.byref(it),
                              _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
@@ -633,7 +635,7 @@ def plss_eg_solve(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, 
 def plss_eg_profile(ctx: Ctx, k: int) -> dict:
     ms = np.zeros(5)
     _check(load_library().plss_eg_profile(ctx.handle, int(k), _ptr(ms)), ctx.handle)
-    return dict(zip(["sketch", "gemvT", "tri", "gemv", "k1"], ms.tolist()))
+    return dict(zip(["sketch", "gemvT", "tri", "gemv", "k1"], ms.tolist()))   # QR: "tri" = reflector + T
 
 
 def plss_destroy(ctx: Ctx):

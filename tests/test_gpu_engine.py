@@ -1,5 +1,6 @@
 """GPU parity of the growing-sketch engine (include/plss.h plss_eg_*) against
-the oracle (oracle/engine.py, Thm 2.1 / Cor 2.2) for residual, identity and Gaussian sketch columns:
+the oracle (oracle/engine.py: Thm 2.1 / Cor 2.2, and the QR variant of section 2.3 against a LAPACK
+Householder QR of Y_k each step) for residual, identity and Gaussian sketch columns:
 residual history within 1e-9 over the first 50 steps, final x within 1e-7, equal step counts,
 outcomes and skips; the residual sketch also reproduces the PLSS oracle (Thm 4.1) and the identity
 sketch the PLSS Kaczmarz GPU path.
@@ -57,17 +58,27 @@ CASES = {
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("sketch", ["residual", "identity", "gaussian"])
 @pytest.mark.parametrize("slabs", [1, 3])
-def test_engine_parity(pkg, case, sketch, slabs):
+@pytest.mark.parametrize("factor", ["triangular", "qr"])
+def test_engine_parity(pkg, case, sketch, slabs, factor):
     make, steps, kmax = CASES[case]
     s = make()
     rows = np.resize(np.random.default_rng(7).permutation(s.m), steps)
-    ref = engine.tri_engine(s.scipy_csr(), s.b, sketch=sketch, maxit=steps, tol=1e-12, rows=rows, seed=5,
-                            kmax=kmax)
+    run = engine.tri_engine if factor == "triangular" else engine.qr_engine
+    ref = run(s.scipy_csr(), s.b, sketch=sketch, maxit=steps, tol=1e-12, rows=rows, seed=5, kmax=kmax)
     ctx = _ctx(pkg, s, slabs=slabs)
     res = pkg.plss_eg_solve(ctx, torch.from_numpy(s.b).cuda(), sketch=sketch, kmax=kmax, rows=rows, seed=5,
-                            maxit=steps, tol=1e-12, want_diag=True)
+                            maxit=steps, tol=1e-12, want_diag=True, factor=factor)
     pkg.plss_destroy(ctx)
     _compare(res, ref)
+
+
+def test_qr_and_triangular_agree_on_gpu(pkg):
+    s = plss_gen.make_config("C2s")
+    ctx = _ctx(pkg, s)
+    a = pkg.plss_eg_solve(ctx, s.b, sketch="gaussian", seed=9, maxit=80, tol=0.0, factor="triangular")
+    q = pkg.plss_eg_solve(ctx, s.b, sketch="gaussian", seed=9, maxit=80, tol=0.0, factor="qr")
+    pkg.plss_destroy(ctx)
+    np.testing.assert_allclose(q["hist"], a["hist"], rtol=1e-9)
 
 
 def test_residual_sketch_matches_plss_oracle(pkg):
