@@ -94,6 +94,7 @@ CASES = {
     "C1_r10": (lambda: plss_gen.make_config("C1"), dict(r=10, maxit=60)),
     "small_r5_sparse": (lambda: _small(2), dict(r=5, maxit=80, density=0.2)),
     "C2s_r10": (lambda: plss_gen.make_config("C2s"), dict(r=10, maxit=25)),
+    "C2s_r5_sparse": (lambda: plss_gen.make_config("C2s"), dict(r=5, maxit=25, density=0.02)),
     "C4xs_r5": (lambda: plss_gen.make_config("C4xs"), dict(r=5, maxit=25)),
     "C3_32_r40": (lambda: plss_gen.make_config("C3", N=32), dict(r=40, maxit=30)),
 }
