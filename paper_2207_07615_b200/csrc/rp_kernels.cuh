@@ -183,6 +183,24 @@ __global__ void __launch_bounds__(RP_NT) k_rp_gen(RpArgs a) {
   }
 }
 
+#ifndef PLSS_RP_PF
+#define PLSS_RP_PF 64             // L2 prefetch-size qualifier on the S row gathers: with .L2::64B a
+                                  // random row miss costs ~90 B of DRAM instead of ~160 B (uniform-
+                                  // only probe: 79 vs 125 GB per A^T S), DESIGN.md section 13
+#endif
+__device__ __forceinline__ float rp_ld_s(const float* p) {
+#if PLSS_RP_PF == 64
+  float v;
+  asm volatile("ld.global.nc.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#elif PLSS_RP_PF == 128
+  float v;
+  asm volatile("ld.global.nc.L2::128B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
 __device__ __forceinline__ int ld_stream_i32(const int32_t* p, uint64_t pol) {
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(RP_NT) k_rp_spmm(RpArgs a) {
 #pragma unroll
           for (int w = 0; w < CPL; ++w) {
             const int c = g + w * G;
-            sv[u][w] = (u0 + u < cnt && c < r) ? __ldg(a.S + (int64_t)iu * ld + c) : 0.0f;
+            sv[u][w] = (u0 + u < cnt && c < r) ? rp_ld_s(a.S + (int64_t)iu * ld + c) : 0.0f;
           }
         }
 #pragma unroll
