@@ -11,8 +11,9 @@
 //   k_eg_row    identity sketch: one CTA swaps row i into the dense y (y_k = a_i), s^T r = r[i]
 //   k_eg_gauss  Gaussian sketch: s_i = binary32 normal (randomized projection's generator, r = 1),
 //               partials of s^T r; y = A^T s follows by the K2 segments
-//   k_eg_gemvT  partials of Y^T y and y^T y over CTA b's row range: a warp per column j, lanes over
-//               the rows (coalesced 256-byte reads of Y, y from L1), fixed butterfly per column
+//   k_eg_gemvT  partials of Y^T y and y^T y: 2D grid (2048-row ranges x 32-column groups), a warp
+//               per column, lanes over the rows (coalesced 256-byte reads of Y, y from L1), fixed
+//               butterfly per column
 //   k_eg_red    fixed-order sums of the partials (a warp per entry, many CTAs): g, y^T y, s^T r
 //   k_eg_triu   u = D R^T g: a warp per column of R (coalesced), many CTAs
 //   k_eg_trit   t_hat = R u: CTAs of 32 rows, 8 warps striding the columns (coalesced 256-byte
@@ -36,7 +37,8 @@
 namespace plss {
 
 constexpr int EG_NT = 256;
-constexpr int EG_TILE = 2048;            // y rows per shared-memory tile (gemvT)
+constexpr int EG_RT = 2048;              // rows per CTA of the Y^T y kernel (grid.x = row ranges)
+constexpr int EG_CT = 32;                // columns per CTA of the Y^T y kernel (grid.y = column groups)
 constexpr double EG_SKIP_REL = 1e-14;
 
 enum { EG_RESIDUAL = 0, EG_IDENTITY = 1, EG_GAUSSIAN = 2 };
@@ -119,8 +121,9 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gauss(EgArgs a) {
   if (threadIdx.x == 0) a.part_rs[blockIdx.x] = acc;
 }
 
-// partials of g_j = Y[:, j]^T y (j < hk) and y^T y over CTA b's contiguous row range: warp w takes
-// columns w, w + 8, ..., four at a time (independent loads in flight), lanes stride the rows
+// partials of g_j = Y[:, j]^T y (j < hk) and y^T y: CTA (x, y) covers rows [x RT, (x+1) RT) and
+// columns [y CT, (y+1) CT); warp w takes columns w, w + 8, w + 16, w + 24 at once (8 independent
+// loads per lane step), lanes stride the rows (64 per lane per column, amortizing the butterfly)
 template <int SRC>                      // 0: y (Y^T y and y^T y), 1: w = v (QR: V^T v)
 __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   if (eg_done(a)) return;
@@ -128,10 +131,10 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   const double* vec = SRC == 0 ? a.y : a.w;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = EG_NT / 32;
-  const int64_t per = (a.n + gridDim.x - 1) / gridDim.x;
-  const int64_t l0 = (int64_t)blockIdx.x * per, l1 = min(a.n, l0 + per);
+  const int64_t l0 = (int64_t)blockIdx.x * EG_RT, l1 = min(a.n, l0 + EG_RT);
   double* out = a.part + (size_t)blockIdx.x * (a.kmax + 1);
-  if (SRC == 0 && warp == 0) {
+  const int jc0 = blockIdx.y * EG_CT;
+  if (SRC == 0 && warp == 0 && blockIdx.y == 0) {
     double yy = 0.0;
     for (int64_t l = l0 + lane; l < l1; l += 32) {
       const double v = __ldg(vec + l);
@@ -141,8 +144,9 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
     if (lane == 0) out[a.kmax] = yy;
   }
   // columns j, j + NW, j + 2 NW, j + 3 NW at once, rows two per lane step: 8 independent loads
-  int j = warp;
-  for (; j + 3 * NW < hk; j += 4 * NW) {
+  const int jend = min(hk, jc0 + EG_CT);
+  int j = jc0 + warp;
+  for (; j + 3 * NW < jend; j += 4 * NW) {
     const double* c[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) c[q] = a.Y + (int64_t)(j + q * NW) * a.n;
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
       if (lane == 0) out[j + q * NW] = v;
     }
   }
-  for (; j < hk; j += NW) {
+  for (; j < jend; j += NW) {
     const double* c0 = a.Y + (int64_t)j * a.n;
     double s0 = 0.0;
     for (int64_t l = l0 + lane; l < l1; l += 32) s0 = __dadd_rn(s0, __dmul_rn(__ldg(c0 + l), __ldg(vec + l)));
