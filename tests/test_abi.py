@@ -67,3 +67,24 @@ def test_product_does_not_import_oracle():
 def test_build_targets_sm100a():
     cmd = pbuild.command("/tmp/x.so")
     assert "arch=compute_100a,code=sm_100a" in cmd
+
+
+def test_c_example_compiles_and_links():
+    """include/plss.h is plain C99: examples/solve.c (the ABI without Python) compiles with gcc
+    -Wall -Werror and links against libplss.so (running it needs a GPU: test_gpu_c_example)."""
+    import shutil
+    import subprocess
+    import tempfile
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    from paper_2207_07615_b200 import build as pbuild
+    pbuild.build()
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "solve")
+        cmd = [gcc, "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+               "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "solve.c"), "-o", exe,
+               "-L", os.path.join(ROOT, "paper_2207_07615_b200"), "-lplss", "-L", "/usr/local/cuda/lib64",
+               "-lcudart", "-Wl,-rpath," + os.path.join(ROOT, "paper_2207_07615_b200")]
+        subprocess.run(cmd, check=True, capture_output=True, text=True)
+        assert os.path.exists(exe)
