@@ -102,7 +102,9 @@ plss_status plss_create(const plss_matrix *A, const plss_options *opt, void *wor
 
 /* Distributed row-block ctx: this rank owns rows [row_offset, row_offset + A->m)
  * of a global m_global x n matrix; x, p, y are replicated. Each iteration does local A p and
- * A^T r and ONE ncclAllReduce(sum, fp64) of n+1 values (partial y and the local rho).
+ * A^T r and an ncclAllReduce(sum, fp64) of n+1 values (partial y and the local rho). When the last
+ * K2 segment is SELL-32 with a sigma perm, A^T r runs as column chunks (PLSS_DIST_CHUNKS, default 4)
+ * and each chunk is all-reduced on a second stream while the next one computes.
  * id: 128 bytes from plss_get_unique_id on rank 0, broadcast by the caller (e.g. through
  * torch.distributed). Collective: every rank must call it. Errors: as plss_create + E_NCCL. */
 plss_status plss_get_unique_id(uint8_t id[128]);

@@ -29,6 +29,7 @@ using namespace plss;
 namespace {
 
 constexpr int MAXG = 2048;           // upper bound on persistent-CTA grid sizes (partials)
+constexpr int DCH_MAX = 8;           // column chunks of the last K2 segment on a distributed ctx
 constexpr int SCAN_ITEMS = 16;       // setup scan: items per thread
 constexpr size_t ALIGN = 256;
 
@@ -111,7 +112,7 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
     L->window = !(o.flags & 2);
     L->s1win = take(8 * (size_t)(L->s1sp / 4 + 2 * S + 2));     // window blocks: nsb >= 4 slices
     L->s2win = take(8 * (size_t)(L->s2sp / 4 + 2 * S + 2));
-    L->cblk = take(4 * (size_t)(MAXG + 1) * 2 * S);
+    L->cblk = take(4 * (size_t)(MAXG + 1) * (2 * S + DCH_MAX));
     // units of one segment: slices + long rows (<= nnz / (LONGROW + 1) of them)
     L->slpart = take(16 * (size_t)(std::max(m, n) / 32 + nnz / (LONGROW + 1) + 4));
     L->s1auxn = 2 * (m / 32 + nnz / (LONGROW + 1) + 4 * S + 8);
@@ -208,6 +209,13 @@ struct plss_ctx {
   cudaGraphExec_t graph_chunk = nullptr, graph_one = nullptr;
   // distributed (created by plss_create_dist, any nranks >= 1)
   bool dist = false;
+  // the last K2 segment split into column chunks, each all-reduced on comm_stream while the next
+  // chunk computes (drows: first row of each chunk and n + 1 at the end)
+  std::vector<SpmvSeg> dch;
+  std::vector<int> gch;
+  std::vector<int64_t> drows;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ch[DCH_MAX] = {}, ev_join = nullptr;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // solve state
@@ -296,15 +304,28 @@ static int grid_for(int64_t work_units, int occ_per_sm, int sms) {
 // enqueue one loop step (also used inside graph capture)
 static plss_status enqueue_step(plss_ctx* ctx) {
   cudaStream_t st = ctx->stream;
+  const bool chunked = ctx->dist && !ctx->dch.empty();
   for (int s = 0; s < ctx->S; ++s) {
     launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
-    if (ctx->seg2[s].finalize)
+    if (chunked && s == ctx->S - 1) {
+      // last slab: column chunks, each all-reduced on comm_stream while the next one computes
+      for (size_t c = 0; c < ctx->dch.size(); ++c) {
+        launch_spmv<ROLE_K2>(ctx->dch[c], ctx->gch[c], st);
+        CK(cudaEventRecord(ctx->ev_ch[c], st));
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ch[c], 0));
+        NK(ncclAllReduce(ctx->y + ctx->drows[c], ctx->y + ctx->drows[c], (size_t)(ctx->drows[c + 1] - ctx->drows[c]),
+                         ncclFloat64, ncclSum, ctx->comm, ctx->comm_stream));
+      }
+      CK(cudaEventRecord(ctx->ev_join, ctx->comm_stream));
+      CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    } else if (ctx->seg2[s].finalize) {
       launch_spmv<ROLE_K2DOTS>(ctx->seg2[s], ctx->g2[s], st);
-    else
+    } else {
       launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
+    }
   }
   if (ctx->dist) {
-    NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
+    if (!chunked) NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
     k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
                                            ctx->part2, ctx->counters + 1, ctx->wi);
   }
@@ -417,6 +438,42 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   a.slpart = (double*)(ctx->ws + ctx->L.slpart);
   a.fmt = 3;
   *grid_out = grid;
+  return PLSS_OK;
+}
+
+// Split a fmt 3 K2 segment with a sigma perm into `nch` column chunks at sigma-window boundaries:
+// slices [sl0, sl1) of window-aligned ranges keep their absolute rows (perm) and y-staging windows
+// (wrow0), and get their own entry-balanced CTA ranges. Used by the distributed step to all-reduce
+// a finished chunk of y while the next one computes.
+static plss_status make_chunks(plss_ctx* ctx, const SpmvSeg& a, SellPool& pool, int sms, int nch) {
+  ctx->dch.clear();
+  ctx->gch.clear();
+  ctx->drows.clear();
+  if (a.fmt != 3 || !a.perm || a.gsort || nch < 2) return PLSS_OK;
+  const int nwin = (a.nslices + SPW - 1) / SPW;
+  nch = std::min(nch, std::min(nwin, DCH_MAX));
+  if (nch < 2) return PLSS_OK;
+  for (int c = 0; c < nch; ++c) {
+    const int w0 = (int)((int64_t)nwin * c / nch), w1 = (int)((int64_t)nwin * (c + 1) / nch);
+    SpmvSeg b = a;
+    const int sl0 = w0 * SPW, sl1 = std::min(w1 * SPW, a.nslices);
+    b.sptr = a.sptr + sl0;
+    b.perm = a.perm + (size_t)sl0 * 32;
+    b.nslices = sl1 - sl0;
+    b.wrow0 = w0 * SIGMA;
+    b.fmt = 1;                                       // make_contig turns it into fmt 3 with its ranges
+    b.uw = nullptr;
+    int grid = 1;
+    plss_status st = make_contig(ctx, b, pool, sms, &grid);
+    if (st != PLSS_OK) return st;
+    ctx->dch.push_back(b);
+    ctx->gch.push_back(grid);
+    ctx->drows.push_back((int64_t)w0 * SIGMA);
+  }
+  ctx->drows.push_back(ctx->n + 1);                  // the last chunk's all-reduce carries rho too
+  CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  for (int c = 0; c < nch; ++c) CK(cudaEventCreateWithFlags(&ctx->ev_ch[c], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   return PLSS_OK;
 }
 
@@ -863,6 +920,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     }
   }
   CK(cudaGetLastError());
+  if (dist && L.sell) {
+    const plss_status st2 = make_chunks(ctx, ctx->seg2[S - 1], pool2, sms, env_int("PLSS_DIST_CHUNKS", 4));
+    if (st2 != PLSS_OK) return st2;
+  }
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gdots = grid_for((n + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gnorm = grid_for((m + NT - 1) / NT + 1, occ_vec, sms);
@@ -1157,7 +1218,10 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
     for (auto& a : ctx->seg2) c += a.fmt == 2;
     *window_segments = c;
   }
-  if (launches_per_step) *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0);
+  // our kernels per loop step: K1 and K2 per slab (the last K2 as column chunks on a chunked
+  // distributed ctx), K3, and the distributed dots / tail kernel
+  if (launches_per_step)
+    *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0) + (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1);
   if (slabs) *slabs = ctx->S;
   if (tile_nnz) *tile_nnz = TILE;
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];
@@ -1943,6 +2007,9 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->eg_graph_chunk) cudaGraphExecDestroy(ctx->eg_graph_chunk);
   if (ctx->eg_graph_one) cudaGraphExecDestroy(ctx->eg_graph_one);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (auto& e : ctx->ev_ch) if (e) cudaEventDestroy(e);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->h_done) cudaFreeHost(ctx->h_done);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);

@@ -105,6 +105,8 @@ struct SpmvSeg {
   // ring of `ring` doubles in shared memory, every other entry from global memory
   int32_t win, ring, nblocks, glen, nsb;
   int32_t row0;              // first row of this segment in the matrix (ablation experiments only)
+  int32_t wrow0;             // first row of the segment's sigma window 0 (0; a column chunk of a K2
+                             // segment, see plss.cu make_chunks, starts at a later window)
   // Globally length-sorted SELL (power-law rows, fmt 3 only): perm is a global row order, rows
   // longer than LONGROW are not in the slices but are warp units nslices .. nslices+nlong-1
   // (row lrows[u - nslices], entries [lptr[row], lptr[row+1]) of the segment's CSR-like arrays).
@@ -888,7 +890,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       last = __shfl_sync(FULL, last, 0);
       if (last) {                                               // window complete: write it out
         __threadfence_block();                                  // the other warps' s_y stores are visible
-        const int r0 = w * SIGMA;
+        const int r0 = a.wrow0 + w * SIGMA;
 #pragma unroll
         for (int u = 0; u < SIGMA / 32; ++u) {
           const int r = r0 + u * 32 + lane;

@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 import plss_gen  # noqa: E402
 
 
-def gloo_solve(s, blk, dist, torch, maxit):
+def gloo_solve(s, blk, dist, torch, maxit, chunks=1):
     import oracle
     n = s.n
     r = blk["b"].copy()
@@ -37,7 +37,14 @@ def gloo_solve(s, blk, dist, torch, maxit):
             r = r - oracle.spmv(blk["m"], blk["row_ptr"], blk["col_idx"], blk["val"], p)
         buf[:n] = torch.from_numpy(oracle.spmvT(n, blk["col_ptr"], blk["row_idx"], blk["val_t"], r))
         buf[n] = float(r @ r)
-        dist.all_reduce(buf)                           # the one collective per iteration
+        if chunks <= 1:
+            dist.all_reduce(buf)                       # the one collective per iteration
+        else:                                          # the chunked variant (plss.cu make_chunks):
+            bounds = [(c * (n + 1)) // chunks for c in range(chunks + 1)]   # contiguous slices of the
+            for c0, c1 in zip(bounds[:-1], bounds[1:]):                    # buffer, the last one with rho
+                part = buf[c0:c1].clone()
+                dist.all_reduce(part)
+                buf[c0:c1] = part
         y = buf[:n].numpy()
         rho = float(buf[n])
         h = np.sqrt(rho) / nbd
@@ -65,6 +72,7 @@ def main():
     ap.add_argument("--backend", default="gloo")
     ap.add_argument("--out", required=True)
     ap.add_argument("--config", default="C2s")
+    ap.add_argument("--chunks", type=int, default=1)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -81,7 +89,7 @@ def main():
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         assert isinstance(obj[0], bytes) and len(obj[0]) == 128
-        hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit)
+        hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit, args.chunks)
     else:
         import paper_2207_07615_b200 as pkg
         torch.cuda.set_device(local)

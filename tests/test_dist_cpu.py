@@ -18,12 +18,12 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _run(world, cfg, tmp_path):
-    out = tmp_path / f"res_{world}.npz"
+def _run(world, cfg, tmp_path, chunks=1):
+    out = tmp_path / f"res_{world}_{chunks}.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--backend", "gloo", "--out", str(out),
-           "--config", cfg]
+           "--config", cfg, "--chunks", str(chunks)]
     env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1")
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env, capture_output=True)
     return np.load(out)
@@ -37,6 +37,16 @@ def test_row_blocks_world2_match_oracle(tmp_path):
     k = min(50, len(ref["hist"]))
     assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
     assert np.linalg.norm(r["x"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
+
+
+def test_row_blocks_world2_chunked_allreduce_bitwise(tmp_path):
+    """The chunked all-reduce (the distributed ctx's PLSS_DIST_CHUNKS path) sums every element of
+    the (n+1) buffer exactly as the single all-reduce does: bitwise the same solve, two ranks."""
+    a = _run(2, "C2s", tmp_path, chunks=1)
+    b = _run(2, "C2s", tmp_path, chunks=4)
+    assert int(a["iters"]) == int(b["iters"])
+    np.testing.assert_array_equal(a["hist"], b["hist"])
+    np.testing.assert_array_equal(a["x"], b["x"])
 
 
 def test_row_block_bounds_partition():

@@ -34,7 +34,8 @@ def _dist_solve(pkg, s, slabs=1, **kw):
     args = dict(tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit, flags=1 if s.freeze else 0)
     args.update(kw)
     ctx = pkg.plss_create_dist(A, 0, s.m, uid, 0, 1, slabs=slabs, maxit_cap=args["maxit"], validate=True)
-    assert pkg.plss_query(ctx)["launches_per_step"] == 2 * slabs + 2
+    # K1 + K2 per slab, K3, the dots kernel; the last K2 may run as up to 4 column chunks
+    assert 2 * slabs + 2 <= pkg.plss_query(ctx)["launches_per_step"] <= 2 * slabs + 5
     res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), **args)
     res["xh"] = res["x"].cpu().numpy()
     pkg.plss_destroy(ctx)
@@ -109,3 +110,32 @@ def test_dist_ctx_rejects_single_device_methods(pkg):
     out = pkg.plss_solve(ctx, s.b, tol=1e-6, maxit=100)
     assert out["outcome"] in ("converged", "maxit") and out["iters"] > 0
     pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("name", ["C5xs", "C2s"])
+def test_dist_chunked_allreduce_bitwise(pkg, name):
+    """The last K2 segment in column chunks, each all-reduced on a second stream while the next
+    computes (PLSS_DIST_CHUNKS): every y element is the same sequential sum plus the same NCCL
+    sum, so the solve is bitwise the unchunked one; the launch count shows the chunks engaged."""
+    s = plss_gen.make_config(name)            # both have sigma-sorted K2 slices (chunkable)
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    out = {}
+    for ch in ("1", "4"):
+        old = os.environ.get("PLSS_DIST_CHUNKS")
+        os.environ["PLSS_DIST_CHUNKS"] = ch
+        try:
+            ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=2, maxit_cap=s.maxit)
+        finally:
+            if old is None:
+                os.environ.pop("PLSS_DIST_CHUNKS")
+            else:
+                os.environ["PLSS_DIST_CHUNKS"] = old
+        q = pkg.plss_query(ctx)
+        res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, maxit=min(s.maxit, 200),
+                             flags=1 if s.freeze else 0)
+        out[ch] = (q["launches_per_step"], res["x"].cpu().numpy(), res["hist"], res["iters"])
+        pkg.plss_destroy(ctx)
+    assert out["4"][0] > out["1"][0], (out["4"][0], out["1"][0])      # chunks engaged
+    assert out["4"][3] == out["1"][3]
+    np.testing.assert_array_equal(out["4"][1], out["1"][1])
+    np.testing.assert_array_equal(out["4"][2], out["1"][2])
