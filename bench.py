@@ -167,6 +167,7 @@ def workload_label(name):
         "C5": "C5: m=64M n=8M, 12 nnz/row (6 banded +-1024 of i*n/m, 6 uniform), N(0,1), 768M nnz",
         "C3": "C3: 5-point Laplacian-like 2048^2 grid, 21M nnz",
         "C4": "C4: power-law Zipf(2.1) rows clipped [1,4096], m=2M n=8M",
+        "C4alt": "C4-alt: power-law Zipf(1.845) rows clipped [1,4096] (mean ~12), m=2M n=8M, 23.6M nnz",
         "C2": "C2: m=200k n=100k, 8 uniform nnz/row",
     }.get(name, name)
 
@@ -181,6 +182,9 @@ def cpu_sample(name):
         return plss_gen.make_config("C3", N=512), "C3 recipe at 512^2 (1/16 scale)"
     if name == "C4":
         return plss_gen.make_config("C4", m=200_000, n=800_000, support=8000), "C4 recipe at 1/10 scale"
+    if name == "C4alt":
+        return (plss_gen.make_config("C4alt", m=200_000, n=800_000, support=8000),
+                "C4-alt recipe at 1/10 scale")
     return plss_gen.make_config(name), f"{name} full"
 
 

@@ -160,6 +160,13 @@ plss_status plss_column_norms(plss_ctx *ctx, double *c);
 plss_status plss_spmv(plss_ctx *ctx, const double *x, double *y);
 plss_status plss_spmvT(plss_ctx *ctx, const double *u, double *v);
 
+/* The true residual of an iterate (the solve stops on the recursive residual of
+ * Algorithm 1; report the true one once at exit): out[0] = ||b - A x||_2, out[1] = ||b||_2 (host,
+ * 2 doubles). b: host or dev, m (local) doubles; x: host or dev, n doubles. One SpMV (the sequential
+ * row sums of plss_spmv) and a fixed-order reduction; on a distributed ctx the sums of squares are
+ * all-reduced (collective: every rank calls it). Synchronizes. */
+plss_status plss_true_residual(plss_ctx *ctx, const double *b, const double *x, double *out);
+
 /* Per-kernel device time of k loop steps launched one kernel at a time (not graphs), with CUDA
  * events on the ctx stream around each launch; call after plss_start. ms (host, 5 doubles)
  * receives the average per step of: K1 (all slabs), K2 (all slabs), the NCCL all-reduce,

@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1151,6 +1152,53 @@ plss_status plss_spmvT(plss_ctx* ctx, const double* u, double* v) {
   CK(cudaGetLastError());
   if (out != v && ctx->n > 0) CK(cudaMemcpyAsync(v, out, 8 * (size_t)ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return sync_out(ctx);
+}
+
+plss_status plss_true_residual(plss_ctx* ctx, const double* b, const double* x, double* out) {
+  if (!ctx || !out || (!b && ctx->m > 0) || (!x && ctx->n > 0)) return PLSS_E_INVALID;
+  if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  cudaStream_t st = ctx->stream;
+  const int64_t m = ctx->m, n = ctx->n;
+  const int grid = ctx->gnorm;
+  double *ax = nullptr, *db = nullptr, *dx = nullptr, *part = nullptr, *res = nullptr;
+  unsigned* cnt = nullptr;
+  const size_t mb = 8 * (size_t)std::max<int64_t>(m, 1), nb = 8 * (size_t)std::max<int64_t>(n, 1);
+  CK(cudaMallocAsync((void**)&ax, mb + 16, st));
+  CK(cudaMallocAsync((void**)&part, 16 * (size_t)grid + 16, st));
+  CK(cudaMallocAsync((void**)&res, 16, st));
+  CK(cudaMallocAsync((void**)&cnt, 16, st));
+  CK(cudaMemsetAsync(cnt, 0, 16, st));
+  CK(cudaMemsetAsync(res, 0, 16, st));
+  const double* bd = b;
+  const double* xd = x;
+  if (m > 0 && !is_device_ptr(b)) {
+    CK(cudaMallocAsync((void**)&db, mb, st));
+    CK(cudaMemcpyAsync(db, b, 8 * (size_t)m, cudaMemcpyHostToDevice, st));
+    bd = db;
+  }
+  if (n > 0 && !is_device_ptr(x)) {
+    CK(cudaMallocAsync((void**)&dx, nb + 16, st));
+    CK(cudaMemcpyAsync(dx, x, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+    xd = dx;
+  }
+  for (int s = 0; s < ctx->S; ++s) {                 // ax = A x (sequential row sums)
+    SpmvSeg a = ctx->seg1[s];
+    a.g = xd;
+    a.out = ax + ctx->R[s];
+    a.ctl = nullptr;
+    launch_spmv<ROLE_PLAIN>(a, ctx->g1[s], st);
+  }
+  if (m > 0) k_true_resid<<<grid, NT, 0, st>>>(bd, ax, m, part, cnt, res);
+  CK(cudaGetLastError());
+  if (ctx->dist) NK(ncclAllReduce(res, res, 2, ncclFloat64, ncclSum, ctx->comm, st));
+  double h[2] = {0.0, 0.0};
+  CK(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, st));
+  for (void* q : {(void*)ax, (void*)db, (void*)dx, (void*)part, (void*)res, (void*)cnt})
+    if (q) CK(cudaFreeAsync(q, st));
+  CK(cudaStreamSynchronize(st));
+  out[0] = std::sqrt(h[0]);
+  out[1] = std::sqrt(h[1]);
   return sync_out(ctx);
 }
 

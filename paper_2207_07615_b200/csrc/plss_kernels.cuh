@@ -1255,6 +1255,21 @@ __global__ void k_win_chain(int2* wlo, const int32_t* cblk, int grid, int win, i
 // CTA c of a windowed launch owns blocks [cblk[c], cblk[c+1]): the first block whose stored
 // entries start at or after c/grid of the segment's total (work balance when row lengths vary,
 // e.g. C5's K2 slabs where a band of columns holds 9x the entries of the rest).
+// out = {sum (b - ax)^2, sum b^2} over this rank's rows: fixed per-thread order, block trees, last
+// CTA sums the CTA pairs in index order (deterministic). plss_true_residual.
+__global__ void __launch_bounds__(NT) k_true_resid(const double* __restrict__ b, const double* __restrict__ ax,
+                                                   long long m, double* part, unsigned* counter, double* out) {
+  __shared__ double sm[2][MAXW];
+  double s0 = 0.0, s1 = 0.0;
+  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < m; i += (long long)gridDim.x * NT) {
+    const double d = __dadd_rn(b[i], -ax[i]);
+    s0 = __dadd_rn(s0, __dmul_rn(d, d));
+    s1 = __dadd_rn(s1, __dmul_rn(b[i], b[i]));
+  }
+  if (!publish_and_elect(s0, s1, part, part, gridDim.x, counter, sm)) return;
+  if (threadIdx.x == 0) { out[0] = s0; out[1] = s1; }
+}
+
 __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, int nblocks, int grid,
                              int32_t* cblk, int unit_cost) {
   // w: prefix over units (nunits+1 entries); unit cost = (w[u+1] - w[u]) * wscale + UNIT_COST

@@ -30,7 +30,7 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile",
            "plss_kz_workspace_bytes", "plss_kz_solve", "plss_kz_start", "plss_kz_step", "plss_kz_finish",
            "plss_kz_profile", "plss_eg_workspace_bytes", "plss_eg_solve", "plss_eg_start", "plss_eg_step",
-           "plss_eg_finish", "plss_eg_profile"]
+           "plss_eg_finish", "plss_eg_profile", "plss_true_residual"]
 
 
 class PlssError(RuntimeError):
@@ -142,6 +142,8 @@ def load_library(path: str = None):
     lib.plss_eg_solve.restype = st
     lib.plss_eg_profile.argtypes = [P, I32, P]
     lib.plss_eg_profile.restype = st
+    lib.plss_true_residual.argtypes = [P, P, P, P]
+    lib.plss_true_residual.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
     lib.plss_status_str.argtypes = [st]
@@ -361,6 +363,14 @@ def plss_column_norms(ctx: Ctx, out=None):
         out = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
     _check(load_library().plss_column_norms(ctx.handle, _ptr(out)), ctx.handle)
     return out
+
+
+def plss_true_residual(ctx: Ctx, b, x) -> dict:
+    """||b - A x|| and ||b|| (and their ratio) for an iterate x (host or device)."""
+    out = np.zeros(2)
+    _check(load_library().plss_true_residual(ctx.handle, _ptr(b), _ptr(x), _ptr(out)), ctx.handle)
+    return {"abs": float(out[0]), "norm_b": float(out[1]),
+            "rel": float(out[0] / out[1]) if out[1] > 0 else float(out[0])}
 
 
 def plss_spmv(ctx: Ctx, x, y):

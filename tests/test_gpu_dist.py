@@ -139,3 +139,15 @@ def test_dist_chunked_allreduce_bitwise(pkg, name):
     assert out["4"][3] == out["1"][3]
     np.testing.assert_array_equal(out["4"][1], out["1"][1])
     np.testing.assert_array_equal(out["4"][2], out["1"][2])
+
+
+def test_dist_true_residual(pkg):
+    s = plss_gen.make_config("C2s")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, maxit_cap=s.maxit)
+    res = pkg.plss_solve(ctx, s.b, tol=s.tol, maxit=s.maxit)
+    t = pkg.plss_true_residual(ctx, s.b, res["x"])
+    x = res["x"].cpu().numpy()
+    ref = np.linalg.norm(s.b - oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x)) / np.linalg.norm(s.b)
+    pkg.plss_destroy(ctx)
+    assert abs(t["rel"] - ref) <= 1e-12

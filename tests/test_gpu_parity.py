@@ -410,3 +410,24 @@ def test_plssw_rejects_bad_weights(pkg):
     with pytest.raises(pkg.PlssError, match="invalid"):
         pkg.plss_set_wi(ctx, w)
     pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("name", ["C2s", "C4xs", "C1"])
+def test_true_residual_at_exit(pkg, name):
+    """the solve stops on the recursive residual; plss_true_residual reports
+    ||b - A x|| / ||b|| once at exit. Checked against the oracle's own SpMV of the returned x (both
+    sums per row are sequential and bitwise equal; only the final norm's order differs), host and
+    device arguments, and against the recursive history at convergence."""
+    s = plss_gen.make_config(name)
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create(A, maxit_cap=s.maxit)
+    res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, maxit=s.maxit)
+    x = res["x"].cpu().numpy()
+    ref = np.linalg.norm(s.b - oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x))
+    for b_arg, x_arg in ((s.b, x), (torch.from_numpy(s.b).cuda(), res["x"])):
+        t = pkg.plss_true_residual(ctx, b_arg, x_arg)
+        assert abs(t["abs"] - ref) <= 1e-12 * np.linalg.norm(s.b)
+        assert abs(t["norm_b"] - np.linalg.norm(s.b)) <= 1e-13 * np.linalg.norm(s.b)
+    if res["outcome"] == "converged":                 # recursive and true residual agree at the end
+        assert t["rel"] <= 10 * s.tol + 1e-13
+    pkg.plss_destroy(ctx)
