@@ -256,6 +256,9 @@ def main():
     ap.add_argument("--plss-w", action="store_true",
                     help="PLSS W: WI = diag(||A_{:,j}||) (the paper's second variant; default PLSS, WI = I)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rhs", default="xstar", choices=["xstar", "paper"],
+                    help="paper: the paper's protocol right-hand side x = ones, x(1) = 10, b = A x (P:L987), "
+                         "a labelled protocol-fidelity variant (SURVEY 8d)")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e / profile / cpu legs")
     ap.add_argument("--method", default="plss", choices=["plss", "rp", "kz", "eg"],
@@ -322,6 +325,12 @@ def main():
                               window=not args.no_window)
     q = pkg.plss_query(ctx)
     b = w["b"]
+    if args.rhs == "paper":                                   # b = A x_p with x_p = ones, x_p(1) = 10
+        xp = torch.ones(n, dtype=torch.float64, device=dev)
+        xp[0] = 10.0
+        b = torch.empty(m_l, dtype=torch.float64, device=dev)
+        pkg.plss_spmv(ctx, xp, b)
+        del xp
     if args.plss_w:
         pkg.plss_set_wi(ctx, pkg.plss_column_norms(ctx))
     torch.cuda.synchronize()
@@ -394,6 +403,8 @@ def main():
                        "slabs": q["slabs"], "sell_segments": q["sell_segments"],
                        "window_segments": q["window_segments"], "freeze_mode": True,
                        "tol": 0.0, "variant": "PLSS W (WI = diag(||A_:,j||))" if args.plss_w else "PLSS (WI = I)",
+                       "rhs": ("paper: x = ones, x(1) = 10, b = A x (P:L987)" if args.rhs == "paper"
+                               else "b = A x*, x* ~ N(0,1)"),
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
                        "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8"},
             "achieved_gbs": B_global * iters_per_s / 1e9,

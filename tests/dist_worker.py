@@ -90,6 +90,11 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         assert isinstance(obj[0], bytes) and len(obj[0]) == 128
         hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit, args.chunks)
+        for arr in (np.asarray(hist, dtype=np.float64), x):    # replicated decisions, bitwise (8e)
+            t = torch.from_numpy(np.ascontiguousarray(arr))
+            ts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(ts, t)
+            assert all(torch.equal(ts[0], q) for q in ts)
     else:
         import paper_2207_07615_b200 as pkg
         torch.cuda.set_device(local)
@@ -101,13 +106,15 @@ def main():
                                    blk["col_ptr"], blk["row_idx"], blk["val_t"])
         ctx = pkg.plss_create_dist(A, blk["row_offset"], s.m, obj[0], rank, world, maxit_cap=s.maxit,
                                    validate=True)
-        res = pkg.plss_solve(ctx, torch.from_numpy(blk["b"]).cuda(), tol=s.tol, maxit=s.maxit)
+        res = pkg.plss_solve(ctx, torch.from_numpy(blk["b"]).cuda(), tol=s.tol, maxit=s.maxit, want_diag=True)
         hist, x, iters = res["hist"], res["x"].cpu().numpy(), res["iters"]
-        # every rank holds the same replicated x, bitwise
-        xt = torch.from_numpy(x).cuda()
-        xs = [torch.empty_like(xt) for _ in range(world)]
-        dist.all_gather(xs, xt)
-        assert all(torch.equal(xs[0], q) for q in xs)
+        # every rank holds the same replicated x and took the same decisions from the
+        # same scalars -- rho, phi, psi, theta, tau, beta, gamma of every iteration, bitwise
+        for arr in (x, res["diag"].reshape(-1)):
+            t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+            ts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(ts, t)
+            assert all(torch.equal(ts[0], q) for q in ts)
         pkg.plss_destroy(ctx)
     if rank == 0:
         np.savez(args.out, hist=hist, x=x, iters=iters)
