@@ -779,8 +779,32 @@ def main_eg(args):
                     "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
                     "note": "one plss_eg_solve from pinned host b to host x + history (from history 0)"},
             "clocks": clk.summary(), "final_hist": float(fin["hist_full"][W + K])}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = eg_cpu_leg(s, workload_label(name), rows, sk, fac, B)
     print(json.dumps(line), flush=True)
     pkg.plss_destroy(ctx)
+
+
+def eg_cpu_leg(s, label, rows, sk, fac, window_bytes, budget_s=15.0):
+    """The engine oracle for a bounded number of steps from history 0; its algorithmic GB/s
+    converts to it/s for the GPU's timed window (as kz_cpu_leg)."""
+    from oracle import engine as oeg
+    run = oeg.tri_engine if fac == "triangular" else oeg.qr_engine
+    bfn = eg_bytes_per_iter if fac == "triangular" else eg_qr_bytes_per_iter
+    A = s.scipy_csr()
+    t0 = time.perf_counter()
+    run(A, s.b, sketch=sk, maxit=5, rows=rows, seed=1)
+    t1 = (time.perf_counter() - t0) / 5
+    k = int(max(10, min(200, budget_s / max(t1 * 8, 1e-6))))
+    t0 = time.perf_counter()
+    run(A, s.b, sketch=sk, maxit=k, rows=rows, seed=1)
+    t = time.perf_counter() - t0
+    gbs = sum(bfn(s.m, s.n, s.nnz, h, sk) for h in range(k)) / t / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+    return {"value": gbs * 1e9 / window_bytes, "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": f"{label}; the first {k} engine steps ({fac}, {sk} sketch) of the oracle in {t:.1f} s = "
+                      f"{gbs:.2f} GB/s algorithmic (numpy/scipy, BLAS threads up to {cores}); it/s scaled to the "
+                      f"GPU's timed window by algorithmic bytes/iter", "oracle_gbs": gbs}
 
 
 if __name__ == "__main__":
