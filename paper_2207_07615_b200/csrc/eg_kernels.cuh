@@ -38,6 +38,7 @@ namespace plss {
 
 constexpr int EG_NT = 256;
 constexpr int EG_RT = 2048;              // rows per CTA of the Y^T y kernel (grid.x = row ranges)
+constexpr int EG_RT_SMALL = 512;         // ... while few column groups are active (small history)
 constexpr int EG_CT = 32;                // columns per CTA of the Y^T y kernel (grid.y = column groups)
 constexpr double EG_SKIP_REL = 1e-14;
 
@@ -124,14 +125,22 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gauss(EgArgs a) {
 // partials of g_j = Y[:, j]^T y (j < hk) and y^T y: CTA (x, y) covers rows [x RT, (x+1) RT) and
 // columns [y CT, (y+1) CT); warp w takes columns w, w + 8, w + 16, w + 24 at once (8 independent
 // loads per lane step), lanes stride the rows (64 per lane per column, amortizing the butterfly)
-template <int SRC>                      // 0: y (Y^T y and y^T y), 1: w = v (QR: V^T v)
+// Two instances run per step: RT = EG_RT_SMALL while ceil(n / EG_RT) * ceil(hk / EG_CT) CTAs would
+// leave the GPU under-filled (small histories), RT = EG_RT otherwise; the other one exits at once.
+__device__ __forceinline__ int eg_rt(const EgArgs& a, int hk) {
+  const int64_t big = ((a.n + EG_RT - 1) / EG_RT) * (int64_t)((hk + EG_CT - 1) / EG_CT);
+  return big >= 2 * 148 ? EG_RT : EG_RT_SMALL;
+}
+template <int SRC, int RT = EG_RT>      // SRC 0: y (Y^T y and y^T y), 1: w = v (QR: V^T v)
 __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   if (eg_done(a)) return;
   const int hk = a.st->hk;
+  if (eg_rt(a, hk) != RT) return;
   const double* vec = SRC == 0 ? a.y : a.w;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = EG_NT / 32;
-  const int64_t l0 = (int64_t)blockIdx.x * EG_RT, l1 = min(a.n, l0 + EG_RT);
+  if ((int64_t)blockIdx.x * RT >= a.n && !(blockIdx.x == 0)) return;
+  const int64_t l0 = (int64_t)blockIdx.x * RT, l1 = min(a.n, l0 + RT);
   double* out = a.part + (size_t)blockIdx.x * (a.kmax + 1);
   const int jc0 = blockIdx.y * EG_CT;
   if (SRC == 0 && warp == 0 && blockIdx.y == 0) {
@@ -194,7 +203,9 @@ __global__ void __launch_bounds__(EG_NT) k_eg_red(EgArgs a) {
   double s = 0.0;
   if (e <= hk) {
     const int col = e < hk ? e : K;
-    for (int g = lane; g < a.grid_t; g += 32) s = __dadd_rn(s, a.part[(size_t)g * (K + 1) + col]);
+    const int rt = eg_rt(a, DST == 1 ? hk : hk);
+    const int nr = (int)((a.n + rt - 1) / rt);        // row ranges of the Y^T y instance that ran
+    for (int g = lane; g < nr; g += 32) s = __dadd_rn(s, a.part[(size_t)g * (K + 1) + col]);
   } else if (a.mode == EG_GAUSSIAN) {
     for (int g = lane; g < a.grid_s; g += 32) s = __dadd_rn(s, a.part_rs[g]);
   }

@@ -1828,7 +1828,7 @@ plss_status plss_kz_profile(plss_ctx* ctx, int32_t k, double* ms) {
 // ---- growing-sketch engine, triangular factorization (eg_kernels.cuh) --------
 static void eg_grids(const plss_ctx* ctx, int* g_t, int* g_s, int* g_g) {
   const int sms = rp_sms(ctx);
-  *g_t = (int)std::max<int64_t>(1, (ctx->n + EG_RT - 1) / EG_RT);          // row ranges of Y^T y
+  *g_t = (int)std::max<int64_t>(1, (ctx->n + EG_RT_SMALL - 1) / EG_RT_SMALL);   // max row ranges of Y^T y
   *g_s = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->m + EG_NT - 1) / EG_NT, 4 * (int64_t)sms));
   *g_g = (int)std::max<int64_t>(1, std::min<int64_t>((ctx->n + 63) / 64, 8 * (int64_t)sms));
 }
@@ -1854,8 +1854,10 @@ static void eg_enqueue_sketch(plss_ctx* ctx, cudaStream_t st) {
 static void eg_enqueue_factor(plss_ctx* ctx, cudaStream_t st, cudaEvent_t ev_a, cudaEvent_t ev_b) {
   const EgArgs& a = ctx->eg;
   const int gred = (a.kmax + 2 + EG_NT / 32 - 1) / (EG_NT / 32);
-  const dim3 gT(a.grid_t, (a.kmax + EG_CT - 1) / EG_CT);
-  k_eg_gemvT<0><<<gT, EG_NT, 0, st>>>(a);
+  const int gy = (a.kmax + EG_CT - 1) / EG_CT;
+  const dim3 gT((unsigned)std::max<int64_t>(1, (a.n + EG_RT - 1) / EG_RT), gy), gTs((unsigned)a.grid_t, gy);
+  k_eg_gemvT<0, EG_RT><<<gT, EG_NT, 0, st>>>(a);
+  k_eg_gemvT<0, EG_RT_SMALL><<<gTs, EG_NT, 0, st>>>(a);
   k_eg_red<0><<<gred, EG_NT, 0, st>>>(a);
   if (ev_a) cudaEventRecord(ev_a, st);
   if (a.factor == 0) {
@@ -1867,7 +1869,8 @@ static void eg_enqueue_factor(plss_ctx* ctx, cudaStream_t st, cudaEvent_t ev_a, 
     k_qr_b<<<gred, EG_NT, 0, st>>>(a);
     k_qr_w<<<a.grid_g, EG_NT, 0, st>>>(a);
     k_qr_v<<<a.grid_s, EG_NT, 0, st>>>(a);
-    k_eg_gemvT<1><<<gT, EG_NT, 0, st>>>(a);
+    k_eg_gemvT<1, EG_RT><<<gT, EG_NT, 0, st>>>(a);
+    k_eg_gemvT<1, EG_RT_SMALL><<<gTs, EG_NT, 0, st>>>(a);
     k_eg_red<1><<<gred, EG_NT, 0, st>>>(a);
     k_qr_tri<<<a.grid_tri, EG_NT, 0, st>>>(a);
     if (ev_b) cudaEventRecord(ev_b, st);
