@@ -47,6 +47,16 @@ def eg_bytes_per_iter(m, n, nnz, hk, sketch):
     return sk + 16 * n * hk + 48 * n + 8 * hk * hk + 12 * nnz + 4 * (m + 1) + 8 * n + 16 * m
 
 
+def eg_launches_per_step(sketch, factor, slabs):
+    """Our kernels per engine step (plss.cu eg_enqueue_step): the sketch (identity: k_eg_row;
+    Gaussian: k_eg_gauss + K2 per slab; residual: K2 per slab), two Y^T y instances + k_eg_red,
+    triangular: k_eg_triu, k_eg_trit, k_eg_gemv / QR: k_qr_b, k_qr_w, k_qr_v, two V^T v instances,
+    k_eg_red, k_qr_tri, k_eg_gemv; K1 per slab."""
+    sk = {"identity": 1, "gaussian": 1 + slabs, "residual": slabs}[sketch]
+    fac = 3 if factor == "triangular" else 8
+    return sk + 3 + fac + slabs
+
+
 def eg_qr_bytes_per_iter(m, n, nnz, hk, sketch):
     """The QR variant streams the store four times (V^T y, y - V b, V^T v, e_h - V z)."""
     return eg_bytes_per_iter(m, n, nnz, hk, sketch) + 16 * n * hk + 48 * n
@@ -659,7 +669,8 @@ def main_kz(args):
                          "unit": "GB/s", "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak, "traffic": None,
                          "peak_source": peak_src, "algorithmic_bytes_per_step": dom_bytes,
                          "kernel_ms_per_step": dom_ms, "history_at_profile": hk_prof},
-            "kernels_ms_per_step": kt, "gpu_launches": K * (3 + q["slabs"]),
+            # per step: k_kz_gemv, the plain SpMV (one launch per slab), k_kz_resid (row prep fused)
+            "kernels_ms_per_step": kt, "gpu_launches": K * (2 + q["slabs"]),
             "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": (8 * m + 4 * (W + K)) / (W + K),
                     "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
                     "note": "one plss_kz_solve from pinned host b and host rows to host x + history "
@@ -774,7 +785,7 @@ def main_eg(args):
                          "unit": "GB/s", "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak, "traffic": None,
                          "peak_source": peak_src, "algorithmic_bytes_per_step": dom_bytes,
                          "kernel_ms_per_step": dom_ms, "history_at_profile": hk_prof},
-            "kernels_ms_per_step": kt, "gpu_launches": K * (5 + 2 * q["slabs"]),
+            "kernels_ms_per_step": kt, "gpu_launches": K * eg_launches_per_step(sk, fac, q["slabs"]),
             "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": 8 * m / (W + K),
                     "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
                     "note": "one plss_eg_solve from pinned host b to host x + history (from history 0)"},
