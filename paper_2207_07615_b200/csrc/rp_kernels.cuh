@@ -80,16 +80,14 @@ __device__ __forceinline__ void rp_sincos_2pi32(float u2, float& sin_t, float& c
   cs = __fadd_rn(__fmul_rn(cs, p2), 1.0f / 24.0f);
   cs = __fadd_rn(__fmul_rn(cs, p2), -0.5f);
   cs = __fadd_rn(__fmul_rn(cs, p2), 1.0f);
-  switch (o) {
-    case 0: sin_t = sn; cos_t = cs; break;
-    case 1: sin_t = cs; cos_t = sn; break;
-    case 2: sin_t = cs; cos_t = -sn; break;
-    case 3: sin_t = sn; cos_t = -cs; break;
-    case 4: sin_t = -sn; cos_t = -cs; break;
-    case 5: sin_t = -cs; cos_t = -sn; break;
-    case 6: sin_t = -cs; cos_t = sn; break;
-    default: sin_t = -sn; cos_t = cs; break;
-  }
+  // octant symmetries without divergent branches (lanes hold random octants): swap sin / cos for
+  // o in {1,2,5,6}, negate sin for o >= 4 and cos for o in {2,3,4,5} -- exact, so bitwise the
+  // oracle's table (0: (s, c), 1: (c, s), 2: (c, -s), 3: (s, -c), 4: (-s, -c), 5: (-c, -s),
+  // 6: (-c, s), 7: (-s, c))
+  const bool swp = ((o + 1) >> 1) & 1;
+  const float a = swp ? cs : sn, b = swp ? sn : cs;
+  sin_t = o >= 4 ? -a : a;
+  cos_t = (((o + 2) >> 2) & 1) ? -b : b;
 }
 // the binary32 normal pair (S[i, 2q], S[i, 2q+1]) of pair counter `base` = ((k 2^32 + i) h + q):
 // Box-Muller from one 64-bit word (no rejection, so warps never diverge)
