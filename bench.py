@@ -669,8 +669,11 @@ def main_kz(args):
                          "unit": "GB/s", "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak, "traffic": None,
                          "peak_source": peak_src, "algorithmic_bytes_per_step": dom_bytes,
                          "kernel_ms_per_step": dom_ms, "history_at_profile": hk_prof},
-            # per step: k_kz_gemv, the plain SpMV (one launch per slab), k_kz_resid (row prep fused)
-            "kernels_ms_per_step": kt, "gpu_launches": K * (2 + q["slabs"]),
+            # per step: k_kz_gemv and k_kz_resid (row prep fused), plus the plain SpMV per slab unless
+            # every row has <= 32 entries (then k_kz_resid computes (A p)_l itself)
+            "kernels_ms_per_step": kt,
+            "gpu_launches": K * (2 + (0 if (int(np.diff(s.row_ptr).max()) <= 32
+                                            and os.environ.get("PLSS_KZ_FUSE", "1") != "0") else q["slabs"])),
             "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": (8 * m + 4 * (W + K)) / (W + K),
                     "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
                     "note": "one plss_kz_solve from pinned host b and host rows to host x + history "

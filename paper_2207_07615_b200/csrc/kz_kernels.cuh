@@ -58,7 +58,9 @@ struct KzArgs {
   Ctl* ctl;
   double* rec;
   int32_t grid_gemv, grid_res;
+  int32_t fused;             // rows <= KZ_FUSE_MAXROW: k_kz_resid computes (A p)_l itself
 };
+constexpr int KZ_FUSE_MAXROW = 32;
 
 __device__ __forceinline__ bool kz_done(const KzArgs& a) { return a.ctl->done != 0; }
 
@@ -159,6 +161,9 @@ __global__ void __launch_bounds__(KZ_NT) k_kz_gemv(KzArgs a) {
   if (threadIdx.x == 0) a.part_th[blockIdx.x] = th;
 }
 
+// FUSED: (A p)_l is this thread's own sequential ascending sum over row l (rows of <= KZ_FUSE_MAXROW
+// entries; bitwise the plain SpMV's value), replacing the separate SpMV launch and its apk pass
+template <bool FUSED>
 __global__ void __launch_bounds__(KZ_NT) k_kz_resid(KzArgs a) {
   if (kz_done(a)) return;
   __shared__ double sm[2][MAXW];
@@ -169,7 +174,14 @@ __global__ void __launch_bounds__(KZ_NT) k_kz_resid(KzArgs a) {
   double* APnew = a.AP + hk;
   double rho = 0.0, zero = 0.0;
   for (int64_t l = l0 + threadIdx.x; l < l1; l += KZ_NT) {
-    const double q = a.apk[l];
+    double q;
+    if (FUSED) {
+      q = 0.0;
+      const int e1 = a.row_ptr[l + 1];
+      for (int e = a.row_ptr[l]; e < e1; ++e) q = __dadd_rn(q, __dmul_rn(a.val[e], __ldg(a.pk + a.col_idx[e])));
+    } else {
+      q = a.apk[l];
+    }
     const double rl = __dadd_rn(a.r[l], -q);
     a.r[l] = rl;
     if (!skip) APnew[l * a.kmax] = q;

@@ -1678,8 +1678,12 @@ static plss_status kz_enqueue_step(plss_ctx* ctx) {
   cudaStream_t st = ctx->stream;
   const KzArgs& a = ctx->kz;
   k_kz_gemv<<<a.grid_gemv, KZ_NT, 0, st>>>(a);
-  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
-  k_kz_resid<<<a.grid_res, KZ_NT, 0, st>>>(a);
+  if (a.fused) {
+    k_kz_resid<true><<<a.grid_res, KZ_NT, 0, st>>>(a);
+  } else {
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
+    k_kz_resid<false><<<a.grid_res, KZ_NT, 0, st>>>(a);
+  }
   CK(cudaGetLastError());
   return PLSS_OK;
 }
@@ -1749,6 +1753,18 @@ plss_status plss_kz_start(plss_ctx* ctx, int32_t kmax, void* workspace, size_t w
   CK(cudaMemsetAsync(a.counter, 0, 256, st));
   if (n > 0) CK(cudaMemsetAsync(a.arow, 0, 8 * n, st));
   CK(cudaStreamSynchronize(st));   // hrows / s0 are host temporaries
+  {                                                  // short rows only: fuse (A p)_l into k_kz_resid
+    int32_t* dmax = nullptr;
+    int32_t hmax = 0;
+    CK(cudaMallocAsync((void**)&dmax, sizeof(int32_t), st));
+    CK(cudaMemsetAsync(dmax, 0, sizeof(int32_t), st));
+    if (m > 0) k_max_row_len<<<(unsigned)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(a.row_ptr, (long long)m, dmax);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&hmax, dmax, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(dmax, st));
+    CK(cudaStreamSynchronize(st));
+    a.fused = (hmax <= KZ_FUSE_MAXROW && env_int("PLSS_KZ_FUSE", 1) != 0) ? 1 : 0;
+  }
   ctx->kz = a;
   k_kz_prep<<<1, KZ_NT, 0, st>>>(a);   // the first step's row; later steps' rows are prepared by k_kz_resid
   CK(cudaGetLastError());
@@ -1806,9 +1822,11 @@ plss_status plss_kz_profile(plss_ctx* ctx, int32_t k, double* ms) {
     CK(cudaEventRecord(ev[1], st));     // row preparation is fused into k_kz_resid (slot 0 stays ~0)
     k_kz_gemv<<<a.grid_gemv, KZ_NT, 0, st>>>(a);
     CK(cudaEventRecord(ev[2], st));
-    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
+    if (!a.fused)
+      for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_PLAIN>(ctx->kz_seg[s], ctx->g1[s], st);
     CK(cudaEventRecord(ev[3], st));
-    k_kz_resid<<<a.grid_res, KZ_NT, 0, st>>>(a);
+    if (a.fused) k_kz_resid<true><<<a.grid_res, KZ_NT, 0, st>>>(a);
+    else k_kz_resid<false><<<a.grid_res, KZ_NT, 0, st>>>(a);
     CK(cudaEventRecord(ev[4], st));
     CK(cudaGetLastError());
     CK(cudaEventSynchronize(ev[4]));

@@ -1270,6 +1270,15 @@ __global__ void __launch_bounds__(NT) k_true_resid(const double* __restrict__ b,
   if (threadIdx.x == 0) { out[0] = s0; out[1] = s1; }
 }
 
+// *out = max_i (row_ptr[i+1] - row_ptr[i]) over i < m (atomicMax; order-independent)
+__global__ void k_max_row_len(const int32_t* __restrict__ row_ptr, long long m, int32_t* out) {
+  int32_t mx = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    mx = max(mx, row_ptr[i + 1] - row_ptr[i]);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(out, mx);
+}
+
 __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, int nblocks, int grid,
                              int32_t* cblk, int unit_cost) {
   // w: prefix over units (nunits+1 entries); unit cost = (w[u+1] - w[u]) * wscale + UNIT_COST

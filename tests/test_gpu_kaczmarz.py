@@ -138,3 +138,27 @@ def test_start_step_finish_and_errors(pkg):
     out = pkg.plss_solve(ctx, s.b, tol=1e-8, maxit=1000)
     assert out["outcome"] == "converged"
     pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("case", ["C2s", "C3_32"])
+def test_fused_residual_bitwise(pkg, case):
+    """Short rows (<= 32 entries): k_kz_resid computes (A p)_l itself instead of the separate plain
+    SpMV -- the same sequential ascending sum, so the run is bitwise the unfused one."""
+    s = plss_gen.make_config("C3", N=32) if case == "C3_32" else plss_gen.make_config(case)
+    rows = np.random.default_rng(4).permutation(s.m)[:120]
+    out = []
+    for fuse in ("1", "0"):
+        old = os.environ.get("PLSS_KZ_FUSE")
+        os.environ["PLSS_KZ_FUSE"] = fuse
+        try:
+            ctx = _ctx(pkg, s, slabs=2)
+            r = pkg.plss_kz_solve(ctx, s.b, rows, maxit=120, tol=0.0)
+            pkg.plss_destroy(ctx)
+        finally:
+            if old is None:
+                os.environ.pop("PLSS_KZ_FUSE")
+            else:
+                os.environ["PLSS_KZ_FUSE"] = old
+        out.append(r)
+    np.testing.assert_array_equal(out[0]["x"].cpu().numpy(), out[1]["x"].cpu().numpy())
+    np.testing.assert_array_equal(out[0]["hist"], out[1]["hist"])
