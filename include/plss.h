@@ -84,6 +84,10 @@ typedef struct {
   int32_t flags;       /* bit0: disable the SELL-32 format (saves its ~2 x 1.15 nnz x 12 B of
                           workspace); bit1: disable the shared-memory windows of the gathered
                           vector (SELL segments then gather every entry from global memory);
+                          bit2 (distributed ctx only): the reduce-scatter step -- y is
+                          reduce-scattered to column shards of n / nranks, phi / psi and K3 run
+                          on the shard, one all-reduce carries {rho, phi, psi, theta}, p is
+                          all-gathered; x is gathered by plss_finish (then collective);
                           other bits must be 0                                             */
 } plss_options;
 

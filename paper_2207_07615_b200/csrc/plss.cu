@@ -31,6 +31,7 @@ namespace {
 
 constexpr int MAXG = 2048;           // upper bound on persistent-CTA grid sizes (partials)
 constexpr int DCH_MAX = 8;           // column chunks of the last K2 segment on a distributed ctx
+constexpr int64_t DPAD = 64 * 32;    // vector slack for the reduce-scatter step (64 ranks x 32)
 constexpr int SCAN_ITEMS = 16;       // setup scan: items per thread
 constexpr size_t ALIGN = 256;
 
@@ -79,9 +80,11 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o2 = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o2; };
   L->r = take(8 * m);
-  L->y = take(8 * (n + 1));      // dist: y | rho (the all-reduce buffer)
-  L->p = take(8 * n);
-  L->x = take(8 * n);
+  // dist: y | rho (the all-reduce buffer); DPAD slack lets the reduce-scatter step pad y, p, x to
+  // nranks x (32-aligned shard) doubles for up to 64 ranks
+  L->y = take(8 * (n + 1 + DPAD));
+  L->p = take(8 * (n + DPAD));
+  L->x = take(8 * (n + DPAD));
   L->rec = take(8 * (size_t)(L->maxit_cap + 1) * REC);
   L->ctl = take(sizeof(Ctl));
   L->counters = take(64 * sizeof(unsigned));
@@ -217,6 +220,10 @@ struct plss_ctx {
   std::vector<int64_t> drows;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ch[DCH_MAX] = {}, ev_join = nullptr;
+  // reduce-scatter / all-gather step (options.flags bit2): column shard [c0, c0 + nsh) of the
+  // padded nranks x cnt vectors; scalars[4..7] = {rho, phi, psi, theta} partials, all-reduced
+  bool rsag = false;
+  int64_t cnt = 0, c0 = 0, nsh = 0;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   // solve state
@@ -324,6 +331,21 @@ static plss_status enqueue_step(plss_ctx* ctx) {
     } else {
       launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
     }
+  }
+  if (ctx->rsag) {
+    // reduce-scatter y to this rank's shard, shard dots, one all-reduce of 4 scalars, the tails,
+    // K3 on the shard, all-gather p (K1 gathers all of p)
+    double* sc = ctx->scalars + 4;
+    NK(ncclReduceScatter(ctx->y, ctx->y + ctx->c0, (size_t)ctx->cnt, ncclFloat64, ncclSum, ctx->comm, st));
+    k_dots_shard<<<ctx->gdots, NT, 0, st>>>(ctx->y + ctx->c0, ctx->p + ctx->c0, ctx->nsh, ctx->ctl, ctx->part2,
+                                            ctx->counters + 1, ctx->wi ? ctx->wi + ctx->c0 : nullptr, sc);
+    NK(ncclAllReduce(sc, sc, 4, ncclFloat64, ncclSum, ctx->comm, st));
+    k_tail_rsag<<<1, 1, 0, st>>>(ctx->ctl, ctx->rec, sc);
+    k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p + ctx->c0, ctx->y + ctx->c0, ctx->x + ctx->c0, ctx->nsh, ctx->ctl, ctx->rec,
+                                       ctx->part3, ctx->counters + 2, ctx->wi ? ctx->wi + ctx->c0 : nullptr, sc + 3);
+    NK(ncclAllGather(ctx->p + ctx->c0, ctx->p, (size_t)ctx->cnt, ncclFloat64, ctx->comm, st));
+    CK(cudaGetLastError());
+    return PLSS_OK;
   }
   if (ctx->dist) {
     if (!chunked) NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
@@ -672,7 +694,16 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (!A->row_ptr || !A->col_ptr || (A->nnz > 0 && (!A->col_idx || !A->val || !A->row_idx || !A->val_t))) {
     set_err(ctx, "NULL matrix array"); return PLSS_E_INVALID;
   }
-  if (opt && (opt->flags & ~3) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & ~7) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & 4) && !dist) { set_err(ctx, "options.flags bit2 needs a distributed ctx"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & 4) && ctx->nranks > 64) { set_err(ctx, "reduce-scatter step: at most 64 ranks"); return PLSS_E_INVALID; }
+  if (dist && opt && (opt->flags & 4)) {
+    ctx->rsag = true;
+    ctx->cnt = (A->n + ctx->nranks - 1) / ctx->nranks;
+    ctx->cnt = (ctx->cnt + 31) / 32 * 32;
+    ctx->c0 = (int64_t)ctx->rank * ctx->cnt;
+    ctx->nsh = std::max<int64_t>(0, std::min<int64_t>(A->n, ctx->c0 + ctx->cnt) - ctx->c0);
+  }
   {
     const void* arrs[6] = {A->row_ptr, A->col_idx, A->val, A->col_ptr, A->row_idx, A->val_t};
     for (const void* q : arrs)
@@ -845,7 +876,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.counter = ctx->counters + 0;
     a.ctl = ctx->ctl;
     a.rec = ctx->rec;
-    a.rho_out = ctx->y + n;
+    a.rho_out = ctx->rsag ? ctx->scalars + 4 : ctx->y + n;
     t1off += nt + 1;
     ctx->g1[s] = grid_for(nt, occ[ROLE_K1], sms);
     if (L.sell) {
@@ -921,7 +952,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     }
   }
   CK(cudaGetLastError());
-  if (dist && L.sell) {
+  if (dist && L.sell && !ctx->rsag) {
     const plss_status st2 = make_chunks(ctx, ctx->seg2[S - 1], pool2, sms, env_int("PLSS_DIST_CHUNKS", 4));
     if (st2 != PLSS_OK) return st2;
   }
@@ -1039,6 +1070,12 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
       CK(cudaMemsetAsync(ctx->x, 0, 8 * (size_t)n, st));
     }
   }
+  if (ctx->rsag) {                                  // padding beyond n of the reduce-scattered y and of p
+    const size_t pad = (size_t)(ctx->cnt * ctx->nranks - n);
+    CK(cudaMemsetAsync(ctx->y + n, 0, 8 * (pad + 1), st));
+    CK(cudaMemsetAsync(ctx->p + n, 0, 8 * pad, st));
+    CK(cudaMemsetAsync(ctx->scalars + 4, 0, 32, st));
+  }
   if (ctx->dist) {
     k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 0, ctx->scalars);
     CK(cudaGetLastError());
@@ -1071,6 +1108,8 @@ plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, 
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->started) { set_err(ctx, "plss_finish before plss_start"); return PLSS_E_STATE; }
   cudaStream_t st = ctx->stream;
+  if (ctx->rsag)                                    // x lives as column shards: gather (collective)
+    NK(ncclAllGather(ctx->x + ctx->c0, ctx->x, (size_t)ctx->cnt, ncclFloat64, ctx->comm, st));
   if (x && ctx->n > 0)
     CK(cudaMemcpyAsync(x, ctx->x, 8 * (size_t)ctx->n, is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -1220,6 +1259,21 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       else launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
       CK(cudaEventRecord(ev[q++], st));
     }
+    if (ctx->rsag) {                               // collectives (RS, AR, AG) | shard dots + tail | K3
+      double* sc = ctx->scalars + 4;
+      NK(ncclReduceScatter(ctx->y, ctx->y + ctx->c0, (size_t)ctx->cnt, ncclFloat64, ncclSum, ctx->comm, st));
+      NK(ncclAllReduce(sc, sc, 4, ncclFloat64, ncclSum, ctx->comm, st));
+      NK(ncclAllGather(ctx->p + ctx->c0, ctx->p, (size_t)ctx->cnt, ncclFloat64, ctx->comm, st));
+      CK(cudaEventRecord(ev[q++], st));
+      k_dots_shard<<<ctx->gdots, NT, 0, st>>>(ctx->y + ctx->c0, ctx->p + ctx->c0, ctx->nsh, ctx->ctl, ctx->part2,
+                                              ctx->counters + 1, ctx->wi ? ctx->wi + ctx->c0 : nullptr, sc);
+      k_tail_rsag<<<1, 1, 0, st>>>(ctx->ctl, ctx->rec, sc);
+      CK(cudaEventRecord(ev[q++], st));
+      k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p + ctx->c0, ctx->y + ctx->c0, ctx->x + ctx->c0, ctx->nsh, ctx->ctl,
+                                         ctx->rec, ctx->part3, ctx->counters + 2,
+                                         ctx->wi ? ctx->wi + ctx->c0 : nullptr, sc + 3);
+      CK(cudaEventRecord(ev[q++], st));
+    } else {
     if (ctx->dist) {
       NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
       CK(cudaEventRecord(ev[q++], st));
@@ -1230,6 +1284,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
     k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
                                        ctx->counters + 2, ctx->wi);
     CK(cudaEventRecord(ev[q++], st));
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     float t;
@@ -1269,7 +1324,8 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   // our kernels per loop step: K1 and K2 per slab (the last K2 as column chunks on a chunked
   // distributed ctx), K3, and the distributed dots / tail kernel
   if (launches_per_step)
-    *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0) + (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1);
+    *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0) + (ctx->rsag ? 1 : 0) +
+                         (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1);
   if (slabs) *slabs = ctx->S;
   if (tile_nnz) *tile_nnz = TILE;
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];

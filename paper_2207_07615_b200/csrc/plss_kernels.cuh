@@ -1362,10 +1362,12 @@ __global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double
 // ---------------------------------------------------------------------------------------------
 // K3: p <- beta p + gamma y; theta = p^T p; x <- x + p  (L811-813); init: p = gamma y (L795)
 // ---------------------------------------------------------------------------------------------
+// theta_out != NULL (the reduce-scatter distributed step, K3 on this rank's column shard): the
+// shard's p^T p goes there (summed across ranks with the next step's scalars) instead of c->theta
 __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
                                                  double* __restrict__ x, long long n, Ctl* c,
                                                  double* rec, double* partial, unsigned* counter,
-                                                 const double* __restrict__ wi) {
+                                                 const double* __restrict__ wi, double* theta_out = nullptr) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
   const bool wtd = wi != nullptr && c->weighted;       // theta = p^T (WI p) under PLSS W (L812)
@@ -1412,8 +1414,12 @@ __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const d
   }
   if (!publish_and_elect(acc, dummy, partial, partial, gridDim.x, counter, sm)) return;
   if (threadIdx.x != 0) return;
-  c->theta = acc;                                               // theta = p^T p (L812)
-  rec[(size_t)k * REC + 4] = acc;
+  if (theta_out) {
+    *theta_out = acc;                                           // shard partial of theta
+  } else {
+    c->theta = acc;                                             // theta = p^T p (L812)
+    rec[(size_t)k * REC + 4] = acc;
+  }
   c->iters = k + 1;
   if (k + 1 >= c->maxit) {
     c->done = 1;
@@ -1424,6 +1430,44 @@ __global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const d
 // ---------------------------------------------------------------------------------------------
 // distributed: phi, psi over the replicated (all-reduced) y, then both tails (K2b)
 // ---------------------------------------------------------------------------------------------
+// reduce-scatter distributed step: partials of phi = y^T (WI y) and psi = y^T p over this rank's
+// column shard (y <- WIy in place under PLSS W), into scal[1], scal[2] (scal[0] = the local rho
+// from K1, scal[3] = the shard's theta from the previous K3); then one all-reduce of scal[0..3]
+__global__ void __launch_bounds__(NT) k_dots_shard(double* __restrict__ y, const double* __restrict__ p,
+                                                   long long nsh, Ctl* c, double* partial, unsigned* counter,
+                                                   const double* __restrict__ wi, double* scal) {
+  __shared__ double sm[2][MAXW];
+  if (c->done) return;
+  const bool wtd = wi != nullptr && c->weighted;
+  double a0 = 0.0, a1 = 0.0;
+  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < nsh; i += (long long)gridDim.x * NT) {
+    const double yy = y[i];
+    if (wtd) {
+      const double wy = __ddiv_rn(yy, wi[i]);
+      y[i] = wy;
+      a0 = fma(yy, wy, a0);
+      a1 = fma(wy, p[i], a1);
+    } else {
+      a0 = fma(yy, yy, a0);
+      a1 = fma(yy, p[i], a1);
+    }
+  }
+  if (!publish_and_elect(a0, a1, partial, partial, gridDim.x, counter, sm)) return;
+  if (threadIdx.x == 0) { scal[1] = a0; scal[2] = a1; }
+}
+
+// the replicated scalar tails from the all-reduced scal = {rho, phi, psi, theta of p_{k-1}}
+__global__ void k_tail_rsag(Ctl* c, double* rec, const double* scal) {
+  if (c->done) return;
+  const int k = c->iters;
+  if (k > 0) {
+    c->theta = scal[3];
+    rec[(size_t)(k - 1) * REC + 4] = scal[3];
+  }
+  tail_rho(c, rec, scal[0]);
+  if (!c->done) tail_y(c, rec, scal[1], scal[2]);
+}
+
 __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const double* __restrict__ p,
                                                   long long n, const double* rho_g, Ctl* c,
                                                   double* rec, double* partial, unsigned* counter,

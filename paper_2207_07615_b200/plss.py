@@ -210,8 +210,9 @@ class Matrix:
                            1 if validate else 0)
 
 
-def _opts(slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True):
-    return plss_options(int(slabs), int(graph_chunk), int(maxit_cap), (0 if sell else 1) | (0 if window else 2))
+def _opts(slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True, rsag=False):
+    return plss_options(int(slabs), int(graph_chunk), int(maxit_cap),
+                        (0 if sell else 1) | (0 if window else 2) | (4 if rsag else 0))
 
 
 def plss_workspace_bytes(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True) -> int:
@@ -282,13 +283,14 @@ def plss_get_unique_id() -> bytes:
 
 def plss_create_dist(A_local: Matrix, row_offset: int, m_global: int, uid: bytes, rank: int, nranks: int,
                      slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False, sell=True,
-                     window=True) -> Ctx:
+                     window=True, rsag=False) -> Ctx:
+    """rsag: the reduce-scatter / all-gather step (include/plss.h, options.flags bit2)."""
     lib = load_library()
     nbytes = plss_workspace_bytes(A_local, slabs, graph_chunk, maxit_cap, sell, window)
     ws = _alloc_workspace(nbytes, A_local.row_ptr.device)
     h = ctypes.c_void_p()
     ms = A_local.c_struct(validate)
-    o = _opts(slabs, graph_chunk, maxit_cap, sell, window)
+    o = _opts(slabs, graph_chunk, maxit_cap, sell, window, rsag)
     _check(lib.plss_create_dist(ctypes.byref(ms), int(row_offset), int(m_global), uid, int(rank), int(nranks),
                                 ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream), ctypes.byref(h)))
     return Ctx(h, A_local, ws, stream, maxit_cap)

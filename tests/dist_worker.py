@@ -67,12 +67,70 @@ def gloo_solve(s, blk, dist, torch, maxit, chunks=1):
     return np.array(hist), x, iters
 
 
+def gloo_solve_rsag(s, blk, dist, torch, maxit):
+    """The reduce-scatter step's decomposition (plss.cu, options.flags bit2): y reduce-scattered to
+    column shards of cnt = 32-aligned ceil(n / G) (emulated: all-reduce, keep the shard -- gloo has
+    no reduce-scatter), phi / psi / theta as shard partials summed in ONE all-reduce of 4 scalars
+    with the local rho, K3 on the shard, p all-gathered, x gathered at the end."""
+    import oracle
+    n = s.n
+    G, g = dist.get_world_size(), dist.get_rank()
+    cnt = -(-n // G)
+    cnt = -(-cnt // 32) * 32
+    c0, c1 = g * cnt, min(n, (g + 1) * cnt)
+    r = blk["b"].copy()
+    nb2 = torch.tensor([float(r @ r)], dtype=torch.float64)
+    dist.all_reduce(nb2)
+    nbd = float(np.sqrt(nb2.item()))
+    p = np.zeros(G * cnt)
+    x = np.zeros(G * cnt)
+    hist, iters, theta_g = [], 0, 0.0
+    while True:
+        if iters > 0:
+            r = r - oracle.spmv(blk["m"], blk["row_ptr"], blk["col_idx"], blk["val"], p[:n])
+        yfull = torch.zeros(G * cnt, dtype=torch.float64)
+        yfull[:n] = torch.from_numpy(oracle.spmvT(n, blk["col_ptr"], blk["row_idx"], blk["val_t"], r))
+        dist.all_reduce(yfull)                           # = reduce-scatter, then keep the shard
+        ysh = yfull[c0:c1].numpy()
+        psh = p[c0:c1]
+        sc = torch.tensor([float(r @ r), float(ysh @ ysh), float(ysh @ psh), theta_g], dtype=torch.float64)
+        dist.all_reduce(sc)                              # the one scalar all-reduce
+        rho, phi, theta = float(sc[0]), float(sc[1]), float(sc[3])
+        h = np.sqrt(rho) / nbd
+        hist.append(h)
+        if rho == 0.0 or h <= s.tol:
+            break
+        if iters == 0:
+            pn = (rho / phi) * ysh
+        else:
+            tau = np.sqrt(theta * phi) / rho
+            beta = 1.0 / ((tau - 1.0) * (tau + 1.0))
+            gamma = (theta / rho) * beta
+            pn = beta * psh + gamma * ysh
+        theta_g = float(pn @ pn)
+        x[c0:c1] = x[c0:c1] + pn
+        shard = torch.zeros(cnt, dtype=torch.float64)
+        shard[:c1 - c0] = torch.from_numpy(pn)
+        parts = [torch.empty(cnt, dtype=torch.float64) for _ in range(G)]
+        dist.all_gather(parts, shard)                    # all-gather p
+        p = torch.cat(parts).numpy()
+        iters += 1
+        if iters >= maxit:
+            break
+    xs = torch.from_numpy(np.ascontiguousarray(x[c0:c0 + cnt]) if c1 > c0 else np.zeros(cnt))
+    xs = torch.cat([xs, torch.zeros(cnt - xs.numel(), dtype=torch.float64)]) if xs.numel() < cnt else xs
+    parts = [torch.empty(cnt, dtype=torch.float64) for _ in range(G)]
+    dist.all_gather(parts, xs)                           # x gathered at finish
+    return np.array(hist), torch.cat(parts).numpy()[:n], iters
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--backend", default="gloo")
     ap.add_argument("--out", required=True)
     ap.add_argument("--config", default="C2s")
     ap.add_argument("--chunks", type=int, default=1)
+    ap.add_argument("--rsag", action="store_true")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -89,7 +147,10 @@ def main():
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         assert isinstance(obj[0], bytes) and len(obj[0]) == 128
-        hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit, args.chunks)
+        if args.rsag:
+            hist, x, iters = gloo_solve_rsag(s, blk, dist, torch, s.maxit)
+        else:
+            hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit, args.chunks)
         for arr in (np.asarray(hist, dtype=np.float64), x):    # replicated decisions, bitwise (8e)
             t = torch.from_numpy(np.ascontiguousarray(arr))
             ts = [torch.empty_like(t) for _ in range(world)]

@@ -18,12 +18,12 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _run(world, cfg, tmp_path, chunks=1):
-    out = tmp_path / f"res_{world}_{chunks}.npz"
+def _run(world, cfg, tmp_path, chunks=1, rsag=False):
+    out = tmp_path / f"res_{world}_{chunks}_{int(rsag)}.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--backend", "gloo", "--out", str(out),
-           "--config", cfg, "--chunks", str(chunks)]
+           "--config", cfg, "--chunks", str(chunks)] + (["--rsag"] if rsag else [])
     env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1")
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env, capture_output=True)
     return np.load(out)
@@ -47,6 +47,18 @@ def test_row_blocks_world2_chunked_allreduce_bitwise(tmp_path):
     assert int(a["iters"]) == int(b["iters"])
     np.testing.assert_array_equal(a["hist"], b["hist"])
     np.testing.assert_array_equal(a["x"], b["x"])
+
+
+def test_row_blocks_world2_reduce_scatter_step(tmp_path):
+    """The reduce-scatter / all-gather decomposition (options.flags bit2) with two ranks: each owns
+    a 32-aligned column shard of y, p, x; the scalars are shard partials in one all-reduce."""
+    s = plss_gen.make_config("C2s")
+    ref = oracle.plss_system(s)
+    r = _run(2, "C2s", tmp_path, rsag=True)
+    assert abs(int(r["iters"]) - ref["iters"]) <= max(1, int(np.ceil(0.02 * ref["iters"])))
+    k = min(50, len(ref["hist"]))
+    assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+    assert np.linalg.norm(r["x"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
 
 
 def test_row_block_bounds_partition():

@@ -151,3 +151,50 @@ def test_dist_true_residual(pkg):
     ref = np.linalg.norm(s.b - oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x)) / np.linalg.norm(s.b)
     pkg.plss_destroy(ctx)
     assert abs(t["rel"] - ref) <= 1e-12
+
+
+@pytest.mark.parametrize("name,slabs,weighted,x0", [("C2s", 1, False, False), ("C5xs", 2, False, False),
+                                                   ("C4xs", 2, False, False), ("C2s", 2, True, False),
+                                                   ("C3_64", 1, False, True)])
+def test_dist_reduce_scatter_step(pkg, name, slabs, weighted, x0):
+    """options.flags bit2 (the reduce-scatter / all-gather step, SURVEY 8e improvement 2) on a
+    single rank: parity with the oracle (the shard is the whole vector; the dots are shard partials
+    summed by the all-reduce), and agreement with the all-reduce step over the live iterations."""
+    s = plss_gen.make_config("C3", N=64) if name == "C3_64" else plss_gen.make_config(name)
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    xin = np.random.default_rng(3).standard_normal(s.n) if x0 else None
+    out = {}
+    for rsag in (True, False):
+        ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=slabs, maxit_cap=s.maxit,
+                                   rsag=rsag, validate=True)
+        wi = None
+        if weighted:
+            wi = pkg.plss_column_norms(ctx)
+            pkg.plss_set_wi(ctx, wi)
+        res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), None if xin is None else torch.from_numpy(xin).cuda(),
+                             tol=s.tol, maxit=s.maxit, flags=1 if s.freeze else 0)
+        res["xh"] = res["x"].cpu().numpy()
+        out[rsag] = (res, None if wi is None else wi.cpu().numpy())
+        pkg.plss_destroy(ctx)
+    res, wih = out[True]
+    ref = oracle.plss_system(s, x0=xin, wi=wih)
+    from test_gpu_parity import _assert_parity, _floor
+    _assert_parity(res, ref, _floor(s, ref, x0=xin), s)
+    h1, h0 = res["hist"], out[False][0]["hist"]
+    k = min(len(h1), len(h0), 25)
+    live = h0[:k] > 1e-10
+    assert np.max(np.abs(h1[:k] - h0[:k])[live] / h0[:k][live]) <= 1e-10
+
+
+def test_reduce_scatter_needs_dist(pkg):
+    s = plss_gen.make_config("C2s")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    import ctypes
+    lib = pkg.load_library()
+    from paper_2207_07615_b200.plss import _opts, _alloc_workspace, _aligned
+    ms = A.c_struct()
+    o = _opts(rsag=True)
+    nbytes = pkg.plss_workspace_bytes(A)
+    ws = _alloc_workspace(nbytes, "cuda")
+    h = ctypes.c_void_p()
+    assert lib.plss_create(ctypes.byref(ms), ctypes.byref(o), _aligned(ws), nbytes, None, ctypes.byref(h)) != 0
