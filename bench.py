@@ -266,9 +266,13 @@ def main():
     ap.add_argument("--plss-w", action="store_true",
                     help="PLSS W: WI = diag(||A_{:,j}||) (the paper's second variant; default PLSS, WI = I)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--dist-step", default="allreduce", choices=["allreduce", "rsag"],
-                    help="N > 1: allreduce = one all-reduce of n+1 values, overlapped with K2 in column chunks; "
-                         "rsag = reduce-scatter y, shard dots / K3, all-reduce 4 scalars, all-gather p")
+    ap.add_argument("--dist-step", default="allreduce", choices=["allreduce", "rsag", "peer"],
+                    help="N > 1: allreduce = one NCCL all-reduce of n+1 values, overlapped with K2 in column chunks; "
+                         "rsag = reduce-scatter y, shard dots / K3, all-reduce 4 scalars, all-gather p; "
+                         "peer = the library's own peer-memory all-reduce kernels (NVLink loads / stores), "
+                         "overlapped with K2 in column chunks")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="N = 1: run the distributed ctx on one rank (measures the dist step's own cost)")
     ap.add_argument("--rhs", default="xstar", choices=["xstar", "paper"],
                     help="paper: the paper's protocol right-hand side x = ones, x(1) = 10, b = A x (P:L987), "
                          "a labelled protocol-fidelity variant (SURVEY 8d)")
@@ -326,14 +330,15 @@ def main():
     A = pkg.Matrix(m_l, n, w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])
     stream = torch.cuda.Stream(device=dev)
     maxit_cap = args.warmup + args.steps + max(args.profile_steps, 1) + 8
-    if world > 1:
+    if world > 1 or args.force_dist:
         uid = pkg.plss_get_unique_id() if rank == 0 else bytes(128)
         obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
         ctx = pkg.plss_create_dist(A, w["row_offset"], w["m_global"], obj[0], rank, world,
                                    slabs=args.slabs, maxit_cap=maxit_cap, stream=stream,
                                    sell=not args.no_sell, window=not args.no_window,
-                                   rsag=args.dist_step == "rsag")
+                                   rsag=args.dist_step == "rsag", peer=args.dist_step == "peer")
     else:
         ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=maxit_cap, stream=stream, sell=not args.no_sell,
                               window=not args.no_window)
@@ -414,7 +419,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_label(w["name"]), "m": w["m_global"], "n": n,
                        "nnz": w["nnz_global"],
-                       "parallelism": (f"row-block dp{world} ({args.dist_step})" if world > 1 else "single"),
+                       "parallelism": (f"row-block dp{world} ({args.dist_step})" if world > 1 or args.force_dist
+                                       else "single"),
                        "slabs": q["slabs"], "sell_segments": q["sell_segments"],
                        "window_segments": q["window_segments"], "freeze_mode": True,
                        "tol": 0.0, "variant": "PLSS W (WI = diag(||A_:,j||))" if args.plss_w else "PLSS (WI = I)",

@@ -88,6 +88,15 @@ typedef struct {
                           reduce-scattered to column shards of n / nranks, phi / psi and K3 run
                           on the shard, one all-reduce carries {rho, phi, psi, theta}, p is
                           all-gathered; x is gathered by plss_finish (then collective);
+                          bit3 (distributed ctx only, <= 8 ranks, not with bit2): the
+                          peer-memory step (SURVEY 8(e) improvement 3) -- instead of
+                          ncclAllReduce, the library's own kernels sum y | rho over the ranks
+                          through NVLink peer memory: per K2 column chunk each rank sums its
+                          column shard of every rank's partial in rank order 0..G-1 and stores
+                          the sum into every rank's y, overlapped with the next chunk's K2.
+                          The ctx then also cudaMallocs 2 x 8(n+2) B + 1 KB of device memory
+                          (CUDA IPC needs an allocation base), and every rank's region is
+                          mapped by CUDA IPC at create (all ranks on one node);
                           other bits must be 0                                             */
 } plss_options;
 
@@ -163,6 +172,18 @@ plss_status plss_column_norms(plss_ctx *ctx, double *c);
  * v: dev n). Sums are sequential in ascending index order per output element. Synchronous. */
 plss_status plss_spmv(plss_ctx *ctx, const double *x, double *y);
 plss_status plss_spmvT(plss_ctx *ctx, const double *u, double *v);
+
+/* Test entry point of the peer-memory step (options.flags bit3): one step of its all-reduce over
+ * G <= 8 VIRTUAL ranks on the current device, the reduce kernels launched cooperatively with one
+ * grid row per virtual rank (their CTAs wait on one another). part[h], red[h]: device buffers of
+ * virtual rank h (its partial and its reduced vector, >= bounds[nch] doubles, 16-byte aligned);
+ * flags[h]: rank h's 256-word flag block (device, zeroed before the first call, then left to the
+ * library: it carries the step epoch across calls). Chunks c = [bounds[c], bounds[c+1]),
+ * 1 <= nch <= 8 (host array of nch + 1 non-decreasing offsets). After the call red[h][j] =
+ * ((part[0][j] + part[1][j]) + ...) + part[G-1][j] (binary64, rank order) for every h and every j
+ * in [bounds[0], bounds[nch]); nothing else is written. Synchronizes `cuda_stream`. */
+plss_status plss_peer_reduce_emulate(int32_t G, double *const *part, double *const *red, uint32_t *const *flags,
+                                     int32_t nch, const int64_t *bounds, void *cuda_stream);
 
 /* The true residual of an iterate (the solve stops on the recursive residual of
  * Algorithm 1; report the true one once at exit): out[0] = ||b - A x||_2, out[1] = ||b||_2 (host,

@@ -13,6 +13,7 @@
 #include "rp_kernels.cuh"
 #include "kz_kernels.cuh"
 #include "eg_kernels.cuh"
+#include "peer_kernels.cuh"
 
 #include <nccl.h>
 
@@ -31,6 +32,7 @@ namespace {
 
 constexpr int MAXG = 2048;           // upper bound on persistent-CTA grid sizes (partials)
 constexpr int DCH_MAX = 8;           // column chunks of the last K2 segment on a distributed ctx
+static_assert(DCH_MAX <= PEER_NCH, "peer flag blocks cover every chunk");
 constexpr int64_t DPAD = 64 * 32;    // vector slack for the reduce-scatter step (64 ranks x 32)
 constexpr int SCAN_ITEMS = 16;       // setup scan: items per thread
 constexpr size_t ALIGN = 256;
@@ -226,6 +228,17 @@ struct plss_ctx {
   int64_t cnt = 0, c0 = 0, nsh = 0;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  // peer-memory all-reduce (options.flags bit3, peer_kernels.cuh): a region the library allocates
+  // (cudaMalloc, so that CUDA IPC can map it) = [reduced y | rho][partial y | rho][flag block];
+  // y points at the partial (what K1 / K2 write), yred at the reduced vector (what the dots, the
+  // tails and K3 read); ptab holds every rank's region as mapped in this process
+  bool peer = false;
+  char* sym = nullptr;
+  size_t sym_yb = 0;
+  double* yred = nullptr;
+  PeerTab ptab{};
+  std::vector<void*> ipc_open;
+  int peer_gx = 1;
   // solve state
   bool started = false;
   int maxit = 0, flags = 0;
@@ -309,6 +322,21 @@ static int grid_for(int64_t work_units, int occ_per_sm, int sms) {
   return (int)std::max<int64_t>(1, g);
 }
 
+// peer-memory reduce of chunk c = elements [lo, hi) of y | rho (this rank's shard, to every rank)
+static void peer_reduce(plss_ctx* ctx, int c, int64_t lo, int64_t hi, cudaStream_t s) {
+  k_peer_reduce<<<dim3(ctx->peer_gx, 1), PEER_NT, 0, s>>>(ctx->ptab, ctx->nranks, ctx->rank, c, (long long)lo,
+                                                          (long long)hi, ctx->ctl);
+}
+static int peer_nch(const plss_ctx* ctx) { return ctx->dch.empty() ? 1 : (int)ctx->dch.size(); }
+// all chunks, in order, on one stream (unchunked step, plss_profile)
+static void peer_reduce_all(plss_ctx* ctx, cudaStream_t s) {
+  if (ctx->dch.empty()) {
+    peer_reduce(ctx, 0, 0, ctx->n + 1, s);
+  } else {
+    for (int c = 0; c < (int)ctx->dch.size(); ++c) peer_reduce(ctx, c, ctx->drows[c], ctx->drows[c + 1], s);
+  }
+}
+
 // enqueue one loop step (also used inside graph capture)
 static plss_status enqueue_step(plss_ctx* ctx) {
   cudaStream_t st = ctx->stream;
@@ -321,8 +349,11 @@ static plss_status enqueue_step(plss_ctx* ctx) {
         launch_spmv<ROLE_K2>(ctx->dch[c], ctx->gch[c], st);
         CK(cudaEventRecord(ctx->ev_ch[c], st));
         CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ch[c], 0));
-        NK(ncclAllReduce(ctx->y + ctx->drows[c], ctx->y + ctx->drows[c], (size_t)(ctx->drows[c + 1] - ctx->drows[c]),
-                         ncclFloat64, ncclSum, ctx->comm, ctx->comm_stream));
+        if (ctx->peer)
+          peer_reduce(ctx, (int)c, ctx->drows[c], ctx->drows[c + 1], ctx->comm_stream);
+        else
+          NK(ncclAllReduce(ctx->y + ctx->drows[c], ctx->y + ctx->drows[c], (size_t)(ctx->drows[c + 1] - ctx->drows[c]),
+                           ncclFloat64, ncclSum, ctx->comm, ctx->comm_stream));
       }
       CK(cudaEventRecord(ctx->ev_join, ctx->comm_stream));
       CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
@@ -347,12 +378,19 @@ static plss_status enqueue_step(plss_ctx* ctx) {
     CK(cudaGetLastError());
     return PLSS_OK;
   }
+  double* yv = ctx->y;
   if (ctx->dist) {
-    if (!chunked) NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
-    k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
+    if (ctx->peer) {
+      if (!chunked) peer_reduce(ctx, 0, 0, ctx->n + 1, st);
+      k_peer_wait<<<1, 64, 0, st>>>(ctx->ptab, ctx->nranks, peer_nch(ctx), ctx->rank, ctx->ctl);
+      yv = ctx->yred;
+    } else if (!chunked) {
+      NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
+    }
+    k_dots_tail<<<ctx->gdots, NT, 0, st>>>(yv, ctx->p, ctx->n, yv + ctx->n, ctx->ctl, ctx->rec,
                                            ctx->part2, ctx->counters + 1, ctx->wi);
   }
-  k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
+  k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
                                      ctx->counters + 2, ctx->wi);
   CK(cudaGetLastError());
   return PLSS_OK;
@@ -694,7 +732,13 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (!A->row_ptr || !A->col_ptr || (A->nnz > 0 && (!A->col_idx || !A->val || !A->row_idx || !A->val_t))) {
     set_err(ctx, "NULL matrix array"); return PLSS_E_INVALID;
   }
-  if (opt && (opt->flags & ~7) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & ~15) != 0) { set_err(ctx, "unknown options.flags bits"); return PLSS_E_INVALID; }
+  if (opt && (opt->flags & 8)) {
+    if (!dist) { set_err(ctx, "options.flags bit3 needs a distributed ctx"); return PLSS_E_INVALID; }
+    if (opt->flags & 4) { set_err(ctx, "options.flags bit2 and bit3 are exclusive"); return PLSS_E_INVALID; }
+    if (ctx->nranks > PEER_MAX) { set_err(ctx, "peer-memory step: at most 8 ranks"); return PLSS_E_INVALID; }
+    ctx->peer = true;
+  }
   if (opt && (opt->flags & 4) && !dist) { set_err(ctx, "options.flags bit2 needs a distributed ctx"); return PLSS_E_INVALID; }
   if (opt && (opt->flags & 4) && ctx->nranks > 64) { set_err(ctx, "reduce-scatter step: at most 64 ranks"); return PLSS_E_INVALID; }
   if (dist && opt && (opt->flags & 4)) {
@@ -738,6 +782,14 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   ctx->scalars = (double*)(w + L.scalars);
   ctx->wi = (double*)(w + L.wi);
   int* d_err = (int*)(w + L.err);
+  if (ctx->peer) {
+    ctx->sym_yb = align_up(8 * (size_t)(A->n + 2));
+    const size_t bytes = 2 * ctx->sym_yb + 4 * (size_t)PF_WORDS;
+    CK(cudaMalloc((void**)&ctx->sym, bytes));
+    CK(cudaMemsetAsync(ctx->sym, 0, bytes, ctx->stream ? ctx->stream : nullptr));
+    ctx->yred = (double*)ctx->sym;
+    ctx->y = (double*)(ctx->sym + ctx->sym_yb);
+  }
   CK(cudaMemsetAsync(ctx->counters, 0, 64 * sizeof(unsigned), st));
   CK(cudaMemsetAsync(ctx->part1, 0, 16 * (size_t)MAXG * L.S, st));
   CK(cudaMemsetAsync(ctx->part2, 0, 16 * (size_t)MAXG, st));
@@ -969,6 +1021,47 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   return PLSS_OK;
 }
 
+// peer-memory step: map every rank's region (CUDA IPC handles, all-gathered over the ctx's own
+// communicator) and size the reduce grid
+static plss_status peer_connect(plss_ctx* ctx) {
+  const int G = ctx->nranks;
+  cudaStream_t st = ctx->stream;
+  std::vector<cudaIpcMemHandle_t> hs(G);
+  if (G > 1) {
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    CK(cudaIpcGetMemHandle(&hs[ctx->rank], ctx->sym));
+    char* d = nullptr;
+    CK(cudaMallocAsync((void**)&d, hb * G, st));
+    CK(cudaMemcpyAsync(d + hb * ctx->rank, &hs[ctx->rank], hb, cudaMemcpyHostToDevice, st));
+    NK(ncclAllGather(d + hb * ctx->rank, d, hb, ncclUint8, ctx->comm, st));
+    CK(cudaMemcpyAsync(hs.data(), d, hb * G, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  for (int h = 0; h < G; ++h) {
+    char* base = ctx->sym;
+    if (h != ctx->rank) {
+      void* q = nullptr;
+      CK(cudaIpcOpenMemHandle(&q, hs[h], cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_open.push_back(q);
+      base = (char*)q;
+    }
+    ctx->ptab.red[h] = (double*)base;
+    ctx->ptab.part[h] = (const double*)(base + ctx->sym_yb);
+    ctx->ptab.flg[h] = (unsigned*)(base + 2 * ctx->sym_yb);
+  }
+  int sms = 1;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+  const int64_t per = (ctx->n + 1) / peer_nch(ctx) / G + 2;              // shard of a chunk
+  int occ = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_peer_reduce, PEER_NT, 0));
+  const int cap = std::max(1, occ) * sms;                              // co-resident (see k_peer_reduce)
+  const int gx = env_int("PLSS_PEER_GX", 0);
+  ctx->peer_gx = gx > 0 ? std::min(gx, cap)
+                        : (int)std::max<int64_t>(1, std::min<int64_t>((per / 4 + PEER_NT - 1) / PEER_NT, cap));
+  return PLSS_OK;
+}
+
 static plss_status finish_create(plss_ctx* ctx) {
   // graphs are captured after setup so their nodes carry the final kernel parameters
   // (the device state they read is reset by plss_start); capture does not execute kernels
@@ -1029,6 +1122,7 @@ plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int
     ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, u, rank);
     if (r != ncclSuccess) { set_err(ctx, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); st = PLSS_E_NCCL; }
   }
+  if (st == PLSS_OK && ctx->peer) st = peer_connect(ctx);
   if (st == PLSS_OK) st = finish_create(ctx);
   if (st != PLSS_OK) { g_last_error = ctx->err; plss_destroy(ctx); return st; }
   *out = ctx;
@@ -1118,8 +1212,12 @@ plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, 
     rec.resize((size_t)(ctx->maxit + 1) * REC);
     CK(cudaMemcpyAsync(rec.data(), ctx->rec, 8 * rec.size(), cudaMemcpyDeviceToHost, st));
   }
+  unsigned peer_err = 0;
+  if (ctx->peer)
+    CK(cudaMemcpyAsync(&peer_err, ctx->ptab.flg[ctx->rank] + PF_ERR, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (sync_out(ctx) != PLSS_OK) return PLSS_E_CUDA;
+  if (peer_err) { set_err(ctx, "peer-memory step: a rank did not arrive within 20 s"); return PLSS_E_CUDA; }
   const Ctl& c = *ctx->h_ctl;
   if (iters) *iters = c.iters;
   if (outcome) *outcome = c.done ? (plss_outcome)c.outcome : PLSS_RUNNING;
@@ -1274,14 +1372,21 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
                                          ctx->wi ? ctx->wi + ctx->c0 : nullptr, sc + 3);
       CK(cudaEventRecord(ev[q++], st));
     } else {
+    double* yv = ctx->y;
     if (ctx->dist) {
-      NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
+      if (ctx->peer) {                             // peer reduce of every chunk + wait
+        peer_reduce_all(ctx, st);
+        k_peer_wait<<<1, 64, 0, st>>>(ctx->ptab, ctx->nranks, peer_nch(ctx), ctx->rank, ctx->ctl);
+        yv = ctx->yred;
+      } else {
+        NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
+      }
       CK(cudaEventRecord(ev[q++], st));
-      k_dots_tail<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->y + ctx->n, ctx->ctl, ctx->rec,
+      k_dots_tail<<<ctx->gdots, NT, 0, st>>>(yv, ctx->p, ctx->n, yv + ctx->n, ctx->ctl, ctx->rec,
                                              ctx->part2, ctx->counters + 1, ctx->wi);
       CK(cudaEventRecord(ev[q++], st));
     }
-    k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
+    k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
                                        ctx->counters + 2, ctx->wi);
     CK(cudaEventRecord(ev[q++], st));
     }
@@ -1325,7 +1430,8 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   // distributed ctx), K3, and the distributed dots / tail kernel
   if (launches_per_step)
     *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0) + (ctx->rsag ? 1 : 0) +
-                         (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1);
+                         (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1) +
+                         (ctx->peer ? peer_nch(ctx) + 1 : 0);
   if (slabs) *slabs = ctx->S;
   if (tile_nnz) *tile_nnz = TILE;
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];
@@ -2131,6 +2237,8 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->kz_graph_one) cudaGraphExecDestroy(ctx->kz_graph_one);
   if (ctx->eg_graph_chunk) cudaGraphExecDestroy(ctx->eg_graph_chunk);
   if (ctx->eg_graph_one) cudaGraphExecDestroy(ctx->eg_graph_one);
+  for (void* q : ctx->ipc_open) cudaIpcCloseMemHandle(q);
+  if (ctx->sym) cudaFree(ctx->sym);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& e : ctx->ev_ch) if (e) cudaEventDestroy(e);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -2161,6 +2269,57 @@ const char* plss_status_str(plss_status s) {
 const char* plss_last_error(const plss_ctx* ctx) {
   if (ctx) return ctx->err.c_str();
   return g_last_error.c_str();
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// test entry point: one step of the peer-memory all-reduce over G virtual ranks on this device
+// (peer_kernels.cuh: the kernels of the distributed step, launched cooperatively with one grid row
+// per virtual rank, since their CTAs wait on one another)
+plss_status plss_peer_reduce_emulate(int32_t G, double* const* part, double* const* red, uint32_t* const* flags,
+                                     int32_t nch, const int64_t* bounds, void* cuda_stream) {
+  if (G < 1 || G > PEER_MAX || nch < 1 || nch > PEER_NCH || !part || !red || !flags || !bounds) {
+    g_last_error = "invalid argument";
+    return PLSS_E_INVALID;
+  }
+  for (int c = 0; c < nch; ++c)
+    if (bounds[c] < 0 || bounds[c + 1] < bounds[c]) { g_last_error = "bounds must be non-decreasing"; return PLSS_E_INVALID; }
+  PeerTab t{};
+  for (int h = 0; h < G; ++h) {
+    if (!part[h] || !red[h] || !flags[h]) { g_last_error = "NULL buffer"; return PLSS_E_INVALID; }
+    t.part[h] = part[h];
+    t.red[h] = red[h];
+    t.flg[h] = flags[h];
+  }
+  int dev = 0, sms = 1, occ = 1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_peer_reduce, PEER_NT, 0);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  int gx = std::max(1, std::min(16, occ * sms / G));
+  int zero = 0;
+  const Ctl* noctl = nullptr;
+  for (int c = 0; c < nch && e == cudaSuccess; ++c) {
+    long long lo = bounds[c], hi = bounds[c + 1];
+    void* args[] = {&t, &G, &zero, &c, &lo, &hi, &noctl};
+    e = cudaLaunchCooperativeKernel((const void*)k_peer_reduce, dim3(gx, G), dim3(PEER_NT), args, 0, s);
+  }
+  if (e == cudaSuccess) {
+    void* args[] = {&t, &G, &nch, &zero, &noctl};
+    e = cudaLaunchCooperativeKernel((const void*)k_peer_wait, dim3(1, G), dim3(64), args, 0, s);
+  }
+  unsigned err = 0;
+  for (int h = 0; h < G && e == cudaSuccess; ++h) {
+    unsigned v = 0;
+    e = cudaMemcpyAsync(&v, flags[h] + PF_ERR, sizeof v, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    err |= v;
+  }
+  if (e != cudaSuccess) { g_last_error = cudaGetErrorString(e); return PLSS_E_CUDA; }
+  if (err) { g_last_error = "peer-memory step: a virtual rank did not arrive within 20 s"; return PLSS_E_CUDA; }
+  return PLSS_OK;
 }
 
 }  // extern "C"

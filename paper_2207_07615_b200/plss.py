@@ -30,7 +30,7 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile",
            "plss_kz_workspace_bytes", "plss_kz_solve", "plss_kz_start", "plss_kz_step", "plss_kz_finish",
            "plss_kz_profile", "plss_eg_workspace_bytes", "plss_eg_solve", "plss_eg_start", "plss_eg_step",
-           "plss_eg_finish", "plss_eg_profile", "plss_true_residual"]
+           "plss_eg_finish", "plss_eg_profile", "plss_true_residual", "plss_peer_reduce_emulate"]
 
 
 class PlssError(RuntimeError):
@@ -144,6 +144,8 @@ def load_library(path: str = None):
     lib.plss_eg_profile.restype = st
     lib.plss_true_residual.argtypes = [P, P, P, P]
     lib.plss_true_residual.restype = st
+    lib.plss_peer_reduce_emulate.argtypes = [I32, P, P, P, I32, P, P]
+    lib.plss_peer_reduce_emulate.restype = st
     lib.plss_destroy.argtypes = [P]
     lib.plss_destroy.restype = None
     lib.plss_status_str.argtypes = [st]
@@ -210,9 +212,9 @@ class Matrix:
                            1 if validate else 0)
 
 
-def _opts(slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True, rsag=False):
+def _opts(slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True, rsag=False, peer=False):
     return plss_options(int(slabs), int(graph_chunk), int(maxit_cap),
-                        (0 if sell else 1) | (0 if window else 2) | (4 if rsag else 0))
+                        (0 if sell else 1) | (0 if window else 2) | (4 if rsag else 0) | (8 if peer else 0))
 
 
 def plss_workspace_bytes(A: Matrix, slabs=0, graph_chunk=0, maxit_cap=0, sell=True, window=True) -> int:
@@ -283,14 +285,15 @@ def plss_get_unique_id() -> bytes:
 
 def plss_create_dist(A_local: Matrix, row_offset: int, m_global: int, uid: bytes, rank: int, nranks: int,
                      slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False, sell=True,
-                     window=True, rsag=False) -> Ctx:
-    """rsag: the reduce-scatter / all-gather step (include/plss.h, options.flags bit2)."""
+                     window=True, rsag=False, peer=False) -> Ctx:
+    """rsag: the reduce-scatter / all-gather step (include/plss.h, options.flags bit2); peer: the
+    peer-memory all-reduce step (options.flags bit3)."""
     lib = load_library()
     nbytes = plss_workspace_bytes(A_local, slabs, graph_chunk, maxit_cap, sell, window)
     ws = _alloc_workspace(nbytes, A_local.row_ptr.device)
     h = ctypes.c_void_p()
     ms = A_local.c_struct(validate)
-    o = _opts(slabs, graph_chunk, maxit_cap, sell, window, rsag)
+    o = _opts(slabs, graph_chunk, maxit_cap, sell, window, rsag, peer)
     _check(lib.plss_create_dist(ctypes.byref(ms), int(row_offset), int(m_global), uid, int(rank), int(nranks),
                                 ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream), ctypes.byref(h)))
     return Ctx(h, A_local, ws, stream, maxit_cap)
@@ -373,6 +376,20 @@ def plss_true_residual(ctx: Ctx, b, x) -> dict:
     _check(load_library().plss_true_residual(ctx.handle, _ptr(b), _ptr(x), _ptr(out)), ctx.handle)
     return {"abs": float(out[0]), "norm_b": float(out[1]),
             "rel": float(out[0] / out[1]) if out[1] > 0 else float(out[0])}
+
+
+def plss_peer_reduce_emulate(parts, reds, flags, bounds, stream=None):
+    """One step of the peer-memory all-reduce over len(parts) virtual ranks on one device
+    (include/plss.h): parts / reds float64 device tensors, flags int32 device tensors of 256 words
+    (zeroed before the first step, then kept), bounds the nch + 1 chunk offsets."""
+    G = len(parts)
+    if not (len(reds) == len(flags) == G):
+        raise PlssError("parts, reds and flags need one buffer per virtual rank")
+    arr = lambda ts: (ctypes.c_void_p * G)(*[t.data_ptr() for t in ts])  # noqa: E731
+    b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    _check(load_library().plss_peer_reduce_emulate(int(G), arr(parts), arr(reds), arr(flags), int(len(b) - 1),
+                                                   b.ctypes.data, _stream_ptr(stream)))
+    return reds
 
 
 def plss_spmv(ctx: Ctx, x, y):
