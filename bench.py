@@ -151,9 +151,22 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------------------------
-def load_workload(name, rank, world, device):
-    """Returns dict of device tensors for this rank's row block + metadata."""
+def load_workload(name, rank, world, device, partition="rows"):
+    """Returns dict of device tensors for this rank's row block (or column block) + metadata."""
     import torch
+    if partition == "cols":
+        if name == "C5":
+            raise SystemExit("--partition cols: C5 (m > n) is a row-block workload; use C4 / C4alt / C2")
+        s = plss_gen.make_config(name)
+        blk = plss_gen.col_block(s, world, rank)
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)  # noqa: E731
+        return {"name": name, "m": s.m, "n": blk["n"], "n_global": s.n, "col_offset": blk["col_offset"],
+                "row_offset": 0, "m_global": s.m,
+                "row_ptr": t(blk["row_ptr"], torch.int32), "col_idx": t(blk["col_idx"], torch.int32),
+                "val": t(blk["val"], torch.float64), "col_ptr": t(blk["col_ptr"], torch.int32),
+                "row_idx": t(blk["row_idx"], torch.int32), "val_t": t(blk["val_t"], torch.float64),
+                "b": t(blk["b"], torch.float64), "tol": 0.0, "tol_mode": 0, "freeze": True,
+                "nnz_global": s.nnz}
     if name == "C5":
         m, n = 64_000_000, 8_000_000
         r0, r1 = plss_gen.row_block_bounds(m, world, rank)
@@ -271,6 +284,9 @@ def main():
                          "rsag = reduce-scatter y, shard dots / K3, all-reduce 4 scalars, all-gather p; "
                          "peer = the library's own peer-memory all-reduce kernels (NVLink loads / stores), "
                          "overlapped with K2 in column chunks")
+    ap.add_argument("--partition", default="rows", choices=["rows", "cols"],
+                    help="distributed partition: row blocks (x, p, y replicated; all-reduce of n + 1) or "
+                         "column blocks (r replicated; all-reduces of m + 1 and 2), for m < n")
     ap.add_argument("--force-dist", action="store_true",
                     help="N = 1: run the distributed ctx on one rank (measures the dist step's own cost)")
     ap.add_argument("--rhs", default="xstar", choices=["xstar", "paper"],
@@ -324,7 +340,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    w = load_workload(args.workload, rank, world, dev)
+    w = load_workload(args.workload, rank, world, dev, args.partition)
     m_l, n = w["m"], w["n"]
     nnz_l = int(w["col_idx"].numel())
     A = pkg.Matrix(m_l, n, w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])
@@ -335,10 +351,15 @@ def main():
         obj = [uid]
         if world > 1:
             dist.broadcast_object_list(obj, src=0)
-        ctx = pkg.plss_create_dist(A, w["row_offset"], w["m_global"], obj[0], rank, world,
-                                   slabs=args.slabs, maxit_cap=maxit_cap, stream=stream,
-                                   sell=not args.no_sell, window=not args.no_window,
-                                   rsag=args.dist_step == "rsag", peer=args.dist_step == "peer")
+        if args.partition == "cols":
+            ctx = pkg.plss_create_dist_cols(A, w["col_offset"], w["n_global"], obj[0], rank, world,
+                                            slabs=args.slabs, maxit_cap=maxit_cap, stream=stream,
+                                            sell=not args.no_sell, window=not args.no_window)
+        else:
+            ctx = pkg.plss_create_dist(A, w["row_offset"], w["m_global"], obj[0], rank, world,
+                                       slabs=args.slabs, maxit_cap=maxit_cap, stream=stream,
+                                       sell=not args.no_sell, window=not args.no_window,
+                                       rsag=args.dist_step == "rsag", peer=args.dist_step == "peer")
     else:
         ctx = pkg.plss_create(A, slabs=args.slabs, maxit_cap=maxit_cap, stream=stream, sell=not args.no_sell,
                               window=not args.no_window)
@@ -373,7 +394,8 @@ def main():
         ms = float(t.item())
     fin = pkg.plss_finish(ctx, None, want_hist=True)
     iters_per_s = args.steps / (ms / 1e3)
-    B_global = plss_gen.bytes_per_iter(w["m_global"], n, w["nnz_global"])
+    n_global = w.get("n_global", n)
+    B_global = plss_gen.bytes_per_iter(w["m_global"], n_global, w["nnz_global"])
     if args.ncu:
         if rank == 0:
             print(json.dumps({"ncu_run": True, "ms_per_step": ms / args.steps}), flush=True)
@@ -417,9 +439,11 @@ def main():
             "metric": METRIC, "value": iters_per_s, "unit": "it/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_label(w["name"]), "m": w["m_global"], "n": n,
+            "config": {"workload": workload_label(w["name"]), "m": w["m_global"], "n": n_global,
                        "nnz": w["nnz_global"],
-                       "parallelism": (f"row-block dp{world} ({args.dist_step})" if world > 1 or args.force_dist
+                       "parallelism": (f"column-block dp{world}" if args.partition == "cols" and
+                                       (world > 1 or args.force_dist)
+                                       else f"row-block dp{world} ({args.dist_step})" if world > 1 or args.force_dist
                                        else "single"),
                        "slabs": q["slabs"], "sell_segments": q["sell_segments"],
                        "window_segments": q["window_segments"], "freeze_mode": True,

@@ -126,6 +126,25 @@ plss_status plss_create_dist(const plss_matrix *A_local, int64_t row_offset, int
                              const plss_options *opt, void *workspace, size_t ws_bytes,
                              void *cuda_stream, plss_ctx **out);
 
+/* Distributed column-block ctx ("column-block alternative", for m < n): this rank owns
+ * columns [col_offset, col_offset + A_local->n) of a global m x n_global matrix. A_local is that
+ * column block as an m x n_local matrix: CSR over LOCAL column indices (global column - col_offset)
+ * and the CSC of its columns (row indices global, 0..m-1). r (m) is replicated; x, p, y are this
+ * rank's column shards. Per iteration: K1 computes u <- u - A_g p_g (u = r on rank 0, u = 0 on the
+ * others), one ncclAllReduce of m+1 values (u and the previous K3's theta partial) gives every
+ * rank r = r - A p; rho = r^T r, the stop test and the rho tail run replicated; K2 forms y_g =
+ * A_g^T r over the local columns; phi, psi partials go through an ncclAllReduce of 2 values; K3
+ * updates the shard. Messages are m+1 and 2 doubles instead of n+1 (C4: 2M vs 8M).
+ * In this mode: plss_start / plss_solve take the full b (m, the same on every rank) and x0 / x as
+ * this rank's shard (n_local); plss_column_norms gives the local columns' norms (whole columns, no
+ * collective); plss_set_wi takes the local shard; plss_spmv / plss_spmvT are the local products
+ * A_g x_g and A_g^T u; plss_true_residual takes the full b and the local x shard (collective).
+ * options.flags bit2 / bit3 are rejected (E_INVALID). Collective. Errors: as plss_create_dist. */
+plss_status plss_create_dist_cols(const plss_matrix *A_local, int64_t col_offset, int64_t n_global,
+                                  const uint8_t id[128], int32_t rank, int32_t nranks,
+                                  const plss_options *opt, void *workspace, size_t ws_bytes,
+                                  void *cuda_stream, plss_ctx **out);
+
 /* Full solve = plss_start + plss_step until done + plss_finish.
  *  b      : host or dev, m (local rows on a rank) doubles.
  *  x0     : host or dev, n doubles, or NULL for x0 = 0.

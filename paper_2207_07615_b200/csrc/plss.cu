@@ -81,7 +81,7 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   const int64_t tiles2 = nnz / TILE + S * (n / RCAP) + 2 * S + 2; // K2 tile descriptors
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o2 = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o2; };
-  L->r = take(8 * m);
+  L->r = take(8 * (m + 2));          // r[m]: theta partial of the column-block step
   // dist: y | rho (the all-reduce buffer); DPAD slack lets the reduce-scatter step pad y, p, x to
   // nranks x (32-aligned shard) doubles for up to 64 ranks
   L->y = take(8 * (n + 1 + DPAD));
@@ -139,7 +139,7 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   L->buf = L->y;
   L->wi = take(8 * (size_t)(n + 1));   // PLSS W: the diagonal of WI (16-byte reads in K3)
   L->err = take(64);
-  L->scalars = take(64);
+  L->scalars = take(128);
   L->total = off;
   return true;
 }
@@ -232,6 +232,10 @@ struct plss_ctx {
   // (cudaMalloc, so that CUDA IPC can map it) = [reduced y | rho][partial y | rho][flag block];
   // y points at the partial (what K1 / K2 write), yred at the reduced vector (what the dots, the
   // tails and K3 read); ptab holds every rank's region as mapped in this process
+  // column blocks (plss_create_dist_cols): this rank owns columns [col_offset, col_offset + n) of
+  // an m x n_global matrix; r (m) is replicated, x / p / y are this rank's column shards
+  bool cols = false;
+  int64_t col_offset = 0, n_global = 0;
   bool peer = false;
   char* sym = nullptr;
   size_t sym_yb = 0;
@@ -337,8 +341,31 @@ static void peer_reduce_all(plss_ctx* ctx, cudaStream_t s) {
   }
 }
 
+// column-block step: K1 (u <- u - A_g p_g; u = r on rank 0, 0 elsewhere), all-reduce of u | theta_g,
+// rho tail, K2 (y_g = A_g^T r), phi / psi partials, all-reduce of 2 scalars, y tail, K3 on the
+// shard (theta_g into r[m] for the next all-reduce), ranks > 0 zero u again
+static plss_status enqueue_step_cols(plss_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  const int64_t m = ctx->m;
+  double* sc = ctx->scalars + 4;
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
+  NK(ncclAllReduce(ctx->r, ctx->r, (size_t)m + 1, ncclFloat64, ncclSum, ctx->comm, st));
+  k_rho_tail<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->rec, ctx->partn, ctx->counters + 3);
+  for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
+  k_dots_shard<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->ctl, ctx->part2, ctx->counters + 1,
+                                          ctx->wi, sc);
+  NK(ncclAllReduce(sc + 1, sc + 1, 2, ncclFloat64, ncclSum, ctx->comm, st));
+  k_tail_phi<<<1, 1, 0, st>>>(ctx->ctl, ctx->rec, sc);
+  k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
+                                     ctx->counters + 2, ctx->wi, ctx->r + m);
+  if (ctx->rank > 0 && m > 0) CK(cudaMemsetAsync(ctx->r, 0, 8 * (size_t)m, st));
+  CK(cudaGetLastError());
+  return PLSS_OK;
+}
+
 // enqueue one loop step (also used inside graph capture)
 static plss_status enqueue_step(plss_ctx* ctx) {
+  if (ctx->cols) return enqueue_step_cols(ctx);
   cudaStream_t st = ctx->stream;
   const bool chunked = ctx->dist && !ctx->dch.empty();
   for (int s = 0; s < ctx->S; ++s) {
@@ -928,7 +955,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.counter = ctx->counters + 0;
     a.ctl = ctx->ctl;
     a.rec = ctx->rec;
-    a.rho_out = ctx->rsag ? ctx->scalars + 4 : ctx->y + n;
+    a.rho_out = ctx->rsag ? ctx->scalars + 4 : ctx->cols ? ctx->scalars + 8 : ctx->y + n;
     t1off += nt + 1;
     ctx->g1[s] = grid_for(nt, occ[ROLE_K1], sms);
     if (L.sell) {
@@ -1004,7 +1031,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     }
   }
   CK(cudaGetLastError());
-  if (dist && L.sell && !ctx->rsag) {
+  if (dist && L.sell && !ctx->rsag && !ctx->cols) {
     const plss_status st2 = make_chunks(ctx, ctx->seg2[S - 1], pool2, sms, env_int("PLSS_DIST_CHUNKS", 4));
     if (st2 != PLSS_OK) return st2;
   }
@@ -1129,6 +1156,34 @@ plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int
   return PLSS_OK;
 }
 
+plss_status plss_create_dist_cols(const plss_matrix* A_local, int64_t col_offset, int64_t n_global,
+                                  const uint8_t id[128], int32_t rank, int32_t nranks, const plss_options* opt,
+                                  void* workspace, size_t ws_bytes, void* cuda_stream, plss_ctx** out) {
+  if (!A_local || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) { g_last_error = "invalid argument"; return PLSS_E_INVALID; }
+  if (col_offset < 0 || col_offset + A_local->n > n_global) { g_last_error = "column block outside the global matrix"; return PLSS_E_DIM; }
+  if (opt && (opt->flags & 12)) { g_last_error = "options.flags bit2 / bit3 are row-block steps"; return PLSS_E_INVALID; }
+  *out = nullptr;
+  plss_ctx* ctx = new (std::nothrow) plss_ctx();
+  if (!ctx) return PLSS_E_NOMEM;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  ctx->dist = true;
+  ctx->cols = true;
+  ctx->col_offset = col_offset;
+  ctx->n_global = n_global;
+  plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, true);
+  if (st == PLSS_OK) {
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, u, rank);
+    if (r != ncclSuccess) { set_err(ctx, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); st = PLSS_E_NCCL; }
+  }
+  if (st == PLSS_OK) st = finish_create(ctx);
+  if (st != PLSS_OK) { g_last_error = ctx->err; plss_destroy(ctx); return st; }
+  *out = ctx;
+  return PLSS_OK;
+}
+
 plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
                        int32_t maxit, int32_t flags) {
   if (!ctx) return PLSS_E_INVALID;
@@ -1170,7 +1225,13 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
     CK(cudaMemsetAsync(ctx->p + n, 0, 8 * pad, st));
     CK(cudaMemsetAsync(ctx->scalars + 4, 0, 32, st));
   }
-  if (ctx->dist) {
+  if (ctx->cols) {
+    // b is replicated: ||b|| locally (the same bytes, the same sum on every rank); then the
+    // all-reduced u of the first K1 must sum to b - A x0: ranks > 0 start from u = 0
+    k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 1, nullptr);
+    if (ctx->rank > 0 && m > 0) CK(cudaMemsetAsync(ctx->r, 0, 8 * (size_t)m, st));
+    CK(cudaMemsetAsync(ctx->r + m, 0, 8, st));
+  } else if (ctx->dist) {
     k_norm_b<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->partn, ctx->counters + 3, 0, ctx->scalars);
     CK(cudaGetLastError());
     NK(ncclAllReduce(ctx->scalars, ctx->scalars, 1, ncclFloat64, ncclSum, ctx->comm, st));
@@ -1326,9 +1387,11 @@ plss_status plss_true_residual(plss_ctx* ctx, const double* b, const double* x, 
     a.ctl = nullptr;
     launch_spmv<ROLE_PLAIN>(a, ctx->g1[s], st);
   }
+  if (ctx->cols && m > 0)                    // column blocks: A x = sum over ranks of A_g x_g
+    NK(ncclAllReduce(ax, ax, (size_t)m, ncclFloat64, ncclSum, ctx->comm, st));
   if (m > 0) k_true_resid<<<grid, NT, 0, st>>>(bd, ax, m, part, cnt, res);
   CK(cudaGetLastError());
-  if (ctx->dist) NK(ncclAllReduce(res, res, 2, ncclFloat64, ncclSum, ctx->comm, st));
+  if (ctx->dist && !ctx->cols) NK(ncclAllReduce(res, res, 2, ncclFloat64, ncclSum, ctx->comm, st));
   double h[2] = {0.0, 0.0};
   CK(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, st));
   for (void* q : {(void*)ax, (void*)db, (void*)dx, (void*)part, (void*)res, (void*)cnt})
@@ -1347,7 +1410,37 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
   std::vector<cudaEvent_t> ev(nev);
   for (auto& e : ev) CK(cudaEventCreate(&e));
   double acc[5] = {0, 0, 0, 0, 0};
-  for (int it = 0; it < k; ++it) {
+  for (int it = 0; it < k && ctx->cols; ++it) {
+    // column blocks: K1 | all-reduce of u + rho tail | K2 | dots + all-reduce + phi tail | K3
+    const int64_t m = ctx->m;
+    double* sc = ctx->scalars + 4;
+    CK(cudaEventRecord(ev[0], st));
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K1>(ctx->seg1[s], ctx->g1[s], st);
+    CK(cudaEventRecord(ev[1], st));
+    NK(ncclAllReduce(ctx->r, ctx->r, (size_t)m + 1, ncclFloat64, ncclSum, ctx->comm, st));
+    k_rho_tail<<<ctx->gnorm, NT, 0, st>>>(ctx->r, m, ctx->ctl, ctx->rec, ctx->partn, ctx->counters + 3);
+    CK(cudaEventRecord(ev[2], st));
+    for (int s = 0; s < ctx->S; ++s) launch_spmv<ROLE_K2>(ctx->seg2[s], ctx->g2[s], st);
+    CK(cudaEventRecord(ev[3], st));
+    k_dots_shard<<<ctx->gdots, NT, 0, st>>>(ctx->y, ctx->p, ctx->n, ctx->ctl, ctx->part2, ctx->counters + 1,
+                                            ctx->wi, sc);
+    NK(ncclAllReduce(sc + 1, sc + 1, 2, ncclFloat64, ncclSum, ctx->comm, st));
+    k_tail_phi<<<1, 1, 0, st>>>(ctx->ctl, ctx->rec, sc);
+    CK(cudaEventRecord(ev[4], st));
+    k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, ctx->y, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
+                                       ctx->counters + 2, ctx->wi, ctx->r + m);
+    if (ctx->rank > 0 && m > 0) CK(cudaMemsetAsync(ctx->r, 0, 8 * (size_t)m, st));
+    CK(cudaEventRecord(ev[5], st));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    const int slot[5] = {0, 2, 1, 3, 4};           // k1, all-reduce + rho tail, k2, dots, k3
+    for (int j = 0; j < 5; ++j) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
+      acc[slot[j]] += t;
+    }
+  }
+  for (int it = 0; it < k && !ctx->cols; ++it) {
     int q = 0;
     CK(cudaEventRecord(ev[q++], st));
     for (int s = 0; s < ctx->S; ++s) {
@@ -1428,7 +1521,9 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   }
   // our kernels per loop step: K1 and K2 per slab (the last K2 as column chunks on a chunked
   // distributed ctx), K3, and the distributed dots / tail kernel
-  if (launches_per_step)
+  if (launches_per_step && ctx->cols)          // K1, K2 per slab; rho tail, dots, phi tail, K3
+    *launches_per_step = 2 * ctx->S + 4;
+  else if (launches_per_step)
     *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0) + (ctx->rsag ? 1 : 0) +
                          (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1) +
                          (ctx->peer ? peer_nch(ctx) + 1 : 0);
@@ -1472,7 +1567,8 @@ plss_status plss_column_norms(plss_ctx* ctx, double* c) {
   const unsigned g = (unsigned)((n + 255) / 256);
   k_colsq<<<g, 256, 0, st>>>(ctx->A.col_ptr, ctx->A.val_t, n, tmp);
   CK(cudaGetLastError());
-  if (ctx->dist) NK(ncclAllReduce(tmp, tmp, (size_t)n, ncclFloat64, ncclSum, ctx->comm, st));
+  if (ctx->dist && !ctx->cols)              // column blocks hold whole columns
+    NK(ncclAllReduce(tmp, tmp, (size_t)n, ncclFloat64, ncclSum, ctx->comm, st));
   k_colnorm_finish<<<g, 256, 0, st>>>(tmp, n);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(c, tmp, 8 * (size_t)n, is_device_ptr(c) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));

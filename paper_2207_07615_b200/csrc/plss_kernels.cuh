@@ -1468,6 +1468,33 @@ __global__ void k_tail_rsag(Ctl* c, double* rec, const double* scal) {
   if (!c->done) tail_y(c, rec, scal[1], scal[2]);
 }
 
+// column-block distributed step (plss_create_dist_cols, SURVEY 8(e) "column-block alternative"):
+// r is replicated and was just all-reduced (r <- r - sum_g A_g p_g, with r[m] = sum_g theta_g of the
+// previous K3); rho = r^T r (every rank the same fixed-order sum of the same bytes), theta, the
+// stop test and the rho tail
+__global__ void __launch_bounds__(NT) k_rho_tail(const double* __restrict__ r, long long m, Ctl* c,
+                                                 double* rec, double* partial, unsigned* counter) {
+  __shared__ double sm[2][MAXW];
+  if (c->done) return;
+  double a0 = 0.0, dummy = 0.0;
+  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < m; i += (long long)gridDim.x * NT)
+    a0 = fma(r[i], r[i], a0);
+  if (!publish_and_elect(a0, dummy, partial, partial, gridDim.x, counter, sm)) return;
+  if (threadIdx.x != 0) return;
+  const int k = c->iters;
+  if (k > 0) {
+    c->theta = r[m];
+    rec[(size_t)(k - 1) * REC + 4] = r[m];
+  }
+  tail_rho(c, rec, a0);
+}
+
+// column-block step: the y tail from the all-reduced scal[1] = phi, scal[2] = psi
+__global__ void k_tail_phi(Ctl* c, double* rec, const double* scal) {
+  if (c->done) return;
+  tail_y(c, rec, scal[1], scal[2]);
+}
+
 __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const double* __restrict__ p,
                                                   long long n, const double* rho_g, Ctl* c,
                                                   double* rec, double* partial, unsigned* counter,

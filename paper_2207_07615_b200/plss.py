@@ -30,7 +30,8 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_rp_step", "plss_rp_finish", "plss_rp_sketch", "plss_spmmT", "plss_rp_profile",
            "plss_kz_workspace_bytes", "plss_kz_solve", "plss_kz_start", "plss_kz_step", "plss_kz_finish",
            "plss_kz_profile", "plss_eg_workspace_bytes", "plss_eg_solve", "plss_eg_start", "plss_eg_step",
-           "plss_eg_finish", "plss_eg_profile", "plss_true_residual", "plss_peer_reduce_emulate"]
+           "plss_eg_finish", "plss_eg_profile", "plss_true_residual", "plss_peer_reduce_emulate",
+           "plss_create_dist_cols"]
 
 
 class PlssError(RuntimeError):
@@ -144,6 +145,8 @@ def load_library(path: str = None):
     lib.plss_eg_profile.restype = st
     lib.plss_true_residual.argtypes = [P, P, P, P]
     lib.plss_true_residual.restype = st
+    lib.plss_create_dist_cols.argtypes = lib.plss_create_dist.argtypes
+    lib.plss_create_dist_cols.restype = st
     lib.plss_peer_reduce_emulate.argtypes = [I32, P, P, P, I32, P, P]
     lib.plss_peer_reduce_emulate.restype = st
     lib.plss_destroy.argtypes = [P]
@@ -296,6 +299,22 @@ def plss_create_dist(A_local: Matrix, row_offset: int, m_global: int, uid: bytes
     o = _opts(slabs, graph_chunk, maxit_cap, sell, window, rsag, peer)
     _check(lib.plss_create_dist(ctypes.byref(ms), int(row_offset), int(m_global), uid, int(rank), int(nranks),
                                 ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream), ctypes.byref(h)))
+    return Ctx(h, A_local, ws, stream, maxit_cap)
+
+
+def plss_create_dist_cols(A_local: Matrix, col_offset: int, n_global: int, uid: bytes, rank: int, nranks: int,
+                          slabs=0, graph_chunk=0, maxit_cap=20000, stream=None, validate=False, sell=True,
+                          window=True) -> Ctx:
+    """Column-block distributed ctx (include/plss.h): A_local = the m x n_local block of columns
+    [col_offset, col_offset + n_local), local column indices in its CSR; x / x0 are shards."""
+    lib = load_library()
+    nbytes = plss_workspace_bytes(A_local, slabs, graph_chunk, maxit_cap, sell, window)
+    ws = _alloc_workspace(nbytes, A_local.row_ptr.device)
+    h = ctypes.c_void_p()
+    ms = A_local.c_struct(validate)
+    o = _opts(slabs, graph_chunk, maxit_cap, sell, window)
+    _check(lib.plss_create_dist_cols(ctypes.byref(ms), int(col_offset), int(n_global), uid, int(rank), int(nranks),
+                                     ctypes.byref(o), _aligned(ws), nbytes, _stream_ptr(stream), ctypes.byref(h)))
     return Ctx(h, A_local, ws, stream, maxit_cap)
 
 

@@ -327,3 +327,17 @@ def row_block(sysm: System, G: int, g: int) -> dict:
     cp, ri, vt = csr_to_csc(r1 - r0, sysm.n, rp, ci, v)
     return {"row_offset": r0, "m": r1 - r0, "n": sysm.n, "row_ptr": rp, "col_idx": ci, "val": v,
             "col_ptr": cp, "row_idx": ri, "val_t": vt, "b": sysm.b[r0:r1]}
+
+
+def col_block(sysm: System, G: int, g: int) -> dict:
+    """Column block g (columns [c0, c1) = row_block_bounds(n, G, g)) as an m x (c1 - c0) matrix:
+    its CSC slice (rows global) and the CSR over local column indices; b is the full right-hand side
+    (replicated in the column-block partition)."""
+    c0, c1 = row_block_bounds(sysm.n, G, g)
+    a, e = int(sysm.col_ptr[c0]), int(sysm.col_ptr[c1])
+    cp = (sysm.col_ptr[c0:c1 + 1] - a).astype(np.int32)
+    ri = sysm.row_idx[a:e]
+    vt = sysm.val_t[a:e]
+    rp, ci, v = csr_to_csc(c1 - c0, sysm.m, cp, ri, vt)       # the transpose of a CSC is its CSR
+    return {"col_offset": c0, "m": sysm.m, "n": c1 - c0, "row_ptr": rp, "col_idx": ci, "val": v,
+            "col_ptr": cp, "row_idx": ri, "val_t": vt, "b": sysm.b}

@@ -124,6 +124,60 @@ def gloo_solve_rsag(s, blk, dist, torch, maxit):
     return np.array(hist), torch.cat(parts).numpy()[:n], iters
 
 
+def gloo_solve_cols(s, blk, dist, torch, maxit):
+    """The column-block decomposition (plss.cu enqueue_step_cols, plss_create_dist_cols): r
+    replicated, x / p / y column shards. u <- u - A_g p_g (u = r on rank 0, 0 elsewhere), ONE
+    all-reduce of u | theta_g gives r = r - A p and theta; rho = r^T r replicated; y_g = A_g^T r;
+    phi, psi as shard partials in an all-reduce of 2; K3 on the shard; x gathered at the end."""
+    import oracle
+    m, n_l = s.m, blk["n"]
+    G, g = dist.get_world_size(), dist.get_rank()
+    b = blk["b"]
+    nbd = float(np.sqrt(b @ b))
+    u = b.copy() if g == 0 else np.zeros(m)
+    p = np.zeros(n_l)
+    x = np.zeros(n_l)
+    hist, iters, theta_g = [], 0, 0.0
+    while True:
+        if iters > 0:
+            u = u - oracle.spmv(m, blk["row_ptr"], blk["col_idx"], blk["val"], p)
+        buf = torch.zeros(m + 1, dtype=torch.float64)
+        buf[:m] = torch.from_numpy(u)
+        buf[m] = theta_g
+        dist.all_reduce(buf)                             # r = r - A p and theta, on every rank
+        r = buf[:m].numpy().copy()
+        theta = float(buf[m])
+        rho = float(r @ r)
+        h = np.sqrt(rho) / nbd
+        hist.append(h)
+        if rho == 0.0 or h <= s.tol:
+            break
+        y = oracle.spmvT(n_l, blk["col_ptr"], blk["row_idx"], blk["val_t"], r)
+        sc = torch.tensor([float(y @ y), float(y @ p)], dtype=torch.float64)
+        dist.all_reduce(sc)                              # phi, psi
+        phi = float(sc[0])
+        if iters == 0:
+            p = (rho / phi) * y
+        else:
+            tau = np.sqrt(theta * phi) / rho
+            beta = 1.0 / ((tau - 1.0) * (tau + 1.0))
+            gamma = (theta / rho) * beta
+            p = beta * p + gamma * y
+        theta_g = float(p @ p)
+        x = x + p
+        u = r if g == 0 else np.zeros(m)
+        iters += 1
+        if iters >= maxit:
+            break
+    width = -(-s.n // G) + 1
+    xs = torch.zeros(width, dtype=torch.float64)
+    xs[:n_l] = torch.from_numpy(x)
+    parts = [torch.empty(width, dtype=torch.float64) for _ in range(G)]
+    dist.all_gather(parts, xs)
+    bounds = [plss_gen.row_block_bounds(s.n, G, h) for h in range(G)]
+    return np.array(hist), np.concatenate([parts[h][:c1 - c0].numpy() for h, (c0, c1) in enumerate(bounds)]), iters
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--backend", default="gloo")
@@ -131,13 +185,17 @@ def main():
     ap.add_argument("--config", default="C2s")
     ap.add_argument("--chunks", type=int, default=1)
     ap.add_argument("--rsag", action="store_true")
+    ap.add_argument("--cols", action="store_true", help="column-block partition")
+    ap.add_argument("--maxit", type=int, default=0, help="cap the config's maxit")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     s = plss_gen.make_config(args.config)
-    blk = plss_gen.row_block(s, world, rank)
+    if args.maxit > 0:
+        s.maxit = min(s.maxit, args.maxit)
+    blk = plss_gen.col_block(s, world, rank) if args.cols else plss_gen.row_block(s, world, rank)
     if args.backend == "gloo":
         dist.init_process_group("gloo")
         uid = None
@@ -147,7 +205,9 @@ def main():
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         assert isinstance(obj[0], bytes) and len(obj[0]) == 128
-        if args.rsag:
+        if args.cols:
+            hist, x, iters = gloo_solve_cols(s, blk, dist, torch, s.maxit)
+        elif args.rsag:
             hist, x, iters = gloo_solve_rsag(s, blk, dist, torch, s.maxit)
         else:
             hist, x, iters = gloo_solve(s, blk, dist, torch, s.maxit, args.chunks)
@@ -163,12 +223,25 @@ def main():
         uid = pkg.plss_get_unique_id() if rank == 0 else None
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
-        A = pkg.Matrix.from_arrays(blk["m"], s.n, blk["row_ptr"], blk["col_idx"], blk["val"],
+        A = pkg.Matrix.from_arrays(blk["m"], blk["n"], blk["row_ptr"], blk["col_idx"], blk["val"],
                                    blk["col_ptr"], blk["row_idx"], blk["val_t"])
-        ctx = pkg.plss_create_dist(A, blk["row_offset"], s.m, obj[0], rank, world, maxit_cap=s.maxit,
-                                   validate=True)
+        if args.cols:
+            ctx = pkg.plss_create_dist_cols(A, blk["col_offset"], s.n, obj[0], rank, world, maxit_cap=s.maxit,
+                                            validate=True)
+        else:
+            ctx = pkg.plss_create_dist(A, blk["row_offset"], s.m, obj[0], rank, world, maxit_cap=s.maxit,
+                                       validate=True)
         res = pkg.plss_solve(ctx, torch.from_numpy(blk["b"]).cuda(), tol=s.tol, maxit=s.maxit, want_diag=True)
         hist, x, iters = res["hist"], res["x"].cpu().numpy(), res["iters"]
+        if args.cols:                                    # x is sharded by columns: gather it
+            width = -(-s.n // world) + 1
+            xs = torch.zeros(width, dtype=torch.float64, device="cuda")
+            xs[:blk["n"]] = res["x"]
+            parts = [torch.empty_like(xs) for _ in range(world)]
+            dist.all_gather(parts, xs)
+            x = np.concatenate([parts[h][:c1 - c0].cpu().numpy()
+                                for h, (c0, c1) in enumerate(plss_gen.row_block_bounds(s.n, world, q)
+                                                             for q in range(world))])
         # every rank holds the same replicated x and took the same decisions from the
         # same scalars -- rho, phi, psi, theta, tau, beta, gamma of every iteration, bitwise
         for arr in (x, res["diag"].reshape(-1)):

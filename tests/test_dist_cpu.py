@@ -5,6 +5,7 @@ import subprocess
 import sys
 
 import numpy as np
+import pytest
 
 import oracle
 import plss_gen
@@ -18,12 +19,12 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _run(world, cfg, tmp_path, chunks=1, rsag=False):
-    out = tmp_path / f"res_{world}_{chunks}_{int(rsag)}.npz"
+def _run(world, cfg, tmp_path, chunks=1, rsag=False, cols=False, maxit=0):
+    out = tmp_path / f"res_{world}_{chunks}_{int(rsag)}_{int(cols)}.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), "--backend", "gloo", "--out", str(out),
-           "--config", cfg, "--chunks", str(chunks)] + (["--rsag"] if rsag else [])
+           "--config", cfg, "--chunks", str(chunks)] + (["--rsag"] if rsag else []) + (["--cols"] if cols else []) + ["--maxit", str(maxit)]
     env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1")
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env, capture_output=True)
     return np.load(out)
@@ -59,6 +60,38 @@ def test_row_blocks_world2_reduce_scatter_step(tmp_path):
     k = min(50, len(ref["hist"]))
     assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
     assert np.linalg.norm(r["x"] - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-7
+
+
+@pytest.mark.parametrize("cfg,maxit", [("C2s", 0), ("C4xs", 60)])
+def test_column_blocks_world2_match_oracle(tmp_path, cfg, maxit):
+    """The column-block decomposition (plss_create_dist_cols) with two ranks: a full solve (C2s) and
+    the first 60 steps of the underdetermined power-law system (C4xs: m < n, where the all-reduce of
+    m + 1 values is the smaller message; its full solve takes ~5.5k ill-conditioned steps whose
+    count moves with rounding)."""
+    s = plss_gen.make_config(cfg)
+    if maxit:
+        s.maxit = maxit
+    ref = oracle.plss_system(s)
+    r = _run(2, cfg, tmp_path, cols=True, maxit=maxit)
+    from test_gpu_parity import _assert_parity, _floor          # the floor-aware bars (SURVEY 8c-11)
+    res = {"hist": r["hist"], "xh": r["x"], "iters": int(r["iters"]),
+           "outcome": "maxit" if int(r["iters"]) >= s.maxit else "converged"}
+    _assert_parity(res, ref, _floor(s, ref), s)
+
+
+def test_column_block_slices():
+    s = plss_gen.make_config("C2s")
+    A = s.scipy_csr().toarray()
+    for G in (1, 3):
+        for g in range(G):
+            blk = plss_gen.col_block(s, G, g)
+            c0 = blk["col_offset"]
+            d = np.zeros((s.m, blk["n"]))
+            for i in range(s.m):
+                for k in range(blk["row_ptr"][i], blk["row_ptr"][i + 1]):
+                    d[i, blk["col_idx"][k]] = blk["val"][k]
+            np.testing.assert_array_equal(d, A[:, c0:c0 + blk["n"]])
+            assert np.all(np.diff(blk["row_ptr"]) >= 0)
 
 
 def test_row_block_bounds_partition():

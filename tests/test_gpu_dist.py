@@ -198,3 +198,65 @@ def test_reduce_scatter_needs_dist(pkg):
     ws = _alloc_workspace(nbytes, "cuda")
     h = ctypes.c_void_p()
     assert lib.plss_create(ctypes.byref(ms), ctypes.byref(o), _aligned(ws), nbytes, None, ctypes.byref(h)) != 0
+
+
+@pytest.mark.parametrize("name,slabs,weighted,x0", [("C2s", 1, False, False), ("C5xs", 2, False, False),
+                                                   ("C4xs", 1, False, False), ("C2s", 2, True, False),
+                                                   ("C3_64", 1, False, True)])
+def test_dist_column_block_step(pkg, name, slabs, weighted, x0):
+    """plss_create_dist_cols (the column-block partition) on a single rank: the block is
+    the whole matrix; K1 into u, all-reduce of u | theta, replicated rho tail, K2 over the local
+    columns, phi / psi all-reduce, shard K3. Parity with the oracle, agreement with the row-block
+    step over the live iterations, and the true residual of its x."""
+    s = plss_gen.make_config("C3", N=64) if name == "C3_64" else plss_gen.make_config(name)
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    xin = np.random.default_rng(3).standard_normal(s.n) if x0 else None
+    out = {}
+    for cols in (True, False):
+        mk = pkg.plss_create_dist_cols if cols else pkg.plss_create_dist
+        ctx = mk(A, 0, s.n if cols else s.m, pkg.plss_get_unique_id(), 0, 1, slabs=slabs, maxit_cap=s.maxit,
+                 validate=True)
+        if cols:
+            assert pkg.plss_query(ctx)["launches_per_step"] == 2 * pkg.plss_query(ctx)["slabs"] + 4
+        wi = None
+        if weighted:
+            wi = pkg.plss_column_norms(ctx)
+            pkg.plss_set_wi(ctx, wi)
+        res = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), None if xin is None else torch.from_numpy(xin).cuda(),
+                             tol=s.tol, maxit=s.maxit, flags=1 if s.freeze else 0)
+        res["xh"] = res["x"].cpu().numpy()
+        if cols:
+            t = pkg.plss_true_residual(ctx, s.b, res["x"])
+            ref_t = np.linalg.norm(s.b - oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, res["xh"]))
+            assert abs(t["abs"] - ref_t) <= 1e-12 * max(ref_t, np.linalg.norm(s.b))
+        out[cols] = (res, None if wi is None else wi.cpu().numpy())
+        pkg.plss_destroy(ctx)
+    res, wih = out[True]
+    if weighted:
+        np.testing.assert_array_equal(wih, out[False][1])          # whole columns: same norms
+    ref = oracle.plss_system(s, x0=xin, wi=wih)
+    from test_gpu_parity import _assert_parity, _floor, HIST_TOL
+    fl = _floor(s, ref, x0=xin)
+    _assert_parity(res, ref, fl, s)
+    h1, h0 = res["hist"], out[False][0]["hist"]
+    k = min(len(h1), len(h0), 25, fl["kf"])                    # within the fp64 floor (SURVEY 8c-11)
+    live = h0[:k] > 1e-10
+    assert np.max(np.abs(h1[:k] - h0[:k])[live] / h0[:k][live]) <= HIST_TOL
+
+
+def test_column_block_rejects_row_block_steps(pkg):
+    s = plss_gen.make_config("C2s")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    import ctypes
+    from paper_2207_07615_b200.plss import _opts, _alloc_workspace, _aligned
+    lib = pkg.load_library()
+    ms = A.c_struct()
+    nbytes = pkg.plss_workspace_bytes(A)
+    ws = _alloc_workspace(nbytes, "cuda")
+    uid = pkg.plss_get_unique_id()
+    for o in (_opts(rsag=True), _opts(peer=True)):
+        h = ctypes.c_void_p()
+        assert lib.plss_create_dist_cols(ctypes.byref(ms), 0, s.n, uid, 0, 1, ctypes.byref(o), _aligned(ws), nbytes,
+                                         None, ctypes.byref(h)) != 0
+    with pytest.raises(pkg.PlssError):                      # block outside the global matrix
+        pkg.plss_create_dist_cols(A, 1, s.n, uid, 0, 1)
