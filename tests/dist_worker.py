@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--chunks", type=int, default=1)
     ap.add_argument("--rsag", action="store_true")
     ap.add_argument("--cols", action="store_true", help="column-block partition")
+    ap.add_argument("--peer", action="store_true", help="nccl backend: the peer-memory all-reduce step")
     ap.add_argument("--maxit", type=int, default=0, help="cap the config's maxit")
     args = ap.parse_args()
     import torch
@@ -230,7 +231,7 @@ def main():
                                             validate=True)
         else:
             ctx = pkg.plss_create_dist(A, blk["row_offset"], s.m, obj[0], rank, world, maxit_cap=s.maxit,
-                                       validate=True)
+                                       validate=True, rsag=args.rsag, peer=args.peer)
         res = pkg.plss_solve(ctx, torch.from_numpy(blk["b"]).cuda(), tol=s.tol, maxit=s.maxit, want_diag=True)
         hist, x, iters = res["hist"], res["x"].cpu().numpy(), res["iters"]
         if args.cols:                                    # x is sharded by columns: gather it

@@ -62,12 +62,16 @@ def test_dist_zero_rhs(pkg):
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_two_ranks_torchrun(tmp_path):
+@pytest.mark.parametrize("mode", ["allreduce", "rsag", "peer", "cols"])
+def test_two_ranks_torchrun(tmp_path, mode):
+    """Two ranks on two GPUs: every distributed step (the chunked NCCL all-reduce, the reduce-scatter
+    step, the peer-memory step over CUDA IPC, the column-block partition); the worker also checks
+    that both ranks hold bitwise the same x and per-iteration scalars."""
     script = os.path.join(ROOT, "tests", "dist_worker.py")
     out = tmp_path / "res.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", script, "--backend", "nccl",
-           "--out", str(out)]
+           "--out", str(out), "--config", "C5xs"] + ([] if mode == "allreduce" else [f"--{mode}"])
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
     r = np.load(out)
     s = plss_gen.make_config("C5xs")
