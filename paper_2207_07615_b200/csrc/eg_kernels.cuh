@@ -155,6 +155,43 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemvT(EgArgs a) {
   // columns j, j + NW, j + 2 NW, j + 3 NW at once, rows two per lane step: 8 independent loads
   const int jend = min(hk, jc0 + EG_CT);
   int j = jc0 + warp;
+  if (((a.n & 1) | ((reinterpret_cast<uintptr_t>(vec) | reinterpret_cast<uintptr_t>(a.Y)) & 15)) == 0) {
+    // even n, aligned: 16-byte loads of row pairs (2p, 2p + 1), 2 pairs per lane step (8 x 16 B
+    // in flight per lane); per column the lane sums its pairs in order, then the fixed butterfly
+    const double2* v2 = reinterpret_cast<const double2*>(vec);
+    const int64_t p1 = l1 >> 1;
+    for (; j + 3 * NW < jend; j += 4 * NW) {
+      const double2* c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] = reinterpret_cast<const double2*>(a.Y + (int64_t)(j + q * NW) * a.n);
+      double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+      int64_t pp = (l0 >> 1) + lane;
+      for (; pp + 32 < p1; pp += 64) {
+        const double2 y0 = __ldg(v2 + pp), y1 = __ldg(v2 + pp + 32);
+        double2 v0[4], v1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { v0[q] = __ldg(c[q] + pp); v1[q] = __ldg(c[q] + pp + 32); }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          sa[q] = __dadd_rn(__dadd_rn(sa[q], __dmul_rn(v0[q].x, y0.x)), __dmul_rn(v0[q].y, y0.y));
+          sb[q] = __dadd_rn(__dadd_rn(sb[q], __dmul_rn(v1[q].x, y1.x)), __dmul_rn(v1[q].y, y1.y));
+        }
+      }
+      if (pp < p1) {
+        const double2 y0 = __ldg(v2 + pp);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 v0 = __ldg(c[q] + pp);
+          sa[q] = __dadd_rn(__dadd_rn(sa[q], __dmul_rn(v0.x, y0.x)), __dmul_rn(v0.y, y0.y));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double v = warp_sum(__dadd_rn(sa[q], sb[q]));
+        if (lane == 0) out[j + q * NW] = v;
+      }
+    }
+  }
   for (; j + 3 * NW < jend; j += 4 * NW) {
     const double* c[4];
 #pragma unroll
