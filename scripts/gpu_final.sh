@@ -18,5 +18,5 @@ timeout 600 python bench.py --workload C4 --no-cpu-baseline > gpurun_out/bench_$
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_ref.json 2>/dev/null; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_(sell|spmv|pxupdate|dots_tail|norm_b|set_nbd)' -c 400 --csv \
   --log-file gpurun_out/launches_${TAG}.csv python bench.py --ncu --steps 2 --warmup 1 > /dev/null 2>&1; echo "ncu list rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_sell|k_spmv|k_pxupdate' -s 17 -c 5 \
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_sell<|k_spmv<|k_pxupdate' -s 8 -c 6 \
   -o gpurun_out/prof_${TAG} -f python bench.py --ncu --steps 2 --warmup 1 > /dev/null 2>&1; echo "ncu full rc=$?"
