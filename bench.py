@@ -249,12 +249,24 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_label(name)},
+            "data": "synthetic", "config": {"workload": workload_label(name), **full_dims_of(name),
+                                            "parallelism": "oracle on 1 host core", "freeze_mode": True,
+                                            "tol": 0.0},
             "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": "oracle",
                              "sample": f"{label}; each step one oracle loop step; it/s scaled to the "
                                        f"full workload by algorithmic bytes/iter ({gbs:.2f} GB/s)"},
             "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def full_dims_of(name):
+    """m, n, nnz of the full workload (the config keys of our arm's line)."""
+    if name == "C5":
+        return {"m": 64_000_000, "n": 8_000_000, "nnz": 768_000_000}
+    if name == "C3":
+        return {"m": 2048 ** 2, "n": 2048 ** 2, "nnz": 5 * 2048 ** 2 - 4 * 2048}
+    s = plss_gen.make_config(name)
+    return {"m": s.m, "n": s.n, "nnz": s.nnz}
 
 
 def full_bytes_of(name):
