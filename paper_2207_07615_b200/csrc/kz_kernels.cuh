@@ -126,6 +126,65 @@ __global__ void __launch_bounds__(KZ_NT) k_kz_gemv(KzArgs a) {
   const int j0 = (int)((int64_t)hk * js / KZ_JS), j1 = (int)((int64_t)hk * (js + 1) / KZ_JS);
   double* Pnew = a.P + (int64_t)hk * a.n;
   double th = 0.0, zero = 0.0;
+  if (((a.n & 1) | ((reinterpret_cast<uintptr_t>(a.P) | reinterpret_cast<uintptr_t>(a.arow) |
+                      reinterpret_cast<uintptr_t>(a.pk) | reinterpret_cast<uintptr_t>(a.x)) & 15)) == 0) {
+    // even n, aligned P: a thread takes rows (l, l + 1) of a 2 KZ_TL-row tile with 16-byte loads
+    // (8 columns x 16 B in flight); each row's sum keeps its ascending-j order
+    __shared__ double2 part2[KZ_JS][KZ_TL];
+    for (int64_t l0 = (int64_t)blockIdx.x * 2 * KZ_TL; l0 < a.n; l0 += (int64_t)gridDim.x * 2 * KZ_TL) {
+      const int64_t l = l0 + 2 * tl;
+      double2 t = make_double2(0.0, 0.0);
+      if (l < a.n) {
+        int j = j0;
+        for (; j + 8 <= j1; j += 8) {
+          double2 pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pv[u] = __ldg(reinterpret_cast<const double2*>(a.P + (int64_t)(j + u) * a.n + l));
+          double wv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) wv[u] = __ldg(a.w + j + u);
+          asm volatile("" ::: "memory");           // all 8 row-pair loads issue before the first use
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double wj = wv[u];
+            t.x = __dadd_rn(t.x, __dmul_rn(pv[u].x, wj));
+            t.y = __dadd_rn(t.y, __dmul_rn(pv[u].y, wj));
+          }
+        }
+        for (; j < j1; ++j) {
+          const double2 pv = __ldg(reinterpret_cast<const double2*>(a.P + (int64_t)j * a.n + l));
+          const double wj = __ldg(a.w + j);
+          t.x = __dadd_rn(t.x, __dmul_rn(pv.x, wj));
+          t.y = __dadd_rn(t.y, __dmul_rn(pv.y, wj));
+        }
+      }
+      part2[js][tl] = t;
+      __syncthreads();
+      if (js == 0 && l < a.n) {
+        double2 tt = part2[0][tl];
+#pragma unroll
+        for (int q = 1; q < KZ_JS; ++q) { tt.x = __dadd_rn(tt.x, part2[q][tl].x); tt.y = __dadd_rn(tt.y, part2[q][tl].y); }
+        const double2 ar = *reinterpret_cast<const double2*>(a.arow + l);
+        double2 p2v;
+        p2v.x = skip ? 0.0 : __dmul_rn(gamma, __dadd_rn(ar.x, -tt.x));
+        p2v.y = skip ? 0.0 : __dmul_rn(gamma, __dadd_rn(ar.y, -tt.y));
+        *reinterpret_cast<double2*>(a.pk + l) = p2v;
+        if (!skip) {
+          *reinterpret_cast<double2*>(Pnew + l) = p2v;
+          double2 xx = *reinterpret_cast<const double2*>(a.x + l);
+          xx.x = __dadd_rn(xx.x, p2v.x);
+          xx.y = __dadd_rn(xx.y, p2v.y);
+          *reinterpret_cast<double2*>(a.x + l) = xx;
+        }
+        th = __dadd_rn(th, __dmul_rn(p2v.x, p2v.x));
+        th = __dadd_rn(th, __dmul_rn(p2v.y, p2v.y));
+      }
+      __syncthreads();
+    }
+    block_sum2(th, zero, sm);
+    if (threadIdx.x == 0) a.part_th[blockIdx.x] = th;
+    return;
+  }
   for (int64_t l0 = (int64_t)blockIdx.x * KZ_TL; l0 < a.n; l0 += (int64_t)gridDim.x * KZ_TL) {
     const int64_t l = l0 + tl;
     double t = 0.0;
