@@ -320,13 +320,46 @@ __global__ void __launch_bounds__(EG_NT) k_eg_trit(EgArgs a) {
   rk[5] = (double)st->hk;
 }
 
-// p = coef (y - Y t_hat): tiles of 64 l, 4 groups each summing a quarter of the history columns.
+// sum over history columns j in [j0, j1), ascending, of Y[j][l] w_j for the row pair (l, l + 1):
+// 16-byte loads of 8 columns per batch (Y column-major with an even leading dimension n)
+__device__ __forceinline__ double2 eg_pair_sum(const double* Y, int64_t n, const double* w, int j0, int j1,
+                                               int64_t l) {
+  double2 t = make_double2(0.0, 0.0);
+  int j = j0;
+  for (; j + 8 <= j1; j += 8) {
+    double2 pv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pv[u] = __ldg(reinterpret_cast<const double2*>(Y + (int64_t)(j + u) * n + l));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double wj = __ldg(w + j + u);
+      t.x = __dadd_rn(t.x, __dmul_rn(pv[u].x, wj));
+      t.y = __dadd_rn(t.y, __dmul_rn(pv[u].y, wj));
+    }
+  }
+  for (; j < j1; ++j) {
+    const double2 pv = __ldg(reinterpret_cast<const double2*>(Y + (int64_t)j * n + l));
+    const double wj = __ldg(w + j);
+    t.x = __dadd_rn(t.x, __dmul_rn(pv.x, wj));
+    t.y = __dadd_rn(t.y, __dmul_rn(pv.y, wj));
+  }
+  return t;
+}
+__device__ __forceinline__ bool eg_pairs_ok(const EgArgs& a) {
+  return ((a.n & 1) | ((reinterpret_cast<uintptr_t>(a.Y) | reinterpret_cast<uintptr_t>(a.y) |
+                        reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.x) |
+                        reinterpret_cast<uintptr_t>(a.w)) & 15)) == 0;
+}
+
+// p = coef (y - Y t_hat): tiles of 64 l (128 l as row pairs with 16-byte loads when n is even),
+// 4 groups each summing a quarter of the history columns, quarters added in order.
 // QR: p = coef (e_h - V z) over the h + 1 columns of V_{h+1} (the new column is already in V).
 template <int QR>
 __global__ void __launch_bounds__(EG_NT) k_eg_gemv(EgArgs a) {
   if (eg_done(a)) return;
   constexpr int TL = 64, JS = EG_NT / TL;
   __shared__ double part[JS][TL];
+  __shared__ double2 part2[JS][TL];
   const EgState* st = a.st;
   const int hu = st->hk_use, skip = st->skip;
   const int hk = QR ? hu + 1 : hu;
@@ -335,6 +368,31 @@ __global__ void __launch_bounds__(EG_NT) k_eg_gemv(EgArgs a) {
   const int tl = threadIdx.x % TL, js = threadIdx.x / TL;
   const int j0 = (int)((int64_t)hk * js / JS), j1 = (int)((int64_t)hk * (js + 1) / JS);
   double* Ynew = a.Y + (int64_t)hu * a.n;
+  if (eg_pairs_ok(a)) {
+    for (int64_t l0 = (int64_t)blockIdx.x * 2 * TL; l0 < a.n; l0 += (int64_t)gridDim.x * 2 * TL) {
+      const int64_t l = l0 + 2 * tl;
+      part2[js][tl] = l < a.n ? eg_pair_sum(a.Y, a.n, wt, j0, j1, l) : make_double2(0.0, 0.0);
+      __syncthreads();
+      if (js == 0 && l < a.n) {
+        double2 tt = part2[0][tl];
+#pragma unroll
+        for (int q = 1; q < JS; ++q) { tt.x = __dadd_rn(tt.x, part2[q][tl].x); tt.y = __dadd_rn(tt.y, part2[q][tl].y); }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t le = l + e;
+          const double yl = QR ? (le == hu ? 1.0 : 0.0) : a.y[le];
+          const double pl = skip ? 0.0 : __dmul_rn(coef, __dadd_rn(yl, e ? -tt.y : -tt.x));
+          a.p[le] = pl;
+          if (!skip) {
+            if (!QR) Ynew[le] = yl;
+            a.x[le] = __dadd_rn(a.x[le], pl);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
   for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < a.n; l0 += (int64_t)gridDim.x * TL) {
     const int64_t l = l0 + tl;
     double t = 0.0;
@@ -393,7 +451,27 @@ __global__ void __launch_bounds__(EG_NT) k_qr_w(EgArgs a) {
   const int tl = threadIdx.x % TL, js = threadIdx.x / TL;
   const int j0 = (int)((int64_t)hk * js / JS), j1 = (int)((int64_t)hk * (js + 1) / JS);
   double sig = 0.0, z = 0.0;
-  for (int64_t l0 = (int64_t)blockIdx.x * TL; l0 < a.n; l0 += (int64_t)gridDim.x * TL) {
+  const bool pairs = eg_pairs_ok(a);
+  __shared__ double2 part2[JS][TL];
+  for (int64_t l0 = (int64_t)blockIdx.x * 2 * TL; pairs && l0 < a.n; l0 += (int64_t)gridDim.x * 2 * TL) {
+    const int64_t l = l0 + 2 * tl;            // row pairs with 16-byte loads (n even)
+    part2[js][tl] = l < a.n ? eg_pair_sum(a.Y, a.n, a.uv, j0, j1, l) : make_double2(0.0, 0.0);
+    __syncthreads();
+    if (js == 0 && l < a.n) {
+      double2 tt = part2[0][tl];
+#pragma unroll
+      for (int q = 1; q < JS; ++q) { tt.x = __dadd_rn(tt.x, part2[q][tl].x); tt.y = __dadd_rn(tt.y, part2[q][tl].y); }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t le = l + e;
+        const double wl = __dadd_rn(a.y[le], e ? -tt.y : -tt.x);
+        a.w[le] = wl;
+        if (le >= hk) sig = __dadd_rn(sig, __dmul_rn(wl, wl));
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t l0 = (int64_t)blockIdx.x * TL; !pairs && l0 < a.n; l0 += (int64_t)gridDim.x * TL) {
     const int64_t l = l0 + tl;
     double t = 0.0;
     if (l < a.n) {
