@@ -1503,7 +1503,7 @@ __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const 
   if (c->done) return;
   const bool wtd = wi != nullptr && c->weighted;
   double a0 = 0.0, a1 = 0.0;
-  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT) {
+  auto one = [&](long long i) {
     const double yy = y[i];
     if (wtd) {                                      // y <- WIy in place (what K3 consumes)
       const double wy = __ddiv_rn(yy, wi[i]);
@@ -1513,6 +1513,30 @@ __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const 
       a0 = fma(yy, yy, a0);
     }
     a1 = fma(yy, p[i], a1);
+  };
+  const long long stride = (long long)gridDim.x * NT;
+  if (((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(wi)) & 15) == 0) {
+    // 16-byte loads of element pairs; the odd last element by thread 0 of CTA 0
+    const long long n2 = n >> 1;
+    for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n2; i += stride) {
+      const double2 yy = reinterpret_cast<const double2*>(y)[i];
+      const double2 pp = reinterpret_cast<const double2*>(p)[i];
+      if (wtd) {
+        const double2 ww = reinterpret_cast<const double2*>(wi)[i];
+        const double2 wy = make_double2(__ddiv_rn(yy.x, ww.x), __ddiv_rn(yy.y, ww.y));
+        reinterpret_cast<double2*>(y)[i] = wy;
+        a0 = fma(yy.x, wy.x, a0);
+        a0 = fma(yy.y, wy.y, a0);
+      } else {
+        a0 = fma(yy.x, yy.x, a0);
+        a0 = fma(yy.y, yy.y, a0);
+      }
+      a1 = fma(yy.x, pp.x, a1);
+      a1 = fma(yy.y, pp.y, a1);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) one(n - 1);
+  } else {
+    for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += stride) one(i);
   }
   if (!publish_and_elect(a0, a1, partial, partial, gridDim.x, counter, sm)) return;
   if (threadIdx.x != 0) return;
