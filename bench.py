@@ -716,9 +716,12 @@ def main_kz(args):
     pin_b.copy_(b.cpu())
     pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    pkg.plss_kz_solve(ctx, pin_b, rows, kmax=cap, tol=0.0, maxit=W + K, x=pin_x)
-    t_e2e = time.perf_counter() - t0
+    ts = []
+    for _ in range(3):              # a ~0.1 s solve: the median of 3 against host-side hiccups
+        t0 = time.perf_counter()
+        pkg.plss_kz_solve(ctx, pin_b, rows, kmax=cap, tol=0.0, maxit=W + K, x=pin_x)
+        ts.append(time.perf_counter() - t0)
+    t_e2e = sorted(ts)[1]
     line = {"metric": KZ_METRIC, "value": its, "unit": "it/s", "n_gpus": 1, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
@@ -739,7 +742,7 @@ def main_kz(args):
                                             and os.environ.get("PLSS_KZ_FUSE", "1") != "0") else q["slabs"])),
             "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": (8 * m + 4 * (W + K)) / (W + K),
                     "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
-                    "note": "one plss_kz_solve from pinned host b and host rows to host x + history "
+                    "note": "median of 3 plss_kz_solve calls from pinned host b and host rows to host x + history "
                             "(steps from history 0, so cheaper on average than the timed window)"},
             "clocks": clk.summary(), "final_hist": float(fin["hist_full"][W + K])}
     if not args.no_cpu_baseline:
@@ -834,9 +837,13 @@ def main_eg(args):
     pin_b.copy_(b.cpu())
     pin_x = torch.empty(n, dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    pkg.plss_eg_solve(ctx, pin_b, sketch=sk, kmax=cap, rows=rows, seed=1, tol=0.0, maxit=W + K, x=pin_x, factor=fac)
-    t_e2e = time.perf_counter() - t0
+    ts = []
+    for _ in range(3):              # a ~0.1 s solve: the median of 3 against host-side hiccups
+        t0 = time.perf_counter()
+        pkg.plss_eg_solve(ctx, pin_b, sketch=sk, kmax=cap, rows=rows, seed=1, tol=0.0, maxit=W + K, x=pin_x,
+                          factor=fac)
+        ts.append(time.perf_counter() - t0)
+    t_e2e = sorted(ts)[1]
     line = {"metric": EG_METRIC, "value": its, "unit": "it/s", "n_gpus": 1, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
@@ -854,7 +861,7 @@ def main_eg(args):
             "kernels_ms_per_step": kt, "gpu_launches": K * eg_launches_per_step(sk, fac, q["slabs"]),
             "e2e": {"value": (W + K) / t_e2e, "unit": "it/s", "h2d_bytes_per_step": 8 * m / (W + K),
                     "d2h_bytes_per_step": (8 * n + 8 * (W + K + 1)) / (W + K), "solve_iters": W + K,
-                    "note": "one plss_eg_solve from pinned host b to host x + history (from history 0)"},
+                    "note": "median of 3 plss_eg_solve calls from pinned host b to host x + history (from history 0)"},
             "clocks": clk.summary(), "final_hist": float(fin["hist_full"][W + K])}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = eg_cpu_leg(s, workload_label(name), rows, sk, fac, B)
