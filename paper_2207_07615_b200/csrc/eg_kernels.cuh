@@ -11,7 +11,7 @@
 //   k_eg_row    identity sketch: one CTA swaps row i into the dense y (y_k = a_i), s^T r = r[i]
 //   k_eg_gauss  Gaussian sketch: s_i = binary32 normal (randomized projection's generator, r = 1),
 //               partials of s^T r; y = A^T s follows by the K2 segments
-//   k_eg_gemvT  partials of Y^T y and y^T y: 2D grid (2048-row ranges x 32-column groups), a warp
+//   k_eg_gemvT  partials of Y^T y and y^T y: 2D grid (4096-row ranges x 32-column groups), a warp
 //               per column, lanes over the rows (coalesced 256-byte reads of Y, y from L1), fixed
 //               butterfly per column
 //   k_eg_red    fixed-order sums of the partials (a warp per entry, many CTAs): g, y^T y, s^T r
@@ -37,7 +37,10 @@
 namespace plss {
 
 constexpr int EG_NT = 256;
-constexpr int EG_RT = 2048;              // rows per CTA of the Y^T y kernel (grid.x = row ranges)
+#ifndef PLSS_EG_RT
+#define PLSS_EG_RT 4096               // 2048: -1.6% engine step rate on C2 (scripts/gpu_egrt.sh)
+#endif
+constexpr int EG_RT = PLSS_EG_RT;        // rows per CTA of the Y^T y kernel (grid.x = row ranges)
 constexpr int EG_RT_SMALL = 512;         // ... while few column groups are active (small history)
 constexpr int EG_CT = 32;                // columns per CTA of the Y^T y kernel (grid.y = column groups)
 constexpr double EG_SKIP_REL = 1e-14;
