@@ -431,3 +431,23 @@ def test_true_residual_at_exit(pkg, name):
     if res["outcome"] == "converged":                 # recursive and true residual agree at the end
         assert t["rel"] <= 10 * s.tol + 1e-13
     pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("m,n", [(0, 5), (5, 0), (0, 0)])
+def test_degenerate_dimensions(pkg, m, n):
+    """Zero rows or columns: the ctx builds, b has no residual to reduce (||b|| = 0 or A^T r = 0),
+    the solve reports converged / y_vanished without launching a bad grid, the SpMVs are no-ops."""
+    s = plss_gen._finish("degenerate", m, n, np.zeros(m + 1, np.int64), np.zeros(0, np.int32), np.zeros(0), None,
+                         1e-8, 0, 5, b=np.ones(m))
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    assert res["iters"] == ref["iters"] == 0
+    assert res["outcome"] == ref["outcome"]
+    assert res["xh"].shape == (n,)
+    A = _matrix(pkg, s)
+    ctx = pkg.plss_create(A, maxit_cap=5, validate=True)
+    y = torch.empty(m, dtype=torch.float64, device="cuda")
+    v = torch.empty(n, dtype=torch.float64, device="cuda")
+    pkg.plss_spmv(ctx, torch.zeros(n, dtype=torch.float64, device="cuda"), y)
+    pkg.plss_spmvT(ctx, torch.zeros(m, dtype=torch.float64, device="cuda"), v)
+    pkg.plss_destroy(ctx)
