@@ -1,0 +1,55 @@
+"""CPU checks of bench.py's driver contract: the reference arm (the oracle on the host cores) prints
+one JSON line with the keys the driver reads, ranks > 0 of a torchrun launch print nothing and exit
+0, and our arm fails loudly on a machine without a GPU (no CPU fallback)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(args, env_extra=None, timeout=600):
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1")
+    env.update(env_extra or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, env=env,
+                          capture_output=True, text=True, timeout=timeout)
+
+
+def test_reference_arm_line():
+    r = _bench(["--impl", "reference", "--steps", "1", "--warmup", "1", "--workload", "C2"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "it/s" and d["higher_is_better"] is True
+    assert d["steps"] == 1 and d["warmup"] == 1
+    assert d["config"]["workload"].startswith("C2") and d["config"]["n"] == 100_000
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_other_ranks_silent():
+    r = _bench(["--impl", "reference", "--steps", "1", "--warmup", "1"],
+               {"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_our_arm_fails_loudly_without_gpu():
+    r = _bench(["--steps", "1", "--warmup", "3", "--workload", "C2"], timeout=300)
+    assert r.returncode != 0
+    assert r.stdout.strip() == ""                      # no JSON line from a CPU fallback
+
+
+def test_apportion():
+    sys.path.insert(0, ROOT)
+    import bench
+    kt = {"k1": 2.0, "k2": 3.0, "k3": 0.0}
+    assert bench._apportion(6.0, kt, "k2") == pytest.approx(3.6)
+    assert bench._apportion(6.0, {"k1": 0.0}, "k1") == 0.0
