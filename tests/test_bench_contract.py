@@ -53,3 +53,27 @@ def test_apportion():
     kt = {"k1": 2.0, "k2": 3.0, "k3": 0.0}
     assert bench._apportion(6.0, kt, "k2") == pytest.approx(3.6)
     assert bench._apportion(6.0, {"k1": 0.0}, "k1") == 0.0
+
+
+@pytest.mark.gpu
+def test_our_arm_line_on_gpu():
+    """Our arm on a small workload: one JSON line with the contract's keys (roofline, cpu_baseline,
+    e2e with its copy bytes, clocks, gpu_launches)."""
+    env = dict(os.environ)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "C2", "--steps", "20",
+                        "--warmup", "3"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] == 3
+    assert d["dtype"] == "f64" and d["data"] == "synthetic" and d["vs_baseline"] is None
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0 and 0 < rf["frac"] < 1.5
+    assert rf["frac"] == pytest.approx(rf["achieved"] / rf["peak"])
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 20 * 3
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
