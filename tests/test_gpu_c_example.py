@@ -26,3 +26,26 @@ def test_c_example_solves():
         out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
         assert out.returncode == 0, out.stdout + out.stderr
         assert "PLSS:" in out.stdout and "outcome 0" in out.stdout, out.stdout
+
+
+@pytest.mark.parametrize("partition,step", [("rows", "allreduce"), ("rows", "rsag"), ("rows", "peer"),
+                                            ("cols", "allreduce")])
+def test_dist_example_one_process(partition, step, tmp_path):
+    """examples/dist_solve.py under torchrun with one process (the pods have one GPU): every
+    partition / step converges and reports a true residual within the tolerance."""
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "examples", "dist_solve.py"), "--partition", partition, "--step", step],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [ln for ln in r.stdout.splitlines() if "GPU(s)" in ln]
+    assert line and "converged" in line[0], r.stdout
+    tr = float(line[0].split("true residual ")[1].split(",")[0])
+    assert tr <= 1e-7
