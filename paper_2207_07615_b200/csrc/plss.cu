@@ -299,6 +299,8 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
   else if (a.fmt == 3 && a.nlong > 0)
     k_sell<ROLE, 1024, true><<<grid, 1024, 0, st>>>(a);            // gsort: no y staging
+  else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort && a.sig == SIGMA_WIDE)
+    k_sell<ROLE, 1024, false, true, SIGMA_WIDE><<<grid, 1024, YSTAGE_SMEM_WIDE, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort)     // K2 with a sigma perm: staged y
     k_sell<ROLE, 1024, false, true><<<grid, 1024, YSTAGE_SMEM, st>>>(a);
   else if (a.fmt == 3)
@@ -512,6 +514,7 @@ static int env_int(const char* name, int dflt) {
 static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sms, int* grid_out) {
   if (a.fmt != 1) return PLSS_OK;
   const int nunits = a.nslices + a.nlong;
+  const int NSB = nsb_of(a.sig ? a.sig : SIGMA);     // the k_sell instantiation's block (a.sig)
   const int nblocks = (nunits + NSB - 1) / NSB;
   const int grid = std::max(1, std::min(std::min(nblocks, sms), MAXG));
   int32_t* cblk = pool.cblk + pool.used_c;
@@ -541,6 +544,7 @@ static plss_status make_chunks(plss_ctx* ctx, const SpmvSeg& a, SellPool& pool, 
   ctx->gch.clear();
   ctx->drows.clear();
   if (a.fmt != 3 || !a.perm || a.gsort || nch < 2) return PLSS_OK;
+  const int sigw = a.sig ? a.sig : SIGMA, SPW = sigw / 32;
   const int nwin = (a.nslices + SPW - 1) / SPW;
   nch = std::min(nch, std::min(nwin, DCH_MAX));
   if (nch < 2) return PLSS_OK;
@@ -551,7 +555,7 @@ static plss_status make_chunks(plss_ctx* ctx, const SpmvSeg& a, SellPool& pool, 
     b.sptr = a.sptr + sl0;
     b.perm = a.perm + (size_t)sl0 * 32;
     b.nslices = sl1 - sl0;
-    b.wrow0 = w0 * SIGMA;
+    b.wrow0 = w0 * sigw;
     b.fmt = 1;                                       // make_contig turns it into fmt 3 with its ranges
     b.uw = nullptr;
     int grid = 1;
@@ -559,7 +563,7 @@ static plss_status make_chunks(plss_ctx* ctx, const SpmvSeg& a, SellPool& pool, 
     if (st != PLSS_OK) return st;
     ctx->dch.push_back(b);
     ctx->gch.push_back(grid);
-    ctx->drows.push_back((int64_t)w0 * SIGMA);
+    ctx->drows.push_back((int64_t)w0 * sigw);
   }
   ctx->drows.push_back(ctx->n + 1);                  // the last chunk's all-reduce carries rho too
   CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
@@ -701,7 +705,8 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   return PLSS_OK;
 }
 
-static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool, int sms, int occ) {
+static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool, int sms, int occ,
+                            bool wide_ok = false) {
   cudaStream_t st = ctx->stream;
   const int64_t nrows = a.nrows;
   const int64_t nsl = (nrows + 31) / 32;
@@ -716,10 +721,18 @@ static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool
   k_row_len<<<g, 256, 0, st>>>(a.ptr, nrows, len);
   int64_t steps = 0;
   const int32_t* use_perm = nullptr;
-  for (int pass = 0; pass < 2; ++pass) {
+  // pass 0: no sort; 1: sigma windows of SIGMA rows; 2 (K2 segments): of SIGMA_WIDE rows (sparse
+  // columns of power-law matrices: C4 0.335 vs 0.355 ms per step)
+  const int npass = wide_ok ? 3 : 2;
+  a.sig = 0;
+  for (int pass = 0; pass < npass; ++pass) {
     if (pass == 1) {
-      k_sigma_sort<<<(unsigned)((nrows + SIGMA - 1) / SIGMA), SIGMA_NT, 0, st>>>(len, nrows, nsl * 32, perm);
+      k_sigma_sort<SIGMA><<<(unsigned)((nrows + SIGMA - 1) / SIGMA), SIGMA_NT, 0, st>>>(len, nrows, nsl * 32, perm);
       use_perm = perm;
+    } else if (pass == 2) {
+      k_sigma_sort<SIGMA_WIDE><<<(unsigned)((nrows + SIGMA_WIDE - 1) / SIGMA_WIDE), SIGMA_NT, 0, st>>>(len, nrows,
+                                                                                                   nsl * 32, perm);
+      a.sig = SIGMA_WIDE;
     }
     k_slice_len<<<gs, 256, 0, st>>>(len, use_perm, nrows, nsl, sp);
     if (scan_excl(ctx, sp, nsl + 1, blk) != PLSS_OK) return PLSS_E_CUDA;
@@ -731,7 +744,7 @@ static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool
     const int64_t padded = steps * 32 - (nsl * 32 - nrows) * (int64_t)(tot[1] - tot[0]);
     const double limit = pass == 0 ? 1.03 : 1.15;
     if ((double)padded <= limit * (double)nnz_seg + 1024.0) break;
-    if (pass == 1) return try_sell_global(ctx, a, nnz_seg, pool);   // power-law rows
+    if (pass == npass - 1) { a.sig = 0; return try_sell_global(ctx, a, nnz_seg, pool); }   // power-law rows
   }
   if (pool.used + steps * 32 > pool.cap) return PLSS_OK;
   int32_t* sidx = pool.idx + pool.used;
@@ -897,6 +910,10 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
                             YSTAGE_SMEM));
     CK(cudaFuncSetAttribute(k_sell<ROLE_K2DOTS, 1024, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             YSTAGE_SMEM));
+    CK(cudaFuncSetAttribute(k_sell<ROLE_K2, 1024, false, true, SIGMA_WIDE>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_SMEM_WIDE));
+    CK(cudaFuncSetAttribute(k_sell<ROLE_K2DOTS, 1024, false, true, SIGMA_WIDE>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, YSTAGE_SMEM_WIDE));
   }
   // Shared-memory windows (fmt 2) are opt-in: correct and bit-exact, but on every config measured
   // slower than L1-cached gathers ("Windows"). opt.flags bit1 disables them
@@ -1025,7 +1042,9 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     t2off += nt + 1;
     ctx->g2[s] = grid_for(nt, occ[a.finalize ? ROLE_K2DOTS : ROLE_K2], sms);
     if (L.sell) {
-      if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool2, sms, occ_sell) != PLSS_OK) return PLSS_E_CUDA;
+      if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool2, sms, occ_sell, win2 == 0 && env_int("PLSS_SIGWIDE", 1))
+          != PLSS_OK)
+        return PLSS_E_CUDA;
       if (a.fmt == 1) ctx->g2[s] = sell_grid(a);
       if (try_window(ctx, a, a.g, ctx->R[s + 1] - ctx->R[s], ctx->E[s + 1] - ctx->E[s], win2, nsb2, pool2, sms,
                      &ctx->g2[s]) != PLSS_OK)

@@ -105,6 +105,8 @@ struct SpmvSeg {
   // ring of `ring` doubles in shared memory, every other entry from global memory
   int32_t win, ring, nblocks, glen, nsb;
   int32_t row0;              // first row of this segment in the matrix (ablation experiments only)
+  int32_t sig;               // sigma window of this segment's sort: 0 = SIGMA, or SIGMA_WIDE (K2
+                             // segments whose SIGMA windows leave too much padding, C4's columns)
   int32_t wrow0;             // first row of the segment's sigma window 0 (0; a column chunk of a K2
                              // segment, see plss.cu make_chunks, starts at a later window)
   // Globally length-sorted SELL (power-law rows, fmt 3 only): perm is a global row order, rows
@@ -605,6 +607,9 @@ constexpr int NSB = SPW > 16 ? SPW : 16;
 // and the ring of per-window staging decisions (YD windows)
 constexpr int YQ = PLSS_YQ;
 constexpr int YSTAGE_SMEM = YQ * SIGMA * 8;
+constexpr int SIGMA_WIDE = 2 * SIGMA;    // the wider window a K2 segment may take (a.sig)
+constexpr int YSTAGE_SMEM_WIDE = YQ * SIGMA_WIDE * 8;
+__host__ __device__ constexpr int nsb_of(int sig) { return sig / 32 > 16 ? sig / 32 : 16; }
 constexpr int YD = 1024;
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
@@ -708,8 +713,11 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 // Slice metadata (start, length, this lane's row) is loaded one slice ahead, so a slice's stream
 // loads wait for DRAM only, not for an L2 round trip to sptr / perm first.
 // LU: the segment has long-row units (gsort); YS: the K2 segment's y is staged (sigma perm)
-template <int ROLE, int BS = NT, bool LU = false, bool YS = false>
+template <int ROLE, int BS = NT, bool LU = false, bool YS = false, int SIGT = SIGMA>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
+  constexpr int SPW = SIGT / 32;                 // this instantiation's sigma window (a.sig)
+  constexpr int NSB = nsb_of(SIGT);
+  constexpr int SIGMA = SIGT;
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
   constexpr int P = DYN ? PLSS_PAIR : 1;         // slices per warp unit
@@ -1305,6 +1313,7 @@ __global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
 }
 // sigma-sort: within each window of SIGMA rows, slots ordered by length descending (stable)
 constexpr int SIGMA_NT = SIGMA < 256 ? SIGMA : 256;   // threads of the sigma-sort kernel
+template <int SIGMA = plss::SIGMA>
 __global__ void __launch_bounds__(SIGMA_NT) k_sigma_sort(const int32_t* len, long long nrows, long long nslots,
                                                          int32_t* perm) {
   // stable radix sort of the window by (length descending, row ascending); missing rows last
