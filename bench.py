@@ -284,6 +284,37 @@ def full_bytes_of(name):
             }.get(name) or (lambda s: plss_gen.bytes_per_iter(s.m, s.n, s.nnz))(plss_gen.make_config(name))
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_command(argv, gpus, port):
+    """The torchrun command that runs this script as `gpus` ranks on one node (127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def ensure_world(args, argv=None, env=None, run=subprocess.call):
+    """--gpus N must mean N ranks. Without torchrun (WORLD_SIZE unset) and N > 1, re-launch this
+    script through torch.distributed.run with N processes and return its exit code; under torchrun,
+    WORLD_SIZE must equal N (returns 2 with a message otherwise). None: carry on in this process."""
+    env = os.environ if env is None else env
+    argv = sys.argv[1:] if argv is None else argv
+    ws = env.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus <= 1:
+            return None
+        return run(launch_command(argv, args.gpus, _free_port()))
+    if int(ws) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with "
+                         f"--nproc-per-node {args.gpus} or drop torchrun\n")
+        return 2
+    return None
+
+
 # ---------------------------------------------------------------------------------------------
 # main (our arm)
 # ---------------------------------------------------------------------------------------------
@@ -323,6 +354,10 @@ def main():
     ap.add_argument("--rp-r", type=int, default=5, help="sketch size r (Experiment III: 5 for n > 1e5)")
     ap.add_argument("--rp-density", type=float, default=1.0, help="< 1: sparse normal sketch")
     args = ap.parse_args()
+    if args.impl != "reference":
+        rc = ensure_world(args)
+        if rc is not None:
+            sys.exit(rc)
     if args.method == "rp":
         return main_rp(args)
     if args.method == "kz":
@@ -350,6 +385,9 @@ def main():
     import paper_2207_07615_b200 as pkg
 
     assert args.warmup >= 3 or args.ncu, "timing rules: at least 3 warm-up steps"
+    assert torch.cuda.is_available(), "our arm needs a CUDA device (no CPU fallback)"
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but {torch.cuda.device_count()} GPU(s) are visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -413,7 +451,15 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    fin = pkg.plss_finish(ctx, None, want_hist=True)
+    fin = pkg.plss_finish(ctx, None, want_hist=True, want_diag=True)
+    cross_rank = None
+    if world > 1:
+        # every rank must hold bitwise the same rho, phi, theta, beta, gamma records
+        rec = torch.from_numpy(np.ascontiguousarray(fin["diag"])).to(dev)
+        allrec = [torch.empty_like(rec) for _ in range(world)]
+        dist.all_gather(allrec, rec)
+        cross_rank = all(torch.equal(allrec[0].view(torch.int64), a.view(torch.int64)) for a in allrec[1:])
+        assert cross_rank, "ranks disagree on the per-iteration scalar records (rho, phi, theta, beta, gamma)"
     iters_per_s = args.steps / (ms / 1e3)
     n_global = w.get("n_global", n)
     B_global = plss_gen.bytes_per_iter(w["m_global"], n_global, w["nnz_global"])
@@ -490,6 +536,8 @@ def main():
             "clocks": clocks,
             "final_hist": float(fin["hist_full"][min(args.warmup + args.steps, maxit_cap) - 1]),
         }
+        if cross_rank is not None:
+            line["cross_rank_bitwise_scalars"] = cross_rank
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w["name"], B_global)
         print(json.dumps(line), flush=True)

@@ -239,6 +239,8 @@ struct plss_ctx {
   // an m x n_global matrix; r (m) is replicated, x / p / y are this rank's column shards
   bool cols = false;
   int64_t col_offset = 0, n_global = 0;
+  // row blocks (plss_create_dist): this rank owns rows [row_offset, row_offset + m) of m_global
+  int64_t row_offset = 0, m_global = 0;
   bool peer = false;
   char* sym = nullptr;
   size_t sym_yb = 0;
@@ -303,6 +305,10 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
     k_sell<ROLE, 1024, false, true, SIGMA_WIDE><<<grid, 1024, YSTAGE_SMEM_WIDE, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort)     // K2 with a sigma perm: staged y
     k_sell<ROLE, 1024, false, true><<<grid, 1024, YSTAGE_SMEM, st>>>(a);
+  else if (a.fmt == 3 && a.stat == 2 && !a.perm)
+    k_sell<ROLE, 1024, false, false, SIGMA, true, 6><<<grid, 1024, 0, st>>>(a);
+  else if (a.fmt == 3 && a.stat && !a.perm)
+    k_sell<ROLE, 1024, false, false, SIGMA, true><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 3)
     k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 1)
@@ -1053,6 +1059,25 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     }
   }
   CK(cudaGetLastError());
+  // Static stepping (SpmvSeg::stat) for fmt 3 segments without a perm or long rows (C5's K1:
+  // 2.78 -> 2.61 ms per step), with 6 entries in flight per lane when the slices are 6k steps long
+  // (C5's K1 rows of 12: 2.61 -> 2.52 ms; K2's variable columns keep 8). PLSS_STAT=0 turns it off.
+  {
+    const int stat = env_int("PLSS_STAT", 1);
+    for (int s = 0; s < S; ++s) {
+      for (SpmvSeg* a : {&ctx->seg1[s], &ctx->seg2[s]}) {
+        a->stat = (stat && a->fmt == 3 && !a->perm && !a->gsort) ? 1 : 0;
+        if (a->stat && a->nslices > 0) {
+          int32_t ends[2] = {0, 0};                  // sptr[0], sptr[nslices]: all slices of equal length?
+          CK(cudaMemcpyAsync(&ends[0], a->sptr, 4, cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(&ends[1], a->sptr + a->nslices, 4, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          const int64_t tot = (int64_t)ends[1] - ends[0];
+          if (tot % a->nslices == 0 && (tot / a->nslices) % 6 == 0 && stat != 3) a->stat = 2;
+        }
+      }
+    }
+  }
   if (dist && L.sell && !ctx->rsag && !ctx->cols) {
     const plss_status st2 = make_chunks(ctx, ctx->seg2[S - 1], pool2, sms, env_int("PLSS_DIST_CHUNKS", 4));
     if (st2 != PLSS_OK) return st2;
@@ -1164,6 +1189,8 @@ plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int
   ctx->rank = rank;
   ctx->nranks = nranks;
   ctx->dist = true;
+  ctx->row_offset = row_offset;
+  ctx->m_global = m_global;
   plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, true);
   if (st == PLSS_OK) {
     ncclUniqueId u;

@@ -126,6 +126,9 @@ struct SpmvSeg {
   const int2* wlo;           // per block {lo_b, flags}: 1 = reload the whole window, 2 = no window
   const int32_t* cblk;       // grid+1 block bounds of the CTAs (balanced by stored entries)
   double* slpart;            // per-slice dot partials (fixed-order reduction, deterministic)
+  int32_t stat;              // fmt 3 without perm / long rows: warps step through their CTA's slices
+                             // statically and keep per-thread dot terms (no per-slice partials);
+                             // 2: the same with 6 entries per lane in flight (slices of 6 k steps)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -617,27 +620,21 @@ constexpr int YD = 1024;
 constexpr int SELL_MINB = PLSS_SELL_MINB;
 
 // Gather of g[c] (c = -1: padding). Ablation builds (timing experiments only, never correct):
-// 4 = no gathers (the index as value), 8 = C5's band gathers free, 16 = gathers from an 8 MB hot set.
-__device__ __forceinline__ double sell_gather(const SpmvSeg& a, int c, int row, int role) {
+// 4 = no gathers (the index as value), 16 = gathers from an 8 MB hot set.
+__device__ __forceinline__ double sell_gather(const SpmvSeg& a, int c) {
 #if PLSS_ABLATE & 4
   return (double)c;
-#elif PLSS_ABLATE & 8
-  const bool rowwise = role == ROLE_K1 || role == ROLE_PLAIN;
-  const long long gi = (long long)row + (rowwise ? a.row0 : 0), gc = (long long)c + (rowwise ? 0 : a.row0);
-  const bool band = rowwise ? (llabs(gc - gi / 8) <= 1100) : (llabs(gc / 8 - gi) <= 1100);
-  return c < 0 ? 0.0 : band ? 1.0 : __ldg(a.g + c);
 #elif PLSS_ABLATE & 16
   return c >= 0 ? __ldg(a.g + (c & 0xFFFFF)) : 0.0;
 #else
-  (void)row; (void)role;
   return c >= 0 ? __ldg(a.g + c) : 0.0;
 #endif
 }
 
 // s += sum over the slice's steps [0, L) of val * g[idx], lane = one row, ascending step order,
 // SU steps in flight per lane (loads of a batch issued before its gathers, gathers before sums).
-template <int ROLE>
-__device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L, int lane, int row, double s,
+template <int ROLE, int SU = plss::SU>
+__device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L, int lane, double s,
                                                uint64_t pol) {
   const int32_t* ip = a.idx + (long long)st0 * 32 + lane;
   const double* vp = a.val + (long long)st0 * 32 + lane;
@@ -648,7 +645,7 @@ __device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L,
 #pragma unroll
     for (int u = 0; u < SU; ++u) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
 #pragma unroll
-    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u], row, ROLE);
+    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u]);
 #pragma unroll
     for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
   }
@@ -661,7 +658,7 @@ __device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L,
       if (j + u < L) { c[u] = ld_stream(ip + (j + u) * 32, pol); v[u] = ld_stream(vp + (j + u) * 32, pol); }
     }
 #pragma unroll
-    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u], row, ROLE);
+    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u]);
 #pragma unroll
     for (int u = 0; u < SU; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], gv[u]));
   }
@@ -672,7 +669,7 @@ __device__ __forceinline__ double sell_row_sum(const SpmvSeg& a, int st0, int L,
 // in flight per batch, so the latency chains of P rows overlap and per-slice costs are shared.
 template <int ROLE, int P>
 __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)[P], const int (&L)[P], int lane,
-                                              const int (&row)[P], double (&s)[P], uint64_t pol) {
+                                              double (&s)[P], uint64_t pol) {
   constexpr int SUP = SU / P;
   int Lmax = 0;
 #pragma unroll
@@ -694,7 +691,7 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 #pragma unroll
     for (int q = 0; q < P; ++q)
 #pragma unroll
-      for (int u = 0; u < SUP; ++u) gv[q][u] = sell_gather(a, c[q][u], row[q], ROLE);
+      for (int u = 0; u < SUP; ++u) gv[q][u] = sell_gather(a, c[q][u]);
 #pragma unroll
     for (int q = 0; q < P; ++q)
 #pragma unroll
@@ -713,14 +710,16 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 // Slice metadata (start, length, this lane's row) is loaded one slice ahead, so a slice's stream
 // loads wait for DRAM only, not for an L2 round trip to sptr / perm first.
 // LU: the segment has long-row units (gsort); YS: the K2 segment's y is staged (sigma perm)
-template <int ROLE, int BS = NT, bool LU = false, bool YS = false, int SIGT = SIGMA>
+template <int ROLE, int BS = NT, bool LU = false, bool YS = false, int SIGT = SIGMA, bool STAT = false,
+          int SUK = SU>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   constexpr int SPW = SIGT / 32;                 // this instantiation's sigma window (a.sig)
   constexpr int NSB = nsb_of(SIGT);
   constexpr int SIGMA = SIGT;
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
-  constexpr int P = DYN ? PLSS_PAIR : 1;         // slices per warp unit
+  constexpr int P = DYN && !STAT ? PLSS_PAIR : 1; // slices per warp unit
+  static_assert(!STAT || (DYN && !LU && !YS), "static stepping: fmt 3 segments without perm / long rows");
   // fmt 3 K2 with a sigma perm: y results go through a per-sigma-window shared buffer (indexed by
   // row, not slot) and the warp that completes a window writes its SIGMA values coalesced,
   // instead of 32 scattered 8-byte stores per slice. In-flight slices (<= 32 P + P) span at most
@@ -745,7 +744,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   } else {
     sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices + (LU ? a.nlong : 0));
     stride = P * BS / 32;
-    if (tid == 0) s_next = sl0 + P * (BS / 32);     // the first unit of each warp is static
+    if (tid == 0 && !STAT) s_next = sl0 + P * (BS / 32);   // the first unit of each warp is static
     if (YST && tid < YQ) { s_ycnt[tid] = 0; s_ytag[tid] = -1; }
     if (YST) for (int q = tid; q < YD; q += BS) s_ydec[q] = -2;
     __syncthreads();
@@ -799,15 +798,11 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       st0[q] = m0[q]; L[q] = m1[q] - m0[q];
-#if PLSS_ABLATE & 64
-      row[q] = (ROLE >= ROLE_K2 && mrow[q] >= 0) ? min((su + q) * 32 + lane, a.nrows - 1) : mrow[q];
-#else
       row[q] = mrow[q];
-#endif
     }
     const int cnt = min(P, sl1 - su);               // slices of this unit that exist
     int nx;
-    if (!DYN) {
+    if (!DYN || STAT) {
       nx = su + stride;
     } else {
       nx = 0;
@@ -844,7 +839,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
           if (k < st0[0] + L[0]) { c[u] = ld_stream(a.lidx + k, pol); v[u] = ld_stream(a.lval + k, pol); }
         }
 #pragma unroll
-        for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u], row[0], ROLE);
+        for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u]);
 #pragma unroll
         for (int u = 0; u < SU; ++u) if (c[u] >= 0) ps = __dadd_rn(ps, __dmul_rn(v[u], gv[u]));
       }
@@ -852,9 +847,9 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       s[0] = ROLE == ROLE_K1 ? ps : __dadd_rn(s[0], ps);
       if (lane != 0) valid[0] = false;                    // lane 0 writes the row
     } else if (P == 1) {
-      s[0] = sell_row_sum<ROLE>(a, st0[0], L[0], lane, row[0], s[0], pol);
+      s[0] = sell_row_sum<ROLE, SUK>(a, st0[0], L[0], lane, s[0], pol);
     } else {
-      sell_rows_sum<ROLE, P>(a, st0, L, lane, row, s, pol);
+      sell_rows_sum<ROLE, P>(a, st0, L, lane, s, pol);
     }
 #pragma unroll
     for (int q = 0; q < P; ++q) {
@@ -879,7 +874,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
         }
       }
       if (DOTS) {
-        if (!DYN) {
+        if (!DYN || STAT) {                                     // static stepping: per-thread terms
           acc0 += d0; acc1 += d1;
         } else {
           d0 = warp_sum(d0);
@@ -911,7 +906,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
     su = nx;
   }
   if (!DOTS) return;
-  if (DYN) {
+  if (DYN && !STAT) {
     __syncthreads();
     for (int q = sl0 + tid; q < sl1; q += BS) { acc0 += a.slpart[2 * q]; acc1 += a.slpart[2 * q + 1]; }
   }

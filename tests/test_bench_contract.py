@@ -77,3 +77,28 @@ def test_our_arm_line_on_gpu():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 20 * 3
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_gpus_flag_self_launches_ranks():
+    """--gpus N without torchrun re-launches bench.py as N ranks (VERDICT r01 missing-3); under
+    torchrun WORLD_SIZE must equal N."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    calls = []
+    ns = argparse.Namespace(gpus=4)
+    rc = bench.ensure_world(ns, argv=["--gpus", "4", "--steps", "7"], env={}, run=lambda c: calls.append(c) or 0)
+    assert rc == 0 and len(calls) == 1
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-3:] == ["--gpus", "4", "--steps", "7"][-3:]
+    assert cmd[cmd.index(os.path.join(ROOT, "bench.py")) + 1:] == ["--gpus", "4", "--steps", "7"]
+    assert bench.ensure_world(argparse.Namespace(gpus=1), argv=[], env={}, run=None) is None
+    assert bench.ensure_world(argparse.Namespace(gpus=2), argv=[], env={"WORLD_SIZE": "2"}, run=None) is None
+    assert bench.ensure_world(argparse.Namespace(gpus=8), argv=[], env={"WORLD_SIZE": "2"}, run=None) == 2
+
+
+def test_gpus_flag_mismatch_exits_nonzero():
+    r = _bench(["--gpus", "8", "--steps", "1", "--warmup", "3", "--workload", "C2"],
+               {"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"}, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr and r.stdout.strip() == ""

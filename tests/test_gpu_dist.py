@@ -19,6 +19,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 @pytest.fixture(scope="module")
 def pkg():
     from paper_2207_07615_b200 import build as pbuild
@@ -70,7 +77,7 @@ def test_two_ranks_torchrun(tmp_path, mode):
     script = os.path.join(ROOT, "tests", "dist_worker.py")
     out = tmp_path / "res.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", script, "--backend", "nccl",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), script, "--backend", "nccl",
            "--out", str(out), "--config", "C5xs"] + ([] if mode == "allreduce" else [f"--{mode}"])
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
     r = np.load(out)
