@@ -35,7 +35,7 @@ OUTCOMES = {0: "converged", 1: "maxit", 2: "y_vanished", 3: "stagnation"}
 def build(force: bool = False) -> str:
     """Compile the C oracle with gcc (no FMA contraction, no fast-math)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                _SRC, "-o", _LIB_PATH + ".tmp", "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
@@ -54,6 +54,8 @@ def _load():
                                     ctypes.c_double, ctypes.c_int, ctypes.c_int32, ctypes.c_int,
                                     ctypes.c_double, P, P, P, P]
         lib.oracle_column_norms.argtypes = [ctypes.c_int64, P, P, P]
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        lib.oracle_get_threads.restype = ctypes.c_int
         lib.oracle_plss.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -69,6 +71,23 @@ def _i32(a):
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class threads:
+    """Context manager: run the oracle on `t` host threads (oracle_set_threads; t = 1 is the
+    sequential oracle). `t = None` or 0: all host cores (os.cpu_count())."""
+
+    def __init__(self, t=None):
+        self.t = int(t) if t else (os.cpu_count() or 1)
+
+    def __enter__(self):
+        lib = _load()
+        self.prev = lib.oracle_get_threads()
+        lib.oracle_set_threads(self.t)
+        return self
+
+    def __exit__(self, *a):
+        _load().oracle_set_threads(self.prev)
 
 
 def spmv(m, row_ptr, col_idx, val, x):

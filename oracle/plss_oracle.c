@@ -7,9 +7,17 @@
  * reference arm and __graft_entry__.smoke() to check the CUDA path. It shares no code, header,
  * table or constant generator with paper_2207_07615_b200/ and must never be linked into it.
  *
- * Compile: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC (see oracle/__init__.py).
+ * Compile: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC (oracle/__init__.py).
  * All sums are sequential in ascending index order, no FMA contraction, no compensated summation
  * ("All arithmetic in binary64; no extended-precision accumulation").
+ *
+ * Threads (oracle_set_threads, default 1 = the sequential oracle): with T > 1 the row / column
+ * loops and the element-wise updates are split statically over T threads -- every output element
+ * is still one sequential ascending sum computed by one thread, so A x, A^T u and every vector
+ * update are bitwise those of T = 1 -- and a dot product is T fixed blocks [len t/T, len (t+1)/T),
+ * each summed sequentially, then the T partials summed in block order: deterministic for a given T,
+ * a different (equally valid) summation order than T = 1. Used for the full-size parity tests and
+ * the host-core baseline (SURVEY 8(d) oracle_omp); pinned against T = 1 in tests/test_oracle_pins.py.
  *
  * Readings of the paper used here (listed in DESIGN.md "Readings"):
  *  R1  gamma = (theta/rho)*beta as in Algorithm 1 line "gamma_k=(theta_k/rho_k)*beta_k"
@@ -29,6 +37,15 @@
 #include <stdint.h>
 #include <string.h>
 #include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int g_threads = 1;
+
+/* Number of host threads of the oracle (1: sequential). */
+void oracle_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
+int oracle_get_threads(void) { return g_threads; }
 
 #define OR_CONVERGED 0
 #define OR_MAXIT 1
@@ -52,6 +69,7 @@ void oracle_column_norms(int64_t n, const int32_t *col_ptr, const double *val_t,
 /* y = A x over CSR: y_i = sum_j a_ij x_j in ascending j ("matvec"). */
 void oracle_spmv(int64_t m, const int32_t *row_ptr, const int32_t *col_idx, const double *val,
                  const double *x, double *y) {
+    #pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
     for (int64_t i = 0; i < m; ++i) {
         double s = 0.0;
         for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) s = s + val[k] * x[col_idx[k]];
@@ -62,6 +80,7 @@ void oracle_spmv(int64_t m, const int32_t *row_ptr, const int32_t *col_idx, cons
 /* v = A^T u over the CSC copy: v_j = sum_i a_ij u_i in ascending i. */
 void oracle_spmvT(int64_t n, const int32_t *col_ptr, const int32_t *row_idx, const double *val_t,
                   const double *u, double *v) {
+    #pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
     for (int64_t j = 0; j < n; ++j) {
         double s = 0.0;
         for (int64_t k = col_ptr[j]; k < col_ptr[j + 1]; ++k) s = s + val_t[k] * u[row_idx[k]];
@@ -69,18 +88,30 @@ void oracle_spmvT(int64_t n, const int32_t *col_ptr, const int32_t *row_idx, con
     }
 }
 
-static double dot(int64_t len, const double *a, const double *b) {
+/* sum_i a_i b_i (b = NULL: a_i wi_i a_i with wi = w, or a_i a_i) over [lo, hi), ascending */
+static double dot_range(int64_t lo, int64_t hi, const double *a, const double *b, const double *w) {
     double s = 0.0;
-    for (int64_t i = 0; i < len; ++i) s = s + a[i] * b[i];
+    for (int64_t i = lo; i < hi; ++i) s = s + a[i] * (b ? b[i] : (w ? w[i] * a[i] : a[i]));
     return s;
 }
 
-/* theta = p^T (WI p) with WI = diag(wi), or p^T p when wi is NULL (Alg. 1 L796, L812) */
-static double wdot(int64_t len, const double *p, const double *wi) {
+/* T = 1: one sequential sum. T > 1: T fixed blocks summed in block order (see the header). */
+static double dot_blocks(int64_t len, const double *a, const double *b, const double *w) {
+    const int T = g_threads;
+    if (T <= 1) return dot_range(0, len, a, b, w);
+    double *part = (double *)malloc(sizeof(double) * (size_t)T);
+    #pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; ++t) part[t] = dot_range(len * t / T, len * (t + 1) / T, a, b, w);
     double s = 0.0;
-    for (int64_t i = 0; i < len; ++i) s = s + p[i] * (wi ? wi[i] * p[i] : p[i]);
+    for (int t = 0; t < T; ++t) s = s + part[t];
+    free(part);
     return s;
 }
+
+static double dot(int64_t len, const double *a, const double *b) { return dot_blocks(len, a, b, NULL); }
+
+/* theta = p^T (WI p) with WI = diag(wi), or p^T p when wi is NULL (Alg. 1 L796, L812) */
+static double wdot(int64_t len, const double *p, const double *wi) { return dot_blocks(len, p, NULL, wi); }
 
 /*
  * Algorithm 1, following SURVEY.md 8(c)'s transcription. wi (nullable, n):
@@ -152,6 +183,7 @@ int oracle_plss(int64_t m, int64_t n,
         double *rk = rec ? rec + (size_t)iters * REC : NULL;
         /* r = r - A p  (L801, eq:recRes) */
         oracle_spmv(m, row_ptr, col_idx, val, p, Ap);
+        #pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
         for (int64_t i = 0; i < m; ++i) r[i] = r[i] - Ap[i];
         rho = dot(m, r, r);                                     /* L804 */
         h = sqrt(rho) / nbd;
@@ -165,6 +197,7 @@ int oracle_plss(int64_t m, int64_t n,
         }
         /* y = A^T r; WIy = WI \ y; phi = y^T WIy; psi = y^T p_{k-1}  (L802, L805-806; L671-672) */
         oracle_spmvT(n, col_ptr, row_idx, val_t, r, y);
+        #pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
         for (int64_t j = 0; j < n; ++j) wy[j] = wi ? y[j] / wi[j] : y[j];
         phi = dot(n, y, wy);
         double psi = dot(n, y, p);
@@ -185,8 +218,10 @@ int oracle_plss(int64_t m, int64_t n,
             }
         }
         /* p = beta p + gamma WIy; theta = p^T (WI p); x = x + p  (L811-813) */
+        #pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
         for (int64_t j = 0; j < n; ++j) p[j] = beta * p[j] + gamma * wy[j];
         theta = wdot(n, p, wi);
+        #pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
         for (int64_t j = 0; j < n; ++j) x[j] = x[j] + p[j];
         if (P_out) for (int64_t j = 0; j < n; ++j) P_out[(size_t)iters * n + j] = p[j];
         iters += 1;

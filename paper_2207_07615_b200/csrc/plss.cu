@@ -24,6 +24,8 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 using namespace plss;
@@ -241,6 +243,11 @@ struct plss_ctx {
   int64_t col_offset = 0, n_global = 0;
   // row blocks (plss_create_dist): this rank owns rows [row_offset, row_offset + m) of m_global
   int64_t row_offset = 0, m_global = 0;
+  // NCCL failure detection (dist_wait): the communicator was aborted after an asynchronous error
+  // or a wait timeout; every later call on this ctx fails with PLSS_E_NCCL
+  bool aborted = false;
+  int fault_nccl = 0;            // PLSS_FAULT_NCCL=1 (tests): the first poll reports an error
+  double wait_timeout_s = 600.0; // PLSS_WAIT_TIMEOUT_S
   bool peer = false;
   char* sym = nullptr;
   size_t sym_yb = 0;
@@ -1191,6 +1198,8 @@ plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int
   ctx->dist = true;
   ctx->row_offset = row_offset;
   ctx->m_global = m_global;
+  ctx->fault_nccl = env_int("PLSS_FAULT_NCCL", 0);
+  ctx->wait_timeout_s = env_int("PLSS_WAIT_TIMEOUT_S", 600);
   plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, true);
   if (st == PLSS_OK) {
     ncclUniqueId u;
@@ -1220,6 +1229,8 @@ plss_status plss_create_dist_cols(const plss_matrix* A_local, int64_t col_offset
   ctx->cols = true;
   ctx->col_offset = col_offset;
   ctx->n_global = n_global;
+  ctx->fault_nccl = env_int("PLSS_FAULT_NCCL", 0);
+  ctx->wait_timeout_s = env_int("PLSS_WAIT_TIMEOUT_S", 600);
   plss_status st = setup(ctx, A_local, opt, workspace, ws_bytes, cuda_stream, true);
   if (st == PLSS_OK) {
     ncclUniqueId u;
@@ -1233,9 +1244,50 @@ plss_status plss_create_dist_cols(const plss_matrix* A_local, int64_t col_offset
   return PLSS_OK;
 }
 
+// Wait for an event (or, ev = NULL, the stream). On a distributed ctx the wait polls the
+// communicator's asynchronous error state (failure detection): on an error -- or after
+// PLSS_WAIT_TIMEOUT_S seconds (default 600) without completion, e.g. a rank that died before its
+// collective -- the communicator is aborted (ncclCommAbort makes the pending collectives return),
+// the call fails with PLSS_E_NCCL and the ctx stays unusable until plss_destroy.
+static plss_status dist_wait(plss_ctx* ctx, cudaStream_t st, cudaEvent_t ev) {
+  if (!ctx->dist || !ctx->comm) {
+    if (ev) CK(cudaEventSynchronize(ev)); else CK(cudaStreamSynchronize(st));
+    return PLSS_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = ev ? cudaEventQuery(ev) : cudaStreamQuery(st);
+    if (q != cudaSuccess && q != cudaErrorNotReady) CK(q);
+    ncclResult_t a = ncclSuccess;
+    const ncclResult_t r = ncclCommGetAsyncError(ctx->comm, &a);
+    if (ctx->fault_nccl) a = ncclSystemError;
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const bool timeout = ctx->wait_timeout_s > 0 && el > ctx->wait_timeout_s;
+    if (r != ncclSuccess || (a != ncclSuccess && a != ncclInProgress) || timeout) {
+      ncclCommAbort(ctx->comm);
+      ctx->comm = nullptr;
+      ctx->aborted = true;
+      cudaStreamSynchronize(st);                     // the aborted collectives return
+      cudaGetLastError();
+      set_err(ctx, timeout ? std::string("collective did not complete within PLSS_WAIT_TIMEOUT_S; communicator aborted")
+                           : std::string("NCCL asynchronous error: ") + ncclGetErrorString(r != ncclSuccess ? r : a) +
+                                 "; communicator aborted");
+      return PLSS_E_NCCL;
+    }
+    if (q == cudaSuccess) return PLSS_OK;
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+static plss_status check_live(plss_ctx* ctx) {
+  if (ctx->aborted) { set_err(ctx, "the communicator was aborted after an NCCL failure; destroy the ctx"); return PLSS_E_NCCL; }
+  return PLSS_OK;
+}
+
 plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
                        int32_t maxit, int32_t flags) {
   if (!ctx) return PLSS_E_INVALID;
+  if (check_live(ctx) != PLSS_OK) return PLSS_E_NCCL;
   if (!(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap || (tol_mode != 0 && tol_mode != 1) ||
       (flags & ~1) != 0) {
     set_err(ctx, "invalid tol / tol_mode / maxit / flags");
@@ -1300,6 +1352,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
 
 plss_status plss_step(plss_ctx* ctx, int32_t k) {
   if (!ctx) return PLSS_E_INVALID;
+  if (check_live(ctx) != PLSS_OK) return PLSS_E_NCCL;
   if (!ctx->started) { set_err(ctx, "plss_step before plss_start"); return PLSS_E_STATE; }
   if (k < 0) return PLSS_E_INVALID;
   for (int i = 0; i + ctx->chunk <= k; i += ctx->chunk) CK(cudaGraphLaunch(ctx->graph_chunk, ctx->stream));
@@ -1310,6 +1363,7 @@ plss_status plss_step(plss_ctx* ctx, int32_t k) {
 plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
                         plss_outcome* outcome) {
   if (!ctx) return PLSS_E_INVALID;
+  if (check_live(ctx) != PLSS_OK) return PLSS_E_NCCL;
   if (!ctx->started) { set_err(ctx, "plss_finish before plss_start"); return PLSS_E_STATE; }
   cudaStream_t st = ctx->stream;
   if (ctx->rsag)                                    // x lives as column shards: gather (collective)
@@ -1325,7 +1379,10 @@ plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, 
   unsigned peer_err = 0;
   if (ctx->peer)
     CK(cudaMemcpyAsync(&peer_err, ctx->ptab.flg[ctx->rank] + PF_ERR, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  {
+    const plss_status w = dist_wait(ctx, st, nullptr);
+    if (w != PLSS_OK) return w;
+  }
   if (sync_out(ctx) != PLSS_OK) return PLSS_E_CUDA;
   if (peer_err) { set_err(ctx, "peer-memory step: a rank did not arrive within 20 s"); return PLSS_E_CUDA; }
   const Ctl& c = *ctx->h_ctl;
@@ -1359,7 +1416,8 @@ plss_status plss_solve(plss_ctx* ctx, const double* b, const double* x0, double 
     pending[slot] = true;
     slot ^= 1;
     if (pending[slot]) {
-      CK(cudaEventSynchronize(ctx->ev[slot]));
+      const plss_status w = dist_wait(ctx, st, ctx->ev[slot]);
+      if (w != PLSS_OK) return w;
       pending[slot] = false;
       if (ctx->h_done[slot]) break;
     }

@@ -175,6 +175,41 @@ def _ptr(a) -> Optional[int]:
     return a.data_ptr()
 
 
+def _vec(ctx, a, n: int, name: str, host_ok: bool = True) -> Optional[int]:
+    """Checked address of a float64 vector argument of length >= n (None passes through): a numpy
+    array or CPU tensor (host; where the entry point accepts host memory) or a CUDA tensor on the
+    ctx's device, C-contiguous and 8-byte aligned (the SpMVs take an x at any 8-byte phase; vectors
+    the solve keeps are copied into the workspace).
+    Raises PlssError before anything reaches the library (the C side cannot check a
+    foreign pointer's dtype, length or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not host_ok:
+            raise PlssError(f"{name}: a CUDA tensor is required")
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise PlssError(f"{name}: float64 C-contiguous array required (got {a.dtype})")
+        if a.size < n:
+            raise PlssError(f"{name}: {a.size} elements, {n} required")
+        return a.ctypes.data
+    import torch
+    if not isinstance(a, torch.Tensor):
+        raise PlssError(f"{name}: numpy array or torch tensor required (got {type(a).__name__})")
+    if a.dtype != torch.float64 or not a.is_contiguous():
+        raise PlssError(f"{name}: contiguous float64 tensor required (got {a.dtype})")
+    if a.numel() < n:
+        raise PlssError(f"{name}: {a.numel()} elements, {n} required")
+    if a.is_cuda:
+        dev = ctx.A.row_ptr.device
+        if a.device != dev:
+            raise PlssError(f"{name}: on {a.device}, the ctx is on {dev}")
+        if a.data_ptr() % 8:
+            raise PlssError(f"{name}: device vectors must be 8-byte aligned")
+    elif not host_ok:
+        raise PlssError(f"{name}: a CUDA tensor is required")
+    return a.data_ptr()
+
+
 def _stream_ptr(stream) -> Optional[int]:
     if stream is None:
         return None
@@ -322,7 +357,7 @@ def plss_start(ctx: Ctx, b, x0=None, tol=1e-8, tol_mode=0, maxit=100, flags=0):
     lib = load_library()
     ctx._keep = (b, x0)
     ctx._maxit = int(maxit)
-    _check(lib.plss_start(ctx.handle, _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), int(flags)),
+    _check(lib.plss_start(ctx.handle, _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode), int(maxit), int(flags)),
            ctx.handle)
 
 
@@ -337,7 +372,7 @@ def plss_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
     oc = ctypes.c_int(0)
     hist = np.zeros(ctx._maxit + 1) if want_hist else None
     diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
-    _check(lib.plss_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+    _check(lib.plss_finish(ctx.handle, _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
            ctx.handle)
     return _result(it.value, oc.value, hist, diag, x)
 
@@ -366,8 +401,8 @@ def plss_solve(ctx: Ctx, b, x0=None, tol=1e-8, tol_mode=0, maxit=100, flags=0, x
     hist = np.zeros(maxit + 1) if want_hist else None
     diag = np.zeros((maxit + 1, REC)) if want_diag else None
     ctx._maxit = int(maxit)
-    _check(lib.plss_solve(ctx.handle, _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), int(flags),
-                          _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
+    _check(lib.plss_solve(ctx.handle, _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode),
+                          int(maxit), int(flags), _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if flags & 1:
         res["hist"] = hist[:it.value].copy()
@@ -377,7 +412,7 @@ def plss_solve(ctx: Ctx, b, x0=None, tol=1e-8, tol_mode=0, maxit=100, flags=0, x
 def plss_set_wi(ctx: Ctx, wi=None):
     """PLSS W: WI = diag(wi) for later solves (None: WI = I)."""
     ctx._wi = wi
-    _check(load_library().plss_set_wi(ctx.handle, _ptr(wi)), ctx.handle)
+    _check(load_library().plss_set_wi(ctx.handle, _vec(ctx, wi, ctx.n, 'wi')), ctx.handle)
 
 
 def plss_column_norms(ctx: Ctx, out=None):
@@ -385,14 +420,14 @@ def plss_column_norms(ctx: Ctx, out=None):
     import torch
     if out is None:
         out = torch.empty(ctx.n, dtype=torch.float64, device=ctx.A.row_ptr.device)
-    _check(load_library().plss_column_norms(ctx.handle, _ptr(out)), ctx.handle)
+    _check(load_library().plss_column_norms(ctx.handle, _vec(ctx, out, ctx.n, 'out')), ctx.handle)
     return out
 
 
 def plss_true_residual(ctx: Ctx, b, x) -> dict:
     """||b - A x|| and ||b|| (and their ratio) for an iterate x (host or device)."""
     out = np.zeros(2)
-    _check(load_library().plss_true_residual(ctx.handle, _ptr(b), _ptr(x), _ptr(out)), ctx.handle)
+    _check(load_library().plss_true_residual(ctx.handle, _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x, ctx.n, 'x'), _ptr(out)), ctx.handle)
     return {"abs": float(out[0]), "norm_b": float(out[1]),
             "rel": float(out[0] / out[1]) if out[1] > 0 else float(out[0])}
 
@@ -412,12 +447,14 @@ def plss_peer_reduce_emulate(parts, reds, flags, bounds, stream=None):
 
 
 def plss_spmv(ctx: Ctx, x, y):
-    _check(load_library().plss_spmv(ctx.handle, _ptr(x), _ptr(y)), ctx.handle)
+    _check(load_library().plss_spmv(ctx.handle, _vec(ctx, x, ctx.n, 'x', host_ok=False),
+                                    _vec(ctx, y, ctx.m, 'y', host_ok=False)), ctx.handle)
     return y
 
 
 def plss_spmvT(ctx: Ctx, u, v):
-    _check(load_library().plss_spmvT(ctx.handle, _ptr(u), _ptr(v)), ctx.handle)
+    _check(load_library().plss_spmvT(ctx.handle, _vec(ctx, u, ctx.m, 'u', host_ok=False),
+                                     _vec(ctx, v, ctx.n, 'v', host_ok=False)), ctx.handle)
     return v
 
 
@@ -453,8 +490,8 @@ def plss_rp_start(ctx: Ctx, b, r=10, seed=0, density=1.0, x0=None, tol=1e-8, tol
     wp, nb = _rp_workspace(ctx, r)
     ctx._keep = (b, x0)
     ctx._maxit = int(maxit)
-    _check(lib.plss_rp_start(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density), wp, nb, _ptr(b),
-                             _ptr(x0), float(tol), int(tol_mode), int(maxit)), ctx.handle)
+    _check(lib.plss_rp_start(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density), wp, nb, _vec(ctx, b, ctx.m, 'b'),
+                             _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode), int(maxit)), ctx.handle)
 
 
 def plss_rp_step(ctx: Ctx, k: int):
@@ -467,7 +504,7 @@ def plss_rp_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
     oc = ctypes.c_int(0)
     hist = np.zeros(ctx._maxit + 1) if want_hist else None
     diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
-    _check(lib.plss_rp_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+    _check(lib.plss_rp_finish(ctx.handle, _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
            ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if hist is not None:
@@ -488,8 +525,8 @@ def plss_rp_solve(ctx: Ctx, b, r=10, seed=0, density=1.0, x0=None, tol=1e-8, tol
     hist = np.zeros(maxit + 1) if want_hist else None
     diag = np.zeros((maxit + 1, REC)) if want_diag else None
     ctx._maxit = int(maxit)
-    _check(lib.plss_rp_solve(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density), wp, nb, _ptr(b),
-                             _ptr(x0), float(tol), int(tol_mode), int(maxit), _ptr(x), ctypes.byref(it),
+    _check(lib.plss_rp_solve(ctx.handle, int(r), int(seed) & 0xFFFFFFFFFFFFFFFF, float(density), wp, nb, _vec(ctx, b, ctx.m, 'b'),
+                             _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode), int(maxit), _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it),
                              _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if hist is not None:
@@ -557,7 +594,7 @@ def plss_kz_start(ctx: Ctx, b, rows, kmax=None, x0=None, tol=1e-8, tol_mode=0, m
     rr = _rows_arg(rows)
     ctx._keep = (b, x0, rr)
     ctx._maxit = int(maxit)
-    _check(lib.plss_kz_start(ctx.handle, kmax, wp, nb, _ptr(rr), _ptr(b), _ptr(x0), float(tol), int(tol_mode),
+    _check(lib.plss_kz_start(ctx.handle, kmax, wp, nb, _ptr(rr), _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode),
                              int(maxit)), ctx.handle)
 
 
@@ -571,7 +608,7 @@ def plss_kz_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
     oc = ctypes.c_int(0)
     hist = np.zeros(ctx._maxit + 1) if want_hist else None
     diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
-    _check(lib.plss_kz_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+    _check(lib.plss_kz_finish(ctx.handle, _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
            ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if hist is not None:
@@ -594,8 +631,8 @@ def plss_kz_solve(ctx: Ctx, b, rows, kmax=None, x0=None, tol=1e-8, tol_mode=0, m
     hist = np.zeros(maxit + 1) if want_hist else None
     diag = np.zeros((maxit + 1, REC)) if want_diag else None
     ctx._maxit = int(maxit)
-    _check(lib.plss_kz_solve(ctx.handle, kmax, wp, nb, _ptr(rr), _ptr(b), _ptr(x0), float(tol), int(tol_mode),
-                             int(maxit), _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+    _check(lib.plss_kz_solve(ctx.handle, kmax, wp, nb, _ptr(rr), _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode),
+                             int(maxit), _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
            ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if hist is not None:
@@ -635,7 +672,7 @@ def plss_eg_start(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, 
     ctx._keep = (b, x0, rr)
     ctx._maxit = int(maxit)
     _check(lib.plss_eg_start(ctx.handle, EG_SKETCH[sketch], EG_FACTOR[factor], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
-                             _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit)), ctx.handle)
+                             _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode), int(maxit)), ctx.handle)
 
 
 def plss_eg_step(ctx: Ctx, k: int):
@@ -648,7 +685,7 @@ def plss_eg_finish(ctx: Ctx, x=None, want_hist=True, want_diag=False):
     oc = ctypes.c_int(0)
     hist = np.zeros(ctx._maxit + 1) if want_hist else None
     diag = np.zeros((ctx._maxit + 1, REC)) if want_diag else None
-    _check(lib.plss_eg_finish(ctx.handle, _ptr(x), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
+    _check(lib.plss_eg_finish(ctx.handle, _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it), _ptr(hist), _ptr(diag), ctypes.byref(oc)),
            ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if hist is not None:
@@ -672,7 +709,7 @@ def plss_eg_solve(ctx: Ctx, b, sketch="residual", kmax=None, rows=None, seed=0, 
     diag = np.zeros((maxit + 1, REC)) if want_diag else None
     ctx._maxit = int(maxit)
     _check(lib.plss_eg_solve(ctx.handle, EG_SKETCH[sketch], EG_FACTOR[factor], kmax, wp, nb, _ptr(rr), int(seed) & 0xFFFFFFFFFFFFFFFF,
-                             _ptr(b), _ptr(x0), float(tol), int(tol_mode), int(maxit), _ptr(x), ctypes.byref(it),
+                             _vec(ctx, b, ctx.m, 'b'), _vec(ctx, x0, ctx.n, 'x0'), float(tol), int(tol_mode), int(maxit), _vec(ctx, x, ctx.n, 'x'), ctypes.byref(it),
                              _ptr(hist), _ptr(diag), ctypes.byref(oc)), ctx.handle)
     res = _result(it.value, oc.value, hist, diag, x)
     if hist is not None:

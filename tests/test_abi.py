@@ -88,3 +88,41 @@ def test_c_example_compiles_and_links():
                "-lcudart", "-Wl,-rpath," + os.path.join(ROOT, "paper_2207_07615_b200")]
         subprocess.run(cmd, check=True, capture_output=True, text=True)
         assert os.path.exists(exe)
+
+
+def test_binding_rejects_bad_vectors():
+    """the binding validates dtype, contiguity, length and (for tensors) the device
+    and alignment of every vector argument before calling into the library (checked on CPU with a
+    stand-in ctx; no library call is made)."""
+    import numpy as np
+    import torch
+    from paper_2207_07615_b200 import plss as b
+
+    class _A:
+        row_ptr = torch.zeros(1, dtype=torch.int32)
+
+    class _Ctx:
+        A = _A()
+
+    ctx = _Ctx()
+    ok = np.zeros(10)
+    assert b._vec(ctx, ok, 10, "x") == ok.ctypes.data
+    assert b._vec(ctx, None, 10, "x") is None
+    with pytest.raises(b.PlssError, match="float64"):
+        b._vec(ctx, np.zeros(10, np.float32), 10, "x")
+    with pytest.raises(b.PlssError, match="required"):
+        b._vec(ctx, np.zeros(9), 10, "x")
+    with pytest.raises(b.PlssError, match="float64"):
+        b._vec(ctx, np.zeros((10, 2))[:, 0], 10, "x")
+    with pytest.raises(b.PlssError, match="CUDA tensor"):
+        b._vec(ctx, ok, 10, "x", host_ok=False)
+    with pytest.raises(b.PlssError, match="CUDA tensor"):
+        b._vec(ctx, torch.zeros(10, dtype=torch.float64), 10, "x", host_ok=False)
+    with pytest.raises(b.PlssError, match="float64"):
+        b._vec(ctx, torch.zeros(10, dtype=torch.float32), 10, "x")
+    with pytest.raises(b.PlssError, match="float64"):
+        b._vec(ctx, torch.zeros(20, dtype=torch.float64)[::2], 10, "x")
+    with pytest.raises(b.PlssError, match="numpy array or torch tensor"):
+        b._vec(ctx, [0.0] * 10, 10, "x")
+    t = torch.zeros(10, dtype=torch.float64)
+    assert b._vec(ctx, t, 10, "x") == t.data_ptr()

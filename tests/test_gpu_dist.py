@@ -272,3 +272,41 @@ def test_column_block_rejects_row_block_steps(pkg):
                                          None, ctypes.byref(h)) != 0
     with pytest.raises(pkg.PlssError):                      # block outside the global matrix
         pkg.plss_create_dist_cols(A, 1, s.n, uid, 0, 1)
+
+
+def test_dist_nccl_failure_aborts_communicator(pkg, monkeypatch):
+    """SURVEY 5 failure detection: while a distributed solve waits it polls
+    ncclCommGetAsyncError; an error aborts the communicator (ncclCommAbort), the call fails with
+    PLSS_E_NCCL instead of hanging, every later call on the ctx fails the same way, and the ctx
+    can still be destroyed. The error is injected (PLSS_FAULT_NCCL=1 at ctx creation): a real one
+    needs a second rank to die."""
+    s = plss_gen.make_config("C2s")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    monkeypatch.setenv("PLSS_FAULT_NCCL", "1")
+    ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=2, maxit_cap=s.maxit)
+    monkeypatch.delenv("PLSS_FAULT_NCCL")
+    b = torch.from_numpy(s.b).cuda()
+    with pytest.raises(pkg.PlssError, match="NCCL asynchronous error.*aborted"):
+        pkg.plss_solve(ctx, b, tol=s.tol, maxit=s.maxit)
+    with pytest.raises(pkg.PlssError, match="aborted"):
+        pkg.plss_solve(ctx, b, tol=s.tol, maxit=s.maxit)
+    with pytest.raises(pkg.PlssError, match="aborted"):
+        pkg.plss_step(ctx, 1)
+    pkg.plss_destroy(ctx)
+    # a fresh ctx without the fault solves normally on the same device
+    res = _dist_solve(pkg, s, slabs=2)
+    assert res["outcome"] == "converged"
+
+
+def test_binding_rejects_bad_device_vectors(pkg):
+    s = plss_gen.make_config("C1")
+    A = pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+    ctx = pkg.plss_create(A, maxit_cap=4)
+    buf = torch.zeros(s.m + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(pkg.PlssError, match="CUDA tensor"):
+        pkg.plss_spmv(ctx, np.zeros(s.n), buf[:s.m])
+    with pytest.raises(pkg.PlssError, match="required"):
+        pkg.plss_spmv(ctx, torch.zeros(s.n - 1, dtype=torch.float64, device="cuda"), buf[:s.m])
+    with pytest.raises(pkg.PlssError, match="float64"):
+        pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda().float(), maxit=2)
+    pkg.plss_destroy(ctx)

@@ -1,11 +1,17 @@
 """GPU parity: libplss (through the C ABI) vs the CPU oracle on the same seeded inputs.
 
-Bars (BASELINE.json north_star): relative residual history within 1e-9 over the first
+Bars (BASELINE.json north_star), fixed: relative residual history within 1e-9 over the first
 min(50, K_f) iterations (K_f = the window where two valid oracle orderings agree to 1e-11,
-SURVEY 8c-11), final ||x_gpu - x_oracle|| / ||x_oracle|| <= 1e-7, iterations within 2%.
+SURVEY 8c-11, measured over 5 row permutations in tests/golden/parity_floor.json), final
+||x_gpu - x_oracle|| / ||x_oracle|| <= 1e-7, iterations within 2%. A bar is never widened: where
+the oracle disagrees with a row-permuted copy of itself by more than a bar (ill-conditioned C4
+runs, DESIGN R11), a miss of that bar is reported as an explicit xfail naming the floor.
 SpMV outputs of rows with <= LONGROW (128) entries are sequential ascending-index sums on both
 sides: bit-exact. Longer rows use a fixed warp tree: within n*eps*sum|a_ij x_j| of the oracle.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -17,7 +23,10 @@ pytestmark = pytest.mark.gpu
 
 HIST_TOL = 1e-9
 X_TOL = 1e-7
+IT_TOL = 0.02
 LONGROW = 128
+with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "parity_floor.json")) as _f:
+    FLOOR = json.load(_f)             # scripts/parity_floor.py (oracle vs 5 row-permuted oracles)
 
 
 def _assert_spmv(got, ptr, idx, val, vec, ref):
@@ -66,32 +75,52 @@ def _permuted(s, seed=3):
                             s.maxit, b=s.b[perm], freeze=s.freeze)
 
 
-def _floor(s, ref, x0=None, kmax=50):
+def _floor(s, ref, x0=None, kmax=50, key=None):
     """The fp64 parity floor: a second valid oracle ordering (row-permuted A, b)
     run with the same settings. Returns K_f (iterations where the two agree to 1e-11 in hist),
-    their iteration-count difference and their final-x difference."""
+    their iteration-count difference and their final-x difference. With `key`, merged with the
+    5-permutation distribution of tests/golden/parity_floor.json (smallest K_f, largest
+    differences)."""
     other = oracle.plss_system(_permuted(s), x0=x0, maxit=ref["rec"].shape[0] - 1)
     h0, h1 = ref["hist"], other["hist"]
     k = min(len(h0), len(h1), kmax)
     rel = np.abs(h0[:k] - h1[:k]) / np.maximum(h0[:k], 1e-300)
     bad = np.nonzero(rel > 1e-11)[0]
     nx = np.linalg.norm(ref["x"])
-    return {"kf": int(bad[0]) if bad.size else k, "diters": abs(other["iters"] - ref["iters"]),
-            "dx": np.linalg.norm(other["x"] - ref["x"]) / (nx if nx > 0 else 1.0)}
+    fl = {"kf": int(bad[0]) if bad.size else k, "diters": abs(other["iters"] - ref["iters"]),
+          "dx": np.linalg.norm(other["x"] - ref["x"]) / (nx if nx > 0 else 1.0)}
+    return _merge_golden(fl, key, ref)
+
+
+def _merge_golden(fl, key, ref):
+    g = FLOOR.get(key) if key else None
+    if g is not None and g["iters"] == ref["iters"]:
+        fl = {"kf": min(fl["kf"], g["kf_min"]), "diters": max(fl["diters"], g["diters_max"]),
+              "dx": max(fl["dx"], g["dx_max"])}
+    return fl
 
 
 def _assert_parity(res, ref, fl, s):
-    """BASELINE bars, widened only where the oracle disagrees with itself by more (the floor)."""
+    """The north_star bars, fixed (no widening): same outcome, hist within 1e-9 for k <= min(50,
+    K_f), iterations within 2%, x within 1e-7. A bar the oracle itself misses against a row-permuted
+    copy (fl) becomes an explicit xfail when the GPU misses it too."""
     assert res["outcome"] == ref["outcome"], (res["outcome"], ref["outcome"])
-    it_tol = max(1, int(np.ceil(0.02 * ref["iters"])), 3 * fl["diters"])
-    assert abs(res["iters"] - ref["iters"]) <= it_tol, (res["iters"], ref["iters"], fl)
-    k = min(fl["kf"], len(res["hist"]), len(ref["hist"]))
+    k = min(fl["kf"], 50, len(res["hist"]), len(ref["hist"]))
     assert k >= 1
     h_err = np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / np.maximum(ref["hist"][:k], 1e-300))
     assert h_err <= HIST_TOL, (h_err, k)
+    it_bar = max(1, int(np.ceil(IT_TOL * ref["iters"])))
+    d_it = abs(res["iters"] - ref["iters"])
     nx = np.linalg.norm(ref["x"])
     x_err = np.linalg.norm(res["xh"] - ref["x"]) / (nx if nx > 0 else 1.0)
-    assert x_err <= max(X_TOL, 3 * fl["dx"]), (x_err, fl)
+    if d_it > it_bar and fl["diters"] > it_bar:
+        pytest.xfail(f"iterations {res['iters']} vs {ref['iters']}: the oracle's own row-permutation floor "
+                     f"({fl['diters']}) exceeds the 2% bar ({it_bar})")
+    assert d_it <= it_bar, (res["iters"], ref["iters"], it_bar)
+    if x_err > X_TOL and fl["dx"] > X_TOL:
+        pytest.xfail(f"x error {x_err:.2e}: the oracle's own row-permutation floor ({fl['dx']:.2e}) "
+                     f"exceeds the 1e-7 bar")
+    assert x_err <= X_TOL, (x_err, fl)
     return h_err, x_err
 
 
@@ -177,16 +206,22 @@ def test_worked_example(pkg):
     assert abs(d[0, 7] - 5 / 17) <= 1e-15 and abs(d[1, 6] - 9 / 25) <= 1e-15 and abs(d[1, 7] - 17 / 20) <= 1e-15
 
 
-@pytest.mark.parametrize("name,slabs,sell", [("C1", 0, True), ("C2s", 0, True), ("C2s", 3, True),
-                                             ("C2s", 3, False), ("C4s", 0, True), ("C4xs", 0, True),
-                                             ("C5xs", 0, True), ("C5xs", 4, True), ("C5xs", 4, False)])
-def test_solve_parity(pkg, name, slabs, sell):
+@pytest.mark.parametrize("name,slabs,sell,cap", [
+    ("C1", 0, True, 0), ("C2s", 0, True, 0), ("C2s", 3, True, 0), ("C2s", 3, False, 0),
+    # C4s (20k x 80k, ill-conditioned): its x window (the largest cap at which 5 row-permuted oracles
+    # stay within 1e-9 in x: 10, tests/golden/parity_floor.json) with every bar, and 400 capped
+    # steps, where the floor is 1.7e-2 in x (only the history window and the invariants bind)
+    ("C4s", 0, True, 10), ("C4s", 0, True, 400), ("C4xs", 0, True, 0),
+    ("C5xs", 0, True, 0), ("C5xs", 4, True, 0), ("C5xs", 4, False, 0),
+    # C5s: 640k x 80k with C5's +-1024 band, the default 10-slab y-staged schedule of the timed C5
+    ("C5s", 10, True, 0)])
+def test_solve_parity(pkg, name, slabs, sell, cap):
     s = plss_gen.make_config(name)
-    if name == "C4s":
-        s.maxit = 400          # ill-conditioned; not converged: compared within the parity floor
+    if cap:
+        s.maxit = cap
     ref = oracle.plss_system(s)
     res = _gpu_solve(pkg, s, slabs=slabs, sell=sell)
-    _assert_parity(res, ref, _floor(s, ref), s)
+    _assert_parity(res, ref, _floor(s, ref, key=name), s)
     if name.startswith("C4"):
         empty = np.diff(s.col_ptr) == 0      # x in range(A^T): empty columns stay exactly 0
         assert empty.any() and np.all(res["xh"][empty] == 0.0)
@@ -196,7 +231,7 @@ def test_solve_parity_c3_scaled(pkg):
     s = plss_gen.make_config("C3", N=128)
     ref = oracle.plss_system(s)
     res = _gpu_solve(pkg, s)
-    _assert_parity(res, ref, _floor(s, ref), s)
+    _assert_parity(res, ref, _floor(s, ref, key="C3_128"), s)
     assert np.max(np.abs(res["xh"] - 1.0)) <= 1e-5
 
 
@@ -356,15 +391,12 @@ def test_slabs_agree(pkg):
 # weights phi, K3 weights theta
 # ---------------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name,slabs", [("C1", 0), ("C2s", 0), ("C2s", 3), ("C4s", 0), ("C4xs", 0),
-                                        ("C5xs", 0), ("C5xs", 4)])
-def test_plssw_solve_parity(pkg, name, slabs):
+@pytest.mark.parametrize("name,slabs,cap", [("C1", 0, 0), ("C2s", 0, 0), ("C2s", 3, 0), ("C4s", 0, 10),
+                                            ("C4xs", 0, 0), ("C5xs", 0, 0), ("C5xs", 4, 0)])
+def test_plssw_solve_parity(pkg, name, slabs, cap):
     s = plss_gen.make_config(name)
-    if name.startswith("C4"):
-        # ill-conditioned: thousands of iterations past the loss of orthogonality make the count
-        # rounding-sensitive beyond a single permuted-oracle floor sample (R11); compare the
-        # capped runs within the floor instead
-        s.maxit = 400
+    if cap:
+        s.maxit = cap              # C4s: its x window (tests/golden/parity_floor.json, C4s_W)
     A = _matrix(pkg, s)
     ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=s.maxit, validate=True)
     c = pkg.plss_column_norms(ctx)
@@ -383,7 +415,7 @@ def test_plssw_solve_parity(pkg, name, slabs):
     nx = np.linalg.norm(ref["x"])
     fl = {"kf": int(bad[0]) if bad.size else k, "diters": abs(other["iters"] - ref["iters"]),
           "dx": np.linalg.norm(other["x"] - ref["x"]) / (nx if nx > 0 else 1.0)}
-    _assert_parity(res, ref, fl, s)
+    _assert_parity(res, ref, _merge_golden(fl, name + "_W", ref), s)
     # WI-orthogonality identity psi_k = -rho_{k-1}, as for PLSS (invariant under the transform)
     d = res["diag"]
     live = [kk for kk in range(1, min(res["iters"], 20)) if d[kk, 0] > 1e-8]
@@ -394,8 +426,7 @@ def test_plssw_solve_parity(pkg, name, slabs):
     plain = pkg.plss_solve(ctx, torch.from_numpy(s.b).cuda(), tol=s.tol, tol_mode=s.tol_mode, maxit=s.maxit,
                            flags=1 if s.freeze else 0)
     ref0 = oracle.plss_system(s)
-    assert plain["iters"] == ref0["iters"] or abs(plain["iters"] - ref0["iters"]) <= max(1, int(0.02 * ref0["iters"])) \
-        or name.startswith("C4")
+    assert abs(plain["iters"] - ref0["iters"]) <= max(1, int(np.ceil(IT_TOL * ref0["iters"])))
     pkg.plss_destroy(ctx)
 
 
@@ -451,3 +482,31 @@ def test_degenerate_dimensions(pkg, m, n):
     pkg.plss_spmv(ctx, torch.zeros(n, dtype=torch.float64, device="cuda"), y)
     pkg.plss_spmvT(ctx, torch.zeros(m, dtype=torch.float64, device="cuda"), v)
     pkg.plss_destroy(ctx)
+
+
+def test_stagnation_outcome(pkg):
+    """STAGNATION (tau - 1 <= 1e-14) on the GPU: A = [1; 1], b = e_1 has tau = 1
+    exactly at the first loop step (worked by hand in test_oracle_pins.py); the outcome, the one
+    applied update and the record match the oracle, normal and freeze mode."""
+    s = plss_gen.from_dense(np.array([[1.0], [1.0]]), np.array([1.0, 0.0]), tol=1e-12, maxit=10)
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    assert res["outcome"] == ref["outcome"] == "stagnation" and res["iters"] == ref["iters"] == 1
+    assert res["xh"].tolist() == ref["x"].tolist() == [1.0]
+    assert res["diag"][1, 0] == ref["rec"][1, 0] == 1.0
+    res = _gpu_solve(pkg, s, tol=0.0, maxit=6, flags=1)
+    assert res["outcome"] == "stagnation" and res["iters"] == 6 and res["xh"].tolist() == [1.0]
+
+
+def test_stagnation_inconsistent_random(pkg):
+    """An inconsistent 300 x 100 system: the recursive residual stops moving once it reaches
+    b's component outside range(A) and the guard fires; outcome and step count equal the
+    oracle's (201 steps)."""
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((300, 100))
+    s = plss_gen.from_dense(A, rng.standard_normal(300), tol=1e-12, maxit=400)
+    ref = oracle.plss_system(s)
+    res = _gpu_solve(pkg, s)
+    assert ref["outcome"] == "stagnation"
+    assert res["outcome"] == "stagnation"
+    assert abs(res["iters"] - ref["iters"]) <= max(1, int(np.ceil(IT_TOL * ref["iters"])))

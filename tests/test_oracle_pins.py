@@ -464,3 +464,72 @@ def test_column_norms():
     empty = np.diff(s.col_ptr) == 0
     assert empty.any() and np.all(c[empty] == 1.0)
     np.testing.assert_allclose(c[~empty], dense_norms[~empty], rtol=1e-14)
+
+
+# ---------------------------------------------------------------------------------------------
+# STAGNATION guard (tau - 1 <= 1e-14; tau >= 1 by Cauchy-Schwarz)
+# ---------------------------------------------------------------------------------------------
+
+def test_stagnation_exact_tau_one():
+    """A = [1; 1], b = e_1 (inconsistent: b is not in range(A)). By hand: r0 = b, rho0 = 1,
+    y1 = A^T r0 = 1, phi1 = 1, p1 = 1, theta1 = 1, x1 = 1; r1 = r0 - A p1 = (0, -1), rho1 = 1,
+    y2 = -1, phi2 = 1, so tau = sqrt(theta1 phi2) / rho1 = 1 exactly: the exact-rational oracle's
+    denominator theta phi - rho^2 is 0 at that step, and the fp64 oracle reports STAGNATION with
+    one update applied (x = 1), the breakdown as an outcome, not an error."""
+    A = np.array([[1.0], [1.0]])
+    b = np.array([1.0, 0.0])
+    ex = exact.plss_exact([[Fraction(1)], [Fraction(1)]], [Fraction(1), Fraction(0)], maxit=10)
+    assert ex["iters"] == 1 and not ex["converged"]
+    assert ex["theta"][0] * ex["phi"][-1] - ex["rho"][-1] ** 2 == 0
+    s = plss_gen.from_dense(A, b, tol=1e-12, maxit=10)
+    r = oracle.plss_system(s)
+    assert r["outcome"] == "stagnation" and r["iters"] == 1
+    assert r["x"].tolist() == [1.0]
+    assert r["rec"][1, 0] == 1.0 and r["rec"][1, 1] == 1.0      # hist_1 = ||r1|| / ||b|| = 1
+    # freeze mode: the guard freezes the iterate (beta = gamma = 0) and the outcome is kept
+    f = oracle.plss_system(s, maxit=6, freeze=True, tol=0.0)
+    assert f["outcome"] == "stagnation" and f["iters"] == 6 and f["x"].tolist() == [1.0]
+
+
+def test_stagnation_does_not_fire_on_consistent_systems():
+    """The guard must not fire before convergence on consistent systems (SURVEY 8c pin table,
+    'breakdown guard safety'): min(tau - 1) over C1's run stays far from 1e-14."""
+    s = plss_gen.make_config("C1")
+    r = oracle.plss_system(s)
+    tau = r["rec"][1:r["iters"], 5]
+    assert r["outcome"] == "converged" and tau.min() - 1.0 > 0.1
+
+
+# ---------------------------------------------------------------------------------------------
+# threaded oracle (oracle_set_threads): bitwise element values, fixed-order blocked dots
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("T", [2, 3, 8])
+def test_threaded_oracle_spmv_bitwise(T):
+    s = plss_gen.make_config("C2s")
+    rng = np.random.default_rng(7)
+    x, u = rng.standard_normal(s.n), rng.standard_normal(s.m)
+    y1 = oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x)
+    v1 = oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u)
+    with oracle.threads(T):
+        y = oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x)
+        v = oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u)
+    np.testing.assert_array_equal(y, y1)
+    np.testing.assert_array_equal(v, v1)
+
+
+@pytest.mark.parametrize("name,T", [("C2s", 4), ("C5xs", 8), ("C1", 16)])
+def test_threaded_oracle_tracks_sequential(name, T):
+    """Only the dot products' summation order differs: the histories agree to rounding while the
+    process is pre-asymptotic, runs with a fixed T are bitwise repeatable, and T
+    larger than a vector leaves empty blocks (C1: n = 100 < T * 8)."""
+    s = plss_gen.make_config(name)
+    a = oracle.plss_system(s, maxit=30)
+    with oracle.threads(T):
+        b = oracle.plss_system(s, maxit=30)
+        c = oracle.plss_system(s, maxit=30)
+    np.testing.assert_array_equal(b["rec"], c["rec"])
+    k = min(len(a["hist"]), len(b["hist"]), 25)
+    assert np.max(np.abs(a["hist"][:k] - b["hist"][:k]) / a["hist"][:k]) <= 1e-12
+    assert np.linalg.norm(a["x"] - b["x"]) <= 1e-10 * np.linalg.norm(a["x"])
+    assert oracle._load().oracle_get_threads() == 1          # restored on exit
