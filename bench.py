@@ -205,7 +205,8 @@ def workload_label(name):
 
 
 # ---------------------------------------------------------------------------------------------
-# CPU baseline: the oracle on a bounded 1/100-scale sample of the same recipe
+# CPU baseline: the oracle on the same arrays (host copies), a bounded number of real steps
+# (cpu_sample: the 1/100-scale samples the other methods' legs still use)
 # ---------------------------------------------------------------------------------------------
 def cpu_sample(name):
     if name == "C5":
@@ -220,50 +221,106 @@ def cpu_sample(name):
     return plss_gen.make_config(name), f"{name} full"
 
 
-def run_oracle_steps(s, steps):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_threads():
+    """Host threads of the oracle baseline: every core (SURVEY 8(d) oracle_omp), or
+    PLSS_ORACLE_THREADS."""
+    return int(os.environ.get("PLSS_ORACLE_THREADS", "0")) or os.cpu_count() or 1
+
+
+def host_arrays(w):
+    """Host (numpy) copies of a workload's device arrays: the bytes the GPU streams, for the oracle."""
+    h = {k: w[k].cpu().numpy() for k in ("row_ptr", "col_idx", "val", "col_ptr", "row_idx", "val_t", "b")}
+    h.update(m=int(w["m"]), n=int(w["n"]))
+    return h
+
+
+def oracle_run(h, steps, threads):
+    """`steps` freeze-mode steps of the oracle (initialization + steps - 1 loop steps: each one
+    SpMV pair and the vector work, as a GPU step) on `threads` host threads; seconds."""
     import oracle
-    t0 = time.perf_counter()
-    oracle.plss(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t, s.b, tol=0.0,
-                maxit=steps, freeze=True)
-    return time.perf_counter() - t0
+    with oracle.threads(threads):
+        t0 = time.perf_counter()
+        oracle.plss(h["m"], h["n"], h["row_ptr"], h["col_idx"], h["val"], h["col_ptr"], h["row_idx"], h["val_t"],
+                    h["b"], tol=0.0, maxit=steps, freeze=True)
+        return time.perf_counter() - t0
 
 
-def cpu_baseline(name, full_bytes, budget_s=15.0):
-    s, label = cpu_sample(name)
-    sb = plss_gen.bytes_per_iter(s.m, s.n, s.nnz)
-    t1 = run_oracle_steps(s, 5)
-    steps = int(max(5, min(2000, budget_s / max(t1 / 5, 1e-6))))
-    t = run_oracle_steps(s, steps)
-    gbs = sb * steps / t / 1e9
-    return {"value": gbs * 1e9 / full_bytes, "unit": "it/s", "cores": 1, "kind": "oracle",
-            "sample": f"{label}; {steps} loop steps in {t:.1f} s = {gbs:.2f} GB/s algorithmic; "
-                      f"it/s scaled to the full workload by algorithmic bytes/iter",
-            "oracle_gbs": gbs}
+def cpu_baseline(name, h, full_bytes, budget_s=20.0):
+    """The oracle as it stands on the box's host cores, on the full workload's own arrays (host
+    copies), for a bounded number of real steps: the threaded oracle (SURVEY 8(d) oracle_omp,
+    every core) and one step of the sequential oracle (oracle_seq)."""
+    T = oracle_threads()
+    t1 = oracle_run(h, 1, T)
+    steps = int(max(2, min(500, budget_s / max(t1, 1e-6))))
+    t = oracle_run(h, steps, T)
+    its = steps / t
+    ts = oracle_run(h, 1, 1) if t1 * T <= 30.0 else None
+    gbs = full_bytes * its / 1e9
+    seq = f"; the sequential oracle (1 thread): {1.0 / ts:.3f} it/s over 1 step" if ts else ""
+    return {"value": its, "unit": "it/s", "cores": T, "kind": "oracle", "cpu_model": cpu_model(),
+            "cpu_count": os.cpu_count(),
+            "sample": f"the oracle on the full {name} arrays (host copies of the bench's own): {steps} freeze-mode "
+                      f"steps on {T} threads (oracle_set_threads: static row / column split, blocked dots) in "
+                      f"{t:.1f} s = {gbs:.2f} GB/s algorithmic{seq}",
+            "oracle_gbs": gbs, "oracle_seq_its": (1.0 / ts) if ts else None}
 
 
 # ---------------------------------------------------------------------------------------------
 # reference arm (--impl reference): the oracle as it stands, rank 0 only
 # ---------------------------------------------------------------------------------------------
+def reference_inputs(name):
+    """The workload our arm times at N = 1, as host arrays. C5 comes from plss_gen.make_c5_torch on
+    the box's GPU when it has one (input synthesis only; the oracle runs on the host), else from the
+    same recipe on the CPU generator (a different stream, labelled)."""
+    if name == "C5":
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        d = plss_gen.make_c5_torch(device=dev)
+        h = host_arrays(d)
+        del d
+        if dev == "cuda":
+            torch.cuda.empty_cache()
+        return h, ("generated by make_c5_torch on the GPU (the bench's arrays)" if dev == "cuda"
+                   else "generated by make_c5_torch on the CPU generator (another stream than the GPU arm's)")
+    s = plss_gen.make_config(name)
+    h = {"row_ptr": s.row_ptr, "col_idx": s.col_idx, "val": s.val, "col_ptr": s.col_ptr, "row_idx": s.row_idx,
+         "val_t": s.val_t, "b": s.b, "m": s.m, "n": s.n}
+    return h, "plss_gen recipe (the bench's arrays)"
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     name = args.workload
     full = full_bytes_of(name)
-    s, label = cpu_sample(name)
-    sb = plss_gen.bytes_per_iter(s.m, s.n, s.nnz)
-    run_oracle_steps(s, max(1, args.warmup))
-    t = run_oracle_steps(s, args.steps)
-    gbs = sb * args.steps / t / 1e9
-    value = gbs * 1e9 / full
+    h, src = reference_inputs(name)
+    T = oracle_threads()
+    oracle_run(h, max(1, args.warmup), T)
+    t = oracle_run(h, args.steps, T)
+    value = args.steps / t
     line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_label(name), **full_dims_of(name),
-                                            "parallelism": "oracle on 1 host core", "freeze_mode": True,
+                                            "parallelism": f"oracle on {T} host threads", "freeze_mode": True,
                                             "tol": 0.0},
-            "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{label}; each step one oracle loop step; it/s scaled to the "
-                                       f"full workload by algorithmic bytes/iter ({gbs:.2f} GB/s)"},
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": T, "kind": "oracle", "cpu_model": cpu_model(),
+                             "cpu_count": os.cpu_count(),
+                             "sample": f"the full {name} workload ({src}); {args.steps} timed freeze-mode steps "
+                                       f"after {max(1, args.warmup)} warm-up steps of the oracle on {T} threads "
+                                       f"(oracle_set_threads); {full * value / 1e9:.2f} GB/s algorithmic"},
             "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -539,7 +596,7 @@ def main():
         if cross_rank is not None:
             line["cross_rank_bitwise_scalars"] = cross_rank
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(w["name"], B_global)
+            line["cpu_baseline"] = cpu_baseline(w["name"], host_arrays(w), B_global)
         print(json.dumps(line), flush=True)
     pkg.plss_destroy(ctx)
     if world > 1:

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _bench(args, env_extra=None, timeout=600):
-    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1")
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", OMP_NUM_THREADS="1", PLSS_ORACLE_THREADS="1")
     env.update(env_extra or {})
     return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, env=env,
                           capture_output=True, text=True, timeout=timeout)
@@ -32,6 +32,7 @@ def test_reference_arm_line():
     assert d["config"]["workload"].startswith("C2") and d["config"]["n"] == 100_000
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["cpu_count"] >= 1 and cb["cpu_model"] and d["ms_per_step"] == pytest.approx(1e3 / d["value"])
     assert d["e2e"] == {"value": d["value"], "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
