@@ -221,6 +221,18 @@ plss_status plss_profile(plss_ctx *ctx, int32_t k, double *ms);
  * window, grid sizes of the first K1 / K2 launch, how many of the 2*slabs SpMV segments use
  * the SELL-32 format (the rest use TMA-staged CSR tiles) and how many of those gather through a
  * shared-memory window of the gathered vector. Any pointer may be NULL. */
+/* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
+ * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:
+ * out (host, 4 * grid uint64) = {start ns, end ns (%globaltimer), stored entries, units} per CTA
+ * of the persistent grid; *grid receives the grid size. PLSS_E_STATE without PLSS_DBG_CTA. */
+plss_status plss_debug_cta_times(plss_ctx *ctx, int32_t which, int32_t slab, uint64_t *out, int32_t *grid);
+
+/* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
+ * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:
+ * out (host, 4 * grid uint64) = {start ns, end ns (%globaltimer), stored entries, units} per CTA
+ * of the persistent grid; *grid receives the grid size. PLSS_E_STATE without PLSS_DBG_CTA. */
+plss_status plss_debug_cta_times(plss_ctx *ctx, int32_t which, int32_t slab, uint64_t *out, int32_t *grid);
+
 plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t *slabs,
                        int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2,
                        int32_t *sell_segments, int32_t *window_segments);

@@ -246,6 +246,7 @@ struct plss_ctx {
   // NCCL failure detection (dist_wait): the communicator was aborted after an asynchronous error
   // or a wait timeout; every later call on this ctx fails with PLSS_E_NCCL
   bool aborted = false;
+  std::vector<void*> dbg_bufs;   // PLSS_DBG_CTA buffers
   int fault_nccl = 0;            // PLSS_FAULT_NCCL=1 (tests): the first poll reports an error
   double wait_timeout_s = 600.0; // PLSS_WAIT_TIMEOUT_S
   bool peer = false;
@@ -533,8 +534,10 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   int32_t* cblk = pool.cblk + pool.used_c;
   // CTA balance: a unit costs its stored entries plus a fixed overhead (metadata loads, row
   // outputs, dot partial); sigma-permuted slices also pay the scattered / staged y. Measured best:
-  // 128 entries (C4's global-sort segments; 256: -15%), 256 for sigma-permuted ones (C5 K2 +3%).
-  const int uc = (a.perm && !a.gsort) ? env_int("PLSS_UC_SIG", 256) : env_int("PLSS_UC", 128);
+  // 256 for sigma-permuted ones (C5 K2 +3%), 32 for globally sorted ones (C4's K1 0.160 -> 0.123 ms:
+  // the CTAs of long rows were the stragglers, scripts/cta_balance.py), 128 otherwise.
+  const int uc = (a.perm && !a.gsort) ? env_int("PLSS_UC_SIG", 256)
+                 : a.gsort ? env_int("PLSS_UC_GS", 32) : env_int("PLSS_UC", 128);
   if (a.uw)
     k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk, uc);
   else
@@ -1066,6 +1069,15 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     }
   }
   CK(cudaGetLastError());
+  // Diagnostics: per-CTA timing of the fmt 3 launches (plss_debug_cta_times)
+  if (env_int("PLSS_DBG_CTA", 0)) {
+    for (int s = 0; s < S; ++s)
+      for (SpmvSeg* a : {&ctx->seg1[s], &ctx->seg2[s]}) {
+        CK(cudaMalloc((void**)&a->ctat, 4 * 8 * (size_t)MAXG));
+        CK(cudaMemsetAsync(a->ctat, 0, 4 * 8 * (size_t)MAXG, st));
+        ctx->dbg_bufs.push_back(a->ctat);
+      }
+  }
   // Static stepping (SpmvSeg::stat) for fmt 3 segments without a perm or long rows (C5's K1:
   // 2.78 -> 2.61 ms per step), with 6 entries in flight per lane when the slices are 6k steps long
   // (C5's K1 rows of 12: 2.61 -> 2.52 ms; K2's variable columns keep 8). PLSS_STAT=0 turns it off.
@@ -1638,6 +1650,16 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   if (tile_nnz) *tile_nnz = TILE;
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];
   if (grid_k2) *grid_k2 = ctx->g2.empty() ? 0 : ctx->g2[0];
+  return PLSS_OK;
+}
+
+plss_status plss_debug_cta_times(plss_ctx* ctx, int32_t which, int32_t slab, uint64_t* out, int32_t* grid) {
+  if (!ctx || !out || !grid || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
+  const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
+  *grid = which == 1 ? ctx->g1[slab] : ctx->g2[slab];
+  if (!a.ctat) { set_err(ctx, "create the ctx with PLSS_DBG_CTA=1"); return PLSS_E_STATE; }
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(out, a.ctat, 4 * 8 * (size_t)(*grid), cudaMemcpyDeviceToHost));
   return PLSS_OK;
 }
 
@@ -2443,6 +2465,7 @@ void plss_destroy(plss_ctx* ctx) {
   for (void* q : ctx->ipc_open) cudaIpcCloseMemHandle(q);
   if (ctx->sym) cudaFree(ctx->sym);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (void* q : ctx->dbg_bufs) cudaFree(q);
   for (auto& e : ctx->ev_ch) if (e) cudaEventDestroy(e);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);

@@ -126,6 +126,8 @@ struct SpmvSeg {
   const int2* wlo;           // per block {lo_b, flags}: 1 = reload the whole window, 2 = no window
   const int32_t* cblk;       // grid+1 block bounds of the CTAs (balanced by stored entries)
   double* slpart;            // per-slice dot partials (fixed-order reduction, deterministic)
+  unsigned long long* ctat;  // diagnostics (a -DPLSS_DBGCTA build with PLSS_DBG_CTA=1, plss_debug_cta_times): per CTA of fmt 3 its
+                             // start / end %globaltimer, stored entries and units processed; or NULL
   int32_t stat;              // fmt 3 without perm / long rows: warps step through their CTA's slices
                              // statically and keep per-thread dot terms (no per-slice partials);
                              // 2: the same with 6 entries per lane in flight (slices of 6 k steps)
@@ -604,7 +606,7 @@ constexpr int NSB = SPW > 16 ? SPW : 16;
 #define PLSS_PAIR 1                     // fmt 3: consecutive slices a warp sums together
 #endif
 #ifndef PLSS_YQ
-#define PLSS_YQ 8
+#define PLSS_YQ 6
 #endif
 // fmt 3 K2: sigma windows staged in shared memory at once (dynamic smem, YQ * SIGMA * 8 bytes),
 // and the ring of per-window staging decisions (YD windows)
@@ -791,6 +793,13 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       for (int f = sl0; f < min(sl0 + P * (BS / 32), sl1); f += SPW) ydecide(f);
     __syncthreads();
   }
+#ifdef PLSS_DBGCTA
+  unsigned long long dbg_entries = 0, dbg_units = 0;
+  if (DYN && a.ctat && tid == 0) {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.ctat[4 * blockIdx.x] = t;
+  }
+#endif
   if (su < sl1) meta(su);
   while (su < sl1) {
     const bool stage = YSTG && a.perm && !a.gsort && ymode(su);
@@ -812,6 +821,10 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       }
       nx = __shfl_sync(FULL, nx, 0);
     }
+#ifdef PLSS_DBGCTA
+    if (DYN && a.ctat && lane == 0)
+      for (int q = 0; q < P; ++q) if (su + q < sl1) { dbg_entries += (LU && su + q >= a.nslices) ? L[q] : 32ull * L[q]; dbg_units++; }
+#endif
     if (nx < sl1) meta(nx);
     bool valid[P];
     double s[P], r_old[P];
@@ -905,6 +918,21 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
     }
     su = nx;
   }
+#ifdef PLSS_DBGCTA
+  if (DYN && a.ctat) {                              // diagnostics build only (uniform branch)
+    __shared__ unsigned long long s_dbg[2];
+    if (tid == 0) { s_dbg[0] = 0; s_dbg[1] = 0; }
+    __syncthreads();
+    if (lane == 0) { atomicAdd(&s_dbg[0], dbg_entries); atomicAdd(&s_dbg[1], dbg_units); }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.ctat[4 * blockIdx.x + 1] = t;
+      a.ctat[4 * blockIdx.x + 2] = s_dbg[0];
+      a.ctat[4 * blockIdx.x + 3] = s_dbg[1];
+    }
+  }
+#endif
   if (!DOTS) return;
   if (DYN && !STAT) {
     __syncthreads();

@@ -16,7 +16,9 @@ run old PLSS_LIB=$OLD
 run new_l0_s0 PLSS_LOCW=0 PLSS_STAT=0
 run new_l16k_s0 PLSS_LOCW=16384 PLSS_STAT=0
 run new_l0_s1 PLSS_LOCW=0 PLSS_STAT=1
+L=$PWD/paper_2207_07615_b200
 run def
-run stat_su8 PLSS_STAT=3
+run yq6 PLSS_LIB=$L/libplss_yq6.so
+run yq4 PLSS_LIB=$L/libplss_yq4.so
 run def2
-run stat_su8b PLSS_STAT=3
+run yq6b PLSS_LIB=$L/libplss_yq6.so
