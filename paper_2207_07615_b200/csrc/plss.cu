@@ -126,8 +126,8 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
     L->cblk = take(4 * (size_t)(MAXG + 1) * (2 * S + DCH_MAX));
     // units of one segment: slices + long rows (<= nnz / (LONGROW + 1) of them)
     L->slpart = take(16 * (size_t)(std::max(m, n) / 32 + nnz / (LONGROW + 1) + 4));
-    L->s1auxn = 2 * (m / 32 + nnz / (LONGROW + 1) + 4 * S + 8);
-    L->s2auxn = 2 * ((int64_t)S * (n / 32) + nnz / (LONGROW + 1) + 4 * S + 8);
+    L->s1auxn = 2 * (m / 32 + 4 * S + 8) + 6 * (nnz / (LONGROW + 1) + 2);
+    L->s2auxn = 2 * ((int64_t)S * (n / 32) + 4 * S + 8) + 6 * (nnz / (LONGROW + 1) + 2);
     L->s1aux = take(4 * (size_t)L->s1auxn);
     L->s2aux = take(4 * (size_t)L->s2auxn);
   }
@@ -307,8 +307,16 @@ template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
   if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
-  else if (a.fmt == 3 && a.nlong > 0)
-    k_sell<ROLE, 1024, true><<<grid, 1024, 0, st>>>(a);            // gsort: no y staging
+  else if (a.fmt == 3 && a.nlong > 0) {
+    // gsort with long rows: the slices, then k_longrows (one CTA per long row), which publishes its
+    // dot terms in the partial slot after the slices' CTAs and finalizes the segment if it must
+    SpmvSeg b = a;
+    b.finalize = 0;
+    k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);                   // gsort: no y staging
+    SpmvSeg c = a;
+    c.partial = a.partial + 2 * (size_t)grid;
+    k_longrows<ROLE><<<a.nlong, NT, 0, st>>>(c);
+  }
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort && a.sig == SIGMA_WIDE)
     k_sell<ROLE, 1024, false, true, SIGMA_WIDE><<<grid, 1024, YSTAGE_SMEM_WIDE, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort)     // K2 with a sigma perm: staged y
@@ -527,7 +535,7 @@ static int env_int(const char* name, int dflt) {
 // One 1024-thread CTA per SM over contiguous entry-balanced slice ranges (fmt 3).
 static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sms, int* grid_out) {
   if (a.fmt != 1) return PLSS_OK;
-  const int nunits = a.nslices + a.nlong;
+  const int nunits = a.nslices;                      // long rows run in k_longrows (launch_spmv)
   const int NSB = nsb_of(a.sig ? a.sig : SIGMA);     // the k_sell instantiation's block (a.sig)
   const int nblocks = (nunits + NSB - 1) / NSB;
   const int grid = std::max(1, std::min(std::min(nblocks, sms), MAXG));
@@ -658,9 +666,11 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   }
   const int64_t nshort = nrows - (int64_t)lrows.size();
   const int64_t nsl = (nshort + 31) / 32;
-  const int64_t nunits = nsl + (int64_t)lrows.size();
+  const int64_t nlr = (int64_t)lrows.size();
+  const int64_t nunits = nsl;                       // long rows run in k_longrows, not as k_sell units
+  const int64_t aux_need = nlr + 4 * nlr + 2 + nunits + 1;   // lrows, lrowd (2 doubles), align, uw
   if (pool.used_slots + nsl * 32 > pool.slots || pool.used_sp + nsl + 1 > pool.sp ||
-      pool.used_aux + (int64_t)lrows.size() + nunits + 1 > pool.auxn)
+      pool.used_aux + aux_need > pool.auxn)
     return PLSS_OK;
   // stable counting sort, length descending
   std::vector<int64_t> off(LONGROW + 2, 0);
@@ -679,17 +689,15 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
     stored += 32 * L;
   }
   sp[nsl] = (int32_t)steps;
-  for (size_t k = 0; k < lrows.size(); ++k) {
-    uw[nsl + k] = (int32_t)stored;
-    stored += len[lrows[k]];
-  }
   uw[nunits] = (int32_t)stored;
+  for (size_t k = 0; k < lrows.size(); ++k) stored += len[lrows[k]];
   if (stored >= (1ll << 31) || pool.used + steps * 32 > pool.cap) return PLSS_OK;
   if ((double)(steps * 32) > 1.15 * (double)nnz_seg + 32.0 * 32 * (LONGROW + 1)) return PLSS_OK;
   int32_t* d_perm = pool.perm + pool.used_slots;
   int32_t* d_sp = pool.sptr + pool.used_sp;
   int32_t* d_lrows = pool.aux + pool.used_aux;
-  int32_t* d_uw = d_lrows + lrows.size();
+  double* d_lrowd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(d_lrows + nlr) + 7) & ~(uintptr_t)7);
+  int32_t* d_uw = reinterpret_cast<int32_t*>(d_lrowd + 2 * nlr);
   CK(cudaMemcpyAsync(d_perm, perm.data(), 4 * perm.size(), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_sp, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice, st));
   if (!lrows.empty()) CK(cudaMemcpyAsync(d_lrows, lrows.data(), 4 * lrows.size(), cudaMemcpyHostToDevice, st));
@@ -708,6 +716,8 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   a.perm = d_perm;
   a.nlong = (int32_t)lrows.size();
   a.lrows = d_lrows;
+  a.lrowd = d_lrowd;
+  a.lcounter = ctx->counters + 8;
   a.lptr = a.ptr;
   a.lidx = a.idx;
   a.lval = a.val;
@@ -717,7 +727,7 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   pool.used += steps * 32;
   pool.used_slots += nsl * 32;
   pool.used_sp += nsl + 1;
-  pool.used_aux += (int64_t)lrows.size() + nunits + 1;
+  pool.used_aux += aux_need;
   return PLSS_OK;
 }
 

@@ -115,6 +115,10 @@ struct SpmvSeg {
   int32_t gsort, nlong;
   const int32_t* lrows;
   const int32_t* lptr;
+  // k_longrows (launch_spmv runs it after the segment's slices): per long row its dot terms
+  // (2 doubles, reduced in row order by the last CTA) and that CTA's election counter
+  double* lrowd;
+  unsigned* lcounter;
   const int32_t* lidx;
   const double* lval;
   const int32_t* uw;         // nunits+1 prefix of stored entries per unit (CTA balance), or NULL
@@ -954,6 +958,97 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 }
 
 // ---------------------------------------------------------------------------------------------
+// Long rows (> LONGROW entries) of a globally sorted segment (C4's power-law rows), launched by
+// launch_spmv right after the segment's slices: one 256-thread CTA per row, entries strided over
+// the CTA (coalesced), SU loads in flight per thread, a fixed tree (warp butterflies, then the 8
+// warp sums in order). Row epilogues as k_sell's. Dot terms per row go to lrowd; the last CTA
+// (atomic ticket) sums them in row order (deterministic) into this launch's partial slot
+// a.partial[0..1] and, if the segment finalizes, sums all partial pairs in index order and runs the
+// tail. Separated from k_sell because its long-row path, inlined there, pushed the kernel past 64
+// registers: ptxas then serialized the gathers of every batch (C4's long-row CTAs ran at half the
+// per-entry rate of the slices).
+template <int ROLE>
+__global__ void __launch_bounds__(NT) k_longrows(SpmvSeg a) {
+  __shared__ double sm[2][MAXW];
+  __shared__ double s_w[NT / 32];
+  __shared__ int s_last;
+  if (a.ctl != nullptr && a.ctl->done) return;
+  constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
+  const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pol = a.pol_first;
+  const int k = blockIdx.x;
+  const int r = a.lrows[k];
+  const int e0 = a.lptr[r], e1 = a.lptr[r + 1];
+  double start = 0.0;
+  if (tid == 0 && (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate))) start = a.out[r];
+  double ps = 0.0;
+  for (int k0 = e0; k0 < e1; k0 += NT * SU) {
+    int32_t c[SU];
+    double v[SU], gv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int q = k0 + u * NT + tid;
+      c[u] = -1;
+      if (q < e1) { c[u] = ld_stream(a.lidx + q, pol); v[u] = ld_stream(a.lval + q, pol); }
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u]);
+#pragma unroll
+    for (int u = 0; u < SU; ++u) if (c[u] >= 0) ps = __dadd_rn(ps, __dmul_rn(v[u], gv[u]));
+  }
+  ps = warp_sum(ps);
+  if (lane == 0) s_w[warp] = ps;
+  __syncthreads();
+  double d0 = 0.0, d1 = 0.0;
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t = __dadd_rn(t, s_w[w]);
+    if (ROLE == ROLE_PLAIN) {
+      a.out[r] = t;
+    } else if (ROLE == ROLE_K1) {
+      const double rn = __dsub_rn(start, t);                   // r_i <- r_i - (A p)_i
+      a.out[r] = rn;
+      d0 = rn * rn;
+    } else {
+      const double yv = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, r, __dadd_rn(start, t), d0, d1)
+                                            : __dadd_rn(start, t);
+      a.out[r] = yv;
+    }
+    if (DOTS) {
+      a.lrowd[2 * k] = d0;
+      a.lrowd[2 * k + 1] = d1;
+      __threadfence();
+      s_last = atomicAdd(a.lcounter, 1u) == gridDim.x - 1;
+    }
+  }
+  if (!DOTS) return;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double s0 = 0.0, s1 = 0.0;                                    // row order, fixed shape
+  for (int q = tid; q < (int)gridDim.x; q += NT) { s0 += __ldcg(a.lrowd + 2 * q); s1 += __ldcg(a.lrowd + 2 * q + 1); }
+  block_sum2(s0, s1, sm);
+  if (tid == 0) {
+    *a.lcounter = 0u;
+    a.partial[0] = s0;
+    a.partial[1] = s1;
+  }
+  if (!a.finalize) return;
+  __threadfence();
+  __syncthreads();
+  double t0 = 0.0, t1 = 0.0;
+  for (int q = tid; q < a.nparts; q += NT) { t0 += __ldcg(a.part_base + 2 * q); t1 += __ldcg(a.part_base + 2 * q + 1); }
+  block_sum2(t0, t1, sm);
+  if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = t0;
+    else tail_rho(a.ctl, a.rec, t0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, t0, t1);
+  }
+}
+
 // K1 / K2 / plain SpMV over SELL-32 with a sliding shared-memory WINDOW of the gathered vector.
 // Banded matrices (C3's stencil, C5's band half) gather most entries of a run of rows from a
 // narrow range of g. Each CTA walks a contiguous, entry-balanced range of blocks (nsb slices

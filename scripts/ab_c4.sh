@@ -13,6 +13,10 @@ PY
 }
 
 run def
-for uc in 32 64; do for lch in 256 512 4096; do run uc${uc}_lch$lch PLSS_UC=$uc PLSS_LCH=$lch; done; done
-run uc128_lch4096 PLSS_LCH=4096
+for uc in 16 64 128; do run ucgs$uc PLSS_UC_GS=$uc; done
+BARGS="--workload C4alt"
+run alt_def
+run alt_uc64 PLSS_UC_GS=64
+run alt_uc128 PLSS_UC_GS=128
+BARGS=""
 run def2
