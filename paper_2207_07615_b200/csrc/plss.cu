@@ -305,7 +305,9 @@ static void set_err(plss_ctx* ctx, const std::string& s) {
 
 template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
-  if (a.fmt == 2)
+  if (a.fmt == 5)
+    k_scalar<ROLE><<<grid, NT, 0, st>>>(a);
+  else if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
   else if (a.fmt == 3 && a.nlong > 0) {
     // gsort with long rows: the slices, then k_longrows (one CTA per long row), which publishes its
@@ -731,6 +733,29 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   return PLSS_OK;
 }
 
+// A segment of short rows (mean <= SCALAR_MEAN entries, none above SCALAR_MAX: C4's and C4-alt's
+// columns) takes fmt 5, a thread per row over its own arrays (k_scalar); PLSS_SCALAR=0 disables.
+static plss_status try_scalar(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, int sms, int* grid_out) {
+  if (!env_int("PLSS_SCALAR", 1) || a.nrows == 0 || nnz_seg > (int64_t)SCALAR_MEAN * a.nrows) return PLSS_OK;
+  cudaStream_t st = ctx->stream;
+  int32_t* len = (int32_t*)(ctx->ws + ctx->L.scratch);
+  int* d_max = (int*)(ctx->ws + ctx->L.err + 8);
+  CK(cudaMemsetAsync(d_max, 0, 4, st));
+  k_max_len<<<(unsigned)((a.nrows + 255) / 256), 256, 0, st>>>(a.ptr, a.nrows, d_max);
+  CK(cudaGetLastError());
+  int mx = 0;
+  CK(cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  (void)len;
+  if (mx > SCALAR_MAX) return PLSS_OK;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scalar<ROLE_K2DOTS>, NT, 0));
+  a.fmt = 5;
+  *grid_out = (int)std::max<int64_t>(1, std::min<int64_t>((a.nrows + NT - 1) / NT, (int64_t)std::max(1, occ) * sms));
+  *grid_out = std::min(*grid_out, MAXG);
+  return PLSS_OK;
+}
+
 static plss_status try_sell(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool, int sms, int occ,
                             bool wide_ok = false) {
   cudaStream_t st = ctx->stream;
@@ -1068,7 +1093,9 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     t2off += nt + 1;
     ctx->g2[s] = grid_for(nt, occ[a.finalize ? ROLE_K2DOTS : ROLE_K2], sms);
     if (L.sell) {
-      if (try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool2, sms, occ_sell, win2 == 0 && env_int("PLSS_SIGWIDE", 1))
+      if (try_scalar(ctx, a, ctx->E[s + 1] - ctx->E[s], sms, &ctx->g2[s]) != PLSS_OK) return PLSS_E_CUDA;
+      if (a.fmt == 0 &&
+          try_sell(ctx, a, ctx->E[s + 1] - ctx->E[s], pool2, sms, occ_sell, win2 == 0 && env_int("PLSS_SIGWIDE", 1))
           != PLSS_OK)
         return PLSS_E_CUDA;
       if (a.fmt == 1) ctx->g2[s] = sell_grid(a);
@@ -1638,8 +1665,8 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   if (!ctx) return PLSS_E_INVALID;
   if (sell_segments) {
     int c = 0;
-    for (auto& a : ctx->seg1) c += a.fmt >= 1;
-    for (auto& a : ctx->seg2) c += a.fmt >= 1;
+    for (auto& a : ctx->seg1) c += a.fmt >= 1 && a.fmt <= 3;
+    for (auto& a : ctx->seg2) c += a.fmt >= 1 && a.fmt <= 3;
     *sell_segments = c;
   }
   if (window_segments) {

@@ -97,7 +97,9 @@ struct SpmvSeg {
   // SELL-32 format (fmt = 1): slice s holds rows perm[32s .. 32s+31] column-major, entry j of
   // its lane l at (sptr[s] + j) * 32 + l; padding entries have index -1
   int32_t fmt;               // 0: CSR tiles through TMA (k_spmv), 1: SELL-32 (k_sell),
-                             // 2: SELL-32 + shared-memory window of g (k_sellw)
+                             // 2: SELL-32 + shared-memory window of g (k_sellw), 3: SELL-32 over
+                             // per-SM slice ranges (k_sell<.., 1024>), 5: a thread per short row
+                             // over the original arrays (k_scalar)
   int32_t nslices;
   const int32_t* sptr;       // nslices+1 slice starts in 32-entry steps
   const int32_t* perm;       // slot -> segment-local row (sigma-sorted), -1 for padding; or NULL
@@ -958,6 +960,80 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 }
 
 // ---------------------------------------------------------------------------------------------
+// Segments of short rows (fmt 5: mean length <= SCALAR_MEAN, none longer than SCALAR_MAX; C4's
+// columns: 1.05 entries on average, 35% empty): a thread per row over the original CSR-like arrays
+// -- no SELL copy, no padding, no permutation. Rows are dealt grid-stride (a warp takes 32
+// consecutive rows: coalesced ptr, output and p reads, nearly contiguous entries); each thread sums
+// its row sequentially in ascending order (bitwise the oracle), accumulates its dot terms in a
+// fixed order, and the CTA partials go through the usual fixed-order reduction. 2048 threads per
+// SM at <= 32 registers (the weighted K2 variant spills a few bytes outside the row loop): the row
+// loop is latency-bound, so more rows are in flight than the slice kernel's 32 warps keep. A
+// thread-per-row tail for the short rows of globally sorted K1 segments was measured slower than
+// their SELL slices (C4 K1 0.132 vs 0.110 ms): it serializes perm -> row pointer -> entries.
+constexpr int SCALAR_MEAN = 4;
+constexpr int SCALAR_MAX = 32;
+#ifndef PLSS_SCB
+#define PLSS_SCB 2
+#endif
+constexpr int SCB = PLSS_SCB;           // entries per thread in flight (rows are short)
+#ifndef PLSS_SCMINB
+#define PLSS_SCMINB 8                   // CTAs per SM (2048 threads: C4 K2 0.104 -> 0.089 ms vs 6)
+#endif
+template <int ROLE>
+__global__ void __launch_bounds__(NT, PLSS_SCMINB) k_scalar(SpmvSeg a) {
+  __shared__ double sm[2][MAXW];
+  if (a.ctl != nullptr && a.ctl->done) return;
+  constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
+  const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
+  const uint64_t pol = a.pol_first;
+  double acc0 = 0.0, acc1 = 0.0;
+  const long long stride = (long long)gridDim.x * NT;
+  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < a.nrows; i += stride) {
+    const int e0 = a.ptr[i], e1 = a.ptr[i + 1];
+    double sv = 0.0;
+    if (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate)) sv = a.out[i];
+    double s = (ROLE == ROLE_K1) ? 0.0 : sv;
+    for (int e = e0; e < e1; e += SCB) {
+      int32_t c[SCB];
+      double v[SCB], g[SCB];
+#pragma unroll
+      for (int u = 0; u < SCB; ++u) {
+        c[u] = -1;
+        if (e + u < e1) { c[u] = ld_stream(a.idx + e + u, pol); v[u] = ld_stream(a.val + e + u, pol); }
+      }
+#pragma unroll
+      for (int u = 0; u < SCB; ++u) g[u] = sell_gather(a, c[u]);
+#pragma unroll
+      for (int u = 0; u < SCB; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], g[u]));
+    }
+    double d0 = 0.0, d1 = 0.0;
+    if (ROLE == ROLE_PLAIN) {
+      a.out[i] = s;
+    } else if (ROLE == ROLE_K1) {
+      const double rn = __dsub_rn(sv, s);                        // r_i <- r_i - (A p)_i
+      a.out[i] = rn;
+      d0 = rn * rn;
+    } else {
+      a.out[i] = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, i, s, d0, d1) : s;
+    }
+    if (DOTS) { acc0 += d0; acc1 += d1; }
+  }
+  if (!DOTS) return;
+  if (!a.finalize) {
+    block_sum2(acc0, acc1, sm);
+    if (threadIdx.x == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
+    return;
+  }
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (threadIdx.x != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = acc0;
+    else tail_rho(a.ctl, a.rec, acc0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, acc0, acc1);
+  }
+}
+
 // Long rows (> LONGROW entries) of a globally sorted segment (C4's power-law rows), launched by
 // launch_spmv right after the segment's slices: one 256-thread CTA per row, entries strided over
 // the CTA (coalesced), SU loads in flight per thread, a fixed tree (warp butterflies, then the 8
@@ -1425,6 +1501,10 @@ __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, 
 }
 
 // ---- SELL-32 construction (setup, once per segment) ------------------------------------------
+__global__ void k_max_len(const int32_t* ptr, long long nrows, int* mx) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) atomicMax(mx, ptr[i + 1] - ptr[i]);
+}
 __global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nrows) len[i] = ptr[i + 1] - ptr[i];

@@ -13,10 +13,12 @@ PY
 }
 
 run def
-for uc in 16 64 128; do run ucgs$uc PLSS_UC_GS=$uc; done
+run ls2 PLSS_LSHORT=2
+run ls8 PLSS_LSHORT=8
+run ls0 PLSS_LSHORT=0
 BARGS="--workload C4alt"
 run alt_def
-run alt_uc64 PLSS_UC_GS=64
-run alt_uc128 PLSS_UC_GS=128
+run alt_ls8 PLSS_LSHORT=8
+run alt_ls0 PLSS_LSHORT=0
 BARGS=""
 run def2
