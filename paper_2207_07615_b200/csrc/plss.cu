@@ -126,8 +126,8 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
     L->cblk = take(4 * (size_t)(MAXG + 1) * (2 * S + DCH_MAX));
     // units of one segment: slices + long rows (<= nnz / (LONGROW + 1) of them)
     L->slpart = take(16 * (size_t)(std::max(m, n) / 32 + nnz / (LONGROW + 1) + 4));
-    L->s1auxn = 2 * (m / 32 + 4 * S + 8) + 6 * (nnz / (LONGROW + 1) + 2);
-    L->s2auxn = 2 * ((int64_t)S * (n / 32) + 4 * S + 8) + 6 * (nnz / (LONGROW + 1) + 2);
+    L->s1auxn = 2 * (m / 32 + 4 * S + 8) + 8 * (nnz / (LONGROW + 1) + 2);
+    L->s2auxn = 2 * ((int64_t)S * (n / 32) + 4 * S + 8) + 8 * (nnz / (LONGROW + 1) + 2);
     L->s1aux = take(4 * (size_t)L->s1auxn);
     L->s2aux = take(4 * (size_t)L->s2auxn);
   }
@@ -670,7 +670,7 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   const int64_t nsl = (nshort + 31) / 32;
   const int64_t nlr = (int64_t)lrows.size();
   const int64_t nunits = nsl;                       // long rows run in k_longrows, not as k_sell units
-  const int64_t aux_need = nlr + 4 * nlr + 2 + nunits + 1;   // lrows, lrowd (2 doubles), align, uw
+  const int64_t aux_need = 3 * nlr + 4 * nlr + 2 + nunits + 1;   // lrows, lbeg (2), lrowd (2 doubles), align, uw
   if (pool.used_slots + nsl * 32 > pool.slots || pool.used_sp + nsl + 1 > pool.sp ||
       pool.used_aux + aux_need > pool.auxn)
     return PLSS_OK;
@@ -697,12 +697,34 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   if ((double)(steps * 32) > 1.15 * (double)nnz_seg + 32.0 * 32 * (LONGROW + 1)) return PLSS_OK;
   int32_t* d_perm = pool.perm + pool.used_slots;
   int32_t* d_sp = pool.sptr + pool.used_sp;
+  // long rows longest first (CTA k of k_longrows takes the k-th: the longest start in the first
+  // wave), each with its absolute entry range (no lrows -> row pointer load chain on the device)
+  int32_t p0 = 0;
+  CK(cudaMemcpyAsync(&p0, a.ptr, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> rstart;
+  if (!lrows.empty()) {
+    std::vector<int64_t> pre(nrows + 1, p0);
+    for (int64_t i = 0; i < nrows; ++i) pre[i + 1] = pre[i] + len[i];
+    std::stable_sort(lrows.begin(), lrows.end(), [&](int32_t x, int32_t y) { return len[x] > len[y]; });
+    rstart.resize(lrows.size());
+    for (size_t k = 0; k < lrows.size(); ++k) rstart[k] = pre[lrows[k]];
+  }
+  std::vector<int32_t> lbeg(2 * lrows.size());
+  for (size_t k = 0; k < lrows.size(); ++k) {
+    lbeg[2 * k] = (int32_t)rstart[k];
+    lbeg[2 * k + 1] = (int32_t)(rstart[k] + len[lrows[k]]);
+  }
   int32_t* d_lrows = pool.aux + pool.used_aux;
-  double* d_lrowd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(d_lrows + nlr) + 7) & ~(uintptr_t)7);
+  int32_t* d_lbeg = d_lrows + nlr;
+  double* d_lrowd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(d_lbeg + 2 * nlr) + 7) & ~(uintptr_t)7);
   int32_t* d_uw = reinterpret_cast<int32_t*>(d_lrowd + 2 * nlr);
   CK(cudaMemcpyAsync(d_perm, perm.data(), 4 * perm.size(), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_sp, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice, st));
-  if (!lrows.empty()) CK(cudaMemcpyAsync(d_lrows, lrows.data(), 4 * lrows.size(), cudaMemcpyHostToDevice, st));
+  if (!lrows.empty()) {
+    CK(cudaMemcpyAsync(d_lrows, lrows.data(), 4 * lrows.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_lbeg, lbeg.data(), 4 * lbeg.size(), cudaMemcpyHostToDevice, st));
+  }
   CK(cudaMemcpyAsync(d_uw, uw.data(), 4 * uw.size(), cudaMemcpyHostToDevice, st));
   int32_t* sidx = pool.idx + pool.used;
   double* sval = pool.val + pool.used;
@@ -719,6 +741,7 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   a.nlong = (int32_t)lrows.size();
   a.lrows = d_lrows;
   a.lrowd = d_lrowd;
+  a.lbeg = d_lbeg;
   a.lcounter = ctx->counters + 8;
   a.lptr = a.ptr;
   a.lidx = a.idx;

@@ -121,6 +121,9 @@ struct SpmvSeg {
   // (2 doubles, reduced in row order by the last CTA) and that CTA's election counter
   double* lrowd;
   unsigned* lcounter;
+  const int32_t* lbeg;       // k_longrows: entry range [lbeg[2k], lbeg[2k+1]) of long row k (absolute
+                             // positions; setup orders the long rows by length, longest first)
+  
   const int32_t* lidx;
   const double* lval;
   const int32_t* uw;         // nunits+1 prefix of stored entries per unit (CTA balance), or NULL
@@ -1055,7 +1058,7 @@ __global__ void __launch_bounds__(NT) k_longrows(SpmvSeg a) {
   const uint64_t pol = a.pol_first;
   const int k = blockIdx.x;
   const int r = a.lrows[k];
-  const int e0 = a.lptr[r], e1 = a.lptr[r + 1];
+  const int e0 = a.lbeg[2 * k], e1 = a.lbeg[2 * k + 1];      // independent of r: no load chain
   double start = 0.0;
   if (tid == 0 && (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate))) start = a.out[r];
   double ps = 0.0;
@@ -1503,7 +1506,10 @@ __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, 
 // ---- SELL-32 construction (setup, once per segment) ------------------------------------------
 __global__ void k_max_len(const int32_t* ptr, long long nrows, int* mx) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nrows) atomicMax(mx, ptr[i + 1] - ptr[i]);
+  int l = i < nrows ? ptr[i + 1] - ptr[i] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(FULL, l, o));
+  if ((threadIdx.x & 31) == 0 && l > 0) atomicMax(mx, l);
 }
 __global__ void k_row_len(const int32_t* ptr, long long nrows, int32_t* len) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -13,12 +13,7 @@ PY
 }
 
 run def
-run ls2 PLSS_LSHORT=2
-run ls8 PLSS_LSHORT=8
-run ls0 PLSS_LSHORT=0
 BARGS="--workload C4alt"
 run alt_def
-run alt_ls8 PLSS_LSHORT=8
-run alt_ls0 PLSS_LSHORT=0
 BARGS=""
 run def2
