@@ -96,15 +96,20 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic(workload, kernel_class, launches_per_step, capture="r01_ncu_traffic_c5.json"):
-    """DRAM bytes (read + write) per step of the dominant kernel class, from the committed
-    `ncu --set full` capture (profiles/r01_ncu_traffic_c5*.json: per-launch averages x launches
-    per step). None when no capture of this workload exists."""
+def _traffic(workload, kernel_class, launches_per_step, capture=None):
+    """DRAM bytes (read + write) per step of a kernel class, from the committed `ncu --set full`
+    capture of the workload (profiles/r02_ncu_traffic_<workload>.json: one whole step of the round-2
+    build, scripts/ncu_traffic.py; the randomized-projection capture keeps its round-1 per-launch
+    form). None when no capture of this workload exists."""
+    capture = capture or f"r02_ncu_traffic_{workload.lower()}.json"
     path = os.path.join(ROOT, "profiles", capture)
-    if workload != "C5" or not os.path.exists(path):
+    if not os.path.exists(path):
         return None, None
     with open(path) as f:
         d = json.load(f)
+    if "per_step" in d:
+        e = d["per_step"].get(kernel_class)
+        return (None, None) if e is None else (e["dram_bytes"], f"{os.path.relpath(path, ROOT)}: {d['source']}")
     e = d["per_launch"].get(kernel_class)
     if e is None:
         return None, None
@@ -695,7 +700,7 @@ def main_rp(args):
     dom_ms = _apportion(ms / args.steps, kt, {"rp_spmm_AtS": "spmm", "rp_sketch_gen": "gen", "k1_spmv_csr_resid": "k1",
                                               "rp_gram": "gram", "rp_update": "update"}[dom])
     peak, peak_src = _peaks()
-    traffic, traffic_src = (_traffic(name, dom, 1, "r01_ncu_traffic_c5_rp.json") if (r == 5 and dens == 1.0)
+    traffic, traffic_src = (_traffic(name, dom, 1, "r01_ncu_traffic_c5_rp.json") if (name == "C5" and r == 5 and dens == 1.0)
                             else (None, None))
     pin_b = torch.empty(w["m"], dtype=torch.float64, pin_memory=True)
     pin_b.copy_(b.cpu())
