@@ -657,7 +657,7 @@ static plss_status try_window(plss_ctx* ctx, SpmvSeg& a, const double* g, int64_
 static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, SellPool& pool) {
   cudaStream_t st = ctx->stream;
   const int64_t nrows = a.nrows;
-  if (PLSS_PAIR > 1 || !env_int("PLSS_GSORT", 1)) return PLSS_OK;   // long-row units: one slice per unit
+  if (!env_int("PLSS_GSORT", 1)) return PLSS_OK;
   std::vector<int32_t> len(nrows);
   CK(cudaMemcpyAsync(len.data(), ctx->ws + ctx->L.scratch, 4 * (size_t)nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
