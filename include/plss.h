@@ -221,6 +221,14 @@ plss_status plss_profile(plss_ctx *ctx, int32_t k, double *ms);
  * window, grid sizes of the first K1 / K2 launch, how many of the 2*slabs SpMV segments use
  * the SELL-32 format (the rest use TMA-staged CSR tiles) and how many of those gather through a
  * shared-memory window of the gathered vector. Any pointer may be NULL. */
+/* The format a ctx chose for K1 (which = 1) or K2 (which = 2) of row slab `slab`:
+ * info[0] fmt (0 CSR tiles, 1 SELL-32 grid-stride, 2 SELL-32 + shared-memory window, 3 SELL-32 over
+ * per-SM ranges, 5 a thread per short row), info[1] the sigma window of a sigma-permuted SELL segment
+ * (512 or 1024; 0 otherwise), info[2] 1 if globally length-sorted, info[3] SELL slices, info[4] long
+ * rows (run by k_longrows), info[5] static stepping (1, or 2 with 6 entries in flight), info[6] the
+ * grid, info[7] the segment's rows. PLSS_E_INVALID for a bad ctx / which / slab. */
+plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[8]);
+
 /* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
  * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:
  * out (host, 4 * grid uint64) = {start ns, end ns (%globaltimer), stored entries, units} per CTA

@@ -13,5 +13,5 @@ from .plss import (  # noqa: F401
     plss_rp_solve, plss_rp_start, plss_rp_step, plss_rp_finish, plss_rp_sketch, plss_spmmT, plss_rp_profile, rp_ld,
     plss_kz_solve, plss_kz_start, plss_kz_step, plss_kz_finish, plss_kz_profile,
     plss_eg_solve, plss_eg_start, plss_eg_step, plss_eg_finish, plss_eg_profile,
-    plss_true_residual, plss_peer_reduce_emulate, plss_create_dist_cols, plss_debug_cta_times,
+    plss_true_residual, plss_peer_reduce_emulate, plss_create_dist_cols, plss_debug_cta_times, plss_query_segment,
 )

@@ -1713,6 +1713,20 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   return PLSS_OK;
 }
 
+plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[8]) {
+  if (!ctx || !info || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
+  const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
+  info[0] = a.fmt;
+  info[1] = a.fmt >= 1 && a.fmt <= 3 && a.perm && !a.gsort ? (a.sig ? a.sig : SIGMA) : 0;
+  info[2] = a.gsort;
+  info[3] = a.nslices;
+  info[4] = a.nlong;
+  info[5] = a.stat;
+  info[6] = which == 1 ? ctx->g1[slab] : ctx->g2[slab];
+  info[7] = a.nrows;
+  return PLSS_OK;
+}
+
 plss_status plss_debug_cta_times(plss_ctx* ctx, int32_t which, int32_t slab, uint64_t* out, int32_t* grid) {
   if (!ctx || !out || !grid || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
   const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];

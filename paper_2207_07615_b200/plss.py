@@ -31,7 +31,7 @@ SYMBOLS = ["plss_workspace_bytes", "plss_create", "plss_get_unique_id", "plss_cr
            "plss_kz_workspace_bytes", "plss_kz_solve", "plss_kz_start", "plss_kz_step", "plss_kz_finish",
            "plss_kz_profile", "plss_eg_workspace_bytes", "plss_eg_solve", "plss_eg_start", "plss_eg_step",
            "plss_eg_finish", "plss_eg_profile", "plss_true_residual", "plss_peer_reduce_emulate",
-           "plss_create_dist_cols", "plss_debug_cta_times"]
+           "plss_create_dist_cols", "plss_debug_cta_times", "plss_query_segment"]
 
 
 class PlssError(RuntimeError):
@@ -149,8 +149,12 @@ def load_library(path: str = None):
     lib.plss_create_dist_cols.restype = st
     lib.plss_peer_reduce_emulate.argtypes = [I32, P, P, P, I32, P, P]
     lib.plss_peer_reduce_emulate.restype = st
+    lib.plss_query_segment.argtypes = [P, I32, I32, P]
+    lib.plss_query_segment.restype = st
     lib.plss_debug_cta_times.argtypes = [P, I32, I32, P, ctypes.POINTER(I32)]
     lib.plss_debug_cta_times.restype = st
+    lib.plss_query_segment.argtypes = [P, I32, I32, P]
+    lib.plss_query_segment.restype = st
     lib.plss_debug_cta_times.argtypes = [P, I32, I32, P, ctypes.POINTER(I32)]
     lib.plss_debug_cta_times.restype = st
     lib.plss_destroy.argtypes = [P]
@@ -450,6 +454,14 @@ def plss_peer_reduce_emulate(parts, reds, flags, bounds, stream=None):
     return reds
 
 
+def plss_query_segment(ctx: Ctx, which: int, slab: int = 0) -> dict:
+    """The format chosen for K1 (which = 1) / K2 (which = 2) of a row slab (include/plss.h)."""
+    info = np.zeros(8, dtype=np.int32)
+    _check(load_library().plss_query_segment(ctx.handle, int(which), int(slab), info.ctypes.data), ctx.handle)
+    keys = ("fmt", "sig", "gsort", "nslices", "nlong", "stat", "grid", "rows")
+    return {k: int(v) for k, v in zip(keys, info)}
+
+
 def plss_debug_cta_times(ctx: Ctx, which: int, slab: int = 0):
     """Diagnostics (PLSS_DBG_CTA=1 at create): per-CTA {start ns, end ns, entries, units} of the
     last K1 (which = 1) / K2 (which = 2) launch of a slab, as an int64 array [grid, 4]."""
@@ -458,6 +470,14 @@ def plss_debug_cta_times(ctx: Ctx, which: int, slab: int = 0):
     _check(load_library().plss_debug_cta_times(ctx.handle, int(which), int(slab), out.ctypes.data, ctypes.byref(g)),
            ctx.handle)
     return out[:4 * g.value].reshape(g.value, 4).astype(np.int64)
+
+
+def plss_query_segment(ctx: Ctx, which: int, slab: int = 0) -> dict:
+    """The format chosen for K1 (which = 1) / K2 (which = 2) of a row slab (include/plss.h)."""
+    info = np.zeros(8, dtype=np.int32)
+    _check(load_library().plss_query_segment(ctx.handle, int(which), int(slab), info.ctypes.data), ctx.handle)
+    keys = ("fmt", "sig", "gsort", "nslices", "nlong", "stat", "grid", "rows")
+    return {k: int(v) for k, v in zip(keys, info)}
 
 
 def plss_debug_cta_times(ctx: Ctx, which: int, slab: int = 0):

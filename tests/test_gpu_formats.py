@@ -1,0 +1,155 @@
+"""GPU: which format each segment takes (plss_query_segment) and the round-2 formats
+against the oracle: static stepping (C5's K1), globally sorted rows with the long ones in
+k_longrows (C4's K1), a thread per short column (k_scalar, C4's K2), and the 1024-row sigma windows
+of K2 (the SIGMA_WIDE path had no test of its own), each bitwise on its SpMV outputs,
+repeatable, and inside a solve (also on a single-rank chunked distributed ctx)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import plss_gen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2207_07615_b200 import build as pbuild
+    pbuild.build()
+    import paper_2207_07615_b200 as p
+    p.load_library()
+    assert torch.cuda.is_available()
+    return p
+
+
+class _env:
+    def __init__(self, **kw):
+        self.kw = {k: str(v) for k, v in kw.items()}
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kw}
+        os.environ.update(self.kw)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _matrix(pkg, s):
+    return pkg.Matrix.from_arrays(s.m, s.n, s.row_ptr, s.col_idx, s.val, s.col_ptr, s.row_idx, s.val_t)
+
+
+def _spmv_pair(pkg, ctx, s, x, u):
+    y = torch.empty(s.m, dtype=torch.float64, device="cuda")
+    v = torch.empty(s.n, dtype=torch.float64, device="cuda")
+    pkg.plss_spmv(ctx, torch.from_numpy(x).cuda(), y)
+    pkg.plss_spmvT(ctx, torch.from_numpy(u).cuda(), v)
+    return y.cpu().numpy(), v.cpu().numpy()
+
+
+def _check(got, ptr, idx, val, vec, ref):
+    lens = np.diff(ptr)
+    short = lens <= 128
+    np.testing.assert_array_equal(got[short], ref[short])
+    for i in np.nonzero(~short)[0]:
+        seg = slice(ptr[i], ptr[i + 1])
+        assert abs(got[i] - ref[i]) <= 2.3e-16 * lens[i] * np.sum(np.abs(val[seg] * vec[idx[seg]]))
+
+
+def _spmv_bitwise_repeatable(pkg, ctx, s, seed=1):
+    rng = np.random.default_rng(seed)
+    x, u = rng.standard_normal(s.n), rng.standard_normal(s.m)
+    y, v = _spmv_pair(pkg, ctx, s, x, u)
+    _check(y, s.row_ptr, s.col_idx, s.val, x, oracle.spmv(s.m, s.row_ptr, s.col_idx, s.val, x))
+    _check(v, s.col_ptr, s.row_idx, s.val_t, u, oracle.spmvT(s.n, s.col_ptr, s.row_idx, s.val_t, u))
+    for _ in range(3):
+        y2, v2 = _spmv_pair(pkg, ctx, s, x, u)
+        np.testing.assert_array_equal(y2, y)
+        np.testing.assert_array_equal(v2, v)
+
+
+def test_c5_formats_static_k1_sigma_k2(pkg):
+    s = plss_gen.make_config("C5xs")
+    ctx = pkg.plss_create(_matrix(pkg, s), slabs=4, maxit_cap=8)
+    for sl in range(4):
+        k1 = pkg.plss_query_segment(ctx, 1, sl)
+        k2 = pkg.plss_query_segment(ctx, 2, sl)
+        assert k1["fmt"] == 3 and k1["stat"] == 2 and k1["gsort"] == 0     # rows of 12: 6 in flight
+        assert k2["fmt"] == 3 and k2["sig"] == 512 and k2["stat"] == 0
+    _spmv_bitwise_repeatable(pkg, ctx, s)
+    pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("name", ["C4s", "C4xs"])
+def test_c4_formats_longrows_and_scalar(pkg, name):
+    s = plss_gen.make_config(name)
+    ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=8)
+    k1 = pkg.plss_query_segment(ctx, 1, 0)
+    k2 = pkg.plss_query_segment(ctx, 2, 0)
+    assert k1["fmt"] == 3 and k1["gsort"] == 1 and k1["nlong"] == int((np.diff(s.row_ptr) > 128).sum()) > 0
+    assert k2["fmt"] == 5                                   # columns of ~1 entry: a thread per column
+    _spmv_bitwise_repeatable(pkg, ctx, s)
+    pkg.plss_destroy(ctx)
+
+
+def test_k2_wide_sigma_windows(pkg):
+    """With k_scalar off, C4s's K2 columns (power-law transposed: 35% empty) leave > 15% padding in
+    512-row sigma windows and take 1024-row ones (SIGMA_WIDE, y staged in shared memory);
+    PLSS_SIGWIDE=0 sends them to the global sort. Both bitwise and repeatable, and the solve agrees
+    with the default formats' solve within the parity floor."""
+    s = plss_gen.make_config("C4s")
+    with _env(PLSS_SCALAR=0):
+        ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+    k2 = pkg.plss_query_segment(ctx, 2, 0)
+    assert k2["fmt"] == 3 and k2["sig"] == 1024 and k2["gsort"] == 0, k2
+    _spmv_bitwise_repeatable(pkg, ctx, s)
+    b = torch.from_numpy(s.b).cuda()
+    wide = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
+    pkg.plss_destroy(ctx)
+    with _env(PLSS_SCALAR=0, PLSS_SIGWIDE=0):
+        ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+    k2 = pkg.plss_query_segment(ctx, 2, 0)
+    assert k2["fmt"] == 3 and k2["sig"] == 0 and k2["gsort"] == 1, k2
+    _spmv_bitwise_repeatable(pkg, ctx, s)
+    glob = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
+    pkg.plss_destroy(ctx)
+    ref = oracle.plss_system(s, maxit=40)
+    k = 12                                                   # C4s's K_f is 16 (tests/golden/parity_floor.json)
+    for res in (wide, glob):
+        assert np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+
+
+def test_wide_sigma_chunked_dist_single_rank(pkg):
+    """the column chunks of the distributed step (make_chunks) follow the segment's sigma
+    window; a single-rank NCCL ctx whose last K2 segment has 1024-row windows solves like the plain
+    ctx and bitwise like its own unchunked form."""
+    s = plss_gen.make_config("C4s")
+    A = _matrix(pkg, s)
+    b = torch.from_numpy(s.b).cuda()
+    out = {}
+    for chunks in (1, 4):
+        with _env(PLSS_SCALAR=0, PLSS_DIST_CHUNKS=chunks):
+            ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=1, maxit_cap=60)
+        assert pkg.plss_query_segment(ctx, 2, 0)["sig"] == 1024
+        out[chunks] = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
+        out[chunks]["xh"] = out[chunks]["x"].cpu().numpy()
+        pkg.plss_destroy(ctx)
+    np.testing.assert_array_equal(out[1]["hist"], out[4]["hist"])
+    np.testing.assert_array_equal(out[1]["xh"], out[4]["xh"])
+    ref = oracle.plss_system(s, maxit=40)
+    assert np.max(np.abs(out[4]["hist"][:12] - ref["hist"][:12]) / ref["hist"][:12]) <= 1e-9
+
+
+def test_query_segment_rejects_bad_arguments(pkg):
+    s = plss_gen.make_config("C1")
+    ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=4)
+    for which, slab in ((0, 0), (3, 0), (1, 5), (2, -1)):
+        with pytest.raises(pkg.PlssError):
+            pkg.plss_query_segment(ctx, which, slab)
+    pkg.plss_destroy(ctx)
