@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
       }
       nx = __shfl_sync(FULL, nx, 0);
     }
-#ifdef PLSS_DBGCTA
+#if defined(PLSS_DBGCTA) && PLSS_DBGCTA > 1
     if (DYN && a.ctat && lane == 0)
       for (int q = 0; q < P; ++q) if (su + q < sl1) { dbg_entries += (LU && su + q >= a.nslices) ? L[q] : 32ull * L[q]; dbg_units++; }
 #endif

@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--slab", type=int, default=0)
+    ap.add_argument("--all-slabs", action="store_true", help="one line per slab: K1 / K2 max and median CTA us")
     args = ap.parse_args()
     import torch
     import paper_2207_07615_b200 as pkg
@@ -29,6 +30,30 @@ def main():
     A = pkg.Matrix(w["m"], w["n"], w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])
     ctx = pkg.plss_create(A, maxit_cap=16)
     pkg.plss_solve(ctx, w["b"], tol=0.0, maxit=6, flags=1)
+    if args.all_slabs:
+        S = pkg.plss_query(ctx)["slabs"]
+        ev = []
+        for sl in range(S):
+            for which in (1, 2):
+                t = pkg.plss_debug_cta_times(ctx, which, sl)
+                ev.append((f"K{which}_{sl}", t[:, 0].min(), t[:, 1].max()))
+        t0 = ev[0][1]
+        print("timeline of the last step (us from K1_0's first CTA): launch [start, end] gap-before")
+        prev = None
+        for name, a, b in ev:
+            gap = (a - prev) / 1e3 if prev is not None else 0.0
+            print(f"   {name:6s} [{(a - t0) / 1e3:8.1f}, {(b - t0) / 1e3:8.1f}]  gap {gap:6.1f}")
+            prev = b
+        for sl in range(S):
+            line = []
+            for which in (1, 2):
+                t = pkg.plss_debug_cta_times(ctx, which, sl)
+                dur = (t[:, 1] - t[:, 0]) / 1e3
+                span = (t[:, 1].max() - t[:, 0].min()) / 1e3
+                line.append(f"K{which} max {dur.max():6.1f} med {np.median(dur):6.1f} span {span:6.1f}")
+            print(f"slab {sl}: " + " | ".join(line))
+        pkg.plss_destroy(ctx)
+        return
     for which, name in ((1, "K1"), (2, "K2")):
         t = pkg.plss_debug_cta_times(ctx, which, args.slab)
         dur = (t[:, 1] - t[:, 0]) / 1e3
