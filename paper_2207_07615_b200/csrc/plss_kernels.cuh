@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
     for (int q = 0; q < P; ++q) {
       valid[q] = row[q] >= 0 && row[q] < a.nrows;
       s[q] = 0.0;
-#if !(PLSS_ABLATE & 32)
+#if !(PLSS_ABLATE & (32 | 64))
       if (ROLE >= ROLE_K2 && valid[q] && a.accumulate) s[q] = a.out[row[q]];
 #endif
       r_old[q] = (ROLE == ROLE_K1 && valid[q]) ? a.out[row[q]] : 0.0;   // issued early
