@@ -761,7 +761,6 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
 static plss_status try_scalar(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, int sms, int* grid_out) {
   if (!env_int("PLSS_SCALAR", 1) || a.nrows == 0 || nnz_seg > (int64_t)SCALAR_MEAN * a.nrows) return PLSS_OK;
   cudaStream_t st = ctx->stream;
-  int32_t* len = (int32_t*)(ctx->ws + ctx->L.scratch);
   int* d_max = (int*)(ctx->ws + ctx->L.err + 8);
   CK(cudaMemsetAsync(d_max, 0, 4, st));
   k_max_len<<<(unsigned)((a.nrows + 255) / 256), 256, 0, st>>>(a.ptr, a.nrows, d_max);
@@ -769,7 +768,6 @@ static plss_status try_scalar(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, int sm
   int mx = 0;
   CK(cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  (void)len;
   if (mx > SCALAR_MAX) return PLSS_OK;
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scalar<ROLE_K2DOTS>, NT, 0));
