@@ -285,6 +285,88 @@ __global__ void __launch_bounds__(1024, 1) k1x(const int32_t* __restrict__ idx, 
 }
 __global__ void fill_sptr(int32_t* sptr, int n) { int i = blockIdx.x * blockDim.x + threadIdx.x; if (i <= n) sptr[i] = i * L; }
 
+
+// 128-bit per-lane stream loads (the north star names 128-bit vectorised loads
+// of the idx / val streams): slice layout with 4 steps of a lane's indices in one int4 and 2 steps
+// of its values in one double2 (lane l, steps 4q..4q+3 at idx4[(s*L/4 + q)*32 + l]).
+__global__ void relayout_v(const int32_t* idx, const double* val, int4* idx4, double2* val2, int nslices) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)nslices * 32) return;
+  const long long s = t / 32, l = t % 32;
+  for (int q = 0; q < L / 4; ++q) {
+    int4 v;
+    v.x = idx[(s * L + 4 * q + 0) * 32 + l]; v.y = idx[(s * L + 4 * q + 1) * 32 + l];
+    v.z = idx[(s * L + 4 * q + 2) * 32 + l]; v.w = idx[(s * L + 4 * q + 3) * 32 + l];
+    idx4[(s * (L / 4) + q) * 32 + l] = v;
+  }
+  for (int q = 0; q < L / 2; ++q) {
+    double2 v;
+    v.x = val[(s * L + 2 * q) * 32 + l]; v.y = val[(s * L + 2 * q + 1) * 32 + l];
+    val2[(s * (L / 2) + q) * 32 + l] = v;
+  }
+}
+__device__ __forceinline__ int4 ldi4_stream(const int4* p) {
+  int4 v; asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p)); return v;
+}
+__device__ __forceinline__ double2 ldd2_stream(const double2* p) {
+  double2 v; asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p)); return v;
+}
+__global__ void __launch_bounds__(1024, 1) k1v(const int4* __restrict__ idx4, const double2* __restrict__ val2,
+                                              const double* __restrict__ p, double* __restrict__ r, int nslices) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = (int)((long long)nslices * blockIdx.x / gridDim.x), s1 = (int)((long long)nslices * (blockIdx.x + 1) / gridDim.x);
+  for (int s = s0 + warp; s < s1; s += 32) {
+    const long long row = (long long)s * 32 + lane;
+    const double rold = r[row];
+    double sum = 0.0;
+#pragma unroll
+    for (int h = 0; h < L / 6; ++h) {                     // two batches of 6 steps
+      int c[6]; double v[6], g[6];
+      const int4 a0 = ldi4_stream(idx4 + ((long long)s * (L / 4) + 3 * h / 2) * 32 + lane);
+      (void)a0;
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        const int j = 6 * h + u;
+        const int4 q4 = ldi4_stream(idx4 + ((long long)s * (L / 4) + j / 4) * 32 + lane);
+        c[u] = (j & 3) == 0 ? q4.x : (j & 3) == 1 ? q4.y : (j & 3) == 2 ? q4.z : q4.w;
+      }
+#pragma unroll
+      for (int u = 0; u < 6; u += 2) {
+        const double2 d2 = ldd2_stream(val2 + ((long long)s * (L / 2) + (6 * h + u) / 2) * 32 + lane);
+        v[u] = d2.x; v[u + 1] = d2.y;
+      }
+#pragma unroll
+      for (int u = 0; u < 6; ++u) g[u] = __ldg(p + c[u]);
+#pragma unroll
+      for (int u = 0; u < 6; ++u) sum = __dadd_rn(sum, __dmul_rn(v[u], g[u]));
+    }
+    r[row] = rold - sum;
+  }
+}
+// the same with all 12 indices from 3 int4 loads and 12 values from 6 double2 loads up front
+__global__ void __launch_bounds__(1024, 1) k1v12(const int4* __restrict__ idx4, const double2* __restrict__ val2,
+                                                const double* __restrict__ p, double* __restrict__ r, int nslices) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = (int)((long long)nslices * blockIdx.x / gridDim.x), s1 = (int)((long long)nslices * (blockIdx.x + 1) / gridDim.x);
+  for (int s = s0 + warp; s < s1; s += 32) {
+    const long long row = (long long)s * 32 + lane;
+    const double rold = r[row];
+    int4 q[3]; double2 d[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q[k] = ldi4_stream(idx4 + ((long long)s * 3 + k) * 32 + lane);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d[k] = ldd2_stream(val2 + ((long long)s * 6 + k) * 32 + lane);
+    const int c[12] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w, q[2].x, q[2].y, q[2].z, q[2].w};
+    double g[12];
+#pragma unroll
+    for (int u = 0; u < 12; ++u) g[u] = __ldg(p + c[u]);
+    double sum = 0.0;
+#pragma unroll
+    for (int u = 0; u < 12; ++u) sum = __dadd_rn(sum, __dmul_rn(u & 1 ? d[u / 2].y : d[u / 2].x, g[u]));
+    r[row] = rold - sum;
+  }
+}
+
 // Split layout: band part (6 steps) from the shared-memory window, uniform part (6 steps) from
 // global memory; no per-lane branch.
 template <int BS>
@@ -539,6 +621,17 @@ int main() {
     a.pol_first = 0;
     rep("libplss k_sell<K1,1024,STAT> policy 0", timeit([&] { plss::k_sell<plss::ROLE_K1, 1024, false, false, plss::SIGMA, true><<<sms, 1024>>>(a); }), k1_bytes, nnz);
     CK(cudaFree(sptr)); CK(cudaFree(slpart)); CK(cudaFree(cblk)); CK(cudaFree(part)); CK(cudaFree(cnt));
+  }
+
+  {
+    int4* idx4; double2* val2;
+    CK(cudaMalloc(&idx4, nnz * 4)); CK(cudaMalloc(&val2, nnz * 8));
+    relayout_v<<<(nsl * 32 + 255) / 256, 256>>>(idx, val, idx4, val2, nsl);
+    CK(cudaDeviceSynchronize());
+    rep("K1 128-bit lanes: int4 idx + double2 val, batches of 6", timeit([&] { k1v<<<sms, 1024>>>(idx4, val2, p, r, nsl); }), k1_bytes, nnz);
+    rep("K1 128-bit lanes: all 12 up front", timeit([&] { k1v12<<<sms, 1024>>>(idx4, val2, p, r, nsl); }), k1_bytes, nnz);
+    rep("K1 plain (reference, SU 6)", K1(k1<0, 1024, 6>, 1024, sms, 0, 0), k1_bytes, nnz);
+    CK(cudaFree(idx4)); CK(cudaFree(val2));
   }
   if (getenv("BB_ALL")) for (int ch : {64, 256, 1024}) {
     char nm[96];
