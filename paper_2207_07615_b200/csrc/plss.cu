@@ -1698,12 +1698,16 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   }
   // our kernels per loop step: K1 and K2 per slab (the last K2 as column chunks on a chunked
   // distributed ctx), K3, and the distributed dots / tail kernel
+  // (+1 for every globally sorted segment with long rows: k_longrows runs after its slices)
+  int extra = 0;
+  for (auto& a : ctx->seg1) extra += (a.fmt == 3 && a.nlong > 0) ? 1 : 0;
+  for (auto& a : ctx->seg2) extra += (a.fmt == 3 && a.nlong > 0) ? 1 : 0;
   if (launches_per_step && ctx->cols)          // K1, K2 per slab; rho tail, dots, phi tail, K3
-    *launches_per_step = 2 * ctx->S + 4;
+    *launches_per_step = 2 * ctx->S + 4 + extra;
   else if (launches_per_step)
     *launches_per_step = 2 * ctx->S + 1 + (ctx->dist ? 1 : 0) + (ctx->rsag ? 1 : 0) +
                          (ctx->dch.empty() ? 0 : (int)ctx->dch.size() - 1) +
-                         (ctx->peer ? peer_nch(ctx) + 1 : 0);
+                         (ctx->peer ? peer_nch(ctx) + 1 : 0) + extra;
   if (slabs) *slabs = ctx->S;
   if (tile_nnz) *tile_nnz = TILE;
   if (grid_k1) *grid_k1 = ctx->g1.empty() ? 0 : ctx->g1[0];

@@ -229,7 +229,10 @@ def test_dist_column_block_step(pkg, name, slabs, weighted, x0):
         ctx = mk(A, 0, s.n if cols else s.m, pkg.plss_get_unique_id(), 0, 1, slabs=slabs, maxit_cap=s.maxit,
                  validate=True)
         if cols:
-            assert pkg.plss_query(ctx)["launches_per_step"] == 2 * pkg.plss_query(ctx)["slabs"] + 4
+            S = pkg.plss_query(ctx)["slabs"]
+            extra = sum(1 for w in (1, 2) for sl in range(S)            # k_longrows after a gsort segment
+                        if pkg.plss_query_segment(ctx, w, sl)["fmt"] == 3 and pkg.plss_query_segment(ctx, w, sl)["nlong"] > 0)
+            assert pkg.plss_query(ctx)["launches_per_step"] == 2 * S + 4 + extra
         wi = None
         if weighted:
             wi = pkg.plss_column_norms(ctx)

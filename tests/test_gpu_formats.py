@@ -94,6 +94,7 @@ def test_c4_formats_longrows_and_scalar(pkg, name):
     k2 = pkg.plss_query_segment(ctx, 2, 0)
     assert k1["fmt"] == 3 and k1["gsort"] == 1 and k1["nlong"] == int((np.diff(s.row_ptr) > 128).sum()) > 0
     assert k2["fmt"] == 5                                   # columns of ~1 entry: a thread per column
+    assert pkg.plss_query(ctx)["launches_per_step"] == 4    # k_sell + k_longrows, k_scalar, K3
     _spmv_bitwise_repeatable(pkg, ctx, s)
     pkg.plss_destroy(ctx)
 
