@@ -582,7 +582,10 @@ def main():
                        "rhs": ("paper: x = ones, x(1) = 10, b = A x (P:L987)" if args.rhs == "paper"
                                else "b = A x*, x* ~ N(0,1)"),
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
-                       "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8"},
+                       "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8",
+                       "workspace_gb": round(ctx.workspace.numel() / 1e9, 3),
+                       "matrix_gb": round(sum(t.numel() * t.element_size() for t in (
+                           w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])) / 1e9, 3)},
             "achieved_gbs": B_global * iters_per_s / 1e9,
             "achieved_frac_of_peak": B_global * iters_per_s / 1e9 / peak,
             "achieved_frac_of_8tbs": B_global * iters_per_s / 1e9 / 8000.0,

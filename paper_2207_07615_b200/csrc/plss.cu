@@ -133,9 +133,15 @@ bool compute_layout(const plss_matrix* A, const plss_options* opt, bool dist, La
   }
   L->scratch_blk = take(4 * (size_t)((std::max(m, n) + 2) / (NT * SCAN_ITEMS) + 2));
   if (S > 1) {
-    L->sptr = take(4 * (size_t)S * (n + 1));
-    L->sidx = take(4 * (size_t)nnz);
-    L->sval = take(8 * (size_t)nnz);
+    // the slab-major CSC: in the workspace without SELL-32; with it, a setup-time allocation that
+    // is released once every K2 segment streams its own SELL copy (setup, "slab-major CSC")
+    if (!L->sell) {
+      L->sptr = take(4 * (size_t)S * (n + 1));
+      L->sidx = take(4 * (size_t)nnz);
+      L->sval = take(8 * (size_t)nnz);
+    } else {
+      L->sptr = L->sidx = L->sval = 0;
+    }
     L->scan_cnt = take(4 * (size_t)(n + 1));
     L->scan_blk = take(4 * (size_t)((n + 1) / (NT * SCAN_ITEMS) + 2));
   } else {
@@ -247,6 +253,7 @@ struct plss_ctx {
   // or a wait timeout; every later call on this ctx fails with PLSS_E_NCCL
   bool aborted = false;
   std::vector<void*> dbg_bufs;   // PLSS_DBG_CTA buffers
+  char* slabmajor = nullptr;     // the slab-major CSC when SELL is on and a K2 segment still reads it
   int fault_nccl = 0;            // PLSS_FAULT_NCCL=1 (tests): the first poll reports an error
   double wait_timeout_s = 600.0; // PLSS_WAIT_TIMEOUT_S
   bool peer = false;
@@ -1063,9 +1070,19 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   int32_t *sptr = nullptr, *sidx = nullptr;
   double* sval = nullptr;
   if (S > 1) {
-    sptr = (int32_t*)(w + L.sptr);
-    sidx = (int32_t*)(w + L.sidx);
-    sval = (double*)(w + L.sval);
+    if (L.sell) {
+      // setup-time slab-major CSC (9.5 GB for C5): freed below unless a K2 segment keeps reading it
+      const size_t b_sptr = align_up(4 * (size_t)S * (n + 1)), b_sidx = align_up(4 * (size_t)std::max<int64_t>(nnz, 1));
+      const size_t bytes = b_sptr + b_sidx + 8 * (size_t)std::max<int64_t>(nnz, 1);
+      CK(cudaMalloc((void**)&ctx->slabmajor, bytes));
+      sptr = (int32_t*)ctx->slabmajor;
+      sidx = (int32_t*)(ctx->slabmajor + b_sptr);
+      sval = (double*)(ctx->slabmajor + b_sptr + b_sidx);
+    } else {
+      sptr = (int32_t*)(w + L.sptr);
+      sidx = (int32_t*)(w + L.sidx);
+      sval = (double*)(w + L.sval);
+    }
     int32_t* blk = (int32_t*)(w + L.scan_blk);
     const long long len = n + 1;
     for (int s = 0; s < S; ++s) {
@@ -1158,6 +1175,19 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (dist && L.sell && !ctx->rsag && !ctx->cols) {
     const plss_status st2 = make_chunks(ctx, ctx->seg2[S - 1], pool2, sms, env_int("PLSS_DIST_CHUNKS", 4));
     if (st2 != PLSS_OK) return st2;
+  }
+  // release the setup-time slab-major CSC when no K2 segment reads it after setup: SELL formats read
+  // their own copies; CSR tiles (fmt 0), a thread per column (fmt 5) and the long rows of a globally
+  // sorted segment (k_longrows) read the slab-major arrays
+  if (ctx->slabmajor) {
+    bool keep = false;
+    for (auto& a : ctx->seg2) keep |= a.fmt == 0 || a.fmt == 5 || (a.gsort && a.nlong > 0);
+    if (!keep) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(ctx->slabmajor));
+      ctx->slabmajor = nullptr;
+      for (auto& a : ctx->seg2) { a.ptr = nullptr; a.desc = nullptr; }   // not read by the SELL formats
+    }
   }
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gdots = grid_for((n + NT - 1) / NT + 1, occ_vec, sms);
@@ -2542,6 +2572,7 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->sym) cudaFree(ctx->sym);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* q : ctx->dbg_bufs) cudaFree(q);
+  if (ctx->slabmajor) cudaFree(ctx->slabmajor);
   for (auto& e : ctx->ev_ch) if (e) cudaEventDestroy(e);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
