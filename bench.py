@@ -116,6 +116,29 @@ def _traffic(workload, kernel_class, launches_per_step, capture=None):
     return e["dram_bytes"] * launches_per_step, f"{os.path.relpath(path, ROOT)}: {d['source']}"
 
 
+# The second roofline of the SpMV pair: bytes moved from L2 to the SMs per step (32-byte
+# sectors: a random 8-byte gather moves one) against the highest rate measured for them on this pool's
+# B200s (scripts/gather_l2_bench.cu: random gathers from an L2-resident vector, 10.05 TB/s;
+# profiles/r02_gather_l2_bench.txt). The per-step bytes come from the committed whole-step ncu capture.
+L2_TO_SM_PEAK_GBS = 10050.0
+
+
+def _l2_roofline(workload, step_ms):
+    path = os.path.join(ROOT, "profiles", f"r02_ncu_traffic_{workload.lower()}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    tot = sum(v.get("l2_to_sm_bytes", 0.0) for v in d.get("per_step", {}).values())
+    if tot <= 0:
+        return None
+    ach = tot / (step_ms / 1e3) / 1e9
+    return {"bound": "l2_to_sm_sectors", "achieved": ach, "peak": L2_TO_SM_PEAK_GBS, "unit": "GB/s",
+            "frac": ach / L2_TO_SM_PEAK_GBS, "bytes_per_step": tot,
+            "source": f"{os.path.relpath(path, ROOT)} (l1tex__m_xbar2l1tex_read_bytes, whole step); peak: "
+                      "profiles/r02_gather_l2_bench.txt"}
+
+
 # ---------------------------------------------------------------------------------------------
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------------------------
@@ -596,6 +619,7 @@ def main():
                          "kernel_ms_per_step_profile": dom_prof_ms,
                          "timing": "the timed region's ms per step x the kernel's share of plss_profile"},
             "kernels_ms_per_step": kt,
+            "roofline_l2": _l2_roofline(w["name"], ms / args.steps) if world == 1 and not args.force_dist else None,
             "gpu_launches": args.steps * q["launches_per_step"],
             "e2e": e2e,
             "clocks": clocks,
