@@ -254,6 +254,8 @@ struct plss_ctx {
   bool aborted = false;
   std::vector<void*> dbg_bufs;   // PLSS_DBG_CTA buffers
   char* slabmajor = nullptr;     // the slab-major CSC when SELL is on and a K2 segment still reads it
+  cudaStream_t fork_stream = nullptr;          // k_longrows' concurrent stream (launch_spmv)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int fault_nccl = 0;            // PLSS_FAULT_NCCL=1 (tests): the first poll reports an error
   double wait_timeout_s = 600.0; // PLSS_WAIT_TIMEOUT_S
   bool peer = false;
@@ -317,14 +319,27 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
   else if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
   else if (a.fmt == 3 && a.nlong > 0) {
-    // gsort with long rows: the slices, then k_longrows (one CTA per long row), which publishes its
-    // dot terms in the partial slot after the slices' CTAs and finalizes the segment if it must
+    // gsort with long rows: the slices and k_longrows (one CTA per long row) run concurrently
+    // (k_longrows forked onto a second stream, joined before the next launch): its CTAs fill the SMs
+    // the slices' CTAs free. It publishes its dot terms in the partial slot after the slices' CTAs;
+    // the slices' CTAs and its last CTA elect the finalizing CTA together
     SpmvSeg b = a;
-    b.finalize = 0;
-    k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);                   // gsort: no y staging
+    b.elect_extra = 1;
     SpmvSeg c = a;
     c.partial = a.partial + 2 * (size_t)grid;
-    k_longrows<ROLE><<<a.nlong, NT, 0, st>>>(c);
+    c.elect_total = grid + 1;
+    cudaStream_t st2 = (cudaStream_t)a.fork_stream;
+    if (st2) {
+      cudaEventRecord((cudaEvent_t)a.fork_ev, st);
+      cudaStreamWaitEvent(st2, (cudaEvent_t)a.fork_ev, 0);
+      k_longrows<ROLE><<<a.nlong, NT, 0, st2>>>(c);
+      cudaEventRecord((cudaEvent_t)a.join_ev, st2);
+      k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);                 // gsort: no y staging
+      cudaStreamWaitEvent(st, (cudaEvent_t)a.join_ev, 0);
+    } else {
+      k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);
+      k_longrows<ROLE><<<a.nlong, NT, 0, st>>>(c);
+    }
   }
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort && a.sig == SIGMA_WIDE)
     k_sell<ROLE, 1024, false, true, SIGMA_WIDE><<<grid, 1024, YSTAGE_SMEM_WIDE, st>>>(a);
@@ -547,7 +562,14 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   const int nunits = a.nslices;                      // long rows run in k_longrows (launch_spmv)
   const int NSB = nsb_of(a.sig ? a.sig : SIGMA);     // the k_sell instantiation's block (a.sig)
   const int nblocks = (nunits + NSB - 1) / NSB;
-  const int grid = std::max(1, std::min(std::min(nblocks, sms), MAXG));
+  // a gsort segment's long rows run concurrently in k_longrows (launch_spmv): leave them SMs in
+  // proportion to their share of the entries (PLSS_LSHARE percent of it)
+  int sms_k = sms;
+  if (a.gsort && a.nlong > 0 && a.long_entries > 0) {
+    const double frac = (double)a.long_entries / (double)(a.long_entries + a.short_entries);
+    sms_k = std::max(1, sms - (int)std::lround(sms * frac * env_int("PLSS_LSHARE", 0) / 100.0));
+  }
+  const int grid = std::max(1, std::min(std::min(nblocks, sms_k), MAXG));
   int32_t* cblk = pool.cblk + pool.used_c;
   // CTA balance: a unit costs its stored entries plus a fixed overhead (metadata loads, row
   // outputs, dot partial); sigma-permuted slices also pay the scattered / staged y. Measured best:
@@ -699,7 +721,9 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   }
   sp[nsl] = (int32_t)steps;
   uw[nunits] = (int32_t)stored;
+  a.short_entries = stored;
   for (size_t k = 0; k < lrows.size(); ++k) stored += len[lrows[k]];
+  a.long_entries = stored - a.short_entries;
   if (stored >= (1ll << 31) || pool.used + steps * 32 > pool.cap) return PLSS_OK;
   if ((double)(steps * 32) > 1.15 * (double)nnz_seg + 32.0 * 32 * (LONGROW + 1)) return PLSS_OK;
   int32_t* d_perm = pool.perm + pool.used_slots;
@@ -1175,6 +1199,19 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
   if (dist && L.sell && !ctx->rsag && !ctx->cols) {
     const plss_status st2 = make_chunks(ctx, ctx->seg2[S - 1], pool2, sms, env_int("PLSS_DIST_CHUNKS", 4));
     if (st2 != PLSS_OK) return st2;
+  }
+  // k_longrows' fork / join (launch_spmv): one non-blocking stream and two events per ctx
+  if (env_int("PLSS_FORK", 1)) {
+    bool any = false;
+    for (auto* v : {&ctx->seg1, &ctx->seg2}) for (auto& a : *v) any |= a.fmt == 3 && a.nlong > 0;
+    if (any) {
+      CK(cudaStreamCreateWithFlags(&ctx->fork_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+      for (auto* v : {&ctx->seg1, &ctx->seg2})
+        for (auto& a : *v)
+          if (a.fmt == 3 && a.nlong > 0) { a.fork_stream = ctx->fork_stream; a.fork_ev = ctx->fork_ev; a.join_ev = ctx->join_ev; }
+    }
   }
   // release the setup-time slab-major CSC when no K2 segment reads it after setup: SELL formats read
   // their own copies; CSR tiles (fmt 0), a thread per column (fmt 5) and the long rows of a globally
@@ -2573,6 +2610,9 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* q : ctx->dbg_bufs) cudaFree(q);
   if (ctx->slabmajor) cudaFree(ctx->slabmajor);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  if (ctx->fork_stream) cudaStreamDestroy(ctx->fork_stream);
   for (auto& e : ctx->ev_ch) if (e) cudaEventDestroy(e);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);

@@ -121,6 +121,14 @@ struct SpmvSeg {
   // (2 doubles, reduced in row order by the last CTA) and that CTA's election counter
   double* lrowd;
   unsigned* lcounter;
+  // k_longrows runs concurrently with the segment's slices (launch_spmv forks it onto a second
+  // stream): the slices' CTAs and k_longrows' last CTA (elect_extra = 1 arrival) elect together the
+  // CTA that finalizes; elect_total = the slices' grid + 1
+  int32_t elect_extra, elect_total;
+  long long long_entries, short_entries;   // setup: entries of the long rows / of the slices
+  void* fork_stream;         // host handles (cudaStream_t, cudaEvent_t x 2) for that fork / join
+  void* fork_ev;
+  void* join_ev;
   const int32_t* lbeg;       // k_longrows: entry range [lbeg[2k], lbeg[2k+1]) of long row k (absolute
                              // positions; setup orders the long rows by length, longest first)
   
@@ -230,7 +238,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[MA
 // (a, b) = totals in thread 0.
 __device__ __forceinline__ bool publish_and_elect(double& a, double& b, double* partial,
                                                   const double* part_base, int nparts,
-                                                  unsigned* counter, double (*sm)[MAXW]) {
+                                                  unsigned* counter, double (*sm)[MAXW], int extra = 0) {
   __shared__ int s_last;
   block_sum2(a, b, sm);
   if (threadIdx.x == 0) {
@@ -238,7 +246,7 @@ __device__ __forceinline__ bool publish_and_elect(double& a, double& b, double* 
     partial[2 * blockIdx.x + 1] = b;
     __threadfence();
     unsigned prev = atomicAdd(counter, 1u);
-    s_last = (prev == gridDim.x - 1);
+    s_last = (prev == gridDim.x - 1 + extra);     // extra: arrivals of a concurrent launch (k_longrows)
   }
   __syncthreads();
   if (!s_last) return false;
@@ -952,7 +960,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
     if (tid == 0) { a.partial[2 * blockIdx.x] = acc0; a.partial[2 * blockIdx.x + 1] = acc1; }
     return;
   }
-  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm)) return;
+  if (!publish_and_elect(acc0, acc1, a.partial, a.part_base, a.nparts, a.counter, sm, a.elect_extra)) return;
   if (tid != 0) return;
   if (ROLE == ROLE_K1) {
     if (a.dist) *a.rho_out = acc0;
@@ -1108,14 +1116,21 @@ __global__ void __launch_bounds__(NT) k_longrows(SpmvSeg a) {
   double s0 = 0.0, s1 = 0.0;                                    // row order, fixed shape
   for (int q = tid; q < (int)gridDim.x; q += NT) { s0 += __ldcg(a.lrowd + 2 * q); s1 += __ldcg(a.lrowd + 2 * q + 1); }
   block_sum2(s0, s1, sm);
+  __shared__ int s_fin;
   if (tid == 0) {
     *a.lcounter = 0u;
     a.partial[0] = s0;
     a.partial[1] = s1;
+    s_fin = 0;
+    if (a.finalize) {                                 // one more arrival in the slices' election
+      __threadfence();
+      s_fin = atomicAdd(a.counter, 1u) == (unsigned)(a.elect_total - 1);
+    }
   }
-  if (!a.finalize) return;
-  __threadfence();
   __syncthreads();
+  if (!s_fin) return;
+  __threadfence();
+  if (tid == 0) *a.counter = 0u;
   double t0 = 0.0, t1 = 0.0;
   for (int q = tid; q < a.nparts; q += NT) { t0 += __ldcg(a.part_base + 2 * q); t1 += __ldcg(a.part_base + 2 * q + 1); }
   block_sum2(t0, t1, sm);
