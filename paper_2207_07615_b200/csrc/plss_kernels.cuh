@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
           acc0 += d0; acc1 += d1;
         } else {
           d0 = warp_sum(d0);
-          d1 = warp_sum(d1);
+          if (ROLE == ROLE_K2DOTS) d1 = warp_sum(d1);             // K1 has no second dot (d1 = 0)
           if (lane == 0) { a.slpart[2 * (su + q)] = d0; a.slpart[2 * (su + q) + 1] = d1; }
         }
       }
