@@ -111,9 +111,9 @@ struct SpmvSeg {
                              // segments whose SIGMA windows leave too much padding, C4's columns)
   int32_t wrow0;             // first row of the segment's sigma window 0 (0; a column chunk of a K2
                              // segment, see plss.cu make_chunks, starts at a later window)
-  // Globally length-sorted SELL (power-law rows, fmt 3 only): perm is a global row order, rows
-  // longer than LONGROW are not in the slices but are warp units nslices .. nslices+nlong-1
-  // (row lrows[u - nslices], entries [lptr[row], lptr[row+1]) of the segment's CSR-like arrays).
+  // Globally length-sorted SELL (power-law rows, fmt 3 only): perm is a global row order; the nlong
+  // rows longer than LONGROW are not in the slices but run in k_longrows, one CTA per row (row
+  // lrows[k], entries of the segment's CSR-like arrays lidx / lval)
   int32_t gsort, nlong;
   const int32_t* lrows;
   const int32_t* lptr;
@@ -728,7 +728,8 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 //   slice order (deterministic).
 // Slice metadata (start, length, this lane's row) is loaded one slice ahead, so a slice's stream
 // loads wait for DRAM only, not for an L2 round trip to sptr / perm first.
-// LU: the segment has long-row units (gsort); YS: the K2 segment's y is staged (sigma perm)
+// LU: unused since round 2 (a globally sorted segment's long rows run in k_longrows; must be
+// false); YS: the K2 segment's y is staged (sigma perm)
 template <int ROLE, int BS = NT, bool LU = false, bool YS = false, int SIGT = SIGMA, bool STAT = false,
           int SUK = SU>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
@@ -738,7 +739,8 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
   constexpr int P = DYN && !STAT ? PLSS_PAIR : 1; // slices per warp unit
-  static_assert(!STAT || (DYN && !LU && !YS), "static stepping: fmt 3 segments without perm / long rows");
+  static_assert(!LU, "long rows run in k_longrows");
+  static_assert(!STAT || (DYN && !YS), "static stepping: fmt 3 segments without perm / long rows");
   // fmt 3 K2 with a sigma perm: y results go through a per-sigma-window shared buffer (indexed by
   // row, not slot) and the warp that completes a window writes its SIGMA values coalesced,
   // instead of 32 scattered 8-byte stores per slice. In-flight slices (<= 32 P + P) span at most
@@ -761,7 +763,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   if (!DYN) {
     sl0 = blockIdx.x * (NT / 32); sl1 = a.nslices; stride = gridDim.x * (NT / 32);
   } else {
-    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices + (LU ? a.nlong : 0));
+    sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices);
     stride = P * BS / 32;
     if (tid == 0 && !STAT) s_next = sl0 + P * (BS / 32);   // the first unit of each warp is static
     if (YST && tid < YQ) { s_ycnt[tid] = 0; s_ytag[tid] = -1; }
@@ -773,10 +775,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
   auto meta = [&](int t) {
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      if (LU && t + q < sl1 && t + q >= a.nslices) {   // long-row unit (gsort): whole warp, one row
-        const int r = a.lrows[t + q - a.nslices];
-        m0[q] = a.lptr[r]; m1[q] = a.lptr[r + 1]; mrow[q] = r;
-      } else if (t + q < sl1) {
+      if (t + q < sl1) {
         m0[q] = a.sptr[t + q]; m1[q] = a.sptr[t + q + 1];
         mrow[q] = a.perm ? a.perm[(t + q) * 32 + lane] : (t + q) * 32 + lane;
       } else {
@@ -840,7 +839,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
     }
 #if defined(PLSS_DBGCTA) && PLSS_DBGCTA > 1
     if (DYN && a.ctat && lane == 0)
-      for (int q = 0; q < P; ++q) if (su + q < sl1) { dbg_entries += (LU && su + q >= a.nslices) ? L[q] : 32ull * L[q]; dbg_units++; }
+      for (int q = 0; q < P; ++q) if (su + q < sl1) { dbg_entries += 32ull * L[q]; dbg_units++; }
 #endif
     if (nx < sl1) meta(nx);
     bool valid[P];
@@ -854,29 +853,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
 #endif
       r_old[q] = (ROLE == ROLE_K1 && valid[q]) ? a.out[row[q]] : 0.0;   // issued early
     }
-    const bool longu = LU && DYN && P == 1 && su >= a.nslices;   // warp-uniform
-    if (longu) {
-      // long row (> LONGROW entries): lane-strided partial sums, fixed butterfly, added to the
-      // row's start value (r for K1 is subtracted below; y of earlier slabs for K2)
-      double ps = 0.0;
-      for (int k0 = st0[0]; k0 < st0[0] + L[0]; k0 += 32 * SU) {
-        int32_t c[SU];
-        double v[SU], gv[SU];
-#pragma unroll
-        for (int u = 0; u < SU; ++u) {
-          const int k = k0 + u * 32 + lane;
-          c[u] = -1;
-          if (k < st0[0] + L[0]) { c[u] = ld_stream(a.lidx + k, pol); v[u] = ld_stream(a.lval + k, pol); }
-        }
-#pragma unroll
-        for (int u = 0; u < SU; ++u) gv[u] = sell_gather(a, c[u]);
-#pragma unroll
-        for (int u = 0; u < SU; ++u) if (c[u] >= 0) ps = __dadd_rn(ps, __dmul_rn(v[u], gv[u]));
-      }
-      ps = warp_sum(ps);
-      s[0] = ROLE == ROLE_K1 ? ps : __dadd_rn(s[0], ps);
-      if (lane != 0) valid[0] = false;                    // lane 0 writes the row
-    } else if (P == 1) {
+    if (P == 1) {
       s[0] = sell_row_sum<ROLE, SUK>(a, st0[0], L[0], lane, s[0], pol);
     } else {
       sell_rows_sum<ROLE, P>(a, st0, L, lane, s, pol);
