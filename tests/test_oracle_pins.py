@@ -518,16 +518,18 @@ def test_threaded_oracle_spmv_bitwise(T):
     np.testing.assert_array_equal(v, v1)
 
 
-@pytest.mark.parametrize("name,T", [("C2s", 4), ("C5xs", 8), ("C1", 16)])
-def test_threaded_oracle_tracks_sequential(name, T):
+@pytest.mark.parametrize("name,T,weighted", [("C2s", 4, False), ("C5xs", 8, False), ("C1", 16, False),
+                                             ("C2s", 3, True), ("C5xs", 8, True)])
+def test_threaded_oracle_tracks_sequential(name, T, weighted):
     """Only the dot products' summation order differs: the histories agree to rounding while the
     process is pre-asymptotic, runs with a fixed T are bitwise repeatable, and T
     larger than a vector leaves empty blocks (C1: n = 100 < T * 8)."""
     s = plss_gen.make_config(name)
-    a = oracle.plss_system(s, maxit=30)
+    wi = oracle.column_norms(s.n, s.col_ptr, s.val_t) if weighted else None   # PLSS W: the blocked wdot
+    a = oracle.plss_system(s, maxit=30, wi=wi)
     with oracle.threads(T):
-        b = oracle.plss_system(s, maxit=30)
-        c = oracle.plss_system(s, maxit=30)
+        b = oracle.plss_system(s, maxit=30, wi=wi)
+        c = oracle.plss_system(s, maxit=30, wi=wi)
     np.testing.assert_array_equal(b["rec"], c["rec"])
     k = min(len(a["hist"]), len(b["hist"]), 25)
     assert np.max(np.abs(a["hist"][:k] - b["hist"][:k]) / a["hist"][:k]) <= 1e-12
