@@ -221,29 +221,25 @@ plss_status plss_profile(plss_ctx *ctx, int32_t k, double *ms);
  * window, grid sizes of the first K1 / K2 launch, how many of the 2*slabs SpMV segments use
  * the SELL-32 format (the rest use TMA-staged CSR tiles) and how many of those gather through a
  * shared-memory window of the gathered vector. Any pointer may be NULL. */
+plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t *slabs,
+                       int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2,
+                       int32_t *sell_segments, int32_t *window_segments);
+
 /* The format a ctx chose for K1 (which = 1) or K2 (which = 2) of row slab `slab`:
  * info[0] fmt (0 CSR tiles, 1 SELL-32 grid-stride, 2 SELL-32 + shared-memory window, 3 SELL-32 over
  * per-SM ranges, 5 a thread per short row), info[1] the sigma window of a sigma-permuted SELL segment
  * (512 or 1024; 0 otherwise), info[2] 1 if globally length-sorted, info[3] SELL slices, info[4] long
- * rows (run by k_longrows), info[5] static stepping (1, or 2 with 6 entries in flight), info[6] the
- * grid, info[7] the segment's rows. PLSS_E_INVALID for a bad ctx / which / slab. */
-plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[8]);
+ * rows (run by k_longchunks, or by k_longrows when info[8] = 0), info[5] static stepping (1, or 2
+ * with 6 entries in flight), info[6] the grid, info[7] the segment's rows, info[8] the long rows'
+ * chunks of LCH entries (k_longchunks; 0 without long rows or with PLSS_LCHUNK=0). PLSS_E_INVALID
+ * for a bad ctx / which / slab. */
+plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[9]);
 
 /* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
  * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:
  * out (host, 4 * grid uint64) = {start ns, end ns (%globaltimer), stored entries, units} per CTA
  * of the persistent grid; *grid receives the grid size. PLSS_E_STATE without PLSS_DBG_CTA. */
 plss_status plss_debug_cta_times(plss_ctx *ctx, int32_t which, int32_t slab, uint64_t *out, int32_t *grid);
-
-/* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
- * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:
- * out (host, 4 * grid uint64) = {start ns, end ns (%globaltimer), stored entries, units} per CTA
- * of the persistent grid; *grid receives the grid size. PLSS_E_STATE without PLSS_DBG_CTA. */
-plss_status plss_debug_cta_times(plss_ctx *ctx, int32_t which, int32_t slab, uint64_t *out, int32_t *grid);
-
-plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t *slabs,
-                       int32_t *tile_nnz, int32_t *grid_k1, int32_t *grid_k2,
-                       int32_t *sell_segments, int32_t *window_segments);
 
 /* ---- Randomized projection ("Rand. Proj.", the paper's comparison method) ----
  * eq:pkLong with W = I and a fresh random sketch S_k in R^{m x r} each

@@ -253,6 +253,7 @@ struct plss_ctx {
   // or a wait timeout; every later call on this ctx fails with PLSS_E_NCCL
   bool aborted = false;
   std::vector<void*> dbg_bufs;   // PLSS_DBG_CTA buffers
+  std::vector<void*> chunk_bufs; // k_longchunks' chunk tables, row counters and partials (one per segment)
   char* slabmajor = nullptr;     // the slab-major CSC when SELL is on and a K2 segment still reads it
   cudaStream_t fork_stream = nullptr;          // k_longrows' concurrent stream (launch_spmv)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
@@ -312,6 +313,15 @@ static void set_err(plss_ctx* ctx, const std::string& s) {
   g_last_error = s;
 }
 
+// the long rows of a globally sorted segment: a warp per chunk (k_longchunks), else a CTA per row
+template <int ROLE>
+static void launch_long(const SpmvSeg& c, cudaStream_t st) {
+  if (c.lchunk)
+    k_longchunks<ROLE><<<(c.nchunks + NT / 32 - 1) / (NT / 32), NT, 0, st>>>(c);
+  else
+    k_longrows<ROLE><<<c.nlong, NT, 0, st>>>(c);
+}
+
 template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
   if (a.fmt == 5)
@@ -332,13 +342,13 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
     if (st2) {
       cudaEventRecord((cudaEvent_t)a.fork_ev, st);
       cudaStreamWaitEvent(st2, (cudaEvent_t)a.fork_ev, 0);
-      k_longrows<ROLE><<<a.nlong, NT, 0, st2>>>(c);
+      launch_long<ROLE>(c, st2);
       cudaEventRecord((cudaEvent_t)a.join_ev, st2);
       k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);                 // gsort: no y staging
       cudaStreamWaitEvent(st, (cudaEvent_t)a.join_ev, 0);
     } else {
       k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);
-      k_longrows<ROLE><<<a.nlong, NT, 0, st>>>(c);
+      launch_long<ROLE>(c, st);
     }
   }
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort && a.sig == SIGMA_WIDE)
@@ -757,6 +767,34 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
     CK(cudaMemcpyAsync(d_lbeg, lbeg.data(), 4 * lbeg.size(), cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemcpyAsync(d_uw, uw.data(), 4 * uw.size(), cudaMemcpyHostToDevice, st));
+  // k_longchunks: the long rows in chunks of LCH entries (longest row first, a row's chunks
+  // consecutive), per row its chunk count and a finished-chunk counter, per chunk a partial
+  std::vector<int32_t> lnch(lrows.size());
+  std::vector<int4> chunks;
+  if (!lrows.empty() && env_int("PLSS_LCHUNK", 1)) {
+    for (size_t k = 0; k < lrows.size(); ++k) {
+      const int32_t first = (int32_t)chunks.size();
+      for (int32_t e = lbeg[2 * k]; e < lbeg[2 * k + 1]; e += LCH)
+        chunks.push_back(make_int4(e, std::min(e + LCH, lbeg[2 * k + 1]), (int32_t)k, first));
+      lnch[k] = (int32_t)chunks.size() - first;
+    }
+    const size_t ngroup = (lnch.size() + 31) / 32;
+    const size_t b_ch = align_up(16 * chunks.size()), b_n = align_up(4 * lnch.size()), b_c = align_up(4 * lnch.size()),
+                 b_gc = align_up(4 * ngroup), b_gd = align_up(16 * ngroup);
+    char* buf = nullptr;
+    CK(cudaMalloc((void**)&buf, b_ch + b_n + b_c + b_gc + b_gd + 8 * chunks.size()));
+    ctx->chunk_bufs.push_back(buf);
+    CK(cudaMemcpyAsync(buf, chunks.data(), 16 * chunks.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(buf + b_ch, lnch.data(), 4 * lnch.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(buf + b_ch + b_n, 0, b_c + b_gc, st));     // row and group counters
+    a.lchunk = (const int4*)buf;
+    a.lnch = (const int32_t*)(buf + b_ch);
+    a.lrcnt = (unsigned*)(buf + b_ch + b_n);
+    a.lgcnt = (unsigned*)(buf + b_ch + b_n + b_c);
+    a.lgd = (double*)(buf + b_ch + b_n + b_c + b_gc);
+    a.lcpart = (double*)(buf + b_ch + b_n + b_c + b_gc + b_gd);
+    a.nchunks = (int32_t)chunks.size();
+  }
   int32_t* sidx = pool.idx + pool.used;
   double* sval = pool.val + pool.used;
   if (nsl > 0)
@@ -1225,6 +1263,14 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
       ctx->slabmajor = nullptr;
       for (auto& a : ctx->seg2) { a.ptr = nullptr; a.desc = nullptr; }   // not read by the SELL formats
     }
+  }
+  // One slab on one device: the finalizing sums need only the partial slots the launch writes
+  // (grid, + 1 for a globally sorted segment's long rows); the other slots hold zeros, so the
+  // totals are bitwise the same and the electing CTA (or k_longchunks' warp) reads ~150 pairs
+  // instead of MAXG
+  if (!dist && S == 1) {
+    ctx->seg1[0].nparts = std::min(MAXG, ctx->g1[0] + 1);
+    ctx->seg2[0].nparts = std::min(MAXG, ctx->g2[0] + 1);
   }
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gdots = grid_for((n + NT - 1) / NT + 1, occ_vec, sms);
@@ -1782,7 +1828,7 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   return PLSS_OK;
 }
 
-plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[8]) {
+plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[9]) {
   if (!ctx || !info || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
   const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
   info[0] = a.fmt;
@@ -1793,6 +1839,7 @@ plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab,
   info[5] = a.stat;
   info[6] = which == 1 ? ctx->g1[slab] : ctx->g2[slab];
   info[7] = a.nrows;
+  info[8] = a.lchunk ? a.nchunks : 0;
   return PLSS_OK;
 }
 
@@ -2609,6 +2656,7 @@ void plss_destroy(plss_ctx* ctx) {
   if (ctx->sym) cudaFree(ctx->sym);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* q : ctx->dbg_bufs) cudaFree(q);
+  for (void* q : ctx->chunk_bufs) cudaFree(q);
   if (ctx->slabmajor) cudaFree(ctx->slabmajor);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);

@@ -134,6 +134,19 @@ struct SpmvSeg {
   
   const int32_t* lidx;
   const double* lval;
+  // k_longchunks (the default for long rows): long row k split into chunks of LCH entries, chunk c
+  // = {e0, e1, k, first chunk of row k} (rows longest first, a row's chunks consecutive); a warp
+  // per chunk; lnch[k] chunks of row k; lrcnt[k] its finished chunks (the warp finishing the last
+  // one sums the row's chunk partials lcpart[] in chunk order and resets it); NULL: k_longrows
+  const int4* lchunk;
+  const int32_t* lnch;
+  unsigned* lrcnt;
+  double* lcpart;
+  int32_t nchunks;
+  // row dot terms reduced in two fixed levels: groups of 32 rows (lgcnt[g]: finished rows of group
+  // g; its last finisher sums lrowd over the group into lgd[g]), then the ngroup group sums
+  unsigned* lgcnt;
+  double* lgd;
   const int32_t* uw;         // nunits+1 prefix of stored entries per unit (CTA balance), or NULL
   // L2 cache policies (createpolicy values computed once at setup by k_policies). Passed as kernel
   // parameters they sit in uniform registers: a per-thread createpolicy result costs one R2UR
@@ -232,6 +245,58 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[MA
   __syncthreads();
 }
 
+// The finalizing sum of all partial pairs, in one fixed shape whatever the CTA size (>= FIN_NT
+// threads): thread t < FIN_NT sums pairs t, t + FIN_NT, ... sequentially, each warp butterflies,
+// thread 0 adds the FIN_NT / 32 warp sums in order. A k_sell CTA (1024 threads) and a k_longchunks
+// warp (fin_sum2_warp) reach bitwise the same totals, so it does not matter which one finalizes.
+constexpr int FIN_NT = 256;
+// s0 += base[2q], s1 += base[2q + 1] for q = q0, q0 + step, ... < n in that order (the plain
+// sequential sum), with the loads issued 8 at a time: the serial tails of one warp (k_longchunks)
+// otherwise wait for one L2 round trip per term. Out-of-range terms add +0.0, an exact identity
+// here (a sum started at +0.0 never becomes -0.0 under round-to-nearest).
+__device__ __forceinline__ void seq_add2(const double* base, int q0, int n, int step, double& s0, double& s1) {
+  for (int q = q0; q < n; q += 8 * step) {
+    double x0[8], x1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int qq = q + u * step;
+      x0[u] = qq < n ? __ldcg(base + 2 * qq) : 0.0;
+      x1[u] = qq < n ? __ldcg(base + 2 * qq + 1) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { s0 += x0[u]; s1 += x1[u]; }
+  }
+}
+__device__ __forceinline__ void final_sum2(const double* part_base, int nparts, double& a, double& b,
+                                           double (*sm)[MAXW]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int F = blockDim.x < FIN_NT ? blockDim.x : FIN_NT;
+  double s0 = 0.0, s1 = 0.0;
+  if (threadIdx.x < F) seq_add2(part_base, threadIdx.x, nparts, F, s0, s1);
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  __syncthreads();                                   // sm may still be read by an earlier block_sum2
+  if (lane == 0) { sm[0][warp] = s0; sm[1][warp] = s1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int w = 0; w < F / 32; ++w) { t0 += sm[0][w]; t1 += sm[1][w]; }
+    a = t0; b = t1;
+  }
+}
+// the same shape computed by one warp (every lane returns the totals)
+__device__ __forceinline__ void final_sum2_warp(const double* part_base, int nparts, double& a, double& b) {
+  const int lane = threadIdx.x & 31;
+  double t0 = 0.0, t1 = 0.0;
+  for (int w = 0; w < FIN_NT / 32; ++w) {
+    double s0 = 0.0, s1 = 0.0;
+    seq_add2(part_base, w * 32 + lane, nparts, FIN_NT, s0, s1);
+    t0 += warp_sum(s0);
+    t1 += warp_sum(s1);
+  }
+  a = t0; b = t1;
+}
+
 // Last-CTA election. Every CTA publishes its partial pair; the CTA that arrives last
 // (atomic ticket) sums ALL pairs in index order -- the ticket decides only who sums, never the
 // order, so the result is deterministic. Returns true in every thread of the last CTA, with
@@ -251,13 +316,8 @@ __device__ __forceinline__ bool publish_and_elect(double& a, double& b, double* 
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
-  double s0 = 0.0, s1 = 0.0;
-  for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
-    s0 += __ldcg(part_base + 2 * q);
-    s1 += __ldcg(part_base + 2 * q + 1);
-  }
-  block_sum2(s0, s1, sm);
-  if (threadIdx.x == 0) { a = s0; b = s1; *counter = 0u; }
+  final_sum2(part_base, nparts, a, b, sm);
+  if (threadIdx.x == 0) *counter = 0u;
   return true;
 }
 
@@ -1109,9 +1169,147 @@ __global__ void __launch_bounds__(NT) k_longrows(SpmvSeg a) {
   __threadfence();
   if (tid == 0) *a.counter = 0u;
   double t0 = 0.0, t1 = 0.0;
-  for (int q = tid; q < a.nparts; q += NT) { t0 += __ldcg(a.part_base + 2 * q); t1 += __ldcg(a.part_base + 2 * q + 1); }
-  block_sum2(t0, t1, sm);
+  final_sum2(a.part_base, a.nparts, t0, t1, sm);
   if (tid != 0) return;
+  if (ROLE == ROLE_K1) {
+    if (a.dist) *a.rho_out = t0;
+    else tail_rho(a.ctl, a.rec, t0);
+  } else if (ROLE == ROLE_K2DOTS) {
+    tail_y(a.ctl, a.rec, t0, t1);
+  }
+}
+
+// Long rows of a globally sorted segment in chunks of LCH entries (the default; k_longrows is the
+// CTA-per-row alternative, PLSS_LCHUNK=0): a warp per chunk, LCU entries per lane in flight (one
+// load batch), so short long rows (C4's are 129 .. 4096 entries, ~500 on average) no longer leave
+// most of a 256-thread CTA idle for a whole CTA lifetime (k_longrows: 41 us for C4's 2.7M long-row
+// entries). A chunk's sum: each lane's entries u = 0 .. LCU-1 sequentially, then the warp
+// butterfly; a row's sum: its chunk sums in chunk order, added by the warp that finishes the row's
+// last chunk (a per-row counter decides who, never the order). Row dot terms are reduced in row
+// order by the warp that finishes the last row, then the joint election with the slices' CTAs as in
+// k_longrows (final_sum2_warp: the same shape as the CTAs' final_sum2).
+#ifndef PLSS_LCU
+#define PLSS_LCU 12
+#endif
+constexpr int LCU = PLSS_LCU;
+constexpr int LCH = 32 * LCU;
+template <int ROLE>
+__global__ void __launch_bounds__(NT) k_longchunks(SpmvSeg a) {
+  if (a.ctl != nullptr && a.ctl->done) return;
+  constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
+  const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  if (c >= a.nchunks) return;
+  const uint64_t pol = a.pol_first;
+  const int4 d = a.lchunk[c];                                   // e0, e1, row k, first chunk of k
+  int32_t ci[LCU];
+  double v[LCU], g[LCU];
+#pragma unroll
+  for (int u = 0; u < LCU; ++u) {
+    const int q = d.x + u * 32 + lane;
+    ci[u] = -1;
+    if (q < d.y) { ci[u] = ld_stream(a.lidx + q, pol); v[u] = ld_stream(a.lval + q, pol); }
+  }
+  const int nch = a.lnch[d.z];
+  // the row's output slot and its old value, loaded early in case this warp finishes the row
+  const int r = lane == 0 ? a.lrows[d.z] : 0;
+  double start = 0.0;
+  if (lane == 0 && (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate))) start = a.out[r];
+#pragma unroll
+  for (int u = 0; u < LCU; ++u) g[u] = sell_gather(a, ci[u]);
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < LCU; ++u) if (ci[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], g[u]));
+  s = warp_sum(s);
+  int last = 1;
+  if (nch > 1) {
+    if (lane == 0) {
+      a.lcpart[c] = s;
+      __threadfence();
+      last = atomicAdd(a.lrcnt + d.z, 1u) == (unsigned)(nch - 1);
+    }
+    last = __shfl_sync(FULL, last, 0);
+  }
+  if (!last) return;
+  int fin = 0;
+  if (lane == 0) {
+    double d0 = 0.0, d1 = 0.0;
+    double t = s;
+    if (nch > 1) {                                              // the row's chunk sums in chunk order
+      __threadfence();
+      t = 0.0;
+      for (int j0 = 0; j0 < nch; j0 += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = j0 + u < nch ? __ldcg(a.lcpart + d.w + j0 + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) if (j0 + u < nch) t = __dadd_rn(t, x[u]);
+      }
+      a.lrcnt[d.z] = 0u;
+    }
+    if (ROLE == ROLE_PLAIN) {
+      a.out[r] = t;
+    } else if (ROLE == ROLE_K1) {
+      const double rn = __dsub_rn(start, t);                   // r_i <- r_i - (A p)_i
+      a.out[r] = rn;
+      d0 = rn * rn;
+    } else {
+      a.out[r] = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, r, __dadd_rn(start, t), d0, d1)
+                                     : __dadd_rn(start, t);
+    }
+    if (DOTS) {
+      a.lrowd[2 * d.z] = d0;
+      a.lrowd[2 * d.z + 1] = d1;
+      __threadfence();
+      const int grp = d.z >> 5, gsz = min(32, a.nlong - (grp << 5));
+      fin = atomicAdd(a.lgcnt + grp, 1u) == (unsigned)(gsz - 1);  // this row completes its group
+    }
+  }
+  if (!DOTS) return;
+  fin = __shfl_sync(FULL, fin, 0);
+  if (!fin) return;
+  __threadfence();
+  const int grp = d.z >> 5, ngroup = (a.nlong + 31) >> 5;
+  {                                                             // the group's 32 rows, butterfly
+    const int q = (grp << 5) + lane;
+    double s0 = q < a.nlong ? __ldcg(a.lrowd + 2 * q) : 0.0;
+    double s1 = q < a.nlong ? __ldcg(a.lrowd + 2 * q + 1) : 0.0;
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    fin = 0;
+    if (lane == 0) {
+      a.lgd[2 * grp] = s0;
+      a.lgd[2 * grp + 1] = s1;
+      a.lgcnt[grp] = 0u;
+      __threadfence();
+      fin = atomicAdd(a.lcounter, 1u) == (unsigned)(ngroup - 1);
+    }
+    fin = __shfl_sync(FULL, fin, 0);
+    if (!fin) return;
+    __threadfence();
+  }
+  double s0 = 0.0, s1 = 0.0;                                    // the group sums in group order
+  seq_add2(a.lgd, lane, ngroup, 32, s0, s1);
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  int efin = 0;
+  if (lane == 0) {
+    *a.lcounter = 0u;
+    a.partial[0] = s0;
+    a.partial[1] = s1;
+    if (a.finalize) {                                           // one more arrival in the slices' election
+      __threadfence();
+      efin = atomicAdd(a.counter, 1u) == (unsigned)(a.elect_total - 1);
+    }
+  }
+  efin = __shfl_sync(FULL, efin, 0);
+  if (!efin) return;
+  __threadfence();
+  double t0, t1;
+  final_sum2_warp(a.part_base, a.nparts, t0, t1);
+  if (lane != 0) return;
+  *a.counter = 0u;
   if (ROLE == ROLE_K1) {
     if (a.dist) *a.rho_out = t0;
     else tail_rho(a.ctl, a.rec, t0);

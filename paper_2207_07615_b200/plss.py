@@ -456,27 +456,9 @@ def plss_peer_reduce_emulate(parts, reds, flags, bounds, stream=None):
 
 def plss_query_segment(ctx: Ctx, which: int, slab: int = 0) -> dict:
     """The format chosen for K1 (which = 1) / K2 (which = 2) of a row slab (include/plss.h)."""
-    info = np.zeros(8, dtype=np.int32)
+    info = np.zeros(9, dtype=np.int32)
     _check(load_library().plss_query_segment(ctx.handle, int(which), int(slab), info.ctypes.data), ctx.handle)
-    keys = ("fmt", "sig", "gsort", "nslices", "nlong", "stat", "grid", "rows")
-    return {k: int(v) for k, v in zip(keys, info)}
-
-
-def plss_debug_cta_times(ctx: Ctx, which: int, slab: int = 0):
-    """Diagnostics (PLSS_DBG_CTA=1 at create): per-CTA {start ns, end ns, entries, units} of the
-    last K1 (which = 1) / K2 (which = 2) launch of a slab, as an int64 array [grid, 4]."""
-    out = np.zeros(4 * 2048, dtype=np.uint64)
-    g = ctypes.c_int32(0)
-    _check(load_library().plss_debug_cta_times(ctx.handle, int(which), int(slab), out.ctypes.data, ctypes.byref(g)),
-           ctx.handle)
-    return out[:4 * g.value].reshape(g.value, 4).astype(np.int64)
-
-
-def plss_query_segment(ctx: Ctx, which: int, slab: int = 0) -> dict:
-    """The format chosen for K1 (which = 1) / K2 (which = 2) of a row slab (include/plss.h)."""
-    info = np.zeros(8, dtype=np.int32)
-    _check(load_library().plss_query_segment(ctx.handle, int(which), int(slab), info.ctypes.data), ctx.handle)
-    keys = ("fmt", "sig", "gsort", "nslices", "nlong", "stat", "grid", "rows")
+    keys = ("fmt", "sig", "gsort", "nslices", "nlong", "stat", "grid", "rows", "nchunks")
     return {k: int(v) for k, v in zip(keys, info)}
 
 

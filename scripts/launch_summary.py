@@ -4,7 +4,7 @@ import re
 import sys
 from collections import defaultdict
 
-OURS = re.compile(r"k_(?:spmv|sellw?)<(\d)[^>]*>|k_rp_[a-z]+|k_kz_[a-z]+|k_eg_[a-zT]+|k_pxupdate|k_norm_b|k_dots_tail|k_set_nbd|k_tile_|k_scan_|k_slab_|k_validate")
+OURS = re.compile(r"k_(?:spmv|sellw?|longrows|longchunks|scalar)<(\d)[^>]*>|k_rp_[a-z]+|k_kz_[a-z]+|k_eg_[a-zT]+|k_pxupdate|k_norm_b|k_dots_tail|k_set_nbd|k_tile_|k_scan_|k_slab_|k_validate")
 ROLE = {"0": "k_spmv<plain>", "1": "k1_spmv_csr_resid", "2": "k2_spmv_csc_gather", "3": "k2_spmv_csc_gather+dots"}
 
 

@@ -4,7 +4,7 @@ profiles/*_traffic_*.json (the `roofline.traffic` figure bench.py reports).
     usage: ncu_traffic.py REPORT.ncu-rep STEPS SOURCE-NOTE
 
 A class's launches may be several kernels per step (K1 of a globally sorted segment = k_sell + its
-long rows' k_longrows; K1 / K2 of S row slabs = S launches each): their bytes are summed over the
+long rows' k_longchunks; K1 / K2 of S row slabs = S launches each): their bytes are summed over the
 report and divided by the number of steps captured."""
 import csv
 import json
@@ -12,7 +12,7 @@ import re
 import subprocess
 import sys
 
-KIND = re.compile(r"k_(?:spmv|sellw?|longrows|scalar)<(\d)|k_(pxupdate)|k_rp_(spmm|gen|gram|update)|k_kz_(gemv|resid)")
+KIND = re.compile(r"k_(?:spmv|sellw?|longrows|longchunks|scalar)<(\d)|k_(pxupdate)|k_rp_(spmm|gen|gram|update)|k_kz_(gemv|resid)")
 NAME = {"1": "k1_spmv_csr_resid", "2": "k2_spmv_csc_gather", "3": "k2_spmv_csc_gather", "pxupdate": "k3_pxupdate",
         "spmm": "rp_spmm_AtS", "gen": "rp_sketch_gen", "gram": "rp_gram", "update": "rp_update",
         "gemv": "kz_gemv_history", "resid": "kz_resid"}

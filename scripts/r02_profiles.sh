@@ -3,7 +3,7 @@
 # list of the C5 bench command, and one `ncu --set full` capture of a whole step for C5, C4, C3
 # (each command runs once without ncu first). Outputs under gpurun_out/r02_*.
 set -u
-K='regex:k_sell|k_pxupdate|k_longrows|k_scalar'
+K='regex:k_sell|k_pxupdate|k_longrows|k_longchunks|k_scalar'
 python bench.py > gpurun_out/r02_bench_c5.json 2> gpurun_out/r02_bench_c5.err
 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/r02_bench_c5_reference.json 2>/dev/null
 for w in C4 C3 C4alt; do

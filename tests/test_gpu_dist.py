@@ -230,7 +230,7 @@ def test_dist_column_block_step(pkg, name, slabs, weighted, x0):
                  validate=True)
         if cols:
             S = pkg.plss_query(ctx)["slabs"]
-            extra = sum(1 for w in (1, 2) for sl in range(S)            # k_longrows after a gsort segment
+            extra = sum(1 for w in (1, 2) for sl in range(S)            # k_longchunks beside a gsort segment
                         if pkg.plss_query_segment(ctx, w, sl)["fmt"] == 3 and pkg.plss_query_segment(ctx, w, sl)["nlong"] > 0)
             assert pkg.plss_query(ctx)["launches_per_step"] == 2 * S + 4 + extra
         wi = None

@@ -1,6 +1,6 @@
 """GPU: which format each segment takes (plss_query_segment) and the round-2 formats
 against the oracle: static stepping (C5's K1), globally sorted rows with the long ones in
-k_longrows (C4's K1), a thread per short column (k_scalar, C4's K2), and the 1024-row sigma windows
+k_longchunks (C4's K1; k_longrows with PLSS_LCHUNK=0), a thread per short column (k_scalar, C4's K2), and the 1024-row sigma windows
 of K2 (the SIGMA_WIDE path had no test of its own), each bitwise on its SpMV outputs,
 repeatable, and inside a solve (also on a single-rank chunked distributed ctx)."""
 import os
@@ -94,7 +94,7 @@ def test_c4_formats_longrows_and_scalar(pkg, name):
     k2 = pkg.plss_query_segment(ctx, 2, 0)
     assert k1["fmt"] == 3 and k1["gsort"] == 1 and k1["nlong"] == int((np.diff(s.row_ptr) > 128).sum()) > 0
     assert k2["fmt"] == 5                                   # columns of ~1 entry: a thread per column
-    assert pkg.plss_query(ctx)["launches_per_step"] == 4    # k_sell + k_longrows, k_scalar, K3
+    assert pkg.plss_query(ctx)["launches_per_step"] == 4    # k_sell + k_longchunks, k_scalar, K3
     _spmv_bitwise_repeatable(pkg, ctx, s)
     pkg.plss_destroy(ctx)
 
@@ -154,3 +154,68 @@ def test_query_segment_rejects_bad_arguments(pkg):
         with pytest.raises(pkg.PlssError):
             pkg.plss_query_segment(ctx, which, slab)
     pkg.plss_destroy(ctx)
+
+
+def _long_rows_system(transpose=False, seed=7):
+    """Short rows (1 .. 8 entries) plus 70 long ones (> LONGROW = 128 entries: 129 .. 5000, chunk
+    boundaries of LCH = 384 straddled, 70 = two full groups of 32 rows and a ragged one) in random
+    positions; distinct uniform columns, U(-1, 1) values, b = A x*. transpose: the same matrix
+    transposed, so K2's columns are the long ones."""
+    rng = np.random.default_rng(seed)
+    m, n = 20000, 30000
+    lens = rng.integers(1, 9, size=m)
+    fixed = [129, 130, 383, 384, 385, 767, 768, 769, 1000, 1152, 4096, 5000]
+    extra = rng.integers(129, 3000, size=70 - len(fixed))
+    pos = rng.choice(m, size=70, replace=False)
+    lens[pos] = np.concatenate([fixed, extra])
+    ptr = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    idx = np.concatenate([np.sort(rng.choice(n, size=L, replace=False)) for L in lens])
+    val = rng.uniform(-1, 1, size=ptr[-1])
+    if transpose:
+        import scipy.sparse as sp
+        At = sp.csr_matrix((val, idx, ptr), shape=(m, n)).T.tocsr()
+        At.sort_indices()
+        m, n, ptr, idx, val = n, m, At.indptr, At.indices, At.data
+    xs = rng.standard_normal(n)
+    return plss_gen._finish("longrows" + ("T" if transpose else ""), m, n, ptr, idx, val, xs, 1e-10, 0, 40)
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+def test_long_rows_in_chunks(pkg, transpose):
+    """k_longchunks (a warp per chunk of LCH entries, rows finished by their last chunk's warp, row
+    dot terms in two fixed levels, joint election with the slices' CTAs): K1's long rows (or K2's
+    long columns for the transposed matrix) -- chunk count as set up, SpMV bitwise on short rows and
+    within the tree-sum bound on long ones, repeatable; the solve bitwise the same whether or not
+    k_longchunks runs concurrently with the slices (so whichever launch finalizes, the totals are
+    the same: final_sum2's fixed shape), bitwise repeatable, and against the oracle within the bar."""
+    s = _long_rows_system(transpose)
+    which = 2 if transpose else 1
+    lens = np.diff(s.col_ptr if transpose else s.row_ptr)
+    ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+    seg = pkg.plss_query_segment(ctx, which, 0)
+    L = lens[lens > 128]
+    assert seg["fmt"] == 3 and seg["gsort"] == 1 and seg["nlong"] == len(L) == 70, seg
+    assert seg["nchunks"] == int(np.sum((L + 383) // 384)), seg
+    _spmv_bitwise_repeatable(pkg, ctx, s)
+    b = torch.from_numpy(s.b).cuda()
+    runs = [pkg.plss_solve(ctx, b, tol=s.tol, maxit=40) for _ in range(2)]
+    pkg.plss_destroy(ctx)
+    with _env(PLSS_FORK=0):
+        ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+    runs.append(pkg.plss_solve(ctx, b, tol=s.tol, maxit=40))
+    pkg.plss_destroy(ctx)
+    for r in runs[1:]:
+        assert r["iters"] == runs[0]["iters"]
+        np.testing.assert_array_equal(r["hist"], runs[0]["hist"])
+        np.testing.assert_array_equal(r["x"].cpu().numpy(), runs[0]["x"].cpu().numpy())
+    with _env(PLSS_LCHUNK=0):                                  # the CTA-per-row k_longrows
+        ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+    assert pkg.plss_query_segment(ctx, which, 0)["nchunks"] == 0
+    _spmv_bitwise_repeatable(pkg, ctx, s)
+    rows = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
+    pkg.plss_destroy(ctx)
+    ref = oracle.plss_system(s, maxit=40)
+    k = min(20, len(ref["hist"]) - 1)
+    for res in (runs[0], rows):
+        assert np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
