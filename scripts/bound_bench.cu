@@ -283,6 +283,44 @@ __global__ void __launch_bounds__(1024, 1) k1x(const int32_t* __restrict__ idx, 
   }
   if (acc == 1234.5) r[0] = acc;
 }
+
+// 24-bit column indices (round 3 question: do fewer stream bytes per entry move the L2 -> SM bound?):
+// the low 16 bits of every index in a u16 SELL array and the high 8 bits in a u8 SELL array
+// (3 bytes per entry instead of 4: 96 instead of 128 bytes per warp step).
+__global__ void split_idx24(const int32_t* idx, uint16_t* lo, uint8_t* hi, long long n) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) { lo[t] = (uint16_t)(idx[t] & 0xFFFF); hi[t] = (uint8_t)(idx[t] >> 16); }
+}
+template <int SU>
+__global__ void __launch_bounds__(1024, 1) k1c(const uint16_t* __restrict__ lo, const uint8_t* __restrict__ hi,
+                                              const double* __restrict__ val, const double* __restrict__ p,
+                                              double* __restrict__ r, int nslices) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = (int)((long long)nslices * blockIdx.x / gridDim.x), s1 = (int)((long long)nslices * (blockIdx.x + 1) / gridDim.x);
+  for (int s = s0 + warp; s < s1; s += 32) {
+    const long long row = (long long)s * 32 + lane;
+    const double rold = r[row];
+    double sum = 0.0;
+    const long long b = (long long)s * L * 32 + lane;
+#pragma unroll
+    for (int j0 = 0; j0 < L; j0 += SU) {
+      int32_t c[SU]; double v[SU], g[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        unsigned a, h;
+        asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=r"(a) : "l"(lo + b + (j0 + u) * 32));
+        asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=r"(h) : "l"(hi + b + (j0 + u) * 32));
+        c[u] = (int32_t)(a | (h << 16));
+        v[u] = lds_stream(val + b + (j0 + u) * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) g[u] = __ldg(p + c[u]);
+#pragma unroll
+      for (int u = 0; u < SU; ++u) sum = __dadd_rn(sum, __dmul_rn(v[u], g[u]));
+    }
+    r[row] = rold - sum;
+  }
+}
 __global__ void fill_sptr(int32_t* sptr, int n) { int i = blockIdx.x * blockDim.x + threadIdx.x; if (i <= n) sptr[i] = i * L; }
 
 
@@ -550,6 +588,20 @@ int main() {
     return timeit([&] { kern<<<grid, bs, smem>>>(idx, val, p, r, nsl, chunk); });
   };
   printf("== K1 slab: %d rows x %d entries (6 band + 6 uniform), SELL-32\n", RS, L);
+  if (getenv("BB_IDX24")) {
+    uint16_t* lo; uint8_t* hi;
+    CK(cudaMalloc(&lo, nnz * 2)); CK(cudaMalloc(&hi, nnz));
+    split_idx24<<<(unsigned)((nnz + 255) / 256), 256>>>(idx, lo, hi, nnz);
+    CK(cudaDeviceSynchronize());
+    for (int rep_ = 0; rep_ < 3; ++rep_) {
+      rep("K1 plain 32-bit idx (SU 6)", K1(k1<0, 1024, 6>, 1024, sms, 0, 0), k1_bytes, nnz);
+      rep("K1 24-bit idx u16+u8 (SU 6)", timeit([&] { k1c<6><<<sms, 1024>>>(lo, hi, val, p, r, nsl); }), k1_bytes, nnz);
+      rep("K1 24-bit idx u16+u8 (SU 12)", timeit([&] { k1c<12><<<sms, 1024>>>(lo, hi, val, p, r, nsl); }), k1_bytes, nnz);
+      rep("K1 no gathers (SU 6)", K1(k1<3, 1024, 6>, 1024, sms, 0, 0), k1_bytes, 0);
+    }
+    CK(cudaFree(lo)); CK(cudaFree(hi));
+    if (getenv("BB_ONLY")) return 0;
+  }
   rep("K1 full (1024 x 1/SM, SU 6)", K1(k1<0, 1024, 6>, 1024, sms, 0, 0), k1_bytes, nnz);
   rep("K1 full (1024 x 1/SM, SU 12)", K1(k1<0, 1024, 12>, 1024, sms, 0, 0), k1_bytes, nnz);
   rep("K1 full (512 x 2/SM, SU 6)", K1(k1<0, 512, 6>, 512, 2 * sms, 0, 0), k1_bytes, nnz);
