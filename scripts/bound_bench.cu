@@ -321,6 +321,74 @@ __global__ void __launch_bounds__(1024, 1) k1c(const uint16_t* __restrict__ lo, 
     r[row] = rold - sum;
   }
 }
+
+// CTA-level TMA staging of the streams (round 3 question: do bulk copies, which do not go through
+// the LSU / L1 request path, leave more of the SM's L2 request throughput to the gathers?). Each
+// CTA's slice range is contiguous in the SELL arrays; one producer thread streams it in stages of
+// SPS slices (idx and val blocks, two bulk copies per stage) into an NST-stage ring; consumer warp
+// w takes slice w of each stage, reads its 12 indices and values from shared memory into
+// registers, releases the stage, then issues its 12 gathers.
+template <int NWC, int NST, int SUB>
+__global__ void __launch_bounds__((NWC + 1) * 32, 1) k1t(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                        const double* __restrict__ p, double* __restrict__ r, int nslices,
+                                                        uint64_t pol) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int SPS = NWC;
+  constexpr int IB = SPS * L * 32 * 4, VB = SPS * L * 32 * 8, SB = IB + VB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + NST * SB);
+  uint64_t* empty = full + NST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = (int)((long long)nslices * blockIdx.x / gridDim.x), s1 = (int)((long long)nslices * (blockIdx.x + 1) / gridDim.x);
+  const int nst = (s1 - s0 + SPS - 1) / SPS;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NST; ++k) { plss::mbar_init(&full[k], 1); plss::mbar_init(&empty[k], NWC); }
+    plss::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == NWC) {
+    if (lane == 0) {
+      for (int t = 0; t < nst; ++t) {
+        const int k = t % NST;
+        if (t >= NST) plss::mbar_wait(&empty[k], ((t / NST) - 1) & 1);
+        const int sa = s0 + t * SPS, sb = min(s1, sa + SPS);
+        const unsigned ib = (unsigned)(sb - sa) * L * 32 * 4, vb = (unsigned)(sb - sa) * L * 32 * 8;
+        plss::mbar_expect_tx(&full[k], ib + vb);
+        plss::tma_load(smraw + k * SB, idx + (long long)sa * L * 32, ib, &full[k], pol);
+        plss::tma_load(smraw + k * SB + IB, val + (long long)sa * L * 32, vb, &full[k], pol);
+      }
+    }
+    return;
+  }
+  for (int t = 0; t < nst; ++t) {
+    const int k = t % NST;
+    const int s = s0 + t * SPS + warp;
+    const long long row = (long long)s * 32 + lane;
+    double rold = 0.0;
+    if (s < s1) rold = r[row];
+    plss::mbar_wait(&full[k], (t / NST) & 1);
+    int32_t c[L]; double v[L];
+    if (s < s1) {
+      const int32_t* ip = reinterpret_cast<const int32_t*>(smraw + k * SB) + warp * L * 32 + lane;
+      const double* vp = reinterpret_cast<const double*>(smraw + k * SB + IB) + warp * L * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < L; ++j) { c[j] = ip[j * 32]; v[j] = vp[j * 32]; }
+    }
+    __syncwarp();
+    if (lane == 0) plss::mbar_arrive(&empty[k]);
+    if (s < s1) {
+      double sum = 0.0;
+#pragma unroll
+      for (int j0 = 0; j0 < L; j0 += SUB) {
+        double g[SUB];
+#pragma unroll
+        for (int u = 0; u < SUB; ++u) g[u] = __ldg(p + c[j0 + u]);
+#pragma unroll
+        for (int u = 0; u < SUB; ++u) sum = __dadd_rn(sum, __dmul_rn(v[j0 + u], g[u]));
+      }
+      r[row] = rold - sum;
+    }
+  }
+}
 __global__ void fill_sptr(int32_t* sptr, int n) { int i = blockIdx.x * blockDim.x + threadIdx.x; if (i <= n) sptr[i] = i * L; }
 
 
@@ -588,6 +656,33 @@ int main() {
     return timeit([&] { kern<<<grid, bs, smem>>>(idx, val, p, r, nsl, chunk); });
   };
   printf("== K1 slab: %d rows x %d entries (6 band + 6 uniform), SELL-32\n", RS, L);
+  if (getenv("BB_TMA")) {
+    uint64_t pol_first;
+    {
+      uint64_t* d_pol; CK(cudaMalloc(&d_pol, 16));
+      plss::k_policies<<<1, 1>>>(d_pol);
+      uint64_t pols[2]; CK(cudaMemcpy(pols, d_pol, 16, cudaMemcpyDeviceToHost));
+      pol_first = pols[0];
+    }
+    auto T = [&](auto kern, int nwc, int nst, const char* nm) {
+      const int smem = nst * nwc * L * 32 * 12 + 2 * nst * 8;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      rep(nm, timeit([&] { kern<<<sms, (nwc + 1) * 32, smem>>>(idx, val, p, r, nsl, pol_first); }), k1_bytes, nnz);
+      CK(cudaGetLastError());
+    };
+    for (int rep_ = 0; rep_ < 2; ++rep_) {
+      rep("K1 plain 32-bit idx (SU 6)", K1(k1<0, 1024, 6>, 1024, sms, 0, 0), k1_bytes, nnz);
+      T(k1t<8, 2, 12>, 8, 2, "K1 TMA streams 8 warps x 2 stages (36 KB), 12 gathers");
+      T(k1t<8, 3, 12>, 8, 3, "K1 TMA streams 8 warps x 3 stages (36 KB), 12 gathers");
+      T(k1t<4, 2, 12>, 4, 2, "K1 TMA streams 4 warps x 2 stages (18 KB), 12 gathers");
+      T(k1t<4, 4, 12>, 4, 4, "K1 TMA streams 4 warps x 4 stages (18 KB), 12 gathers");
+      T(k1t<2, 4, 12>, 2, 4, "K1 TMA streams 2 warps x 4 stages (9 KB), 12 gathers");
+      T(k1t<8, 4, 12>, 8, 4, "K1 TMA streams 8 warps x 4 stages (36 KB), 12 gathers");
+      T(k1t<16, 2, 12>, 16, 2, "K1 TMA streams 16 warps x 2 stages (72 KB), 12 gathers");
+      T(k1t<4, 8, 12>, 4, 8, "K1 TMA streams 4 warps x 8 stages (18 KB), 12 gathers");
+    }
+    if (getenv("BB_ONLY")) return 0;
+  }
   if (getenv("BB_IDX24")) {
     uint16_t* lo; uint8_t* hi;
     CK(cudaMalloc(&lo, nnz * 2)); CK(cudaMalloc(&hi, nnz));
