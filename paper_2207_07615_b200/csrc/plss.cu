@@ -344,13 +344,15 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
       cudaStreamWaitEvent(st2, (cudaEvent_t)a.fork_ev, 0);
       launch_long<ROLE>(c, st2);
       cudaEventRecord((cudaEvent_t)a.join_ev, st2);
-      k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);                 // gsort: no y staging
+      k_sell<ROLE, 1024, false, false, SIGMA, false, SU, GS_NSB><<<grid, 1024, 0, st>>>(b);   // gsort: no y staging
       cudaStreamWaitEvent(st, (cudaEvent_t)a.join_ev, 0);
     } else {
-      k_sell<ROLE, 1024><<<grid, 1024, 0, st>>>(b);
+      k_sell<ROLE, 1024, false, false, SIGMA, false, SU, GS_NSB><<<grid, 1024, 0, st>>>(b);
       launch_long<ROLE>(c, st);
     }
   }
+  else if (a.fmt == 3 && a.gsort)
+    k_sell<ROLE, 1024, false, false, SIGMA, false, SU, GS_NSB><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort && a.sig == SIGMA_WIDE)
     k_sell<ROLE, 1024, false, true, SIGMA_WIDE><<<grid, 1024, YSTAGE_SMEM_WIDE, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort)     // K2 with a sigma perm: staged y
@@ -570,7 +572,7 @@ static int env_int(const char* name, int dflt) {
 static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sms, int* grid_out) {
   if (a.fmt != 1) return PLSS_OK;
   const int nunits = a.nslices;                      // long rows run in k_longrows (launch_spmv)
-  const int NSB = nsb_of(a.sig ? a.sig : SIGMA);     // the k_sell instantiation's block (a.sig)
+  const int NSB = a.gsort ? GS_NSB : nsb_of(a.sig ? a.sig : SIGMA);   // the k_sell instantiation's block
   const int nblocks = (nunits + NSB - 1) / NSB;
   // a gsort segment's long rows run concurrently in k_longrows (launch_spmv): leave them SMs in
   // proportion to their share of the entries (PLSS_LSHARE percent of it)
@@ -583,10 +585,12 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   int32_t* cblk = pool.cblk + pool.used_c;
   // CTA balance: a unit costs its stored entries plus a fixed overhead (metadata loads, row
   // outputs, dot partial); sigma-permuted slices also pay the scattered / staged y. Measured best:
-  // 256 for sigma-permuted ones (C5 K2 +3%), 32 for globally sorted ones (C4's K1 0.160 -> 0.123 ms:
-  // the CTAs of long rows were the stragglers, scripts/cta_balance.py), 128 otherwise.
+  // 256 for sigma-permuted ones (C5 K2 +3%), 48 for globally sorted ones at single-slice
+  // granularity (GS_NSB; 32 with blocks of 16: C4's K1 0.160 -> 0.123 ms when the CTAs of long
+  // rows were the stragglers, scripts/cta_balance.py; 48 vs 32 since k_longchunks: C4 0.2303 ->
+  // 0.2274, C4-alt 0.3910 -> 0.3834 ms per step), 128 otherwise.
   const int uc = (a.perm && !a.gsort) ? env_int("PLSS_UC_SIG", 256)
-                 : a.gsort ? env_int("PLSS_UC_GS", 32) : env_int("PLSS_UC", 128);
+                 : a.gsort ? env_int("PLSS_UC_GS", 48) : env_int("PLSS_UC", 128);
   if (a.uw)
     k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk, uc);
   else

@@ -692,6 +692,13 @@ constexpr int YSTAGE_SMEM = YQ * SIGMA * 8;
 constexpr int SIGMA_WIDE = 2 * SIGMA;    // the wider window a K2 segment may take (a.sig)
 constexpr int YSTAGE_SMEM_WIDE = YQ * SIGMA_WIDE * 8;
 __host__ __device__ constexpr int nsb_of(int sig) { return sig / 32 > 16 ? sig / 32 : 16; }
+// CTA-range granularity of globally length-sorted segments (no sigma windows to align to): their
+// longest slices hold up to 32 * LONGROW entries each, so blocks of 16 of them overshot a CTA's
+// share (C4-alt's first CTA held two such blocks, 128K entries against a 59K median)
+#ifndef PLSS_GS_NSB
+#define PLSS_GS_NSB 1
+#endif
+constexpr int GS_NSB = PLSS_GS_NSB;
 constexpr int YD = 1024;
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
@@ -791,10 +798,10 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 // LU: unused since round 2 (a globally sorted segment's long rows run in k_longrows; must be
 // false); YS: the K2 segment's y is staged (sigma perm)
 template <int ROLE, int BS = NT, bool LU = false, bool YS = false, int SIGT = SIGMA, bool STAT = false,
-          int SUK = SU>
+          int SUK = SU, int GNSB = 0>
 __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
   constexpr int SPW = SIGT / 32;                 // this instantiation's sigma window (a.sig)
-  constexpr int NSB = nsb_of(SIGT);
+  constexpr int NSB = GNSB ? GNSB : nsb_of(SIGT); // CTA-range granularity (slices)
   constexpr int SIGMA = SIGT;
   constexpr bool DYN = BS != NT;
   constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
