@@ -245,6 +245,15 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double (*sm)[MA
   __syncthreads();
 }
 
+// Streaming vector kernels (K3, the norms): at least 6 CTAs of NT threads per SM (<= 40 registers,
+// no spills). Their finalizing sum (final_sum2's 8 loads in flight) otherwise raised k_pxupdate to
+// 62 registers and 4 CTAs per SM (C4's K3 0.056 -> 0.065 ms); the dots kernels of the distributed
+// steps would spill ~100 bytes under the bound and keep their own.
+#ifndef PLSS_VEC_MINB
+#define PLSS_VEC_MINB 6
+#endif
+constexpr int VEC_MINB = PLSS_VEC_MINB;
+
 // The finalizing sum of all partial pairs, in one fixed shape whatever the CTA size (>= FIN_NT
 // threads): thread t < FIN_NT sums pairs t, t + FIN_NT, ... sequentially, each warp butterflies,
 // thread 0 adds the FIN_NT / 32 warp sums in order. A k_sell CTA (1024 threads) and a k_longchunks
@@ -1774,7 +1783,7 @@ __global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double
 // ---------------------------------------------------------------------------------------------
 // theta_out != NULL (the reduce-scatter distributed step, K3 on this rank's column shard): the
 // shard's p^T p goes there (summed across ranks with the next step's scalars) instead of c->theta
-__global__ void __launch_bounds__(NT) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
+__global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
                                                  double* __restrict__ x, long long n, Ctl* c,
                                                  double* rec, double* partial, unsigned* counter,
                                                  const double* __restrict__ wi, double* theta_out = nullptr) {
@@ -1882,7 +1891,7 @@ __global__ void k_tail_rsag(Ctl* c, double* rec, const double* scal) {
 // r is replicated and was just all-reduced (r <- r - sum_g A_g p_g, with r[m] = sum_g theta_g of the
 // previous K3); rho = r^T r (every rank the same fixed-order sum of the same bytes), theta, the
 // stop test and the rho tail
-__global__ void __launch_bounds__(NT) k_rho_tail(const double* __restrict__ r, long long m, Ctl* c,
+__global__ void __launch_bounds__(NT, VEC_MINB) k_rho_tail(const double* __restrict__ r, long long m, Ctl* c,
                                                  double* rec, double* partial, unsigned* counter) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
@@ -1956,7 +1965,7 @@ __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const 
 }
 
 // ||b||^2 (or the local share of it) into ctl->nb2; non-dist also sets nbd.
-__global__ void __launch_bounds__(NT) k_norm_b(const double* __restrict__ r, long long m, Ctl* c,
+__global__ void __launch_bounds__(NT, VEC_MINB) k_norm_b(const double* __restrict__ r, long long m, Ctl* c,
                                                double* partial, unsigned* counter, int set_nbd,
                                                double* out) {
   __shared__ double sm[2][MAXW];
