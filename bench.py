@@ -558,7 +558,9 @@ def main():
     pkg.plss_step(ctx, 3)
     kt = pkg.plss_profile(ctx, max(1, args.profile_steps))
     k1_bytes = 12 * nnz_l + 4 * (m_l + 1) + 8 * n + 16 * m_l
-    k2_bytes = 12 * nnz_l + 4 * (n + 1) + 8 * m_l + 16 * n
+    # K2 writes y (8n); it reads p (8n) for psi only where K3 does not sum it (R25)
+    psi3 = pkg.plss_query_segment(ctx, 2, q["slabs"] - 1)["psi3"] and not args.plss_w
+    k2_bytes = 12 * nnz_l + 4 * (n + 1) + 8 * m_l + (8 if psi3 else 16) * n
     k3_bytes = 40 * n
     classes = {"k1_spmv_csr_resid": (kt["k1"], k1_bytes), "k2_spmv_csc_gather": (kt["k2"], k2_bytes),
                "k3_pxupdate": (kt["k3"], k3_bytes)}
@@ -605,7 +607,7 @@ def main():
                        "rhs": ("paper: x = ones, x(1) = 10, b = A x (P:L987)" if args.rhs == "paper"
                                else "b = A x*, x* ~ N(0,1)"),
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
-                       "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8",
+                       "bytes_per_step_model": "24 nnz + 28 m + 60 n + 8 (DESIGN.md R25)",
                        "workspace_gb": round(ctx.workspace.numel() / 1e9, 3),
                        "matrix_gb": round(sum(t.numel() * t.element_size() for t in (
                            w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])) / 1e9, 3)},

@@ -481,7 +481,7 @@ static plss_status enqueue_step(plss_ctx* ctx) {
                                            ctx->part2, ctx->counters + 1, ctx->wi);
   }
   k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
-                                     ctx->counters + 2, ctx->wi);
+                                     ctx->counters + 2, ctx->wi, nullptr, ctx->seg2[ctx->S - 1].psi3);
   CK(cudaGetLastError());
   return PLSS_OK;
 }
@@ -1191,6 +1191,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     a.nparts = MAXG;
     a.accumulate = (s > 0);
     a.finalize = (!dist && s == S - 1);
+    a.psi3 = (a.finalize && env_int("PLSS_PSI3", 1)) ? 1 : 0;   // psi summed by K3 (k2_final)
     a.counter = ctx->counters + 1;
     a.ctl = ctx->ctl;
     a.rec = ctx->rec;
@@ -1774,7 +1775,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       CK(cudaEventRecord(ev[q++], st));
     }
     k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
-                                       ctx->counters + 2, ctx->wi);
+                                       ctx->counters + 2, ctx->wi, nullptr, ctx->seg2[ctx->S - 1].psi3);
     CK(cudaEventRecord(ev[q++], st));
     }
     CK(cudaGetLastError());
@@ -1832,7 +1833,7 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   return PLSS_OK;
 }
 
-plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[9]) {
+plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[10]) {
   if (!ctx || !info || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
   const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
   info[0] = a.fmt;
@@ -1844,6 +1845,7 @@ plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab,
   info[6] = which == 1 ? ctx->g1[slab] : ctx->g2[slab];
   info[7] = a.nrows;
   info[8] = a.lchunk ? a.nchunks : 0;
+  info[9] = a.psi3;
   return PLSS_OK;
 }
 

@@ -125,6 +125,7 @@ struct SpmvSeg {
   // stream): the slices' CTAs and k_longrows' last CTA (elect_extra = 1 arrival) elect together the
   // CTA that finalizes; elect_total = the slices' grid + 1
   int32_t elect_extra, elect_total;
+  int32_t psi3;              // K2's finalizing segment on one device: psi left to K3 (k2_final)
   long long long_entries, short_entries;   // setup: entries of the long rows / of the slices
   void* fork_stream;         // host handles (cudaStream_t, cudaEvent_t x 2) for that fork / join
   void* fork_ev;
@@ -209,16 +210,18 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
 
 // K2's last slab (phi, psi): y_j = s gives phi's term y_j WIy_j and psi's y_j p_j; returns what K3
 // consumes, WIy_j = y_j / wi_j under PLSS W (WI \\ y applied element-wise, L805, L819-821), else y_j.
-__device__ __forceinline__ double k2_final(const double* wi, bool wtd, const double* pv, long long row, double s,
-                                           double& d0, double& d1) {
+// psi3 (one device, WI = I): psi is summed by K3, which reads y and p_{k-1} coalesced anyway, so K2
+// reads no p (C5's last slab: scattered per sigma window; C4's columns: 64 MB)
+__device__ __forceinline__ double k2_final(const SpmvSeg& a, bool wtd, long long row, double s, double& d0,
+                                           double& d1) {
   if (wtd) {
-    const double wy = __ddiv_rn(s, wi[row]);
+    const double wy = __ddiv_rn(s, a.wi[row]);
     d0 = s * wy;
-    d1 = s * pv[row];
+    d1 = s * a.pv[row];
     return wy;
   }
   d0 = s * s;
-  d1 = s * pv[row];
+  d1 = a.psi3 ? 0.0 : s * a.pv[row];
   return s;
 }
 
@@ -637,7 +640,7 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv(SpmvSeg a) {
           acc0 = fma(rn, rn, acc0);
         } else if (ROLE == ROLE_K2DOTS) {
           double d0, d1;
-          a.out[i] = k2_final(a.wi, wtd, a.pv, i, s, d0, d1);  // y_j (WIy_j under PLSS W)
+          a.out[i] = k2_final(a, wtd, i, s, d0, d1);  // y_j (WIy_j under PLSS W)
           acc0 += d0;
           acc1 += d1;
         } else {
@@ -950,7 +953,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a
           if (s[q] == 1234.5) a.out[row[q]] = s[q];             // ablation: no y write
 #else
           // y_j, or under PLSS W in the last slab WIy_j (what K3 consumes)
-          const double yv = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, row[q], s[q], d0, d1) : s[q];
+          const double yv = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, row[q], s[q], d0, d1) : s[q];
           if (stage) s_y[((su + q) / SPW) % YQ][row[q] % SIGMA] = yv;  // staged
           else a.out[row[q]] = yv;
 #endif
@@ -1078,7 +1081,7 @@ __global__ void __launch_bounds__(NT, PLSS_SCMINB) k_scalar(SpmvSeg a) {
       a.out[i] = rn;
       d0 = rn * rn;
     } else {
-      a.out[i] = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, i, s, d0, d1) : s;
+      a.out[i] = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, i, s, d0, d1) : s;
     }
     if (DOTS) { acc0 += d0; acc1 += d1; }
   }
@@ -1151,7 +1154,7 @@ __global__ void __launch_bounds__(NT) k_longrows(SpmvSeg a) {
       a.out[r] = rn;
       d0 = rn * rn;
     } else {
-      const double yv = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, r, __dadd_rn(start, t), d0, d1)
+      const double yv = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, r, __dadd_rn(start, t), d0, d1)
                                             : __dadd_rn(start, t);
       a.out[r] = yv;
     }
@@ -1271,7 +1274,7 @@ __global__ void __launch_bounds__(NT) k_longchunks(SpmvSeg a) {
       a.out[r] = rn;
       d0 = rn * rn;
     } else {
-      a.out[r] = ROLE == ROLE_K2DOTS ? k2_final(a.wi, wtd, a.pv, r, __dadd_rn(start, t), d0, d1)
+      a.out[r] = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, r, __dadd_rn(start, t), d0, d1)
                                      : __dadd_rn(start, t);
     }
     if (DOTS) {
@@ -1534,7 +1537,7 @@ __global__ void __launch_bounds__(NTW, 1) k_sellw(SpmvSeg a) {
           a.out[row] = rn;
           d0 = rn * rn;
         } else if (ROLE == ROLE_K2DOTS) {
-          a.out[row] = k2_final(a.wi, wtd, a.pv, row, s, d0, d1);   // y_j (WIy_j under PLSS W)
+          a.out[row] = k2_final(a, wtd, row, s, d0, d1);   // y_j (WIy_j under PLSS W)
         } else {
           a.out[row] = s;                                       // y_j
         }
@@ -1786,14 +1789,17 @@ __global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double
 __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
                                                  double* __restrict__ x, long long n, Ctl* c,
                                                  double* rec, double* partial, unsigned* counter,
-                                                 const double* __restrict__ wi, double* theta_out = nullptr) {
+                                                 const double* __restrict__ wi, double* theta_out = nullptr,
+                                                 int psi_here = 0) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
   const bool wtd = wi != nullptr && c->weighted;       // theta = p^T (WI p) under PLSS W (L812)
   const int k = c->iters;
   const bool init = (k == 0);
   const double beta = c->beta, gamma = c->gamma;
-  double acc = 0.0, dummy = 0.0;
+  // psi = y_k^T p_{k-1} (L806, diagnostic) summed here when K2 left it (SpmvSeg::psi3, WI = I)
+  const bool psi = psi_here && !wtd && !init;
+  double acc = 0.0, acc1 = 0.0;
   const long long n2 = n >> 1;
   const long long stride = (long long)gridDim.x * NT;
   double2* p2 = reinterpret_cast<double2*>(p);
@@ -1809,6 +1815,10 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
       const double2 po = p2[i];
       pp.x = __dadd_rn(__dmul_rn(beta, po.x), __dmul_rn(gamma, yy.x));
       pp.y = __dadd_rn(__dmul_rn(beta, po.y), __dmul_rn(gamma, yy.y));
+      if (psi) {
+        acc1 = fma(yy.x, po.x, acc1);
+        acc1 = fma(yy.y, po.y, acc1);
+      }
     }
     p2[i] = pp;
     double2 xx = __ldcs(x2 + i);
@@ -1826,13 +1836,18 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const long long i = n - 1;
+    if (psi) acc1 = fma(y[i], p[i], acc1);
     const double pp = init ? __dmul_rn(gamma, y[i]) : __dadd_rn(__dmul_rn(beta, p[i]), __dmul_rn(gamma, y[i]));
     p[i] = pp;
     x[i] = __dadd_rn(x[i], pp);
     acc = fma(pp, wtd ? wi[i] * pp : pp, acc);
   }
-  if (!publish_and_elect(acc, dummy, partial, partial, gridDim.x, counter, sm)) return;
+  if (!publish_and_elect(acc, acc1, partial, partial, gridDim.x, counter, sm)) return;
   if (threadIdx.x != 0) return;
+  if (psi) {
+    c->psi = acc1;
+    rec[(size_t)k * REC + 3] = acc1;
+  }
   if (theta_out) {
     *theta_out = acc;                                           // shard partial of theta
   } else {

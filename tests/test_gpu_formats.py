@@ -219,3 +219,39 @@ def test_long_rows_in_chunks(pkg, transpose):
     k = min(20, len(ref["hist"]) - 1)
     for res in (runs[0], rows):
         assert np.max(np.abs(res["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+
+
+@pytest.mark.parametrize("name,slabs", [("C5xs", 4), ("C4xs", 1), ("C1", 1)])
+def test_psi_summed_in_k3(pkg, name, slabs):
+    """DESIGN.md R25: on one device with WI = I, K2's finalizing segment reads no p and K3 sums
+    psi = y_k^T p_{k-1} from the y and p it reads anyway (psi3). Every other scalar record is
+    bitwise the same as with psi summed in K2 (PLSS_PSI3=0); psi agrees to rounding and keeps the
+    identity psi = -rho. Under PLSS W (and on a distributed ctx) K2 keeps summing psi."""
+    s = plss_gen.make_config(name)
+    A = _matrix(pkg, s)
+    b = torch.from_numpy(s.b).cuda()
+    runs = {}
+    for flag in (1, 0):
+        with _env(PLSS_PSI3=flag):
+            ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=40)
+        S = pkg.plss_query(ctx)["slabs"]
+        assert [pkg.plss_query_segment(ctx, 2, sl)["psi3"] for sl in range(S)] == [0] * (S - 1) + [flag]
+        runs[flag] = pkg.plss_solve(ctx, b, tol=0.0, maxit=30, flags=1, want_diag=True)
+        if flag:
+            pkg.plss_set_wi(ctx, pkg.plss_column_norms(ctx))
+            runs["w1"] = pkg.plss_solve(ctx, b, tol=0.0, maxit=30, flags=1, want_diag=True)
+        else:
+            pkg.plss_set_wi(ctx, pkg.plss_column_norms(ctx))
+            runs["w0"] = pkg.plss_solve(ctx, b, tol=0.0, maxit=30, flags=1, want_diag=True)
+        pkg.plss_destroy(ctx)
+    d1, d0 = runs[1]["diag"], runs[0]["diag"]
+    live = np.arange(1, 30)
+    for col in (0, 1, 2, 4, 5, 6, 7):                      # hist, rho, phi, theta, tau, beta, gamma
+        np.testing.assert_array_equal(d1[:31, col], d0[:31, col])
+    np.testing.assert_allclose(d1[live, 3], d0[live, 3], rtol=1e-12, atol=0)
+    assert np.all(np.abs(d1[live, 3] / d1[live, 1] + 1) <= 1e-9)         # psi = -rho
+    np.testing.assert_array_equal(runs["w1"]["diag"], runs["w0"]["diag"])  # PLSS W: psi from K2 either way
+    with _env(PLSS_DIST_CHUNKS=1):
+        ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=1, maxit_cap=8)
+    assert pkg.plss_query_segment(ctx, 2, 0)["psi3"] == 0
+    pkg.plss_destroy(ctx)
