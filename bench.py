@@ -558,10 +558,12 @@ def main():
     pkg.plss_step(ctx, 3)
     kt = pkg.plss_profile(ctx, max(1, args.profile_steps))
     k1_bytes = 12 * nnz_l + 4 * (m_l + 1) + 8 * n + 16 * m_l
-    # K2 writes y (8n); it reads p (8n) for psi only where K3 does not sum it (R25)
-    psi3 = pkg.plss_query_segment(ctx, 2, q["slabs"] - 1)["psi3"] and not args.plss_w
-    k2_bytes = 12 * nnz_l + 4 * (n + 1) + 8 * m_l + (8 if psi3 else 16) * n
+    # SURVEY 8(d)'s per-kernel figures (K2's includes the p read for psi, which one device sums in
+    # K3 instead: DESIGN.md R25; the ncu traffic shows the bytes actually moved)
+    k2_bytes = 12 * nnz_l + 4 * (n + 1) + 8 * m_l + 16 * n
     k3_bytes = 40 * n
+    s2 = pkg.plss_query_segment(ctx, 2, q["slabs"] - 1)
+    fused = world == 1 and not args.force_dist and not args.plss_w and bool(s2["psi3"]) and bool(s2["xdefer"])
     classes = {"k1_spmv_csr_resid": (kt["k1"], k1_bytes), "k2_spmv_csc_gather": (kt["k2"], k2_bytes),
                "k3_pxupdate": (kt["k3"], k3_bytes)}
     dom = max(classes, key=lambda c: classes[c][0])
@@ -607,13 +609,18 @@ def main():
                        "rhs": ("paper: x = ones, x(1) = 10, b = A x (P:L987)" if args.rhs == "paper"
                                else "b = A x*, x* ~ N(0,1)"),
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
-                       "bytes_per_step_model": "24 nnz + 28 m + 60 n + 8 (DESIGN.md R25)",
+                       "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8 (SURVEY 8(d))",
                        "workspace_gb": round(ctx.workspace.numel() / 1e9, 3),
                        "matrix_gb": round(sum(t.numel() * t.element_size() for t in (
                            w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])) / 1e9, 3)},
             "achieved_gbs": B_global * iters_per_s / 1e9,
             "achieved_frac_of_peak": B_global * iters_per_s / 1e9 / peak,
             "achieved_frac_of_8tbs": B_global * iters_per_s / 1e9 / 8000.0,
+            # the same rate on the bytes the fused one-device step's data flow needs (psi in K3, x
+            # every other step: 24 nnz + 28 m + 52 n + 8, R25); None where not fused
+            "achieved_frac_of_peak_fused_flow": (
+                plss_gen.bytes_per_iter_fused(w["m_global"], n_global, w["nnz_global"]) * iters_per_s / 1e9 / peak
+                if fused else None),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,

@@ -232,9 +232,10 @@ plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t 
  * rows (run by k_longchunks, or by k_longrows when info[8] = 0), info[5] static stepping (1, or 2
  * with 6 entries in flight), info[6] the grid, info[7] the segment's rows, info[8] the long rows'
  * chunks of LCH entries (k_longchunks; 0 without long rows or with PLSS_LCHUNK=0), info[9] 1 if the
- * segment (K2's finalizing one, one device) leaves psi = y^T p_{k-1} to K3 and reads no p (DESIGN.md
- * R25). PLSS_E_INVALID for a bad ctx / which / slab. */
-plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[10]);
+ * segment (K2's finalizing one, one device) leaves psi = y^T p_{k-1} to K3 and reads no p, info[10]
+ * 1 if the ctx's K3 updates x every other step (one device; plss_finish applies a pending update)
+ * (R25). PLSS_E_INVALID for a bad ctx / which / slab. */
+plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[11]);
 
 /* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
  * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:

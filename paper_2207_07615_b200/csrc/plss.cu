@@ -201,6 +201,7 @@ bool is_device_ptr(const void* p) {
 }  // namespace
 
 struct plss_ctx {
+  bool xdefer = false;         // K3 updates x every other step (K3_XDEFER; one device, PLSS path)
   int dev = 0;
   cudaStream_t stream = nullptr;       // work stream (the caller's, or our own if it passed NULL)
   cudaStream_t user_stream = nullptr;  // the caller's stream
@@ -427,6 +428,13 @@ static plss_status enqueue_step_cols(plss_ctx* ctx) {
 }
 
 // enqueue one loop step (also used inside graph capture)
+// K3's options on the plain (one device, row-slab) step: psi summed in K3 when K2's finalizing
+// segment left it (R25), x updated every other step (K3_XDEFER, flushed by plss_finish)
+static int k3_opts(const plss_ctx* ctx) {
+  if (ctx->dist || ctx->cols || ctx->rsag) return 0;
+  return (ctx->seg2[ctx->S - 1].psi3 ? K3_PSI : 0) | (ctx->xdefer ? K3_XDEFER : 0);
+}
+
 static plss_status enqueue_step(plss_ctx* ctx) {
   if (ctx->cols) return enqueue_step_cols(ctx);
   cudaStream_t st = ctx->stream;
@@ -481,7 +489,7 @@ static plss_status enqueue_step(plss_ctx* ctx) {
                                            ctx->part2, ctx->counters + 1, ctx->wi);
   }
   k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
-                                     ctx->counters + 2, ctx->wi, nullptr, ctx->seg2[ctx->S - 1].psi3);
+                                     ctx->counters + 2, ctx->wi, nullptr, k3_opts(ctx));
   CK(cudaGetLastError());
   return PLSS_OK;
 }
@@ -1277,6 +1285,7 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     ctx->seg1[0].nparts = std::min(MAXG, ctx->g1[0] + 1);
     ctx->seg2[0].nparts = std::min(MAXG, ctx->g2[0] + 1);
   }
+  ctx->xdefer = !dist && !ctx->cols && !ctx->rsag && env_int("PLSS_XDEFER", 1);
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gdots = grid_for((n + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gnorm = grid_for((m + NT - 1) / NT + 1, occ_vec, sms);
@@ -1556,6 +1565,11 @@ plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, 
   cudaStream_t st = ctx->stream;
   if (ctx->rsag)                                    // x lives as column shards: gather (collective)
     NK(ncclAllGather(ctx->x + ctx->c0, ctx->x, (size_t)ctx->cnt, ncclFloat64, ctx->comm, st));
+  if (ctx->xdefer && ctx->n > 0) {                  // x lags one update (K3_XDEFER): x <- x + p
+    k_xflush<<<ctx->g3, NT, 0, st>>>(ctx->x, ctx->p, ctx->n, ctx->ctl);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(&ctx->ctl->xlag, 0, sizeof(int32_t), st));
+  }
   if (x && ctx->n > 0)
     CK(cudaMemcpyAsync(x, ctx->x, 8 * (size_t)ctx->n, is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -1775,7 +1789,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       CK(cudaEventRecord(ev[q++], st));
     }
     k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
-                                       ctx->counters + 2, ctx->wi, nullptr, ctx->seg2[ctx->S - 1].psi3);
+                                       ctx->counters + 2, ctx->wi, nullptr, k3_opts(ctx));
     CK(cudaEventRecord(ev[q++], st));
     }
     CK(cudaGetLastError());
@@ -1833,7 +1847,7 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   return PLSS_OK;
 }
 
-plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[10]) {
+plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[11]) {
   if (!ctx || !info || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
   const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
   info[0] = a.fmt;
@@ -1846,6 +1860,7 @@ plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab,
   info[7] = a.nrows;
   info[8] = a.lchunk ? a.nchunks : 0;
   info[9] = a.psi3;
+  info[10] = ctx->xdefer ? 1 : 0;
   return PLSS_OK;
 }
 

@@ -67,6 +67,7 @@ struct Ctl {
   double nb2;       // ||b||^2 (local on a rank before the all-reduce)
   int32_t iters, maxit, done, frozen, stopped, outcome, freeze, tol_mode;
   int32_t weighted; // PLSS W: WI = diag(wi) (Algorithm 1 with B^T B)
+  int32_t xlag;     // K3_XDEFER: x lacks the current p (x_k = x + p); plss_finish applies it
 };
 
 enum Role { ROLE_PLAIN = 0, ROLE_K1 = 1, ROLE_K2 = 2, ROLE_K2DOTS = 3 };
@@ -1784,13 +1785,23 @@ __global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double
 // ---------------------------------------------------------------------------------------------
 // K3: p <- beta p + gamma y; theta = p^T p; x <- x + p  (L811-813); init: p = gamma y (L795)
 // ---------------------------------------------------------------------------------------------
+constexpr int K3_PSI = 1, K3_XDEFER = 2;         // k_pxupdate options (one device, PLSS path)
+
+// plss_finish under K3_XDEFER: x <- x + p when x lags (Ctl::xlag; the host clears the flag after)
+__global__ void __launch_bounds__(NT, VEC_MINB) k_xflush(double* __restrict__ x, const double* __restrict__ p,
+                                                       long long n, const Ctl* c) {
+  if (!c->xlag) return;
+  for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT)
+    x[i] = __dadd_rn(x[i], p[i]);
+}
+
 // theta_out != NULL (the reduce-scatter distributed step, K3 on this rank's column shard): the
 // shard's p^T p goes there (summed across ranks with the next step's scalars) instead of c->theta
 __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ p, const double* __restrict__ y,
                                                  double* __restrict__ x, long long n, Ctl* c,
                                                  double* rec, double* partial, unsigned* counter,
                                                  const double* __restrict__ wi, double* theta_out = nullptr,
-                                                 int psi_here = 0) {
+                                                 int opts = 0) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
   const bool wtd = wi != nullptr && c->weighted;       // theta = p^T (WI p) under PLSS W (L812)
@@ -1798,7 +1809,11 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
   const bool init = (k == 0);
   const double beta = c->beta, gamma = c->gamma;
   // psi = y_k^T p_{k-1} (L806, diagnostic) summed here when K2 left it (SpmvSeg::psi3, WI = I)
-  const bool psi = psi_here && !wtd && !init;
+  const bool psi = (opts & K3_PSI) && !wtd && !init;
+  // K3_XDEFER: x is updated every other step, x <- (x + p_{k-1}) + p_k when it lags (bitwise the
+  // two sequential updates of L813); the other steps leave x (Ctl::xlag, plss_finish applies it)
+  const bool defer = opts & K3_XDEFER;
+  const bool lag = defer && c->xlag;
   double acc = 0.0, acc1 = 0.0;
   const long long n2 = n >> 1;
   const long long stride = (long long)gridDim.x * NT;
@@ -1807,12 +1822,12 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
   const double2* y2 = reinterpret_cast<const double2*>(y);
   for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n2; i += stride) {
     const double2 yy = __ldcs(y2 + i);
-    double2 pp;
+    double2 pp, po = make_double2(0.0, 0.0);
     if (init) {
       pp.x = __dmul_rn(gamma, yy.x);
       pp.y = __dmul_rn(gamma, yy.y);
     } else {
-      const double2 po = p2[i];
+      po = p2[i];
       pp.x = __dadd_rn(__dmul_rn(beta, po.x), __dmul_rn(gamma, yy.x));
       pp.y = __dadd_rn(__dmul_rn(beta, po.y), __dmul_rn(gamma, yy.y));
       if (psi) {
@@ -1821,10 +1836,16 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
       }
     }
     p2[i] = pp;
-    double2 xx = __ldcs(x2 + i);
-    xx.x = __dadd_rn(xx.x, pp.x);
-    xx.y = __dadd_rn(xx.y, pp.y);
-    __stcs(x2 + i, xx);
+    if (!defer || lag) {
+      double2 xx = __ldcs(x2 + i);
+      if (lag) {
+        xx.x = __dadd_rn(xx.x, po.x);
+        xx.y = __dadd_rn(xx.y, po.y);
+      }
+      xx.x = __dadd_rn(xx.x, pp.x);
+      xx.y = __dadd_rn(xx.y, pp.y);
+      __stcs(x2 + i, xx);
+    }
     if (wtd) {
       const double2 w = __ldg(reinterpret_cast<const double2*>(wi) + i);
       acc = fma(pp.x, w.x * pp.x, acc);
@@ -1837,9 +1858,10 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const long long i = n - 1;
     if (psi) acc1 = fma(y[i], p[i], acc1);
-    const double pp = init ? __dmul_rn(gamma, y[i]) : __dadd_rn(__dmul_rn(beta, p[i]), __dmul_rn(gamma, y[i]));
+    const double po = init ? 0.0 : p[i];
+    const double pp = init ? __dmul_rn(gamma, y[i]) : __dadd_rn(__dmul_rn(beta, po), __dmul_rn(gamma, y[i]));
     p[i] = pp;
-    x[i] = __dadd_rn(x[i], pp);
+    if (!defer || lag) x[i] = __dadd_rn(lag ? __dadd_rn(x[i], po) : x[i], pp);
     acc = fma(pp, wtd ? wi[i] * pp : pp, acc);
   }
   if (!publish_and_elect(acc, acc1, partial, partial, gridDim.x, counter, sm)) return;
@@ -1848,6 +1870,7 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
     c->psi = acc1;
     rec[(size_t)k * REC + 3] = acc1;
   }
+  if (defer) c->xlag = lag ? 0 : 1;
   if (theta_out) {
     *theta_out = acc;                                           // shard partial of theta
   } else {

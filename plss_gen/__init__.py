@@ -63,13 +63,18 @@ class System:
 
 
 def bytes_per_iter(m: int, n: int, nnz: int) -> int:
-    """Algorithmic HBM bytes of one iteration: 24 nnz + 28 m + 60 n (+8).
+    """Algorithmic HBM bytes of one iteration: 24 nnz + 28 m + 68 n (+8).
 
-    K1: 12 nnz + 4(m+1) + 8n + 16m;  K2: 12 nnz + 4(n+1) + 8m + 8n (y);  K3: 40n.
-    SURVEY 8(d) wrote 68 n: its K2 also read p (8n) for the diagnostic psi = y^T p_{k-1}, which
-    K3 reads anyway to update p; psi is summed there (R25), so p is read once per step.
+    K1: 12 nnz + 4(m+1) + 8n + 16m;  K2: 12 nnz + 4(n+1) + 8m + 8n + 8n;  K3: 40n.
     """
-    return 24 * nnz + 28 * m + 60 * n + 8
+    return 24 * nnz + 28 * m + 68 * n + 8
+
+
+def bytes_per_iter_fused(m: int, n: int, nnz: int) -> int:
+    """The bytes the one-device PLSS step's own data flow needs (R25): SURVEY 8(d)'s
+    B_iter less K2's p read for psi (summed in K3 from the p it reads anyway, 8n) and half of K3's
+    x read + write (x updated every other step, 8n on average): 24 nnz + 28 m + 52 n (+8)."""
+    return 24 * nnz + 28 * m + 52 * n + 8
 
 
 # ----------------------------------------------------------------------------------------------

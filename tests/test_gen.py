@@ -91,6 +91,7 @@ def test_row_blocks_cover_rows():
 
 
 def test_bytes_per_iter_model():
-    # SURVEY 8(d)'s B_iter less K2's p read for psi (summed in K3, R25): 24 nnz + 28 m + 60 n (+8)
+    # B_iter = 24 nnz + 28 m + 68 n (+8); the fused one-device flow (R25) 16 n less
     assert plss_gen.bytes_per_iter(64_000_000, 8_000_000, 768_000_000) == \
-        24 * 768_000_000 + 28 * 64_000_000 + 60 * 8_000_000 + 8
+        24 * 768_000_000 + 28 * 64_000_000 + 68 * 8_000_000 + 8
+    assert plss_gen.bytes_per_iter(5, 7, 11) - plss_gen.bytes_per_iter_fused(5, 7, 11) == 16 * 7

@@ -255,3 +255,43 @@ def test_psi_summed_in_k3(pkg, name, slabs):
         ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=1, maxit_cap=8)
     assert pkg.plss_query_segment(ctx, 2, 0)["psi3"] == 0
     pkg.plss_destroy(ctx)
+
+
+@pytest.mark.parametrize("name,slabs", [("C5xs", 4), ("C4xs", 1), ("C1", 1)])
+def test_x_every_other_step(pkg, name, slabs):
+    """DESIGN.md R25: on one device K3 updates x every other step, x <- (x + p_{k-1}) + p_k, and
+    plss_finish applies a pending update -- bitwise the sequential x_k = x_{k-1} + p_k (L813) after
+    any number of steps, also across start / step / finish / step / finish and early stops."""
+    s = plss_gen.make_config(name)
+    A = _matrix(pkg, s)
+    b = torch.from_numpy(s.b).cuda()
+    out = {}
+    for flag in (1, 0):
+        with _env(PLSS_XDEFER=flag):
+            ctx = pkg.plss_create(A, slabs=slabs, maxit_cap=40)
+        assert pkg.plss_query_segment(ctx, 1, 0)["xdefer"] == flag
+        for maxit in (29, 30):                                    # odd and even step counts
+            r = pkg.plss_solve(ctx, b, tol=0.0, maxit=maxit, flags=1, want_diag=True)
+            out[flag, maxit] = (r["x"].cpu().numpy(), r["diag"])
+        r = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)           # stops on the tolerance (or maxit)
+        out[flag, "tol"] = (r["x"].cpu().numpy(), r["iters"])
+        pkg.plss_start(ctx, b, None, tol=0.0, maxit=40, flags=1)
+        xs = []
+        for k in (7, 6, 1):
+            pkg.plss_step(ctx, k)
+            xb = torch.empty(s.n, dtype=torch.float64, device="cuda")
+            pkg.plss_finish(ctx, x=xb)
+            xs.append(xb.cpu().numpy())
+        out[flag, "split"] = xs
+        pkg.plss_destroy(ctx)
+    for key in ((29,), (30,)):
+        np.testing.assert_array_equal(out[1, key[0]][0], out[0, key[0]][0])
+        np.testing.assert_array_equal(out[1, key[0]][1], out[0, key[0]][1])
+    np.testing.assert_array_equal(out[1, "tol"][0], out[0, "tol"][0])
+    assert out[1, "tol"][1] == out[0, "tol"][1]
+    for a, c in zip(out[1, "split"], out[0, "split"]):
+        np.testing.assert_array_equal(a, c)
+    with _env(PLSS_DIST_CHUNKS=1):
+        ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=1, maxit_cap=8)
+    assert pkg.plss_query_segment(ctx, 1, 0)["xdefer"] == 0
+    pkg.plss_destroy(ctx)
