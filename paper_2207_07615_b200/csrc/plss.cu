@@ -345,15 +345,15 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
       cudaStreamWaitEvent(st2, (cudaEvent_t)a.fork_ev, 0);
       launch_long<ROLE>(c, st2);
       cudaEventRecord((cudaEvent_t)a.join_ev, st2);
-      k_sell<ROLE, 1024, false, false, SIGMA, false, SU, GS_NSB><<<grid, 1024, 0, st>>>(b);   // gsort: no y staging
+      k_sell<ROLE, 1024, false, false, SIGMA, false, GS_SU, GS_NSB><<<grid, 1024, 0, st>>>(b);   // gsort: no y staging
       cudaStreamWaitEvent(st, (cudaEvent_t)a.join_ev, 0);
     } else {
-      k_sell<ROLE, 1024, false, false, SIGMA, false, SU, GS_NSB><<<grid, 1024, 0, st>>>(b);
+      k_sell<ROLE, 1024, false, false, SIGMA, false, GS_SU, GS_NSB><<<grid, 1024, 0, st>>>(b);
       launch_long<ROLE>(c, st);
     }
   }
   else if (a.fmt == 3 && a.gsort)
-    k_sell<ROLE, 1024, false, false, SIGMA, false, SU, GS_NSB><<<grid, 1024, 0, st>>>(a);
+    k_sell<ROLE, 1024, false, false, SIGMA, false, GS_SU, GS_NSB><<<grid, 1024, 0, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort && a.sig == SIGMA_WIDE)
     k_sell<ROLE, 1024, false, true, SIGMA_WIDE><<<grid, 1024, YSTAGE_SMEM_WIDE, st>>>(a);
   else if (a.fmt == 3 && ROLE >= ROLE_K2 && a.perm && !a.gsort)     // K2 with a sigma perm: staged y
@@ -589,7 +589,7 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
     const double frac = (double)a.long_entries / (double)(a.long_entries + a.short_entries);
     sms_k = std::max(1, sms - (int)std::lround(sms * frac * env_int("PLSS_LSHARE", 0) / 100.0));
   }
-  const int grid = std::max(1, std::min(std::min(nblocks, sms_k), MAXG));
+  const int grid = std::max(1, std::min(std::min(nblocks, sms_k * (a.gsort ? GS_MINB : 1)), MAXG));
   int32_t* cblk = pool.cblk + pool.used_c;
   // CTA balance: a unit costs its stored entries plus a fixed overhead (metadata loads, row
   // outputs, dot partial); sigma-permuted slices also pay the scattered / staged y. Measured best:

@@ -712,6 +712,14 @@ __host__ __device__ constexpr int nsb_of(int sig) { return sig / 32 > 16 ? sig /
 #define PLSS_GS_NSB 1
 #endif
 constexpr int GS_NSB = PLSS_GS_NSB;
+#ifndef PLSS_GS_MINB
+#define PLSS_GS_MINB 1                  // 1024-thread CTAs per SM of globally sorted segments
+#endif
+constexpr int GS_MINB = PLSS_GS_MINB;
+#ifndef PLSS_GS_SU
+#define PLSS_GS_SU PLSS_SU              // their entries per lane in flight
+#endif
+constexpr int GS_SU = PLSS_GS_SU;
 constexpr int YD = 1024;
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
@@ -812,7 +820,7 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
 // false); YS: the K2 segment's y is staged (sigma perm)
 template <int ROLE, int BS = NT, bool LU = false, bool YS = false, int SIGT = SIGMA, bool STAT = false,
           int SUK = SU, int GNSB = 0>
-__global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : 1) k_sell(SpmvSeg a) {
+__global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : GNSB ? GS_MINB : 1) k_sell(SpmvSeg a) {
   constexpr int SPW = SIGT / 32;                 // this instantiation's sigma window (a.sig)
   constexpr int NSB = GNSB ? GNSB : nsb_of(SIGT); // CTA-range granularity (slices)
   constexpr int SIGMA = SIGT;
