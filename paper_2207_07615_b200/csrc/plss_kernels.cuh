@@ -1794,6 +1794,13 @@ __global__ void k_sell_fill(const int32_t* ptr, const int32_t* idx, const double
 // K3: p <- beta p + gamma y; theta = p^T p; x <- x + p  (L811-813); init: p = gamma y (L795)
 // ---------------------------------------------------------------------------------------------
 constexpr int K3_PSI = 1, K3_XDEFER = 2;         // k_pxupdate options (one device, PLSS path)
+#ifndef PLSS_K3X
+#define PLSS_K3X 1                                   // K3 loads x together with y and p
+#endif
+#ifndef PLSS_K3U
+#define PLSS_K3U 1                                   // K3 loop unroll
+#endif
+constexpr int K3U = PLSS_K3U;
 
 // plss_finish under K3_XDEFER: x <- x + p when x lags (Ctl::xlag; the host clears the flag after)
 __global__ void __launch_bounds__(NT, VEC_MINB) k_xflush(double* __restrict__ x, const double* __restrict__ p,
@@ -1828,9 +1835,15 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
   double2* p2 = reinterpret_cast<double2*>(p);
   double2* x2 = reinterpret_cast<double2*>(x);
   const double2* y2 = reinterpret_cast<const double2*>(y);
+  const bool xupd = !defer || lag;
+#pragma unroll K3U
   for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n2; i += stride) {
     const double2 yy = __ldcs(y2 + i);
     double2 pp, po = make_double2(0.0, 0.0);
+#if PLSS_K3X
+    double2 xx = make_double2(0.0, 0.0);
+    if (xupd) xx = __ldcs(x2 + i);                   // issued with y and p: one latency per element
+#endif
     if (init) {
       pp.x = __dmul_rn(gamma, yy.x);
       pp.y = __dmul_rn(gamma, yy.y);
@@ -1844,8 +1857,10 @@ __global__ void __launch_bounds__(NT, VEC_MINB) k_pxupdate(double* __restrict__ 
       }
     }
     p2[i] = pp;
-    if (!defer || lag) {
+    if (xupd) {
+#if !PLSS_K3X
       double2 xx = __ldcs(x2 + i);
+#endif
       if (lag) {
         xx.x = __dadd_rn(xx.x, po.x);
         xx.y = __dadd_rn(xx.y, po.y);
