@@ -201,7 +201,8 @@ bool is_device_ptr(const void* p) {
 }  // namespace
 
 struct plss_ctx {
-  bool xdefer = false;         // K3 updates x every other step (K3_XDEFER; one device, PLSS path)
+  bool xdefer = false;         // K3 updates x every other step (K3_XDEFER; row-slab steps)
+  int psi_dots = 0;            // row blocks: k_dots_tail leaves psi to K3 (K3_PSI)
   int dev = 0;
   cudaStream_t stream = nullptr;       // work stream (the caller's, or our own if it passed NULL)
   cudaStream_t user_stream = nullptr;  // the caller's stream
@@ -428,11 +429,13 @@ static plss_status enqueue_step_cols(plss_ctx* ctx) {
 }
 
 // enqueue one loop step (also used inside graph capture)
-// K3's options on the plain (one device, row-slab) step: psi summed in K3 when K2's finalizing
-// segment left it (R25), x updated every other step (K3_XDEFER, flushed by plss_finish)
+// K3's options on the row-slab steps (one device, or row blocks with the all-reduce / peer step): psi
+// summed in K3 when K2's finalizing segment (or k_dots_tail) left it (R25), x updated every
+// other step (K3_XDEFER, flushed by plss_finish)
 static int k3_opts(const plss_ctx* ctx) {
-  if (ctx->dist || ctx->cols || ctx->rsag) return 0;
-  return (ctx->seg2[ctx->S - 1].psi3 ? K3_PSI : 0) | (ctx->xdefer ? K3_XDEFER : 0);
+  if (ctx->cols || ctx->rsag) return 0;
+  const bool psi = ctx->dist ? ctx->psi_dots : ctx->seg2[ctx->S - 1].psi3;
+  return (psi ? K3_PSI : 0) | (ctx->xdefer ? K3_XDEFER : 0);
 }
 
 static plss_status enqueue_step(plss_ctx* ctx) {
@@ -486,7 +489,7 @@ static plss_status enqueue_step(plss_ctx* ctx) {
       NK(ncclAllReduce(ctx->y, ctx->y, (size_t)ctx->n + 1, ncclFloat64, ncclSum, ctx->comm, st));
     }
     k_dots_tail<<<ctx->gdots, NT, 0, st>>>(yv, ctx->p, ctx->n, yv + ctx->n, ctx->ctl, ctx->rec,
-                                           ctx->part2, ctx->counters + 1, ctx->wi);
+                                           ctx->part2, ctx->counters + 1, ctx->wi, ctx->psi_dots);
   }
   k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,
                                      ctx->counters + 2, ctx->wi, nullptr, k3_opts(ctx));
@@ -1285,7 +1288,8 @@ static plss_status setup(plss_ctx* ctx, const plss_matrix* A, const plss_options
     ctx->seg1[0].nparts = std::min(MAXG, ctx->g1[0] + 1);
     ctx->seg2[0].nparts = std::min(MAXG, ctx->g2[0] + 1);
   }
-  ctx->xdefer = !dist && !ctx->cols && !ctx->rsag && env_int("PLSS_XDEFER", 1);
+  ctx->xdefer = !ctx->cols && !ctx->rsag && env_int("PLSS_XDEFER", 1);
+  ctx->psi_dots = (dist && !ctx->cols && !ctx->rsag && env_int("PLSS_PSI3", 1)) ? 1 : 0;
   ctx->g3 = grid_for((n / 2 + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gdots = grid_for((n + NT - 1) / NT + 1, occ_vec, sms);
   ctx->gnorm = grid_for((m + NT - 1) / NT + 1, occ_vec, sms);
@@ -1785,7 +1789,7 @@ plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
       }
       CK(cudaEventRecord(ev[q++], st));
       k_dots_tail<<<ctx->gdots, NT, 0, st>>>(yv, ctx->p, ctx->n, yv + ctx->n, ctx->ctl, ctx->rec,
-                                             ctx->part2, ctx->counters + 1, ctx->wi);
+                                             ctx->part2, ctx->counters + 1, ctx->wi, ctx->psi_dots);
       CK(cudaEventRecord(ev[q++], st));
     }
     k_pxupdate<<<ctx->g3, NT, 0, st>>>(ctx->p, yv, ctx->x, ctx->n, ctx->ctl, ctx->rec, ctx->part3,

@@ -1978,10 +1978,11 @@ __global__ void k_tail_phi(Ctl* c, double* rec, const double* scal) {
 __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const double* __restrict__ p,
                                                   long long n, const double* rho_g, Ctl* c,
                                                   double* rec, double* partial, unsigned* counter,
-                                                  const double* __restrict__ wi) {
+                                                  const double* __restrict__ wi, int psi_k3 = 0) {
   __shared__ double sm[2][MAXW];
   if (c->done) return;
   const bool wtd = wi != nullptr && c->weighted;
+  const bool psi = !psi_k3 || wtd;                 // else K3 sums psi (K3_PSI) and p is not read here
   double a0 = 0.0, a1 = 0.0;
   auto one = [&](long long i) {
     const double yy = y[i];
@@ -1992,7 +1993,7 @@ __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const 
     } else {
       a0 = fma(yy, yy, a0);
     }
-    a1 = fma(yy, p[i], a1);
+    if (psi) a1 = fma(yy, p[i], a1);
   };
   const long long stride = (long long)gridDim.x * NT;
   if (((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(wi)) & 15) == 0) {
@@ -2000,7 +2001,7 @@ __global__ void __launch_bounds__(NT) k_dots_tail(double* __restrict__ y, const 
     const long long n2 = n >> 1;
     for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n2; i += stride) {
       const double2 yy = reinterpret_cast<const double2*>(y)[i];
-      const double2 pp = reinterpret_cast<const double2*>(p)[i];
+      const double2 pp = psi ? reinterpret_cast<const double2*>(p)[i] : make_double2(0.0, 0.0);
       if (wtd) {
         const double2 ww = reinterpret_cast<const double2*>(wi)[i];
         const double2 wy = make_double2(__ddiv_rn(yy.x, ww.x), __ddiv_rn(yy.y, ww.y));

@@ -291,7 +291,17 @@ def test_x_every_other_step(pkg, name, slabs):
     assert out[1, "tol"][1] == out[0, "tol"][1]
     for a, c in zip(out[1, "split"], out[0, "split"]):
         np.testing.assert_array_equal(a, c)
-    with _env(PLSS_DIST_CHUNKS=1):
-        ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=1, maxit_cap=8)
-    assert pkg.plss_query_segment(ctx, 1, 0)["xdefer"] == 0
-    pkg.plss_destroy(ctx)
+    # the row-block step (single-rank NCCL ctx, chunked all-reduce): x every other step and psi in K3
+    # (k_dots_tail reads no p) as well; x and every record but psi bitwise their every-step forms
+    dist_out = {}
+    for flag in (1, 0):
+        with _env(PLSS_DIST_CHUNKS=4, PLSS_XDEFER=flag, PLSS_PSI3=flag):
+            ctx = pkg.plss_create_dist(A, 0, s.m, pkg.plss_get_unique_id(), 0, 1, slabs=1, maxit_cap=40)
+        assert pkg.plss_query_segment(ctx, 1, 0)["xdefer"] == flag
+        r = pkg.plss_solve(ctx, b, tol=0.0, maxit=29, flags=1, want_diag=True)
+        dist_out[flag] = (r["x"].cpu().numpy(), r["diag"])
+        pkg.plss_destroy(ctx)
+    np.testing.assert_array_equal(dist_out[1][0], dist_out[0][0])
+    for col in (0, 1, 2, 4, 5, 6, 7):
+        np.testing.assert_array_equal(dist_out[1][1][:, col], dist_out[0][1][:, col])
+    np.testing.assert_allclose(dist_out[1][1][1:30, 3], dist_out[0][1][1:30, 3], rtol=1e-12, atol=0)
