@@ -48,7 +48,8 @@ int auto_slabs(int64_t m) {
   if (env && std::atoi(env) > 0) return std::atoi(env);
   // r slab kept L2-resident between K1_s and K2_s; more slabs cost a y read-modify-write each.
   // C5 (512 MB of r), ms per step over 3 interleaved runs: 8 slabs 6.05-6.07, 9 5.96-5.97,
-  // 10 5.93-5.94, 11 5.98-6.01, 12 6.09-6.11, 16 6.48 (scripts/gpu_slabs.sh)
+  // 10 5.93-5.94, 11 5.98-6.01, 12 6.09-6.11, 16 6.48 (scripts/gpu_slabs.sh); re-checked on the
+  // final round-2 build, two interleaved runs: 8 5.48-5.49, 9 5.43-5.44, 10 5.42, 11 5.49
   const int64_t slab_bytes = 52ll << 20;
   int64_t s = (m * 8 + slab_bytes - 1) / slab_bytes;
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
