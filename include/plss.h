@@ -167,7 +167,9 @@ plss_status plss_solve(plss_ctx *ctx, const double *b, const double *x0, double 
 /* Asynchronous pieces of plss_solve (same argument meaning), for timing and pipelining:
  * plss_start copies b / x0 in and resets the device state; plss_step enqueues k more loop steps
  * (CUDA graphs; steps after the stop condition are no-ops); plss_finish synchronizes and copies
- * out x, iters, hist, diag, outcome. */
+ * out x, iters, hist, diag, outcome. Between plss_step and plss_finish the device copy of x may lag
+ * the last update p_k by one (the row-slab steps update x every other step, R25);
+ * plss_finish applies it, and stepping may continue after plss_finish. */
 plss_status plss_start(plss_ctx *ctx, const double *b, const double *x0, double tol,
                        int32_t tol_mode, int32_t maxit, int32_t flags);
 plss_status plss_step(plss_ctx *ctx, int32_t k);
