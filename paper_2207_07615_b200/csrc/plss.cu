@@ -328,7 +328,7 @@ static void launch_long(const SpmvSeg& c, cudaStream_t st) {
 template <int ROLE>
 static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
   if (a.fmt == 5)
-    k_scalar<ROLE><<<grid, NT, 0, st>>>(a);
+    a.scb == 3 ? k_scalar<ROLE, 3><<<grid, NT, 0, st>>>(a) : k_scalar<ROLE, 2><<<grid, NT, 0, st>>>(a);
   else if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
   else if (a.fmt == 3 && a.nlong > 0) {
@@ -857,6 +857,7 @@ static plss_status try_scalar(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, int sm
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scalar<ROLE_K2DOTS>, NT, 0));
   a.fmt = 5;
+  a.scb = (nnz_seg < 2 * a.nrows && env_int("PLSS_SCB3", 1)) ? 3 : 2;   // mean < 2 entries: 3 in flight
   *grid_out = (int)std::max<int64_t>(1, std::min<int64_t>((a.nrows + NT - 1) / NT, (int64_t)std::max(1, occ) * sms));
   *grid_out = std::min(*grid_out, MAXG);
   return PLSS_OK;

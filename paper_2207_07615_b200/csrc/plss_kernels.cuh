@@ -127,6 +127,7 @@ struct SpmvSeg {
   // CTA that finalizes; elect_total = the slices' grid + 1
   int32_t elect_extra, elect_total;
   int32_t psi3;              // K2's finalizing segment on one device: psi left to K3 (k2_final)
+  int32_t scb;               // fmt 5: entries per thread in flight (k_scalar's SCBT: 2 or 3)
   long long long_entries, short_entries;   // setup: entries of the long rows / of the slices
   void* fork_stream;         // host handles (cudaStream_t, cudaEvent_t x 2) for that fork / join
   void* fork_ev;
@@ -1051,11 +1052,13 @@ constexpr int SCALAR_MAX = 32;
 #ifndef PLSS_SCB
 #define PLSS_SCB 2
 #endif
-constexpr int SCB = PLSS_SCB;           // entries per thread in flight (rows are short)
+constexpr int SCB = PLSS_SCB;           // entries per thread in flight (rows are short); segments
+                                        // of mean < 2 entries take 3 (SpmvSeg::scb; C4's columns:
+                                        // K2 0.079 -> 0.075 ms, C4-alt's mean-3 columns lose with 3)
 #ifndef PLSS_SCMINB
 #define PLSS_SCMINB 8                   // CTAs per SM (2048 threads: C4 K2 0.104 -> 0.089 ms vs 6)
 #endif
-template <int ROLE>
+template <int ROLE, int SCBT = SCB>
 __global__ void __launch_bounds__(NT, PLSS_SCMINB) k_scalar(SpmvSeg a) {
   __shared__ double sm[2][MAXW];
   if (a.ctl != nullptr && a.ctl->done) return;
@@ -1069,18 +1072,18 @@ __global__ void __launch_bounds__(NT, PLSS_SCMINB) k_scalar(SpmvSeg a) {
     double sv = 0.0;
     if (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate)) sv = a.out[i];
     double s = (ROLE == ROLE_K1) ? 0.0 : sv;
-    for (int e = e0; e < e1; e += SCB) {
-      int32_t c[SCB];
-      double v[SCB], g[SCB];
+    for (int e = e0; e < e1; e += SCBT) {
+      int32_t c[SCBT];
+      double v[SCBT], g[SCBT];
 #pragma unroll
-      for (int u = 0; u < SCB; ++u) {
+      for (int u = 0; u < SCBT; ++u) {
         c[u] = -1;
         if (e + u < e1) { c[u] = ld_stream(a.idx + e + u, pol); v[u] = ld_stream(a.val + e + u, pol); }
       }
 #pragma unroll
-      for (int u = 0; u < SCB; ++u) g[u] = sell_gather(a, c[u]);
+      for (int u = 0; u < SCBT; ++u) g[u] = sell_gather(a, c[u]);
 #pragma unroll
-      for (int u = 0; u < SCB; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], g[u]));
+      for (int u = 0; u < SCBT; ++u) if (c[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], g[u]));
     }
     double d0 = 0.0, d1 = 0.0;
     if (ROLE == ROLE_PLAIN) {
