@@ -610,6 +610,8 @@ def main():
                                else "b = A x*, x* ~ N(0,1)"),
                        "l2": f"inputs larger than L2: {B_global / 1e9:.2f} GB algorithmic per step",
                        "bytes_per_step_model": "24 nnz + 28 m + 68 n + 8 (SURVEY 8(d))",
+                       "vector_work": ("rho in K1, phi in K2's last slab, theta + psi in K3, x every other step "
+                                       "(DESIGN.md R25)" if fused else "as SURVEY 8(d)"),
                        "workspace_gb": round(ctx.workspace.numel() / 1e9, 3),
                        "matrix_gb": round(sum(t.numel() * t.element_size() for t in (
                            w["row_ptr"], w["col_idx"], w["val"], w["col_ptr"], w["row_idx"], w["val_t"])) / 1e9, 3)},
