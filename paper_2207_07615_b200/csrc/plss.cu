@@ -603,7 +603,12 @@ static plss_status make_contig(plss_ctx* ctx, SpmvSeg& a, SellPool& pool, int sm
   // 0.2274, C4-alt 0.3910 -> 0.3834 ms per step), 128 otherwise.
   const int uc = (a.perm && !a.gsort) ? env_int("PLSS_UC_SIG", 256)
                  : a.gsort ? env_int("PLSS_UC_GS", 48) : env_int("PLSS_UC", 128);
-  if (a.uw)
+  // one-step slices in k_sell's batched phase 2 (globally sorted): PLSS_UC_S1 per slice beyond its
+  // 32 stored entries
+  if (a.uw && a.s1on)
+    k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk, uc,
+                                                              a.s1beg, env_int("PLSS_UC_S1", 16));
+  else if (a.uw)
     k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.uw, 1, nunits, NSB, nblocks, grid, cblk, uc);
   else
     k_cta_ranges<<<(grid + 256) / 256, 256, 0, ctx->stream>>>(a.sptr, 32, nunits, NSB, nblocks, grid, cblk, uc);
@@ -747,6 +752,10 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   }
   sp[nsl] = (int32_t)steps;
   uw[nunits] = (int32_t)stored;
+  // the tail of one-step slices, then of empty ones (sorted last): k_sell's batched phase 2
+  int64_t s1beg = nsl, s1end = nsl;
+  for (int64_t s2 = nsl; s2 > 0 && sp[s2] - sp[s2 - 1] <= 1; --s2) s1beg = s2 - 1;
+  for (int64_t s2 = nsl; s2 > s1beg && sp[s2] == sp[s2 - 1]; --s2) s1end = s2 - 1;
   a.short_entries = stored;
   for (size_t k = 0; k < lrows.size(); ++k) stored += len[lrows[k]];
   a.long_entries = stored - a.short_entries;
@@ -834,6 +843,10 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
   a.uw = d_uw;
   a.idx = sidx;
   a.val = sval;
+  a.s1on = s1beg < nsl && env_int("PLSS_S1", 1);
+  a.s1beg = (int32_t)s1beg;
+  a.s1end = (int32_t)s1end;
+  a.s1step0 = sp[s1beg];
   pool.used += steps * 32;
   pool.used_slots += nsl * 32;
   pool.used_sp += nsl + 1;
@@ -1853,7 +1866,7 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   return PLSS_OK;
 }
 
-plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[11]) {
+plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[13]) {
   if (!ctx || !info || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
   const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
   info[0] = a.fmt;
@@ -1867,6 +1880,8 @@ plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab,
   info[8] = a.lchunk ? a.nchunks : 0;
   info[9] = a.psi3;
   info[10] = ctx->xdefer ? 1 : 0;
+  info[11] = a.fmt == 3 && a.gsort && a.s1on ? a.s1beg : -1;
+  info[12] = a.fmt == 3 && a.gsort && a.s1on ? a.s1end : -1;
   return PLSS_OK;
 }
 

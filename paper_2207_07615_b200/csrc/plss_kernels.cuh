@@ -164,6 +164,11 @@ struct SpmvSeg {
   int32_t stat;              // fmt 3 without perm / long rows: warps step through their CTA's slices
                              // statically and keep per-thread dot terms (no per-slice partials);
                              // 2: the same with 6 entries per lane in flight (slices of 6 k steps)
+  // Globally sorted segments: the tail of slices of one step (rows of one entry: 64% of C4's rows)
+  // and of no step (empty rows) runs in batches of S1B slices per warp (k_sell's second phase):
+  // slices [s1beg, s1end) have one step each, slice t's at step s1step0 + t - s1beg; slices from
+  // s1end on have none. s1on = 0: no such phase.
+  int32_t s1on, s1beg, s1end, s1step0;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -721,6 +726,10 @@ constexpr int GS_MINB = PLSS_GS_MINB;
 #define PLSS_GS_SU PLSS_SU              // their entries per lane in flight
 #endif
 constexpr int GS_SU = PLSS_GS_SU;
+#ifndef PLSS_S1B
+#define PLSS_S1B 6                      // one-step slices of a globally sorted segment per warp batch
+#endif
+constexpr int S1B = PLSS_S1B;
 constexpr int YD = 1024;
 #ifndef PLSS_YSTAGE
 #define PLSS_YSTAGE 1
@@ -838,6 +847,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : GNSB ? GS_MINB : 1)
   static_assert(SPW % P == 0 && NSB % P == 0, "a warp unit must not straddle a sigma window");
   __shared__ double sm[2][MAXW];
   __shared__ int s_next;
+  __shared__ int s_next1;                           // GNSB: next batch of one-step slices (phase 2)
   extern __shared__ __align__(16) double s_ydyn[];  // [YQ][SIGMA] when YST (dynamic smem)
   double (*s_y)[SIGMA] = reinterpret_cast<double (*)[SIGMA]>(s_ydyn);
   __shared__ int s_ycnt[YST ? YQ : 1];
@@ -848,12 +858,17 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : GNSB ? GS_MINB : 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = a.pol_first;
   double acc0 = 0.0, acc1 = 0.0;
-  int sl0, sl1, stride;
+  int sl0, sl1, slE, stride;
   if (!DYN) {
     sl0 = blockIdx.x * (NT / 32); sl1 = a.nslices; stride = gridDim.x * (NT / 32);
+    slE = sl1;
   } else {
     sl0 = a.cblk[blockIdx.x] * NSB; sl1 = min(a.cblk[blockIdx.x + 1] * NSB, a.nslices);
+    slE = sl1;                                      // the CTA's whole range (its dot partials)
+    // globally sorted: the one-step (and empty) slices [s1beg, slE) run in phase 2, by batches
+    if (GNSB && a.s1on) sl1 = max(sl0, min(sl1, a.s1beg));
     stride = P * BS / 32;
+    if (GNSB && tid == 0) s_next1 = max(sl0, a.s1on ? a.s1beg : slE);
     if (tid == 0 && !STAT) s_next = sl0 + P * (BS / 32);   // the first unit of each warp is static
     if (YST && tid < YQ) { s_ycnt[tid] = 0; s_ytag[tid] = -1; }
     if (YST) for (int q = tid; q < YD; q += BS) s_ydec[q] = -2;
@@ -1001,6 +1016,63 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : GNSB ? GS_MINB : 1)
     }
     su = nx;
   }
+  // Phase 2 (globally sorted segments): one-step and empty slices, S1B of them per warp batch. Their
+  // slots are consecutive, so a batch's perm, idx and val loads are S1B independent coalesced loads
+  // per lane, then S1B gathers and output loads, instead of one slice's dependent chain at a time
+  // (C4: 64% of the rows have one entry). Each row's sum is its one product added to 0 (or to y),
+  // as in sell_row_sum; dot partials per slice into slpart, as in phase 1.
+  if (GNSB && a.s1on) {
+    constexpr int S1B = ROLE == ROLE_K2DOTS && plss::S1B > 4 ? 4 : plss::S1B;  // K2DOTS: no spills
+    for (;;) {
+      int b = 0;
+      if (lane == 0) b = atomicAdd(&s_next1, S1B);
+      b = __shfl_sync(FULL, b, 0);
+      if (b >= slE) break;
+      int row[S1B], c[S1B];
+      double v[S1B], gv[S1B], s[S1B], r_old[S1B];
+#pragma unroll
+      for (int q = 0; q < S1B; ++q) {
+        const int t = b + q;
+        row[q] = t < slE ? a.perm[(long long)t * 32 + lane] : -1;
+        c[q] = -1;
+        if (t < slE && t < a.s1end) {
+          const long long e = ((long long)a.s1step0 + (t - a.s1beg)) * 32 + lane;
+          c[q] = ld_stream(a.idx + e, pol);
+          v[q] = ld_stream(a.val + e, pol);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < S1B; ++q) {
+        const bool valid = row[q] >= 0 && row[q] < a.nrows;
+        s[q] = (ROLE >= ROLE_K2 && valid && a.accumulate) ? a.out[row[q]] : 0.0;
+        r_old[q] = (ROLE == ROLE_K1 && valid) ? a.out[row[q]] : 0.0;
+        gv[q] = sell_gather(a, c[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < S1B; ++q) {
+        const int t = b + q;
+        if (t >= slE) break;
+        if (c[q] >= 0) s[q] = __dadd_rn(s[q], __dmul_rn(v[q], gv[q]));
+        double d0 = 0.0, d1 = 0.0;
+        if (row[q] >= 0 && row[q] < a.nrows) {
+          if (ROLE == ROLE_PLAIN) {
+            a.out[row[q]] = s[q];
+          } else if (ROLE == ROLE_K1) {
+            const double rn = __dsub_rn(r_old[q], s[q]);
+            a.out[row[q]] = rn;
+            d0 = rn * rn;
+          } else {
+            a.out[row[q]] = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, row[q], s[q], d0, d1) : s[q];
+          }
+        }
+        if (DOTS) {
+          d0 = warp_sum(d0);
+          if (ROLE == ROLE_K2DOTS) d1 = warp_sum(d1);
+          if (lane == 0) { a.slpart[2 * t] = d0; a.slpart[2 * t + 1] = d1; }
+        }
+      }
+    }
+  }
 #ifdef PLSS_DBGCTA
   if (DYN && a.ctat) {                              // diagnostics build only (uniform branch)
     __shared__ unsigned long long s_dbg[2];
@@ -1019,7 +1091,7 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : GNSB ? GS_MINB : 1)
   if (!DOTS) return;
   if (DYN && !STAT) {
     __syncthreads();
-    for (int q = sl0 + tid; q < sl1; q += BS) { acc0 += a.slpart[2 * q]; acc1 += a.slpart[2 * q + 1]; }
+    for (int q = sl0 + tid; q < slE; q += BS) { acc0 += a.slpart[2 * q]; acc1 += a.slpart[2 * q + 1]; }
   }
   if (!a.finalize) {
     block_sum2(acc0, acc1, sm);
@@ -1706,19 +1778,24 @@ __global__ void k_max_row_len(const int32_t* __restrict__ row_ptr, long long m, 
 }
 
 __global__ void k_cta_ranges(const int32_t* w, int wscale, int nunits, int nsb, int nblocks, int grid,
-                             int32_t* cblk, int unit_cost) {
+                             int32_t* cblk, int unit_cost, int s1beg = 0x7fffffff, int s1_cost = 0) {
   // w: prefix over units (nunits+1 entries); unit cost = (w[u+1] - w[u]) * wscale + UNIT_COST
   // (a unit also costs its metadata loads, row outputs and dot partial: without that term the
-  // empty slices of a segment -- C4's empty columns sort last -- all fall to the last CTA)
+  // empty slices of a segment -- C4's empty columns sort last -- all fall to the last CTA);
+  // units from s1beg on (k_sell's batched one-step slices) cost s1_cost instead of UNIT_COST
   const long long UNIT_COST = unit_cost;
-  const long long total = (long long)w[nunits] * wscale + (long long)nunits * UNIT_COST;
+  auto pre = [&](int u) -> long long {
+    return (long long)w[u] * wscale + (long long)u * UNIT_COST -
+           (long long)max(0, u - s1beg) * (UNIT_COST - s1_cost);
+  };
+  const long long total = pre(nunits);
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= grid; c += gridDim.x * blockDim.x) {
     const long long target = (total * c + grid - 1) / grid;
     int lo = 0, hi = nblocks;                                   // first b with start(b) >= target
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       const int u = min(mid * nsb, nunits);
-      if ((long long)w[u] * wscale + (long long)u * UNIT_COST < target) lo = mid + 1; else hi = mid;
+      if (pre(u) < target) lo = mid + 1; else hi = mid;
     }
     cblk[c] = c == 0 ? 0 : c == grid ? nblocks : lo;
   }

@@ -3,6 +3,7 @@ against the oracle: static stepping (C5's K1), globally sorted rows with the lon
 k_longchunks (C4's K1; k_longrows with PLSS_LCHUNK=0), a thread per short column (k_scalar, C4's K2), and the 1024-row sigma windows
 of K2 (the SIGMA_WIDE path had no test of its own), each bitwise on its SpMV outputs,
 repeatable, and inside a solve (also on a single-rank chunked distributed ctx)."""
+import json
 import os
 
 import numpy as np
@@ -93,6 +94,10 @@ def test_c4_formats_longrows_and_scalar(pkg, name):
     k1 = pkg.plss_query_segment(ctx, 1, 0)
     k2 = pkg.plss_query_segment(ctx, 2, 0)
     assert k1["fmt"] == 3 and k1["gsort"] == 1 and k1["nlong"] == int((np.diff(s.row_ptr) > 128).sum()) > 0
+    # the one-entry rows (sorted last) run in k_sell's batched phase 2: from the first slice whose
+    # longest row has one entry; the rows have >= 1 entry, so there is no empty slice
+    lens = np.sort(np.diff(s.row_ptr)[np.diff(s.row_ptr) <= 128])[::-1]
+    assert k1["s1beg"] == (int(np.argmax(lens <= 1)) + 31) // 32 and k1["s1end"] == k1["nslices"], k1
     assert k2["fmt"] == 5                                   # columns of ~1 entry: a thread per column
     assert pkg.plss_query(ctx)["launches_per_step"] == 4    # k_sell + k_longchunks, k_scalar, K3
     _spmv_bitwise_repeatable(pkg, ctx, s)
@@ -117,6 +122,7 @@ def test_k2_wide_sigma_windows(pkg):
         ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
     k2 = pkg.plss_query_segment(ctx, 2, 0)
     assert k2["fmt"] == 3 and k2["sig"] == 0 and k2["gsort"] == 1, k2
+    assert 0 < k2["s1beg"] < k2["s1end"] < k2["nslices"], k2     # one-entry columns, then empty ones
     _spmv_bitwise_repeatable(pkg, ctx, s)
     glob = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
     pkg.plss_destroy(ctx)
@@ -305,3 +311,30 @@ def test_x_every_other_step(pkg, name, slabs):
     for col in (0, 1, 2, 4, 5, 6, 7):
         np.testing.assert_array_equal(dist_out[1][1][:, col], dist_out[0][1][:, col])
     np.testing.assert_allclose(dist_out[1][1][1:30, 3], dist_out[0][1][1:30, 3], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("name", ["C4s", "C4xs"])
+def test_batched_one_step_slices_bitwise(pkg, name):
+    """k_sell's batched phase 2 for the one-entry rows of a globally sorted K1 segment computes each
+    row's sum, r update and per-slice dot partial as the one-slice-at-a-time path does: with the
+    same CTA ranges (the batched slices costed like the others, PLSS_UC_S1=48) a solve is bitwise
+    the PLSS_S1=0 solve (history, x, scalar records); with the default costing it still agrees with
+    the oracle over the parity window."""
+    s = plss_gen.make_config(name)
+    b = torch.from_numpy(s.b).cuda()
+    runs = {}
+    for lab, env in (("off", dict(PLSS_S1=0)), ("same", dict(PLSS_UC_S1=48)), ("default", {})):
+        with _env(**env):
+            ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+        k1 = pkg.plss_query_segment(ctx, 1, 0)
+        assert (k1["s1beg"] >= 0) == (lab != "off"), (lab, k1)
+        res = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
+        runs[lab] = (res["hist"], res["x"].cpu().numpy())
+        pkg.plss_destroy(ctx)
+    np.testing.assert_array_equal(runs["same"][0], runs["off"][0])
+    np.testing.assert_array_equal(runs["same"][1], runs["off"][1])
+    ref = oracle.plss_system(s, maxit=40)
+    with open(os.path.join(os.path.dirname(__file__), "golden", "parity_floor.json")) as f:
+        k = json.load(f)[name]["kf_min"]                     # the window two oracle orderings agree on
+    h = runs["default"][0]
+    assert np.max(np.abs(h[:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
