@@ -237,9 +237,10 @@ plss_status plss_query(const plss_ctx *ctx, int32_t *launches_per_step, int32_t 
  * segment (K2's finalizing one, one device) leaves psi = y^T p_{k-1} to K3 and reads no p, info[10]
  * 1 if the ctx's K3 updates x every other step (one device; plss_finish applies a pending update)
  * (R25), info[11] / info[12] the first one-step slice / the first empty slice of a globally
- * sorted segment, whose tail k_sell runs in batches of one-step slices (-1: no batched tail).
+ * sorted segment, whose tail k_sell runs in batches of one-step slices (-1: no batched tail),
+ * info[13] 1 if k_sell runs the segment's long-row chunks itself (no k_longchunks launch).
  * PLSS_E_INVALID for a bad ctx / which / slab. */
-plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[13]);
+plss_status plss_query_segment(const plss_ctx *ctx, int32_t which, int32_t slab, int32_t info[14]);
 
 /* Diagnostics (not part of the method): per-CTA record of the last launch of K1 (which = 1) or K2
  * (which = 2) of row slab `slab`, for ctxs created with the environment variable PLSS_DBG_CTA=1:

@@ -331,6 +331,14 @@ static void launch_spmv(const SpmvSeg& a, int grid, cudaStream_t st) {
     a.scb == 3 ? k_scalar<ROLE, 3><<<grid, NT, 0, st>>>(a) : k_scalar<ROLE, 2><<<grid, NT, 0, st>>>(a);
   else if (a.fmt == 2)
     k_sellw<ROLE><<<grid, NTW, (size_t)a.ring * 8, st>>>(a);
+  else if (a.fmt == 3 && a.nlong > 0 && a.lin) {
+    // gsort with long rows in chunks run by k_sell itself (phase 0): its long-row partial pair sits
+    // after the CTAs' and arrives in the election as one more (never the last: its CTA is still out)
+    SpmvSeg b = a;
+    b.elect_extra = 1;
+    b.elect_total = grid + 1;
+    k_sell<ROLE, 1024, false, false, SIGMA, false, GS_SU, GS_NSB><<<grid, 1024, 0, st>>>(b);
+  }
   else if (a.fmt == 3 && a.nlong > 0) {
     // gsort with long rows: the slices and k_longrows (one CTA per long row) run concurrently
     // (k_longrows forked onto a second stream, joined before the next launch): its CTAs fill the SMs
@@ -819,6 +827,7 @@ static plss_status try_sell_global(plss_ctx* ctx, SpmvSeg& a, int64_t nnz_seg, S
     a.lgd = (double*)(buf + b_ch + b_n + b_c + b_gc);
     a.lcpart = (double*)(buf + b_ch + b_n + b_c + b_gc + b_gd);
     a.nchunks = (int32_t)chunks.size();
+    a.lin = env_int("PLSS_LIN", 0);                 // opt-in: measured slower
   }
   int32_t* sidx = pool.idx + pool.used;
   double* sval = pool.val + pool.used;
@@ -1851,8 +1860,8 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   // distributed ctx), K3, and the distributed dots / tail kernel
   // (+1 for every globally sorted segment with long rows: k_longrows runs after its slices)
   int extra = 0;
-  for (auto& a : ctx->seg1) extra += (a.fmt == 3 && a.nlong > 0) ? 1 : 0;
-  for (auto& a : ctx->seg2) extra += (a.fmt == 3 && a.nlong > 0) ? 1 : 0;
+  for (auto& a : ctx->seg1) extra += (a.fmt == 3 && a.nlong > 0 && !a.lin) ? 1 : 0;
+  for (auto& a : ctx->seg2) extra += (a.fmt == 3 && a.nlong > 0 && !a.lin) ? 1 : 0;
   if (launches_per_step && ctx->cols)          // K1, K2 per slab; rho tail, dots, phi tail, K3
     *launches_per_step = 2 * ctx->S + 4 + extra;
   else if (launches_per_step)
@@ -1866,7 +1875,7 @@ plss_status plss_query(const plss_ctx* ctx, int32_t* launches_per_step, int32_t*
   return PLSS_OK;
 }
 
-plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[13]) {
+plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab, int32_t info[14]) {
   if (!ctx || !info || (which != 1 && which != 2) || slab < 0 || slab >= ctx->S) return PLSS_E_INVALID;
   const SpmvSeg& a = which == 1 ? ctx->seg1[slab] : ctx->seg2[slab];
   info[0] = a.fmt;
@@ -1882,6 +1891,7 @@ plss_status plss_query_segment(const plss_ctx* ctx, int32_t which, int32_t slab,
   info[10] = ctx->xdefer ? 1 : 0;
   info[11] = a.fmt == 3 && a.gsort && a.s1on ? a.s1beg : -1;
   info[12] = a.fmt == 3 && a.gsort && a.s1on ? a.s1end : -1;
+  info[13] = a.fmt == 3 && a.nlong > 0 && a.lin ? 1 : 0;
   return PLSS_OK;
 }
 

@@ -169,6 +169,9 @@ struct SpmvSeg {
   // slices [s1beg, s1end) have one step each, slice t's at step s1step0 + t - s1beg; slices from
   // s1end on have none. s1on = 0: no such phase.
   int32_t s1on, s1beg, s1end, s1step0;
+  // Globally sorted segments with long rows in chunks: 1 = k_sell runs the chunks itself (phase 0),
+  // 0 = a concurrent k_longchunks launch
+  int32_t lin;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -817,6 +820,142 @@ __device__ __forceinline__ void sell_rows_sum(const SpmvSeg& a, const int (&st0)
   }
 }
 
+// Long rows of a globally sorted segment in chunks of LCH entries (the default; k_longrows is the
+// CTA-per-row alternative, PLSS_LCHUNK=0): a warp per chunk, LCU entries per lane in flight (one
+// load batch), so short long rows (C4's are 129 .. 4096 entries, ~500 on average) no longer leave
+// most of a 256-thread CTA idle for a whole CTA lifetime (k_longrows: 41 us for C4's 2.7M long-row
+// entries). A chunk's sum: each lane's entries u = 0 .. LCU-1 sequentially, then the warp
+// butterfly; a row's sum: its chunk sums in chunk order, added by the warp that finishes the row's
+// last chunk (a per-row counter decides who, never the order). Row dot terms are reduced in row
+// order by the warp that finishes the last row, then the joint election with the slices' CTAs as in
+// k_longrows (final_sum2_warp: the same shape as the CTAs' final_sum2).
+#ifndef PLSS_LCU
+#define PLSS_LCU 12
+#endif
+constexpr int LCU = PLSS_LCU;
+constexpr int LCH = 32 * LCU;
+#ifndef PLSS_LCB
+#define PLSS_LCB 6                      // k_sell's phase 0: a chunk's entries per lane per load batch
+#endif
+constexpr int LCB = PLSS_LCB;
+// One chunk c of a long row, by one warp (k_longchunks, or k_sell's phase 0 for a globally sorted
+// segment). LB entries per lane per load batch, LCU / LB batches: a lane's entries are summed in
+// order u = 0 .. LCU-1 whatever LB is. lpart: the long rows' partial pair slot (after the slices'
+// CTAs). Returns true in every lane of the warp that must finalize the joint election (only
+// possible in k_longchunks: inside k_sell the warp's own CTA has not arrived yet).
+template <int ROLE, int LB>
+__device__ __forceinline__ bool longchunk_warp(const SpmvSeg& a, int c, double* lpart, bool wtd, int lane) {
+  static_assert(LCU % LB == 0, "whole batches");
+  constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
+  const uint64_t pol = a.pol_first;
+  const int4 d = a.lchunk[c];                                   // e0, e1, row k, first chunk of k
+  const int nch = a.lnch[d.z];
+  // the row's output slot and its old value, loaded early in case this warp finishes the row
+  const int r = lane == 0 ? a.lrows[d.z] : 0;
+  double start = 0.0;
+  if (lane == 0 && (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate))) start = a.out[r];
+  double s = 0.0;
+#pragma unroll
+  for (int u0 = 0; u0 < LCU; u0 += LB) {
+    int32_t ci[LB];
+    double v[LB], g[LB];
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int q = d.x + (u0 + u) * 32 + lane;
+      ci[u] = -1;
+      if (q < d.y) { ci[u] = ld_stream(a.lidx + q, pol); v[u] = ld_stream(a.lval + q, pol); }
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) g[u] = sell_gather(a, ci[u]);
+#pragma unroll
+    for (int u = 0; u < LB; ++u) if (ci[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], g[u]));
+  }
+  s = warp_sum(s);
+  int last = 1;
+  if (nch > 1) {
+    if (lane == 0) {
+      a.lcpart[c] = s;
+      __threadfence();
+      last = atomicAdd(a.lrcnt + d.z, 1u) == (unsigned)(nch - 1);
+    }
+    last = __shfl_sync(FULL, last, 0);
+  }
+  if (!last) return false;
+  int fin = 0;
+  if (lane == 0) {
+    double d0 = 0.0, d1 = 0.0;
+    double t = s;
+    if (nch > 1) {                                              // the row's chunk sums in chunk order
+      __threadfence();
+      t = 0.0;
+      for (int j0 = 0; j0 < nch; j0 += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = j0 + u < nch ? __ldcg(a.lcpart + d.w + j0 + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) if (j0 + u < nch) t = __dadd_rn(t, x[u]);
+      }
+      a.lrcnt[d.z] = 0u;
+    }
+    if (ROLE == ROLE_PLAIN) {
+      a.out[r] = t;
+    } else if (ROLE == ROLE_K1) {
+      const double rn = __dsub_rn(start, t);                   // r_i <- r_i - (A p)_i
+      a.out[r] = rn;
+      d0 = rn * rn;
+    } else {
+      a.out[r] = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, r, __dadd_rn(start, t), d0, d1)
+                                     : __dadd_rn(start, t);
+    }
+    if (DOTS) {
+      a.lrowd[2 * d.z] = d0;
+      a.lrowd[2 * d.z + 1] = d1;
+      __threadfence();
+      const int grp = d.z >> 5, gsz = min(32, a.nlong - (grp << 5));
+      fin = atomicAdd(a.lgcnt + grp, 1u) == (unsigned)(gsz - 1);  // this row completes its group
+    }
+  }
+  if (!DOTS) return false;
+  fin = __shfl_sync(FULL, fin, 0);
+  if (!fin) return false;
+  __threadfence();
+  const int grp = d.z >> 5, ngroup = (a.nlong + 31) >> 5;
+  {                                                             // the group's 32 rows, butterfly
+    const int q = (grp << 5) + lane;
+    double s0 = q < a.nlong ? __ldcg(a.lrowd + 2 * q) : 0.0;
+    double s1 = q < a.nlong ? __ldcg(a.lrowd + 2 * q + 1) : 0.0;
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    fin = 0;
+    if (lane == 0) {
+      a.lgd[2 * grp] = s0;
+      a.lgd[2 * grp + 1] = s1;
+      a.lgcnt[grp] = 0u;
+      __threadfence();
+      fin = atomicAdd(a.lcounter, 1u) == (unsigned)(ngroup - 1);
+    }
+    fin = __shfl_sync(FULL, fin, 0);
+    if (!fin) return false;
+    __threadfence();
+  }
+  double s0 = 0.0, s1 = 0.0;                                    // the group sums in group order
+  seq_add2(a.lgd, lane, ngroup, 32, s0, s1);
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  int efin = 0;
+  if (lane == 0) {
+    *a.lcounter = 0u;
+    lpart[0] = s0;
+    lpart[1] = s1;
+    if (a.finalize) {                                           // one more arrival in the slices' election
+      __threadfence();
+      efin = atomicAdd(a.counter, 1u) == (unsigned)(a.elect_total - 1);
+    }
+  }
+  efin = __shfl_sync(FULL, efin, 0);
+  return efin != 0;
+}
+
 // BS = NT (fmt 1): persistent grid, slices dealt round-robin over all warps of the grid; each
 //   thread accumulates its rows' dot contributions (static assignment: deterministic).
 // BS = 1024 (fmt 3): one CTA per SM walks the contiguous, entry-balanced slice range
@@ -920,6 +1059,16 @@ __global__ void __launch_bounds__(BS, BS == NT ? SELL_MINB : GNSB ? GS_MINB : 1)
     a.ctat[4 * blockIdx.x] = t;
   }
 #endif
+  // Phase 0 (globally sorted segments with long rows, lin): the long rows' chunks, dealt statically
+  // (chunk c to CTA c mod grid, warp c / grid mod 32), LCB entries per lane per load batch, instead
+  // of a concurrent k_longchunks launch: that launch's CTAs could not share an SM with this kernel's
+  // 1024 x 64 registers and ran on the SMs its CTAs had freed. Opt-in (PLSS_LIN=1): it loses on C4
+  // (0.1994 vs 0.1935 ms per step) and C4-alt (0.381 vs 0.358): the CTAs' balanced slice shares
+  // then finish later, while the separate launch used the SMs of the CTAs that finished first.
+  if (GNSB && a.lin) {
+    for (int c = blockIdx.x + gridDim.x * warp; c < a.nchunks; c += gridDim.x * (BS / 32))
+      longchunk_warp<ROLE, LCB>(a, c, a.partial + 2 * gridDim.x, wtd, lane);   // never the election's last
+  }
   if (su < sl1) meta(su);
   while (su < sl1) {
     const bool stage = YSTG && a.perm && !a.gsort && ymode(su);
@@ -1282,132 +1431,14 @@ __global__ void __launch_bounds__(NT) k_longrows(SpmvSeg a) {
   }
 }
 
-// Long rows of a globally sorted segment in chunks of LCH entries (the default; k_longrows is the
-// CTA-per-row alternative, PLSS_LCHUNK=0): a warp per chunk, LCU entries per lane in flight (one
-// load batch), so short long rows (C4's are 129 .. 4096 entries, ~500 on average) no longer leave
-// most of a 256-thread CTA idle for a whole CTA lifetime (k_longrows: 41 us for C4's 2.7M long-row
-// entries). A chunk's sum: each lane's entries u = 0 .. LCU-1 sequentially, then the warp
-// butterfly; a row's sum: its chunk sums in chunk order, added by the warp that finishes the row's
-// last chunk (a per-row counter decides who, never the order). Row dot terms are reduced in row
-// order by the warp that finishes the last row, then the joint election with the slices' CTAs as in
-// k_longrows (final_sum2_warp: the same shape as the CTAs' final_sum2).
-#ifndef PLSS_LCU
-#define PLSS_LCU 12
-#endif
-constexpr int LCU = PLSS_LCU;
-constexpr int LCH = 32 * LCU;
 template <int ROLE>
 __global__ void __launch_bounds__(NT) k_longchunks(SpmvSeg a) {
   if (a.ctl != nullptr && a.ctl->done) return;
-  constexpr bool DOTS = ROLE == ROLE_K1 || ROLE == ROLE_K2DOTS;
   const bool wtd = ROLE == ROLE_K2DOTS && a.wi != nullptr && a.ctl != nullptr && a.ctl->weighted;
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   if (c >= a.nchunks) return;
-  const uint64_t pol = a.pol_first;
-  const int4 d = a.lchunk[c];                                   // e0, e1, row k, first chunk of k
-  int32_t ci[LCU];
-  double v[LCU], g[LCU];
-#pragma unroll
-  for (int u = 0; u < LCU; ++u) {
-    const int q = d.x + u * 32 + lane;
-    ci[u] = -1;
-    if (q < d.y) { ci[u] = ld_stream(a.lidx + q, pol); v[u] = ld_stream(a.lval + q, pol); }
-  }
-  const int nch = a.lnch[d.z];
-  // the row's output slot and its old value, loaded early in case this warp finishes the row
-  const int r = lane == 0 ? a.lrows[d.z] : 0;
-  double start = 0.0;
-  if (lane == 0 && (ROLE == ROLE_K1 || ((ROLE == ROLE_K2 || ROLE == ROLE_K2DOTS) && a.accumulate))) start = a.out[r];
-#pragma unroll
-  for (int u = 0; u < LCU; ++u) g[u] = sell_gather(a, ci[u]);
-  double s = 0.0;
-#pragma unroll
-  for (int u = 0; u < LCU; ++u) if (ci[u] >= 0) s = __dadd_rn(s, __dmul_rn(v[u], g[u]));
-  s = warp_sum(s);
-  int last = 1;
-  if (nch > 1) {
-    if (lane == 0) {
-      a.lcpart[c] = s;
-      __threadfence();
-      last = atomicAdd(a.lrcnt + d.z, 1u) == (unsigned)(nch - 1);
-    }
-    last = __shfl_sync(FULL, last, 0);
-  }
-  if (!last) return;
-  int fin = 0;
-  if (lane == 0) {
-    double d0 = 0.0, d1 = 0.0;
-    double t = s;
-    if (nch > 1) {                                              // the row's chunk sums in chunk order
-      __threadfence();
-      t = 0.0;
-      for (int j0 = 0; j0 < nch; j0 += 8) {
-        double x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = j0 + u < nch ? __ldcg(a.lcpart + d.w + j0 + u) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) if (j0 + u < nch) t = __dadd_rn(t, x[u]);
-      }
-      a.lrcnt[d.z] = 0u;
-    }
-    if (ROLE == ROLE_PLAIN) {
-      a.out[r] = t;
-    } else if (ROLE == ROLE_K1) {
-      const double rn = __dsub_rn(start, t);                   // r_i <- r_i - (A p)_i
-      a.out[r] = rn;
-      d0 = rn * rn;
-    } else {
-      a.out[r] = ROLE == ROLE_K2DOTS ? k2_final(a, wtd, r, __dadd_rn(start, t), d0, d1)
-                                     : __dadd_rn(start, t);
-    }
-    if (DOTS) {
-      a.lrowd[2 * d.z] = d0;
-      a.lrowd[2 * d.z + 1] = d1;
-      __threadfence();
-      const int grp = d.z >> 5, gsz = min(32, a.nlong - (grp << 5));
-      fin = atomicAdd(a.lgcnt + grp, 1u) == (unsigned)(gsz - 1);  // this row completes its group
-    }
-  }
-  if (!DOTS) return;
-  fin = __shfl_sync(FULL, fin, 0);
-  if (!fin) return;
-  __threadfence();
-  const int grp = d.z >> 5, ngroup = (a.nlong + 31) >> 5;
-  {                                                             // the group's 32 rows, butterfly
-    const int q = (grp << 5) + lane;
-    double s0 = q < a.nlong ? __ldcg(a.lrowd + 2 * q) : 0.0;
-    double s1 = q < a.nlong ? __ldcg(a.lrowd + 2 * q + 1) : 0.0;
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    fin = 0;
-    if (lane == 0) {
-      a.lgd[2 * grp] = s0;
-      a.lgd[2 * grp + 1] = s1;
-      a.lgcnt[grp] = 0u;
-      __threadfence();
-      fin = atomicAdd(a.lcounter, 1u) == (unsigned)(ngroup - 1);
-    }
-    fin = __shfl_sync(FULL, fin, 0);
-    if (!fin) return;
-    __threadfence();
-  }
-  double s0 = 0.0, s1 = 0.0;                                    // the group sums in group order
-  seq_add2(a.lgd, lane, ngroup, 32, s0, s1);
-  s0 = warp_sum(s0);
-  s1 = warp_sum(s1);
-  int efin = 0;
-  if (lane == 0) {
-    *a.lcounter = 0u;
-    a.partial[0] = s0;
-    a.partial[1] = s1;
-    if (a.finalize) {                                           // one more arrival in the slices' election
-      __threadfence();
-      efin = atomicAdd(a.counter, 1u) == (unsigned)(a.elect_total - 1);
-    }
-  }
-  efin = __shfl_sync(FULL, efin, 0);
-  if (!efin) return;
+  if (!longchunk_warp<ROLE, LCU>(a, c, a.partial, wtd, lane)) return;
   __threadfence();
   double t0, t1;
   final_sum2_warp(a.part_base, a.nparts, t0, t1);

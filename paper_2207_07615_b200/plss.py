@@ -456,10 +456,10 @@ def plss_peer_reduce_emulate(parts, reds, flags, bounds, stream=None):
 
 def plss_query_segment(ctx: Ctx, which: int, slab: int = 0) -> dict:
     """The format chosen for K1 (which = 1) / K2 (which = 2) of a row slab (include/plss.h)."""
-    info = np.zeros(13, dtype=np.int32)
+    info = np.zeros(14, dtype=np.int32)
     _check(load_library().plss_query_segment(ctx.handle, int(which), int(slab), info.ctypes.data), ctx.handle)
     keys = ("fmt", "sig", "gsort", "nslices", "nlong", "stat", "grid", "rows", "nchunks", "psi3", "xdefer",
-            "s1beg", "s1end")
+            "s1beg", "s1end", "lin")
     return {k: int(v) for k, v in zip(keys, info)}
 
 

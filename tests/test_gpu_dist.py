@@ -230,8 +230,8 @@ def test_dist_column_block_step(pkg, name, slabs, weighted, x0):
                  validate=True)
         if cols:
             S = pkg.plss_query(ctx)["slabs"]
-            extra = sum(1 for w in (1, 2) for sl in range(S)            # k_longchunks beside a gsort segment
-                        if pkg.plss_query_segment(ctx, w, sl)["fmt"] == 3 and pkg.plss_query_segment(ctx, w, sl)["nlong"] > 0)
+            qs = [pkg.plss_query_segment(ctx, w, sl) for w in (1, 2) for sl in range(S)]
+            extra = sum(1 for q in qs if q["fmt"] == 3 and q["nlong"] > 0 and not q["lin"])  # a long-row launch
             assert pkg.plss_query(ctx)["launches_per_step"] == 2 * S + 4 + extra
         wi = None
         if weighted:

@@ -99,7 +99,7 @@ def test_c4_formats_longrows_and_scalar(pkg, name):
     lens = np.sort(np.diff(s.row_ptr)[np.diff(s.row_ptr) <= 128])[::-1]
     assert k1["s1beg"] == (int(np.argmax(lens <= 1)) + 31) // 32 and k1["s1end"] == k1["nslices"], k1
     assert k2["fmt"] == 5                                   # columns of ~1 entry: a thread per column
-    assert pkg.plss_query(ctx)["launches_per_step"] == 4    # k_sell + k_longchunks, k_scalar, K3
+    assert k1["lin"] == 0 and pkg.plss_query(ctx)["launches_per_step"] == 4   # k_sell + k_longchunks, k_scalar, K3
     _spmv_bitwise_repeatable(pkg, ctx, s)
     pkg.plss_destroy(ctx)
 
@@ -338,3 +338,24 @@ def test_batched_one_step_slices_bitwise(pkg, name):
         k = json.load(f)[name]["kf_min"]                     # the window two oracle orderings agree on
     h = runs["default"][0]
     assert np.max(np.abs(h[:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["C4s", "C4xs"])
+def test_inline_long_row_chunks_bitwise(pkg, name):
+    """k_sell's phase 0 (opt-in, PLSS_LIN=1) runs the long rows' chunks with the same per-lane
+    order, chunk order, row-dot groups and partial slot as the concurrent k_longchunks launch (the
+    default): the solves are bitwise equal (history, x), and one launch per step fewer."""
+    s = plss_gen.make_config(name)
+    b = torch.from_numpy(s.b).cuda()
+    runs = {}
+    for lab, env in (("launch", {}), ("inline", dict(PLSS_LIN=1))):
+        with _env(**env):
+            ctx = pkg.plss_create(_matrix(pkg, s), maxit_cap=60)
+        runs[lab + "_launches"] = pkg.plss_query(ctx)["launches_per_step"]
+        _spmv_bitwise_repeatable(pkg, ctx, s)
+        res = pkg.plss_solve(ctx, b, tol=s.tol, maxit=40)
+        runs[lab] = (res["hist"], res["x"].cpu().numpy(), res["iters"])
+        pkg.plss_destroy(ctx)
+    assert runs["inline_launches"] == runs["launch_launches"] - 1
+    np.testing.assert_array_equal(runs["inline"][0], runs["launch"][0])
+    np.testing.assert_array_equal(runs["inline"][1], runs["launch"][1])
