@@ -16,6 +16,7 @@
 #include "peer_kernels.cuh"
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -27,6 +28,18 @@
 #include <chrono>
 #include <thread>
 #include <vector>
+
+// NVTX range around a host entry point or a graph chunk (tracing): a no-op unless
+// a tool (nsys, ncu --nvtx) is attached. The loop's kernels run inside CUDA graphs, so the ranges
+// mark the host calls and each chunk launch; kernels are told apart by name.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace plss;
 
@@ -1389,6 +1402,7 @@ size_t plss_workspace_bytes(const plss_matrix* A, const plss_options* opt) {
 
 plss_status plss_create(const plss_matrix* A, const plss_options* opt, void* workspace, size_t ws_bytes,
                         void* cuda_stream, plss_ctx** out) {
+  NvtxRange nvtx_("plss_create");
   if (!A || !out) { g_last_error = "NULL argument"; return PLSS_E_INVALID; }
   *out = nullptr;
   plss_ctx* ctx = new (std::nothrow) plss_ctx();
@@ -1413,6 +1427,7 @@ plss_status plss_get_unique_id(uint8_t id[128]) {
 plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int64_t m_global,
                              const uint8_t id[128], int32_t rank, int32_t nranks, const plss_options* opt,
                              void* workspace, size_t ws_bytes, void* cuda_stream, plss_ctx** out) {
+  NvtxRange nvtx_("plss_create_dist");
   if (!A_local || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) { g_last_error = "invalid argument"; return PLSS_E_INVALID; }
   if (row_offset < 0 || row_offset + A_local->m > m_global) { g_last_error = "row block outside the global matrix"; return PLSS_E_DIM; }
   *out = nullptr;
@@ -1442,6 +1457,7 @@ plss_status plss_create_dist(const plss_matrix* A_local, int64_t row_offset, int
 plss_status plss_create_dist_cols(const plss_matrix* A_local, int64_t col_offset, int64_t n_global,
                                   const uint8_t id[128], int32_t rank, int32_t nranks, const plss_options* opt,
                                   void* workspace, size_t ws_bytes, void* cuda_stream, plss_ctx** out) {
+  NvtxRange nvtx_("plss_create_dist_cols");
   if (!A_local || !out || !id || nranks < 1 || rank < 0 || rank >= nranks) { g_last_error = "invalid argument"; return PLSS_E_INVALID; }
   if (col_offset < 0 || col_offset + A_local->n > n_global) { g_last_error = "column block outside the global matrix"; return PLSS_E_DIM; }
   if (opt && (opt->flags & 12)) { g_last_error = "options.flags bit2 / bit3 are row-block steps"; return PLSS_E_INVALID; }
@@ -1475,6 +1491,7 @@ plss_status plss_create_dist_cols(const plss_matrix* A_local, int64_t col_offset
 // collective -- the communicator is aborted (ncclCommAbort makes the pending collectives return),
 // the call fails with PLSS_E_NCCL and the ctx stays unusable until plss_destroy.
 static plss_status dist_wait(plss_ctx* ctx, cudaStream_t st, cudaEvent_t ev) {
+  NvtxRange nvtx_("plss: wait (stream / NCCL async-error poll)");
   if (!ctx->dist || !ctx->comm) {
     if (ev) CK(cudaEventSynchronize(ev)); else CK(cudaStreamSynchronize(st));
     return PLSS_OK;
@@ -1511,6 +1528,7 @@ static plss_status check_live(plss_ctx* ctx) {
 
 plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
                        int32_t maxit, int32_t flags) {
+  NvtxRange nvtx_("plss_start");
   if (!ctx) return PLSS_E_INVALID;
   if (check_live(ctx) != PLSS_OK) return PLSS_E_NCCL;
   if (!(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap || (tol_mode != 0 && tol_mode != 1) ||
@@ -1576,6 +1594,7 @@ plss_status plss_start(plss_ctx* ctx, const double* b, const double* x0, double 
 }
 
 plss_status plss_step(plss_ctx* ctx, int32_t k) {
+  NvtxRange nvtx_("plss_step");
   if (!ctx) return PLSS_E_INVALID;
   if (check_live(ctx) != PLSS_OK) return PLSS_E_NCCL;
   if (!ctx->started) { set_err(ctx, "plss_step before plss_start"); return PLSS_E_STATE; }
@@ -1587,6 +1606,7 @@ plss_status plss_step(plss_ctx* ctx, int32_t k) {
 
 plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
                         plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_finish");
   if (!ctx) return PLSS_E_INVALID;
   if (check_live(ctx) != PLSS_OK) return PLSS_E_NCCL;
   if (!ctx->started) { set_err(ctx, "plss_finish before plss_start"); return PLSS_E_STATE; }
@@ -1626,6 +1646,7 @@ plss_status plss_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, 
 plss_status plss_solve(plss_ctx* ctx, const double* b, const double* x0, double tol, int32_t tol_mode,
                        int32_t maxit, int32_t flags, double* x, int32_t* iters, double* hist, double* diag,
                        plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_solve");
   plss_status s = plss_start(ctx, b, x0, tol, tol_mode, maxit, flags);
   if (s != PLSS_OK) return s;
   cudaStream_t st = ctx->stream;
@@ -1635,6 +1656,7 @@ plss_status plss_solve(plss_ctx* ctx, const double* b, const double* x0, double 
   while (issued < maxit) {
     const bool full = (maxit - issued) >= ctx->chunk;
     if (full) {
+      NvtxRange chunk_("plss_solve: graph chunk");
       CK(cudaGraphLaunch(ctx->graph_chunk, st));
       issued += ctx->chunk;
     } else {
@@ -1656,6 +1678,7 @@ plss_status plss_solve(plss_ctx* ctx, const double* b, const double* x0, double 
 }
 
 plss_status plss_spmv(plss_ctx* ctx, const double* x, double* y) {
+  NvtxRange nvtx_("plss_spmv");
   if (!ctx || (!x && ctx->n > 0) || (!y && ctx->m > 0)) return PLSS_E_INVALID;
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
   for (int s = 0; s < ctx->S; ++s) {
@@ -1671,6 +1694,7 @@ plss_status plss_spmv(plss_ctx* ctx, const double* x, double* y) {
 }
 
 plss_status plss_spmvT(plss_ctx* ctx, const double* u, double* v) {
+  NvtxRange nvtx_("plss_spmvT");
   if (!ctx || (!u && ctx->m > 0) || (!v && ctx->n > 0)) return PLSS_E_INVALID;
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
   // slabs accumulate into the output, whose slices are re-read by TMA: use the (aligned,
@@ -1691,6 +1715,7 @@ plss_status plss_spmvT(plss_ctx* ctx, const double* u, double* v) {
 }
 
 plss_status plss_true_residual(plss_ctx* ctx, const double* b, const double* x, double* out) {
+  NvtxRange nvtx_("plss_true_residual");
   if (!ctx || !out || (!b && ctx->m > 0) || (!x && ctx->n > 0)) return PLSS_E_INVALID;
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
   cudaStream_t st = ctx->stream;
@@ -1740,6 +1765,7 @@ plss_status plss_true_residual(plss_ctx* ctx, const double* b, const double* x, 
 }
 
 plss_status plss_profile(plss_ctx* ctx, int32_t k, double* ms) {
+  NvtxRange nvtx_("plss_profile");
   if (!ctx || !ms || k < 1) return PLSS_E_INVALID;
   if (!ctx->started) { set_err(ctx, "plss_profile before plss_start"); return PLSS_E_STATE; }
   cudaStream_t st = ctx->stream;
@@ -1906,6 +1932,7 @@ plss_status plss_debug_cta_times(plss_ctx* ctx, int32_t which, int32_t slab, uin
 }
 
 plss_status plss_set_wi(plss_ctx* ctx, const double* wi) {
+  NvtxRange nvtx_("plss_set_wi");
   if (!ctx) return PLSS_E_INVALID;
   if (!wi) { ctx->weighted = false; return PLSS_OK; }
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
@@ -1927,6 +1954,7 @@ plss_status plss_set_wi(plss_ctx* ctx, const double* wi) {
 }
 
 plss_status plss_column_norms(plss_ctx* ctx, double* c) {
+  NvtxRange nvtx_("plss_column_norms");
   if (!ctx || (!c && ctx->n > 0)) return PLSS_E_INVALID;
   if (sync_in(ctx) != PLSS_OK) return PLSS_E_CUDA;
   cudaStream_t st = ctx->stream;
@@ -2151,6 +2179,7 @@ size_t plss_rp_workspace_bytes(const plss_ctx* ctx, int32_t r) {
 plss_status plss_rp_start(plss_ctx* ctx, int32_t r, uint64_t seed, double density, void* workspace,
                           size_t ws_bytes, const double* b, const double* x0, double tol, int32_t tol_mode,
                           int32_t maxit) {
+  NvtxRange nvtx_("plss_rp_start");
   if (!ctx) return PLSS_E_INVALID;
   if (!rp_valid(ctx, r, density) || !(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap ||
       (tol_mode != 0 && tol_mode != 1)) {
@@ -2180,6 +2209,7 @@ plss_status plss_rp_start(plss_ctx* ctx, int32_t r, uint64_t seed, double densit
 }
 
 plss_status plss_rp_step(plss_ctx* ctx, int32_t k) {
+  NvtxRange nvtx_("plss_rp_step");
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->rp_started) { set_err(ctx, "plss_rp_step before plss_rp_start"); return PLSS_E_STATE; }
   if (k < 0) return PLSS_E_INVALID;
@@ -2190,6 +2220,7 @@ plss_status plss_rp_step(plss_ctx* ctx, int32_t k) {
 
 plss_status plss_rp_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
                            plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_rp_finish");
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->rp_started) { set_err(ctx, "plss_rp_finish before plss_rp_start"); return PLSS_E_STATE; }
   return alt_finish(ctx, x, iters, hist, diag, outcome);
@@ -2199,6 +2230,7 @@ plss_status plss_rp_solve(plss_ctx* ctx, int32_t r, uint64_t seed, double densit
                           size_t ws_bytes, const double* b, const double* x0, double tol, int32_t tol_mode,
                           int32_t maxit, double* x, int32_t* iters, double* hist, double* diag,
                           plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_rp_solve");
   plss_status s = plss_rp_start(ctx, r, seed, density, workspace, ws_bytes, b, x0, tol, tol_mode, maxit);
   if (s != PLSS_OK) return s;
   if ((s = alt_run(ctx, ctx->rp_graph_chunk, ctx->rp_graph_one, maxit)) != PLSS_OK) return s;
@@ -2326,6 +2358,7 @@ size_t plss_kz_workspace_bytes(const plss_ctx* ctx, int32_t kmax) {
 
 plss_status plss_kz_start(plss_ctx* ctx, int32_t kmax, void* workspace, size_t ws_bytes, const int32_t* rows,
                           const double* b, const double* x0, double tol, int32_t tol_mode, int32_t maxit) {
+  NvtxRange nvtx_("plss_kz_start");
   if (!ctx) return PLSS_E_INVALID;
   if (ctx->dist || kmax < 1 || !(tol >= 0.0) || maxit < 1 || maxit > ctx->L.maxit_cap ||
       (tol_mode != 0 && tol_mode != 1) || !rows) {
@@ -2413,6 +2446,7 @@ plss_status plss_kz_start(plss_ctx* ctx, int32_t kmax, void* workspace, size_t w
 }
 
 plss_status plss_kz_step(plss_ctx* ctx, int32_t k) {
+  NvtxRange nvtx_("plss_kz_step");
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->kz_started) { set_err(ctx, "plss_kz_step before plss_kz_start"); return PLSS_E_STATE; }
   if (k < 0) return PLSS_E_INVALID;
@@ -2423,6 +2457,7 @@ plss_status plss_kz_step(plss_ctx* ctx, int32_t k) {
 
 plss_status plss_kz_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
                            plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_kz_finish");
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->kz_started) { set_err(ctx, "plss_kz_finish before plss_kz_start"); return PLSS_E_STATE; }
   return alt_finish(ctx, x, iters, hist, diag, outcome);
@@ -2431,6 +2466,7 @@ plss_status plss_kz_finish(plss_ctx* ctx, double* x, int32_t* iters, double* his
 plss_status plss_kz_solve(plss_ctx* ctx, int32_t kmax, void* workspace, size_t ws_bytes, const int32_t* rows,
                           const double* b, const double* x0, double tol, int32_t tol_mode, int32_t maxit, double* x,
                           int32_t* iters, double* hist, double* diag, plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_kz_solve");
   plss_status s = plss_kz_start(ctx, kmax, workspace, ws_bytes, rows, b, x0, tol, tol_mode, maxit);
   if (s != PLSS_OK) return s;
   if ((s = alt_run(ctx, ctx->kz_graph_chunk, ctx->kz_graph_one, maxit)) != PLSS_OK) return s;
@@ -2543,6 +2579,7 @@ size_t plss_eg_workspace_bytes(const plss_ctx* ctx, int32_t kmax) {
 plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t factor, int32_t kmax, void* workspace,
                           size_t ws_bytes, const int32_t* rows, uint64_t seed, const double* b, const double* x0,
                           double tol, int32_t tol_mode, int32_t maxit) {
+  NvtxRange nvtx_("plss_eg_start");
   if (!ctx) return PLSS_E_INVALID;
   if (ctx->dist || kmax < 1 || sketch < EG_RESIDUAL || sketch > EG_GAUSSIAN || (factor != 0 && factor != 1) ||
       !(tol >= 0.0) || maxit < 1 ||
@@ -2635,6 +2672,7 @@ plss_status plss_eg_start(plss_ctx* ctx, int32_t sketch, int32_t factor, int32_t
 }
 
 plss_status plss_eg_step(plss_ctx* ctx, int32_t k) {
+  NvtxRange nvtx_("plss_eg_step");
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->eg_started) { set_err(ctx, "plss_eg_step before plss_eg_start"); return PLSS_E_STATE; }
   if (k < 0) return PLSS_E_INVALID;
@@ -2645,6 +2683,7 @@ plss_status plss_eg_step(plss_ctx* ctx, int32_t k) {
 
 plss_status plss_eg_finish(plss_ctx* ctx, double* x, int32_t* iters, double* hist, double* diag,
                            plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_eg_finish");
   if (!ctx) return PLSS_E_INVALID;
   if (!ctx->eg_started) { set_err(ctx, "plss_eg_finish before plss_eg_start"); return PLSS_E_STATE; }
   return alt_finish(ctx, x, iters, hist, diag, outcome);
@@ -2654,6 +2693,7 @@ plss_status plss_eg_solve(plss_ctx* ctx, int32_t sketch, int32_t factor, int32_t
                           size_t ws_bytes, const int32_t* rows, uint64_t seed, const double* b, const double* x0,
                           double tol, int32_t tol_mode, int32_t maxit, double* x, int32_t* iters, double* hist,
                           double* diag, plss_outcome* outcome) {
+  NvtxRange nvtx_("plss_eg_solve");
   plss_status s = plss_eg_start(ctx, sketch, factor, kmax, workspace, ws_bytes, rows, seed, b, x0, tol, tol_mode, maxit);
   if (s != PLSS_OK) return s;
   if ((s = alt_run(ctx, ctx->eg_graph_chunk, ctx->eg_graph_one, maxit)) != PLSS_OK) return s;
