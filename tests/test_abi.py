@@ -126,3 +126,17 @@ def test_binding_rejects_bad_vectors():
         b._vec(ctx, [0.0] * 10, 10, "x")
     t = torch.zeros(10, dtype=torch.float64)
     assert b._vec(ctx, t, 10, "x") == t.data_ptr()
+
+
+def test_entry_points_carry_nvtx_ranges(lib):
+    """the solve entry points, each graph chunk and the NCCL wait open
+    an NVTX range; the range names are string constants of the built library."""
+    blob = open(pbuild.LIB, "rb").read()
+    for name in (b"plss_create", b"plss_start", b"plss_step", b"plss_finish", b"plss_solve", b"plss_spmv",
+                 b"plss_spmvT", b"plss_solve: graph chunk", b"plss: wait (stream / NCCL async-error poll)"):
+        assert name + b"\0" in blob, name
+    src = open(os.path.join(ROOT, "paper_2207_07615_b200", "csrc", "plss.cu")).read()
+    for fn in ("plss_create", "plss_create_dist", "plss_start", "plss_step", "plss_finish", "plss_solve",
+               "plss_spmv", "plss_spmvT", "plss_true_residual"):
+        m = re.search(r"^plss_status " + fn + r"\([^{;]*\)\s*\{\n\s*NvtxRange nvtx_\(\"" + fn + r"\"\);", src, re.M)
+        assert m, fn
